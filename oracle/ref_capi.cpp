@@ -1,0 +1,313 @@
+// ref_capi.cpp -- TEST INFRASTRUCTURE: C API (orc_api.h) over the UNMODIFIED
+// reference library compiled from /root/reference/proj/src by oracle/Makefile.
+// Every call forwards to the reference's own functions; nothing here restates
+// an algorithm.  Output: oracle/_ref/libertinv_ref.so (git-ignored).
+#include <cstring>
+#include <memory>
+#include <stdexcept>
+#include <string>
+
+#include "ertinv/amg.hpp"
+#include "ertinv/fem_mixed.hpp"
+#include "ertinv/inversion.hpp"
+#include "ertinv/linalg.hpp"
+#include "ertinv/mesh.hpp"
+#include "ertinv/minres.hpp"
+#include "ertinv/sparse.hpp"
+#include "orc_api.h"
+
+using namespace ertinv;
+
+namespace {
+thread_local std::string g_err;
+
+template <class F>
+int guard(F&& f) {
+  try {
+    f();
+    return 0;
+  } catch (const std::invalid_argument& e) {
+    g_err = e.what();
+    return 1;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return 2;
+  }
+}
+
+AmgOptions to_opts(const orc_amg_opts* o) {
+  AmgOptions a;
+  if (o) {
+    a.coarse_threshold = o->coarse_threshold;
+    a.strength = o->strength;
+    a.jacobi_damping = o->jacobi_damping;
+    a.prolongation_damping = o->prolongation_damping;
+    a.max_aggregate_size = o->max_aggregate_size;
+    a.max_levels = o->max_levels;
+  }
+  return a;
+}
+}  // namespace
+
+struct orc_problem {
+  bool mixed = false;
+  Mesh mesh;
+  MixedSpaces spaces;
+  SparseMatrix Q, D, S;
+  Vector qinv;
+  AmgHierarchy amg;
+  DenseMatrix J;
+  double beta = 1.0;
+  bool has_J = false;
+  WoodburyPreconditioner pc;
+};
+
+extern "C" {
+
+const char* orc_last_error(void) { return g_err.c_str(); }
+const char* orc_flavor(void) { return "reference"; }
+
+orc_problem* orc_create_mixed(const double* vertices, uint64_t n_vertices, const int64_t* cells,
+                              uint64_t n_cells, const orc_amg_opts* opts) {
+  auto p = std::make_unique<orc_problem>();
+  int rc = guard([&] {
+    std::vector<std::array<double, 2>> v(n_vertices);
+    for (uint64_t i = 0; i < n_vertices; ++i) v[i] = {vertices[2 * i], vertices[2 * i + 1]};
+    std::vector<std::array<std::size_t, 3>> c(n_cells);
+    for (uint64_t i = 0; i < n_cells; ++i)
+      c[i] = {static_cast<std::size_t>(cells[3 * i]), static_cast<std::size_t>(cells[3 * i + 1]),
+              static_cast<std::size_t>(cells[3 * i + 2])};
+    p->mesh = finalize_mesh(std::move(v), std::move(c), {});
+    p->spaces = make_mixed_spaces(p->mesh);
+    p->Q = assemble_Q(p->spaces);
+    p->D = assemble_D(p->spaces);
+    // inversion.cpp:210-212
+    p->qinv = diagonal(p->Q);
+    for (double& x : p->qinv) x = 1.0 / x;
+    p->S = assemble_lumped_schur(p->Q, p->D);
+    p->amg = amg_setup(p->S, to_opts(opts));
+    p->mixed = true;
+    p->pc.q_diag_inv = &p->qinv;
+    p->pc.amg = &p->amg;
+    p->pc.J = nullptr;
+  });
+  if (rc) return nullptr;
+  return p.release();
+}
+
+orc_problem* orc_create_amg_csr(uint64_t n, const int64_t* rowptr, const int64_t* cols,
+                                const double* vals, const orc_amg_opts* opts) {
+  auto p = std::make_unique<orc_problem>();
+  int rc = guard([&] {
+    std::vector<Triplet> trip;
+    for (uint64_t i = 0; i < n; ++i)
+      for (int64_t k = rowptr[i]; k < rowptr[i + 1]; ++k)
+        trip.push_back({i, static_cast<std::size_t>(cols[k]), vals[k]});
+    p->S = from_triplets(n, n, std::move(trip));
+    p->amg = amg_setup(p->S, to_opts(opts));
+  });
+  if (rc) return nullptr;
+  return p.release();
+}
+
+void orc_destroy(orc_problem* p) { delete p; }
+
+int orc_sizes(const orc_problem* p, uint64_t s[8]) {
+  std::memset(s, 0, 8 * sizeof(uint64_t));
+  if (p->mixed) {
+    s[0] = p->spaces.n_flux_dofs;
+    s[1] = p->spaces.n_cell_dofs;
+    s[2] = p->mesh.n_vertices();
+    s[3] = p->mesh.n_cells();
+    s[4] = p->mesh.n_edges();
+    s[6] = p->mesh.boundary_edges.size();
+  } else {
+    s[1] = p->S.n_rows;
+  }
+  s[5] = p->amg.n_levels();
+  s[7] = p->amg.levels.empty() ? 0 : p->amg.levels.back().matrix.n_rows;
+  return 0;
+}
+
+int orc_mesh(const orc_problem* p, int64_t* cells, int64_t* edges, int64_t* cell_edges,
+             int32_t* signs, int64_t* bedges, int32_t* btags) {
+  if (!p->mixed) {
+    g_err = "orc_mesh: not a mixed problem";
+    return 1;
+  }
+  const Mesh& m = p->mesh;
+  for (std::size_t c = 0; c < m.n_cells(); ++c)
+    for (int k = 0; k < 3; ++k) {
+      if (cells) cells[3 * c + k] = static_cast<int64_t>(m.cells[c][k]);
+      if (cell_edges) cell_edges[3 * c + k] = static_cast<int64_t>(m.cell_edges[c][k]);
+      if (signs) signs[3 * c + k] = m.cell_edge_signs[c][k];
+    }
+  for (std::size_t e = 0; e < m.n_edges(); ++e)
+    for (int k = 0; k < 2; ++k)
+      if (edges) edges[2 * e + k] = static_cast<int64_t>(m.edges[e][k]);
+  for (std::size_t b = 0; b < m.boundary_edges.size(); ++b) {
+    if (bedges) bedges[b] = static_cast<int64_t>(m.boundary_edges[b].edge);
+    if (btags) btags[b] = m.boundary_edges[b].tag == BoundaryTag::kSurface ? 0 : 1;
+  }
+  return 0;
+}
+
+int orc_csr(const orc_problem* p, int which, uint64_t level, uint64_t* n_rows, uint64_t* n_cols,
+            uint64_t* nnz, int64_t* rowptr, int64_t* cols, double* vals) {
+  const SparseMatrix* A = nullptr;
+  switch (which) {
+    case 0: A = &p->Q; break;
+    case 1: A = &p->D; break;
+    case 2: A = &p->S; break;
+    case 3:
+    case 4:
+      if (level >= p->amg.n_levels()) {
+        g_err = "orc_csr: level out of range";
+        return 1;
+      }
+      A = which == 3 ? &p->amg.levels[level].matrix : &p->amg.levels[level].prolongation;
+      break;
+    default: g_err = "orc_csr: bad selector"; return 1;
+  }
+  if (n_rows) *n_rows = A->n_rows;
+  if (n_cols) *n_cols = A->n_cols;
+  if (nnz) *nnz = A->nnz();
+  if (rowptr)
+    for (std::size_t i = 0; i < A->row_offsets.size(); ++i) rowptr[i] = static_cast<int64_t>(A->row_offsets[i]);
+  if (cols)
+    for (std::size_t k = 0; k < A->nnz(); ++k) cols[k] = static_cast<int64_t>(A->column_indices[k]);
+  if (vals) std::memcpy(vals, A->values.data(), A->nnz() * sizeof(double));
+  return 0;
+}
+
+int orc_level_inv_diag(const orc_problem* p, uint64_t level, double* out) {
+  if (level >= p->amg.n_levels()) {
+    g_err = "orc_level_inv_diag: level out of range";
+    return 1;
+  }
+  const Vector& d = p->amg.levels[level].inv_diag;
+  std::memcpy(out, d.data(), d.size() * sizeof(double));
+  return 0;
+}
+
+int orc_coarse_cholesky(const orc_problem* p, double* out) {
+  const DenseMatrix& L = p->amg.coarse_cholesky;
+  std::memcpy(out, L.values.data(), L.values.size() * sizeof(double));
+  return 0;
+}
+
+int orc_q_diag_inv(const orc_problem* p, double* out) {
+  std::memcpy(out, p->qinv.data(), p->qinv.size() * sizeof(double));
+  return 0;
+}
+
+int orc_amg_apply(const orc_problem* p, const double* r, double* z) {
+  return guard([&] {
+    const std::size_t n = p->amg.size();
+    const Vector out = amg_apply(p->amg, std::span<const double>(r, n));
+    std::memcpy(z, out.data(), n * sizeof(double));
+  });
+}
+
+int orc_set_jacobian(orc_problem* p, const double* J, uint64_t m, double beta, double timings[3]) {
+  return guard([&] {
+    if (!p->mixed) throw std::invalid_argument("orc_set_jacobian: not a mixed problem");
+    const std::size_t N = p->spaces.n_cell_dofs;
+    p->beta = beta;
+    if (m == 0) {
+      // Laplace-only preconditioner, inversion.cpp:251-256
+      p->has_J = false;
+      p->J = DenseMatrix();
+      p->pc = WoodburyPreconditioner();
+      p->pc.q_diag_inv = &p->qinv;
+      p->pc.amg = &p->amg;
+      p->pc.J = nullptr;
+      p->pc.beta = beta;
+      if (timings) timings[0] = timings[1] = timings[2] = 0.0;
+      return;
+    }
+    p->J = DenseMatrix(m, N);
+    std::memcpy(p->J.values.data(), J, m * N * sizeof(double));
+    p->has_J = true;
+    WoodburyBuildTimings t;
+    p->pc = build_woodbury_preconditioner(p->qinv, p->amg, p->J, beta, &t);
+    if (timings) {
+      timings[0] = t.t_H;
+      timings[1] = t.t_C;
+      timings[2] = t.t_chol;
+    }
+  });
+}
+
+int orc_get_H(const orc_problem* p, double* out) {
+  std::memcpy(out, p->pc.h_hat.values.data(), p->pc.h_hat.values.size() * sizeof(double));
+  return 0;
+}
+
+int orc_get_L(const orc_problem* p, double* out) {
+  const auto& L = p->pc.capacitance_chol;
+  std::memcpy(out, L.values.data(), L.values.size() * sizeof(double));
+  return 0;
+}
+
+int orc_apply_operator(const orc_problem* p, const double* x, double* y) {
+  return guard([&] {
+    SaddleOperator op{&p->Q, &p->D, p->has_J ? &p->J : nullptr, p->beta};
+    const std::size_t n = op.size();
+    const Vector out = op.apply(std::span<const double>(x, n));
+    std::memcpy(y, out.data(), n * sizeof(double));
+  });
+}
+
+int orc_precondition(const orc_problem* p, const double* y, double* z) {
+  return guard([&] {
+    const std::size_t n = p->Q.n_rows + p->D.n_rows;
+    const Vector out = p->pc.apply(std::span<const double>(y, n));
+    std::memcpy(z, out.data(), n * sizeof(double));
+  });
+}
+
+int orc_assemble_rhs(const orc_problem* p, const double* m, const double* m_ref, const double* g,
+                     const double* g_obs, double* rhs) {
+  return guard([&] {
+    const std::size_t N = p->D.n_rows;
+    const std::size_t M = p->J.n_rows;
+    const ModelVector mv(m, m + N), mr(m_ref, m_ref + N);
+    const Vector gv(g, g + M), go(g_obs, g_obs + M);
+    const Vector out = assemble_gn_rhs(mv, mr, gv, go, p->J, p->D, p->beta);
+    std::memcpy(rhs, out.data(), out.size() * sizeof(double));
+  });
+}
+
+int orc_minres(const orc_problem* p, const double* b, const double* x0, double tol, uint64_t maxit,
+               double* x, orc_minres_report* rep, double* he, double* hp, uint64_t cap) {
+  return guard([&] {
+    SaddleOperator op{&p->Q, &p->D, p->has_J ? &p->J : nullptr, p->beta};
+    const std::size_t n = op.size();
+    auto [sol, r] = minres([&op](std::span<const double> v) { return op.apply(v); },
+                           [p](std::span<const double> v) { return p->pc.apply(v); },
+                           std::span<const double>(b, n), std::span<const double>(x0, n), tol,
+                           maxit);
+    std::memcpy(x, sol.data(), n * sizeof(double));
+    rep->iterations = r.iterations;
+    rep->converged = r.converged ? 1 : 0;
+    rep->true_relative_residual = r.true_relative_residual;
+    const std::size_t h = std::min<std::size_t>(cap, r.relative_residuals.size());
+    rep->n_hist = r.relative_residuals.size();
+    for (std::size_t i = 0; i < h; ++i) {
+      if (he) he[i] = r.relative_residuals[i];
+      if (hp) hp[i] = r.pnorm_relative_residuals[i];
+    }
+  });
+}
+
+int orc_dense_cholesky(uint64_t n, const double* C, double* L) {
+  return guard([&] {
+    DenseMatrix Cm(n, n);
+    std::memcpy(Cm.values.data(), C, n * n * sizeof(double));
+    const DenseMatrix Lm = dense_cholesky(Cm);
+    std::memcpy(L, Lm.values.data(), n * n * sizeof(double));
+  });
+}
+
+}  // extern "C"
