@@ -1,0 +1,178 @@
+/*
+ * gnw.h -- C-ABI of the B200-native Woodbury-MINRES Gauss-Newton step solver
+ * (arXiv 2209.02815; reference: /root/reference/proj, "ertinv").
+ *
+ * This is the drop-in boundary.  Plain pointers and
+ * sizes only; no torch or CUDA types.  Every entry point names the reference
+ * interface it replaces.  All floating point is FP64.
+ *
+ *   gnw_assemble         <- make_mixed_spaces + assemble_Q/assemble_D + 1/diag(Q)
+ *                           + amg_setup(assemble_lumped_schur(Q, D), opts)
+ *                           (proj/src/inversion.cpp:196-213; fem_mixed.hpp:28-38;
+ *                           amg.hpp:44; finalize_mesh mesh.hpp:53-55)
+ *   gnw_set_jacobian     <- build_woodbury_preconditioner(q_diag_inv, amg, J, beta,
+ *                           timings*) (inversion.hpp:47-50, inversion.cpp:91-124) and
+ *                           SaddleOperator{&Q, &D, &J, beta} (inversion.cpp:258);
+ *                           m == 0 selects the plain Laplace preconditioner
+ *                           (inversion.cpp:251-256, Alg. 4)
+ *   gnw_apply_operator   <- SaddleOperator::apply (inversion.hpp:25, inversion.cpp:47-69)
+ *   gnw_precondition     <- WoodburyPreconditioner::apply (inversion.hpp:38,
+ *                           inversion.cpp:71-89)
+ *   gnw_amg_apply        <- amg_apply (amg.hpp:47, amg.cpp:189-194)
+ *   gnw_assemble_rhs     <- assemble_gn_rhs (inversion.hpp:53-55, inversion.cpp:126-146)
+ *   gnw_minres_solve     <- minres(apply_A, apply_Pinv, b, x0, tol, maxit)
+ *                           (minres.hpp:29-33, minres.cpp:20-155) with A/P bound to the
+ *                           context's operator and preconditioner
+ *   gnw_dense_cholesky   <- dense_cholesky (linalg.hpp:44, linalg.cpp:88-105), on device
+ *
+ * Error convention (reference: std::invalid_argument / std::runtime_error,
+ * SURVEY.md 8(b)): every call returns GNW_OK or a status; gnw_last_error()
+ * returns the thread-local message, whose text matches the reference's
+ * exception text (e.g. "minres: breakdown (stagnated rotation)").
+ *
+ * Pointer mode: by default vector arguments are HOST pointers (copied in/out
+ * on the context's stream).  gnw_set_pointer_mode(ctx, GNW_DEVICE_POINTERS)
+ * makes them device pointers on the context's device (no copies).
+ */
+#ifndef GNW_H
+#define GNW_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum gnw_status {
+  GNW_OK = 0,
+  GNW_INVALID_ARGUMENT = 1, /* std::invalid_argument in the reference */
+  GNW_NUMERICAL = 2,        /* std::runtime_error in the reference */
+  GNW_DEVICE = 3            /* CUDA / NCCL failure (no reference analogue) */
+} gnw_status;
+
+enum { GNW_HOST_POINTERS = 0, GNW_DEVICE_POINTERS = 1 };
+
+/* Coarsest-level solve of the V-cycle.  GNW_COARSE_INVERSE (default) applies
+ * the explicit inverse of the coarsest Galerkin matrix (one GEMV); the
+ * GNW_COARSE_CHOLESKY mode replays the reference's cholesky_solve
+ * (linalg.cpp:107-123) operation-for-operation so a V-cycle is bit-identical
+ * to amg_apply (used by the parity tests). */
+enum { GNW_COARSE_INVERSE = 0, GNW_COARSE_CHOLESKY = 1 };
+
+/* Preconditioner of the next gnw_set_jacobian (GnConfig::algorithm,
+ * inversion.hpp:64): Alg. 3 Laplace-Woodbury (default) or Alg. 4 Laplace-only,
+ * where J stays in the operator and the Schur block is the bare V-cycle
+ * (inversion.cpp:251-256). */
+enum { GNW_PC_WOODBURY = 0, GNW_PC_LAPLACE = 1 };
+
+typedef struct gnw_ctx gnw_ctx;
+
+/* AmgOptions, proj/include/ertinv/amg.hpp:11-23 (exact_solve is not supported:
+ * it needs a sparse LU and is an oracle-only mode of the reference). */
+typedef struct gnw_amg_options {
+  uint64_t coarse_threshold;   /* default 64 */
+  double strength;             /* default 0.08 */
+  double jacobi_damping;       /* default 2/3 */
+  double prolongation_damping; /* default 2/3 */
+  uint64_t max_aggregate_size; /* default 3 */
+  uint64_t max_levels;         /* default 25 */
+} gnw_amg_options;
+
+/* Raw triangulation, the inputs of finalize_mesh (mesh.hpp:53-55). */
+typedef struct gnw_mesh {
+  uint64_t n_vertices;
+  const double* vertices; /* 2 * n_vertices, (x, z) */
+  uint64_t n_cells;
+  const int64_t* cells;   /* 3 * n_cells vertex ids */
+} gnw_mesh;
+
+/* WoodburyBuildTimings, inversion.hpp:41-45 (seconds, CUDA-event timed). */
+typedef struct gnw_timings {
+  double t_H;
+  double t_C;
+  double t_chol;
+} gnw_timings;
+
+/* MinresReport, minres.hpp:13-22.  The histories are written to caller arrays
+ * (capacity hist_cap); n_hist is the full length (iterations + 1). */
+typedef struct gnw_report {
+  uint64_t iterations;
+  int32_t converged;
+  double true_relative_residual;
+  uint64_t n_hist;
+  double* relative_residuals;       /* may be NULL */
+  double* pnorm_relative_residuals; /* may be NULL */
+  uint64_t hist_cap;
+} gnw_report;
+
+/* Sizes of an assembled context (gnw_get_info). */
+typedef struct gnw_info {
+  uint64_t K;            /* flux dofs = edges */
+  uint64_t N;            /* cell dofs */
+  uint64_t n_vertices;
+  uint64_t n_edges;
+  uint64_t n_boundary_edges;
+  uint64_t n_levels;
+  uint64_t coarse_n;
+  uint64_t m;            /* rows of J (0: Laplace-only) */
+  double beta;
+  uint64_t device_bytes; /* device memory held by the context */
+} gnw_info;
+
+const char* gnw_last_error(void);
+const char* gnw_version(void);
+
+gnw_status gnw_create(int n_devices, const int* devices, gnw_ctx** out);
+void gnw_destroy(gnw_ctx* ctx);
+gnw_status gnw_set_pointer_mode(gnw_ctx* ctx, int mode);
+gnw_status gnw_set_coarse_mode(gnw_ctx* ctx, int mode);
+gnw_status gnw_set_preconditioner(gnw_ctx* ctx, int kind);
+
+gnw_status gnw_assemble(gnw_ctx* ctx, const gnw_mesh* mesh, const gnw_amg_options* opts);
+/* AMG hierarchy alone over an SPD CSR matrix (amg_setup(s_hat, opts)); after
+ * this only gnw_amg_apply is valid. */
+gnw_status gnw_assemble_amg_csr(gnw_ctx* ctx, uint64_t n, const int64_t* rowptr,
+                                const int64_t* cols, const double* vals,
+                                const gnw_amg_options* opts);
+gnw_status gnw_get_info(const gnw_ctx* ctx, gnw_info* info);
+
+gnw_status gnw_set_jacobian(gnw_ctx* ctx, const double* J, uint64_t m, uint64_t n_cells,
+                            double beta, gnw_timings* timings);
+
+gnw_status gnw_apply_operator(gnw_ctx* ctx, const double* x, double* y);
+gnw_status gnw_precondition(gnw_ctx* ctx, const double* y, double* z);
+gnw_status gnw_amg_apply(gnw_ctx* ctx, const double* r, double* z);
+/* H columns S_hat^-1 J^T on device, exported N x m row-major like h_hat. */
+gnw_status gnw_get_woodbury(gnw_ctx* ctx, double* H, double* L);
+gnw_status gnw_assemble_rhs(gnw_ctx* ctx, const double* m, const double* m_ref,
+                            const double* g, const double* g_obs, double* rhs);
+gnw_status gnw_minres_solve(gnw_ctx* ctx, const double* b, const double* x0, double* x,
+                            double tol, uint64_t maxit, gnw_report* report);
+
+/* Structure export for bit-exact parity checks (host arrays).  which: 0=Q 1=D
+ * 2=S_hat 3=A_level 4=P_level; NULL arrays query sizes only. */
+gnw_status gnw_export_csr(const gnw_ctx* ctx, int which, uint64_t level, uint64_t* n_rows,
+                          uint64_t* n_cols, uint64_t* nnz, int64_t* rowptr, int64_t* cols,
+                          double* vals);
+gnw_status gnw_export_mesh(const gnw_ctx* ctx, int64_t* cells, int64_t* edges,
+                           int64_t* cell_edges, int32_t* cell_edge_signs,
+                           int64_t* boundary_edges, int32_t* boundary_tags);
+
+/* dense_cholesky on device (linalg.cpp:88-105), operation order preserved. */
+gnw_status gnw_dense_cholesky(gnw_ctx* ctx, uint64_t n, const double* C, double* L);
+
+/* Device time of the last gnw_minres_solve / set_jacobian, and launch counts. */
+typedef struct gnw_stats {
+  double t_minres;        /* seconds, CUDA events around the MINRES loop */
+  double t_rhs;
+  uint64_t kernel_launches; /* kernels launched by the last solve (graph nodes x iterations) */
+  uint64_t setup_kernel_launches;
+} gnw_stats;
+gnw_status gnw_get_stats(const gnw_ctx* ctx, gnw_stats* stats);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* GNW_H */

@@ -812,6 +812,7 @@ struct orc_problem {
   amg_t amg;
   size_t K, N;
   /* Woodbury state */
+  int pc_laplace; /* Alg. 4: J in the operator, Laplace preconditioner */
   size_t m;
   double beta;
   double* J; /* m x N */
@@ -990,6 +991,7 @@ int orc_set_jacobian(orc_problem* p, const double* J, uint64_t m, double beta, d
   p->m = m;
   p->J = xmalloc(m * N * sizeof(double));
   memcpy(p->J, J, m * N * sizeof(double));
+  if (p->pc_laplace) return 0; /* inversion.cpp:251-256 */
   double t0 = now_s();
   p->H = xmalloc(N * m * sizeof(double));
   double* col = xmalloc(N * sizeof(double));
@@ -1035,6 +1037,11 @@ int orc_set_jacobian(orc_problem* p, const double* J, uint64_t m, double beta, d
   return rc;
 }
 
+int orc_set_pc_laplace(orc_problem* p, int laplace) {
+  p->pc_laplace = laplace != 0;
+  return 0;
+}
+
 int orc_get_H(const orc_problem* p, double* out) {
   memcpy(out, p->H, p->N * p->m * sizeof(double));
   return 0;
@@ -1077,7 +1084,7 @@ static void woodbury_apply(const orc_problem* p, const double* y, double* out) {
   const double* y2 = y + K;
   double* s = out + K;
   amg_cycle(&p->amg, 0, y2, s);
-  if (p->m > 0) {
+  if (p->m > 0 && !p->pc_laplace) {
     double* t = xmalloc(p->m * sizeof(double));
     double* w = xmalloc(N * sizeof(double));
     matvec_transpose(N, p->m, p->H, y2, t);

@@ -87,6 +87,7 @@ class Oracle:
         L.orc_q_diag_inv.argtypes = [C.c_void_p, _dp]
         L.orc_amg_apply.argtypes = [C.c_void_p, _dp, _dp]
         L.orc_set_jacobian.argtypes = [C.c_void_p, C.c_void_p, _u64, C.c_double, _dp]
+        L.orc_set_pc_laplace.argtypes = [C.c_void_p, C.c_int]
         L.orc_get_H.argtypes = [C.c_void_p, _dp]
         L.orc_get_L.argtypes = [C.c_void_p, _dp]
         L.orc_apply_operator.argtypes = [C.c_void_p, _dp, _dp]
@@ -199,7 +200,8 @@ class Problem:
         self.o.check(self.o.L.orc_amg_apply(self.h, r, z))
         return z
 
-    def set_jacobian(self, J: np.ndarray | None, beta: float):
+    def set_jacobian(self, J: np.ndarray | None, beta: float, laplace_pc: bool = False):
+        self.o.check(self.o.L.orc_set_pc_laplace(self.h, 1 if laplace_pc else 0))
         t = np.zeros(3)
         if J is None or J.size == 0:
             self.o.check(self.o.L.orc_set_jacobian(self.h, None, 0, beta, t))

@@ -79,6 +79,10 @@ int orc_amg_apply(const orc_problem* p, const double* r, double* z);
  * plain Laplace preconditioner (inversion.cpp:251-256).  timings: t_H, t_C, t_chol. */
 int orc_set_jacobian(orc_problem* p, const double* J, uint64_t m, double beta,
                      double timings[3]);
+/* Alg. 4 (GnAlgorithm::kLaplaceMinres, inversion.cpp:251-256): the next
+ * orc_set_jacobian keeps J in the operator but builds the plain Laplace
+ * preconditioner (pc.J = nullptr). */
+int orc_set_pc_laplace(orc_problem* p, int laplace);
 int orc_get_H(const orc_problem* p, double* out);   /* N x m row-major */
 int orc_get_L(const orc_problem* p, double* out);   /* m x m row-major */
 

@@ -59,6 +59,7 @@ struct orc_problem {
   DenseMatrix J;
   double beta = 1.0;
   bool has_J = false;
+  bool pc_laplace = false;
   WoodburyPreconditioner pc;
 };
 
@@ -229,6 +230,15 @@ int orc_set_jacobian(orc_problem* p, const double* J, uint64_t m, double beta, d
     p->J = DenseMatrix(m, N);
     std::memcpy(p->J.values.data(), J, m * N * sizeof(double));
     p->has_J = true;
+    if (p->pc_laplace) {  // inversion.cpp:251-256
+      p->pc = WoodburyPreconditioner();
+      p->pc.q_diag_inv = &p->qinv;
+      p->pc.amg = &p->amg;
+      p->pc.J = nullptr;
+      p->pc.beta = beta;
+      if (timings) timings[0] = timings[1] = timings[2] = 0.0;
+      return;
+    }
     WoodburyBuildTimings t;
     p->pc = build_woodbury_preconditioner(p->qinv, p->amg, p->J, beta, &t);
     if (timings) {
@@ -237,6 +247,11 @@ int orc_set_jacobian(orc_problem* p, const double* J, uint64_t m, double beta, d
       timings[2] = t.t_chol;
     }
   });
+}
+
+int orc_set_pc_laplace(orc_problem* p, int laplace) {
+  p->pc_laplace = laplace != 0;
+  return 0;
 }
 
 int orc_get_H(const orc_problem* p, double* out) {

@@ -1,0 +1,156 @@
+// common.cuh -- shared device-side definitions for the gnw kernels (sm_100a).
+//
+// Floating point: the library is compiled with --fmad=false so that every
+// a*b+c written in the reference's evaluation order rounds exactly like the
+// reference's x86-64 build (no FMA contraction).  Kernels that do not need
+// reference-order rounding (tensor-core DGEMM, reductions) say so.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace gnw {
+
+constexpr int kWarp = 32;
+
+// MINRES loop status codes (device -> host).
+enum : int {
+  kRunning = 0,
+  kVerify = 1,      // recurred residual <= tol: host verifies with the true residual
+  kExhausted = 2,   // gamma_{j+1} <= 1e-13 gamma_1 (minres.cpp:122)
+  kMaxit = 3,
+  kErrNotPD = 4,    // "minres: preconditioner is not positive definite"
+  kErrStagnated = 5 // "minres: breakdown (stagnated rotation)"
+};
+
+// Scalar state of the MINRES recurrence (minres.cpp:61-68), device resident.
+struct MinresState {
+  double gamma_prev, gamma_cur, gamma_next;
+  double c_prev, c_cur, c_next;
+  double s_prev, s_cur, s_next;
+  double eta, gamma1, bnorm, tol, exhausted_tol;
+  double delta;          // <A zhat, zhat>
+  double inv_gamma;      // 1 / gamma_cur  (zhat = z * inv_gamma)
+  double coef_v1, coef_v2; // -delta/gamma_cur, -gamma_cur/gamma_prev
+  double alpha2, alpha3, inv_alpha1, tau;
+  double rel;            // ||r|| / ||b|| after the update
+  double scratch[8];
+  long long j;           // iteration index (1-based)
+  long long maxit;
+  long long iterations;  // report.iterations
+  int status;
+  int pad;
+};
+
+// A vector argument that is either a fixed buffer or a slot of a device ring
+// indexed by the MINRES iteration counter: p[(j + off) % mod].
+struct VSel {
+  double* p[3];
+  int mod;
+  int off;
+};
+
+__host__ inline VSel vfixed(double* x) {
+  VSel s;
+  s.p[0] = s.p[1] = s.p[2] = x;
+  s.mod = 1;
+  s.off = 0;
+  return s;
+}
+__host__ inline VSel vring(double* const* ring, int mod, int off) {
+  VSel s;
+  for (int k = 0; k < 3; ++k) s.p[k] = ring[k < mod ? k : 0];
+  s.mod = mod;
+  s.off = off;
+  return s;
+}
+
+__device__ __forceinline__ double* vsel(const VSel& s, const MinresState* st) {
+  if (s.mod == 1) return s.p[0];
+  const int idx = (int)((st->j + s.off) % s.mod);
+  // select without dynamic indexing (keeps the struct in registers, no stack frame)
+  double* p = s.p[0];
+  if (idx == 1) p = s.p[1];
+  if (idx == 2) p = s.p[2];
+  return p;
+}
+
+// Device CSR (int32 indices).
+struct DCsr {
+  int n_rows = 0, n_cols = 0, nnz = 0;
+  int* rowptr = nullptr;
+  int* cols = nullptr;
+  double* vals = nullptr;
+};
+
+// ---------------------------------------------------------------- reductions
+// Deterministic block reduction: warp xor-tree, then warps in index order.
+template <int NV>
+__device__ __forceinline__ void warp_reduce(double (&v)[NV]) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+    for (int k = 0; k < NV; ++k) v[k] += __shfl_xor_sync(0xffffffffu, v[k], o);
+}
+
+// Reduces NV values over the block; result valid in thread 0.  smem needs
+// NV * (blockDim/32) doubles.
+template <int NV>
+__device__ __forceinline__ void block_reduce(double (&v)[NV], double* smem) {
+  warp_reduce<NV>(v);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  if (lane == 0)
+#pragma unroll
+    for (int k = 0; k < NV; ++k) smem[warp * NV + k] = v[k];
+  __syncthreads();
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int k = 0; k < NV; ++k) {
+      double s = 0.0;
+      for (int w = 0; w < nw; ++w) s += smem[w * NV + k];
+      v[k] = s;
+    }
+  }
+  __syncthreads();
+}
+
+// Grid-wide deterministic reduction via the last-arriving block.  Each block
+// writes its NV partials to part[blockIdx.x * NV + k]; the last block sums
+// the partials in block-index order (fixed tree, independent of arrival
+// order) and returns true in ALL its threads with `out` (thread 0) holding
+// the totals.  `counter` must be zero at launch; it is reset by the last block.
+template <int NV>
+__device__ bool grid_reduce_last(double (&v)[NV], double* part, unsigned int* counter, double* smem,
+                                 double (&out)[NV]) {
+  block_reduce<NV>(v, smem);
+  __shared__ bool am_last;
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int k = 0; k < NV; ++k) part[blockIdx.x * NV + k] = v[k];
+    __threadfence();
+    const unsigned prev = atomicAdd(counter, 1u);
+    am_last = (prev == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (!am_last) return false;
+  __threadfence();
+  double acc[NV];
+#pragma unroll
+  for (int k = 0; k < NV; ++k) acc[k] = 0.0;
+  for (int b = threadIdx.x; b < (int)gridDim.x; b += blockDim.x)
+#pragma unroll
+    for (int k = 0; k < NV; ++k) acc[k] += __ldcg(&part[b * NV + k]);
+  block_reduce<NV>(acc, smem);
+#pragma unroll
+  for (int k = 0; k < NV; ++k) out[k] = acc[k];
+  if (threadIdx.x == 0) *counter = 0u;
+  return true;
+}
+
+}  // namespace gnw
+
+#define GNW_CUDA_CHECK(expr)                                                     \
+  do {                                                                           \
+    cudaError_t e__ = (expr);                                                    \
+    if (e__ != cudaSuccess) throw ::gnw::DeviceError(#expr, e__, __FILE__, __LINE__); \
+  } while (0)

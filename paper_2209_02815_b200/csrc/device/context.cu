@@ -1,0 +1,780 @@
+// context.cu -- device-resident Woodbury-MINRES GN-step solver (host driver).
+//
+// One context = one GPU, one stream.  The MINRES loop runs as ONE CUDA graph
+// with a conditional WHILE node whose body is one iteration (7 + 4 x levels
+// kernels); the loop predicate is set on the device by the update kernel, so
+// the host does not synchronise per iteration.  It only wakes up when the
+// recurred residual crosses tol (the reference's true-residual verification,
+// minres.cpp:108-120), on exhaustion, on maxit or on a numerical error.
+#include "context.cuh"
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+
+namespace gnw {
+
+uint64_t launch_count();
+
+void DeviceMemory::release_all() {
+  for (void* p : ptrs) cudaFree(p);
+  ptrs.clear();
+  bytes = 0;
+}
+
+namespace {
+
+DCsr upload_csr(DeviceMemory& mem, const host::Csr& A, cudaStream_t s) {
+  DCsr d;
+  d.n_rows = static_cast<int>(A.n_rows);
+  d.n_cols = static_cast<int>(A.n_cols);
+  d.nnz = static_cast<int>(A.nnz());
+  if (A.nnz() > 0x7fffffffLL || A.n_rows > 0x7fffffffLL) throw std::invalid_argument("matrix too large for int32 indices");
+  std::vector<int> rp(A.rowptr.size());
+  for (size_t i = 0; i < rp.size(); ++i) rp[i] = static_cast<int>(A.rowptr[i]);
+  d.rowptr = mem.alloc<int>(rp.size());
+  d.cols = mem.alloc<int>(A.cols.size());
+  d.vals = mem.alloc<double>(A.vals.size());
+  GNW_CUDA_CHECK(cudaMemcpyAsync(d.rowptr, rp.data(), rp.size() * sizeof(int), cudaMemcpyHostToDevice, s));
+  if (A.nnz()) {
+    GNW_CUDA_CHECK(cudaMemcpyAsync(d.cols, A.cols.data(), A.cols.size() * sizeof(int), cudaMemcpyHostToDevice, s));
+    GNW_CUDA_CHECK(cudaMemcpyAsync(d.vals, A.vals.data(), A.vals.size() * sizeof(double), cudaMemcpyHostToDevice, s));
+  }
+  GNW_CUDA_CHECK(cudaStreamSynchronize(s));  // host vectors are temporaries
+  return d;
+}
+
+template <class T>
+void h2d(T* dst, const T* src, size_t n, cudaStream_t s) {
+  if (n) GNW_CUDA_CHECK(cudaMemcpyAsync(dst, src, n * sizeof(T), cudaMemcpyHostToDevice, s));
+}
+
+VSel ring3(double* const* p, int off) { return vring(p, 3, off); }
+VSel ring2(double* const* p, int off) { return vring(p, 2, off); }
+
+}  // namespace
+
+Context::Context(int device) : device_(device) {
+  if (device_ < 0) return;
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0)
+    throw DeviceError("gnw: no CUDA device available (the product has no CPU fallback)");
+  if (device_ >= n) throw std::invalid_argument("gnw_create: device index out of range");
+  GNW_CUDA_CHECK(cudaSetDevice(device_));
+  cudaDeviceProp prop;
+  GNW_CUDA_CHECK(cudaGetDeviceProperties(&prop, device_));
+  if (prop.major < 10) throw DeviceError("gnw: this build targets sm_100a (B200); found sm_" + std::to_string(prop.major) + std::to_string(prop.minor));
+  sm_count_ = prop.multiProcessorCount;
+  GNW_CUDA_CHECK(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
+  st_ = mem_.alloc<MinresState>(1);
+  st_plain_ = mem_.alloc<MinresState>(1);
+  counters_ = mem_.alloc<unsigned>(16);
+  dflag_ = mem_.alloc<int>(4);
+  GNW_CUDA_CHECK(cudaMemsetAsync(counters_, 0, 16 * sizeof(unsigned), stream_));
+  GNW_CUDA_CHECK(cudaMemsetAsync(st_plain_, 0, sizeof(MinresState), stream_));
+  GNW_CUDA_CHECK(cudaMallocHost(&h_st_, 2 * sizeof(MinresState)));
+  sync();
+}
+
+Context::~Context() {
+  if (device_ < 0) return;
+  cudaSetDevice(device_);
+  destroy_graph();
+  if (stream_) cudaStreamSynchronize(stream_);
+  jmem_.reset();
+  mem_.release_all();
+  if (h_st_) cudaFreeHost(h_st_);
+  if (stream_) cudaStreamDestroy(stream_);
+}
+
+void Context::sync() { GNW_CUDA_CHECK(cudaStreamSynchronize(stream_)); }
+
+void Context::require_device() const {
+  if (device_ < 0) throw DeviceError("gnw: context has no device (created with n_devices = 0)");
+}
+void Context::require_mixed() const {
+  if (!assembled_ || !mixed_) throw std::invalid_argument("gnw: context is not assembled with a mixed problem");
+}
+
+void Context::destroy_graph() {
+  if (graph_exec_) cudaGraphExecDestroy(graph_exec_);
+  if (graph_) cudaGraphDestroy(graph_);
+  graph_exec_ = nullptr;
+  graph_ = nullptr;
+}
+
+// ---------------------------------------------------------------- assembly
+void Context::assemble(const double* vertices, int64_t nv, const int64_t* cells, int64_t nc,
+                       const host::AmgOptions& o) {
+  destroy_graph();
+  mesh_ = host::finalize_mesh(vertices, nv, cells, nc);  // mesh.cpp:85-154
+  Q_ = host::assemble_Q(mesh_);                          // fem_mixed.cpp:29-68
+  D_ = host::assemble_D(mesh_);                          // fem_mixed.cpp:70-82
+  S_ = host::lumped_schur(Q_, D_);                       // fem_mixed.cpp:84-94
+  amg_ = host::amg_setup(S_, o);                         // amg.cpp:115-187
+  K_ = mesh_.ne;
+  N_ = mesh_.nc;
+  mixed_ = true;
+  assembled_ = true;
+  m_ = 0;
+  hist_cap_ = 0;
+  hist_e_ = hist_p_ = nullptr;
+  if (device_ >= 0) {
+    GNW_CUDA_CHECK(cudaSetDevice(device_));
+    jmem_.reset();
+    mem_.release_all();
+    st_ = mem_.alloc<MinresState>(1);
+    st_plain_ = mem_.alloc<MinresState>(1);
+    counters_ = mem_.alloc<unsigned>(16);
+    dflag_ = mem_.alloc<int>(4);
+    GNW_CUDA_CHECK(cudaMemsetAsync(counters_, 0, 16 * sizeof(unsigned), stream_));
+    GNW_CUDA_CHECK(cudaMemsetAsync(st_plain_, 0, sizeof(MinresState), stream_));
+    upload_structure();
+    upload_hierarchy();
+    sync();
+  }
+}
+
+void Context::assemble_amg_csr(int64_t n, const int64_t* rowptr, const int64_t* cols, const double* vals,
+                               const host::AmgOptions& o) {
+  destroy_graph();
+  std::vector<int64_t> r, c;
+  std::vector<double> v;
+  for (int64_t i = 0; i < n; ++i)
+    for (int64_t k = rowptr[i]; k < rowptr[i + 1]; ++k) {
+      r.push_back(i);
+      c.push_back(cols[k]);
+      v.push_back(vals[k]);
+    }
+  S_ = host::from_triplets(n, n, std::move(r), std::move(c), std::move(v));
+  amg_ = host::amg_setup(S_, o);
+  mesh_ = host::Mesh{};
+  Q_ = D_ = host::Csr{};
+  K_ = 0;
+  N_ = n;
+  mixed_ = false;
+  assembled_ = true;
+  m_ = 0;
+  hist_cap_ = 0;
+  hist_e_ = hist_p_ = nullptr;
+  if (device_ >= 0) {
+    GNW_CUDA_CHECK(cudaSetDevice(device_));
+    jmem_.reset();
+    mem_.release_all();
+    st_ = mem_.alloc<MinresState>(1);
+    st_plain_ = mem_.alloc<MinresState>(1);
+    counters_ = mem_.alloc<unsigned>(16);
+    dflag_ = mem_.alloc<int>(4);
+    GNW_CUDA_CHECK(cudaMemsetAsync(counters_, 0, 16 * sizeof(unsigned), stream_));
+    GNW_CUDA_CHECK(cudaMemsetAsync(st_plain_, 0, sizeof(MinresState), stream_));
+    upload_hierarchy();
+    io_a_ = mem_.alloc<double>(n);
+    io_b_ = mem_.alloc<double>(n);
+    sync();
+  }
+}
+
+void Context::upload_structure() {
+  const cudaStream_t s = stream_;
+  op_ = OperatorArgs{};
+  op_.Q = upload_csr(mem_, Q_, s);
+  op_.D = upload_csr(mem_, D_, s);
+  op_.Dt = upload_csr(mem_, host::transpose(D_), s);
+  op_.K = K_;
+  op_.N = N_;
+  std::vector<double> qinv = host::diagonal(Q_);  // inversion.cpp:210-211
+  for (double& v : qinv) v = 1.0 / v;
+  pa_ = PrecArgs{};
+  double* dq = mem_.alloc<double>(K_);
+  h2d(dq, qinv.data(), qinv.size(), s);
+  pa_.qinv = dq;
+  pa_.K = K_;
+  pa_.N = N_;
+  const int64_t n = K_ + N_;
+  b_ = mem_.alloc<double>(n);
+  x_ = mem_.alloc<double>(n);
+  r_ = mem_.alloc<double>(n);
+  az_ = mem_.alloc<double>(n);
+  tmp_ = mem_.alloc<double>(n);
+  tmp2_ = mem_.alloc<double>(n);
+  for (int k = 0; k < 3; ++k) {
+    V_[k] = mem_.alloc<double>(n);
+    W_[k] = mem_.alloc<double>(n);
+    U_[k] = mem_.alloc<double>(n);
+    Vk_[k] = V_[k] + K_;
+  }
+  for (int k = 0; k < 2; ++k) Z_[k] = mem_.alloc<double>(n);
+  io_a_ = mem_.alloc<double>(n);
+  io_b_ = mem_.alloc<double>(n);
+  io_c_ = mem_.alloc<double>(n);
+  io_d_ = mem_.alloc<double>(n);
+  const int64_t nb = (n + 255) / 256 + 16;
+  opart_ = mem_.alloc<double>(nb * 3);
+  fpart_ = mem_.alloc<double>(nb * 3);
+  upart_ = mem_.alloc<double>(nb * 3);
+  rpart_ = mem_.alloc<double>(nb * 3);
+  cpart_ = mem_.alloc<double>(nb * 3);
+  plan_ = row_gemv_plan(N_);
+  n_comb_blocks_ = static_cast<int>((K_ + 255) / 256 + (N_ + plan_.chunk - 1) / plan_.chunk);
+}
+
+void Context::upload_hierarchy() {
+  const cudaStream_t s = stream_;
+  const double omega = amg_.options.jacobi_damping;
+  lv_.clear();
+  vr_.assign(amg_.levels.size(), nullptr);
+  ve_.assign(amg_.levels.size(), nullptr);
+  vres_.assign(amg_.levels.size(), nullptr);
+  vx_.assign(amg_.levels.size(), nullptr);
+  for (size_t l = 0; l < amg_.levels.size(); ++l) {
+    const host::AmgLevel& L = amg_.levels[l];
+    DLevel d;
+    d.n = static_cast<int>(L.A.n_rows);
+    const bool last = (l + 1 == amg_.levels.size());
+    if (!last) {
+      d.A = upload_csr(mem_, L.A, s);
+      d.P = upload_csr(mem_, L.P, s);
+      d.R = upload_csr(mem_, host::transpose(L.P), s);
+      std::vector<double> wd(L.inv_diag.size());
+      for (size_t i = 0; i < wd.size(); ++i) wd[i] = omega * L.inv_diag[i];  // amg.cpp:98 (omega*inv_diag)*r
+      d.wd = mem_.alloc<double>(wd.size());
+      h2d(d.wd, wd.data(), wd.size(), s);
+      sync();
+      vres_[l] = mem_.alloc<double>(d.n);
+      vx_[l] = mem_.alloc<double>(d.n);
+    }
+    if (l > 0) {
+      vr_[l] = mem_.alloc<double>(d.n);
+      ve_[l] = mem_.alloc<double>(d.n);
+    }
+    lv_.push_back(d);
+  }
+  nc_ = static_cast<int>(amg_.nc);
+  const std::vector<double> inv = host::cholesky_inverse(amg_.nc, amg_.coarse_chol);
+  coarse_inv_ = mem_.alloc<double>(inv.size());
+  coarse_L_ = mem_.alloc<double>(amg_.coarse_chol.size());
+  h2d(coarse_inv_, inv.data(), inv.size(), s);
+  h2d(coarse_L_, amg_.coarse_chol.data(), amg_.coarse_chol.size(), s);
+  svc_ = mem_.alloc<double>(std::max<int64_t>(N_, 1));
+  sync();
+}
+
+// ----------------------------------------------------------------- V-cycle
+// amg.cpp:90-111, one symmetric V-cycle; level 0 input may be a ring slot.
+void Context::vcycle(VSel r0, double* out0, const MinresState* st) {
+  const cudaStream_t s = stream_;
+  const int L = static_cast<int>(lv_.size());
+  auto coarse = [&](VSel r, double* x) {
+    if (coarse_mode == 1)
+      coarse_cholesky(coarse_L_, nc_, r, x, st, 1, 1, s);
+    else
+      coarse_inverse(coarse_inv_, nc_, r, x, st, 1, s);
+  };
+  if (L == 1) {
+    coarse(r0, out0);
+    return;
+  }
+  for (int l = 0; l < L - 1; ++l) {
+    const VSel rl = l == 0 ? r0 : vfixed(vr_[l]);
+    vc_down(lv_[l], rl, vres_[l], st, s);
+    vc_restrict(lv_[l], vres_[l], vr_[l + 1], s);
+  }
+  coarse(vfixed(vr_[L - 1]), ve_[L - 1]);
+  for (int l = L - 2; l >= 0; --l) {
+    const VSel rl = l == 0 ? r0 : vfixed(vr_[l]);
+    vc_up1(lv_[l], rl, ve_[l + 1], vx_[l], st, s);
+    vc_up2(lv_[l], rl, vx_[l], l == 0 ? out0 : ve_[l], st, s);
+  }
+}
+
+// Multi-RHS V-cycle over b interleaved columns: r0/out0 are N x b.
+void Context::vcycle_batch(const double* r0, int b, double* out0) {
+  const cudaStream_t s = stream_;
+  const int L = static_cast<int>(lv_.size());
+  DeviceMemory work;
+  std::vector<double*> mr(L, nullptr), me(L, nullptr), mres(L, nullptr), mx(L, nullptr);
+  for (int l = 0; l < L; ++l) {
+    const size_t nl = static_cast<size_t>(lv_[l].n) * b;
+    if (l > 0) {
+      mr[l] = work.alloc<double>(nl);
+      me[l] = work.alloc<double>(nl);
+    }
+    if (l + 1 < L) {
+      mres[l] = work.alloc<double>(nl);
+      mx[l] = work.alloc<double>(nl);
+    }
+  }
+  auto coarse = [&](const double* r, double* x) {
+    if (coarse_mode == 1)
+      coarse_cholesky(coarse_L_, nc_, vfixed(const_cast<double*>(r)), x, st_plain_, b, b, s);
+    else
+      mcoarse_inverse(coarse_inv_, nc_, r, x, b, s);
+  };
+  if (L == 1) {
+    coarse(r0, out0);
+  } else {
+    for (int l = 0; l < L - 1; ++l) {
+      const double* rl = l == 0 ? r0 : mr[l];
+      mvc_down(lv_[l], rl, b, mres[l], b, s);
+      mvc_restrict(lv_[l], mres[l], mr[l + 1], b, s);
+    }
+    coarse(mr[L - 1], me[L - 1]);
+    for (int l = L - 2; l >= 0; --l) {
+      const double* rl = l == 0 ? r0 : mr[l];
+      mvc_up1(lv_[l], rl, b, me[l + 1], mx[l], b, s);
+      mvc_up2(lv_[l], rl, b, mx[l], l == 0 ? out0 : me[l], b, b, s);
+    }
+  }
+  sync();  // `work` is released at scope exit
+}
+
+// ------------------------------------------------------------ stage helpers
+double* Context::stage_in(const double* p, size_t n, double* dev) {
+  if (ptr_mode == 1) return const_cast<double*>(p);
+  h2d(dev, p, n, stream_);
+  return dev;
+}
+void Context::stage_out(double* host, const double* dev, size_t n) {
+  if (ptr_mode == 1) {
+    if (host != dev) GNW_CUDA_CHECK(cudaMemcpyAsync(host, dev, n * sizeof(double), cudaMemcpyDeviceToDevice, stream_));
+    sync();
+    return;
+  }
+  GNW_CUDA_CHECK(cudaMemcpyAsync(host, dev, n * sizeof(double), cudaMemcpyDeviceToHost, stream_));
+  sync();
+}
+
+// ------------------------------------------------------------- Jacobian
+void Context::set_jacobian(const double* J, int64_t m, int64_t n_cells, double beta, double timings[3]) {
+  require_mixed();
+  if (timings) timings[0] = timings[1] = timings[2] = 0.0;
+  if (m > 0 && !(beta > 0.0)) throw std::invalid_argument("build_woodbury_preconditioner: beta <= 0");
+  if (m > 0 && n_cells != N_) throw std::invalid_argument("build_woodbury_preconditioner: J shape mismatch");
+  require_device();
+  destroy_graph();
+  jmem_.reset();
+  dJ_ = dHt_ = dC_ = dL_ = dCinv_ = dY_ = nullptr;
+  m_ = m;
+  beta_ = beta;
+  op_.J = nullptr;
+  op_.m = 0;
+  op_.neg_inv_beta = -1.0 / beta;
+  pa_.m = 0;
+  pa_.Ht = pa_.Cinv = pa_.Lc = nullptr;
+  pa_.neg_inv_beta = -1.0 / beta;
+  if (m == 0) return;  // Laplace-only preconditioner (inversion.cpp:251-256)
+  if (m > 8192) throw std::invalid_argument("gnw_set_jacobian: m > 8192 not supported");
+
+  const cudaStream_t s = stream_;
+  jmem_ = std::make_unique<DeviceMemory>();
+  DeviceMemory& jm = *jmem_;
+  const size_t mN = static_cast<size_t>(m) * N_;
+  dJ_ = jm.alloc<double>(mN);
+  u_ = jm.alloc<double>(m);
+  gpart_ = jm.alloc<double>(static_cast<size_t>(plan_.nchunks) * m);
+  if (ptr_mode == 1)
+    GNW_CUDA_CHECK(cudaMemcpyAsync(dJ_, J, mN * sizeof(double), cudaMemcpyDeviceToDevice, s));
+  else
+    GNW_CUDA_CHECK(cudaMemcpyAsync(dJ_, J, mN * sizeof(double), cudaMemcpyHostToDevice, s));
+  op_.J = dJ_;
+  op_.m = static_cast<int>(m);
+  if (pc_laplace) {  // Alg. 4: J stays in the operator, plain Laplace preconditioner
+    sync();
+    return;
+  }
+  dHt_ = jm.alloc<double>(mN);
+  dC_ = jm.alloc<double>(m * m);
+  dL_ = jm.alloc<double>(m * m);
+  dCinv_ = jm.alloc<double>(m * m);
+  dY_ = jm.alloc<double>(m * m);
+  t_ = jm.alloc<double>(m);
+  t2_ = jm.alloc<double>(m);
+  tpart_ = jm.alloc<double>(static_cast<size_t>(plan_.nchunks) * m);
+
+  cudaEvent_t ev[4];
+  for (auto& e : ev) GNW_CUDA_CHECK(cudaEventCreate(&e));
+  const uint64_t l0 = launch_count();
+  GNW_CUDA_CHECK(cudaEventRecord(ev[0], s));
+  // H = S_hat^-1 J^T by batched V-cycles (inversion.cpp:107-114); stored as Ht (m x N)
+  {
+    size_t free_b = 0, total_b = 0;
+    cudaMemGetInfo(&free_b, &total_b);
+    const double per_col = 8.0 * static_cast<double>(N_) * 6.0;  // level-0 arrays x ~2 for coarser levels
+    int64_t bmax = static_cast<int64_t>(0.5 * static_cast<double>(free_b) / per_col);
+    bmax = std::max<int64_t>(32, std::min<int64_t>(bmax, 512) / 32 * 32);
+    const int b = static_cast<int>(std::min<int64_t>(((m + 31) / 32) * 32, bmax));
+    DeviceMemory bm;
+    double* R0 = bm.alloc<double>(static_cast<size_t>(N_) * b);
+    double* X0 = bm.alloc<double>(static_cast<size_t>(N_) * b);
+    for (int64_t i0 = 0; i0 < m; i0 += b) {
+      const int bb = static_cast<int>(std::min<int64_t>(b, m - i0));
+      transpose_rows_to_batch(dJ_, N_, static_cast<int>(i0), bb, R0, s);
+      vcycle_batch(R0, bb, X0);
+      transpose_batch_to_rows(X0, N_, static_cast<int>(i0), bb, dHt_, s);
+    }
+    GNW_CUDA_CHECK(cudaEventRecord(ev[1], s));
+    sync();
+  }
+  // C = I + (J H)/beta (inversion.cpp:37-43), lower triangle
+  DgemmPlan plan = dgemm_plan(static_cast<int>(m), N_, 0, sm_count_);
+  {
+    DeviceMemory pm;
+    double* part = pm.alloc<double>(static_cast<size_t>(plan.splits) * plan.npairs * plan.tile * plan.tile + 2 * 4096);
+    capacitance_dgemm(dJ_, dHt_, static_cast<int>(m), N_, beta, plan, part, dC_, s);
+    GNW_CUDA_CHECK(cudaEventRecord(ev[2], s));
+    // L = chol(C), retry once after symmetrisation (inversion.cpp:21-35)
+    cholesky(dC_, dL_, static_cast<int>(m), dflag_, s);
+    int fail = 0;
+    GNW_CUDA_CHECK(cudaMemcpyAsync(&fail, dflag_, sizeof(int), cudaMemcpyDeviceToHost, s));
+    sync();
+    if (fail) {
+      DgemmPlan full = dgemm_plan(static_cast<int>(m), N_, 1, sm_count_);
+      DeviceMemory pm2;
+      double* part2 = pm2.alloc<double>(static_cast<size_t>(full.splits) * full.npairs * full.tile * full.tile + 2 * 4096);
+      capacitance_dgemm(dJ_, dHt_, static_cast<int>(m), N_, beta, full, part2, dC_, s);
+      symmetrize(dC_, static_cast<int>(m), s);
+      cholesky(dC_, dL_, static_cast<int>(m), dflag_, s);
+      GNW_CUDA_CHECK(cudaMemcpyAsync(&fail, dflag_, sizeof(int), cudaMemcpyDeviceToHost, s));
+      sync();
+      if (fail) throw std::runtime_error("dense_cholesky: matrix not positive definite");
+    }
+    cholesky_inverse(dL_, dY_, dCinv_, static_cast<int>(m), s);
+    GNW_CUDA_CHECK(cudaEventRecord(ev[3], s));
+    sync();
+  }
+  float ms[3];
+  for (int k = 0; k < 3; ++k) GNW_CUDA_CHECK(cudaEventElapsedTime(&ms[k], ev[k], ev[k + 1]));
+  for (auto& e : ev) cudaEventDestroy(e);
+  if (timings) {
+    timings[0] = ms[0] * 1e-3;
+    timings[1] = ms[1] * 1e-3;
+    timings[2] = ms[2] * 1e-3;
+  }
+  setup_launches = launch_count() - l0;
+  pa_.m = static_cast<int>(m);
+  pa_.Ht = dHt_;
+  pa_.Cinv = dCinv_;
+  pa_.Lc = dL_;
+}
+
+// --------------------------------------------------------------- operator
+void Context::operator_into(VSel x, int scaled, VSel y, MinresState* st, int loop) {
+  if (m_ > 0) {
+    VSel xs = x;  // J acts on the cell part
+    row_gemv(dJ_, static_cast<int>(m_), N_, xs, K_, scaled, st, gpart_, counters_ + 0, u_, plan_, stream_);
+  }
+  saddle_operator(op_, x, scaled, u_, y, st, loop, opart_, counters_ + 1, stream_);
+}
+
+void Context::apply_operator(const double* x, double* y) {
+  require_mixed();
+  require_device();
+  const size_t n = K_ + N_;
+  double* dx = stage_in(x, n, io_a_);
+  double* dy = ptr_mode == 1 ? y : io_b_;
+  operator_into(vfixed(dx), 0, vfixed(dy), st_plain_, 0);
+  stage_out(y, dy, n);
+}
+
+// z = P^-1 y.  In the loop, y = v_next is formed on the fly from Az, v_cur, v_prev.
+void Context::precondition_into(VSel y, VSel yv2, VSel z, MinresState* st, int loop, VSel vcur, VSel vprev) {
+  pa_.exact = coarse_mode;
+  combine_precondition(pa_, loop ? vfixed(az_) : y, vcur, vprev, y, z, loop, st, nullptr, cpart_, tpart_,
+                       counters_ + 2, t_, plan_, stream_);
+  vcycle(yv2, svc_, st);
+  capacitance_solve(pa_, t_, t2_, stream_);
+  finish_precondition(pa_, svc_, t2_, y, z, loop, st, cpart_, n_comb_blocks_, fpart_, counters_ + 3, stream_);
+}
+
+void Context::precondition(const double* y, double* z) {
+  require_mixed();
+  require_device();
+  const size_t n = K_ + N_;
+  double* dy = stage_in(y, n, io_a_);
+  double* dz = ptr_mode == 1 ? z : io_b_;
+  precondition_into(vfixed(dy), vfixed(dy + K_), vfixed(dz), st_plain_, 0, vfixed(dy), vfixed(dy));
+  stage_out(z, dz, n);
+}
+
+void Context::amg_apply(const double* r, double* z) {
+  if (!assembled_) throw std::invalid_argument("amg_apply: empty hierarchy");
+  require_device();
+  const size_t n = N_;
+  double* dr = stage_in(r, n, io_a_);
+  double* dz = ptr_mode == 1 ? z : io_b_;
+  vcycle(vfixed(dr), dz, st_plain_);
+  stage_out(z, dz, n);
+}
+
+void Context::assemble_rhs(const double* mdl, const double* mref, const double* g, const double* gobs, double* rhs) {
+  require_mixed();
+  require_device();
+  if (m_ == 0) throw std::invalid_argument("assemble_gn_rhs: shape mismatch");
+  std::vector<double> dg(m_);
+  std::vector<double> hg(m_), hgo(m_);
+  if (ptr_mode == 1) {
+    GNW_CUDA_CHECK(cudaMemcpy(hg.data(), g, m_ * sizeof(double), cudaMemcpyDeviceToHost));
+    GNW_CUDA_CHECK(cudaMemcpy(hgo.data(), gobs, m_ * sizeof(double), cudaMemcpyDeviceToHost));
+  } else {
+    std::memcpy(hg.data(), g, m_ * sizeof(double));
+    std::memcpy(hgo.data(), gobs, m_ * sizeof(double));
+  }
+  for (int64_t i = 0; i < m_; ++i) dg[i] = hg[i] - hgo[i];  // inversion.cpp:137-138
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  double* dm = stage_in(mdl, N_, io_a_);
+  double* dmr = stage_in(mref, N_, io_b_);
+  h2d(u_, dg.data(), m_, stream_);
+  double* dr = ptr_mode == 1 ? rhs : io_c_;
+  cudaEventRecord(e0, stream_);
+  gnw::assemble_rhs(op_, beta_, dm, dmr, u_, dr, stream_);
+  cudaEventRecord(e1, stream_);
+  stage_out(rhs, dr, K_ + N_);
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, e0, e1);
+  t_rhs = ms * 1e-3;
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+}
+
+// ------------------------------------------------------------------ MINRES
+void Context::build_graph() {
+  destroy_graph();
+  cudaGraph_t g;
+  GNW_CUDA_CHECK(cudaGraphCreate(&g, 0));
+  cudaGraphConditionalHandle h;
+  GNW_CUDA_CHECK(cudaGraphConditionalHandleCreate(&h, g, 1, cudaGraphCondAssignDefault));
+  alignas(cudaGraphNodeParams) unsigned char pbuf[sizeof(cudaGraphNodeParams)] = {};
+  cudaGraphNodeParams& p = *reinterpret_cast<cudaGraphNodeParams*>(pbuf);
+  p.type = cudaGraphNodeTypeConditional;
+  p.conditional.handle = h;
+  p.conditional.type = cudaGraphCondTypeWhile;
+  p.conditional.size = 1;
+  cudaGraphNode_t node;
+  GNW_CUDA_CHECK(cudaGraphAddNode(&node, g, nullptr, 0, &p));
+  cudaGraph_t body = p.conditional.phGraph_out[0];
+  const uint64_t l0 = launch_count();
+  GNW_CUDA_CHECK(cudaStreamBeginCaptureToGraph(stream_, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
+  // iteration j: v_prev = V[j%3], v_cur = V[(j+1)%3], v_next = V[(j+2)%3] (same for w, u);
+  //              z_cur = Z[j%2], z_next = Z[(j+1)%2]
+  try {
+    operator_into(ring2(Z_, 0), 1, vfixed(az_), st_, 1);                      // Az = A zhat, delta
+    precondition_into(ring3(V_, 2), ring3(Vk_, 2), ring2(Z_, 1), st_, 1,       // v_next, z_next = P^-1 v_next,
+                      ring3(V_, 1), ring3(V_, 0));                             // gamma_next, Givens
+    minres_update(K_ + N_, ring2(Z_, 0), vfixed(az_), ring3(W_, 0), ring3(W_, 1), ring3(W_, 2), ring3(U_, 0),
+                  ring3(U_, 1), ring3(U_, 2), x_, r_, st_, hist_e_, hist_p_, hist_cap_, upart_, counters_ + 4,
+                  static_cast<unsigned long long>(h), 1, stream_);
+  } catch (...) {
+    cudaGraph_t dummy;
+    cudaStreamEndCapture(stream_, &dummy);
+    cudaGraphDestroy(g);
+    throw;
+  }
+  GNW_CUDA_CHECK(cudaStreamEndCapture(stream_, &body));
+  graph_nodes_ = launch_count() - l0;
+  GNW_CUDA_CHECK(cudaGraphInstantiate(&graph_exec_, g, 0));
+  graph_ = g;
+}
+
+MinresResult Context::minres(const double* b, const double* x0, double* x, double tol, uint64_t maxit) {
+  if (!(tol > 0.0)) throw std::invalid_argument("minres: tol must be positive");
+  require_mixed();
+  require_device();
+  const int64_t n = K_ + N_;
+  const cudaStream_t s = stream_;
+  MinresResult res;
+  const uint64_t l0 = launch_count();
+  uint64_t graph_iters = 0;
+  uint64_t built_now = 0;
+
+  const long long cap = static_cast<long long>(std::min<uint64_t>(maxit, 4u << 20)) + 1;
+  if (cap > hist_cap_) {
+    destroy_graph();
+    hist_e_ = mem_.alloc<double>(cap);
+    hist_p_ = mem_.alloc<double>(cap);
+    hist_cap_ = cap;
+  }
+  cudaEvent_t e0, e1;
+  GNW_CUDA_CHECK(cudaEventCreate(&e0));
+  GNW_CUDA_CHECK(cudaEventCreate(&e1));
+  if (ptr_mode == 1) {
+    GNW_CUDA_CHECK(cudaMemcpyAsync(b_, b, n * sizeof(double), cudaMemcpyDeviceToDevice, s));
+    GNW_CUDA_CHECK(cudaMemcpyAsync(x_, x0, n * sizeof(double), cudaMemcpyDeviceToDevice, s));
+  } else {
+    h2d(b_, b, n, s);
+    h2d(x_, x0, n, s);
+  }
+  GNW_CUDA_CHECK(cudaEventRecord(e0, s));
+  auto read_plain = [&]() {
+    GNW_CUDA_CHECK(cudaMemcpyAsync(h_st_ + 1, st_plain_, sizeof(MinresState), cudaMemcpyDeviceToHost, s));
+    sync();
+    return h_st_[1];
+  };
+  // r = b - A x  (and ||b||)
+  operator_into(vfixed(x_), 0, vfixed(az_), st_plain_, 0);
+  residual(n, b_, az_, r_, st_plain_, 1, rpart_, counters_ + 5, s);
+  MinresState ps = read_plain();
+  const double bnorm = std::sqrt(ps.scratch[5]);
+  auto finish = [&]() {
+    GNW_CUDA_CHECK(cudaEventRecord(e1, s));
+    sync();
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, e0, e1);
+    t_minres = ms * 1e-3;
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    launches = launch_count() - l0 - built_now + graph_iters * graph_nodes_;
+    stage_out(x, x_, n);
+  };
+  if (bnorm == 0.0) {  // minres.cpp:32-39
+    res.converged = (ps.scratch[4] == 0.0);
+    res.hist_e.push_back(0.0);
+    res.hist_p.push_back(0.0);
+    finish();
+    return res;
+  }
+  // z = P^-1 r, gamma_1 (minres.cpp:44-47)
+  precondition_into(vfixed(r_), vfixed(r_ + K_), vfixed(Z_[1]), st_plain_, 0, vfixed(r_), vfixed(r_));
+  ps = read_plain();
+  const double gamma_sq0 = ps.scratch[0];
+  if (gamma_sq0 < 0.0) throw std::runtime_error("minres: preconditioner is not positive definite");
+  const double gamma1 = std::sqrt(gamma_sq0);
+  const double rel0 = std::sqrt(ps.scratch[4]) / bnorm;  // residual kernel's ||r||^2 (scratch[4] untouched since)
+  res.hist_e.push_back(rel0);
+  res.hist_p.push_back(1.0);
+  if (rel0 <= tol) {
+    res.converged = true;
+    res.true_rel = rel0;
+    finish();
+    return res;
+  }
+  if (gamma1 == 0.0) throw std::runtime_error("minres: breakdown (zero preconditioned residual, nonzero residual)");
+  // initial vectors (minres.cpp:60-63): v_prev = V[1] = 0, v_cur = V[2] = r, w/u = 0
+  fill_zero(V_[1], n, s);
+  GNW_CUDA_CHECK(cudaMemcpyAsync(V_[2], r_, n * sizeof(double), cudaMemcpyDeviceToDevice, s));
+  for (int k = 1; k < 3; ++k) {
+    fill_zero(W_[k], n, s);
+    fill_zero(U_[k], n, s);
+  }
+  MinresState st;
+  std::memset(&st, 0, sizeof st);
+  st.gamma_prev = 1.0;
+  st.gamma_cur = gamma1;
+  st.c_prev = st.c_cur = 1.0;
+  st.s_prev = st.s_cur = 0.0;
+  st.eta = gamma1;
+  st.gamma1 = gamma1;
+  st.bnorm = bnorm;
+  st.tol = tol;
+  st.exhausted_tol = 1e-13 * gamma1;
+  st.inv_gamma = 1.0 / gamma1;
+  st.j = 1;
+  st.maxit = static_cast<long long>(maxit);
+  st.status = maxit >= 1 ? kRunning : kMaxit;
+  *h_st_ = st;
+  GNW_CUDA_CHECK(cudaMemcpyAsync(st_, h_st_, sizeof(MinresState), cudaMemcpyHostToDevice, s));
+  if (!graph_exec_) {
+    build_graph();
+    built_now = graph_nodes_;
+  }
+  std::vector<std::pair<uint64_t, double>> overrides;  // verified residuals replace recurred ones
+  auto true_residual_rel = [&](double* rout) {
+    operator_into(vfixed(x_), 0, vfixed(tmp2_), st_plain_, 0);
+    residual(n, b_, tmp2_, rout, st_plain_, 0, rpart_, counters_ + 5, s);
+    const MinresState q = read_plain();
+    return std::sqrt(q.scratch[4]) / bnorm;
+  };
+  bool done = false;
+  while (!done) {
+    MinresState cur;
+    if (h_st_->status == kRunning) {
+      GNW_CUDA_CHECK(cudaGraphLaunch(graph_exec_, s));
+      GNW_CUDA_CHECK(cudaMemcpyAsync(h_st_, st_, sizeof(MinresState), cudaMemcpyDeviceToHost, s));
+      sync();
+    }
+    cur = *h_st_;
+    graph_iters = static_cast<uint64_t>(cur.iterations);
+    switch (cur.status) {
+      case kErrNotPD: throw std::runtime_error("minres: preconditioner is not positive definite");
+      case kErrStagnated: throw std::runtime_error("minres: breakdown (stagnated rotation)");
+      case kVerify: {  // minres.cpp:108-120: r <- b - A x
+        const double rel_true = true_residual_rel(r_);
+        overrides.emplace_back(cur.iterations, rel_true);
+        if (rel_true <= 10.0 * tol) {
+          res.converged = true;
+          res.true_rel = rel_true;
+          done = true;
+          break;
+        }
+        if (cur.gamma_next <= cur.exhausted_tol) {
+          h_st_->status = kExhausted;
+          continue;
+        }
+        minres_rotate(st_, s);
+        GNW_CUDA_CHECK(cudaMemcpyAsync(h_st_, st_, sizeof(MinresState), cudaMemcpyDeviceToHost, s));
+        sync();
+        break;
+      }
+      case kExhausted: {  // minres.cpp:122-133
+        const double rel_true = true_residual_rel(tmp_);
+        res.true_rel = rel_true;
+        if (rel_true <= 10.0 * tol) {
+          res.converged = true;
+          done = true;
+          break;
+        }
+        throw std::runtime_error("minres: breakdown (Krylov space exhausted before convergence)");
+      }
+      case kMaxit: {  // minres.cpp:150-154
+        res.true_rel = true_residual_rel(tmp_);
+        res.converged = false;
+        done = true;
+        break;
+      }
+      default: throw DeviceError("minres: unexpected device status");
+    }
+  }
+  res.iterations = static_cast<uint64_t>(h_st_->iterations);
+  const uint64_t nh = std::min<uint64_t>(res.iterations + 1, static_cast<uint64_t>(hist_cap_));
+  std::vector<double> he(nh), hp(nh);
+  GNW_CUDA_CHECK(cudaMemcpyAsync(he.data(), hist_e_, nh * sizeof(double), cudaMemcpyDeviceToHost, s));
+  GNW_CUDA_CHECK(cudaMemcpyAsync(hp.data(), hist_p_, nh * sizeof(double), cudaMemcpyDeviceToHost, s));
+  sync();
+  for (uint64_t k = 1; k < nh; ++k) {
+    res.hist_e.push_back(he[k]);
+    res.hist_p.push_back(hp[k]);
+  }
+  for (auto& ov : overrides)
+    if (ov.first < res.hist_e.size()) res.hist_e[ov.first] = ov.second;
+  finish();
+  return res;
+}
+
+void Context::get_woodbury(double* H, double* L) {
+  require_device();
+  if (m_ == 0 || pa_.m == 0) return;
+  if (H) {
+    std::vector<double> ht(static_cast<size_t>(m_) * N_);
+    GNW_CUDA_CHECK(cudaMemcpy(ht.data(), dHt_, ht.size() * sizeof(double), cudaMemcpyDeviceToHost));
+    for (int64_t i = 0; i < m_; ++i)
+      for (int64_t c = 0; c < N_; ++c) H[c * m_ + i] = ht[i * N_ + c];
+  }
+  if (L) GNW_CUDA_CHECK(cudaMemcpy(L, dL_, m_ * m_ * sizeof(double), cudaMemcpyDeviceToHost));
+}
+
+void Context::dense_cholesky(int64_t n, const double* C, double* L) {
+  require_device();
+  DeviceMemory tm;
+  double* dC = tm.alloc<double>(n * n);
+  double* dL = tm.alloc<double>(n * n);
+  h2d(dC, C, n * n, stream_);
+  gnw::cholesky(dC, dL, static_cast<int>(n), dflag_, stream_);
+  int fail = 0;
+  GNW_CUDA_CHECK(cudaMemcpyAsync(&fail, dflag_, sizeof(int), cudaMemcpyDeviceToHost, stream_));
+  GNW_CUDA_CHECK(cudaMemcpyAsync(L, dL, n * n * sizeof(double), cudaMemcpyDeviceToHost, stream_));
+  sync();
+  if (fail) throw std::runtime_error("dense_cholesky: matrix not positive definite");
+}
+
+}  // namespace gnw

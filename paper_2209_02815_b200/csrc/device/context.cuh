@@ -1,0 +1,157 @@
+// context.cuh -- the device-resident solver context behind the gnw C-ABI.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../host/setup.hpp"
+#include "kernels.cuh"
+
+namespace gnw {
+
+struct DeviceError : std::runtime_error {
+  DeviceError(const char* expr, cudaError_t e, const char* file, int line)
+      : std::runtime_error(std::string("CUDA error ") + cudaGetErrorString(e) + " in " + expr + " (" + file + ":" +
+                           std::to_string(line) + ")") {}
+  explicit DeviceError(const std::string& s) : std::runtime_error(s) {}
+};
+
+// Device allocation owned by the context (bytes tracked for gnw_info).
+struct DeviceMemory {
+  std::vector<void*> ptrs;
+  size_t bytes = 0;
+  template <class T>
+  T* alloc(size_t count) {
+    void* p = nullptr;
+    const size_t nb = std::max<size_t>(count, 1) * sizeof(T);
+    GNW_CUDA_CHECK(cudaMalloc(&p, nb));
+    ptrs.push_back(p);
+    bytes += nb;
+    return static_cast<T*>(p);
+  }
+  void release_all();
+  ~DeviceMemory() { release_all(); }
+};
+
+struct MinresResult {
+  std::vector<double> hist_e, hist_p;
+  uint64_t iterations = 0;
+  bool converged = false;
+  double true_rel = 0.0;
+};
+
+class Context {
+ public:
+  explicit Context(int device);  // device < 0: host-only context (setup and export only)
+  ~Context();
+
+  bool has_device() const { return device_ >= 0; }
+  int ptr_mode = 0;
+  int coarse_mode = 0;
+  int pc_laplace = 0;  // GnAlgorithm::kLaplaceMinres (inversion.cpp:251-256)
+
+  void assemble(const double* vertices, int64_t nv, const int64_t* cells, int64_t nc, const host::AmgOptions& o);
+  void assemble_amg_csr(int64_t n, const int64_t* rowptr, const int64_t* cols, const double* vals,
+                        const host::AmgOptions& o);
+  void set_jacobian(const double* J, int64_t m, int64_t n_cells, double beta, double timings[3]);
+  void apply_operator(const double* x, double* y);
+  void precondition(const double* y, double* z);
+  void amg_apply(const double* r, double* z);
+  void assemble_rhs(const double* mdl, const double* mref, const double* g, const double* gobs, double* rhs);
+  MinresResult minres(const double* b, const double* x0, double* x, double tol, uint64_t maxit);
+  void get_woodbury(double* H, double* L);
+  void dense_cholesky(int64_t n, const double* C, double* L);
+
+  // structure
+  const host::Mesh& mesh() const { return mesh_; }
+  const host::Csr& Q() const { return Q_; }
+  const host::Csr& D() const { return D_; }
+  const host::Csr& S() const { return S_; }
+  const host::AmgHierarchy& amg() const { return amg_; }
+  bool mixed() const { return mixed_; }
+  bool assembled() const { return assembled_; }
+  int64_t K() const { return K_; }
+  int64_t N() const { return N_; }
+  int64_t m() const { return m_; }
+  double beta() const { return beta_; }
+  size_t device_bytes() const { return mem_.bytes + (jmem_ ? jmem_->bytes : 0); }
+
+  double t_minres = 0.0, t_rhs = 0.0;
+  uint64_t launches = 0, setup_launches = 0;
+
+ private:
+  void require_device() const;
+  void require_mixed() const;
+  void upload_structure();
+  void upload_hierarchy();
+  void vcycle(VSel r0, double* out0, const MinresState* st);
+  void vcycle_batch(const double* r0, int b, double* out0);
+  void operator_into(VSel x, int scaled, VSel y, MinresState* st, int loop);
+  void precondition_into(VSel y, VSel yv2, VSel z, MinresState* st, int loop, VSel vcur, VSel vprev);
+  void build_graph();
+  void destroy_graph();
+  double* stage_in(const double* p, size_t n, double* dev);
+  void stage_out(double* host, const double* dev, size_t n);
+  void sync();
+
+  int device_ = -1;
+  cudaStream_t stream_ = nullptr;
+  int sm_count_ = 148;
+  DeviceMemory mem_;                      // structure + hierarchy + work vectors
+  std::unique_ptr<DeviceMemory> jmem_;    // Jacobian-dependent buffers
+
+  bool assembled_ = false, mixed_ = false;
+  host::Mesh mesh_;
+  host::Csr Q_, D_, S_;
+  host::AmgHierarchy amg_;
+  int64_t K_ = 0, N_ = 0;
+
+  // device structure
+  OperatorArgs op_{};
+  PrecArgs pa_{};
+  std::vector<DLevel> lv_;
+  double* coarse_inv_ = nullptr;
+  double* coarse_L_ = nullptr;
+  int nc_ = 0;
+  std::vector<double*> vr_, ve_, vres_, vx_;  // single-RHS V-cycle work per level
+  double* svc_ = nullptr;                     // V-cycle output (s)
+
+  // Jacobian / Woodbury
+  int64_t m_ = 0;
+  double beta_ = 1.0;
+  double *dJ_ = nullptr, *dHt_ = nullptr, *dC_ = nullptr, *dL_ = nullptr, *dCinv_ = nullptr, *dY_ = nullptr;
+  double *u_ = nullptr, *t_ = nullptr, *t2_ = nullptr;
+  double *gpart_ = nullptr, *tpart_ = nullptr;
+  RowGemv plan_{};
+
+  // MINRES vectors
+  double *b_ = nullptr, *x_ = nullptr, *r_ = nullptr, *az_ = nullptr, *tmp_ = nullptr, *tmp2_ = nullptr;
+  double* V_[3] = {};
+  double* W_[3] = {};
+  double* U_[3] = {};
+  double* Z_[2] = {};
+  double* Vk_[3] = {};  // V_[k] + K (cell part), V-cycle input ring
+  double *opart_ = nullptr, *cpart_ = nullptr, *fpart_ = nullptr, *upart_ = nullptr, *rpart_ = nullptr;
+  unsigned* counters_ = nullptr;  // 8 counters
+  MinresState* st_ = nullptr;     // loop state
+  MinresState* st_plain_ = nullptr;
+  MinresState* h_st_ = nullptr;   // pinned host mirror
+  double *hist_e_ = nullptr, *hist_p_ = nullptr;
+  long long hist_cap_ = 0;
+  double* io_a_ = nullptr;        // device staging for host-pointer mode
+  double* io_b_ = nullptr;
+  double* io_c_ = nullptr;
+  double* io_d_ = nullptr;
+  int* dflag_ = nullptr;
+
+  cudaGraph_t graph_ = nullptr;
+  cudaGraphExec_t graph_exec_ = nullptr;
+  uint64_t graph_nodes_ = 0;
+  int n_comb_blocks_ = 0;
+};
+
+}  // namespace gnw

@@ -1,0 +1,253 @@
+// gnw_capi.cu -- extern "C" boundary (include/gnw.h) over gnw::Context.
+// Exceptions map to status codes exactly as SURVEY.md 8(b) specifies:
+// std::invalid_argument -> GNW_INVALID_ARGUMENT, gnw::DeviceError -> GNW_DEVICE,
+// any other std::exception -> GNW_NUMERICAL; the message text is the
+// reference's exception text.
+#include <cstring>
+#include <string>
+
+#include "../../../include/gnw.h"
+#include "context.cuh"
+
+using gnw::Context;
+
+struct gnw_ctx {
+  Context* c = nullptr;
+};
+
+namespace {
+thread_local std::string g_err;
+
+template <class F>
+gnw_status guard(F&& f) {
+  try {
+    f();
+    return GNW_OK;
+  } catch (const std::invalid_argument& e) {
+    g_err = e.what();
+    return GNW_INVALID_ARGUMENT;
+  } catch (const gnw::DeviceError& e) {
+    g_err = e.what();
+    return GNW_DEVICE;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return GNW_NUMERICAL;
+  }
+}
+
+gnw::host::AmgOptions to_opts(const gnw_amg_options* o) {
+  gnw::host::AmgOptions a;
+  if (o) {
+    a.coarse_threshold = static_cast<int64_t>(o->coarse_threshold);
+    a.strength = o->strength;
+    a.jacobi_damping = o->jacobi_damping;
+    a.prolongation_damping = o->prolongation_damping;
+    a.max_aggregate_size = static_cast<int64_t>(o->max_aggregate_size);
+    a.max_levels = static_cast<int64_t>(o->max_levels);
+  }
+  return a;
+}
+
+Context& ctx_of(gnw_ctx* c) {
+  if (!c || !c->c) throw std::invalid_argument("gnw: null context");
+  return *c->c;
+}
+const Context& ctx_of(const gnw_ctx* c) {
+  if (!c || !c->c) throw std::invalid_argument("gnw: null context");
+  return *c->c;
+}
+}  // namespace
+
+extern "C" {
+
+const char* gnw_last_error(void) { return g_err.c_str(); }
+const char* gnw_version(void) { return "gnw-b200 0.1 (sm_100a, FP64)"; }
+
+gnw_status gnw_create(int n_devices, const int* devices, gnw_ctx** out) {
+  return guard([&] {
+    if (!out) throw std::invalid_argument("gnw_create: null output");
+    *out = nullptr;
+    if (n_devices > 1) throw std::invalid_argument("gnw_create: one device per context (one process per GPU)");
+    const int dev = n_devices == 0 ? -1 : (devices ? devices[0] : 0);
+    auto* h = new gnw_ctx;
+    try {
+      h->c = new Context(dev);
+    } catch (...) {
+      delete h;
+      throw;
+    }
+    *out = h;
+  });
+}
+
+void gnw_destroy(gnw_ctx* ctx) {
+  if (!ctx) return;
+  delete ctx->c;
+  delete ctx;
+}
+
+gnw_status gnw_set_pointer_mode(gnw_ctx* ctx, int mode) {
+  return guard([&] {
+    if (mode != GNW_HOST_POINTERS && mode != GNW_DEVICE_POINTERS) throw std::invalid_argument("gnw_set_pointer_mode: bad mode");
+    ctx_of(ctx).ptr_mode = mode;
+  });
+}
+
+gnw_status gnw_set_coarse_mode(gnw_ctx* ctx, int mode) {
+  return guard([&] {
+    if (mode != GNW_COARSE_INVERSE && mode != GNW_COARSE_CHOLESKY) throw std::invalid_argument("gnw_set_coarse_mode: bad mode");
+    ctx_of(ctx).coarse_mode = mode;
+  });
+}
+
+gnw_status gnw_set_preconditioner(gnw_ctx* ctx, int kind) {
+  return guard([&] {
+    if (kind != GNW_PC_WOODBURY && kind != GNW_PC_LAPLACE) throw std::invalid_argument("gnw_set_preconditioner: bad kind");
+    ctx_of(ctx).pc_laplace = kind;
+  });
+}
+
+gnw_status gnw_assemble(gnw_ctx* ctx, const gnw_mesh* mesh, const gnw_amg_options* opts) {
+  return guard([&] {
+    if (!mesh || !mesh->vertices || !mesh->cells) throw std::invalid_argument("gnw_assemble: null mesh");
+    ctx_of(ctx).assemble(mesh->vertices, static_cast<int64_t>(mesh->n_vertices), mesh->cells,
+                         static_cast<int64_t>(mesh->n_cells), to_opts(opts));
+  });
+}
+
+gnw_status gnw_assemble_amg_csr(gnw_ctx* ctx, uint64_t n, const int64_t* rowptr, const int64_t* cols,
+                                const double* vals, const gnw_amg_options* opts) {
+  return guard([&] {
+    ctx_of(ctx).assemble_amg_csr(static_cast<int64_t>(n), rowptr, cols, vals, to_opts(opts));
+  });
+}
+
+gnw_status gnw_get_info(const gnw_ctx* ctx, gnw_info* info) {
+  return guard([&] {
+    const Context& c = ctx_of(ctx);
+    std::memset(info, 0, sizeof *info);
+    info->K = c.K();
+    info->N = c.N();
+    info->n_vertices = c.mesh().nv;
+    info->n_edges = c.mesh().ne;
+    info->n_boundary_edges = c.mesh().boundary_edges.size();
+    info->n_levels = c.amg().levels.size();
+    info->coarse_n = c.amg().nc;
+    info->m = c.m();
+    info->beta = c.beta();
+    info->device_bytes = c.device_bytes();
+  });
+}
+
+gnw_status gnw_set_jacobian(gnw_ctx* ctx, const double* J, uint64_t m, uint64_t n_cells, double beta,
+                            gnw_timings* timings) {
+  return guard([&] {
+    double t[3] = {0, 0, 0};
+    ctx_of(ctx).set_jacobian(J, static_cast<int64_t>(m), static_cast<int64_t>(n_cells), beta, t);
+    if (timings) {
+      timings->t_H = t[0];
+      timings->t_C = t[1];
+      timings->t_chol = t[2];
+    }
+  });
+}
+
+gnw_status gnw_apply_operator(gnw_ctx* ctx, const double* x, double* y) {
+  return guard([&] { ctx_of(ctx).apply_operator(x, y); });
+}
+gnw_status gnw_precondition(gnw_ctx* ctx, const double* y, double* z) {
+  return guard([&] { ctx_of(ctx).precondition(y, z); });
+}
+gnw_status gnw_amg_apply(gnw_ctx* ctx, const double* r, double* z) {
+  return guard([&] { ctx_of(ctx).amg_apply(r, z); });
+}
+gnw_status gnw_get_woodbury(gnw_ctx* ctx, double* H, double* L) {
+  return guard([&] { ctx_of(ctx).get_woodbury(H, L); });
+}
+gnw_status gnw_assemble_rhs(gnw_ctx* ctx, const double* m, const double* m_ref, const double* g, const double* g_obs,
+                            double* rhs) {
+  return guard([&] { ctx_of(ctx).assemble_rhs(m, m_ref, g, g_obs, rhs); });
+}
+
+gnw_status gnw_minres_solve(gnw_ctx* ctx, const double* b, const double* x0, double* x, double tol, uint64_t maxit,
+                            gnw_report* report) {
+  return guard([&] {
+    gnw::MinresResult r = ctx_of(ctx).minres(b, x0, x, tol, maxit);
+    if (report) {
+      report->iterations = r.iterations;
+      report->converged = r.converged ? 1 : 0;
+      report->true_relative_residual = r.true_rel;
+      report->n_hist = r.hist_e.size();
+      const uint64_t h = std::min<uint64_t>(report->hist_cap, r.hist_e.size());
+      for (uint64_t k = 0; k < h; ++k) {
+        if (report->relative_residuals) report->relative_residuals[k] = r.hist_e[k];
+        if (report->pnorm_relative_residuals) report->pnorm_relative_residuals[k] = r.hist_p[k];
+      }
+    }
+  });
+}
+
+gnw_status gnw_export_csr(const gnw_ctx* ctx, int which, uint64_t level, uint64_t* n_rows, uint64_t* n_cols,
+                          uint64_t* nnz, int64_t* rowptr, int64_t* cols, double* vals) {
+  return guard([&] {
+    const Context& c = ctx_of(ctx);
+    if (!c.assembled()) throw std::invalid_argument("gnw_export_csr: context not assembled");
+    const gnw::host::Csr* A = nullptr;
+    static const gnw::host::Csr empty{};
+    switch (which) {
+      case 0: A = &c.Q(); break;
+      case 1: A = &c.D(); break;
+      case 2: A = &c.S(); break;
+      case 3:
+      case 4:
+        if (level >= c.amg().levels.size()) throw std::invalid_argument("gnw_export_csr: level out of range");
+        A = which == 3 ? &c.amg().levels[level].A : &c.amg().levels[level].P;
+        break;
+      default: throw std::invalid_argument("gnw_export_csr: bad selector");
+    }
+    if (n_rows) *n_rows = A->n_rows;
+    if (n_cols) *n_cols = A->n_cols;
+    if (nnz) *nnz = A->nnz();
+    if (rowptr) {
+      if (A->rowptr.empty())
+        rowptr[0] = 0;
+      else
+        std::memcpy(rowptr, A->rowptr.data(), A->rowptr.size() * sizeof(int64_t));
+    }
+    if (cols)
+      for (int64_t k = 0; k < A->nnz(); ++k) cols[k] = A->cols[k];
+    if (vals && A->nnz()) std::memcpy(vals, A->vals.data(), A->vals.size() * sizeof(double));
+  });
+}
+
+gnw_status gnw_export_mesh(const gnw_ctx* ctx, int64_t* cells, int64_t* edges, int64_t* cell_edges,
+                           int32_t* cell_edge_signs, int64_t* boundary_edges, int32_t* boundary_tags) {
+  return guard([&] {
+    const Context& c = ctx_of(ctx);
+    if (!c.mixed()) throw std::invalid_argument("gnw_export_mesh: not a mixed problem");
+    const auto& m = c.mesh();
+    if (cells) std::memcpy(cells, m.cells.data(), m.cells.size() * sizeof(int64_t));
+    if (edges) std::memcpy(edges, m.edges.data(), m.edges.size() * sizeof(int64_t));
+    if (cell_edges) std::memcpy(cell_edges, m.cell_edges.data(), m.cell_edges.size() * sizeof(int64_t));
+    if (cell_edge_signs) std::memcpy(cell_edge_signs, m.cell_signs.data(), m.cell_signs.size() * sizeof(int32_t));
+    if (boundary_edges)
+      std::memcpy(boundary_edges, m.boundary_edges.data(), m.boundary_edges.size() * sizeof(int64_t));
+    if (boundary_tags) std::memcpy(boundary_tags, m.boundary_tags.data(), m.boundary_tags.size() * sizeof(int32_t));
+  });
+}
+
+gnw_status gnw_dense_cholesky(gnw_ctx* ctx, uint64_t n, const double* C, double* L) {
+  return guard([&] { ctx_of(ctx).dense_cholesky(static_cast<int64_t>(n), C, L); });
+}
+
+gnw_status gnw_get_stats(const gnw_ctx* ctx, gnw_stats* stats) {
+  return guard([&] {
+    const Context& c = ctx_of(ctx);
+    stats->t_minres = c.t_minres;
+    stats->t_rhs = c.t_rhs;
+    stats->kernel_launches = c.launches;
+    stats->setup_kernel_launches = c.setup_launches;
+  });
+}
+
+}  // extern "C"

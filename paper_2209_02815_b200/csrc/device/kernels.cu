@@ -1,0 +1,1085 @@
+// kernels.cu -- gnw device kernels (sm_100a, FP64).  See kernels.cuh.
+//
+// Bit-exactness notes (compiled with --fmad=false):
+//  * sparse row sums run one thread per row in CSR column order, starting from
+//    0.0, so they round exactly like spmv_add (sparse.cpp:73-83);
+//  * restriction gathers through R = P^T whose rows list fine indices in
+//    ascending order: the same additions as spmv_transpose's scatter
+//    (sparse.cpp:85-95; adding a zero product never changes a sum that
+//    started at +0.0, so the reference's zero-skip is immaterial);
+//  * J^T u, H t, the rhs and all vector recurrences use the reference's
+//    per-element operation order (linalg.cpp:33-54, minres.cpp:11-16).
+// Reductions (dots, J x, H^T y) are deterministic fixed-order trees, not the
+// reference's sequential sums.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cmath>
+#include <stdexcept>
+#include <string>
+
+#include "kernels.cuh"
+
+namespace gnw {
+
+namespace {
+
+constexpr int kTpb = 256;
+
+inline unsigned grid_for(long long n, int tpb = kTpb) {
+  return static_cast<unsigned>((n + tpb - 1) / tpb);
+}
+
+std::atomic<uint64_t> g_launches{0};
+
+inline void check_launch(const char* what) {
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) throw std::runtime_error(std::string("kernel launch failed (") + what + "): " + cudaGetErrorString(e));
+}
+
+__device__ __forceinline__ double ldg(const double* p) { return __ldg(p); }
+
+}  // namespace
+
+uint64_t launch_count() { return g_launches.load(std::memory_order_relaxed); }
+
+// ======================================================================
+// V-cycle, single right-hand side (amg.cpp:90-111)
+// ======================================================================
+
+// resid = r - A (wd .* r)        amg.cpp:98-101
+__global__ void __launch_bounds__(kTpb) k_vc_down(DCsr A, const double* __restrict__ wd, VSel rs,
+                                                  double* __restrict__ resid, const MinresState* st) {
+  const double* __restrict__ r = vsel(rs, st);
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= A.n_rows) return;
+  double s = 0.0;
+  const int k1 = A.rowptr[i + 1];
+  for (int k = A.rowptr[i]; k < k1; ++k) {
+    const int c = A.cols[k];
+    s = s + ldg(&A.vals[k]) * (ldg(&wd[c]) * r[c]);
+  }
+  resid[i] = r[i] + (-1.0 * s);
+}
+
+// rc = P^T resid (gather through R)        amg.cpp:103
+__global__ void __launch_bounds__(kTpb) k_vc_restrict(DCsr R, const double* __restrict__ resid,
+                                                      double* __restrict__ rc) {
+  const int a = blockIdx.x * blockDim.x + threadIdx.x;
+  if (a >= R.n_rows) return;
+  double s = 0.0;
+  const int k1 = R.rowptr[a + 1];
+  for (int k = R.rowptr[a]; k < k1; ++k) s = s + ldg(&R.vals[k]) * resid[R.cols[k]];
+  rc[a] = s;
+}
+
+// x = wd .* r + P ec        amg.cpp:98, :105
+__global__ void __launch_bounds__(kTpb) k_vc_up1(DCsr P, const double* __restrict__ wd, VSel rs,
+                                                 const double* __restrict__ ec, double* __restrict__ x,
+                                                 const MinresState* st) {
+  const double* __restrict__ r = vsel(rs, st);
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= P.n_rows) return;
+  double s = 0.0;
+  const int k1 = P.rowptr[i + 1];
+  for (int k = P.rowptr[i]; k < k1; ++k) s = s + ldg(&P.vals[k]) * ec[P.cols[k]];
+  x[i] = ldg(&wd[i]) * r[i] + 1.0 * s;
+}
+
+// out = x + wd .* (r - A x)        amg.cpp:107-109
+__global__ void __launch_bounds__(kTpb) k_vc_up2(DCsr A, const double* __restrict__ wd, VSel rs,
+                                                 const double* __restrict__ x, double* __restrict__ out,
+                                                 const MinresState* st) {
+  const double* __restrict__ r = vsel(rs, st);
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= A.n_rows) return;
+  double s = 0.0;
+  const int k1 = A.rowptr[i + 1];
+  for (int k = A.rowptr[i]; k < k1; ++k) s = s + ldg(&A.vals[k]) * x[A.cols[k]];
+  const double res = r[i] + (-1.0 * s);
+  out[i] = x[i] + ldg(&wd[i]) * res;
+}
+
+// x[:, q] = Ainv r[:, q]; one warp per (row, rhs), lane-strided partials + xor tree
+__global__ void k_coarse_inverse(const double* __restrict__ Ainv, int n, VSel rs, double* __restrict__ x,
+                                 const MinresState* st, int nrhs) {
+  const double* __restrict__ r = vsel(rs, st);
+  const long long w = (static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (w >= static_cast<long long>(n) * nrhs) return;
+  const int i = static_cast<int>(w / nrhs), q = static_cast<int>(w % nrhs);
+  double acc[1] = {0.0};
+  for (int j = lane; j < n; j += 32) acc[0] = acc[0] + ldg(&Ainv[static_cast<long long>(i) * n + j]) * r[static_cast<long long>(j) * nrhs + q];
+  warp_reduce<1>(acc);
+  if (lane == 0) x[static_cast<long long>(i) * nrhs + q] = acc[0];
+}
+
+// cholesky_solve (linalg.cpp:107-123) replayed exactly, one thread per rhs column
+__global__ void k_coarse_cholesky(const double* __restrict__ L, int n, VSel rs, double* __restrict__ x,
+                                  const MinresState* st, int nrhs, int ld) {
+  const double* __restrict__ r = vsel(rs, st);
+  const int q = blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= nrhs) return;
+  for (int i = 0; i < n; ++i) x[static_cast<long long>(i) * ld + q] = r[static_cast<long long>(i) * ld + q];
+  for (int i = 0; i < n; ++i) {
+    double s = x[static_cast<long long>(i) * ld + q];
+    for (int k = 0; k < i; ++k) s = s - L[static_cast<long long>(i) * n + k] * x[static_cast<long long>(k) * ld + q];
+    x[static_cast<long long>(i) * ld + q] = s / L[static_cast<long long>(i) * n + i];
+  }
+  for (int ii = n - 1; ii >= 0; --ii) {
+    double s = x[static_cast<long long>(ii) * ld + q];
+    for (int k = ii + 1; k < n; ++k) s = s - L[static_cast<long long>(k) * n + ii] * x[static_cast<long long>(k) * ld + q];
+    x[static_cast<long long>(ii) * ld + q] = s / L[static_cast<long long>(ii) * n + ii];
+  }
+}
+
+void vc_down(const DLevel& L, VSel r, double* resid, const MinresState* st, cudaStream_t s) {
+  k_vc_down<<<grid_for(L.n), kTpb, 0, s>>>(L.A, L.wd, r, resid, st);
+  check_launch("vc_down");
+}
+void vc_restrict(const DLevel& L, const double* resid, double* rc, cudaStream_t s) {
+  k_vc_restrict<<<grid_for(L.R.n_rows), kTpb, 0, s>>>(L.R, resid, rc);
+  check_launch("vc_restrict");
+}
+void vc_up1(const DLevel& L, VSel r, const double* ec, double* x, const MinresState* st, cudaStream_t s) {
+  k_vc_up1<<<grid_for(L.n), kTpb, 0, s>>>(L.P, L.wd, r, ec, x, st);
+  check_launch("vc_up1");
+}
+void vc_up2(const DLevel& L, VSel r, const double* x, double* out, const MinresState* st, cudaStream_t s) {
+  k_vc_up2<<<grid_for(L.n), kTpb, 0, s>>>(L.A, L.wd, r, x, out, st);
+  check_launch("vc_up2");
+}
+void coarse_inverse(const double* Ainv, int n, VSel r, double* x, const MinresState* st, int nrhs,
+                    cudaStream_t s) {
+  const long long threads = static_cast<long long>(n) * nrhs * 32;
+  k_coarse_inverse<<<grid_for(threads), kTpb, 0, s>>>(Ainv, n, r, x, st, nrhs);
+  check_launch("coarse_inverse");
+}
+void coarse_cholesky(const double* L, int n, VSel r, double* x, const MinresState* st, int nrhs, int ld,
+                     cudaStream_t s) {
+  k_coarse_cholesky<<<grid_for(nrhs, 64), 64, 0, s>>>(L, n, r, x, st, nrhs, ld);
+  check_launch("coarse_cholesky");
+}
+
+// ======================================================================
+// V-cycle, multiple right-hand sides (X[row * ld + q]); thread (row, q)
+// performs exactly the single-RHS operation sequence on column q.
+// block = (32 q-lanes, 8 rows); grid = (rows/8, b/32)
+// ======================================================================
+__global__ void __launch_bounds__(256) k_mvc_down(DCsr A, const double* __restrict__ wd,
+                                                  const double* __restrict__ r, int ldr,
+                                                  double* __restrict__ resid, int b) {
+  const int i = blockIdx.x * 8 + threadIdx.y;
+  const int q = blockIdx.y * 32 + threadIdx.x;
+  if (i >= A.n_rows || q >= b) return;
+  double s = 0.0;
+  const int k1 = A.rowptr[i + 1];
+  for (int k = A.rowptr[i]; k < k1; ++k) {
+    const int c = A.cols[k];
+    s = s + ldg(&A.vals[k]) * (ldg(&wd[c]) * r[static_cast<long long>(c) * ldr + q]);
+  }
+  resid[static_cast<long long>(i) * b + q] = r[static_cast<long long>(i) * ldr + q] + (-1.0 * s);
+}
+
+__global__ void __launch_bounds__(256) k_mvc_restrict(DCsr R, const double* __restrict__ resid,
+                                                      double* __restrict__ rc, int b) {
+  const int a = blockIdx.x * 8 + threadIdx.y;
+  const int q = blockIdx.y * 32 + threadIdx.x;
+  if (a >= R.n_rows || q >= b) return;
+  double s = 0.0;
+  const int k1 = R.rowptr[a + 1];
+  for (int k = R.rowptr[a]; k < k1; ++k) s = s + ldg(&R.vals[k]) * resid[static_cast<long long>(R.cols[k]) * b + q];
+  rc[static_cast<long long>(a) * b + q] = s;
+}
+
+__global__ void __launch_bounds__(256) k_mvc_up1(DCsr P, const double* __restrict__ wd,
+                                                 const double* __restrict__ r, int ldr,
+                                                 const double* __restrict__ ec, double* __restrict__ x, int b) {
+  const int i = blockIdx.x * 8 + threadIdx.y;
+  const int q = blockIdx.y * 32 + threadIdx.x;
+  if (i >= P.n_rows || q >= b) return;
+  double s = 0.0;
+  const int k1 = P.rowptr[i + 1];
+  for (int k = P.rowptr[i]; k < k1; ++k) s = s + ldg(&P.vals[k]) * ec[static_cast<long long>(P.cols[k]) * b + q];
+  x[static_cast<long long>(i) * b + q] = ldg(&wd[i]) * r[static_cast<long long>(i) * ldr + q] + 1.0 * s;
+}
+
+__global__ void __launch_bounds__(256) k_mvc_up2(DCsr A, const double* __restrict__ wd,
+                                                 const double* __restrict__ r, int ldr,
+                                                 const double* __restrict__ x, double* __restrict__ out,
+                                                 int ldo, int b) {
+  const int i = blockIdx.x * 8 + threadIdx.y;
+  const int q = blockIdx.y * 32 + threadIdx.x;
+  if (i >= A.n_rows || q >= b) return;
+  double s = 0.0;
+  const int k1 = A.rowptr[i + 1];
+  for (int k = A.rowptr[i]; k < k1; ++k) s = s + ldg(&A.vals[k]) * x[static_cast<long long>(A.cols[k]) * b + q];
+  const double res = r[static_cast<long long>(i) * ldr + q] + (-1.0 * s);
+  out[static_cast<long long>(i) * ldo + q] = x[static_cast<long long>(i) * b + q] + ldg(&wd[i]) * res;
+}
+
+void mvc_down(const DLevel& L, const double* r, int ldr, double* resid, int b, cudaStream_t s) {
+  dim3 grid((L.n + 7) / 8, (b + 31) / 32), block(32, 8);
+  k_mvc_down<<<grid, block, 0, s>>>(L.A, L.wd, r, ldr, resid, b);
+  check_launch("mvc_down");
+}
+void mvc_restrict(const DLevel& L, const double* resid, double* rc, int b, cudaStream_t s) {
+  dim3 grid((L.R.n_rows + 7) / 8, (b + 31) / 32), block(32, 8);
+  k_mvc_restrict<<<grid, block, 0, s>>>(L.R, resid, rc, b);
+  check_launch("mvc_restrict");
+}
+void mvc_up1(const DLevel& L, const double* r, int ldr, const double* ec, double* x, int b, cudaStream_t s) {
+  dim3 grid((L.n + 7) / 8, (b + 31) / 32), block(32, 8);
+  k_mvc_up1<<<grid, block, 0, s>>>(L.P, L.wd, r, ldr, ec, x, b);
+  check_launch("mvc_up1");
+}
+void mvc_up2(const DLevel& L, const double* r, int ldr, const double* x, double* out, int ldo, int b,
+             cudaStream_t s) {
+  dim3 grid((L.n + 7) / 8, (b + 31) / 32), block(32, 8);
+  k_mvc_up2<<<grid, block, 0, s>>>(L.A, L.wd, r, ldr, x, out, ldo, b);
+  check_launch("mvc_up2");
+}
+void mcoarse_inverse(const double* Ainv, int n, const double* r, double* x, int b, cudaStream_t s) {
+  const long long threads = static_cast<long long>(n) * b * 32;
+  k_coarse_inverse<<<grid_for(threads), kTpb, 0, s>>>(Ainv, n, vfixed(const_cast<double*>(r)), x, nullptr, b);
+  check_launch("mcoarse_inverse");
+}
+
+// rows [r0, r0+b) of A (row-major, `cols` columns) -> X[c * b + q]
+__global__ void k_transpose_rows_to_batch(const double* __restrict__ A, long long cols, int r0, int b,
+                                          double* __restrict__ X) {
+  __shared__ double tile[32][33];
+  const long long c0 = static_cast<long long>(blockIdx.x) * 32;
+  const int q0 = blockIdx.y * 32;
+  for (int y = threadIdx.y; y < 32; y += 8) {
+    const int q = q0 + y;
+    const long long c = c0 + threadIdx.x;
+    tile[y][threadIdx.x] = (q < b && c < cols) ? A[static_cast<long long>(r0 + q) * cols + c] : 0.0;
+  }
+  __syncthreads();
+  for (int y = threadIdx.y; y < 32; y += 8) {
+    const long long c = c0 + y;
+    const int q = q0 + threadIdx.x;
+    if (c < cols && q < b) X[c * b + q] = tile[threadIdx.x][y];
+  }
+}
+
+__global__ void k_transpose_batch_to_rows(const double* __restrict__ X, long long cols, int r0, int b,
+                                          double* __restrict__ A) {
+  __shared__ double tile[32][33];
+  const long long c0 = static_cast<long long>(blockIdx.x) * 32;
+  const int q0 = blockIdx.y * 32;
+  for (int y = threadIdx.y; y < 32; y += 8) {
+    const long long c = c0 + y;
+    const int q = q0 + threadIdx.x;
+    tile[y][threadIdx.x] = (c < cols && q < b) ? X[c * b + q] : 0.0;
+  }
+  __syncthreads();
+  for (int y = threadIdx.y; y < 32; y += 8) {
+    const int q = q0 + y;
+    const long long c = c0 + threadIdx.x;
+    if (q < b && c < cols) A[static_cast<long long>(r0 + q) * cols + c] = tile[threadIdx.x][y];
+  }
+}
+
+void transpose_rows_to_batch(const double* A, long long cols, int r0, int b, double* X, cudaStream_t s) {
+  dim3 grid(static_cast<unsigned>((cols + 31) / 32), (b + 31) / 32), block(32, 8);
+  k_transpose_rows_to_batch<<<grid, block, 0, s>>>(A, cols, r0, b, X);
+  check_launch("transpose_rows_to_batch");
+}
+void transpose_batch_to_rows(const double* X, long long cols, int r0, int b, double* A, cudaStream_t s) {
+  dim3 grid(static_cast<unsigned>((cols + 31) / 32), (b + 31) / 32), block(32, 8);
+  k_transpose_batch_to_rows<<<grid, block, 0, s>>>(X, cols, r0, b, A);
+  check_launch("transpose_batch_to_rows");
+}
+
+// ======================================================================
+// Row GEMV with chunked columns: out[i] = sum_c A[i, c] x[c] (deterministic)
+// ======================================================================
+RowGemv row_gemv_plan(long long N) {
+  RowGemv p;
+  long long target = (N + 2 * 148 - 1) / (2 * 148);
+  int chunk = 256;
+  while (chunk < target && chunk < 4096) chunk *= 2;
+  p.chunk = chunk;
+  p.nchunks = static_cast<int>((N + chunk - 1) / chunk);
+  return p;
+}
+
+// dot of row segment A[row, c0 : c0+len] with smem x; warp-cooperative
+__device__ __forceinline__ double warp_row_dot(const double* __restrict__ a, const double* __restrict__ xs,
+                                               int len, bool vec_ok, int lane) {
+  double acc = 0.0;
+  if (vec_ok) {
+    const int len2 = len & ~1;
+#pragma unroll 4
+    for (int t = lane * 2; t < len2; t += 64) {
+      const double2 v = __ldg(reinterpret_cast<const double2*>(a + t));
+      acc = acc + v.x * xs[t];
+      acc = acc + v.y * xs[t + 1];
+    }
+    if ((len & 1) && lane == 0) acc = acc + __ldg(a + len - 1) * xs[len - 1];
+  } else {
+    for (int t = lane; t < len; t += 32) acc = acc + __ldg(a + t) * xs[t];
+  }
+  double v[1] = {acc};
+  warp_reduce<1>(v);
+  return v[0];
+}
+
+__global__ void __launch_bounds__(kTpb) k_row_gemv(const double* __restrict__ A, int m, long long N, VSel xs,
+                                                   long long xoff, int scaled, const MinresState* st,
+                                                   double* __restrict__ partial, unsigned* counter,
+                                                   double* __restrict__ out, int chunk) {
+  extern __shared__ double xsm[];
+  const double* __restrict__ x = vsel(xs, st) + xoff;
+  const double sc = scaled ? st->inv_gamma : 1.0;
+  const long long c0 = static_cast<long long>(blockIdx.x) * chunk;
+  const int len = static_cast<int>(min(static_cast<long long>(chunk), N - c0));
+  for (int t = threadIdx.x; t < len; t += blockDim.x) xsm[t] = scaled ? x[c0 + t] * sc : x[c0 + t];
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const bool vec_ok = ((N & 1) == 0);
+  for (int row = warp; row < m; row += nw) {
+    const double d = warp_row_dot(A + static_cast<long long>(row) * N + c0, xsm, len, vec_ok, lane);
+    if (lane == 0) partial[static_cast<long long>(blockIdx.x) * m + row] = d;
+  }
+  // last block reduces over chunks in index order
+  __shared__ bool am_last;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    am_last = (atomicAdd(counter, 1u) == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (!am_last) return;
+  __threadfence();
+  for (int row = threadIdx.x; row < m; row += blockDim.x) {
+    double s = 0.0;
+    for (unsigned b = 0; b < gridDim.x; ++b) s += __ldcg(&partial[static_cast<long long>(b) * m + row]);
+    out[row] = s;
+  }
+  if (threadIdx.x == 0) *counter = 0u;
+}
+
+void row_gemv(const double* A, int m, long long N, VSel x, long long x_off, int scaled, const MinresState* st,
+              double* partial, unsigned* counter, double* out, const RowGemv& plan, cudaStream_t s) {
+  k_row_gemv<<<plan.nchunks, kTpb, plan.chunk * sizeof(double), s>>>(A, m, N, x, x_off, scaled, st, partial,
+                                                                     counter, out, plan.chunk);
+  check_launch("row_gemv");
+}
+
+// ======================================================================
+// Saddle operator  y = [Q x1 + D^T x2 ; D x1 - (1/beta) J^T (J x2)]
+// ======================================================================
+__global__ void __launch_bounds__(kTpb) k_saddle(OperatorArgs op, VSel xs, int scaled, const double* __restrict__ u,
+                                                 VSel ys, MinresState* st, int loop, int nb_edge,
+                                                 double* part, unsigned* counter) {
+  extern __shared__ double usm[];
+  __shared__ double red[kTpb / 32];
+  const double* __restrict__ z = vsel(xs, st);
+  double* __restrict__ y = vsel(ys, st);
+  const double sc = scaled ? st->inv_gamma : 1.0;
+  double dotv[1] = {0.0};
+  if (static_cast<int>(blockIdx.x) < nb_edge) {
+    const long long e = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (e < op.K) {
+      double sq = 0.0;
+      for (int k = op.Q.rowptr[e]; k < op.Q.rowptr[e + 1]; ++k) {
+        const int c = op.Q.cols[k];
+        sq = sq + __ldg(&op.Q.vals[k]) * (scaled ? z[c] * sc : z[c]);
+      }
+      double sd = 0.0;
+      for (int k = op.Dt.rowptr[e]; k < op.Dt.rowptr[e + 1]; ++k) {
+        const long long c = op.K + op.Dt.cols[k];
+        sd = sd + __ldg(&op.Dt.vals[k]) * (scaled ? z[c] * sc : z[c]);
+      }
+      double o = 0.0;
+      o = o + 1.0 * sq;  // spmv_add(*Q, zeta, 1.0, out1)
+      o = o + 1.0 * sd;  // axpy(1.0, dt, out1)
+      y[e] = o;
+      dotv[0] = o * (scaled ? z[e] * sc : z[e]);
+    }
+  } else {
+    if (op.m > 0) {
+      for (int t = threadIdx.x; t < op.m; t += blockDim.x) usm[t] = u[t];
+      __syncthreads();
+    }
+    const long long c = static_cast<long long>(blockIdx.x - nb_edge) * blockDim.x + threadIdx.x;
+    if (c < op.N) {
+      double sd = 0.0;
+      for (int k = op.D.rowptr[c]; k < op.D.rowptr[c + 1]; ++k) {
+        const int e = op.D.cols[k];
+        sd = sd + __ldg(&op.D.vals[k]) * (scaled ? z[e] * sc : z[e]);
+      }
+      double o = 0.0;
+      o = o + 1.0 * sd;  // spmv_add(*D, zeta, 1.0, out2)
+      if (op.m > 0) {    // matvec_transpose(J, J dm), linalg.cpp:45-54
+        double jt = 0.0;
+        const double* __restrict__ Jc = op.J + c;
+#pragma unroll 8
+        for (int i = 0; i < op.m; ++i) jt = jt + __ldg(Jc + static_cast<long long>(i) * op.N) * usm[i];
+        o = o + op.neg_inv_beta * jt;  // axpy(-1.0 / beta, jtjdm, out2)
+      }
+      y[op.K + c] = o;
+      dotv[0] = o * (scaled ? z[op.K + c] * sc : z[op.K + c]);
+    }
+  }
+  double tot[1];
+  if (grid_reduce_last<1>(dotv, part, counter, red, tot) && threadIdx.x == 0) {
+    const double delta = tot[0];
+    if (loop) {
+      st->delta = delta;
+      st->coef_v1 = -delta / st->gamma_cur;
+      st->coef_v2 = -st->gamma_cur / st->gamma_prev;
+    } else {
+      st->scratch[0] = delta;
+    }
+  }
+}
+
+void saddle_operator(const OperatorArgs& op, VSel x, int scaled, const double* u, VSel y, MinresState* st,
+                     int loop, double* partial, unsigned* counter, cudaStream_t s) {
+  const int nbe = static_cast<int>(grid_for(op.K)), nbc = static_cast<int>(grid_for(op.N));
+  k_saddle<<<nbe + nbc, kTpb, std::max(op.m, 1) * sizeof(double), s>>>(op, x, scaled, u, y, st, loop, nbe,
+                                                                       partial, counter);
+  check_launch("saddle_operator");
+}
+
+// ======================================================================
+// Preconditioner (inversion.cpp:71-89) fused with the v-combination
+// ======================================================================
+__global__ void __launch_bounds__(kTpb) k_combine_prec(PrecArgs pa, VSel azs, VSel vcs, VSel vps, VSel vns,
+                                                       VSel zns, int loop, MinresState* st, int nb_edge,
+                                                       int chunk, double* dots_part, double* t_part,
+                                                       unsigned* counter, double* t_out) {
+  extern __shared__ double vsm[];
+  __shared__ double red[3 * (kTpb / 32)];
+  const double* __restrict__ az = vsel(azs, st);
+  double* __restrict__ vn = vsel(vns, st);
+  double* __restrict__ zn = vsel(zns, st);
+  const double c1 = loop ? st->coef_v1 : 0.0, c2 = loop ? st->coef_v2 : 0.0;
+  const double* __restrict__ vc = loop ? vsel(vcs, st) : nullptr;
+  const double* __restrict__ vp = loop ? vsel(vps, st) : nullptr;
+  double d[3] = {0.0, 0.0, 0.0};  // <z, v>, <z, z>, <v, v>
+  if (static_cast<int>(blockIdx.x) < nb_edge) {
+    const long long e = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (e < pa.K) {
+      double v;
+      if (loop) {
+        v = az[e] + c1 * vc[e];  // combine: ca*a + cb*b + cc*c, ca = 1
+        v = v + c2 * vp[e];
+        vn[e] = v;
+      } else {
+        v = az[e];
+      }
+      const double z = __ldg(&pa.qinv[e]) * v;
+      zn[e] = z;
+      d[0] = z * v;
+      d[1] = z * z;
+      d[2] = v * v;
+    }
+    block_reduce<3>(d, red);
+    if (threadIdx.x == 0)
+      for (int k = 0; k < 3; ++k) dots_part[blockIdx.x * 3 + k] = d[k];
+  } else {
+    const long long c0 = static_cast<long long>(blockIdx.x - nb_edge) * chunk;
+    const int len = static_cast<int>(min(static_cast<long long>(chunk), pa.N - c0));
+    for (int t = threadIdx.x; t < len; t += blockDim.x) {
+      const long long i = pa.K + c0 + t;
+      double v;
+      if (loop) {
+        v = az[i] + c1 * vc[i];
+        v = v + c2 * vp[i];
+        vn[i] = v;
+      } else {
+        v = az[i];
+      }
+      vsm[t] = v;
+      d[2] = d[2] + v * v;
+    }
+    block_reduce<3>(d, red);  // also syncs vsm
+    if (threadIdx.x == 0)
+      for (int k = 0; k < 3; ++k) dots_part[blockIdx.x * 3 + k] = d[k];
+    if (pa.m > 0) {
+      const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+      const bool vec_ok = ((pa.N & 1) == 0);
+      const long long cb = blockIdx.x - nb_edge;
+      for (int row = warp; row < pa.m; row += nw) {
+        const double s = warp_row_dot(pa.Ht + static_cast<long long>(row) * pa.N + c0, vsm, len, vec_ok, lane);
+        if (lane == 0) t_part[cb * pa.m + row] = s;
+      }
+    }
+  }
+  if (pa.m == 0) return;
+  // last block: t_out = sum over cell chunks (fixed order)
+  __shared__ bool am_last;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    am_last = (atomicAdd(counter, 1u) == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (!am_last) return;
+  __threadfence();
+  const int nbc = gridDim.x - nb_edge;
+  for (int row = threadIdx.x; row < pa.m; row += blockDim.x) {
+    double s = 0.0;
+    for (int b = 0; b < nbc; ++b) s += __ldcg(&t_part[static_cast<long long>(b) * pa.m + row]);
+    t_out[row] = s;
+  }
+  if (threadIdx.x == 0) *counter = 0u;
+}
+
+void combine_precondition(const PrecArgs& pa, VSel az, VSel vcur, VSel vprev, VSel vnext, VSel znext, int loop,
+                          MinresState* st, double* /*vcopy*/, double* dots_part, double* t_part,
+                          unsigned* counter, double* t_out, const RowGemv& plan, cudaStream_t s) {
+  const int nbe = static_cast<int>(grid_for(pa.K));
+  const int nbc = static_cast<int>((pa.N + plan.chunk - 1) / plan.chunk);
+  k_combine_prec<<<nbe + nbc, kTpb, plan.chunk * sizeof(double), s>>>(pa, az, vcur, vprev, vnext, znext, loop, st,
+                                                                      nbe, plan.chunk, dots_part, t_part, counter,
+                                                                      t_out);
+  check_launch("combine_precondition");
+}
+
+// t2 = Cinv t, warp per row
+__global__ void k_cinv_apply(const double* __restrict__ Cinv, const double* __restrict__ t, double* __restrict__ t2,
+                             int m) {
+  const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (w >= m) return;
+  double acc[1] = {0.0};
+  for (int j = lane; j < m; j += 32) acc[0] = acc[0] + __ldg(&Cinv[static_cast<long long>(w) * m + j]) * t[j];
+  warp_reduce<1>(acc);
+  if (lane == 0) t2[w] = acc[0];
+}
+
+void capacitance_solve(const PrecArgs& pa, const double* t, double* t2, cudaStream_t s) {
+  if (pa.m == 0) return;
+  if (pa.exact) {
+    k_coarse_cholesky<<<1, 64, 0, s>>>(pa.Lc, pa.m, vfixed(const_cast<double*>(t)), t2, nullptr, 1, 1);
+  } else {
+    k_cinv_apply<<<grid_for(static_cast<long long>(pa.m) * 32), kTpb, 0, s>>>(pa.Cinv, t, t2, pa.m);
+  }
+  check_launch("capacitance_solve");
+}
+
+__global__ void __launch_bounds__(kTpb) k_finish_prec(PrecArgs pa, const double* __restrict__ svc,
+                                                      const double* __restrict__ t2, VSel vns, VSel zns, int loop,
+                                                      MinresState* st, const double* __restrict__ dots_edge,
+                                                      int n_edge_blocks, double* part, unsigned* counter) {
+  extern __shared__ double tsm[];
+  __shared__ double red[3 * (kTpb / 32)];
+  const double* __restrict__ vn = vsel(vns, st);
+  double* __restrict__ zn = vsel(zns, st);
+  if (pa.m > 0) {
+    for (int t = threadIdx.x; t < pa.m; t += blockDim.x) tsm[t] = t2[t];
+    __syncthreads();
+  }
+  double d[3] = {0.0, 0.0, 0.0};
+  const long long c = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (c < pa.N) {
+    double z = svc[c];
+    if (pa.m > 0) {  // w = matvec(h_hat, t) row c (linalg.cpp:33-43); s += (-1/beta) w
+      double w = 0.0;
+      const double* __restrict__ Hc = pa.Ht + c;
+#pragma unroll 8
+      for (int q = 0; q < pa.m; ++q) w = w + __ldg(Hc + static_cast<long long>(q) * pa.N) * tsm[q];
+      z = z + pa.neg_inv_beta * w;
+    }
+    zn[pa.K + c] = z;
+    const double v = vn[pa.K + c];
+    d[0] = z * v;
+    d[1] = z * z;
+  }
+  double tot[3];
+  if (!grid_reduce_last<3>(d, part, counter, red, tot)) return;
+  // add the combine kernel's partials (edge blocks: all three; cell blocks: <v,v>)
+  double e3[3] = {0.0, 0.0, 0.0};
+  for (int b = threadIdx.x; b < n_edge_blocks; b += blockDim.x)
+    for (int k = 0; k < 3; ++k) e3[k] += __ldcg(&dots_edge[b * 3 + k]);
+  block_reduce<3>(e3, red);
+  if (threadIdx.x != 0) return;
+  const double gsq = e3[0] + tot[0], zz = e3[1] + tot[1], vv = e3[2] + tot[2];
+  if (!loop) {
+    st->scratch[0] = gsq;
+    st->scratch[1] = zz;
+    st->scratch[2] = vv;
+    return;
+  }
+  // minres.cpp:79-101
+  if (gsq < -1e-12 * (sqrt(zz) * sqrt(vv) + 1.0)) {
+    st->status = kErrNotPD;
+    return;
+  }
+  const double gamma_next = sqrt(fmax(gsq, 0.0));
+  const double delta = st->delta, gc = st->gamma_cur;
+  const double alpha0 = st->c_cur * delta - st->c_prev * st->s_cur * gc;
+  const double alpha1 = sqrt(alpha0 * alpha0 + gamma_next * gamma_next);
+  const double alpha2 = st->s_cur * delta + st->c_prev * st->c_cur * gc;
+  const double alpha3 = st->s_prev * gc;
+  if (alpha1 == 0.0) {
+    st->status = kErrStagnated;
+    return;
+  }
+  st->gamma_next = gamma_next;
+  st->c_next = alpha0 / alpha1;
+  st->s_next = gamma_next / alpha1;
+  st->alpha2 = alpha2;
+  st->alpha3 = alpha3;
+  st->inv_alpha1 = 1.0 / alpha1;
+  st->tau = st->c_next * st->eta;
+  st->eta = -st->s_next * st->eta;
+}
+
+void finish_precondition(const PrecArgs& pa, const double* svc, const double* t2, VSel vnext, VSel znext, int loop,
+                         MinresState* st, const double* dots_edge, int n_edge_blocks, double* part,
+                         unsigned* counter, cudaStream_t s) {
+  k_finish_prec<<<grid_for(pa.N), kTpb, std::max(pa.m, 1) * sizeof(double), s>>>(
+      pa, svc, t2, vnext, znext, loop, st, dots_edge, n_edge_blocks, part, counter);
+  check_launch("finish_precondition");
+}
+
+// ======================================================================
+// MINRES vector recurrences (minres.cpp:93-106) and loop control
+// ======================================================================
+__global__ void __launch_bounds__(kTpb) k_minres_update(long long n, VSel zs, VSel azs, VSel wps, VSel wcs, VSel wns,
+                                                        VSel ups, VSel ucs, VSel uns, double* __restrict__ x,
+                                                        double* __restrict__ r, MinresState* st,
+                                                        double* hist_e, double* hist_p, long long hist_cap,
+                                                        double* part, unsigned* counter,
+                                                        cudaGraphConditionalHandle handle, int use_cond) {
+  __shared__ double red[kTpb / 32];
+  if (st->status != kRunning) {
+    if (use_cond && blockIdx.x == 0 && threadIdx.x == 0) cudaGraphSetConditional(handle, 0);
+    return;
+  }
+  const double* __restrict__ z = vsel(zs, st);
+  const double* __restrict__ az = vsel(azs, st);
+  const double* __restrict__ wp = vsel(wps, st);
+  const double* __restrict__ wc = vsel(wcs, st);
+  double* __restrict__ wn = vsel(wns, st);
+  const double* __restrict__ up = vsel(ups, st);
+  const double* __restrict__ uc = vsel(ucs, st);
+  double* __restrict__ un = vsel(uns, st);
+  const double ig = st->inv_gamma, na3 = -st->alpha3, na2 = -st->alpha2, ia = st->inv_alpha1;
+  const double tau = st->tau, ntau = -tau;
+  double rr[1] = {0.0};
+  for (long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const double zh = z[i] * ig;
+    double w = zh + na3 * wp[i];
+    w = w + na2 * wc[i];
+    w = w * ia;
+    double uu = az[i] + na3 * up[i];
+    uu = uu + na2 * uc[i];
+    uu = uu * ia;
+    wn[i] = w;
+    un[i] = uu;
+    x[i] = x[i] + tau * w;
+    const double ri = r[i] + ntau * uu;
+    r[i] = ri;
+    rr[0] = rr[0] + ri * ri;
+  }
+  double tot[1];
+  if (!grid_reduce_last<1>(rr, part, counter, red, tot) || threadIdx.x != 0) return;
+  const long long j = st->j;
+  const double rel = sqrt(tot[0]) / st->bnorm;
+  st->iterations = j;
+  st->rel = rel;
+  if (j < hist_cap) {
+    hist_e[j] = rel;
+    hist_p[j] = fabs(st->eta) / st->gamma1;
+  }
+  if (rel <= st->tol) {
+    st->status = kVerify;
+  } else if (st->gamma_next <= st->exhausted_tol) {
+    st->status = kExhausted;
+  } else {
+    st->gamma_prev = st->gamma_cur;
+    st->gamma_cur = st->gamma_next;
+    st->c_prev = st->c_cur;
+    st->c_cur = st->c_next;
+    st->s_prev = st->s_cur;
+    st->s_cur = st->s_next;
+    st->inv_gamma = 1.0 / st->gamma_cur;
+    st->j = j + 1;
+    if (j + 1 > st->maxit) st->status = kMaxit;
+  }
+  if (use_cond) cudaGraphSetConditional(handle, st->status == kRunning ? 1u : 0u);
+}
+
+void minres_update(long long n, VSel z, VSel az, VSel wprev, VSel wcur, VSel wnext, VSel uprev, VSel ucur, VSel unext,
+                   double* x, double* r, MinresState* st, double* hist_e, double* hist_p, long long hist_cap,
+                   double* part, unsigned* counter, unsigned long long cond_handle, int use_cond, cudaStream_t s) {
+  const unsigned grid = std::min<unsigned>(grid_for(n), 148u * 8u);
+  k_minres_update<<<grid, kTpb, 0, s>>>(n, z, az, wprev, wcur, wnext, uprev, ucur, unext, x, r, st, hist_e, hist_p,
+                                        hist_cap, part, counter,
+                                        static_cast<cudaGraphConditionalHandle>(cond_handle), use_cond);
+  check_launch("minres_update");
+}
+
+__global__ void k_minres_rotate(MinresState* st) {
+  st->gamma_prev = st->gamma_cur;
+  st->gamma_cur = st->gamma_next;
+  st->c_prev = st->c_cur;
+  st->c_cur = st->c_next;
+  st->s_prev = st->s_cur;
+  st->s_cur = st->s_next;
+  st->inv_gamma = 1.0 / st->gamma_cur;
+  st->j = st->j + 1;
+  st->status = (st->j > st->maxit) ? kMaxit : kRunning;
+}
+
+void minres_rotate(MinresState* st, cudaStream_t s) {
+  k_minres_rotate<<<1, 1, 0, s>>>(st);
+  check_launch("minres_rotate");
+}
+
+__global__ void __launch_bounds__(kTpb) k_residual(long long n, const double* __restrict__ b,
+                                                   const double* __restrict__ y, double* __restrict__ r,
+                                                   MinresState* st, int want_b, double* part, unsigned* counter) {
+  __shared__ double red[2 * (kTpb / 32)];
+  double v[2] = {0.0, 0.0};
+  for (long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const double ri = b[i] - y[i];
+    r[i] = ri;
+    v[0] = v[0] + ri * ri;
+    if (want_b) v[1] = v[1] + b[i] * b[i];
+  }
+  double tot[2];
+  if (grid_reduce_last<2>(v, part, counter, red, tot) && threadIdx.x == 0) {
+    st->scratch[4] = tot[0];
+    if (want_b) st->scratch[5] = tot[1];
+  }
+}
+
+void residual(long long n, const double* b, const double* y, double* r, MinresState* st, int want_b, double* part,
+              unsigned* counter, cudaStream_t s) {
+  const unsigned grid = std::min<unsigned>(grid_for(n), 148u * 8u);
+  k_residual<<<grid, kTpb, 0, s>>>(n, b, y, r, st, want_b, part, counter);
+  check_launch("residual");
+}
+
+__global__ void __launch_bounds__(kTpb) k_dot(long long n, const double* __restrict__ a, const double* __restrict__ b,
+                                              double* out, double* part, unsigned* counter) {
+  __shared__ double red[kTpb / 32];
+  double v[1] = {0.0};
+  for (long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += static_cast<long long>(gridDim.x) * blockDim.x)
+    v[0] = v[0] + a[i] * b[i];
+  double tot[1];
+  if (grid_reduce_last<1>(v, part, counter, red, tot) && threadIdx.x == 0) *out = tot[0];
+}
+
+void dot(long long n, const double* a, const double* b, double* out, double* part, unsigned* counter, cudaStream_t s) {
+  const unsigned grid = std::min<unsigned>(grid_for(n), 148u * 8u);
+  k_dot<<<grid, kTpb, 0, s>>>(n, a, b, out, part, counter);
+  check_launch("dot");
+}
+
+// rhs = [-D^T (m - m_ref); J^T (g - g_obs) / beta]   inversion.cpp:126-146
+__global__ void __launch_bounds__(kTpb) k_rhs(OperatorArgs op, double beta, const double* __restrict__ mdl,
+                                              const double* __restrict__ mref, const double* __restrict__ dg,
+                                              double* __restrict__ rhs, int nb_edge) {
+  extern __shared__ double gsm[];
+  if (static_cast<int>(blockIdx.x) < nb_edge) {
+    const long long e = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (e >= op.K) return;
+    double s = 0.0;
+    for (int k = op.Dt.rowptr[e]; k < op.Dt.rowptr[e + 1]; ++k) {
+      const int c = op.Dt.cols[k];
+      s = s + __ldg(&op.Dt.vals[k]) * (mdl[c] - mref[c]);
+    }
+    rhs[e] = -s;
+  } else {
+    for (int t = threadIdx.x; t < op.m; t += blockDim.x) gsm[t] = dg[t];
+    __syncthreads();
+    const long long c = static_cast<long long>(blockIdx.x - nb_edge) * blockDim.x + threadIdx.x;
+    if (c >= op.N) return;
+    double jt = 0.0;
+    const double* __restrict__ Jc = op.J + c;
+#pragma unroll 8
+    for (int i = 0; i < op.m; ++i) jt = jt + __ldg(Jc + static_cast<long long>(i) * op.N) * gsm[i];
+    rhs[op.K + c] = jt / beta;
+  }
+}
+
+void assemble_rhs(const OperatorArgs& op, double beta, const double* mdl, const double* mref, const double* dg,
+                  double* rhs, cudaStream_t s) {
+  const int nbe = static_cast<int>(grid_for(op.K)), nbc = static_cast<int>(grid_for(op.N));
+  k_rhs<<<nbe + nbc, kTpb, std::max(op.m, 1) * sizeof(double), s>>>(op, beta, mdl, mref, dg, rhs, nbe);
+  check_launch("assemble_rhs");
+}
+
+// ======================================================================
+// Capacitance DGEMM: C = I + (J Ht^T)/beta via split-K FP64 tensor-core DMMA
+// (mma.sync.m8n8k4.f64 -> SASS DMMA; tcgen05 has no kind::f64 on sm_100a).
+// CTA tile 128x128, 8 warps (2 x 4), warp tile 64x32 = 8x4 DMMA tiles,
+// K staged 16 at a time through a 3-stage cp.async ring.
+// ======================================================================
+namespace dg {
+constexpr int BM = 128, BN = 128, BK = 16, LDS = BK + 4, STAGES = 3;
+constexpr int SMEM = STAGES * (BM + BN) * LDS * 8;
+}  // namespace dg
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, int src_bytes) {
+  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "r"(src_bytes));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
+
+__device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};\n"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+
+__global__ void __launch_bounds__(256, 1) k_dgemm_nt(const double* __restrict__ A, const double* __restrict__ B, int m,
+                                                     long long N, long long kchunk, const int2* __restrict__ pairs,
+                                                     int npairs, double* __restrict__ part) {
+  using namespace dg;
+  extern __shared__ __align__(16) double sm[];
+  double* As = sm;                            // [STAGES][BM][LDS]
+  double* Bs = sm + STAGES * BM * LDS;        // [STAGES][BN][LDS]
+  const int2 pr = pairs[blockIdx.x];
+  const int i0 = pr.x * BM, j0 = pr.y * BN;
+  const long long k0 = static_cast<long long>(blockIdx.y) * kchunk;
+  const long long k1 = min(N, k0 + kchunk);
+  const int nkt = static_cast<int>((k1 - k0 + BK - 1) / BK);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int wm = warp >> 2, wn = warp & 3;  // 2 x 4 warps
+
+  auto load_stage = [&](int stage, int kt) {
+    const long long kb = k0 + static_cast<long long>(kt) * BK;
+    // 128 rows x 16 doubles = 1024 16-byte chunks per operand; 4 per thread
+#pragma unroll
+    for (int it = 0; it < 4; ++it) {
+      const int chunk = tid + it * 256;
+      const int row = chunk >> 3, kc = (chunk & 7) * 2;
+      const long long kk = kb + kc;
+      {
+        const int gr = i0 + row;
+        const bool ok = gr < m && kk < k1;
+        const double* src = ok ? A + static_cast<long long>(gr) * N + kk : A;
+        cp_async16(As + (stage * BM + row) * LDS + kc, src, ok ? 16 : 0);
+      }
+      {
+        const int gr = j0 + row;
+        const bool ok = gr < m && kk < k1;
+        const double* src = ok ? B + static_cast<long long>(gr) * N + kk : B;
+        cp_async16(Bs + (stage * BN + row) * LDS + kc, src, ok ? 16 : 0);
+      }
+    }
+  };
+
+  double acc[8][4][2];
+#pragma unroll
+  for (int a = 0; a < 8; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+
+#pragma unroll
+  for (int s = 0; s < STAGES - 1; ++s) {
+    if (s < nkt) load_stage(s, s);
+    cp_async_commit();
+  }
+  for (int kt = 0; kt < nkt; ++kt) {
+    cp_async_wait<STAGES - 2>();
+    __syncthreads();
+    const int nxt = kt + STAGES - 1;
+    if (nxt < nkt) load_stage(nxt % STAGES, nxt);
+    cp_async_commit();
+    const int st = kt % STAGES;
+    const double* as = As + st * BM * LDS;
+    const double* bs = Bs + st * BN * LDS;
+#pragma unroll
+    for (int kk = 0; kk < BK; kk += 4) {
+      double af[8], bf[4];
+#pragma unroll
+      for (int a = 0; a < 8; ++a) af[a] = as[(wm * 64 + a * 8 + (lane >> 2)) * LDS + kk + (lane & 3)];
+#pragma unroll
+      for (int b = 0; b < 4; ++b) bf[b] = bs[(wn * 32 + b * 8 + (lane >> 2)) * LDS + kk + (lane & 3)];
+#pragma unroll
+      for (int a = 0; a < 8; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) dmma(acc[a][b][0], acc[a][b][1], af[a], bf[b]);
+    }
+  }
+  cp_async_wait<0>();
+  // partial tile out: part[(split * npairs + pair)][BM][BN]
+  double* out = part + (static_cast<long long>(blockIdx.y) * npairs + blockIdx.x) * (BM * BN);
+#pragma unroll
+  for (int a = 0; a < 8; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      const int r = wm * 64 + a * 8 + (lane >> 2);
+      const int c = wn * 32 + b * 8 + (lane & 3) * 2;
+      *reinterpret_cast<double2*>(out + r * BN + c) = make_double2(acc[a][b][0], acc[a][b][1]);
+    }
+}
+
+// C[i][j] = (sum_split part) / beta (+1 on the diagonal)   inversion.cpp:37-43
+__global__ void k_dgemm_finalize(const double* __restrict__ part, const int2* __restrict__ pairs, int npairs,
+                                 int splits, int m, double beta, double* __restrict__ C) {
+  using namespace dg;
+  const int p = blockIdx.y;
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= BM * BN) return;
+  const int2 pr = pairs[p];
+  const int i = pr.x * BM + e / BN, j = pr.y * BN + e % BN;
+  if (i >= m || j >= m) return;
+  double s = 0.0;
+  for (int k = 0; k < splits; ++k) s += part[(static_cast<long long>(k) * npairs + p) * (BM * BN) + e];
+  double v = s / beta;
+  if (i == j) v += 1.0;
+  C[static_cast<long long>(i) * m + j] = v;
+}
+
+DgemmPlan dgemm_plan(int m, long long N, int full, int sm_count) {
+  DgemmPlan p;
+  p.tile = dg::BM;
+  p.ntiles = (m + dg::BM - 1) / dg::BM;
+  p.npairs = full ? p.ntiles * p.ntiles : p.ntiles * (p.ntiles + 1) / 2;
+  p.full = full;
+  const long long kblocks = (N + dg::BK - 1) / dg::BK;
+  int splits = std::max(1, (2 * sm_count + p.npairs - 1) / p.npairs);
+  splits = static_cast<int>(std::min<long long>(splits, kblocks));
+  long long kchunk = ((kblocks + splits - 1) / splits) * dg::BK;
+  p.splits = static_cast<int>((N + kchunk - 1) / kchunk);
+  p.kchunk = kchunk;
+  return p;
+}
+
+void capacitance_dgemm(const double* J, const double* Ht, int m, long long N, double beta, const DgemmPlan& plan,
+                       double* part, double* C, cudaStream_t s) {
+  if (N % 2 != 0) throw std::invalid_argument("capacitance_dgemm: N must be even (16-byte rows)");
+  // pair list lives at the end of the partial buffer
+  int2 hp[4096];
+  int np = 0;
+  for (int i = 0; i < plan.ntiles; ++i)
+    for (int j = 0; j < plan.ntiles; ++j)
+      if (plan.full || j <= i) hp[np++] = make_int2(i, j);
+  int2* dpairs = reinterpret_cast<int2*>(part + static_cast<long long>(plan.splits) * plan.npairs * dg::BM * dg::BN);
+  cudaMemcpyAsync(dpairs, hp, np * sizeof(int2), cudaMemcpyHostToDevice, s);
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaFuncSetAttribute(k_dgemm_nt, cudaFuncAttributeMaxDynamicSharedMemorySize, dg::SMEM);
+    attr_set = true;
+  }
+  dim3 grid(plan.npairs, plan.splits);
+  k_dgemm_nt<<<grid, 256, dg::SMEM, s>>>(J, Ht, m, N, plan.kchunk, dpairs, plan.npairs, part);
+  check_launch("dgemm_nt");
+  dim3 g2((dg::BM * dg::BN + 255) / 256, plan.npairs);
+  k_dgemm_finalize<<<g2, 256, 0, s>>>(part, dpairs, plan.npairs, plan.splits, m, beta, C);
+  check_launch("dgemm_finalize");
+}
+
+// ======================================================================
+// Dense Cholesky (linalg.cpp:88-105), single CTA, reference operation order
+// ======================================================================
+__global__ void __launch_bounds__(1024) k_cholesky(const double* __restrict__ C, double* __restrict__ L, int n,
+                                                   int* fail) {
+  __shared__ double ljj_s;
+  __shared__ int bad;
+  if (threadIdx.x == 0) bad = 0;
+  for (long long t = threadIdx.x; t < static_cast<long long>(n) * n; t += blockDim.x) L[t] = 0.0;
+  __syncthreads();
+  for (int j = 0; j < n; ++j) {
+    if (threadIdx.x == 0) {
+      double d = C[static_cast<long long>(j) * n + j];
+      for (int k = 0; k < j; ++k) {
+        const double l = L[static_cast<long long>(j) * n + k];
+        d = d - l * l;
+      }
+      if (!(d > 0.0)) {
+        bad = 1;
+      } else {
+        const double ljj = sqrt(d);
+        L[static_cast<long long>(j) * n + j] = ljj;
+        ljj_s = ljj;
+      }
+    }
+    __syncthreads();
+    if (bad) break;
+    const double ljj = ljj_s;
+    for (int i = j + 1 + threadIdx.x; i < n; i += blockDim.x) {
+      double s = C[static_cast<long long>(i) * n + j];
+      double* Li = L + static_cast<long long>(i) * n;
+      const double* Lj = L + static_cast<long long>(j) * n;
+      for (int k = 0; k < j; ++k) s = s - Li[k] * Lj[k];
+      Li[j] = s / ljj;
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *fail = bad;
+}
+
+void cholesky(const double* C, double* L, int n, int* fail, cudaStream_t s) {
+  k_cholesky<<<1, 1024, 0, s>>>(C, L, n, fail);
+  check_launch("cholesky");
+}
+
+__global__ void k_symmetrize(double* C, int n) {
+  const long long t = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (t >= static_cast<long long>(n) * n) return;
+  const int i = static_cast<int>(t / n), j = static_cast<int>(t % n);
+  if (j <= i) return;
+  const double v = 0.5 * (C[static_cast<long long>(i) * n + j] + C[static_cast<long long>(j) * n + i]);
+  C[static_cast<long long>(i) * n + j] = v;
+  C[static_cast<long long>(j) * n + i] = v;
+}
+
+void symmetrize(double* C, int n, cudaStream_t s) {
+  k_symmetrize<<<grid_for(static_cast<long long>(n) * n), kTpb, 0, s>>>(C, n);
+  check_launch("symmetrize");
+}
+
+// Y = L^-1 (thread per column), then Cinv = Y^T Y
+__global__ void k_trinv(const double* __restrict__ L, double* __restrict__ Y, int n) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= n) return;
+  for (int i = 0; i < j; ++i) Y[static_cast<long long>(i) * n + j] = 0.0;
+  for (int i = j; i < n; ++i) {
+    double s = (i == j) ? 1.0 : 0.0;
+    for (int k = j; k < i; ++k) s = s - L[static_cast<long long>(i) * n + k] * Y[static_cast<long long>(k) * n + j];
+    Y[static_cast<long long>(i) * n + j] = s / L[static_cast<long long>(i) * n + i];
+  }
+}
+
+__global__ void k_syrk_tn(const double* __restrict__ Y, double* __restrict__ Cinv, int n) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x, i = blockIdx.y;
+  if (j >= n || j > i) return;
+  double s = 0.0;
+  for (int k = i; k < n; ++k) s = s + Y[static_cast<long long>(k) * n + i] * Y[static_cast<long long>(k) * n + j];
+  Cinv[static_cast<long long>(i) * n + j] = s;
+  Cinv[static_cast<long long>(j) * n + i] = s;
+}
+
+void cholesky_inverse(const double* L, double* Y, double* Cinv, int n, cudaStream_t s) {
+  k_trinv<<<grid_for(n, 64), 64, 0, s>>>(L, Y, n);
+  check_launch("trinv");
+  dim3 grid(grid_for(n, 128), n);
+  k_syrk_tn<<<grid, 128, 0, s>>>(Y, Cinv, n);
+  check_launch("syrk_tn");
+}
+
+__global__ void k_fill_zero(double* p, long long n) {
+  for (long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += static_cast<long long>(gridDim.x) * blockDim.x)
+    p[i] = 0.0;
+}
+
+void fill_zero(double* p, long long n, cudaStream_t s) {
+  if (n <= 0) return;
+  k_fill_zero<<<std::min<unsigned>(grid_for(n), 148u * 16u), kTpb, 0, s>>>(p, n);
+  check_launch("fill_zero");
+}
+
+}  // namespace gnw

@@ -1,0 +1,139 @@
+// kernels.cuh -- launch interfaces of the gnw device kernels (sm_100a, FP64).
+// Reference citations are to /root/reference/proj.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include "common.cuh"
+
+namespace gnw {
+
+// One level of the device AMG hierarchy (amg.hpp:25-29).  R = P^T stored
+// explicitly so restriction is a gather (rows of R sorted by fine index, which
+// reproduces spmv_transpose's scatter order, sparse.cpp:85-95).
+struct DLevel {
+  DCsr A, P, R;
+  double* wd = nullptr;  // omega * inv_diag (rounded exactly as amg.cpp:98)
+  int n = 0;             // rows of A
+};
+
+// ------------------------------------------------------------------ V-cycle
+// Single right-hand side (amg.cpp:90-111); `r` may be a ring slot (level 0).
+void vc_down(const DLevel& L, VSel r, double* resid, const MinresState* st, cudaStream_t s);
+void vc_restrict(const DLevel& L, const double* resid, double* rc, cudaStream_t s);
+void vc_up1(const DLevel& L, VSel r, const double* ec, double* x, const MinresState* st, cudaStream_t s);
+void vc_up2(const DLevel& L, VSel r, const double* x, double* out, const MinresState* st, cudaStream_t s);
+// coarsest level: x = A_c^-1 r (explicit inverse, warp per row)
+void coarse_inverse(const double* Ainv, int n, VSel r, double* x, const MinresState* st, int nrhs,
+                    cudaStream_t s);
+// coarsest level, reference cholesky_solve replayed (linalg.cpp:107-123), one thread per rhs
+void coarse_cholesky(const double* L, int n, VSel r, double* x, const MinresState* st, int nrhs,
+                     int ld, cudaStream_t s);
+
+// Multi right-hand side (b columns interleaved: X[row * ld + q]); per column
+// bit-identical to the single-RHS kernels.
+void mvc_down(const DLevel& L, const double* r, int ldr, double* resid, int b, cudaStream_t s);
+void mvc_restrict(const DLevel& L, const double* resid, double* rc, int b, cudaStream_t s);
+void mvc_up1(const DLevel& L, const double* r, int ldr, const double* ec, double* x, int b, cudaStream_t s);
+void mvc_up2(const DLevel& L, const double* r, int ldr, const double* x, double* out, int ldo, int b,
+             cudaStream_t s);
+void mcoarse_inverse(const double* Ainv, int n, const double* r, double* x, int b, cudaStream_t s);
+
+// rows [r0, r0+b) of a row-major (rows x cols) matrix -> cols x b interleaved
+void transpose_rows_to_batch(const double* A, long long cols, int r0, int b, double* X, cudaStream_t s);
+// cols x b interleaved -> rows [r0, r0+b) of a row-major (rows x cols) matrix
+void transpose_batch_to_rows(const double* X, long long cols, int r0, int b, double* A, cudaStream_t s);
+
+// ---------------------------------------------------------------- operator
+struct OperatorArgs {
+  DCsr Q, D, Dt;       // Dt = D^T (rows = edges, columns = cells ascending)
+  const double* J = nullptr;  // m x N row-major (nullptr: no low-rank term)
+  int m = 0;
+  long long K = 0, N = 0;
+  double neg_inv_beta = 0.0;  // -1/beta
+};
+
+// u = A[:, ] x2 * scale partial GEMV over rows of a row-major (m x N) matrix,
+// scale = st->inv_gamma when scaled != 0 (zhat = z / gamma), else 1.
+struct RowGemv {
+  int chunk = 0, nchunks = 0;
+};
+RowGemv row_gemv_plan(long long N);
+void row_gemv(const double* A, int m, long long N, VSel x, long long x_off, int scaled,
+              const MinresState* st, double* partial, unsigned* counter, double* out,
+              const RowGemv& plan, cudaStream_t s);
+
+// y = A x (saddle operator, inversion.cpp:47-69) with x = z * scale; u = J x2
+// precomputed.  When `loop`, the last block stores delta = <y, x> and the
+// v-combination coefficients into st (minres.cpp:74-77).
+void saddle_operator(const OperatorArgs& op, VSel x, int scaled, const double* u, VSel y,
+                     MinresState* st, int loop, double* partial, unsigned* counter, cudaStream_t s);
+
+// --------------------------------------------------------- preconditioner
+struct PrecArgs {
+  const double* qinv = nullptr;
+  const double* Ht = nullptr;   // m x N row-major (H^T; h_hat(c, i) = Ht[i * N + c])
+  const double* Cinv = nullptr; // m x m (explicit capacitance inverse)
+  const double* Lc = nullptr;   // m x m lower Cholesky factor of C (exact mode)
+  int m = 0;
+  long long K = 0, N = 0;
+  double neg_inv_beta = 0.0;
+  int exact = 0;
+};
+
+// v_next = Az + c1 v_cur + c2 v_prev (combine, minres.cpp:76-77) or, when
+// !loop, v_next = y (plain preconditioner input); z1 = qinv * v1; partial
+// dots; t = Ht v2 (row GEMV) reduced by the last block into t_out.
+void combine_precondition(const PrecArgs& pa, VSel az, VSel vcur, VSel vprev, VSel vnext, VSel znext,
+                          int loop, MinresState* st, double* vcopy, double* dots_part,
+                          double* t_part, unsigned* counter, double* t_out, const RowGemv& plan,
+                          cudaStream_t s);
+// t2 = C^-1 t (inverse apply) or the exact cholesky_solve (exact mode)
+void capacitance_solve(const PrecArgs& pa, const double* t, double* t2, cudaStream_t s);
+// z2 = s + (-1/beta) H t2; dots <z, v>, ||z||^2; last block: Givens update
+// (minres.cpp:78-101) when loop, else totals to st->scratch.
+void finish_precondition(const PrecArgs& pa, const double* svc, const double* t2, VSel vnext,
+                         VSel znext, int loop, MinresState* st, const double* dots_edge,
+                         int n_edge_blocks, double* part, unsigned* counter, cudaStream_t s);
+
+// w/u/x/r recurrences (minres.cpp:93-106) + ||r||; last block: history,
+// convergence/exhaustion checks, rotation, graph loop condition.
+void minres_update(long long n, VSel z, VSel az, VSel wprev, VSel wcur, VSel wnext, VSel uprev,
+                   VSel ucur, VSel unext, double* x, double* r, MinresState* st, double* hist_e,
+                   double* hist_p, long long hist_cap, double* part, unsigned* counter,
+                   unsigned long long cond_handle, int use_cond, cudaStream_t s);
+// host-driven continuation after a failed verification: rotation + j++
+void minres_rotate(MinresState* st, cudaStream_t s);
+
+// r = b - y and ||r||^2 -> st->scratch[4] (and ||b||^2 -> scratch[5] when want_b)
+void residual(long long n, const double* b, const double* y, double* r, MinresState* st, int want_b,
+              double* part, unsigned* counter, cudaStream_t s);
+// dot products for the generic entry points: out[0] = <a, b>
+void dot(long long n, const double* a, const double* b, double* out, double* part, unsigned* counter,
+         cudaStream_t s);
+
+// rhs = [-D^T (m - m_ref); J^T (g - g_obs) / beta]  (inversion.cpp:126-146)
+void assemble_rhs(const OperatorArgs& op, double beta, const double* mdl, const double* mref,
+                  const double* dg, double* rhs, cudaStream_t s);
+
+// ------------------------------------------------------------- dense / DMMA
+// C = I + (J Ht^T) / beta, lower triangle (or full) by split-K FP64 DMMA.
+struct DgemmPlan {
+  int tile = 0, ntiles = 0, npairs = 0, splits = 0;
+  long long kchunk = 0;
+  int full = 0;
+};
+DgemmPlan dgemm_plan(int m, long long N, int full, int sm_count);
+void capacitance_dgemm(const double* J, const double* Ht, int m, long long N, double beta,
+                       const DgemmPlan& plan, double* part, double* C, cudaStream_t s);
+// dense_cholesky (linalg.cpp:88-105), operation order preserved; *fail = 1 on a
+// non-positive pivot.
+void cholesky(const double* C, double* L, int n, int* fail, cudaStream_t s);
+// symmetrize C in place (cholesky_with_retry, inversion.cpp:24-33)
+void symmetrize(double* C, int n, cudaStream_t s);
+// Cinv = L^-T L^-1
+void cholesky_inverse(const double* L, double* Y, double* Cinv, int n, cudaStream_t s);
+
+void fill_zero(double* p, long long n, cudaStream_t s);
+
+}  // namespace gnw

@@ -1,0 +1,241 @@
+"""Python face of the gnw C-ABI, mirroring the reference's interfaces.
+
+The reference (proj/include/ertinv/inversion.hpp, minres.hpp, amg.hpp) exposes
+``amg_setup``/``amg_apply``, ``build_woodbury_preconditioner``, ``SaddleOperator::apply``,
+``WoodburyPreconditioner::apply``, ``assemble_gn_rhs`` and ``minres``.  ``Context`` binds
+those to one B200 through libgnw.so; every heavy operation runs in the CUDA kernels of
+``csrc/device``.  Errors keep the reference's semantics: ``std::invalid_argument`` ->
+``ValueError``, ``std::runtime_error`` -> ``RuntimeError`` with the same message text.
+
+Vectors may be numpy arrays (host pointers, copied in/out by the library) or, after
+``use_device_pointers()``, torch CUDA float64 tensors (device pointers, no copies).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import dataclasses
+
+import numpy as np
+
+from . import _capi as A
+from .workload import Mesh
+
+
+@dataclasses.dataclass
+class MinresReport:
+    """MinresReport, proj/include/ertinv/minres.hpp:13-22."""
+
+    iterations: int
+    relative_residuals: np.ndarray
+    pnorm_relative_residuals: np.ndarray
+    converged: bool
+    true_relative_residual: float
+
+
+def _dptr(x):
+    """Raw pointer of a numpy array or a torch tensor."""
+    if hasattr(x, "data_ptr"):
+        return x.data_ptr()
+    return x.ctypes.data
+
+
+class Context:
+    """One solver context on one GPU (``device=None``: host-only, setup/export only)."""
+
+    def __init__(self, device: int | None = 0):
+        self.L = A.load()
+        h = C.c_void_p()
+        if device is None:
+            A.check(self.L.gnw_create(0, None, C.byref(h)))
+        else:
+            dev = (C.c_int * 1)(device)
+            A.check(self.L.gnw_create(1, dev, C.byref(h)))
+        self.h = h
+        self.device = device
+        self.device_pointers = False
+        self.K = self.N = self.m = 0
+
+    def close(self):
+        if getattr(self, "h", None) and self.h.value:
+            self.L.gnw_destroy(self.h)
+            self.h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # ----------------------------------------------------------- configuration
+    def use_device_pointers(self, on: bool = True):
+        A.check(self.L.gnw_set_pointer_mode(self.h, A.GNW_DEVICE_POINTERS if on else A.GNW_HOST_POINTERS))
+        self.device_pointers = on
+
+    def set_coarse_mode(self, exact: bool):
+        A.check(self.L.gnw_set_coarse_mode(self.h, A.GNW_COARSE_CHOLESKY if exact else A.GNW_COARSE_INVERSE))
+
+    # ---------------------------------------------------------------- assembly
+    def assemble(self, mesh: Mesh, opts: A.AmgOptions | None = None):
+        """make_mixed_spaces + assemble_Q/D + amg_setup(assemble_lumped_schur(Q, D))."""
+        v = A.f64(mesh.vertices).ravel()
+        c = np.ascontiguousarray(mesh.cells, dtype=np.int64).ravel()
+        m = A._Mesh(mesh.n_vertices, v.ctypes.data, mesh.n_cells, c.ctypes.data)
+        A.check(self.L.gnw_assemble(self.h, C.byref(m), C.byref(opts) if opts is not None else None))
+        info = self.info()
+        self.K, self.N = info["K"], info["N"]
+        self.m = 0
+        return self
+
+    def assemble_amg_csr(self, rowptr, cols, vals, opts: A.AmgOptions | None = None):
+        """amg_setup(s_hat, opts) on a caller CSR matrix (amg.cpp:115-187)."""
+        rowptr = np.ascontiguousarray(rowptr, dtype=np.int64)
+        cols = np.ascontiguousarray(cols, dtype=np.int64)
+        vals = A.f64(vals)
+        A.check(self.L.gnw_assemble_amg_csr(self.h, len(rowptr) - 1, rowptr.ctypes.data, cols.ctypes.data,
+                                            vals.ctypes.data, C.byref(opts) if opts is not None else None))
+        info = self.info()
+        self.K, self.N = 0, info["N"]
+        return self
+
+    def info(self) -> dict:
+        i = A.Info()
+        A.check(self.L.gnw_get_info(self.h, C.byref(i)))
+        return {f: getattr(i, f) for f, _ in A.Info._fields_}
+
+    def stats(self) -> dict:
+        s = A.Stats()
+        A.check(self.L.gnw_get_stats(self.h, C.byref(s)))
+        return {f: getattr(s, f) for f, _ in A.Stats._fields_}
+
+    # ---------------------------------------------------------------- Jacobian
+    def set_jacobian(self, J, beta: float, laplace_pc: bool = False) -> dict:
+        """build_woodbury_preconditioner(q_diag_inv, amg, J, beta, &timings) (inversion.cpp:91-124).
+
+        ``laplace_pc`` keeps J in the operator with the bare Laplace preconditioner
+        (Alg. 4, inversion.cpp:251-256); ``J=None`` drops the low-rank term entirely."""
+        A.check(self.L.gnw_set_preconditioner(self.h, 1 if laplace_pc else 0))
+        t = A.Timings()
+        if J is None:
+            A.check(self.L.gnw_set_jacobian(self.h, None, 0, self.N, beta, C.byref(t)))
+            self.m = 0
+        else:
+            if not self.device_pointers:
+                J = A.f64(J)
+            m, n = J.shape
+            A.check(self.L.gnw_set_jacobian(self.h, _dptr(J), m, n, beta, C.byref(t)))
+            self.m = m
+        self.beta = beta
+        return {"t_H": t.t_H, "t_C": t.t_C, "t_chol": t.t_chol}
+
+    # ----------------------------------------------------------------- applies
+    def _out(self, n, like=None):
+        if self.device_pointers:
+            import torch
+            return torch.empty(n, dtype=torch.float64, device=like.device if like is not None else "cuda")
+        return np.zeros(n)
+
+    def _in(self, x):
+        return x if self.device_pointers else A.f64(x)
+
+    def apply_operator(self, x):
+        """SaddleOperator::apply (inversion.cpp:47-69)."""
+        x = self._in(x)
+        y = self._out(self.K + self.N, x)
+        A.check(self.L.gnw_apply_operator(self.h, _dptr(x), _dptr(y)))
+        return y
+
+    def precondition(self, y):
+        """WoodburyPreconditioner::apply (inversion.cpp:71-89)."""
+        y = self._in(y)
+        z = self._out(self.K + self.N, y)
+        A.check(self.L.gnw_precondition(self.h, _dptr(y), _dptr(z)))
+        return z
+
+    def amg_apply(self, r):
+        """amg_apply (amg.cpp:189-194): one V-cycle."""
+        r = self._in(r)
+        z = self._out(self.N, r)
+        A.check(self.L.gnw_amg_apply(self.h, _dptr(r), _dptr(z)))
+        return z
+
+    def assemble_rhs(self, m, m_ref, g, g_obs):
+        """assemble_gn_rhs (inversion.cpp:126-146)."""
+        m, m_ref, g, g_obs = (self._in(a) for a in (m, m_ref, g, g_obs))
+        out = self._out(self.K + self.N, m)
+        A.check(self.L.gnw_assemble_rhs(self.h, _dptr(m), _dptr(m_ref), _dptr(g), _dptr(g_obs), _dptr(out)))
+        return out
+
+    def minres(self, b, x0=None, tol: float = 1e-8, maxit: int | None = None, hist_cap: int = 1 << 16):
+        """minres(op.apply, pc.apply, b, x0, tol, maxit) (minres.cpp:20-155)."""
+        n = self.K + self.N
+        b = self._in(b)
+        if x0 is None:
+            x0 = self._out(n, b)
+            if self.device_pointers:
+                x0.zero_()
+        else:
+            x0 = self._in(x0)
+        maxit = 2 * n if maxit is None else int(maxit)
+        x = self._out(n, b)
+        he = np.zeros(hist_cap)
+        hp = np.zeros(hist_cap)
+        rep = A.Report(0, 0, 0.0, 0, he.ctypes.data, hp.ctypes.data, hist_cap)
+        A.check(self.L.gnw_minres_solve(self.h, _dptr(b), _dptr(x0), _dptr(x), tol, maxit, C.byref(rep)))
+        nh = min(int(rep.n_hist), hist_cap)
+        return x, MinresReport(int(rep.iterations), he[:nh].copy(), hp[:nh].copy(), bool(rep.converged),
+                               float(rep.true_relative_residual))
+
+    def woodbury_factors(self):
+        """(H, L): H = S_hat^-1 J^T (N x m, h_hat layout) and the capacitance Cholesky factor."""
+        H = np.zeros((self.N, self.m))
+        Lf = np.zeros((self.m, self.m))
+        A.check(self.L.gnw_get_woodbury(self.h, H.ctypes.data, Lf.ctypes.data))
+        return H, Lf
+
+    def dense_cholesky(self, Cm):
+        Cm = A.f64(Cm)
+        out = np.zeros_like(Cm)
+        A.check(self.L.gnw_dense_cholesky(self.h, Cm.shape[0], Cm.ctypes.data, out.ctypes.data))
+        return out
+
+    # ---------------------------------------------------------------- exports
+    def export_csr(self, which: int, level: int = 0):
+        nr, nc, nnz = C.c_uint64(), C.c_uint64(), C.c_uint64()
+        A.check(self.L.gnw_export_csr(self.h, which, level, C.byref(nr), C.byref(nc), C.byref(nnz), None, None, None))
+        rp = np.zeros(nr.value + 1, np.int64)
+        ci = np.zeros(nnz.value, np.int64)
+        va = np.zeros(nnz.value, np.float64)
+        A.check(self.L.gnw_export_csr(self.h, which, level, None, None, None, rp.ctypes.data, ci.ctypes.data,
+                                      va.ctypes.data))
+        return nr.value, nc.value, rp, ci, va
+
+    def export_mesh(self):
+        i = self.info()
+        nc = self.N
+        out = dict(cells=np.zeros(3 * nc, np.int64), edges=np.zeros(2 * i["n_edges"], np.int64),
+                   cell_edges=np.zeros(3 * nc, np.int64), cell_edge_signs=np.zeros(3 * nc, np.int32),
+                   boundary_edges=np.zeros(i["n_boundary_edges"], np.int64),
+                   boundary_tags=np.zeros(i["n_boundary_edges"], np.int32))
+        A.check(self.L.gnw_export_mesh(self.h, *(out[k].ctypes.data for k in (
+            "cells", "edges", "cell_edges", "cell_edge_signs", "boundary_edges", "boundary_tags"))))
+        return out
+
+
+# ---------------------------------------------------------------------------
+# Reference-shaped facade (inversion.hpp / minres.hpp names)
+# ---------------------------------------------------------------------------
+def amg_setup(ctx: Context, rowptr, cols, vals, opts: A.AmgOptions | None = None) -> Context:
+    return ctx.assemble_amg_csr(rowptr, cols, vals, opts)
+
+
+def build_woodbury_preconditioner(ctx: Context, J, beta: float) -> dict:
+    """Returns the WoodburyBuildTimings (t_H, t_C, t_chol); the factors live on the device."""
+    return ctx.set_jacobian(J, beta)
+
+
+def assemble_gn_rhs(ctx: Context, m, m_ref, g, g_obs):
+    return ctx.assemble_rhs(m, m_ref, g, g_obs)
+
+
+def minres(ctx: Context, b, x0=None, tol: float = 1e-8, maxit: int | None = None):
+    return ctx.minres(b, x0, tol, maxit)
