@@ -1,0 +1,355 @@
+#!/usr/bin/env python
+"""bench.py -- GN-step solves/s of the B200 Woodbury-MINRES solver (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C2] [--impl gnw|reference]
+
+Workload (N=1 line): BASELINE.json configs[1] = C2, the configuration the metric is quoted
+on: 512x512 unit square x 2 triangles (N = 524288 cells, K = 787456 edges), synthetic
+J = U diag(s) V^T (m = 256), alpha sweep {1e-4, 1e-3, 1e-2, 1e-1, 1}, MINRES to 1e-8, FP64.
+One STEP = one full GN-step solve = the reference's t_norm (inversion.cpp:242-271):
+build_woodbury_preconditioner (H = S^-1 J^T by V-cycles, C = I + J H / alpha, chol C)
++ assemble_gn_rhs + MINRES; step k uses alpha = sweep[k % 5].  Inputs (J: 1.07 GB, H: 1.07 GB
+per solve) are far larger than the 126 MB L2, so no L2 flush is needed between steps.
+
+* value  -- device-resident inputs (torch CUDA tensors, device-pointer mode), timed with CUDA
+            events on the library's stream; whole-job throughput (N replicas, max over ranks).
+* e2e    -- the same solves through the C-ABI with HOST buffers (pinned): J, m, m_ref, g, g_obs
+            copied H2D every step inside the timed region; rhs and x copied back D2H.
+* roofline -- the dominant per-iteration kernel measured in isolation with CUDA events
+            (gnw_profile_kernel), algorithmic bytes per SURVEY.md 8(d); peak = MEASURED_PEAKS.json.
+* cpu_baseline -- the unmodified reference (oracle/_ref) on this host, 1 core (the reference is
+            single-threaded): a bounded sample of the same C2 solve extrapolated to one full
+            solve with the reference's own iteration count (tests/golden/c2_reference.json).
+
+Multi-GPU: C2 does not shard (replicas only) -- N independent replicas, one
+process per GPU, scaling "weak".  `--impl reference` runs the reference arm (rank 0 only).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "GN-step solves/s (MINRES+Woodbury-MG to 1e-8, FP64); % of HBM roofline"
+UNIT = "GN-step solves/s"
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled DURING the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, smax, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                smax = max(smax, float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[3:7]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"]}
+        loaded = [s for s in sm if s > 0.5 * max(sm)] or sm
+        return {"sm_mhz": statistics.median(loaded), "sm_max_mhz": smax, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def c2_reference_record():
+    path = os.path.join(ROOT, "tests", "golden", "c2_reference.json")
+    try:
+        with open(path) as f:
+            return json.load(f)
+    except Exception:
+        return None
+
+
+def cpu_sample(cfg, inp, alpha, iterations, k_cols=16, k_rows=16, k_iters=10):
+    """Bounded sample of the reference on this host, extrapolated to one full GN-step solve."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import orc  # CPU baseline leg only
+
+    o = orc.Oracle("reference" if orc.available("reference") else "restatement")
+    p = orc.Problem.mixed(o, inp.mesh, orc.AmgOpts.make(coarse_threshold=cfg.coarse_threshold))
+    if o.kind != "reference":
+        raise RuntimeError("reference library oracle/_ref/libertinv_ref.so missing")
+    t0 = time.time()
+    s = p.sample_gnstep(inp.J, alpha, k_cols, k_rows, k_iters)
+    wall = time.time() - t0
+    t_est = s["t_col"] * cfg.m + s["t_row"] * cfg.m + s["t_chol"] + s["t_iter"] * iterations
+    sample = (f"reference (oracle/_ref, -O3 -DNDEBUG) on C2 alpha={alpha:g}: {k_cols} H columns (V-cycles), "
+              f"{k_rows} capacitance rows (matmul), full {cfg.m}x{cfg.m} Cholesky, {k_iters} MINRES iterations "
+              f"({wall:.1f} s of CPU); per-unit times x (m={cfg.m} columns, m rows, {iterations} iterations) "
+              f"-> t_norm = {t_est:.1f} s")
+    return 1.0 / t_est, t_est, s, sample, o.kind
+
+
+def run_reference(args):
+    """--impl reference: the reference's own CPU implementation, bounded samples per step."""
+    ws, rank, local = dist_env()
+    if rank != 0:
+        return
+    from paper_2209_02815_b200 import workload as W
+
+    cfg = W.CONFIGS[args.config]
+    inp = W.gnstep_inputs(cfg.n, cfg.m, cfg.index)
+    rec = c2_reference_record()
+    iters = {r["alpha"]: r["iterations"] for r in rec["runs"]} if rec else {}
+    alphas = list(cfg.alphas)
+    t_total, last = 0.0, None
+    for k in range(args.warmup + args.steps):
+        a = alphas[k % len(alphas)]
+        v, t_est, s, sample, kind = cpu_sample(cfg, inp, a, iters.get(a, 88), k_cols=8, k_rows=8, k_iters=4)
+        if k >= args.warmup:
+            t_total += t_est
+            last = (sample, kind)
+    value = args.steps / t_total
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t_total / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded C2 bundle)",
+            "config": {"workload": "C2", "mesh_n": cfg.n, "m": cfg.m, "alphas": alphas, "tol": 1e-8},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": last[1], "sample": last[0]},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def run_gnw(args):
+    import torch
+
+    ws, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    if ws > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_2209_02815_b200 import AmgOptions, Context, workload as W
+
+    cfg = W.CONFIGS[args.config]
+    inp = W.gnstep_inputs(cfg.n, cfg.m, cfg.index)
+    K, N = W.mixed_sizes(cfg.n)
+    alphas = list(cfg.alphas)
+    tol = 1e-8
+
+    ctx = Context(local)
+    ctx.assemble(inp.mesh, AmgOptions(coarse_threshold=cfg.coarse_threshold))
+    info = ctx.info()
+
+    def barrier():
+        torch.cuda.synchronize()
+        if ws > 1:
+            torch.distributed.barrier()
+        torch.cuda.synchronize()
+
+    def max_over_ranks(x: float) -> float:
+        if ws == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        return float(t.item())
+
+    # ---------------------------------------------------------- device-resident arm
+    ctx.use_device_pointers(True)
+    J_d = torch.from_numpy(inp.J).cuda()
+    dm_d = torch.from_numpy(inp.dm).cuda()
+    dg_d = torch.from_numpy(inp.dg).cuda()
+    zN = torch.zeros(N, dtype=torch.float64, device="cuda")
+    zm = torch.zeros(cfg.m, dtype=torch.float64, device="cuda")
+
+    def solve_dev(alpha):
+        tm = ctx.set_jacobian(J_d, alpha)
+        b = ctx.assemble_rhs(dm_d, zN, dg_d, zm)
+        x, rep = ctx.minres(b, tol=tol)
+        st = ctx.stats()
+        return tm, rep, st
+
+    for k in range(args.warmup):
+        solve_dev(alphas[k % len(alphas)])
+    barrier()
+    per_step = []
+    launches = 0
+    with ClockSampler(local) as clk:
+        ctx.event_record(0)
+        for k in range(args.steps):
+            a = alphas[k % len(alphas)]
+            tm, rep, st = solve_dev(a)
+            launches += int(st["kernel_launches"]) + int(st["setup_kernel_launches"]) + 1
+            per_step.append(dict(alpha=a, iterations=rep.iterations, converged=rep.converged,
+                                 true_rel=rep.true_relative_residual, t_H=tm["t_H"], t_C=tm["t_C"],
+                                 t_chol=tm["t_chol"], t_minres=st["t_minres"]))
+        ctx.event_record(1)
+        elapsed = ctx.event_elapsed(0, 1)
+    barrier()
+    elapsed = max_over_ranks(elapsed)
+    value = ws * args.steps / elapsed
+
+    # ---------------------------------------------------------------- e2e arm
+    ctx.use_device_pointers(False)
+    J_h = torch.from_numpy(inp.J).pin_memory().numpy()
+    dm_h = torch.from_numpy(inp.dm).pin_memory().numpy()
+    dg_h = torch.from_numpy(inp.dg).pin_memory().numpy()
+    zN_h = np.zeros(N)
+    zm_h = np.zeros(cfg.m)
+
+    def solve_host(alpha):
+        ctx.set_jacobian(J_h, alpha)
+        b = ctx.assemble_rhs(dm_h, zN_h, dg_h, zm_h)
+        x, rep = ctx.minres(b, tol=tol)
+        return x, rep
+
+    solve_host(alphas[0])
+    barrier()
+    ctx.event_record(2)
+    for k in range(args.steps):
+        x_h, rep_h = solve_host(alphas[k % len(alphas)])
+    ctx.event_record(3)
+    e2e_elapsed = max_over_ranks(ctx.event_elapsed(2, 3))
+    barrier()
+    h2d = 8 * (cfg.m * N + 3 * N + 2 * cfg.m) + 8 * 2 * (K + N)  # J, m, m_ref, g, g_obs, then b, x0
+    d2h = 8 * (K + N) * 2 + 8 * 2 * (rep_h.iterations + 1)        # rhs, x, residual histories
+
+    # --------------------------------------------------------------- roofline
+    hbm_peak, peak_src = peaks()
+    ctx.use_device_pointers(True)
+    ctx.set_jacobian(J_d, 1e-2)
+    b = ctx.assemble_rhs(dm_d, zN, dg_d, zm)
+    ctx.minres(b, tol=tol)
+    kern = {}
+    for name in ("row_gemv", "saddle", "combine_prec", "finish_prec", "vcycle", "update"):
+        sec, byt = ctx.profile_kernel(name, reps=20)
+        kern[name] = {"ms": sec * 1e3, "GB": byt / 1e9, "GBps": byt / sec / 1e9, "frac": byt / sec / 1e9 / hbm_peak}
+    it_sec, it_bytes = ctx.profile_kernel("iteration")
+    dg_sec, dg_flops = ctx.profile_kernel("dgemm", reps=5)
+    dom = max(("row_gemv", "saddle", "combine_prec", "finish_prec"), key=lambda k: kern[k]["ms"])
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            traffic = json.load(f).get(dom)
+    except Exception:
+        pass
+
+    # ---------------------------------------------------------- CPU baseline
+    cpu = None
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+        rec = c2_reference_record()
+        it_ref = {r["alpha"]: r["iterations"] for r in rec["runs"]}.get(1e-2) if rec else None
+        it_use = it_ref or next(s["iterations"] for s in per_step if s["alpha"] == 1e-2)
+        try:
+            v, t_est, s, sample, kind = cpu_sample(cfg, inp, 1e-2, it_use)
+            cpu = {"value": v, "unit": UNIT, "cores": 1, "kind": kind, "sample": sample}
+        except Exception as e:  # reported, never silently replaced
+            cpu = {"value": None, "unit": UNIT, "cores": 1, "kind": "reference", "sample": f"failed: {e}"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": 1e3 * elapsed / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded C2 bundle)",
+            "config": {"workload": f"C2: unit square n={cfg.n} (N={N} cells, K={K} edges), m={cfg.m}, "
+                                   f"alpha sweep {alphas}, MINRES tol {tol}; one step = one full GN-step solve",
+                       "mesh_n": cfg.n, "m": cfg.m, "alphas": alphas, "tol": tol,
+                       "parallelism": f"replicas x{ws}",
+                       "l2": "no flush: per-solve inputs (J 1.07 GB + H 1.07 GB) exceed the 126 MB L2",
+                       "amg_levels": info["n_levels"], "coarse_n": info["coarse_n"]},
+            "roofline": {"bound": "hbm", "kernel": dom, "achieved": kern[dom]["GBps"], "peak": hbm_peak,
+                         "unit": "GB/s", "frac": kern[dom]["frac"], "traffic": traffic,
+                         "peak_source": peak_src,
+                         "algorithmic_bytes_per_launch": kern[dom]["GB"] * 1e9,
+                         "iteration": {"ms": it_sec * 1e3, "GB": it_bytes / 1e9,
+                                       "GBps": it_bytes / it_sec / 1e9 if it_sec else None,
+                                       "frac": it_bytes / it_sec / 1e9 / hbm_peak if it_sec else None},
+                         "kernels": kern,
+                         "dgemm": {"ms": dg_sec * 1e3, "TFLOPs": dg_flops / dg_sec / 1e12}},
+            "cpu_baseline": cpu,
+            "e2e": {"value": ws * args.steps / e2e_elapsed, "unit": UNIT, "h2d_bytes_per_step": h2d,
+                    "d2h_bytes_per_step": d2h},
+            "gpu_launches": launches,
+            "clocks": clk.summary(),
+            "phases": per_step,
+        }
+        print(json.dumps(line), flush=True)
+    ctx.close()
+    if ws > 1:
+        torch.distributed.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="C2")
+    ap.add_argument("--impl", default="gnw", choices=["gnw", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_gnw(args)
+
+
+if __name__ == "__main__":
+    main()

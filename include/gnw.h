@@ -171,6 +171,28 @@ typedef struct gnw_stats {
 } gnw_stats;
 gnw_status gnw_get_stats(const gnw_ctx* ctx, gnw_stats* stats);
 
+/* CUDA events on the context's stream (slots 0..15) for device-side timing. */
+gnw_status gnw_event_record(gnw_ctx* ctx, int slot);
+gnw_status gnw_event_elapsed(gnw_ctx* ctx, int slot_begin, int slot_end, double* seconds);
+
+/* Kernel-level measurement for the roofline: launches one hot-path kernel in
+ * isolation `reps` times on the context's stream (after one warm-up launch) and
+ * returns its mean CUDA-event duration and its ALGORITHMIC traffic per launch
+ * (bytes; flops for GNW_K_DGEMM), counted as SURVEY.md 8(d) does: every matrix
+ * streamed once, FP64 values 8 B, int32 indices 4 B. */
+enum {
+  GNW_K_ROW_GEMV = 0,      /* u = J x2 (row GEMV over J) */
+  GNW_K_SADDLE = 1,        /* saddle operator incl. J^T u */
+  GNW_K_COMBINE_PREC = 2,  /* v-combine + qinv + H^T v2 */
+  GNW_K_FINISH_PREC = 3,   /* z2 = s - H t / beta + dots + Givens */
+  GNW_K_VCYCLE = 4,        /* one single-RHS V-cycle (all its kernels) */
+  GNW_K_UPDATE = 5,        /* w/u/x/r recurrences */
+  GNW_K_DGEMM = 6,         /* capacitance DGEMM (DMMA), flops */
+  GNW_K_ITERATION = 7      /* one full MINRES iteration (graph body, replayed by the kernels) */
+};
+gnw_status gnw_profile_kernel(gnw_ctx* ctx, int kernel, int reps, double* seconds_per_launch,
+                              double* algorithmic_per_launch);
+
 #ifdef __cplusplus
 }
 #endif

@@ -213,6 +213,15 @@ class Problem:
         self.beta = beta
         return dict(t_H=t[0], t_C=t[1], t_chol=t[2])
 
+    def sample_gnstep(self, J: np.ndarray, beta: float, k_cols: int, k_rows: int, k_iters: int) -> dict:
+        """Bounded CPU timing sample (reference library only); see orc_api.h."""
+        fn = self.o.L.orc_sample_gnstep
+        fn.argtypes = [C.c_void_p, C.c_void_p, _u64, C.c_double, _u64, _u64, _u64, _dp]
+        J = np.ascontiguousarray(J, dtype=np.float64)
+        out = np.zeros(4)
+        self.o.check(fn(self.h, J.ctypes.data, J.shape[0], beta, k_cols, k_rows, k_iters, out))
+        return dict(t_col=out[0], t_row=out[1], t_chol=out[2], t_iter=out[3])
+
     def H(self) -> np.ndarray:
         out = np.zeros(self.N * self.m)
         self.o.check(self.o.L.orc_get_H(self.h, out))

@@ -94,6 +94,11 @@ int orc_minres(const orc_problem* p, const double* b, const double* x0, double t
                uint64_t maxit, double* x, orc_minres_report* rep, double* hist_euclid,
                double* hist_pnorm, uint64_t hist_cap);
 
+/* Bounded timing sample of one GN-step solve (reference library only; see
+ * ref_capi.cpp): out = {s per H column, s per C row, s Cholesky, s per MINRES iteration}. */
+int orc_sample_gnstep(orc_problem* p, const double* J, uint64_t m, double beta, uint64_t k_cols,
+                      uint64_t k_rows, uint64_t k_iters, double out[4]);
+
 /* Dense Cholesky (linalg.cpp:88-105): returns 2 on a non-positive pivot. */
 int orc_dense_cholesky(uint64_t n, const double* C, double* L);
 

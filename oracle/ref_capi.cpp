@@ -2,6 +2,8 @@
 // reference library compiled from /root/reference/proj/src by oracle/Makefile.
 // Every call forwards to the reference's own functions; nothing here restates
 // an algorithm.  Output: oracle/_ref/libertinv_ref.so (git-ignored).
+#include <chrono>
+#include <cmath>
 #include <cstring>
 #include <memory>
 #include <stdexcept>
@@ -313,6 +315,58 @@ int orc_minres(const orc_problem* p, const double* b, const double* x0, double t
       if (he) he[i] = r.relative_residuals[i];
       if (hp) hp[i] = r.pnorm_relative_residuals[i];
     }
+  });
+}
+
+// Bounded CPU sample of one GN-step solve (bench.py cpu_baseline / --impl
+// reference).  Times the reference's own functions on full-size operands:
+//   out[0] seconds per H column (amg_apply of one J row, inversion.cpp:107-114)
+//   out[1] seconds per capacitance row (matmul of k_rows J rows with an N x m
+//          operand, linalg.cpp:56-70; dense J so no zero-skipping)
+//   out[2] seconds of the m x m dense_cholesky (linalg.cpp:88-105), full size
+//   out[3] seconds per MINRES iteration (minres.cpp:70-148) with the full
+//          SaddleOperator and a WoodburyPreconditioner of the full shape (H = 0,
+//          L = I: identical work per apply, guaranteed SPD)
+int orc_sample_gnstep(orc_problem* p, const double* J, uint64_t m, double beta, uint64_t k_cols,
+                      uint64_t k_rows, uint64_t k_iters, double out[4]) {
+  return guard([&] {
+    using Clock = std::chrono::steady_clock;
+    const std::size_t N = p->spaces.n_cell_dofs, K = p->spaces.n_flux_dofs;
+    DenseMatrix Jm(m, N);
+    std::memcpy(Jm.values.data(), J, m * N * sizeof(double));
+    auto t0 = Clock::now();
+    Vector col(N);
+    for (std::size_t i = 0; i < k_cols; ++i) {
+      for (std::size_t c = 0; c < N; ++c) col[c] = Jm(i % m, c);
+      const Vector h = amg_apply(p->amg, col);
+      if (h.empty()) throw std::runtime_error("sample: empty V-cycle");
+    }
+    out[0] = std::chrono::duration<double>(Clock::now() - t0).count() / static_cast<double>(k_cols);
+    DenseMatrix Jsub(k_rows, N);
+    std::memcpy(Jsub.values.data(), J, k_rows * N * sizeof(double));
+    DenseMatrix Hfake(N, m);
+    t0 = Clock::now();
+    DenseMatrix Csub = matmul(Jsub, Hfake);
+    out[1] = std::chrono::duration<double>(Clock::now() - t0).count() / static_cast<double>(k_rows);
+    DenseMatrix Cfull = DenseMatrix::identity(m);
+    t0 = Clock::now();
+    DenseMatrix L = dense_cholesky(Cfull);
+    out[2] = std::chrono::duration<double>(Clock::now() - t0).count();
+    WoodburyPreconditioner pc;
+    pc.q_diag_inv = &p->qinv;
+    pc.amg = &p->amg;
+    pc.J = &Jm;
+    pc.beta = beta;
+    pc.h_hat = std::move(Hfake);
+    pc.capacitance_chol = std::move(L);
+    SaddleOperator op{&p->Q, &p->D, &Jm, beta};
+    Vector b(K + N), x0(K + N, 0.0);
+    for (std::size_t i = 0; i < b.size(); ++i) b[i] = std::sin(0.37 * static_cast<double>(i) + 1.0);
+    t0 = Clock::now();
+    auto res = minres([&op](std::span<const double> v) { return op.apply(v); },
+                      [&pc](std::span<const double> v) { return pc.apply(v); }, b, x0, 1e-300, k_iters);
+    const double tm = std::chrono::duration<double>(Clock::now() - t0).count();
+    out[3] = tm / static_cast<double>(std::max<std::size_t>(res.second.iterations, 1));
   });
 }
 

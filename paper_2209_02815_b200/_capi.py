@@ -70,8 +70,12 @@ EXPORTED = [
     "gnw_set_coarse_mode", "gnw_set_preconditioner", "gnw_assemble", "gnw_assemble_amg_csr", "gnw_get_info",
     "gnw_set_jacobian", "gnw_apply_operator", "gnw_precondition", "gnw_amg_apply",
     "gnw_get_woodbury", "gnw_assemble_rhs", "gnw_minres_solve", "gnw_export_csr",
-    "gnw_export_mesh", "gnw_dense_cholesky", "gnw_get_stats",
+    "gnw_export_mesh", "gnw_dense_cholesky", "gnw_get_stats", "gnw_event_record",
+    "gnw_event_elapsed", "gnw_profile_kernel",
 ]
+
+KERNELS = {"row_gemv": 0, "saddle": 1, "combine_prec": 2, "finish_prec": 3, "vcycle": 4,
+           "update": 5, "dgemm": 6, "iteration": 7}
 
 _lib = None
 
@@ -107,6 +111,9 @@ def load() -> C.CDLL:
     L.gnw_export_mesh.argtypes = [vp, vp, vp, vp, vp, vp, vp]
     L.gnw_dense_cholesky.argtypes = [vp, u64, vp, vp]
     L.gnw_get_stats.argtypes = [vp, C.POINTER(Stats)]
+    L.gnw_event_record.argtypes = [vp, i32]
+    L.gnw_event_elapsed.argtypes = [vp, i32, i32, C.POINTER(dbl)]
+    L.gnw_profile_kernel.argtypes = [vp, i32, i32, C.POINTER(dbl), C.POINTER(dbl)]
     for name in EXPORTED:
         fn = getattr(L, name)
         if name not in ("gnw_last_error", "gnw_version", "gnw_destroy"):

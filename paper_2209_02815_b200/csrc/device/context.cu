@@ -81,6 +81,8 @@ Context::~Context() {
   cudaSetDevice(device_);
   destroy_graph();
   if (stream_) cudaStreamSynchronize(stream_);
+  for (auto& e : events_)
+    if (e) cudaEventDestroy(e);
   jmem_.reset();
   mem_.release_all();
   if (h_st_) cudaFreeHost(h_st_);
@@ -354,6 +356,8 @@ void Context::set_jacobian(const double* J, int64_t m, int64_t n_cells, double b
   destroy_graph();
   jmem_.reset();
   dJ_ = dHt_ = dC_ = dL_ = dCinv_ = dY_ = nullptr;
+  u_ = t_ = t2_ = gpart_ = tpart_ = nullptr;
+  j_borrowed_ = false;
   m_ = m;
   beta_ = beta;
   op_.J = nullptr;
@@ -369,13 +373,19 @@ void Context::set_jacobian(const double* J, int64_t m, int64_t n_cells, double b
   jmem_ = std::make_unique<DeviceMemory>();
   DeviceMemory& jm = *jmem_;
   const size_t mN = static_cast<size_t>(m) * N_;
-  dJ_ = jm.alloc<double>(mN);
   u_ = jm.alloc<double>(m);
   gpart_ = jm.alloc<double>(static_cast<size_t>(plan_.nchunks) * m);
-  if (ptr_mode == 1)
-    GNW_CUDA_CHECK(cudaMemcpyAsync(dJ_, J, mN * sizeof(double), cudaMemcpyDeviceToDevice, s));
-  else
+  if (ptr_mode == 1) {
+    // Device pointers: J is referenced, not copied -- the reference's
+    // SaddleOperator/WoodburyPreconditioner also hold a non-owning pointer to J
+    // (inversion.hpp:21, :35); the caller keeps it alive while the context uses it.
+    dJ_ = const_cast<double*>(J);
+    j_borrowed_ = true;
+  } else {
+    dJ_ = jm.alloc<double>(mN);
+    j_borrowed_ = false;
     GNW_CUDA_CHECK(cudaMemcpyAsync(dJ_, J, mN * sizeof(double), cudaMemcpyHostToDevice, s));
+  }
   op_.J = dJ_;
   op_.m = static_cast<int>(m);
   if (pc_laplace) {  // Alg. 4: J stays in the operator, plain Laplace preconditioner
@@ -736,6 +746,7 @@ MinresResult Context::minres(const double* b, const double* x0, double* x, doubl
     }
   }
   res.iterations = static_cast<uint64_t>(h_st_->iterations);
+  last_iterations = res.iterations;
   const uint64_t nh = std::min<uint64_t>(res.iterations + 1, static_cast<uint64_t>(hist_cap_));
   std::vector<double> he(nh), hp(nh);
   GNW_CUDA_CHECK(cudaMemcpyAsync(he.data(), hist_e_, nh * sizeof(double), cudaMemcpyDeviceToHost, s));
@@ -761,6 +772,115 @@ void Context::get_woodbury(double* H, double* L) {
       for (int64_t c = 0; c < N_; ++c) H[c * m_ + i] = ht[i * N_ + c];
   }
   if (L) GNW_CUDA_CHECK(cudaMemcpy(L, dL_, m_ * m_ * sizeof(double), cudaMemcpyDeviceToHost));
+}
+
+void Context::event_record(int slot) {
+  require_device();
+  if (slot < 0 || slot >= 16) throw std::invalid_argument("gnw_event_record: slot out of range");
+  if (!events_[slot]) GNW_CUDA_CHECK(cudaEventCreate(&events_[slot]));
+  GNW_CUDA_CHECK(cudaEventRecord(events_[slot], stream_));
+}
+
+double Context::event_elapsed(int a, int b) {
+  require_device();
+  if (a < 0 || a >= 16 || b < 0 || b >= 16 || !events_[a] || !events_[b])
+    throw std::invalid_argument("gnw_event_elapsed: slot not recorded");
+  GNW_CUDA_CHECK(cudaEventSynchronize(events_[b]));
+  float ms = 0.f;
+  GNW_CUDA_CHECK(cudaEventElapsedTime(&ms, events_[a], events_[b]));
+  return ms * 1e-3;
+}
+
+// Algorithmic traffic per launch (SURVEY.md 8(d) conventions) and isolated timing.
+void Context::profile_kernel(int kernel, int reps, double* seconds, double* algorithmic) {
+  require_mixed();
+  require_device();
+  if (reps < 1) reps = 1;
+  const cudaStream_t s = stream_;
+  const double K = static_cast<double>(K_), N = static_cast<double>(N_), m = static_cast<double>(m_);
+  const double nnzQ = static_cast<double>(Q_.nnz()), nnzD = static_cast<double>(D_.nnz());
+  double bv = 0.0;  // B_V
+  {
+    const size_t L = amg_.levels.size();
+    for (size_t l = 0; l + 1 < L; ++l) {
+      const double n = static_cast<double>(amg_.levels[l].A.n_rows);
+      const double nA = static_cast<double>(amg_.levels[l].A.nnz()), nP = static_cast<double>(amg_.levels[l].P.nnz());
+      bv += 2 * (12 * nA + 4 * (n + 1)) + 2 * (12 * nP + 4 * (n + 1)) + 16 * n + 48 * n;
+    }
+    const double nl = static_cast<double>(amg_.nc);
+    bv += 8 * nl * nl + 32 * nl;
+  }
+  const double hm = (pa_.m > 0) ? m : 0.0;  // H present (Woodbury)
+  double alg = 0.0;
+  switch (kernel) {
+    case 0: alg = 8 * m * N + 8 * N + 8 * m; break;
+    case 1: alg = (12 * nnzQ + 4 * (K + 1)) + (12 * nnzD + 4 * (K + 1)) + (12 * nnzD + 4 * (N + 1)) + 8 * m * N +
+                  16 * (K + N) + 8 * m;
+      break;
+    case 2: alg = 48 * K + 32 * N + 8 * hm * N; break;
+    case 3: alg = 8 * hm * N + 24 * N + 8 * hm; break;
+    case 4: alg = bv; break;
+    case 5: alg = 96 * (K + N); break;
+    case 6: alg = 2.0 * m * m * N; break;
+    case 7:
+      alg = 16 * m * N + 16 * hm * N + (12 * nnzQ + 4 * (K + 1)) + 2 * (12 * nnzD + 4 * (N + 1)) + bv +
+            8 * (20 * (K + N) + K);
+      break;
+    default: throw std::invalid_argument("gnw_profile_kernel: unknown kernel");
+  }
+  *algorithmic = alg;
+  if (kernel == 7) {
+    *seconds = last_iterations ? t_minres / static_cast<double>(last_iterations) : 0.0;
+    return;
+  }
+  if ((kernel == 0 || kernel == 6) && m_ == 0) throw std::invalid_argument("gnw_profile_kernel: no Jacobian set");
+  const int64_t n = K_ + N_;
+  fill_zero(io_a_, n, s);
+  fill_zero(io_b_, n, s);
+  fill_zero(io_c_, n, s);
+  fill_zero(io_d_, n, s);
+  DeviceMemory pm;
+  double* part = nullptr;
+  DgemmPlan plan{};
+  if (kernel == 6) {
+    plan = dgemm_plan(static_cast<int>(m_), N_, 0, sm_count_);
+    part = pm.alloc<double>(static_cast<size_t>(plan.splits) * plan.npairs * plan.tile * plan.tile + 2 * 4096);
+  }
+  auto launch = [&]() {
+    switch (kernel) {
+      case 0: row_gemv(dJ_, static_cast<int>(m_), N_, vfixed(io_a_), K_, 0, st_plain_, gpart_, counters_ + 0, u_, plan_, s); break;
+      case 1: saddle_operator(op_, vfixed(io_a_), 0, u_ ? u_ : io_d_, vfixed(io_b_), st_plain_, 0, opart_, counters_ + 1, s); break;
+      case 2:
+        combine_precondition(pa_, vfixed(io_a_), vfixed(io_a_), vfixed(io_a_), vfixed(io_a_), vfixed(io_b_), 0,
+                             st_plain_, nullptr, cpart_, tpart_, counters_ + 2, t_, plan_, s);
+        break;
+      case 3:
+        finish_precondition(pa_, svc_, t2_ ? t2_ : io_d_, vfixed(io_a_), vfixed(io_b_), 0, st_plain_, cpart_,
+                            n_comb_blocks_, fpart_, counters_ + 3, s);
+        break;
+      case 4: vcycle(vfixed(io_a_ + K_), io_b_, st_plain_); break;
+      case 5:
+        minres_update(n, vfixed(io_a_), vfixed(io_a_), vfixed(io_a_), vfixed(io_a_), vfixed(io_b_), vfixed(io_a_),
+                      vfixed(io_a_), vfixed(io_c_), io_d_, tmp_, st_plain_, nullptr, nullptr, 0, upart_, counters_ + 4,
+                      0, 0, s);
+        break;
+      case 6: capacitance_dgemm(dJ_, dHt_ ? dHt_ : dJ_, static_cast<int>(m_), N_, beta_, plan, part, dC_ ? dC_ : io_d_, s); break;
+    }
+  };
+  launch();  // warm-up
+  sync();
+  cudaEvent_t e0, e1;
+  GNW_CUDA_CHECK(cudaEventCreate(&e0));
+  GNW_CUDA_CHECK(cudaEventCreate(&e1));
+  GNW_CUDA_CHECK(cudaEventRecord(e0, s));
+  for (int r = 0; r < reps; ++r) launch();
+  GNW_CUDA_CHECK(cudaEventRecord(e1, s));
+  sync();
+  float ms = 0.f;
+  GNW_CUDA_CHECK(cudaEventElapsedTime(&ms, e0, e1));
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  *seconds = ms * 1e-3 / reps;
 }
 
 void Context::dense_cholesky(int64_t n, const double* C, double* L) {

@@ -65,6 +65,10 @@ class Context {
   MinresResult minres(const double* b, const double* x0, double* x, double tol, uint64_t maxit);
   void get_woodbury(double* H, double* L);
   void dense_cholesky(int64_t n, const double* C, double* L);
+  void event_record(int slot);
+  double event_elapsed(int a, int b);
+  void profile_kernel(int kernel, int reps, double* seconds, double* algorithmic);
+  uint64_t last_iterations = 0;
 
   // structure
   const host::Mesh& mesh() const { return mesh_; }
@@ -148,6 +152,8 @@ class Context {
   double* io_d_ = nullptr;
   int* dflag_ = nullptr;
 
+  cudaEvent_t events_[16] = {};
+  bool j_borrowed_ = false;  // device-pointer J referenced, not copied (SaddleOperator holds a pointer)
   cudaGraph_t graph_ = nullptr;
   cudaGraphExec_t graph_exec_ = nullptr;
   uint64_t graph_nodes_ = 0;

@@ -240,6 +240,18 @@ gnw_status gnw_dense_cholesky(gnw_ctx* ctx, uint64_t n, const double* C, double*
   return guard([&] { ctx_of(ctx).dense_cholesky(static_cast<int64_t>(n), C, L); });
 }
 
+gnw_status gnw_event_record(gnw_ctx* ctx, int slot) {
+  return guard([&] { ctx_of(ctx).event_record(slot); });
+}
+
+gnw_status gnw_event_elapsed(gnw_ctx* ctx, int a, int b, double* seconds) {
+  return guard([&] { *seconds = ctx_of(ctx).event_elapsed(a, b); });
+}
+
+gnw_status gnw_profile_kernel(gnw_ctx* ctx, int kernel, int reps, double* seconds, double* algorithmic) {
+  return guard([&] { ctx_of(ctx).profile_kernel(kernel, reps, seconds, algorithmic); });
+}
+
 gnw_status gnw_get_stats(const gnw_ctx* ctx, gnw_stats* stats) {
   return guard([&] {
     const Context& c = ctx_of(ctx);

@@ -185,6 +185,20 @@ class Context:
         return x, MinresReport(int(rep.iterations), he[:nh].copy(), hp[:nh].copy(), bool(rep.converged),
                                float(rep.true_relative_residual))
 
+    def event_record(self, slot: int):
+        A.check(self.L.gnw_event_record(self.h, slot))
+
+    def event_elapsed(self, a: int, b: int) -> float:
+        s = C.c_double()
+        A.check(self.L.gnw_event_elapsed(self.h, a, b, C.byref(s)))
+        return s.value
+
+    def profile_kernel(self, name: str, reps: int = 10):
+        """(seconds per launch, algorithmic bytes-or-flops per launch) of one hot kernel."""
+        sec, alg = C.c_double(), C.c_double()
+        A.check(self.L.gnw_profile_kernel(self.h, A.KERNELS[name], reps, C.byref(sec), C.byref(alg)))
+        return sec.value, alg.value
+
     def woodbury_factors(self):
         """(H, L): H = S_hat^-1 J^T (N x m, h_hat layout) and the capacitance Cholesky factor."""
         H = np.zeros((self.N, self.m))
