@@ -71,6 +71,12 @@ class ClockSampler:
         self.index = index
         self.proc = None
         self.lines = []
+        self.marks = []
+
+    def mark(self):
+        if not self.marks:
+            time.sleep(0.25)  # let the sampler produce lines before the region starts
+        self.marks.append(len(self.lines))
 
     def __enter__(self):
         try:
@@ -98,7 +104,10 @@ class ClockSampler:
     def summary(self):
         sm, smax, reasons = [], 0.0, set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
+        lines = self.lines
+        if len(self.marks) >= 2:  # the timed region (plus one sample either side)
+            lines = self.lines[max(0, self.marks[0] - 1):self.marks[1] + 1]
+        for ln in lines:
             parts = [p.strip() for p in ln.split(",")]
             if len(parts) < 7:
                 continue
@@ -224,22 +233,24 @@ def run_gnw(args):
         st = ctx.stats()
         return tm, rep, st
 
+    clk = ClockSampler(local).__enter__()  # started early: nvidia-smi start-up stays out of the timed region
     for k in range(args.warmup):
         solve_dev(alphas[k % len(alphas)])
     barrier()
     per_step = []
     launches = 0
-    with ClockSampler(local) as clk:
-        ctx.event_record(0)
-        for k in range(args.steps):
-            a = alphas[k % len(alphas)]
-            tm, rep, st = solve_dev(a)
-            launches += int(st["kernel_launches"]) + int(st["setup_kernel_launches"]) + 1
-            per_step.append(dict(alpha=a, iterations=rep.iterations, converged=rep.converged,
-                                 true_rel=rep.true_relative_residual, t_H=tm["t_H"], t_C=tm["t_C"],
-                                 t_chol=tm["t_chol"], t_minres=st["t_minres"]))
-        ctx.event_record(1)
-        elapsed = ctx.event_elapsed(0, 1)
+    clk.mark()
+    ctx.event_record(0)
+    for k in range(args.steps):
+        a = alphas[k % len(alphas)]
+        tm, rep, st = solve_dev(a)
+        launches += int(st["kernel_launches"]) + int(st["setup_kernel_launches"]) + 1
+        per_step.append(dict(alpha=a, iterations=rep.iterations, converged=rep.converged,
+                             true_rel=rep.true_relative_residual, t_H=tm["t_H"], t_C=tm["t_C"],
+                             t_chol=tm["t_chol"], t_minres=st["t_minres"]))
+    ctx.event_record(1)
+    elapsed = ctx.event_elapsed(0, 1)
+    clk.mark()
     barrier()
     elapsed = max_over_ranks(elapsed)
     value = ws * args.steps / elapsed
@@ -329,6 +340,7 @@ def run_gnw(args):
             "phases": per_step,
         }
         print(json.dumps(line), flush=True)
+    clk.__exit__(None, None, None)
     ctx.close()
     if ws > 1:
         torch.distributed.destroy_process_group()

@@ -65,7 +65,10 @@ Context::Context(int device) : device_(device) {
   GNW_CUDA_CHECK(cudaGetDeviceProperties(&prop, device_));
   if (prop.major < 10) throw DeviceError("gnw: this build targets sm_100a (B200); found sm_" + std::to_string(prop.major) + std::to_string(prop.minor));
   sm_count_ = prop.multiProcessorCount;
-  GNW_CUDA_CHECK(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
+  // A blocking stream: ordered with the legacy default stream, so device-pointer
+  // callers (e.g. torch on its default stream) need no extra synchronisation.
+  GNW_CUDA_CHECK(cudaStreamCreateWithFlags(&stream_, cudaStreamDefault));
+  for (auto& e : mev_) GNW_CUDA_CHECK(cudaEventCreate(&e));
   st_ = mem_.alloc<MinresState>(1);
   st_plain_ = mem_.alloc<MinresState>(1);
   counters_ = mem_.alloc<unsigned>(16);
@@ -83,7 +86,12 @@ Context::~Context() {
   if (stream_) cudaStreamSynchronize(stream_);
   for (auto& e : events_)
     if (e) cudaEventDestroy(e);
+  for (auto& e : jev_)
+    if (e) cudaEventDestroy(e);
+  for (auto& e : mev_)
+    if (e) cudaEventDestroy(e);
   jmem_.reset();
+  bmem_.reset();
   mem_.release_all();
   if (h_st_) cudaFreeHost(h_st_);
   if (stream_) cudaStreamDestroy(stream_);
@@ -124,6 +132,11 @@ void Context::assemble(const double* vertices, int64_t nv, const int64_t* cells,
   if (device_ >= 0) {
     GNW_CUDA_CHECK(cudaSetDevice(device_));
     jmem_.reset();
+    bmem_.reset();
+    bmem_b_ = 0;
+    jm_m_ = -1;
+    dJ_ = nullptr;
+    pa_.m = 0;
     mem_.release_all();
     st_ = mem_.alloc<MinresState>(1);
     st_plain_ = mem_.alloc<MinresState>(1);
@@ -162,6 +175,11 @@ void Context::assemble_amg_csr(int64_t n, const int64_t* rowptr, const int64_t* 
   if (device_ >= 0) {
     GNW_CUDA_CHECK(cudaSetDevice(device_));
     jmem_.reset();
+    bmem_.reset();
+    bmem_b_ = 0;
+    jm_m_ = -1;
+    dJ_ = nullptr;
+    pa_.m = 0;
     mem_.release_all();
     st_ = mem_.alloc<MinresState>(1);
     st_plain_ = mem_.alloc<MinresState>(1);
@@ -184,6 +202,8 @@ void Context::upload_structure() {
   op_.Dt = upload_csr(mem_, host::transpose(D_), s);
   op_.K = K_;
   op_.N = N_;
+  dnib_ = mem_.alloc<double>(1);
+  op_.neg_inv_beta = dnib_;
   std::vector<double> qinv = host::diagonal(Q_);  // inversion.cpp:210-211
   for (double& v : qinv) v = 1.0 / v;
   pa_ = PrecArgs{};
@@ -192,6 +212,7 @@ void Context::upload_structure() {
   pa_.qinv = dq;
   pa_.K = K_;
   pa_.N = N_;
+  pa_.neg_inv_beta = dnib_;
   const int64_t n = K_ + N_;
   b_ = mem_.alloc<double>(n);
   x_ = mem_.alloc<double>(n);
@@ -215,9 +236,9 @@ void Context::upload_structure() {
   fpart_ = mem_.alloc<double>(nb * 3);
   upart_ = mem_.alloc<double>(nb * 3);
   rpart_ = mem_.alloc<double>(nb * 3);
-  cpart_ = mem_.alloc<double>(nb * 3);
   plan_ = row_gemv_plan(N_);
   n_comb_blocks_ = static_cast<int>((K_ + 255) / 256 + (N_ + plan_.chunk - 1) / plan_.chunk);
+  cpart_ = mem_.alloc<double>(3 * (static_cast<size_t>(n_comb_blocks_) + 16));  // one triple per combine block
 }
 
 void Context::upload_hierarchy() {
@@ -237,6 +258,11 @@ void Context::upload_hierarchy() {
       d.A = upload_csr(mem_, L.A, s);
       d.P = upload_csr(mem_, L.P, s);
       d.R = upload_csr(mem_, host::transpose(L.P), s);
+      // warp-per-row kernels once rows carry more than ~12 entries (levels >= 1..2)
+      constexpr double kWide = 12.0;
+      d.wideA = L.A.nnz() > kWide * static_cast<double>(L.A.n_rows);
+      d.wideP = L.P.nnz() > kWide * static_cast<double>(L.P.n_rows);
+      d.wideR = L.P.nnz() > kWide * static_cast<double>(L.P.n_cols);
       std::vector<double> wd(L.inv_diag.size());
       for (size_t i = 0; i < wd.size(); ++i) wd[i] = omega * L.inv_diag[i];  // amg.cpp:98 (omega*inv_diag)*r
       d.wd = mem_.alloc<double>(wd.size());
@@ -278,34 +304,62 @@ void Context::vcycle(VSel r0, double* out0, const MinresState* st) {
   }
   for (int l = 0; l < L - 1; ++l) {
     const VSel rl = l == 0 ? r0 : vfixed(vr_[l]);
-    vc_down(lv_[l], rl, vres_[l], st, s);
-    vc_restrict(lv_[l], vres_[l], vr_[l + 1], s);
+    const DLevel lev = level(l);
+    vc_down(lev, rl, vres_[l], st, s);
+    vc_restrict(lev, vres_[l], vr_[l + 1], s);
   }
   coarse(vfixed(vr_[L - 1]), ve_[L - 1]);
   for (int l = L - 2; l >= 0; --l) {
     const VSel rl = l == 0 ? r0 : vfixed(vr_[l]);
-    vc_up1(lv_[l], rl, ve_[l + 1], vx_[l], st, s);
-    vc_up2(lv_[l], rl, vx_[l], l == 0 ? out0 : ve_[l], st, s);
+    const DLevel lev = level(l);
+    vc_up1(lev, rl, ve_[l + 1], vx_[l], st, s);
+    vc_up2(lev, rl, vx_[l], l == 0 ? out0 : ve_[l], st, s);
   }
+}
+
+// Level l as launched: the reference-order (thread-per-row) kernels everywhere in
+// exact mode, warp-per-row kernels on wide levels otherwise.
+DLevel Context::level(int l) const {
+  DLevel d = lv_[l];
+  if (coarse_mode == 1) d.wideA = d.wideP = d.wideR = 0;
+  return d;
+}
+
+// Persistent work arrays of the batched V-cycle (b interleaved columns).
+void Context::ensure_batch(int b) {
+  if (bmem_ && bmem_b_ >= b) return;
+  bmem_.reset();
+  bmem_ = std::make_unique<DeviceMemory>();
+  const int L = static_cast<int>(lv_.size());
+  mr_.assign(L, nullptr);
+  me_.assign(L, nullptr);
+  mres_.assign(L, nullptr);
+  mx_.assign(L, nullptr);
+  for (int l = 0; l < L; ++l) {
+    const size_t nl = static_cast<size_t>(lv_[l].n) * b;
+    if (l > 0) {
+      mr_[l] = bmem_->alloc<double>(nl);
+      me_[l] = bmem_->alloc<double>(nl);
+    }
+    if (l + 1 < L) {
+      mres_[l] = bmem_->alloc<double>(nl);
+      mx_[l] = bmem_->alloc<double>(nl);
+    }
+  }
+  bR0_ = bmem_->alloc<double>(static_cast<size_t>(N_) * b);
+  bX0_ = bmem_->alloc<double>(static_cast<size_t>(N_) * b);
+  bmem_b_ = b;
 }
 
 // Multi-RHS V-cycle over b interleaved columns: r0/out0 are N x b.
 void Context::vcycle_batch(const double* r0, int b, double* out0) {
   const cudaStream_t s = stream_;
   const int L = static_cast<int>(lv_.size());
-  DeviceMemory work;
-  std::vector<double*> mr(L, nullptr), me(L, nullptr), mres(L, nullptr), mx(L, nullptr);
-  for (int l = 0; l < L; ++l) {
-    const size_t nl = static_cast<size_t>(lv_[l].n) * b;
-    if (l > 0) {
-      mr[l] = work.alloc<double>(nl);
-      me[l] = work.alloc<double>(nl);
-    }
-    if (l + 1 < L) {
-      mres[l] = work.alloc<double>(nl);
-      mx[l] = work.alloc<double>(nl);
-    }
-  }
+  ensure_batch(b);
+  std::vector<double*>& mr = mr_;
+  std::vector<double*>& me = me_;
+  std::vector<double*>& mres = mres_;
+  std::vector<double*>& mx = mx_;
   auto coarse = [&](const double* r, double* x) {
     if (coarse_mode == 1)
       coarse_cholesky(coarse_L_, nc_, vfixed(const_cast<double*>(r)), x, st_plain_, b, b, s);
@@ -317,17 +371,18 @@ void Context::vcycle_batch(const double* r0, int b, double* out0) {
   } else {
     for (int l = 0; l < L - 1; ++l) {
       const double* rl = l == 0 ? r0 : mr[l];
-      mvc_down(lv_[l], rl, b, mres[l], b, s);
-      mvc_restrict(lv_[l], mres[l], mr[l + 1], b, s);
+      const DLevel lev = level(l);
+      mvc_down(lev, rl, b, mres[l], b, s);
+      mvc_restrict(lev, mres[l], mr[l + 1], b, s);
     }
     coarse(mr[L - 1], me[L - 1]);
     for (int l = L - 2; l >= 0; --l) {
       const double* rl = l == 0 ? r0 : mr[l];
-      mvc_up1(lv_[l], rl, b, me[l + 1], mx[l], b, s);
-      mvc_up2(lv_[l], rl, b, mx[l], l == 0 ? out0 : me[l], b, b, s);
+      const DLevel lev = level(l);
+      mvc_up1(lev, rl, b, me[l + 1], mx[l], b, s);
+      mvc_up2(lev, rl, b, mx[l], l == 0 ? out0 : me[l], b, b, s);
     }
   }
-  sync();  // `work` is released at scope exit
 }
 
 // ------------------------------------------------------------ stage helpers
@@ -353,84 +408,102 @@ void Context::set_jacobian(const double* J, int64_t m, int64_t n_cells, double b
   if (m > 0 && !(beta > 0.0)) throw std::invalid_argument("build_woodbury_preconditioner: beta <= 0");
   if (m > 0 && n_cells != N_) throw std::invalid_argument("build_woodbury_preconditioner: J shape mismatch");
   require_device();
-  destroy_graph();
-  jmem_.reset();
-  dJ_ = dHt_ = dC_ = dL_ = dCinv_ = dY_ = nullptr;
-  u_ = t_ = t2_ = gpart_ = tpart_ = nullptr;
-  j_borrowed_ = false;
   m_ = m;
   beta_ = beta;
-  op_.J = nullptr;
-  op_.m = 0;
-  op_.neg_inv_beta = -1.0 / beta;
-  pa_.m = 0;
-  pa_.Ht = pa_.Cinv = pa_.Lc = nullptr;
-  pa_.neg_inv_beta = -1.0 / beta;
-  if (m == 0) return;  // Laplace-only preconditioner (inversion.cpp:251-256)
+  {
+    const double nib = -1.0 / beta;  // axpy(-1.0 / beta, ...), inversion.cpp:66, :85
+    GNW_CUDA_CHECK(cudaMemcpyAsync(dnib_, &nib, sizeof(double), cudaMemcpyHostToDevice, stream_));
+  }
+  if (m == 0) {  // no low-rank term at all (J == nullptr in SaddleOperator and preconditioner)
+    destroy_graph();
+    op_.J = nullptr;
+    op_.m = 0;
+    pa_.m = 0;
+    pa_.Ht = pa_.Cinv = pa_.Lc = nullptr;
+    return;
+  }
   if (m > 8192) throw std::invalid_argument("gnw_set_jacobian: m > 8192 not supported");
 
   const cudaStream_t s = stream_;
-  jmem_ = std::make_unique<DeviceMemory>();
-  DeviceMemory& jm = *jmem_;
   const size_t mN = static_cast<size_t>(m) * N_;
-  u_ = jm.alloc<double>(m);
-  gpart_ = jm.alloc<double>(static_cast<size_t>(plan_.nchunks) * m);
+  // Jacobian-shaped buffers persist across calls with the same (m, N, pointer
+  // mode): no cudaMalloc/cudaFree (and no implied device sync) per GN step.
+  const bool want_owned = ptr_mode != 1;
+  if (!jmem_ || jm_m_ != m || jm_owned_ != want_owned) {
+    destroy_graph();
+    jmem_.reset();
+    jmem_ = std::make_unique<DeviceMemory>();
+    DeviceMemory& jm = *jmem_;
+    u_ = jm.alloc<double>(m);
+    gpart_ = jm.alloc<double>(static_cast<size_t>(plan_.nchunks) * m);
+    jown_ = want_owned ? jm.alloc<double>(mN) : nullptr;
+    dHt_ = jm.alloc<double>(mN);
+    dC_ = jm.alloc<double>(m * m);
+    dL_ = jm.alloc<double>(m * m);
+    dCinv_ = jm.alloc<double>(m * m);
+    dY_ = jm.alloc<double>(m * m);
+    t_ = jm.alloc<double>(m);
+    t2_ = jm.alloc<double>(m);
+    tpart_ = jm.alloc<double>(static_cast<size_t>(plan_.nchunks) * m);
+    const DgemmPlan lo = dgemm_plan(static_cast<int>(m), N_, 0, sm_count_);
+    const DgemmPlan fu = dgemm_plan(static_cast<int>(m), N_, 1, sm_count_);
+    const size_t pl = static_cast<size_t>(lo.splits) * lo.npairs * lo.tile * lo.tile;
+    const size_t pf = static_cast<size_t>(fu.splits) * fu.npairs * fu.tile * fu.tile;
+    dpart_ = jm.alloc<double>(std::max(pl, pf) + 2 * 4096);
+    jm_m_ = m;
+    jm_owned_ = want_owned;
+    for (auto& e : jev_)
+      if (!e) GNW_CUDA_CHECK(cudaEventCreate(&e));
+  }
   if (ptr_mode == 1) {
     // Device pointers: J is referenced, not copied -- the reference's
     // SaddleOperator/WoodburyPreconditioner also hold a non-owning pointer to J
     // (inversion.hpp:21, :35); the caller keeps it alive while the context uses it.
+    if (dJ_ != J) destroy_graph();  // the loop graph bakes the J pointer
     dJ_ = const_cast<double*>(J);
     j_borrowed_ = true;
   } else {
-    dJ_ = jm.alloc<double>(mN);
+    dJ_ = jown_;
     j_borrowed_ = false;
     GNW_CUDA_CHECK(cudaMemcpyAsync(dJ_, J, mN * sizeof(double), cudaMemcpyHostToDevice, s));
   }
   op_.J = dJ_;
   op_.m = static_cast<int>(m);
   if (pc_laplace) {  // Alg. 4: J stays in the operator, plain Laplace preconditioner
+    if (pa_.m != 0) destroy_graph();
+    pa_.m = 0;
     sync();
     return;
   }
-  dHt_ = jm.alloc<double>(mN);
-  dC_ = jm.alloc<double>(m * m);
-  dL_ = jm.alloc<double>(m * m);
-  dCinv_ = jm.alloc<double>(m * m);
-  dY_ = jm.alloc<double>(m * m);
-  t_ = jm.alloc<double>(m);
-  t2_ = jm.alloc<double>(m);
-  tpart_ = jm.alloc<double>(static_cast<size_t>(plan_.nchunks) * m);
+  if (pa_.m != static_cast<int>(m)) destroy_graph();
 
-  cudaEvent_t ev[4];
-  for (auto& e : ev) GNW_CUDA_CHECK(cudaEventCreate(&e));
+  cudaEvent_t* ev = jev_;
   const uint64_t l0 = launch_count();
   GNW_CUDA_CHECK(cudaEventRecord(ev[0], s));
   // H = S_hat^-1 J^T by batched V-cycles (inversion.cpp:107-114); stored as Ht (m x N)
   {
-    size_t free_b = 0, total_b = 0;
-    cudaMemGetInfo(&free_b, &total_b);
-    const double per_col = 8.0 * static_cast<double>(N_) * 6.0;  // level-0 arrays x ~2 for coarser levels
-    int64_t bmax = static_cast<int64_t>(0.5 * static_cast<double>(free_b) / per_col);
-    bmax = std::max<int64_t>(32, std::min<int64_t>(bmax, 512) / 32 * 32);
-    const int b = static_cast<int>(std::min<int64_t>(((m + 31) / 32) * 32, bmax));
-    DeviceMemory bm;
-    double* R0 = bm.alloc<double>(static_cast<size_t>(N_) * b);
-    double* X0 = bm.alloc<double>(static_cast<size_t>(N_) * b);
+    int b = bmem_b_;
+    if (b < ((m + 31) / 32) * 32 && b < 512) {
+      size_t free_b = 0, total_b = 0;
+      cudaMemGetInfo(&free_b, &total_b);
+      const double per_col = 8.0 * static_cast<double>(N_) * 8.0;  // level-0 arrays x ~2 for coarser levels
+      int64_t bmax = static_cast<int64_t>(0.5 * static_cast<double>(free_b) / per_col);
+      bmax = std::max<int64_t>(32, std::min<int64_t>(bmax, 512) / 32 * 32);
+      b = static_cast<int>(std::min<int64_t>(((m + 31) / 32) * 32, bmax));
+      ensure_batch(b);
+    }
     for (int64_t i0 = 0; i0 < m; i0 += b) {
       const int bb = static_cast<int>(std::min<int64_t>(b, m - i0));
-      transpose_rows_to_batch(dJ_, N_, static_cast<int>(i0), bb, R0, s);
-      vcycle_batch(R0, bb, X0);
-      transpose_batch_to_rows(X0, N_, static_cast<int>(i0), bb, dHt_, s);
+      transpose_rows_to_batch(dJ_, N_, static_cast<int>(i0), bb, bR0_, s);
+      vcycle_batch(bR0_, bb, bX0_);
+      transpose_batch_to_rows(bX0_, N_, static_cast<int>(i0), bb, dHt_, s);
     }
     GNW_CUDA_CHECK(cudaEventRecord(ev[1], s));
-    sync();
   }
   // C = I + (J H)/beta (inversion.cpp:37-43), lower triangle
   DgemmPlan plan = dgemm_plan(static_cast<int>(m), N_, 0, sm_count_);
   {
-    DeviceMemory pm;
-    double* part = pm.alloc<double>(static_cast<size_t>(plan.splits) * plan.npairs * plan.tile * plan.tile + 2 * 4096);
-    capacitance_dgemm(dJ_, dHt_, static_cast<int>(m), N_, beta, plan, part, dC_, s);
+    capacitance_dgemm(dJ_, dHt_, static_cast<int>(m), N_, beta, plan, dpart_, dC_, s);
     GNW_CUDA_CHECK(cudaEventRecord(ev[2], s));
     // L = chol(C), retry once after symmetrisation (inversion.cpp:21-35)
     cholesky(dC_, dL_, static_cast<int>(m), dflag_, s);
@@ -439,9 +512,7 @@ void Context::set_jacobian(const double* J, int64_t m, int64_t n_cells, double b
     sync();
     if (fail) {
       DgemmPlan full = dgemm_plan(static_cast<int>(m), N_, 1, sm_count_);
-      DeviceMemory pm2;
-      double* part2 = pm2.alloc<double>(static_cast<size_t>(full.splits) * full.npairs * full.tile * full.tile + 2 * 4096);
-      capacitance_dgemm(dJ_, dHt_, static_cast<int>(m), N_, beta, full, part2, dC_, s);
+      capacitance_dgemm(dJ_, dHt_, static_cast<int>(m), N_, beta, full, dpart_, dC_, s);
       symmetrize(dC_, static_cast<int>(m), s);
       cholesky(dC_, dL_, static_cast<int>(m), dflag_, s);
       GNW_CUDA_CHECK(cudaMemcpyAsync(&fail, dflag_, sizeof(int), cudaMemcpyDeviceToHost, s));
@@ -454,7 +525,6 @@ void Context::set_jacobian(const double* J, int64_t m, int64_t n_cells, double b
   }
   float ms[3];
   for (int k = 0; k < 3; ++k) GNW_CUDA_CHECK(cudaEventElapsedTime(&ms[k], ev[k], ev[k + 1]));
-  for (auto& e : ev) cudaEventDestroy(e);
   if (timings) {
     timings[0] = ms[0] * 1e-3;
     timings[1] = ms[1] * 1e-3;
@@ -862,7 +932,7 @@ void Context::profile_kernel(int kernel, int reps, double* seconds, double* algo
       case 5:
         minres_update(n, vfixed(io_a_), vfixed(io_a_), vfixed(io_a_), vfixed(io_a_), vfixed(io_b_), vfixed(io_a_),
                       vfixed(io_a_), vfixed(io_c_), io_d_, tmp_, st_plain_, nullptr, nullptr, 0, upart_, counters_ + 4,
-                      0, 0, s);
+                      0, 2, s);
         break;
       case 6: capacitance_dgemm(dJ_, dHt_ ? dHt_ : dJ_, static_cast<int>(m_), N_, beta_, plan, part, dC_ ? dC_ : io_d_, s); break;
     }

@@ -53,6 +53,10 @@ class Context {
   int ptr_mode = 0;
   int coarse_mode = 0;
   int pc_laplace = 0;  // GnAlgorithm::kLaplaceMinres (inversion.cpp:251-256)
+  void set_coarse(int mode) {
+    if (mode != coarse_mode) destroy_graph();  // the loop graph bakes the kernel choice
+    coarse_mode = mode;
+  }
 
   void assemble(const double* vertices, int64_t nv, const int64_t* cells, int64_t nc, const host::AmgOptions& o);
   void assemble_amg_csr(int64_t n, const int64_t* rowptr, const int64_t* cols, const double* vals,
@@ -94,6 +98,8 @@ class Context {
   void upload_hierarchy();
   void vcycle(VSel r0, double* out0, const MinresState* st);
   void vcycle_batch(const double* r0, int b, double* out0);
+  DLevel level(int l) const;
+  void ensure_batch(int b);
   void operator_into(VSel x, int scaled, VSel y, MinresState* st, int loop);
   void precondition_into(VSel y, VSel yv2, VSel z, MinresState* st, int loop, VSel vcur, VSel vprev);
   void build_graph();
@@ -123,6 +129,10 @@ class Context {
   int nc_ = 0;
   std::vector<double*> vr_, ve_, vres_, vx_;  // single-RHS V-cycle work per level
   double* svc_ = nullptr;                     // V-cycle output (s)
+  std::unique_ptr<DeviceMemory> bmem_;        // batched V-cycle work (persists across set_jacobian)
+  int bmem_b_ = 0;
+  std::vector<double*> mr_, me_, mres_, mx_;
+  double *bR0_ = nullptr, *bX0_ = nullptr;
 
   // Jacobian / Woodbury
   int64_t m_ = 0;
@@ -153,6 +163,13 @@ class Context {
   int* dflag_ = nullptr;
 
   cudaEvent_t events_[16] = {};
+  cudaEvent_t jev_[4] = {};    // set_jacobian phase timers
+  cudaEvent_t mev_[2] = {};    // minres timers
+  int64_t jm_m_ = -1;          // shape of the persistent Jacobian buffers
+  bool jm_owned_ = false;
+  double* jown_ = nullptr;     // owned copy of J (host-pointer mode)
+  double* dpart_ = nullptr;    // DGEMM split-K partials
+  double* dnib_ = nullptr;     // device scalar -1/beta
   bool j_borrowed_ = false;  // device-pointer J referenced, not copied (SaddleOperator holds a pointer)
   cudaGraph_t graph_ = nullptr;
   cudaGraphExec_t graph_exec_ = nullptr;

@@ -96,7 +96,7 @@ gnw_status gnw_set_pointer_mode(gnw_ctx* ctx, int mode) {
 gnw_status gnw_set_coarse_mode(gnw_ctx* ctx, int mode) {
   return guard([&] {
     if (mode != GNW_COARSE_INVERSE && mode != GNW_COARSE_CHOLESKY) throw std::invalid_argument("gnw_set_coarse_mode: bad mode");
-    ctx_of(ctx).coarse_mode = mode;
+    ctx_of(ctx).set_coarse(mode);
   });
 }
 

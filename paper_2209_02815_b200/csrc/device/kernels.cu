@@ -135,19 +135,25 @@ __global__ void k_coarse_cholesky(const double* __restrict__ L, int n, VSel rs, 
   }
 }
 
+void note_launch(const char* what) { check_launch(what); }
+
 void vc_down(const DLevel& L, VSel r, double* resid, const MinresState* st, cudaStream_t s) {
+  if (L.wideA) return vcw_down(L, r, resid, st, s);
   k_vc_down<<<grid_for(L.n), kTpb, 0, s>>>(L.A, L.wd, r, resid, st);
   check_launch("vc_down");
 }
 void vc_restrict(const DLevel& L, const double* resid, double* rc, cudaStream_t s) {
+  if (L.wideR) return vcw_restrict(L, resid, rc, s);
   k_vc_restrict<<<grid_for(L.R.n_rows), kTpb, 0, s>>>(L.R, resid, rc);
   check_launch("vc_restrict");
 }
 void vc_up1(const DLevel& L, VSel r, const double* ec, double* x, const MinresState* st, cudaStream_t s) {
+  if (L.wideP) return vcw_up1(L, r, ec, x, st, s);
   k_vc_up1<<<grid_for(L.n), kTpb, 0, s>>>(L.P, L.wd, r, ec, x, st);
   check_launch("vc_up1");
 }
 void vc_up2(const DLevel& L, VSel r, const double* x, double* out, const MinresState* st, cudaStream_t s) {
+  if (L.wideA) return vcw_up2(L, r, x, out, st, s);
   k_vc_up2<<<grid_for(L.n), kTpb, 0, s>>>(L.A, L.wd, r, x, out, st);
   check_launch("vc_up2");
 }
@@ -221,22 +227,26 @@ __global__ void __launch_bounds__(256) k_mvc_up2(DCsr A, const double* __restric
 }
 
 void mvc_down(const DLevel& L, const double* r, int ldr, double* resid, int b, cudaStream_t s) {
+  if (L.wideA) return mvce_down(L, r, ldr, resid, b, s);
   dim3 grid((L.n + 7) / 8, (b + 31) / 32), block(32, 8);
   k_mvc_down<<<grid, block, 0, s>>>(L.A, L.wd, r, ldr, resid, b);
   check_launch("mvc_down");
 }
 void mvc_restrict(const DLevel& L, const double* resid, double* rc, int b, cudaStream_t s) {
+  if (L.wideR) return mvce_restrict(L, resid, rc, b, s);
   dim3 grid((L.R.n_rows + 7) / 8, (b + 31) / 32), block(32, 8);
   k_mvc_restrict<<<grid, block, 0, s>>>(L.R, resid, rc, b);
   check_launch("mvc_restrict");
 }
 void mvc_up1(const DLevel& L, const double* r, int ldr, const double* ec, double* x, int b, cudaStream_t s) {
+  if (L.wideP) return mvce_up1(L, r, ldr, ec, x, b, s);
   dim3 grid((L.n + 7) / 8, (b + 31) / 32), block(32, 8);
   k_mvc_up1<<<grid, block, 0, s>>>(L.P, L.wd, r, ldr, ec, x, b);
   check_launch("mvc_up1");
 }
 void mvc_up2(const DLevel& L, const double* r, int ldr, const double* x, double* out, int ldo, int b,
              cudaStream_t s) {
+  if (L.wideA) return mvce_up2(L, r, ldr, x, out, ldo, b, s);
   dim3 grid((L.n + 7) / 8, (b + 31) / 32), block(32, 8);
   k_mvc_up2<<<grid, block, 0, s>>>(L.A, L.wd, r, ldr, x, out, ldo, b);
   check_launch("mvc_up2");
@@ -298,36 +308,59 @@ void transpose_batch_to_rows(const double* X, long long cols, int r0, int b, dou
 // ======================================================================
 // Row GEMV with chunked columns: out[i] = sum_c A[i, c] x[c] (deterministic)
 // ======================================================================
+// Column chunks sized so the grid is a multiple of the SM count (148 on B200):
+// every SM streams the same number of bytes (no partial last wave).
 RowGemv row_gemv_plan(long long N) {
   RowGemv p;
-  long long target = (N + 2 * 148 - 1) / (2 * 148);
-  int chunk = 256;
-  while (chunk < target && chunk < 4096) chunk *= 2;
-  p.chunk = chunk;
+  const long long ctas = 148LL * 4;
+  long long chunk = (N + ctas - 1) / ctas;
+  chunk = std::max<long long>(64, (chunk + 63) / 64 * 64);
+  chunk = std::min<long long>(chunk, 4096);
+  p.chunk = static_cast<int>(chunk);
   p.nchunks = static_cast<int>((N + chunk - 1) / chunk);
   return p;
 }
 
-// dot of row segment A[row, c0 : c0+len] with smem x; warp-cooperative
-__device__ __forceinline__ double warp_row_dot(const double* __restrict__ a, const double* __restrict__ xs,
-                                               int len, bool vec_ok, int lane) {
-  double acc = 0.0;
+// R row segments A[row_r, c0 : c0+len] dotted with the smem vector xs, one warp;
+// R independent rows keep R x 2 x 16-byte loads in flight per lane.
+template <int R>
+__device__ __forceinline__ void warp_rows_dot(const double* __restrict__ a, long long ld, int nrows,
+                                              const double* __restrict__ xs, int len, bool vec_ok, int lane,
+                                              double (&out)[R]) {
+  double acc[R];
+#pragma unroll
+  for (int r = 0; r < R; ++r) acc[r] = 0.0;
   if (vec_ok) {
     const int len2 = len & ~1;
-#pragma unroll 4
+#pragma unroll 2
     for (int t = lane * 2; t < len2; t += 64) {
-      const double2 v = __ldg(reinterpret_cast<const double2*>(a + t));
-      acc = acc + v.x * xs[t];
-      acc = acc + v.y * xs[t + 1];
+      const double x0 = xs[t], x1 = xs[t + 1];
+      double2 v[R];
+#pragma unroll
+      for (int r = 0; r < R; ++r)
+        v[r] = r < nrows ? __ldg(reinterpret_cast<const double2*>(a + r * ld + t)) : make_double2(0.0, 0.0);
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        acc[r] = acc[r] + v[r].x * x0;
+        acc[r] = acc[r] + v[r].y * x1;
+      }
     }
-    if ((len & 1) && lane == 0) acc = acc + __ldg(a + len - 1) * xs[len - 1];
+    if ((len & 1) && lane == 0)
+#pragma unroll
+      for (int r = 0; r < R; ++r)
+        if (r < nrows) acc[r] = acc[r] + __ldg(a + r * ld + len - 1) * xs[len - 1];
   } else {
-    for (int t = lane; t < len; t += 32) acc = acc + __ldg(a + t) * xs[t];
+    for (int t = lane; t < len; t += 32)
+#pragma unroll
+      for (int r = 0; r < R; ++r)
+        if (r < nrows) acc[r] = acc[r] + __ldg(a + r * ld + t) * xs[t];
   }
-  double v[1] = {acc};
-  warp_reduce<1>(v);
-  return v[0];
+  warp_reduce<R>(acc);
+#pragma unroll
+  for (int r = 0; r < R; ++r) out[r] = acc[r];
 }
+
+constexpr int kRowsPerWarp = 4;
 
 __global__ void __launch_bounds__(kTpb) k_row_gemv(const double* __restrict__ A, int m, long long N, VSel xs,
                                                    long long xoff, int scaled, const MinresState* st,
@@ -342,9 +375,14 @@ __global__ void __launch_bounds__(kTpb) k_row_gemv(const double* __restrict__ A,
   __syncthreads();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
   const bool vec_ok = ((N & 1) == 0);
-  for (int row = warp; row < m; row += nw) {
-    const double d = warp_row_dot(A + static_cast<long long>(row) * N + c0, xsm, len, vec_ok, lane);
-    if (lane == 0) partial[static_cast<long long>(blockIdx.x) * m + row] = d;
+  for (int row = warp * kRowsPerWarp; row < m; row += nw * kRowsPerWarp) {
+    double d[kRowsPerWarp];
+    const int nr = min(kRowsPerWarp, m - row);
+    warp_rows_dot<kRowsPerWarp>(A + static_cast<long long>(row) * N + c0, N, nr, xsm, len, vec_ok, lane, d);
+    if (lane == 0)
+#pragma unroll
+      for (int r = 0; r < kRowsPerWarp; ++r)
+        if (r < nr) partial[static_cast<long long>(blockIdx.x) * m + row + r] = d[r];
   }
   // last block reduces over chunks in index order
   __shared__ bool am_last;
@@ -421,7 +459,7 @@ __global__ void __launch_bounds__(kTpb) k_saddle(OperatorArgs op, VSel xs, int s
         const double* __restrict__ Jc = op.J + c;
 #pragma unroll 8
         for (int i = 0; i < op.m; ++i) jt = jt + __ldg(Jc + static_cast<long long>(i) * op.N) * usm[i];
-        o = o + op.neg_inv_beta * jt;  // axpy(-1.0 / beta, jtjdm, out2)
+        o = o + *op.neg_inv_beta * jt;  // axpy(-1.0 / beta, jtjdm, out2)
       }
       y[op.K + c] = o;
       dotv[0] = o * (scaled ? z[op.K + c] * sc : z[op.K + c]);
@@ -507,9 +545,15 @@ __global__ void __launch_bounds__(kTpb) k_combine_prec(PrecArgs pa, VSel azs, VS
       const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
       const bool vec_ok = ((pa.N & 1) == 0);
       const long long cb = blockIdx.x - nb_edge;
-      for (int row = warp; row < pa.m; row += nw) {
-        const double s = warp_row_dot(pa.Ht + static_cast<long long>(row) * pa.N + c0, vsm, len, vec_ok, lane);
-        if (lane == 0) t_part[cb * pa.m + row] = s;
+      for (int row = warp * kRowsPerWarp; row < pa.m; row += nw * kRowsPerWarp) {
+        double d[kRowsPerWarp];
+        const int nr = min(kRowsPerWarp, pa.m - row);
+        warp_rows_dot<kRowsPerWarp>(pa.Ht + static_cast<long long>(row) * pa.N + c0, pa.N, nr, vsm, len, vec_ok,
+                                    lane, d);
+        if (lane == 0)
+#pragma unroll
+          for (int r = 0; r < kRowsPerWarp; ++r)
+            if (r < nr) t_part[cb * pa.m + row + r] = d[r];
       }
     }
   }
@@ -586,7 +630,7 @@ __global__ void __launch_bounds__(kTpb) k_finish_prec(PrecArgs pa, const double*
       const double* __restrict__ Hc = pa.Ht + c;
 #pragma unroll 8
       for (int q = 0; q < pa.m; ++q) w = w + __ldg(Hc + static_cast<long long>(q) * pa.N) * tsm[q];
-      z = z + pa.neg_inv_beta * w;
+      z = z + *pa.neg_inv_beta * w;
     }
     zn[pa.K + c] = z;
     const double v = vn[pa.K + c];
@@ -651,7 +695,7 @@ __global__ void __launch_bounds__(kTpb) k_minres_update(long long n, VSel zs, VS
                                                         double* part, unsigned* counter,
                                                         cudaGraphConditionalHandle handle, int use_cond) {
   __shared__ double red[kTpb / 32];
-  if (st->status != kRunning) {
+  if (use_cond != 2 && st->status != kRunning) {  // use_cond == 2: isolated timing, no loop control
     if (use_cond && blockIdx.x == 0 && threadIdx.x == 0) cudaGraphSetConditional(handle, 0);
     return;
   }
@@ -683,7 +727,7 @@ __global__ void __launch_bounds__(kTpb) k_minres_update(long long n, VSel zs, VS
     rr[0] = rr[0] + ri * ri;
   }
   double tot[1];
-  if (!grid_reduce_last<1>(rr, part, counter, red, tot) || threadIdx.x != 0) return;
+  if (!grid_reduce_last<1>(rr, part, counter, red, tot) || threadIdx.x != 0 || use_cond == 2) return;
   const long long j = st->j;
   const double rel = sqrt(tot[0]) / st->bnorm;
   st->iterations = j;

@@ -15,7 +15,20 @@ struct DLevel {
   DCsr A, P, R;
   double* wd = nullptr;  // omega * inv_diag (rounded exactly as amg.cpp:98)
   int n = 0;             // rows of A
+  // warp-per-row kernels (vcycle_wide.cu) for matrices with many entries per row
+  int wideA = 0, wideP = 0, wideR = 0;
 };
+
+// wide-level kernels (vcycle_wide.cu)
+void vcw_down(const DLevel& L, VSel r, double* resid, const MinresState* st, cudaStream_t s);
+void vcw_restrict(const DLevel& L, const double* resid, double* rc, cudaStream_t s);
+void vcw_up1(const DLevel& L, VSel r, const double* ec, double* x, const MinresState* st, cudaStream_t s);
+void vcw_up2(const DLevel& L, VSel r, const double* x, double* out, const MinresState* st, cudaStream_t s);
+void mvce_down(const DLevel& L, const double* r, int ldr, double* resid, int b, cudaStream_t s);
+void mvce_restrict(const DLevel& L, const double* resid, double* rc, int b, cudaStream_t s);
+void mvce_up1(const DLevel& L, const double* r, int ldr, const double* ec, double* x, int b, cudaStream_t s);
+void mvce_up2(const DLevel& L, const double* r, int ldr, const double* x, double* out, int ldo, int b,
+              cudaStream_t s);
 
 // ------------------------------------------------------------------ V-cycle
 // Single right-hand side (amg.cpp:90-111); `r` may be a ring slot (level 0).
@@ -50,7 +63,7 @@ struct OperatorArgs {
   const double* J = nullptr;  // m x N row-major (nullptr: no low-rank term)
   int m = 0;
   long long K = 0, N = 0;
-  double neg_inv_beta = 0.0;  // -1/beta
+  const double* neg_inv_beta = nullptr;  // device scalar -1/beta (graph-stable across beta)
 };
 
 // u = A[:, ] x2 * scale partial GEMV over rows of a row-major (m x N) matrix,
@@ -77,7 +90,7 @@ struct PrecArgs {
   const double* Lc = nullptr;   // m x m lower Cholesky factor of C (exact mode)
   int m = 0;
   long long K = 0, N = 0;
-  double neg_inv_beta = 0.0;
+  const double* neg_inv_beta = nullptr;
   int exact = 0;
 };
 

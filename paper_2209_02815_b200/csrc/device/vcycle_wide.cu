@@ -1,0 +1,185 @@
+// vcycle_wide.cu -- V-cycle kernels for WIDE levels (many nonzeros per row).
+//
+// Thread-per-row CSR (kernels.cu) reproduces the reference's sequential row sums
+// bit for bit, but on the coarse SA-AMG levels rows hold 25..400 entries and
+// only a few hundred rows exist (C2: 5541 x 72, 1147 x 150, then 396..171 dense
+// rows), so one thread walking a row serialises hundreds of dependent loads.
+// Here a warp owns a row: lane l accumulates the entries k = start + l,
+// start + l + 32, ... in order, then the lanes combine through the xor
+// butterfly (16, 8, 4, 2, 1).  That order is deterministic but not the
+// reference's; GNW_COARSE_CHOLESKY ("exact") mode never uses these kernels.
+//
+// The multi-RHS kernels (H = S^-1 J^T, b interleaved columns) run one thread per
+// (row, column) and EMULATE the same lane partition and butterfly with 32
+// register partials, so every column of a batched V-cycle is bit-identical to
+// the single-RHS V-cycle of the MINRES loop.
+#include <cuda_runtime.h>
+
+#include "kernels.cuh"
+
+namespace gnw {
+
+void note_launch(const char* what);
+
+namespace {
+
+__device__ __forceinline__ double tree32(double (&p)[32]) {
+  // lane 0's view of the xor butterfly: own + partner at offsets 16, 8, 4, 2, 1
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+    for (int l = 0; l < o; ++l) p[l] = p[l] + p[l + o];
+  return p[0];
+}
+
+template <class F>
+__device__ __forceinline__ double warp_row(const DCsr& A, int i, int lane, F f) {
+  double acc = 0.0;
+  const int k1 = A.rowptr[i + 1];
+  for (int k = A.rowptr[i] + lane; k < k1; k += 32) acc = acc + __ldg(&A.vals[k]) * f(A.cols[k]);
+  double v[1] = {acc};
+  warp_reduce<1>(v);
+  return v[0];
+}
+
+template <class F>
+__device__ __forceinline__ double emul_row(const DCsr& A, int i, F f) {
+  double p[32];
+  const int k0 = A.rowptr[i], k1 = A.rowptr[i + 1];
+#pragma unroll
+  for (int l = 0; l < 32; ++l) {
+    double acc = 0.0;
+    for (int k = k0 + l; k < k1; k += 32) acc = acc + __ldg(&A.vals[k]) * f(A.cols[k]);
+    p[l] = acc;
+  }
+  return tree32(p);
+}
+
+constexpr int kRowsPerBlock = 8;  // 8 warps, one row each
+
+}  // namespace
+
+// --------------------------------------------------------------- single RHS
+__global__ void __launch_bounds__(256) k_vcw_down(DCsr A, const double* __restrict__ wd, VSel rs,
+                                                  double* __restrict__ resid, const MinresState* st) {
+  const double* __restrict__ r = vsel(rs, st);
+  const int i = blockIdx.x * kRowsPerBlock + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+  if (i >= A.n_rows) return;
+  const double s = warp_row(A, i, lane, [&](int c) { return __ldg(&wd[c]) * r[c]; });
+  if (lane == 0) resid[i] = r[i] + (-1.0 * s);
+}
+
+__global__ void __launch_bounds__(256) k_vcw_restrict(DCsr R, const double* __restrict__ resid,
+                                                      double* __restrict__ rc) {
+  const int a = blockIdx.x * kRowsPerBlock + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+  if (a >= R.n_rows) return;
+  const double s = warp_row(R, a, lane, [&](int c) { return resid[c]; });
+  if (lane == 0) rc[a] = s;
+}
+
+__global__ void __launch_bounds__(256) k_vcw_up1(DCsr P, const double* __restrict__ wd, VSel rs,
+                                                 const double* __restrict__ ec, double* __restrict__ x,
+                                                 const MinresState* st) {
+  const double* __restrict__ r = vsel(rs, st);
+  const int i = blockIdx.x * kRowsPerBlock + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+  if (i >= P.n_rows) return;
+  const double s = warp_row(P, i, lane, [&](int c) { return ec[c]; });
+  if (lane == 0) x[i] = __ldg(&wd[i]) * r[i] + 1.0 * s;
+}
+
+__global__ void __launch_bounds__(256) k_vcw_up2(DCsr A, const double* __restrict__ wd, VSel rs,
+                                                 const double* __restrict__ x, double* __restrict__ out,
+                                                 const MinresState* st) {
+  const double* __restrict__ r = vsel(rs, st);
+  const int i = blockIdx.x * kRowsPerBlock + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+  if (i >= A.n_rows) return;
+  const double s = warp_row(A, i, lane, [&](int c) { return x[c]; });
+  if (lane == 0) {
+    const double res = r[i] + (-1.0 * s);
+    out[i] = x[i] + __ldg(&wd[i]) * res;
+  }
+}
+
+// ---------------------------------------------------------------- multi RHS
+__global__ void __launch_bounds__(256) k_mvce_down(DCsr A, const double* __restrict__ wd,
+                                                   const double* __restrict__ r, int ldr,
+                                                   double* __restrict__ resid, int b) {
+  const int i = blockIdx.x * 8 + threadIdx.y;
+  const int q = blockIdx.y * 32 + threadIdx.x;
+  if (i >= A.n_rows || q >= b) return;
+  const double s = emul_row(A, i, [&](int c) { return __ldg(&wd[c]) * r[static_cast<long long>(c) * ldr + q]; });
+  resid[static_cast<long long>(i) * b + q] = r[static_cast<long long>(i) * ldr + q] + (-1.0 * s);
+}
+
+__global__ void __launch_bounds__(256) k_mvce_restrict(DCsr R, const double* __restrict__ resid,
+                                                       double* __restrict__ rc, int b) {
+  const int a = blockIdx.x * 8 + threadIdx.y;
+  const int q = blockIdx.y * 32 + threadIdx.x;
+  if (a >= R.n_rows || q >= b) return;
+  rc[static_cast<long long>(a) * b + q] = emul_row(R, a, [&](int c) { return resid[static_cast<long long>(c) * b + q]; });
+}
+
+__global__ void __launch_bounds__(256) k_mvce_up1(DCsr P, const double* __restrict__ wd,
+                                                  const double* __restrict__ r, int ldr,
+                                                  const double* __restrict__ ec, double* __restrict__ x, int b) {
+  const int i = blockIdx.x * 8 + threadIdx.y;
+  const int q = blockIdx.y * 32 + threadIdx.x;
+  if (i >= P.n_rows || q >= b) return;
+  const double s = emul_row(P, i, [&](int c) { return ec[static_cast<long long>(c) * b + q]; });
+  x[static_cast<long long>(i) * b + q] = __ldg(&wd[i]) * r[static_cast<long long>(i) * ldr + q] + 1.0 * s;
+}
+
+__global__ void __launch_bounds__(256) k_mvce_up2(DCsr A, const double* __restrict__ wd,
+                                                  const double* __restrict__ r, int ldr,
+                                                  const double* __restrict__ x, double* __restrict__ out,
+                                                  int ldo, int b) {
+  const int i = blockIdx.x * 8 + threadIdx.y;
+  const int q = blockIdx.y * 32 + threadIdx.x;
+  if (i >= A.n_rows || q >= b) return;
+  const double s = emul_row(A, i, [&](int c) { return x[static_cast<long long>(c) * b + q]; });
+  const double res = r[static_cast<long long>(i) * ldr + q] + (-1.0 * s);
+  out[static_cast<long long>(i) * ldo + q] = x[static_cast<long long>(i) * b + q] + __ldg(&wd[i]) * res;
+}
+
+// ------------------------------------------------------------------ launchers
+static unsigned wgrid(int rows) { return static_cast<unsigned>((rows + kRowsPerBlock - 1) / kRowsPerBlock); }
+
+void vcw_down(const DLevel& L, VSel r, double* resid, const MinresState* st, cudaStream_t s) {
+  k_vcw_down<<<wgrid(L.n), 256, 0, s>>>(L.A, L.wd, r, resid, st);
+  note_launch("vcw_down");
+}
+void vcw_restrict(const DLevel& L, const double* resid, double* rc, cudaStream_t s) {
+  k_vcw_restrict<<<wgrid(L.R.n_rows), 256, 0, s>>>(L.R, resid, rc);
+  note_launch("vcw_restrict");
+}
+void vcw_up1(const DLevel& L, VSel r, const double* ec, double* x, const MinresState* st, cudaStream_t s) {
+  k_vcw_up1<<<wgrid(L.n), 256, 0, s>>>(L.P, L.wd, r, ec, x, st);
+  note_launch("vcw_up1");
+}
+void vcw_up2(const DLevel& L, VSel r, const double* x, double* out, const MinresState* st, cudaStream_t s) {
+  k_vcw_up2<<<wgrid(L.n), 256, 0, s>>>(L.A, L.wd, r, x, out, st);
+  note_launch("vcw_up2");
+}
+void mvce_down(const DLevel& L, const double* r, int ldr, double* resid, int b, cudaStream_t s) {
+  dim3 grid((L.n + 7) / 8, (b + 31) / 32), block(32, 8);
+  k_mvce_down<<<grid, block, 0, s>>>(L.A, L.wd, r, ldr, resid, b);
+  note_launch("mvce_down");
+}
+void mvce_restrict(const DLevel& L, const double* resid, double* rc, int b, cudaStream_t s) {
+  dim3 grid((L.R.n_rows + 7) / 8, (b + 31) / 32), block(32, 8);
+  k_mvce_restrict<<<grid, block, 0, s>>>(L.R, resid, rc, b);
+  note_launch("mvce_restrict");
+}
+void mvce_up1(const DLevel& L, const double* r, int ldr, const double* ec, double* x, int b, cudaStream_t s) {
+  dim3 grid((L.n + 7) / 8, (b + 31) / 32), block(32, 8);
+  k_mvce_up1<<<grid, block, 0, s>>>(L.P, L.wd, r, ldr, ec, x, b);
+  note_launch("mvce_up1");
+}
+void mvce_up2(const DLevel& L, const double* r, int ldr, const double* x, double* out, int ldo, int b,
+              cudaStream_t s) {
+  dim3 grid((L.n + 7) / 8, (b + 31) / 32), block(32, 8);
+  k_mvce_up2<<<grid, block, 0, s>>>(L.A, L.wd, r, ldr, x, out, ldo, b);
+  note_launch("mvce_up2");
+}
+
+}  // namespace gnw
