@@ -258,8 +258,8 @@ void Context::upload_hierarchy() {
       d.A = upload_csr(mem_, L.A, s);
       d.P = upload_csr(mem_, L.P, s);
       d.R = upload_csr(mem_, host::transpose(L.P), s);
-      // warp-per-row kernels once rows carry more than ~12 entries (levels >= 1..2)
-      constexpr double kWide = 12.0;
+      // warp-per-row kernels once rows carry more than ~24 entries (C2: levels >= 2)
+      constexpr double kWide = 24.0;
       d.wideA = L.A.nnz() > kWide * static_cast<double>(L.A.n_rows);
       d.wideP = L.P.nnz() > kWide * static_cast<double>(L.P.n_rows);
       d.wideR = L.P.nnz() > kWide * static_cast<double>(L.P.n_cols);
@@ -506,7 +506,7 @@ void Context::set_jacobian(const double* J, int64_t m, int64_t n_cells, double b
     capacitance_dgemm(dJ_, dHt_, static_cast<int>(m), N_, beta, plan, dpart_, dC_, s);
     GNW_CUDA_CHECK(cudaEventRecord(ev[2], s));
     // L = chol(C), retry once after symmetrisation (inversion.cpp:21-35)
-    cholesky(dC_, dL_, static_cast<int>(m), dflag_, s);
+    cholesky_blocked(dC_, dY_, dL_, static_cast<int>(m), dflag_, s);
     int fail = 0;
     GNW_CUDA_CHECK(cudaMemcpyAsync(&fail, dflag_, sizeof(int), cudaMemcpyDeviceToHost, s));
     sync();
@@ -514,7 +514,7 @@ void Context::set_jacobian(const double* J, int64_t m, int64_t n_cells, double b
       DgemmPlan full = dgemm_plan(static_cast<int>(m), N_, 1, sm_count_);
       capacitance_dgemm(dJ_, dHt_, static_cast<int>(m), N_, beta, full, dpart_, dC_, s);
       symmetrize(dC_, static_cast<int>(m), s);
-      cholesky(dC_, dL_, static_cast<int>(m), dflag_, s);
+      cholesky_blocked(dC_, dY_, dL_, static_cast<int>(m), dflag_, s);
       GNW_CUDA_CHECK(cudaMemcpyAsync(&fail, dflag_, sizeof(int), cudaMemcpyDeviceToHost, s));
       sync();
       if (fail) throw std::runtime_error("dense_cholesky: matrix not positive definite");
@@ -958,8 +958,12 @@ void Context::dense_cholesky(int64_t n, const double* C, double* L) {
   DeviceMemory tm;
   double* dC = tm.alloc<double>(n * n);
   double* dL = tm.alloc<double>(n * n);
+  double* dW = tm.alloc<double>(n * n);
   h2d(dC, C, n * n, stream_);
-  gnw::cholesky(dC, dL, static_cast<int>(n), dflag_, stream_);
+  if (coarse_mode == 2)  // single-CTA left-looking variant, kept for cross-checking
+    gnw::cholesky(dC, dL, static_cast<int>(n), dflag_, stream_);
+  else
+    gnw::cholesky_blocked(dC, dW, dL, static_cast<int>(n), dflag_, stream_);
   int fail = 0;
   GNW_CUDA_CHECK(cudaMemcpyAsync(&fail, dflag_, sizeof(int), cudaMemcpyDeviceToHost, stream_));
   GNW_CUDA_CHECK(cudaMemcpyAsync(L, dL, n * n * sizeof(double), cudaMemcpyDeviceToHost, stream_));

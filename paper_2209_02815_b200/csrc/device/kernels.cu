@@ -228,18 +228,21 @@ __global__ void __launch_bounds__(256) k_mvc_up2(DCsr A, const double* __restric
 
 void mvc_down(const DLevel& L, const double* r, int ldr, double* resid, int b, cudaStream_t s) {
   if (L.wideA) return mvce_down(L, r, ldr, resid, b, s);
+  if (b % 2 == 0 && ldr % 2 == 0) return mvc2_down(L, r, ldr, resid, b, s);
   dim3 grid((L.n + 7) / 8, (b + 31) / 32), block(32, 8);
   k_mvc_down<<<grid, block, 0, s>>>(L.A, L.wd, r, ldr, resid, b);
   check_launch("mvc_down");
 }
 void mvc_restrict(const DLevel& L, const double* resid, double* rc, int b, cudaStream_t s) {
   if (L.wideR) return mvce_restrict(L, resid, rc, b, s);
+  if (b % 2 == 0) return mvc2_restrict(L, resid, rc, b, s);
   dim3 grid((L.R.n_rows + 7) / 8, (b + 31) / 32), block(32, 8);
   k_mvc_restrict<<<grid, block, 0, s>>>(L.R, resid, rc, b);
   check_launch("mvc_restrict");
 }
 void mvc_up1(const DLevel& L, const double* r, int ldr, const double* ec, double* x, int b, cudaStream_t s) {
   if (L.wideP) return mvce_up1(L, r, ldr, ec, x, b, s);
+  if (b % 2 == 0 && ldr % 2 == 0) return mvc2_up1(L, r, ldr, ec, x, b, s);
   dim3 grid((L.n + 7) / 8, (b + 31) / 32), block(32, 8);
   k_mvc_up1<<<grid, block, 0, s>>>(L.P, L.wd, r, ldr, ec, x, b);
   check_launch("mvc_up1");
@@ -247,6 +250,7 @@ void mvc_up1(const DLevel& L, const double* r, int ldr, const double* ec, double
 void mvc_up2(const DLevel& L, const double* r, int ldr, const double* x, double* out, int ldo, int b,
              cudaStream_t s) {
   if (L.wideA) return mvce_up2(L, r, ldr, x, out, ldo, b, s);
+  if (b % 2 == 0 && ldr % 2 == 0 && ldo % 2 == 0) return mvc2_up2(L, r, ldr, x, out, ldo, b, s);
   dim3 grid((L.n + 7) / 8, (b + 31) / 32), block(32, 8);
   k_mvc_up2<<<grid, block, 0, s>>>(L.A, L.wd, r, ldr, x, out, ldo, b);
   check_launch("mvc_up2");
@@ -1101,14 +1105,15 @@ __global__ void k_syrk_tn(const double* __restrict__ Y, double* __restrict__ Cin
   const int j = blockIdx.x * blockDim.x + threadIdx.x, i = blockIdx.y;
   if (j >= n || j > i) return;
   double s = 0.0;
-  for (int k = i; k < n; ++k) s = s + Y[static_cast<long long>(k) * n + i] * Y[static_cast<long long>(k) * n + j];
+#pragma unroll 8
+  for (int k = i; k < n; ++k)
+    s = s + __ldg(&Y[static_cast<long long>(k) * n + i]) * __ldg(&Y[static_cast<long long>(k) * n + j]);
   Cinv[static_cast<long long>(i) * n + j] = s;
   Cinv[static_cast<long long>(j) * n + i] = s;
 }
 
 void cholesky_inverse(const double* L, double* Y, double* Cinv, int n, cudaStream_t s) {
-  k_trinv<<<grid_for(n, 64), 64, 0, s>>>(L, Y, n);
-  check_launch("trinv");
+  trinv_blocked(L, Y, n, s);
   dim3 grid(grid_for(n, 128), n);
   k_syrk_tn<<<grid, 128, 0, s>>>(Y, Cinv, n);
   check_launch("syrk_tn");

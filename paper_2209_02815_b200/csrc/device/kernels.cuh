@@ -30,6 +30,13 @@ void mvce_up1(const DLevel& L, const double* r, int ldr, const double* ec, doubl
 void mvce_up2(const DLevel& L, const double* r, int ldr, const double* x, double* out, int ldo, int b,
               cudaStream_t s);
 
+// narrow-level batched kernels, 2 columns per thread (vcycle_batch.cu); even b only
+void mvc2_down(const DLevel& L, const double* r, int ldr, double* resid, int b, cudaStream_t s);
+void mvc2_restrict(const DLevel& L, const double* resid, double* rc, int b, cudaStream_t s);
+void mvc2_up1(const DLevel& L, const double* r, int ldr, const double* ec, double* x, int b, cudaStream_t s);
+void mvc2_up2(const DLevel& L, const double* r, int ldr, const double* x, double* out, int ldo, int b,
+              cudaStream_t s);
+
 // ------------------------------------------------------------------ V-cycle
 // Single right-hand side (amg.cpp:90-111); `r` may be a ring slot (level 0).
 void vc_down(const DLevel& L, VSel r, double* resid, const MinresState* st, cudaStream_t s);
@@ -142,6 +149,11 @@ void capacitance_dgemm(const double* J, const double* Ht, int m, long long N, do
 // dense_cholesky (linalg.cpp:88-105), operation order preserved; *fail = 1 on a
 // non-positive pivot.
 void cholesky(const double* C, double* L, int n, int* fail, cudaStream_t s);
+// the same factorisation, blocked right-looking with per-element sequential
+// updates (dense.cu): bit-identical to the reference, O(m) critical path.  W: m x m work
+void cholesky_blocked(const double* C, double* W, double* L, int n, int* fail, cudaStream_t s);
+// Y = L^-1 by 32-row blocks (dense.cu)
+void trinv_blocked(const double* L, double* Y, int n, cudaStream_t s);
 // symmetrize C in place (cholesky_with_retry, inversion.cpp:24-33)
 void symmetrize(double* C, int n, cudaStream_t s);
 // Cinv = L^-T L^-1

@@ -42,15 +42,20 @@ __device__ __forceinline__ double warp_row(const DCsr& A, int i, int lane, F f) 
   return v[0];
 }
 
+// One pass over the row in groups of 32 consecutive entries; entry k feeds the
+// partial of lane class (k - k0) % 32 -- the same per-class order as warp_row.
 template <class F>
 __device__ __forceinline__ double emul_row(const DCsr& A, int i, F f) {
   double p[32];
-  const int k0 = A.rowptr[i], k1 = A.rowptr[i + 1];
 #pragma unroll
-  for (int l = 0; l < 32; ++l) {
-    double acc = 0.0;
-    for (int k = k0 + l; k < k1; k += 32) acc = acc + __ldg(&A.vals[k]) * f(A.cols[k]);
-    p[l] = acc;
+  for (int l = 0; l < 32; ++l) p[l] = 0.0;
+  const int k0 = A.rowptr[i], k1 = A.rowptr[i + 1];
+  for (int g = k0; g < k1; g += 32) {
+#pragma unroll
+    for (int l = 0; l < 32; ++l) {
+      const int k = g + l;
+      if (k < k1) p[l] = p[l] + __ldg(&A.vals[k]) * f(A.cols[k]);
+    }
   }
   return tree32(p);
 }

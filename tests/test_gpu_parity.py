@@ -85,7 +85,7 @@ def test_device_cholesky_bitwise(oracle, gpu_ctx_factory):
     mesh = W.unit_square_mesh(4)
     ctx = gpu_ctx_factory(mesh)
     rng = np.random.default_rng(3)
-    for n in (1, 2, 7, 64, 200):
+    for n in (1, 2, 7, 31, 32, 33, 64, 200, 300, 513):
         G = rng.standard_normal((n, n))
         Cm = G @ G.T + n * np.eye(n)
         assert np.array_equal(ctx.dense_cholesky(Cm), oracle.dense_cholesky(Cm))
