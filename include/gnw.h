@@ -128,6 +128,14 @@ void gnw_destroy(gnw_ctx* ctx);
 gnw_status gnw_set_pointer_mode(gnw_ctx* ctx, int mode);
 gnw_status gnw_set_coarse_mode(gnw_ctx* ctx, int mode);
 gnw_status gnw_set_preconditioner(gnw_ctx* ctx, int kind);
+/* MINRES loop schedule.  GNW_LOOP_REFERENCE (default) evaluates A zhat exactly as
+ * SaddleOperator::apply does (J zhat2, then J^T u: two sweeps over J).
+ * GNW_LOOP_FUSED uses the Woodbury identity J P22^-1 v2 = C^-1 H^T v2 = t': the
+ * preconditioner's sweep over H also forms q = J^T t', and the next operator
+ * takes J^T u = q / gamma, so J is swept once per iteration instead of twice.
+ * Same operator in exact arithmetic; rounding differs. */
+enum { GNW_LOOP_REFERENCE = 0, GNW_LOOP_FUSED = 1 };
+gnw_status gnw_set_loop_mode(gnw_ctx* ctx, int mode);
 
 gnw_status gnw_assemble(gnw_ctx* ctx, const gnw_mesh* mesh, const gnw_amg_options* opts);
 /* AMG hierarchy alone over an SPD CSR matrix (amg_setup(s_hat, opts)); after

@@ -67,7 +67,7 @@ class Stats(C.Structure):
 # every symbol include/gnw.h declares (checked by tests/test_capi_symbols.py)
 EXPORTED = [
     "gnw_last_error", "gnw_version", "gnw_create", "gnw_destroy", "gnw_set_pointer_mode",
-    "gnw_set_coarse_mode", "gnw_set_preconditioner", "gnw_assemble", "gnw_assemble_amg_csr", "gnw_get_info",
+    "gnw_set_coarse_mode", "gnw_set_preconditioner", "gnw_set_loop_mode", "gnw_assemble", "gnw_assemble_amg_csr", "gnw_get_info",
     "gnw_set_jacobian", "gnw_apply_operator", "gnw_precondition", "gnw_amg_apply",
     "gnw_get_woodbury", "gnw_assemble_rhs", "gnw_minres_solve", "gnw_export_csr",
     "gnw_export_mesh", "gnw_dense_cholesky", "gnw_get_stats", "gnw_event_record",
@@ -97,6 +97,7 @@ def load() -> C.CDLL:
     L.gnw_set_pointer_mode.argtypes = [vp, i32]
     L.gnw_set_coarse_mode.argtypes = [vp, i32]
     L.gnw_set_preconditioner.argtypes = [vp, i32]
+    L.gnw_set_loop_mode.argtypes = [vp, i32]
     L.gnw_assemble.argtypes = [vp, C.POINTER(_Mesh), C.POINTER(AmgOptions)]
     L.gnw_assemble_amg_csr.argtypes = [vp, u64, vp, vp, vp, C.POINTER(AmgOptions)]
     L.gnw_get_info.argtypes = [vp, C.POINTER(Info)]

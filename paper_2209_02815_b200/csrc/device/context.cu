@@ -10,6 +10,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 
 namespace gnw {
@@ -65,6 +66,7 @@ Context::Context(int device) : device_(device) {
   GNW_CUDA_CHECK(cudaGetDeviceProperties(&prop, device_));
   if (prop.major < 10) throw DeviceError("gnw: this build targets sm_100a (B200); found sm_" + std::to_string(prop.major) + std::to_string(prop.minor));
   sm_count_ = prop.multiProcessorCount;
+  if (const char* e = std::getenv("GNW_PAD")) pad_ = std::max(0LL, std::atoll(e) / 2 * 2);
   // A blocking stream: ordered with the legacy default stream, so device-pointer
   // callers (e.g. torch on its default stream) need no extra synchronisation.
   GNW_CUDA_CHECK(cudaStreamCreateWithFlags(&stream_, cudaStreamDefault));
@@ -136,6 +138,7 @@ void Context::assemble(const double* vertices, int64_t nv, const int64_t* cells,
     bmem_b_ = 0;
     jm_m_ = -1;
     dJ_ = nullptr;
+    dq_ = nullptr;
     pa_.m = 0;
     mem_.release_all();
     st_ = mem_.alloc<MinresState>(1);
@@ -179,6 +182,7 @@ void Context::assemble_amg_csr(int64_t n, const int64_t* rowptr, const int64_t* 
     bmem_b_ = 0;
     jm_m_ = -1;
     dJ_ = nullptr;
+    dq_ = nullptr;
     pa_.m = 0;
     mem_.release_all();
     st_ = mem_.alloc<MinresState>(1);
@@ -236,8 +240,8 @@ void Context::upload_structure() {
   fpart_ = mem_.alloc<double>(nb * 3);
   upart_ = mem_.alloc<double>(nb * 3);
   rpart_ = mem_.alloc<double>(nb * 3);
-  plan_ = row_gemv_plan(N_);
-  n_comb_blocks_ = static_cast<int>((K_ + 255) / 256 + (N_ + plan_.chunk - 1) / plan_.chunk);
+  plan_ = row_gemv_plan(N_, 1);  // re-planned for the row count by set_jacobian
+  n_comb_blocks_ = combine_blocks(K_, N_);
   cpart_ = mem_.alloc<double>(3 * (static_cast<size_t>(n_comb_blocks_) + 16));  // one triple per combine block
 }
 
@@ -278,6 +282,14 @@ void Context::upload_hierarchy() {
     lv_.push_back(d);
   }
   nc_ = static_cast<int>(amg_.nc);
+  {  // fused tail: the trailing levels with <= 600k nonzeros each (C1: the whole cycle; C2: levels 2..9)
+    constexpr int64_t kTailNnz = 600000;
+    const int L = static_cast<int>(amg_.levels.size());
+    int l0 = L - 1;
+    while (l0 > 0 && amg_.levels[l0 - 1].A.nnz() <= kTailNnz && (L - 1 - (l0 - 1)) <= kMaxTail) --l0;
+    tail_l0_ = l0;
+    if (const char* e = std::getenv("GNW_TAIL_CLUSTER")) tail_cluster_ = std::atoi(e);
+  }
   const std::vector<double> inv = host::cholesky_inverse(amg_.nc, amg_.coarse_chol);
   coarse_inv_ = mem_.alloc<double>(inv.size());
   coarse_L_ = mem_.alloc<double>(amg_.coarse_chol.size());
@@ -302,14 +314,44 @@ void Context::vcycle(VSel r0, double* out0, const MinresState* st) {
     coarse(r0, out0);
     return;
   }
-  for (int l = 0; l < L - 1; ++l) {
+  // levels [tail_l0_, L) run fused in one cluster launch (vcycle_tail.cu)
+  const int l0 = (tail_cluster_ > 0) ? tail_l0_ : L;
+  for (int l = 0; l < std::min(l0, L - 1); ++l) {
     const VSel rl = l == 0 ? r0 : vfixed(vr_[l]);
     const DLevel lev = level(l);
     vc_down(lev, rl, vres_[l], st, s);
     vc_restrict(lev, vres_[l], vr_[l + 1], s);
   }
-  coarse(vfixed(vr_[L - 1]), ve_[L - 1]);
-  for (int l = L - 2; l >= 0; --l) {
+  if (l0 < L) {
+    TailArgs a;
+    a.nlev = L - 1 - l0;
+    for (int k = 0; k < a.nlev; ++k) {
+      const DLevel d = level(l0 + k);
+      TailLevel& t = a.lv[k];
+      t.A = d.A;
+      t.P = d.P;
+      t.R = d.R;
+      t.wd = d.wd;
+      t.n = d.n;
+      t.wideA = d.wideA;
+      t.wideP = d.wideP;
+      t.wideR = d.wideR;
+      a.res[k] = vres_[l0 + k];
+      a.x[k] = vx_[l0 + k];
+    }
+    for (int k = 0; k <= a.nlev; ++k) {
+      a.r[k] = vr_[l0 + k];
+      a.e[k] = ve_[l0 + k];
+    }
+    a.Ainv = coarse_inv_;
+    a.Lc = coarse_L_;
+    a.nc = nc_;
+    a.exact = coarse_mode == 1;
+    vcycle_tail(a, l0 == 0 ? r0 : vfixed(vr_[l0]), l0 == 0 ? out0 : ve_[l0], st, tail_cluster_, s);
+  } else {
+    coarse(vfixed(vr_[L - 1]), ve_[L - 1]);
+  }
+  for (int l = std::min(l0, L - 1) - 1; l >= 0; --l) {
     const VSel rl = l == 0 ? r0 : vfixed(vr_[l]);
     const DLevel lev = level(l);
     vc_up1(lev, rl, ve_[l + 1], vx_[l], st, s);
@@ -435,9 +477,11 @@ void Context::set_jacobian(const double* J, int64_t m, int64_t n_cells, double b
     jmem_ = std::make_unique<DeviceMemory>();
     DeviceMemory& jm = *jmem_;
     u_ = jm.alloc<double>(m);
+    plan_ = row_gemv_plan(N_, static_cast<int>(m));
     gpart_ = jm.alloc<double>(static_cast<size_t>(plan_.nchunks) * m);
-    jown_ = want_owned ? jm.alloc<double>(mN) : nullptr;
-    dHt_ = jm.alloc<double>(mN);
+    ldh_ = N_ + pad_;
+    jown_ = want_owned ? jm.alloc<double>(static_cast<size_t>(m) * ldh_) : nullptr;
+    dHt_ = jm.alloc<double>(static_cast<size_t>(m) * ldh_);
     dC_ = jm.alloc<double>(m * m);
     dL_ = jm.alloc<double>(m * m);
     dCinv_ = jm.alloc<double>(m * m);
@@ -445,6 +489,7 @@ void Context::set_jacobian(const double* J, int64_t m, int64_t n_cells, double b
     t_ = jm.alloc<double>(m);
     t2_ = jm.alloc<double>(m);
     tpart_ = jm.alloc<double>(static_cast<size_t>(plan_.nchunks) * m);
+    dq_ = jm.alloc<double>(N_);
     const DgemmPlan lo = dgemm_plan(static_cast<int>(m), N_, 0, sm_count_);
     const DgemmPlan fu = dgemm_plan(static_cast<int>(m), N_, 1, sm_count_);
     const size_t pl = static_cast<size_t>(lo.splits) * lo.npairs * lo.tile * lo.tile;
@@ -461,13 +506,20 @@ void Context::set_jacobian(const double* J, int64_t m, int64_t n_cells, double b
     // (inversion.hpp:21, :35); the caller keeps it alive while the context uses it.
     if (dJ_ != J) destroy_graph();  // the loop graph bakes the J pointer
     dJ_ = const_cast<double*>(J);
+    ldj_ = N_;
     j_borrowed_ = true;
   } else {
+    if (dJ_ != jown_) destroy_graph();
     dJ_ = jown_;
+    ldj_ = ldh_;  // owned copy: padded rows like Ht
     j_borrowed_ = false;
-    GNW_CUDA_CHECK(cudaMemcpyAsync(dJ_, J, mN * sizeof(double), cudaMemcpyHostToDevice, s));
+    GNW_CUDA_CHECK(cudaMemcpy2DAsync(dJ_, ldj_ * sizeof(double), J, N_ * sizeof(double), N_ * sizeof(double), m,
+                                     cudaMemcpyHostToDevice, s));
   }
   op_.J = dJ_;
+  op_.ldj = ldj_;
+  pa_.ldj = ldj_;
+  pa_.ldh = ldh_;
   op_.m = static_cast<int>(m);
   if (pc_laplace) {  // Alg. 4: J stays in the operator, plain Laplace preconditioner
     if (pa_.m != 0) destroy_graph();
@@ -494,16 +546,16 @@ void Context::set_jacobian(const double* J, int64_t m, int64_t n_cells, double b
     }
     for (int64_t i0 = 0; i0 < m; i0 += b) {
       const int bb = static_cast<int>(std::min<int64_t>(b, m - i0));
-      transpose_rows_to_batch(dJ_, N_, static_cast<int>(i0), bb, bR0_, s);
+      transpose_rows_to_batch(dJ_, N_, ldj_, static_cast<int>(i0), bb, bR0_, s);
       vcycle_batch(bR0_, bb, bX0_);
-      transpose_batch_to_rows(bX0_, N_, static_cast<int>(i0), bb, dHt_, s);
+      transpose_batch_to_rows(bX0_, N_, ldh_, static_cast<int>(i0), bb, dHt_, s);
     }
     GNW_CUDA_CHECK(cudaEventRecord(ev[1], s));
   }
   // C = I + (J H)/beta (inversion.cpp:37-43), lower triangle
   DgemmPlan plan = dgemm_plan(static_cast<int>(m), N_, 0, sm_count_);
   {
-    capacitance_dgemm(dJ_, dHt_, static_cast<int>(m), N_, beta, plan, dpart_, dC_, s);
+    capacitance_dgemm(dJ_, ldj_, dHt_, ldh_, static_cast<int>(m), N_, beta, plan, dpart_, dC_, s);
     GNW_CUDA_CHECK(cudaEventRecord(ev[2], s));
     // L = chol(C), retry once after symmetrisation (inversion.cpp:21-35)
     cholesky_blocked(dC_, dY_, dL_, static_cast<int>(m), dflag_, s);
@@ -512,7 +564,7 @@ void Context::set_jacobian(const double* J, int64_t m, int64_t n_cells, double b
     sync();
     if (fail) {
       DgemmPlan full = dgemm_plan(static_cast<int>(m), N_, 1, sm_count_);
-      capacitance_dgemm(dJ_, dHt_, static_cast<int>(m), N_, beta, full, dpart_, dC_, s);
+      capacitance_dgemm(dJ_, ldj_, dHt_, ldh_, static_cast<int>(m), N_, beta, full, dpart_, dC_, s);
       symmetrize(dC_, static_cast<int>(m), s);
       cholesky_blocked(dC_, dY_, dL_, static_cast<int>(m), dflag_, s);
       GNW_CUDA_CHECK(cudaMemcpyAsync(&fail, dflag_, sizeof(int), cudaMemcpyDeviceToHost, s));
@@ -538,13 +590,19 @@ void Context::set_jacobian(const double* J, int64_t m, int64_t n_cells, double b
 }
 
 // --------------------------------------------------------------- operator
-void Context::operator_into(VSel x, int scaled, VSel y, MinresState* st, int loop) {
-  if (m_ > 0) {
+// fused: the MINRES loop's A zhat takes J^T u from q = J^T t' (fused_active()).
+void Context::operator_into(VSel x, int scaled, VSel y, MinresState* st, int loop, bool fused) {
+  OperatorArgs op = op_;
+  if (fused) {
+    op.q = dq_;
+  } else if (m_ > 0) {
     VSel xs = x;  // J acts on the cell part
-    row_gemv(dJ_, static_cast<int>(m_), N_, xs, K_, scaled, st, gpart_, counters_ + 0, u_, plan_, stream_);
+    row_gemv(dJ_, static_cast<int>(m_), N_, ldj_, xs, K_, scaled, st, gpart_, counters_ + 0, u_, plan_, stream_);
   }
-  saddle_operator(op_, x, scaled, u_, y, st, loop, opart_, counters_ + 1, stream_);
+  saddle_operator(op, x, scaled, u_, y, st, loop, opart_, counters_ + 1, stream_);
 }
+
+bool Context::fused_active() const { return fused_ && m_ > 0 && pa_.m > 0 && dq_ != nullptr; }
 
 void Context::apply_operator(const double* x, double* y) {
   require_mixed();
@@ -557,13 +615,19 @@ void Context::apply_operator(const double* x, double* y) {
 }
 
 // z = P^-1 y.  In the loop, y = v_next is formed on the fly from Az, v_cur, v_prev.
-void Context::precondition_into(VSel y, VSel yv2, VSel z, MinresState* st, int loop, VSel vcur, VSel vprev) {
+void Context::precondition_into(VSel y, VSel yv2, VSel z, MinresState* st, int loop, VSel vcur, VSel vprev,
+                                bool fused) {
   pa_.exact = coarse_mode;
-  combine_precondition(pa_, loop ? vfixed(az_) : y, vcur, vprev, y, z, loop, st, nullptr, cpart_, tpart_,
+  PrecArgs pa = pa_;
+  if (fused) {  // the finish sweep also forms q = J^T t' for the next operator
+    pa.J = dJ_;
+    pa.q = dq_;
+  }
+  combine_precondition(pa, loop ? vfixed(az_) : y, vcur, vprev, y, z, loop, st, nullptr, cpart_, tpart_,
                        counters_ + 2, t_, plan_, stream_);
   vcycle(yv2, svc_, st);
-  capacitance_solve(pa_, t_, t2_, stream_);
-  finish_precondition(pa_, svc_, t2_, y, z, loop, st, cpart_, n_comb_blocks_, fpart_, counters_ + 3, stream_);
+  capacitance_solve(pa, t_, t2_, stream_);
+  finish_precondition(pa, svc_, t2_, y, z, loop, st, cpart_, n_comb_blocks_, fpart_, counters_ + 3, stream_);
 }
 
 void Context::precondition(const double* y, double* z) {
@@ -639,9 +703,10 @@ void Context::build_graph() {
   // iteration j: v_prev = V[j%3], v_cur = V[(j+1)%3], v_next = V[(j+2)%3] (same for w, u);
   //              z_cur = Z[j%2], z_next = Z[(j+1)%2]
   try {
-    operator_into(ring2(Z_, 0), 1, vfixed(az_), st_, 1);                      // Az = A zhat, delta
+    const bool fu = fused_active();
+    operator_into(ring2(Z_, 0), 1, vfixed(az_), st_, 1, fu);                  // Az = A zhat, delta
     precondition_into(ring3(V_, 2), ring3(Vk_, 2), ring2(Z_, 1), st_, 1,       // v_next, z_next = P^-1 v_next,
-                      ring3(V_, 1), ring3(V_, 0));                             // gamma_next, Givens
+                      ring3(V_, 1), ring3(V_, 0), fu);                         // gamma_next, Givens
     minres_update(K_ + N_, ring2(Z_, 0), vfixed(az_), ring3(W_, 0), ring3(W_, 1), ring3(W_, 2), ring3(U_, 0),
                   ring3(U_, 1), ring3(U_, 2), x_, r_, st_, hist_e_, hist_p_, hist_cap_, upart_, counters_ + 4,
                   static_cast<unsigned long long>(h), 1, stream_);
@@ -715,7 +780,8 @@ MinresResult Context::minres(const double* b, const double* x0, double* x, doubl
     return res;
   }
   // z = P^-1 r, gamma_1 (minres.cpp:44-47)
-  precondition_into(vfixed(r_), vfixed(r_ + K_), vfixed(Z_[1]), st_plain_, 0, vfixed(r_), vfixed(r_));
+  precondition_into(vfixed(r_), vfixed(r_ + K_), vfixed(Z_[1]), st_plain_, 0, vfixed(r_), vfixed(r_),
+                    fused_active());
   ps = read_plain();
   const double gamma_sq0 = ps.scratch[0];
   if (gamma_sq0 < 0.0) throw std::runtime_error("minres: preconditioner is not positive definite");
@@ -837,7 +903,8 @@ void Context::get_woodbury(double* H, double* L) {
   if (m_ == 0 || pa_.m == 0) return;
   if (H) {
     std::vector<double> ht(static_cast<size_t>(m_) * N_);
-    GNW_CUDA_CHECK(cudaMemcpy(ht.data(), dHt_, ht.size() * sizeof(double), cudaMemcpyDeviceToHost));
+    GNW_CUDA_CHECK(cudaMemcpy2D(ht.data(), N_ * sizeof(double), dHt_, ldh_ * sizeof(double), N_ * sizeof(double), m_,
+                                cudaMemcpyDeviceToHost));
     for (int64_t i = 0; i < m_; ++i)
       for (int64_t c = 0; c < N_; ++c) H[c * m_ + i] = ht[i * N_ + c];
   }
@@ -918,7 +985,7 @@ void Context::profile_kernel(int kernel, int reps, double* seconds, double* algo
   }
   auto launch = [&]() {
     switch (kernel) {
-      case 0: row_gemv(dJ_, static_cast<int>(m_), N_, vfixed(io_a_), K_, 0, st_plain_, gpart_, counters_ + 0, u_, plan_, s); break;
+      case 0: row_gemv(dJ_, static_cast<int>(m_), N_, ldj_, vfixed(io_a_), K_, 0, st_plain_, gpart_, counters_ + 0, u_, plan_, s); break;
       case 1: saddle_operator(op_, vfixed(io_a_), 0, u_ ? u_ : io_d_, vfixed(io_b_), st_plain_, 0, opart_, counters_ + 1, s); break;
       case 2:
         combine_precondition(pa_, vfixed(io_a_), vfixed(io_a_), vfixed(io_a_), vfixed(io_a_), vfixed(io_b_), 0,
@@ -934,7 +1001,7 @@ void Context::profile_kernel(int kernel, int reps, double* seconds, double* algo
                       vfixed(io_a_), vfixed(io_c_), io_d_, tmp_, st_plain_, nullptr, nullptr, 0, upart_, counters_ + 4,
                       0, 2, s);
         break;
-      case 6: capacitance_dgemm(dJ_, dHt_ ? dHt_ : dJ_, static_cast<int>(m_), N_, beta_, plan, part, dC_ ? dC_ : io_d_, s); break;
+      case 6: capacitance_dgemm(dJ_, ldj_, dHt_ ? dHt_ : dJ_, dHt_ ? ldh_ : ldj_, static_cast<int>(m_), N_, beta_, plan, part, dC_ ? dC_ : io_d_, s); break;
     }
   };
   launch();  // warm-up

@@ -53,6 +53,12 @@ class Context {
   int ptr_mode = 0;
   int coarse_mode = 0;
   int pc_laplace = 0;  // GnAlgorithm::kLaplaceMinres (inversion.cpp:251-256)
+  // Woodbury-fused MINRES loop: J^T u from the preconditioner sweep
+  void set_fused(int on) {
+    if ((on != 0) != (fused_ != 0)) destroy_graph();
+    fused_ = on != 0;
+  }
+  int fused() const { return fused_; }
   void set_coarse(int mode) {
     if (mode != coarse_mode) destroy_graph();  // the loop graph bakes the kernel choice
     coarse_mode = mode;
@@ -100,8 +106,10 @@ class Context {
   void vcycle_batch(const double* r0, int b, double* out0);
   DLevel level(int l) const;
   void ensure_batch(int b);
-  void operator_into(VSel x, int scaled, VSel y, MinresState* st, int loop);
-  void precondition_into(VSel y, VSel yv2, VSel z, MinresState* st, int loop, VSel vcur, VSel vprev);
+  void operator_into(VSel x, int scaled, VSel y, MinresState* st, int loop, bool fused = false);
+  void precondition_into(VSel y, VSel yv2, VSel z, MinresState* st, int loop, VSel vcur, VSel vprev,
+                         bool fused = false);
+  bool fused_active() const;
   void build_graph();
   void destroy_graph();
   double* stage_in(const double* p, size_t n, double* dev);
@@ -129,6 +137,8 @@ class Context {
   int nc_ = 0;
   std::vector<double*> vr_, ve_, vres_, vx_;  // single-RHS V-cycle work per level
   double* svc_ = nullptr;                     // V-cycle output (s)
+  int tail_l0_ = 0;        // first level of the fused V-cycle tail
+  int tail_cluster_ = 0;   // CTAs in the tail cluster (0: off; env GNW_TAIL_CLUSTER)
   std::unique_ptr<DeviceMemory> bmem_;        // batched V-cycle work (persists across set_jacobian)
   int bmem_b_ = 0;
   std::vector<double*> mr_, me_, mres_, mx_;
@@ -170,6 +180,10 @@ class Context {
   double* jown_ = nullptr;     // owned copy of J (host-pointer mode)
   double* dpart_ = nullptr;    // DGEMM split-K partials
   double* dnib_ = nullptr;     // device scalar -1/beta
+  double* dq_ = nullptr;       // q = J^T t' (fused loop), N
+  long long ldh_ = 0, ldj_ = 0;  // row strides of Ht / J on device
+  long long pad_ = 64;           // row padding (doubles) of owned m x N matrices (env GNW_PAD)
+  int fused_ = 0;
   bool j_borrowed_ = false;  // device-pointer J referenced, not copied (SaddleOperator holds a pointer)
   cudaGraph_t graph_ = nullptr;
   cudaGraphExec_t graph_exec_ = nullptr;

@@ -107,6 +107,13 @@ gnw_status gnw_set_preconditioner(gnw_ctx* ctx, int kind) {
   });
 }
 
+gnw_status gnw_set_loop_mode(gnw_ctx* ctx, int mode) {
+  return guard([&] {
+    if (mode != GNW_LOOP_REFERENCE && mode != GNW_LOOP_FUSED) throw std::invalid_argument("gnw_set_loop_mode: bad mode");
+    ctx_of(ctx).set_fused(mode);
+  });
+}
+
 gnw_status gnw_assemble(gnw_ctx* ctx, const gnw_mesh* mesh, const gnw_amg_options* opts) {
   return guard([&] {
     if (!mesh || !mesh->vertices || !mesh->cells) throw std::invalid_argument("gnw_assemble: null mesh");

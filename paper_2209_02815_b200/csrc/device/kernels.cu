@@ -26,6 +26,8 @@ namespace gnw {
 namespace {
 
 constexpr int kTpb = 256;
+constexpr int kRowsPerWarp = 4;                           // row GEMV: rows per warp
+constexpr int kRowsPerCta = kRowsPerWarp * (kTpb / 32);  // row GEMV: rows per CTA
 
 inline unsigned grid_for(long long n, int tpb = kTpb) {
   return static_cast<unsigned>((n + tpb - 1) / tpb);
@@ -262,7 +264,7 @@ void mcoarse_inverse(const double* Ainv, int n, const double* r, double* x, int 
 }
 
 // rows [r0, r0+b) of A (row-major, `cols` columns) -> X[c * b + q]
-__global__ void k_transpose_rows_to_batch(const double* __restrict__ A, long long cols, int r0, int b,
+__global__ void k_transpose_rows_to_batch(const double* __restrict__ A, long long cols, long long ld, int r0, int b,
                                           double* __restrict__ X) {
   __shared__ double tile[32][33];
   const long long c0 = static_cast<long long>(blockIdx.x) * 32;
@@ -270,7 +272,7 @@ __global__ void k_transpose_rows_to_batch(const double* __restrict__ A, long lon
   for (int y = threadIdx.y; y < 32; y += 8) {
     const int q = q0 + y;
     const long long c = c0 + threadIdx.x;
-    tile[y][threadIdx.x] = (q < b && c < cols) ? A[static_cast<long long>(r0 + q) * cols + c] : 0.0;
+    tile[y][threadIdx.x] = (q < b && c < cols) ? A[static_cast<long long>(r0 + q) * ld + c] : 0.0;
   }
   __syncthreads();
   for (int y = threadIdx.y; y < 32; y += 8) {
@@ -280,7 +282,7 @@ __global__ void k_transpose_rows_to_batch(const double* __restrict__ A, long lon
   }
 }
 
-__global__ void k_transpose_batch_to_rows(const double* __restrict__ X, long long cols, int r0, int b,
+__global__ void k_transpose_batch_to_rows(const double* __restrict__ X, long long cols, long long ld, int r0, int b,
                                           double* __restrict__ A) {
   __shared__ double tile[32][33];
   const long long c0 = static_cast<long long>(blockIdx.x) * 32;
@@ -294,18 +296,20 @@ __global__ void k_transpose_batch_to_rows(const double* __restrict__ X, long lon
   for (int y = threadIdx.y; y < 32; y += 8) {
     const int q = q0 + y;
     const long long c = c0 + threadIdx.x;
-    if (q < b && c < cols) A[static_cast<long long>(r0 + q) * cols + c] = tile[threadIdx.x][y];
+    if (q < b && c < cols) A[static_cast<long long>(r0 + q) * ld + c] = tile[threadIdx.x][y];
   }
 }
 
-void transpose_rows_to_batch(const double* A, long long cols, int r0, int b, double* X, cudaStream_t s) {
+void transpose_rows_to_batch(const double* A, long long cols, long long ld, int r0, int b, double* X,
+                             cudaStream_t s) {
   dim3 grid(static_cast<unsigned>((cols + 31) / 32), (b + 31) / 32), block(32, 8);
-  k_transpose_rows_to_batch<<<grid, block, 0, s>>>(A, cols, r0, b, X);
+  k_transpose_rows_to_batch<<<grid, block, 0, s>>>(A, cols, ld, r0, b, X);
   check_launch("transpose_rows_to_batch");
 }
-void transpose_batch_to_rows(const double* X, long long cols, int r0, int b, double* A, cudaStream_t s) {
+void transpose_batch_to_rows(const double* X, long long cols, long long ld, int r0, int b, double* A,
+                             cudaStream_t s) {
   dim3 grid(static_cast<unsigned>((cols + 31) / 32), (b + 31) / 32), block(32, 8);
-  k_transpose_batch_to_rows<<<grid, block, 0, s>>>(X, cols, r0, b, A);
+  k_transpose_batch_to_rows<<<grid, block, 0, s>>>(X, cols, ld, r0, b, A);
   check_launch("transpose_batch_to_rows");
 }
 
@@ -314,10 +318,13 @@ void transpose_batch_to_rows(const double* X, long long cols, int r0, int b, dou
 // ======================================================================
 // Column chunks sized so the grid is a multiple of the SM count (148 on B200):
 // every SM streams the same number of bytes (no partial last wave).
-RowGemv row_gemv_plan(long long N) {
+// 2-D grid: (column chunk) x (group of 32 rows).  Short-lived CTAs (one 32-row x
+// chunk tile each, ~14 waves at C2) keep every SM streaming to the end.
+RowGemv row_gemv_plan(long long N, int m) {
   RowGemv p;
-  const long long ctas = 148LL * 4;
-  long long chunk = (N + ctas - 1) / ctas;
+  p.ngroups = std::max(1, (m + kRowsPerCta - 1) / kRowsPerCta);
+  const long long ctas = 148LL * 8;
+  long long chunk = (N * p.ngroups + ctas - 1) / ctas;
   chunk = std::max<long long>(64, (chunk + 63) / 64 * 64);
   chunk = std::min<long long>(chunk, 4096);
   p.chunk = static_cast<int>(chunk);
@@ -364,9 +371,8 @@ __device__ __forceinline__ void warp_rows_dot(const double* __restrict__ a, long
   for (int r = 0; r < R; ++r) out[r] = acc[r];
 }
 
-constexpr int kRowsPerWarp = 4;
 
-__global__ void __launch_bounds__(kTpb) k_row_gemv(const double* __restrict__ A, int m, long long N, VSel xs,
+__global__ void __launch_bounds__(kTpb) k_row_gemv(const double* __restrict__ A, int m, long long N, long long ld, VSel xs,
                                                    long long xoff, int scaled, const MinresState* st,
                                                    double* __restrict__ partial, unsigned* counter,
                                                    double* __restrict__ out, int chunk) {
@@ -377,23 +383,26 @@ __global__ void __launch_bounds__(kTpb) k_row_gemv(const double* __restrict__ A,
   const int len = static_cast<int>(min(static_cast<long long>(chunk), N - c0));
   for (int t = threadIdx.x; t < len; t += blockDim.x) xsm[t] = scaled ? x[c0 + t] * sc : x[c0 + t];
   __syncthreads();
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  const bool vec_ok = ((N & 1) == 0);
-  for (int row = warp * kRowsPerWarp; row < m; row += nw * kRowsPerWarp) {
-    double d[kRowsPerWarp];
-    const int nr = min(kRowsPerWarp, m - row);
-    warp_rows_dot<kRowsPerWarp>(A + static_cast<long long>(row) * N + c0, N, nr, xsm, len, vec_ok, lane, d);
-    if (lane == 0)
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const bool vec_ok = ((ld & 1) == 0);
+  {
+    const int row = blockIdx.y * kRowsPerCta + warp * kRowsPerWarp;  // 8 warps x 4 rows
+    if (row < m) {
+      double d[kRowsPerWarp];
+      const int nr = min(kRowsPerWarp, m - row);
+      warp_rows_dot<kRowsPerWarp>(A + static_cast<long long>(row) * ld + c0, ld, nr, xsm, len, vec_ok, lane, d);
+      if (lane == 0)
 #pragma unroll
-      for (int r = 0; r < kRowsPerWarp; ++r)
-        if (r < nr) partial[static_cast<long long>(blockIdx.x) * m + row + r] = d[r];
+        for (int r = 0; r < kRowsPerWarp; ++r)
+          if (r < nr) partial[static_cast<long long>(blockIdx.x) * m + row + r] = d[r];
+    }
   }
   // last block reduces over chunks in index order
   __shared__ bool am_last;
   __syncthreads();
   if (threadIdx.x == 0) {
     __threadfence();
-    am_last = (atomicAdd(counter, 1u) == gridDim.x - 1);
+    am_last = (atomicAdd(counter, 1u) == gridDim.x * gridDim.y - 1);
   }
   __syncthreads();
   if (!am_last) return;
@@ -406,10 +415,12 @@ __global__ void __launch_bounds__(kTpb) k_row_gemv(const double* __restrict__ A,
   if (threadIdx.x == 0) *counter = 0u;
 }
 
-void row_gemv(const double* A, int m, long long N, VSel x, long long x_off, int scaled, const MinresState* st,
-              double* partial, unsigned* counter, double* out, const RowGemv& plan, cudaStream_t s) {
-  k_row_gemv<<<plan.nchunks, kTpb, plan.chunk * sizeof(double), s>>>(A, m, N, x, x_off, scaled, st, partial,
-                                                                     counter, out, plan.chunk);
+void row_gemv(const double* A, int m, long long N, long long ld, VSel x, long long x_off, int scaled,
+              const MinresState* st, double* partial, unsigned* counter, double* out, const RowGemv& plan,
+              cudaStream_t s) {
+  const dim3 grid(plan.nchunks, (m + kRowsPerCta - 1) / kRowsPerCta);
+  k_row_gemv<<<grid, kTpb, plan.chunk * sizeof(double), s>>>(A, m, N, ld, x, x_off, scaled, st, partial, counter, out,
+                                                             plan.chunk);
   check_launch("row_gemv");
 }
 
@@ -458,11 +469,13 @@ __global__ void __launch_bounds__(kTpb) k_saddle(OperatorArgs op, VSel xs, int s
       }
       double o = 0.0;
       o = o + 1.0 * sd;  // spmv_add(*D, zeta, 1.0, out2)
-      if (op.m > 0) {    // matvec_transpose(J, J dm), linalg.cpp:45-54
+      if (op.m > 0 && op.q != nullptr) {  // fused: J^T (J zhat2) = J^T (t' * ig) ~ q * ig (Woodbury identity J z2 = t')
+        o = o + *op.neg_inv_beta * (op.q[c] * sc);
+      } else if (op.m > 0) {  // matvec_transpose(J, J dm), linalg.cpp:45-54
         double jt = 0.0;
         const double* __restrict__ Jc = op.J + c;
 #pragma unroll 8
-        for (int i = 0; i < op.m; ++i) jt = jt + __ldg(Jc + static_cast<long long>(i) * op.N) * usm[i];
+        for (int i = 0; i < op.m; ++i) jt = jt + __ldg(Jc + static_cast<long long>(i) * op.ldj) * usm[i];
         o = o + *op.neg_inv_beta * jt;  // axpy(-1.0 / beta, jtjdm, out2)
       }
       y[op.K + c] = o;
@@ -493,11 +506,12 @@ void saddle_operator(const OperatorArgs& op, VSel x, int scaled, const double* u
 // ======================================================================
 // Preconditioner (inversion.cpp:71-89) fused with the v-combination
 // ======================================================================
-__global__ void __launch_bounds__(kTpb) k_combine_prec(PrecArgs pa, VSel azs, VSel vcs, VSel vps, VSel vns,
-                                                       VSel zns, int loop, MinresState* st, int nb_edge,
-                                                       int chunk, double* dots_part, double* t_part,
-                                                       unsigned* counter, double* t_out) {
-  extern __shared__ double vsm[];
+// v_next = Az + c1 v_cur + c2 v_prev (combine, minres.cpp:76-77; `loop`) or v = y
+// (plain preconditioner input); z1 = qinv .* v1 on the edge part (inversion.cpp:79);
+// per-block partial dots <z, v>, <z, z> (edge part) and <v, v> (all) -> dots_part.
+__global__ void __launch_bounds__(kTpb) k_combine_elem(PrecArgs pa, VSel azs, VSel vcs, VSel vps, VSel vns,
+                                                       VSel zns, int loop, const MinresState* st,
+                                                       double* dots_part) {
   __shared__ double red[3 * (kTpb / 32)];
   const double* __restrict__ az = vsel(azs, st);
   double* __restrict__ vn = vsel(vns, st);
@@ -506,90 +520,38 @@ __global__ void __launch_bounds__(kTpb) k_combine_prec(PrecArgs pa, VSel azs, VS
   const double* __restrict__ vc = loop ? vsel(vcs, st) : nullptr;
   const double* __restrict__ vp = loop ? vsel(vps, st) : nullptr;
   double d[3] = {0.0, 0.0, 0.0};  // <z, v>, <z, z>, <v, v>
-  if (static_cast<int>(blockIdx.x) < nb_edge) {
-    const long long e = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (e < pa.K) {
-      double v;
-      if (loop) {
-        v = az[e] + c1 * vc[e];  // combine: ca*a + cb*b + cc*c, ca = 1
-        v = v + c2 * vp[e];
-        vn[e] = v;
-      } else {
-        v = az[e];
-      }
-      const double z = __ldg(&pa.qinv[e]) * v;
-      zn[e] = z;
+  const long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < pa.K + pa.N) {
+    double v;
+    if (loop) {
+      v = az[i] + c1 * vc[i];  // combine: ca*a + cb*b + cc*c, ca = 1
+      v = v + c2 * vp[i];
+      vn[i] = v;
+    } else {
+      v = az[i];
+    }
+    if (i < pa.K) {
+      const double z = __ldg(&pa.qinv[i]) * v;
+      zn[i] = z;
       d[0] = z * v;
       d[1] = z * z;
-      d[2] = v * v;
     }
-    block_reduce<3>(d, red);
-    if (threadIdx.x == 0)
-      for (int k = 0; k < 3; ++k) dots_part[blockIdx.x * 3 + k] = d[k];
-  } else {
-    const long long c0 = static_cast<long long>(blockIdx.x - nb_edge) * chunk;
-    const int len = static_cast<int>(min(static_cast<long long>(chunk), pa.N - c0));
-    for (int t = threadIdx.x; t < len; t += blockDim.x) {
-      const long long i = pa.K + c0 + t;
-      double v;
-      if (loop) {
-        v = az[i] + c1 * vc[i];
-        v = v + c2 * vp[i];
-        vn[i] = v;
-      } else {
-        v = az[i];
-      }
-      vsm[t] = v;
-      d[2] = d[2] + v * v;
-    }
-    block_reduce<3>(d, red);  // also syncs vsm
-    if (threadIdx.x == 0)
-      for (int k = 0; k < 3; ++k) dots_part[blockIdx.x * 3 + k] = d[k];
-    if (pa.m > 0) {
-      const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-      const bool vec_ok = ((pa.N & 1) == 0);
-      const long long cb = blockIdx.x - nb_edge;
-      for (int row = warp * kRowsPerWarp; row < pa.m; row += nw * kRowsPerWarp) {
-        double d[kRowsPerWarp];
-        const int nr = min(kRowsPerWarp, pa.m - row);
-        warp_rows_dot<kRowsPerWarp>(pa.Ht + static_cast<long long>(row) * pa.N + c0, pa.N, nr, vsm, len, vec_ok,
-                                    lane, d);
-        if (lane == 0)
-#pragma unroll
-          for (int r = 0; r < kRowsPerWarp; ++r)
-            if (r < nr) t_part[cb * pa.m + row + r] = d[r];
-      }
-    }
+    d[2] = v * v;
   }
-  if (pa.m == 0) return;
-  // last block: t_out = sum over cell chunks (fixed order)
-  __shared__ bool am_last;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    __threadfence();
-    am_last = (atomicAdd(counter, 1u) == gridDim.x - 1);
-  }
-  __syncthreads();
-  if (!am_last) return;
-  __threadfence();
-  const int nbc = gridDim.x - nb_edge;
-  for (int row = threadIdx.x; row < pa.m; row += blockDim.x) {
-    double s = 0.0;
-    for (int b = 0; b < nbc; ++b) s += __ldcg(&t_part[static_cast<long long>(b) * pa.m + row]);
-    t_out[row] = s;
-  }
-  if (threadIdx.x == 0) *counter = 0u;
+  block_reduce<3>(d, red);
+  if (threadIdx.x == 0)
+    for (int k = 0; k < 3; ++k) dots_part[blockIdx.x * 3 + k] = d[k];
 }
+
+int combine_blocks(long long K, long long N) { return static_cast<int>(grid_for(K + N)); }
 
 void combine_precondition(const PrecArgs& pa, VSel az, VSel vcur, VSel vprev, VSel vnext, VSel znext, int loop,
                           MinresState* st, double* /*vcopy*/, double* dots_part, double* t_part,
                           unsigned* counter, double* t_out, const RowGemv& plan, cudaStream_t s) {
-  const int nbe = static_cast<int>(grid_for(pa.K));
-  const int nbc = static_cast<int>((pa.N + plan.chunk - 1) / plan.chunk);
-  k_combine_prec<<<nbe + nbc, kTpb, plan.chunk * sizeof(double), s>>>(pa, az, vcur, vprev, vnext, znext, loop, st,
-                                                                      nbe, plan.chunk, dots_part, t_part, counter,
-                                                                      t_out);
-  check_launch("combine_precondition");
+  k_combine_elem<<<combine_blocks(pa.K, pa.N), kTpb, 0, s>>>(pa, az, vcur, vprev, vnext, znext, loop, st, dots_part);
+  check_launch("combine_elem");
+  if (pa.m > 0)  // t = H^T v2 (matvec_transpose(h_hat, y2), inversion.cpp:82): row GEMV over Ht
+    row_gemv(pa.Ht, pa.m, pa.N, pa.ldh, vnext, pa.K, 0, st, t_part, counter, t_out, plan, s);
 }
 
 // t2 = Cinv t, warp per row
@@ -632,8 +594,20 @@ __global__ void __launch_bounds__(kTpb) k_finish_prec(PrecArgs pa, const double*
     if (pa.m > 0) {  // w = matvec(h_hat, t) row c (linalg.cpp:33-43); s += (-1/beta) w
       double w = 0.0;
       const double* __restrict__ Hc = pa.Ht + c;
+      if (pa.q != nullptr) {  // one sweep over H and J: w = (H t')_c, q_c = (J^T t')_c
+        const double* __restrict__ Jc = pa.J + c;
+        double qq = 0.0;
 #pragma unroll 8
-      for (int q = 0; q < pa.m; ++q) w = w + __ldg(Hc + static_cast<long long>(q) * pa.N) * tsm[q];
+        for (int q = 0; q < pa.m; ++q) {
+          const double tq = tsm[q];
+          w = w + __ldg(Hc + static_cast<long long>(q) * pa.ldh) * tq;
+          qq = qq + __ldg(Jc + static_cast<long long>(q) * pa.ldj) * tq;
+        }
+        pa.q[c] = qq;
+      } else {
+#pragma unroll 8
+        for (int q = 0; q < pa.m; ++q) w = w + __ldg(Hc + static_cast<long long>(q) * pa.ldh) * tsm[q];
+      }
       z = z + *pa.neg_inv_beta * w;
     }
     zn[pa.K + c] = z;
@@ -850,7 +824,7 @@ __global__ void __launch_bounds__(kTpb) k_rhs(OperatorArgs op, double beta, cons
     double jt = 0.0;
     const double* __restrict__ Jc = op.J + c;
 #pragma unroll 8
-    for (int i = 0; i < op.m; ++i) jt = jt + __ldg(Jc + static_cast<long long>(i) * op.N) * gsm[i];
+    for (int i = 0; i < op.m; ++i) jt = jt + __ldg(Jc + static_cast<long long>(i) * op.ldj) * gsm[i];
     rhs[op.K + c] = jt / beta;
   }
 }
@@ -889,7 +863,8 @@ __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b)
                : "d"(a), "d"(b));
 }
 
-__global__ void __launch_bounds__(256, 1) k_dgemm_nt(const double* __restrict__ A, const double* __restrict__ B, int m,
+__global__ void __launch_bounds__(256, 1) k_dgemm_nt(const double* __restrict__ A, long long lda,
+                                                     const double* __restrict__ B, long long ldb, int m,
                                                      long long N, long long kchunk, const int2* __restrict__ pairs,
                                                      int npairs, double* __restrict__ part) {
   using namespace dg;
@@ -915,13 +890,13 @@ __global__ void __launch_bounds__(256, 1) k_dgemm_nt(const double* __restrict__ 
       {
         const int gr = i0 + row;
         const bool ok = gr < m && kk < k1;
-        const double* src = ok ? A + static_cast<long long>(gr) * N + kk : A;
+        const double* src = ok ? A + static_cast<long long>(gr) * lda + kk : A;
         cp_async16(As + (stage * BM + row) * LDS + kc, src, ok ? 16 : 0);
       }
       {
         const int gr = j0 + row;
         const bool ok = gr < m && kk < k1;
-        const double* src = ok ? B + static_cast<long long>(gr) * N + kk : B;
+        const double* src = ok ? B + static_cast<long long>(gr) * ldb + kk : B;
         cp_async16(Bs + (stage * BN + row) * LDS + kc, src, ok ? 16 : 0);
       }
     }
@@ -997,7 +972,8 @@ DgemmPlan dgemm_plan(int m, long long N, int full, int sm_count) {
   p.npairs = full ? p.ntiles * p.ntiles : p.ntiles * (p.ntiles + 1) / 2;
   p.full = full;
   const long long kblocks = (N + dg::BK - 1) / dg::BK;
-  int splits = std::max(1, (2 * sm_count + p.npairs - 1) / p.npairs);
+  // one CTA per SM (123 KB smem): at most 2 full waves, never a straggler third wave
+  int splits = std::max(1, (2 * sm_count) / p.npairs);
   splits = static_cast<int>(std::min<long long>(splits, kblocks));
   long long kchunk = ((kblocks + splits - 1) / splits) * dg::BK;
   p.splits = static_cast<int>((N + kchunk - 1) / kchunk);
@@ -1005,9 +981,10 @@ DgemmPlan dgemm_plan(int m, long long N, int full, int sm_count) {
   return p;
 }
 
-void capacitance_dgemm(const double* J, const double* Ht, int m, long long N, double beta, const DgemmPlan& plan,
-                       double* part, double* C, cudaStream_t s) {
-  if (N % 2 != 0) throw std::invalid_argument("capacitance_dgemm: N must be even (16-byte rows)");
+void capacitance_dgemm(const double* J, long long ldj, const double* Ht, long long ldh, int m, long long N,
+                       double beta, const DgemmPlan& plan, double* part, double* C, cudaStream_t s) {
+  if (N % 2 != 0 || ldj % 2 != 0 || ldh % 2 != 0)
+    throw std::invalid_argument("capacitance_dgemm: N and leading dimensions must be even (16-byte rows)");
   // pair list lives at the end of the partial buffer
   int2 hp[4096];
   int np = 0;
@@ -1022,7 +999,7 @@ void capacitance_dgemm(const double* J, const double* Ht, int m, long long N, do
     attr_set = true;
   }
   dim3 grid(plan.npairs, plan.splits);
-  k_dgemm_nt<<<grid, 256, dg::SMEM, s>>>(J, Ht, m, N, plan.kchunk, dpairs, plan.npairs, part);
+  k_dgemm_nt<<<grid, 256, dg::SMEM, s>>>(J, ldj, Ht, ldh, m, N, plan.kchunk, dpairs, plan.npairs, part);
   check_launch("dgemm_nt");
   dim3 g2((dg::BM * dg::BN + 255) / 256, plan.npairs);
   k_dgemm_finalize<<<g2, 256, 0, s>>>(part, dpairs, plan.npairs, plan.splits, m, beta, C);

@@ -19,6 +19,28 @@ struct DLevel {
   int wideA = 0, wideP = 0, wideR = 0;
 };
 
+// Fused coarse tail of the single-RHS V-cycle (vcycle_tail.cu): levels l0..L-1
+// in one cluster launch.  Index k of the arrays is level l0 + k.
+constexpr int kMaxTail = 14;
+struct TailLevel {
+  DCsr A, P, R;
+  const double* wd = nullptr;
+  int n = 0;
+  int wideA = 0, wideP = 0, wideR = 0;
+};
+struct TailArgs {
+  int nlev = 0;  // non-coarsest tail levels; level l0 + nlev is the coarsest
+  TailLevel lv[kMaxTail];
+  const double* Ainv = nullptr;  // coarsest explicit inverse
+  const double* Lc = nullptr;    // coarsest Cholesky factor (exact mode)
+  int nc = 0, exact = 0;
+  double* r[kMaxTail + 1] = {};
+  double* e[kMaxTail + 1] = {};
+  double* res[kMaxTail] = {};
+  double* x[kMaxTail] = {};
+};
+void vcycle_tail(const TailArgs& a, VSel rin, double* out, const MinresState* st, int cluster, cudaStream_t s);
+
 // wide-level kernels (vcycle_wide.cu)
 void vcw_down(const DLevel& L, VSel r, double* resid, const MinresState* st, cudaStream_t s);
 void vcw_restrict(const DLevel& L, const double* resid, double* rc, cudaStream_t s);
@@ -60,9 +82,11 @@ void mvc_up2(const DLevel& L, const double* r, int ldr, const double* x, double*
 void mcoarse_inverse(const double* Ainv, int n, const double* r, double* x, int b, cudaStream_t s);
 
 // rows [r0, r0+b) of a row-major (rows x cols) matrix -> cols x b interleaved
-void transpose_rows_to_batch(const double* A, long long cols, int r0, int b, double* X, cudaStream_t s);
+void transpose_rows_to_batch(const double* A, long long cols, long long ld, int r0, int b, double* X,
+                             cudaStream_t s);
 // cols x b interleaved -> rows [r0, r0+b) of a row-major (rows x cols) matrix
-void transpose_batch_to_rows(const double* X, long long cols, int r0, int b, double* A, cudaStream_t s);
+void transpose_batch_to_rows(const double* X, long long cols, long long ld, int r0, int b, double* A,
+                             cudaStream_t s);
 
 // ---------------------------------------------------------------- operator
 struct OperatorArgs {
@@ -70,16 +94,22 @@ struct OperatorArgs {
   const double* J = nullptr;  // m x N row-major (nullptr: no low-rank term)
   int m = 0;
   long long K = 0, N = 0;
+  long long ldj = 0;  // row stride of J (>= N; padded to spread DRAM channels)
   const double* neg_inv_beta = nullptr;  // device scalar -1/beta (graph-stable across beta)
+  // Woodbury-fused loop: J^T u = (J^T t') / gamma with q = J^T t'
+  // produced by the previous preconditioner pass; J is then not read by the operator.
+  const double* q = nullptr;
 };
 
 // u = A[:, ] x2 * scale partial GEMV over rows of a row-major (m x N) matrix,
 // scale = st->inv_gamma when scaled != 0 (zhat = z / gamma), else 1.
 struct RowGemv {
-  int chunk = 0, nchunks = 0;
+  int chunk = 0, nchunks = 0, ngroups = 0;
 };
-RowGemv row_gemv_plan(long long N);
-void row_gemv(const double* A, int m, long long N, VSel x, long long x_off, int scaled,
+RowGemv row_gemv_plan(long long N, int m);
+// number of blocks of the elementwise combine kernel (dots partials)
+int combine_blocks(long long K, long long N);
+void row_gemv(const double* A, int m, long long N, long long ld, VSel x, long long x_off, int scaled,
               const MinresState* st, double* partial, unsigned* counter, double* out,
               const RowGemv& plan, cudaStream_t s);
 
@@ -97,8 +127,12 @@ struct PrecArgs {
   const double* Lc = nullptr;   // m x m lower Cholesky factor of C (exact mode)
   int m = 0;
   long long K = 0, N = 0;
+  long long ldh = 0, ldj = 0;  // row strides of Ht and J
   const double* neg_inv_beta = nullptr;
   int exact = 0;
+  // fused loop: the finish pass also forms q = J^T t' (J read in the same sweep as H)
+  const double* J = nullptr;
+  double* q = nullptr;
 };
 
 // v_next = Az + c1 v_cur + c2 v_prev (combine, minres.cpp:76-77) or, when
@@ -144,8 +178,8 @@ struct DgemmPlan {
   int full = 0;
 };
 DgemmPlan dgemm_plan(int m, long long N, int full, int sm_count);
-void capacitance_dgemm(const double* J, const double* Ht, int m, long long N, double beta,
-                       const DgemmPlan& plan, double* part, double* C, cudaStream_t s);
+void capacitance_dgemm(const double* J, long long ldj, const double* Ht, long long ldh, int m, long long N,
+                       double beta, const DgemmPlan& plan, double* part, double* C, cudaStream_t s);
 // dense_cholesky (linalg.cpp:88-105), operation order preserved; *fail = 1 on a
 // non-positive pivot.
 void cholesky(const double* C, double* L, int n, int* fail, cudaStream_t s);
