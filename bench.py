@@ -287,12 +287,22 @@ def run_gnw(args):
     b = ctx.assemble_rhs(dm_d, zN, dg_d, zm)
     ctx.minres(b, tol=tol)
     kern = {}
-    for name in ("row_gemv", "saddle", "combine_prec", "finish_prec", "vcycle", "update"):
+    # launches per MINRES iteration: k_row_gemv runs twice (J zhat2 and, inside
+    # combine_prec, H^T v2); everything else once
+    per_iter = {"row_gemv": 2, "saddle": 1, "combine_prec": 1, "finish_prec": 1, "vcycle": 1, "update": 1}
+    for name in per_iter:
         sec, byt = ctx.profile_kernel(name, reps=20)
-        kern[name] = {"ms": sec * 1e3, "GB": byt / 1e9, "GBps": byt / sec / 1e9, "frac": byt / sec / 1e9 / hbm_peak}
+        kern[name] = {"ms": sec * 1e3, "GB": byt / 1e9, "GBps": byt / sec / 1e9, "frac": byt / sec / 1e9 / hbm_peak,
+                      "launches_per_iteration": per_iter[name]}
     it_sec, it_bytes = ctx.profile_kernel("iteration")
     dg_sec, dg_flops = ctx.profile_kernel("dgemm", reps=5)
-    dom = max(("row_gemv", "saddle", "combine_prec", "finish_prec"), key=lambda k: kern[k]["ms"])
+    # share of one iteration per kernel KIND (k_row_gemv: its own J pass + the H^T pass of combine_prec)
+    kind_ms = {"row_gemv": 2 * kern["row_gemv"]["ms"], "saddle": kern["saddle"]["ms"],
+               "finish_prec": kern["finish_prec"]["ms"], "vcycle": kern["vcycle"]["ms"],
+               "update": kern["update"]["ms"]}
+    dom = max(kind_ms, key=kind_ms.get)
+    for k, v in kind_ms.items():
+        kern[k]["iteration_share"] = v / (it_sec * 1e3) if it_sec else None
     traffic = None
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
@@ -323,15 +333,19 @@ def run_gnw(args):
                        "parallelism": f"replicas x{ws}",
                        "l2": "no flush: per-solve inputs (J 1.07 GB + H 1.07 GB) exceed the 126 MB L2",
                        "amg_levels": info["n_levels"], "coarse_n": info["coarse_n"]},
-            "roofline": {"bound": "hbm", "kernel": dom, "achieved": kern[dom]["GBps"], "peak": hbm_peak,
+            "roofline": {"bound": "hbm", "kernel": "k_" + dom, "achieved": kern[dom]["GBps"], "peak": hbm_peak,
                          "unit": "GB/s", "frac": kern[dom]["frac"], "traffic": traffic,
                          "peak_source": peak_src,
                          "algorithmic_bytes_per_launch": kern[dom]["GB"] * 1e9,
+                         "iteration_share": kern[dom]["iteration_share"],
+                         "dmma_peak_tflops": 37.2,
                          "iteration": {"ms": it_sec * 1e3, "GB": it_bytes / 1e9,
                                        "GBps": it_bytes / it_sec / 1e9 if it_sec else None,
                                        "frac": it_bytes / it_sec / 1e9 / hbm_peak if it_sec else None},
                          "kernels": kern,
-                         "dgemm": {"ms": dg_sec * 1e3, "TFLOPs": dg_flops / dg_sec / 1e12}},
+                         "dgemm": {"ms": dg_sec * 1e3, "TFLOPs": dg_flops / dg_sec / 1e12,
+                                   "frac_of_dmma_peak": dg_flops / dg_sec / 1e12 / 37.2,
+                                   "note": "algorithmic 2 m^2 N; lower-triangle tiles only are executed"}},
             "cpu_baseline": cpu,
             "e2e": {"value": ws * args.steps / e2e_elapsed, "unit": UNIT, "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h},

@@ -9,9 +9,41 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <stdexcept>
+#include <string>
+#include <utility>
+
 namespace gnw {
 
 constexpr int kWarp = 32;
+
+// Programmatic dependent launch: every kernel starts with griddep_wait(), so a
+// launch may be issued (and its CTAs made resident) while its predecessor on the
+// stream drains; the wait returns once the predecessor has completed and its
+// memory is visible.  Without the launch attribute the wait is a no-op.
+__device__ __forceinline__ void griddep_wait() {
+  asm volatile("griddepcontrol.wait;\n" ::: "memory");
+  // allow the next kernel's CTAs to be scheduled once every CTA of this grid has started
+  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+}
+
+extern bool g_pdl;  // launch with programmatic stream serialization (env GNW_PDL, default on)
+
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                            Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = g_pdl ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
 
 // MINRES loop status codes (device -> host).
 enum : int {
@@ -149,7 +181,14 @@ __device__ bool grid_reduce_last(double (&v)[NV], double* part, unsigned int* co
 
 }  // namespace gnw
 
-#define GNW_CUDA_CHECK(expr)                                                     \
+#define GNW_LAUNCH(expr)                                                                        \
+  do {                                                                                          \
+    cudaError_t e__ = (expr);                                                                   \
+    if (e__ != cudaSuccess)                                                                     \
+      throw std::runtime_error(std::string("kernel launch failed: ") + cudaGetErrorString(e__)); \
+  } while (0)
+
+#define GNW_CUDA_CHECK(expr)                                                  \
   do {                                                                           \
     cudaError_t e__ = (expr);                                                    \
     if (e__ != cudaSuccess) throw ::gnw::DeviceError(#expr, e__, __FILE__, __LINE__); \

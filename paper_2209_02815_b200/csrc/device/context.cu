@@ -67,6 +67,7 @@ Context::Context(int device) : device_(device) {
   if (prop.major < 10) throw DeviceError("gnw: this build targets sm_100a (B200); found sm_" + std::to_string(prop.major) + std::to_string(prop.minor));
   sm_count_ = prop.multiProcessorCount;
   if (const char* e = std::getenv("GNW_PAD")) pad_ = std::max(0LL, std::atoll(e) / 2 * 2);
+  if (const char* e = std::getenv("GNW_NO_GRAPH")) no_graph_ = std::atoi(e) != 0;
   // A blocking stream: ordered with the legacy default stream, so device-pointer
   // callers (e.g. torch on its default stream) need no extra synchronisation.
   GNW_CUDA_CHECK(cudaStreamCreateWithFlags(&stream_, cudaStreamDefault));
@@ -683,6 +684,19 @@ void Context::assemble_rhs(const double* mdl, const double* mref, const double* 
 }
 
 // ------------------------------------------------------------------ MINRES
+// One MINRES iteration (minres.cpp:70-148) as device work, ring slots chosen on the
+// device from st_->j.  Captured once into the conditional-WHILE graph body, or
+// launched per iteration by the host in GNW_NO_GRAPH (profiling) mode.
+void Context::launch_iteration(unsigned long long cond_handle, int use_cond) {
+  const bool fu = fused_active();
+  operator_into(ring2(Z_, 0), 1, vfixed(az_), st_, 1, fu);                  // Az = A zhat, delta
+  precondition_into(ring3(V_, 2), ring3(Vk_, 2), ring2(Z_, 1), st_, 1,       // v_next, z_next = P^-1 v_next,
+                    ring3(V_, 1), ring3(V_, 0), fu);                         // gamma_next, Givens
+  minres_update(K_ + N_, ring2(Z_, 0), vfixed(az_), ring3(W_, 0), ring3(W_, 1), ring3(W_, 2), ring3(U_, 0),
+                ring3(U_, 1), ring3(U_, 2), x_, r_, st_, hist_e_, hist_p_, hist_cap_, upart_, counters_ + 4,
+                cond_handle, use_cond, stream_);
+}
+
 void Context::build_graph() {
   destroy_graph();
   cudaGraph_t g;
@@ -703,13 +717,7 @@ void Context::build_graph() {
   // iteration j: v_prev = V[j%3], v_cur = V[(j+1)%3], v_next = V[(j+2)%3] (same for w, u);
   //              z_cur = Z[j%2], z_next = Z[(j+1)%2]
   try {
-    const bool fu = fused_active();
-    operator_into(ring2(Z_, 0), 1, vfixed(az_), st_, 1, fu);                  // Az = A zhat, delta
-    precondition_into(ring3(V_, 2), ring3(Vk_, 2), ring2(Z_, 1), st_, 1,       // v_next, z_next = P^-1 v_next,
-                      ring3(V_, 1), ring3(V_, 0), fu);                         // gamma_next, Givens
-    minres_update(K_ + N_, ring2(Z_, 0), vfixed(az_), ring3(W_, 0), ring3(W_, 1), ring3(W_, 2), ring3(U_, 0),
-                  ring3(U_, 1), ring3(U_, 2), x_, r_, st_, hist_e_, hist_p_, hist_cap_, upart_, counters_ + 4,
-                  static_cast<unsigned long long>(h), 1, stream_);
+    launch_iteration(static_cast<unsigned long long>(h), 1);
   } catch (...) {
     cudaGraph_t dummy;
     cudaStreamEndCapture(stream_, &dummy);
@@ -820,7 +828,7 @@ MinresResult Context::minres(const double* b, const double* x0, double* x, doubl
   st.status = maxit >= 1 ? kRunning : kMaxit;
   *h_st_ = st;
   GNW_CUDA_CHECK(cudaMemcpyAsync(st_, h_st_, sizeof(MinresState), cudaMemcpyHostToDevice, s));
-  if (!graph_exec_) {
+  if (!graph_exec_ && !no_graph_) {
     build_graph();
     built_now = graph_nodes_;
   }
@@ -834,13 +842,18 @@ MinresResult Context::minres(const double* b, const double* x0, double* x, doubl
   bool done = false;
   while (!done) {
     MinresState cur;
-    if (h_st_->status == kRunning) {
+    if (h_st_->status == kRunning && no_graph_) {  // host-driven loop (profiling): one sync per iteration
+      launch_iteration(0, 0);
+      GNW_CUDA_CHECK(cudaMemcpyAsync(h_st_, st_, sizeof(MinresState), cudaMemcpyDeviceToHost, s));
+      sync();
+      if (h_st_->status == kRunning) continue;
+    } else if (h_st_->status == kRunning) {
       GNW_CUDA_CHECK(cudaGraphLaunch(graph_exec_, s));
       GNW_CUDA_CHECK(cudaMemcpyAsync(h_st_, st_, sizeof(MinresState), cudaMemcpyDeviceToHost, s));
       sync();
     }
     cur = *h_st_;
-    graph_iters = static_cast<uint64_t>(cur.iterations);
+    graph_iters = no_graph_ ? 0 : static_cast<uint64_t>(cur.iterations);  // direct launches are counted as issued
     switch (cur.status) {
       case kErrNotPD: throw std::runtime_error("minres: preconditioner is not positive definite");
       case kErrStagnated: throw std::runtime_error("minres: breakdown (stagnated rotation)");

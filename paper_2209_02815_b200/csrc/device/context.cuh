@@ -111,6 +111,8 @@ class Context {
                          bool fused = false);
   bool fused_active() const;
   void build_graph();
+  void launch_iteration(unsigned long long cond_handle, int use_cond);
+  bool no_graph_ = false;  // env GNW_NO_GRAPH=1: host-driven loop (for ncu; kernels in conditional graphs are not listed)
   void destroy_graph();
   double* stage_in(const double* p, size_t n, double* dev);
   void stage_out(double* host, const double* dev, size_t n);

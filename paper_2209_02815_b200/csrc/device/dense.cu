@@ -32,6 +32,7 @@ constexpr int PT = 256;      // panel kernel threads per CTA (32 diagonal-block 
 
 __global__ void __launch_bounds__(PT) k_chol_panel(double* __restrict__ W, double* __restrict__ L, int n, int p,
                                                    int* fail) {
+  griddep_wait();
   __shared__ double colk[PW];
   __shared__ int bad;
   if (*fail) return;
@@ -88,6 +89,7 @@ __global__ void __launch_bounds__(PT) k_chol_panel(double* __restrict__ W, doubl
 // trailing update for panel [p, p+w): tiles (ti >= tj) of the rows/cols >= p+w
 __global__ void __launch_bounds__(256) k_chol_update(double* __restrict__ W, const double* __restrict__ L, int n,
                                                      int p, int w, const int* fail) {
+  griddep_wait();
   __shared__ double Li[32][PW + 1], Lj[32][PW + 1];
   if (*fail) return;
   const int q0 = p + w;
@@ -116,6 +118,7 @@ __global__ void __launch_bounds__(256) k_chol_update(double* __restrict__ W, con
 
 __global__ void k_copy_lower_zero_upper(const double* __restrict__ C, double* __restrict__ W, double* __restrict__ L,
                                         int n, int* fail) {
+  griddep_wait();
   const long long e = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (e == 0) *fail = 0;
   if (e >= static_cast<long long>(n) * n) return;
@@ -125,18 +128,18 @@ __global__ void k_copy_lower_zero_upper(const double* __restrict__ C, double* __
 
 void cholesky_blocked(const double* C, double* W, double* L, int n, int* fail, cudaStream_t s) {
   const long long nn = static_cast<long long>(n) * n;
-  k_copy_lower_zero_upper<<<static_cast<unsigned>((nn + 255) / 256), 256, 0, s>>>(C, W, L, n, fail);
+  GNW_LAUNCH(launch_k(k_copy_lower_zero_upper, static_cast<unsigned>((nn + 255) / 256), 256, 0, s, C, W, L, n, fail));
   note_launch("chol_init");
   for (int p = 0; p < n; p += PW) {
     const int w = std::min(PW, n - p);
     const int below = std::max(0, n - p - PW);
     const int ctas = std::max(1, (below + (PT - PW) - 1) / (PT - PW));
-    k_chol_panel<<<ctas, PT, 0, s>>>(W, L, n, p, fail);
+    GNW_LAUNCH(launch_k(k_chol_panel, ctas, PT, 0, s, W, L, n, p, fail));
     note_launch("chol_panel");
     const int rem = n - (p + w);
     if (rem > 0) {
       const int nt = (rem + 31) / 32;
-      k_chol_update<<<nt * (nt + 1) / 2, 256, 0, s>>>(W, L, n, p, w, fail);
+      GNW_LAUNCH(launch_k(k_chol_update, nt * (nt + 1) / 2, 256, 0, s, W, L, n, p, w, fail));
       note_launch("chol_update");
     }
   }
@@ -148,6 +151,7 @@ void cholesky_blocked(const double* C, double* W, double* L, int n, int* fail, c
 // then the 32 x 32 diagonal block is solved row by row through shared memory.
 __global__ void __launch_bounds__(1024) k_trinv_block(const double* __restrict__ L, double* __restrict__ Y, int n,
                                                       int p) {
+  griddep_wait();
   __shared__ double yr[32][33];
   const int r = threadIdx.y;               // row within block
   const int jc = threadIdx.x;              // column within chunk
@@ -177,7 +181,7 @@ __global__ void __launch_bounds__(1024) k_trinv_block(const double* __restrict__
 void trinv_blocked(const double* L, double* Y, int n, cudaStream_t s) {
   for (int p = 0; p < n; p += 32) {
     const int chunks = (std::min(n, p + 32) + 31) / 32;
-    k_trinv_block<<<chunks, dim3(32, 32), 0, s>>>(L, Y, n, p);
+    GNW_LAUNCH(launch_k(k_trinv_block, chunks, dim3(32, 32), 0, s, L, Y, n, p));
     note_launch("trinv_block");
   }
 }

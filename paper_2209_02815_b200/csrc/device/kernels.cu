@@ -16,6 +16,7 @@
 #include <algorithm>
 #include <atomic>
 #include <cmath>
+#include <cstdlib>
 #include <stdexcept>
 #include <string>
 
@@ -47,6 +48,11 @@ __device__ __forceinline__ double ldg(const double* p) { return __ldg(p); }
 
 uint64_t launch_count() { return g_launches.load(std::memory_order_relaxed); }
 
+bool g_pdl = [] {
+  const char* e = std::getenv("GNW_PDL");
+  return e == nullptr || std::atoi(e) != 0;
+}();
+
 // ======================================================================
 // V-cycle, single right-hand side (amg.cpp:90-111)
 // ======================================================================
@@ -54,6 +60,7 @@ uint64_t launch_count() { return g_launches.load(std::memory_order_relaxed); }
 // resid = r - A (wd .* r)        amg.cpp:98-101
 __global__ void __launch_bounds__(kTpb) k_vc_down(DCsr A, const double* __restrict__ wd, VSel rs,
                                                   double* __restrict__ resid, const MinresState* st) {
+  griddep_wait();
   const double* __restrict__ r = vsel(rs, st);
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= A.n_rows) return;
@@ -69,6 +76,7 @@ __global__ void __launch_bounds__(kTpb) k_vc_down(DCsr A, const double* __restri
 // rc = P^T resid (gather through R)        amg.cpp:103
 __global__ void __launch_bounds__(kTpb) k_vc_restrict(DCsr R, const double* __restrict__ resid,
                                                       double* __restrict__ rc) {
+  griddep_wait();
   const int a = blockIdx.x * blockDim.x + threadIdx.x;
   if (a >= R.n_rows) return;
   double s = 0.0;
@@ -81,6 +89,7 @@ __global__ void __launch_bounds__(kTpb) k_vc_restrict(DCsr R, const double* __re
 __global__ void __launch_bounds__(kTpb) k_vc_up1(DCsr P, const double* __restrict__ wd, VSel rs,
                                                  const double* __restrict__ ec, double* __restrict__ x,
                                                  const MinresState* st) {
+  griddep_wait();
   const double* __restrict__ r = vsel(rs, st);
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= P.n_rows) return;
@@ -94,6 +103,7 @@ __global__ void __launch_bounds__(kTpb) k_vc_up1(DCsr P, const double* __restric
 __global__ void __launch_bounds__(kTpb) k_vc_up2(DCsr A, const double* __restrict__ wd, VSel rs,
                                                  const double* __restrict__ x, double* __restrict__ out,
                                                  const MinresState* st) {
+  griddep_wait();
   const double* __restrict__ r = vsel(rs, st);
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= A.n_rows) return;
@@ -107,6 +117,7 @@ __global__ void __launch_bounds__(kTpb) k_vc_up2(DCsr A, const double* __restric
 // x[:, q] = Ainv r[:, q]; one warp per (row, rhs), lane-strided partials + xor tree
 __global__ void k_coarse_inverse(const double* __restrict__ Ainv, int n, VSel rs, double* __restrict__ x,
                                  const MinresState* st, int nrhs) {
+  griddep_wait();
   const double* __restrict__ r = vsel(rs, st);
   const long long w = (static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
@@ -121,6 +132,7 @@ __global__ void k_coarse_inverse(const double* __restrict__ Ainv, int n, VSel rs
 // cholesky_solve (linalg.cpp:107-123) replayed exactly, one thread per rhs column
 __global__ void k_coarse_cholesky(const double* __restrict__ L, int n, VSel rs, double* __restrict__ x,
                                   const MinresState* st, int nrhs, int ld) {
+  griddep_wait();
   const double* __restrict__ r = vsel(rs, st);
   const int q = blockIdx.x * blockDim.x + threadIdx.x;
   if (q >= nrhs) return;
@@ -141,33 +153,33 @@ void note_launch(const char* what) { check_launch(what); }
 
 void vc_down(const DLevel& L, VSel r, double* resid, const MinresState* st, cudaStream_t s) {
   if (L.wideA) return vcw_down(L, r, resid, st, s);
-  k_vc_down<<<grid_for(L.n), kTpb, 0, s>>>(L.A, L.wd, r, resid, st);
+  GNW_LAUNCH(launch_k(k_vc_down, grid_for(L.n), kTpb, 0, s, L.A, L.wd, r, resid, st));
   check_launch("vc_down");
 }
 void vc_restrict(const DLevel& L, const double* resid, double* rc, cudaStream_t s) {
   if (L.wideR) return vcw_restrict(L, resid, rc, s);
-  k_vc_restrict<<<grid_for(L.R.n_rows), kTpb, 0, s>>>(L.R, resid, rc);
+  GNW_LAUNCH(launch_k(k_vc_restrict, grid_for(L.R.n_rows), kTpb, 0, s, L.R, resid, rc));
   check_launch("vc_restrict");
 }
 void vc_up1(const DLevel& L, VSel r, const double* ec, double* x, const MinresState* st, cudaStream_t s) {
   if (L.wideP) return vcw_up1(L, r, ec, x, st, s);
-  k_vc_up1<<<grid_for(L.n), kTpb, 0, s>>>(L.P, L.wd, r, ec, x, st);
+  GNW_LAUNCH(launch_k(k_vc_up1, grid_for(L.n), kTpb, 0, s, L.P, L.wd, r, ec, x, st));
   check_launch("vc_up1");
 }
 void vc_up2(const DLevel& L, VSel r, const double* x, double* out, const MinresState* st, cudaStream_t s) {
   if (L.wideA) return vcw_up2(L, r, x, out, st, s);
-  k_vc_up2<<<grid_for(L.n), kTpb, 0, s>>>(L.A, L.wd, r, x, out, st);
+  GNW_LAUNCH(launch_k(k_vc_up2, grid_for(L.n), kTpb, 0, s, L.A, L.wd, r, x, out, st));
   check_launch("vc_up2");
 }
 void coarse_inverse(const double* Ainv, int n, VSel r, double* x, const MinresState* st, int nrhs,
                     cudaStream_t s) {
   const long long threads = static_cast<long long>(n) * nrhs * 32;
-  k_coarse_inverse<<<grid_for(threads), kTpb, 0, s>>>(Ainv, n, r, x, st, nrhs);
+  GNW_LAUNCH(launch_k(k_coarse_inverse, grid_for(threads), kTpb, 0, s, Ainv, n, r, x, st, nrhs));
   check_launch("coarse_inverse");
 }
 void coarse_cholesky(const double* L, int n, VSel r, double* x, const MinresState* st, int nrhs, int ld,
                      cudaStream_t s) {
-  k_coarse_cholesky<<<grid_for(nrhs, 64), 64, 0, s>>>(L, n, r, x, st, nrhs, ld);
+  GNW_LAUNCH(launch_k(k_coarse_cholesky, grid_for(nrhs, 64), 64, 0, s, L, n, r, x, st, nrhs, ld));
   check_launch("coarse_cholesky");
 }
 
@@ -179,6 +191,7 @@ void coarse_cholesky(const double* L, int n, VSel r, double* x, const MinresStat
 __global__ void __launch_bounds__(256) k_mvc_down(DCsr A, const double* __restrict__ wd,
                                                   const double* __restrict__ r, int ldr,
                                                   double* __restrict__ resid, int b) {
+  griddep_wait();
   const int i = blockIdx.x * 8 + threadIdx.y;
   const int q = blockIdx.y * 32 + threadIdx.x;
   if (i >= A.n_rows || q >= b) return;
@@ -193,6 +206,7 @@ __global__ void __launch_bounds__(256) k_mvc_down(DCsr A, const double* __restri
 
 __global__ void __launch_bounds__(256) k_mvc_restrict(DCsr R, const double* __restrict__ resid,
                                                       double* __restrict__ rc, int b) {
+  griddep_wait();
   const int a = blockIdx.x * 8 + threadIdx.y;
   const int q = blockIdx.y * 32 + threadIdx.x;
   if (a >= R.n_rows || q >= b) return;
@@ -205,6 +219,7 @@ __global__ void __launch_bounds__(256) k_mvc_restrict(DCsr R, const double* __re
 __global__ void __launch_bounds__(256) k_mvc_up1(DCsr P, const double* __restrict__ wd,
                                                  const double* __restrict__ r, int ldr,
                                                  const double* __restrict__ ec, double* __restrict__ x, int b) {
+  griddep_wait();
   const int i = blockIdx.x * 8 + threadIdx.y;
   const int q = blockIdx.y * 32 + threadIdx.x;
   if (i >= P.n_rows || q >= b) return;
@@ -218,6 +233,7 @@ __global__ void __launch_bounds__(256) k_mvc_up2(DCsr A, const double* __restric
                                                  const double* __restrict__ r, int ldr,
                                                  const double* __restrict__ x, double* __restrict__ out,
                                                  int ldo, int b) {
+  griddep_wait();
   const int i = blockIdx.x * 8 + threadIdx.y;
   const int q = blockIdx.y * 32 + threadIdx.x;
   if (i >= A.n_rows || q >= b) return;
@@ -232,21 +248,21 @@ void mvc_down(const DLevel& L, const double* r, int ldr, double* resid, int b, c
   if (L.wideA) return mvce_down(L, r, ldr, resid, b, s);
   if (b % 2 == 0 && ldr % 2 == 0) return mvc2_down(L, r, ldr, resid, b, s);
   dim3 grid((L.n + 7) / 8, (b + 31) / 32), block(32, 8);
-  k_mvc_down<<<grid, block, 0, s>>>(L.A, L.wd, r, ldr, resid, b);
+  GNW_LAUNCH(launch_k(k_mvc_down, grid, block, 0, s, L.A, L.wd, r, ldr, resid, b));
   check_launch("mvc_down");
 }
 void mvc_restrict(const DLevel& L, const double* resid, double* rc, int b, cudaStream_t s) {
   if (L.wideR) return mvce_restrict(L, resid, rc, b, s);
   if (b % 2 == 0) return mvc2_restrict(L, resid, rc, b, s);
   dim3 grid((L.R.n_rows + 7) / 8, (b + 31) / 32), block(32, 8);
-  k_mvc_restrict<<<grid, block, 0, s>>>(L.R, resid, rc, b);
+  GNW_LAUNCH(launch_k(k_mvc_restrict, grid, block, 0, s, L.R, resid, rc, b));
   check_launch("mvc_restrict");
 }
 void mvc_up1(const DLevel& L, const double* r, int ldr, const double* ec, double* x, int b, cudaStream_t s) {
   if (L.wideP) return mvce_up1(L, r, ldr, ec, x, b, s);
   if (b % 2 == 0 && ldr % 2 == 0) return mvc2_up1(L, r, ldr, ec, x, b, s);
   dim3 grid((L.n + 7) / 8, (b + 31) / 32), block(32, 8);
-  k_mvc_up1<<<grid, block, 0, s>>>(L.P, L.wd, r, ldr, ec, x, b);
+  GNW_LAUNCH(launch_k(k_mvc_up1, grid, block, 0, s, L.P, L.wd, r, ldr, ec, x, b));
   check_launch("mvc_up1");
 }
 void mvc_up2(const DLevel& L, const double* r, int ldr, const double* x, double* out, int ldo, int b,
@@ -254,18 +270,19 @@ void mvc_up2(const DLevel& L, const double* r, int ldr, const double* x, double*
   if (L.wideA) return mvce_up2(L, r, ldr, x, out, ldo, b, s);
   if (b % 2 == 0 && ldr % 2 == 0 && ldo % 2 == 0) return mvc2_up2(L, r, ldr, x, out, ldo, b, s);
   dim3 grid((L.n + 7) / 8, (b + 31) / 32), block(32, 8);
-  k_mvc_up2<<<grid, block, 0, s>>>(L.A, L.wd, r, ldr, x, out, ldo, b);
+  GNW_LAUNCH(launch_k(k_mvc_up2, grid, block, 0, s, L.A, L.wd, r, ldr, x, out, ldo, b));
   check_launch("mvc_up2");
 }
 void mcoarse_inverse(const double* Ainv, int n, const double* r, double* x, int b, cudaStream_t s) {
   const long long threads = static_cast<long long>(n) * b * 32;
-  k_coarse_inverse<<<grid_for(threads), kTpb, 0, s>>>(Ainv, n, vfixed(const_cast<double*>(r)), x, nullptr, b);
+  GNW_LAUNCH(launch_k(k_coarse_inverse, grid_for(threads), kTpb, 0, s, Ainv, n, vfixed(const_cast<double*>(r)), x, nullptr, b));
   check_launch("mcoarse_inverse");
 }
 
 // rows [r0, r0+b) of A (row-major, `cols` columns) -> X[c * b + q]
 __global__ void k_transpose_rows_to_batch(const double* __restrict__ A, long long cols, long long ld, int r0, int b,
                                           double* __restrict__ X) {
+  griddep_wait();
   __shared__ double tile[32][33];
   const long long c0 = static_cast<long long>(blockIdx.x) * 32;
   const int q0 = blockIdx.y * 32;
@@ -284,6 +301,7 @@ __global__ void k_transpose_rows_to_batch(const double* __restrict__ A, long lon
 
 __global__ void k_transpose_batch_to_rows(const double* __restrict__ X, long long cols, long long ld, int r0, int b,
                                           double* __restrict__ A) {
+  griddep_wait();
   __shared__ double tile[32][33];
   const long long c0 = static_cast<long long>(blockIdx.x) * 32;
   const int q0 = blockIdx.y * 32;
@@ -303,13 +321,13 @@ __global__ void k_transpose_batch_to_rows(const double* __restrict__ X, long lon
 void transpose_rows_to_batch(const double* A, long long cols, long long ld, int r0, int b, double* X,
                              cudaStream_t s) {
   dim3 grid(static_cast<unsigned>((cols + 31) / 32), (b + 31) / 32), block(32, 8);
-  k_transpose_rows_to_batch<<<grid, block, 0, s>>>(A, cols, ld, r0, b, X);
+  GNW_LAUNCH(launch_k(k_transpose_rows_to_batch, grid, block, 0, s, A, cols, ld, r0, b, X));
   check_launch("transpose_rows_to_batch");
 }
 void transpose_batch_to_rows(const double* X, long long cols, long long ld, int r0, int b, double* A,
                              cudaStream_t s) {
   dim3 grid(static_cast<unsigned>((cols + 31) / 32), (b + 31) / 32), block(32, 8);
-  k_transpose_batch_to_rows<<<grid, block, 0, s>>>(X, cols, ld, r0, b, A);
+  GNW_LAUNCH(launch_k(k_transpose_batch_to_rows, grid, block, 0, s, X, cols, ld, r0, b, A));
   check_launch("transpose_batch_to_rows");
 }
 
@@ -376,6 +394,7 @@ __global__ void __launch_bounds__(kTpb) k_row_gemv(const double* __restrict__ A,
                                                    long long xoff, int scaled, const MinresState* st,
                                                    double* __restrict__ partial, unsigned* counter,
                                                    double* __restrict__ out, int chunk) {
+  griddep_wait();
   extern __shared__ double xsm[];
   const double* __restrict__ x = vsel(xs, st) + xoff;
   const double sc = scaled ? st->inv_gamma : 1.0;
@@ -419,8 +438,8 @@ void row_gemv(const double* A, int m, long long N, long long ld, VSel x, long lo
               const MinresState* st, double* partial, unsigned* counter, double* out, const RowGemv& plan,
               cudaStream_t s) {
   const dim3 grid(plan.nchunks, (m + kRowsPerCta - 1) / kRowsPerCta);
-  k_row_gemv<<<grid, kTpb, plan.chunk * sizeof(double), s>>>(A, m, N, ld, x, x_off, scaled, st, partial, counter, out,
-                                                             plan.chunk);
+  GNW_LAUNCH(launch_k(k_row_gemv, grid, kTpb, plan.chunk * sizeof(double), s, A, m, N, ld, x, x_off, scaled, st, partial, counter, out,
+                                                             plan.chunk));
   check_launch("row_gemv");
 }
 
@@ -430,6 +449,7 @@ void row_gemv(const double* A, int m, long long N, long long ld, VSel x, long lo
 __global__ void __launch_bounds__(kTpb) k_saddle(OperatorArgs op, VSel xs, int scaled, const double* __restrict__ u,
                                                  VSel ys, MinresState* st, int loop, int nb_edge,
                                                  double* part, unsigned* counter) {
+  griddep_wait();
   extern __shared__ double usm[];
   __shared__ double red[kTpb / 32];
   const double* __restrict__ z = vsel(xs, st);
@@ -498,8 +518,8 @@ __global__ void __launch_bounds__(kTpb) k_saddle(OperatorArgs op, VSel xs, int s
 void saddle_operator(const OperatorArgs& op, VSel x, int scaled, const double* u, VSel y, MinresState* st,
                      int loop, double* partial, unsigned* counter, cudaStream_t s) {
   const int nbe = static_cast<int>(grid_for(op.K)), nbc = static_cast<int>(grid_for(op.N));
-  k_saddle<<<nbe + nbc, kTpb, std::max(op.m, 1) * sizeof(double), s>>>(op, x, scaled, u, y, st, loop, nbe,
-                                                                       partial, counter);
+  GNW_LAUNCH(launch_k(k_saddle, nbe + nbc, kTpb, std::max(op.m, 1) * sizeof(double), s, op, x, scaled, u, y, st, loop, nbe,
+                                                                       partial, counter));
   check_launch("saddle_operator");
 }
 
@@ -512,6 +532,7 @@ void saddle_operator(const OperatorArgs& op, VSel x, int scaled, const double* u
 __global__ void __launch_bounds__(kTpb) k_combine_elem(PrecArgs pa, VSel azs, VSel vcs, VSel vps, VSel vns,
                                                        VSel zns, int loop, const MinresState* st,
                                                        double* dots_part) {
+  griddep_wait();
   __shared__ double red[3 * (kTpb / 32)];
   const double* __restrict__ az = vsel(azs, st);
   double* __restrict__ vn = vsel(vns, st);
@@ -548,7 +569,7 @@ int combine_blocks(long long K, long long N) { return static_cast<int>(grid_for(
 void combine_precondition(const PrecArgs& pa, VSel az, VSel vcur, VSel vprev, VSel vnext, VSel znext, int loop,
                           MinresState* st, double* /*vcopy*/, double* dots_part, double* t_part,
                           unsigned* counter, double* t_out, const RowGemv& plan, cudaStream_t s) {
-  k_combine_elem<<<combine_blocks(pa.K, pa.N), kTpb, 0, s>>>(pa, az, vcur, vprev, vnext, znext, loop, st, dots_part);
+  GNW_LAUNCH(launch_k(k_combine_elem, combine_blocks(pa.K, pa.N), kTpb, 0, s, pa, az, vcur, vprev, vnext, znext, loop, st, dots_part));
   check_launch("combine_elem");
   if (pa.m > 0)  // t = H^T v2 (matvec_transpose(h_hat, y2), inversion.cpp:82): row GEMV over Ht
     row_gemv(pa.Ht, pa.m, pa.N, pa.ldh, vnext, pa.K, 0, st, t_part, counter, t_out, plan, s);
@@ -557,6 +578,7 @@ void combine_precondition(const PrecArgs& pa, VSel az, VSel vcur, VSel vprev, VS
 // t2 = Cinv t, warp per row
 __global__ void k_cinv_apply(const double* __restrict__ Cinv, const double* __restrict__ t, double* __restrict__ t2,
                              int m) {
+  griddep_wait();
   const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   if (w >= m) return;
   double acc[1] = {0.0};
@@ -568,9 +590,9 @@ __global__ void k_cinv_apply(const double* __restrict__ Cinv, const double* __re
 void capacitance_solve(const PrecArgs& pa, const double* t, double* t2, cudaStream_t s) {
   if (pa.m == 0) return;
   if (pa.exact) {
-    k_coarse_cholesky<<<1, 64, 0, s>>>(pa.Lc, pa.m, vfixed(const_cast<double*>(t)), t2, nullptr, 1, 1);
+    GNW_LAUNCH(launch_k(k_coarse_cholesky, 1, 64, 0, s, pa.Lc, pa.m, vfixed(const_cast<double*>(t)), t2, nullptr, 1, 1));
   } else {
-    k_cinv_apply<<<grid_for(static_cast<long long>(pa.m) * 32), kTpb, 0, s>>>(pa.Cinv, t, t2, pa.m);
+    GNW_LAUNCH(launch_k(k_cinv_apply, grid_for(static_cast<long long>(pa.m) * 32), kTpb, 0, s, pa.Cinv, t, t2, pa.m));
   }
   check_launch("capacitance_solve");
 }
@@ -579,6 +601,7 @@ __global__ void __launch_bounds__(kTpb) k_finish_prec(PrecArgs pa, const double*
                                                       const double* __restrict__ t2, VSel vns, VSel zns, int loop,
                                                       MinresState* st, const double* __restrict__ dots_edge,
                                                       int n_edge_blocks, double* part, unsigned* counter) {
+  griddep_wait();
   extern __shared__ double tsm[];
   __shared__ double red[3 * (kTpb / 32)];
   const double* __restrict__ vn = vsel(vns, st);
@@ -658,8 +681,8 @@ __global__ void __launch_bounds__(kTpb) k_finish_prec(PrecArgs pa, const double*
 void finish_precondition(const PrecArgs& pa, const double* svc, const double* t2, VSel vnext, VSel znext, int loop,
                          MinresState* st, const double* dots_edge, int n_edge_blocks, double* part,
                          unsigned* counter, cudaStream_t s) {
-  k_finish_prec<<<grid_for(pa.N), kTpb, std::max(pa.m, 1) * sizeof(double), s>>>(
-      pa, svc, t2, vnext, znext, loop, st, dots_edge, n_edge_blocks, part, counter);
+  GNW_LAUNCH(launch_k(k_finish_prec, grid_for(pa.N), kTpb, std::max(pa.m, 1) * sizeof(double), s, 
+      pa, svc, t2, vnext, znext, loop, st, dots_edge, n_edge_blocks, part, counter));
   check_launch("finish_precondition");
 }
 
@@ -672,6 +695,7 @@ __global__ void __launch_bounds__(kTpb) k_minres_update(long long n, VSel zs, VS
                                                         double* hist_e, double* hist_p, long long hist_cap,
                                                         double* part, unsigned* counter,
                                                         cudaGraphConditionalHandle handle, int use_cond) {
+  griddep_wait();
   __shared__ double red[kTpb / 32];
   if (use_cond != 2 && st->status != kRunning) {  // use_cond == 2: isolated timing, no loop control
     if (use_cond && blockIdx.x == 0 && threadIdx.x == 0) cudaGraphSetConditional(handle, 0);
@@ -736,13 +760,14 @@ void minres_update(long long n, VSel z, VSel az, VSel wprev, VSel wcur, VSel wne
                    double* x, double* r, MinresState* st, double* hist_e, double* hist_p, long long hist_cap,
                    double* part, unsigned* counter, unsigned long long cond_handle, int use_cond, cudaStream_t s) {
   const unsigned grid = std::min<unsigned>(grid_for(n), 148u * 8u);
-  k_minres_update<<<grid, kTpb, 0, s>>>(n, z, az, wprev, wcur, wnext, uprev, ucur, unext, x, r, st, hist_e, hist_p,
+  GNW_LAUNCH(launch_k(k_minres_update, grid, kTpb, 0, s, n, z, az, wprev, wcur, wnext, uprev, ucur, unext, x, r, st, hist_e, hist_p,
                                         hist_cap, part, counter,
-                                        static_cast<cudaGraphConditionalHandle>(cond_handle), use_cond);
+                                        static_cast<cudaGraphConditionalHandle>(cond_handle), use_cond));
   check_launch("minres_update");
 }
 
 __global__ void k_minres_rotate(MinresState* st) {
+  griddep_wait();
   st->gamma_prev = st->gamma_cur;
   st->gamma_cur = st->gamma_next;
   st->c_prev = st->c_cur;
@@ -755,13 +780,14 @@ __global__ void k_minres_rotate(MinresState* st) {
 }
 
 void minres_rotate(MinresState* st, cudaStream_t s) {
-  k_minres_rotate<<<1, 1, 0, s>>>(st);
+  GNW_LAUNCH(launch_k(k_minres_rotate, 1, 1, 0, s, st));
   check_launch("minres_rotate");
 }
 
 __global__ void __launch_bounds__(kTpb) k_residual(long long n, const double* __restrict__ b,
                                                    const double* __restrict__ y, double* __restrict__ r,
                                                    MinresState* st, int want_b, double* part, unsigned* counter) {
+  griddep_wait();
   __shared__ double red[2 * (kTpb / 32)];
   double v[2] = {0.0, 0.0};
   for (long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
@@ -781,12 +807,13 @@ __global__ void __launch_bounds__(kTpb) k_residual(long long n, const double* __
 void residual(long long n, const double* b, const double* y, double* r, MinresState* st, int want_b, double* part,
               unsigned* counter, cudaStream_t s) {
   const unsigned grid = std::min<unsigned>(grid_for(n), 148u * 8u);
-  k_residual<<<grid, kTpb, 0, s>>>(n, b, y, r, st, want_b, part, counter);
+  GNW_LAUNCH(launch_k(k_residual, grid, kTpb, 0, s, n, b, y, r, st, want_b, part, counter));
   check_launch("residual");
 }
 
 __global__ void __launch_bounds__(kTpb) k_dot(long long n, const double* __restrict__ a, const double* __restrict__ b,
                                               double* out, double* part, unsigned* counter) {
+  griddep_wait();
   __shared__ double red[kTpb / 32];
   double v[1] = {0.0};
   for (long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
@@ -798,7 +825,7 @@ __global__ void __launch_bounds__(kTpb) k_dot(long long n, const double* __restr
 
 void dot(long long n, const double* a, const double* b, double* out, double* part, unsigned* counter, cudaStream_t s) {
   const unsigned grid = std::min<unsigned>(grid_for(n), 148u * 8u);
-  k_dot<<<grid, kTpb, 0, s>>>(n, a, b, out, part, counter);
+  GNW_LAUNCH(launch_k(k_dot, grid, kTpb, 0, s, n, a, b, out, part, counter));
   check_launch("dot");
 }
 
@@ -806,6 +833,7 @@ void dot(long long n, const double* a, const double* b, double* out, double* par
 __global__ void __launch_bounds__(kTpb) k_rhs(OperatorArgs op, double beta, const double* __restrict__ mdl,
                                               const double* __restrict__ mref, const double* __restrict__ dg,
                                               double* __restrict__ rhs, int nb_edge) {
+  griddep_wait();
   extern __shared__ double gsm[];
   if (static_cast<int>(blockIdx.x) < nb_edge) {
     const long long e = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -832,7 +860,7 @@ __global__ void __launch_bounds__(kTpb) k_rhs(OperatorArgs op, double beta, cons
 void assemble_rhs(const OperatorArgs& op, double beta, const double* mdl, const double* mref, const double* dg,
                   double* rhs, cudaStream_t s) {
   const int nbe = static_cast<int>(grid_for(op.K)), nbc = static_cast<int>(grid_for(op.N));
-  k_rhs<<<nbe + nbc, kTpb, std::max(op.m, 1) * sizeof(double), s>>>(op, beta, mdl, mref, dg, rhs, nbe);
+  GNW_LAUNCH(launch_k(k_rhs, nbe + nbc, kTpb, std::max(op.m, 1) * sizeof(double), s, op, beta, mdl, mref, dg, rhs, nbe));
   check_launch("assemble_rhs");
 }
 
@@ -867,6 +895,7 @@ __global__ void __launch_bounds__(256, 1) k_dgemm_nt(const double* __restrict__ 
                                                      const double* __restrict__ B, long long ldb, int m,
                                                      long long N, long long kchunk, const int2* __restrict__ pairs,
                                                      int npairs, double* __restrict__ part) {
+  griddep_wait();
   using namespace dg;
   extern __shared__ __align__(16) double sm[];
   double* As = sm;                            // [STAGES][BM][LDS]
@@ -951,6 +980,7 @@ __global__ void __launch_bounds__(256, 1) k_dgemm_nt(const double* __restrict__ 
 // C[i][j] = (sum_split part) / beta (+1 on the diagonal)   inversion.cpp:37-43
 __global__ void k_dgemm_finalize(const double* __restrict__ part, const int2* __restrict__ pairs, int npairs,
                                  int splits, int m, double beta, double* __restrict__ C) {
+  griddep_wait();
   using namespace dg;
   const int p = blockIdx.y;
   const int e = blockIdx.x * blockDim.x + threadIdx.x;
@@ -999,10 +1029,10 @@ void capacitance_dgemm(const double* J, long long ldj, const double* Ht, long lo
     attr_set = true;
   }
   dim3 grid(plan.npairs, plan.splits);
-  k_dgemm_nt<<<grid, 256, dg::SMEM, s>>>(J, ldj, Ht, ldh, m, N, plan.kchunk, dpairs, plan.npairs, part);
+  GNW_LAUNCH(launch_k(k_dgemm_nt, grid, 256, dg::SMEM, s, J, ldj, Ht, ldh, m, N, plan.kchunk, dpairs, plan.npairs, part));
   check_launch("dgemm_nt");
   dim3 g2((dg::BM * dg::BN + 255) / 256, plan.npairs);
-  k_dgemm_finalize<<<g2, 256, 0, s>>>(part, dpairs, plan.npairs, plan.splits, m, beta, C);
+  GNW_LAUNCH(launch_k(k_dgemm_finalize, g2, 256, 0, s, part, dpairs, plan.npairs, plan.splits, m, beta, C));
   check_launch("dgemm_finalize");
 }
 
@@ -1011,6 +1041,7 @@ void capacitance_dgemm(const double* J, long long ldj, const double* Ht, long lo
 // ======================================================================
 __global__ void __launch_bounds__(1024) k_cholesky(const double* __restrict__ C, double* __restrict__ L, int n,
                                                    int* fail) {
+  griddep_wait();
   __shared__ double ljj_s;
   __shared__ int bad;
   if (threadIdx.x == 0) bad = 0;
@@ -1047,11 +1078,12 @@ __global__ void __launch_bounds__(1024) k_cholesky(const double* __restrict__ C,
 }
 
 void cholesky(const double* C, double* L, int n, int* fail, cudaStream_t s) {
-  k_cholesky<<<1, 1024, 0, s>>>(C, L, n, fail);
+  GNW_LAUNCH(launch_k(k_cholesky, 1, 1024, 0, s, C, L, n, fail));
   check_launch("cholesky");
 }
 
 __global__ void k_symmetrize(double* C, int n) {
+  griddep_wait();
   const long long t = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (t >= static_cast<long long>(n) * n) return;
   const int i = static_cast<int>(t / n), j = static_cast<int>(t % n);
@@ -1062,12 +1094,13 @@ __global__ void k_symmetrize(double* C, int n) {
 }
 
 void symmetrize(double* C, int n, cudaStream_t s) {
-  k_symmetrize<<<grid_for(static_cast<long long>(n) * n), kTpb, 0, s>>>(C, n);
+  GNW_LAUNCH(launch_k(k_symmetrize, grid_for(static_cast<long long>(n) * n), kTpb, 0, s, C, n));
   check_launch("symmetrize");
 }
 
 // Y = L^-1 (thread per column), then Cinv = Y^T Y
 __global__ void k_trinv(const double* __restrict__ L, double* __restrict__ Y, int n) {
+  griddep_wait();
   const int j = blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= n) return;
   for (int i = 0; i < j; ++i) Y[static_cast<long long>(i) * n + j] = 0.0;
@@ -1079,6 +1112,7 @@ __global__ void k_trinv(const double* __restrict__ L, double* __restrict__ Y, in
 }
 
 __global__ void k_syrk_tn(const double* __restrict__ Y, double* __restrict__ Cinv, int n) {
+  griddep_wait();
   const int j = blockIdx.x * blockDim.x + threadIdx.x, i = blockIdx.y;
   if (j >= n || j > i) return;
   double s = 0.0;
@@ -1092,11 +1126,12 @@ __global__ void k_syrk_tn(const double* __restrict__ Y, double* __restrict__ Cin
 void cholesky_inverse(const double* L, double* Y, double* Cinv, int n, cudaStream_t s) {
   trinv_blocked(L, Y, n, s);
   dim3 grid(grid_for(n, 128), n);
-  k_syrk_tn<<<grid, 128, 0, s>>>(Y, Cinv, n);
+  GNW_LAUNCH(launch_k(k_syrk_tn, grid, 128, 0, s, Y, Cinv, n));
   check_launch("syrk_tn");
 }
 
 __global__ void k_fill_zero(double* p, long long n) {
+  griddep_wait();
   for (long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
        i += static_cast<long long>(gridDim.x) * blockDim.x)
     p[i] = 0.0;
@@ -1104,7 +1139,7 @@ __global__ void k_fill_zero(double* p, long long n) {
 
 void fill_zero(double* p, long long n, cudaStream_t s) {
   if (n <= 0) return;
-  k_fill_zero<<<std::min<unsigned>(grid_for(n), 148u * 16u), kTpb, 0, s>>>(p, n);
+  GNW_LAUNCH(launch_k(k_fill_zero, std::min<unsigned>(grid_for(n), 148u * 16u), kTpb, 0, s, p, n));
   check_launch("fill_zero");
 }
 

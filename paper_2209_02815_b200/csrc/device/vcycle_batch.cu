@@ -23,6 +23,7 @@ __device__ __forceinline__ void st2(double* p, double2 v) { *reinterpret_cast<do
 __global__ void __launch_bounds__(256) k_mvc2_down(DCsr A, const double* __restrict__ wd,
                                                    const double* __restrict__ r, int ldr,
                                                    double* __restrict__ resid, int b) {
+  griddep_wait();
   const int i = blockIdx.x * 8 + threadIdx.y;
   const int q = 2 * (blockIdx.y * 32 + threadIdx.x);
   if (i >= A.n_rows || q >= b) return;
@@ -42,6 +43,7 @@ __global__ void __launch_bounds__(256) k_mvc2_down(DCsr A, const double* __restr
 
 __global__ void __launch_bounds__(256) k_mvc2_restrict(DCsr R, const double* __restrict__ resid,
                                                        double* __restrict__ rc, int b) {
+  griddep_wait();
   const int a = blockIdx.x * 8 + threadIdx.y;
   const int q = 2 * (blockIdx.y * 32 + threadIdx.x);
   if (a >= R.n_rows || q >= b) return;
@@ -61,6 +63,7 @@ __global__ void __launch_bounds__(256) k_mvc2_restrict(DCsr R, const double* __r
 __global__ void __launch_bounds__(256) k_mvc2_up1(DCsr P, const double* __restrict__ wd,
                                                   const double* __restrict__ r, int ldr,
                                                   const double* __restrict__ ec, double* __restrict__ x, int b) {
+  griddep_wait();
   const int i = blockIdx.x * 8 + threadIdx.y;
   const int q = 2 * (blockIdx.y * 32 + threadIdx.x);
   if (i >= P.n_rows || q >= b) return;
@@ -83,6 +86,7 @@ __global__ void __launch_bounds__(256) k_mvc2_up2(DCsr A, const double* __restri
                                                   const double* __restrict__ r, int ldr,
                                                   const double* __restrict__ x, double* __restrict__ out,
                                                   int ldo, int b) {
+  griddep_wait();
   const int i = blockIdx.x * 8 + threadIdx.y;
   const int q = 2 * (blockIdx.y * 32 + threadIdx.x);
   if (i >= A.n_rows || q >= b) return;
@@ -106,20 +110,20 @@ __global__ void __launch_bounds__(256) k_mvc2_up2(DCsr A, const double* __restri
 static dim3 grid2(int rows, int b) { return dim3((rows + 7) / 8, (b / 2 + 31) / 32); }
 
 void mvc2_down(const DLevel& L, const double* r, int ldr, double* resid, int b, cudaStream_t s) {
-  k_mvc2_down<<<grid2(L.n, b), dim3(32, 8), 0, s>>>(L.A, L.wd, r, ldr, resid, b);
+  GNW_LAUNCH(launch_k(k_mvc2_down, grid2(L.n, b), dim3(32, 8), 0, s, L.A, L.wd, r, ldr, resid, b));
   note_launch("mvc2_down");
 }
 void mvc2_restrict(const DLevel& L, const double* resid, double* rc, int b, cudaStream_t s) {
-  k_mvc2_restrict<<<grid2(L.R.n_rows, b), dim3(32, 8), 0, s>>>(L.R, resid, rc, b);
+  GNW_LAUNCH(launch_k(k_mvc2_restrict, grid2(L.R.n_rows, b), dim3(32, 8), 0, s, L.R, resid, rc, b));
   note_launch("mvc2_restrict");
 }
 void mvc2_up1(const DLevel& L, const double* r, int ldr, const double* ec, double* x, int b, cudaStream_t s) {
-  k_mvc2_up1<<<grid2(L.n, b), dim3(32, 8), 0, s>>>(L.P, L.wd, r, ldr, ec, x, b);
+  GNW_LAUNCH(launch_k(k_mvc2_up1, grid2(L.n, b), dim3(32, 8), 0, s, L.P, L.wd, r, ldr, ec, x, b));
   note_launch("mvc2_up1");
 }
 void mvc2_up2(const DLevel& L, const double* r, int ldr, const double* x, double* out, int ldo, int b,
               cudaStream_t s) {
-  k_mvc2_up2<<<grid2(L.n, b), dim3(32, 8), 0, s>>>(L.A, L.wd, r, ldr, x, out, ldo, b);
+  GNW_LAUNCH(launch_k(k_mvc2_up2, grid2(L.n, b), dim3(32, 8), 0, s, L.A, L.wd, r, ldr, x, out, ldo, b));
   note_launch("mvc2_up2");
 }
 

@@ -67,6 +67,7 @@ constexpr int kRowsPerBlock = 8;  // 8 warps, one row each
 // --------------------------------------------------------------- single RHS
 __global__ void __launch_bounds__(256) k_vcw_down(DCsr A, const double* __restrict__ wd, VSel rs,
                                                   double* __restrict__ resid, const MinresState* st) {
+  griddep_wait();
   const double* __restrict__ r = vsel(rs, st);
   const int i = blockIdx.x * kRowsPerBlock + (threadIdx.x >> 5), lane = threadIdx.x & 31;
   if (i >= A.n_rows) return;
@@ -76,6 +77,7 @@ __global__ void __launch_bounds__(256) k_vcw_down(DCsr A, const double* __restri
 
 __global__ void __launch_bounds__(256) k_vcw_restrict(DCsr R, const double* __restrict__ resid,
                                                       double* __restrict__ rc) {
+  griddep_wait();
   const int a = blockIdx.x * kRowsPerBlock + (threadIdx.x >> 5), lane = threadIdx.x & 31;
   if (a >= R.n_rows) return;
   const double s = warp_row(R, a, lane, [&](int c) { return resid[c]; });
@@ -85,6 +87,7 @@ __global__ void __launch_bounds__(256) k_vcw_restrict(DCsr R, const double* __re
 __global__ void __launch_bounds__(256) k_vcw_up1(DCsr P, const double* __restrict__ wd, VSel rs,
                                                  const double* __restrict__ ec, double* __restrict__ x,
                                                  const MinresState* st) {
+  griddep_wait();
   const double* __restrict__ r = vsel(rs, st);
   const int i = blockIdx.x * kRowsPerBlock + (threadIdx.x >> 5), lane = threadIdx.x & 31;
   if (i >= P.n_rows) return;
@@ -95,6 +98,7 @@ __global__ void __launch_bounds__(256) k_vcw_up1(DCsr P, const double* __restric
 __global__ void __launch_bounds__(256) k_vcw_up2(DCsr A, const double* __restrict__ wd, VSel rs,
                                                  const double* __restrict__ x, double* __restrict__ out,
                                                  const MinresState* st) {
+  griddep_wait();
   const double* __restrict__ r = vsel(rs, st);
   const int i = blockIdx.x * kRowsPerBlock + (threadIdx.x >> 5), lane = threadIdx.x & 31;
   if (i >= A.n_rows) return;
@@ -109,6 +113,7 @@ __global__ void __launch_bounds__(256) k_vcw_up2(DCsr A, const double* __restric
 __global__ void __launch_bounds__(256) k_mvce_down(DCsr A, const double* __restrict__ wd,
                                                    const double* __restrict__ r, int ldr,
                                                    double* __restrict__ resid, int b) {
+  griddep_wait();
   const int i = blockIdx.x * 8 + threadIdx.y;
   const int q = blockIdx.y * 32 + threadIdx.x;
   if (i >= A.n_rows || q >= b) return;
@@ -118,6 +123,7 @@ __global__ void __launch_bounds__(256) k_mvce_down(DCsr A, const double* __restr
 
 __global__ void __launch_bounds__(256) k_mvce_restrict(DCsr R, const double* __restrict__ resid,
                                                        double* __restrict__ rc, int b) {
+  griddep_wait();
   const int a = blockIdx.x * 8 + threadIdx.y;
   const int q = blockIdx.y * 32 + threadIdx.x;
   if (a >= R.n_rows || q >= b) return;
@@ -127,6 +133,7 @@ __global__ void __launch_bounds__(256) k_mvce_restrict(DCsr R, const double* __r
 __global__ void __launch_bounds__(256) k_mvce_up1(DCsr P, const double* __restrict__ wd,
                                                   const double* __restrict__ r, int ldr,
                                                   const double* __restrict__ ec, double* __restrict__ x, int b) {
+  griddep_wait();
   const int i = blockIdx.x * 8 + threadIdx.y;
   const int q = blockIdx.y * 32 + threadIdx.x;
   if (i >= P.n_rows || q >= b) return;
@@ -138,6 +145,7 @@ __global__ void __launch_bounds__(256) k_mvce_up2(DCsr A, const double* __restri
                                                   const double* __restrict__ r, int ldr,
                                                   const double* __restrict__ x, double* __restrict__ out,
                                                   int ldo, int b) {
+  griddep_wait();
   const int i = blockIdx.x * 8 + threadIdx.y;
   const int q = blockIdx.y * 32 + threadIdx.x;
   if (i >= A.n_rows || q >= b) return;
@@ -150,40 +158,40 @@ __global__ void __launch_bounds__(256) k_mvce_up2(DCsr A, const double* __restri
 static unsigned wgrid(int rows) { return static_cast<unsigned>((rows + kRowsPerBlock - 1) / kRowsPerBlock); }
 
 void vcw_down(const DLevel& L, VSel r, double* resid, const MinresState* st, cudaStream_t s) {
-  k_vcw_down<<<wgrid(L.n), 256, 0, s>>>(L.A, L.wd, r, resid, st);
+  GNW_LAUNCH(launch_k(k_vcw_down, wgrid(L.n), 256, 0, s, L.A, L.wd, r, resid, st));
   note_launch("vcw_down");
 }
 void vcw_restrict(const DLevel& L, const double* resid, double* rc, cudaStream_t s) {
-  k_vcw_restrict<<<wgrid(L.R.n_rows), 256, 0, s>>>(L.R, resid, rc);
+  GNW_LAUNCH(launch_k(k_vcw_restrict, wgrid(L.R.n_rows), 256, 0, s, L.R, resid, rc));
   note_launch("vcw_restrict");
 }
 void vcw_up1(const DLevel& L, VSel r, const double* ec, double* x, const MinresState* st, cudaStream_t s) {
-  k_vcw_up1<<<wgrid(L.n), 256, 0, s>>>(L.P, L.wd, r, ec, x, st);
+  GNW_LAUNCH(launch_k(k_vcw_up1, wgrid(L.n), 256, 0, s, L.P, L.wd, r, ec, x, st));
   note_launch("vcw_up1");
 }
 void vcw_up2(const DLevel& L, VSel r, const double* x, double* out, const MinresState* st, cudaStream_t s) {
-  k_vcw_up2<<<wgrid(L.n), 256, 0, s>>>(L.A, L.wd, r, x, out, st);
+  GNW_LAUNCH(launch_k(k_vcw_up2, wgrid(L.n), 256, 0, s, L.A, L.wd, r, x, out, st));
   note_launch("vcw_up2");
 }
 void mvce_down(const DLevel& L, const double* r, int ldr, double* resid, int b, cudaStream_t s) {
   dim3 grid((L.n + 7) / 8, (b + 31) / 32), block(32, 8);
-  k_mvce_down<<<grid, block, 0, s>>>(L.A, L.wd, r, ldr, resid, b);
+  GNW_LAUNCH(launch_k(k_mvce_down, grid, block, 0, s, L.A, L.wd, r, ldr, resid, b));
   note_launch("mvce_down");
 }
 void mvce_restrict(const DLevel& L, const double* resid, double* rc, int b, cudaStream_t s) {
   dim3 grid((L.R.n_rows + 7) / 8, (b + 31) / 32), block(32, 8);
-  k_mvce_restrict<<<grid, block, 0, s>>>(L.R, resid, rc, b);
+  GNW_LAUNCH(launch_k(k_mvce_restrict, grid, block, 0, s, L.R, resid, rc, b));
   note_launch("mvce_restrict");
 }
 void mvce_up1(const DLevel& L, const double* r, int ldr, const double* ec, double* x, int b, cudaStream_t s) {
   dim3 grid((L.n + 7) / 8, (b + 31) / 32), block(32, 8);
-  k_mvce_up1<<<grid, block, 0, s>>>(L.P, L.wd, r, ldr, ec, x, b);
+  GNW_LAUNCH(launch_k(k_mvce_up1, grid, block, 0, s, L.P, L.wd, r, ldr, ec, x, b));
   note_launch("mvce_up1");
 }
 void mvce_up2(const DLevel& L, const double* r, int ldr, const double* x, double* out, int ldo, int b,
               cudaStream_t s) {
   dim3 grid((L.n + 7) / 8, (b + 31) / 32), block(32, 8);
-  k_mvce_up2<<<grid, block, 0, s>>>(L.A, L.wd, r, ldr, x, out, ldo, b);
+  GNW_LAUNCH(launch_k(k_mvce_up2, grid, block, 0, s, L.A, L.wd, r, ldr, x, out, ldo, b));
   note_launch("mvce_up2");
 }
 
