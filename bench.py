@@ -51,6 +51,25 @@ def dist_env():
     return ws, rank, local
 
 
+def max_over_ranks_dist(x: float, ws: int) -> float:
+    """Max of a per-rank device time over all ranks (NCCL on GPUs, gloo on CPU)."""
+    if ws == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+
+    dev = "cuda" if dist.get_backend() == "nccl" else "cpu"
+    t = torch.tensor([x], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def replica_throughput(elapsed_local: float, steps: int, ws: int) -> tuple[float, float]:
+    """Whole-job solves/s of N independent replicas: N * steps / (max over ranks of the time)."""
+    el = max_over_ranks_dist(elapsed_local, ws)
+    return ws * steps / el, el
+
+
 def peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -212,11 +231,7 @@ def run_gnw(args):
         torch.cuda.synchronize()
 
     def max_over_ranks(x: float) -> float:
-        if ws == 1:
-            return x
-        t = torch.tensor([x], dtype=torch.float64, device="cuda")
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        return float(t.item())
+        return max_over_ranks_dist(x, ws)
 
     # ---------------------------------------------------------- device-resident arm
     ctx.use_device_pointers(True)
@@ -252,8 +267,7 @@ def run_gnw(args):
     elapsed = ctx.event_elapsed(0, 1)
     clk.mark()
     barrier()
-    elapsed = max_over_ranks(elapsed)
-    value = ws * args.steps / elapsed
+    value, elapsed = replica_throughput(elapsed, args.steps, ws)
 
     # ---------------------------------------------------------------- e2e arm
     ctx.use_device_pointers(False)

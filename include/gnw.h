@@ -170,6 +170,34 @@ gnw_status gnw_export_mesh(const gnw_ctx* ctx, int64_t* cells, int64_t* edges,
 /* dense_cholesky on device (linalg.cpp:88-105), operation order preserved. */
 gnw_status gnw_dense_cholesky(gnw_ctx* ctx, uint64_t n, const double* C, double* L);
 
+/* ---------------------------------------------------------------- ERT (C4/C5)
+ * ElectrodeConfig (survey.hpp:15-21): current electrodes a, b (b = -1: pole at
+ * infinity), receiver dipole m, n, geometric factor k.  Electrode indices refer
+ * to the node list given to gnw_set_electrodes (Mesh::electrode_nodes). */
+typedef struct gnw_ert_config {
+  int64_t a, b, m, n;
+  double k;
+} gnw_ert_config;
+
+typedef struct gnw_ert_stats {
+  double t_assemble;  /* host: P1 stiffness values (assemble_forward, forward.cpp:58-80) */
+  double t_amg;       /* host: amg_setup of the stiffness + upload */
+  double t_solve;     /* device: batched PCG unit-pole solves (solve_unit_pole, forward.cpp:83-98) */
+  double t_jacobian;  /* device: gradients, J rows and g (forward.cpp:122-167) */
+  uint64_t pcg_iterations;
+} gnw_ert_stats;
+
+/* Mesh::electrode_nodes for the assembled mesh; nodes must lie on z = 0. */
+gnw_status gnw_set_electrodes(gnw_ctx* ctx, const int64_t* nodes, uint64_t n);
+/* evaluate_response_and_jacobian (forward.hpp:40-42, forward.cpp:100-172): g (n_cfg)
+ * and J (n_cfg x N row-major) at log-conductivity m (N).  `tol` is the relative
+ * residual of the batched PCG pole solves (the reference factorises exactly). */
+gnw_status gnw_response_jacobian(gnw_ctx* ctx, const double* m, const gnw_ert_config* cfgs, uint64_t n_cfg,
+                                 double* J, double* g, double tol, gnw_ert_stats* stats);
+/* geometric_factor (survey.hpp:33-37, survey.cpp:22-46); b == NULL: pole at infinity. */
+gnw_status gnw_geometric_factor(const double a[3], const double* b, const double m[3], const double n[3], int dim,
+                                double* k);
+
 /* Device time of the last gnw_minres_solve / set_jacobian, and launch counts. */
 typedef struct gnw_stats {
   double t_minres;        /* seconds, CUDA events around the MINRES loop */

@@ -1304,3 +1304,211 @@ int orc_minres(const orc_problem* p, const double* b, const double* x0, double t
 }
 
 int orc_dense_cholesky(uint64_t n, const double* C, double* L) { return dense_cholesky(n, C, L); }
+
+/* ------------------------------------------------------------ ERT (C4/C5) */
+static double dist3(const double* p, const double* q) {
+  return sqrt((p[0] - q[0]) * (p[0] - q[0]) + (p[1] - q[1]) * (p[1] - q[1]) + (p[2] - q[2]) * (p[2] - q[2]));
+}
+
+/* geometric_factor, survey.cpp:22-46 */
+int orc_geometric_factor(const double a[3], const double* b, const double m[3], const double n[3], int dim,
+                         double* k) {
+  if (dim != 2 && dim != 3) return fail(EINV, "geometric_factor: dim must be 2 or 3");
+  const double am = dist3(a, m), an = dist3(a, n);
+  if (am == 0.0 || an == 0.0 || dist3(m, n) == 0.0 ||
+      (b && (dist3(b, m) == 0.0 || dist3(b, n) == 0.0 || dist3(a, b) == 0.0)))
+    return fail(EINV, "geometric_factor: coincident electrodes");
+  const double pi = 3.14159265358979323846;
+  double denom;
+  if (dim == 2) {
+    denom = -log(am) + log(an);
+    if (b) denom += log(dist3(b, m)) - log(dist3(b, n));
+    if (fabs(denom) < 1e-14) return fail(ENUM, "geometric_factor: degenerate configuration (zero log ratio)");
+    *k = pi / denom;
+    return 0;
+  }
+  denom = 1.0 / am - 1.0 / an;
+  if (b) denom += -1.0 / dist3(b, m) + 1.0 / dist3(b, n);
+  if (fabs(denom) < 1e-14) return fail(ENUM, "geometric_factor: degenerate configuration (zero denominator)");
+  *k = 2.0 * pi / denom;
+  return 0;
+}
+
+/* Banded LU without pivoting of an SPD CSR matrix (exact solver standing in for
+ * the reference's Eigen SparseLU, factorization.cpp:14-45). */
+typedef struct {
+  size_t n, bw;
+  double* band; /* row i holds columns [i-bw, i+bw] */
+} band_t;
+#define BAND(f, i, j) ((f)->band[(i) * (2 * (f)->bw + 1) + ((j) + (f)->bw - (i))])
+
+static int band_factor(const csr* A, band_t* f) {
+  size_t bw = 0;
+  for (size_t i = 0; i < A->n_rows; ++i)
+    for (size_t k = A->rowptr[i]; k < A->rowptr[i + 1]; ++k) {
+      size_t j = A->cols[k];
+      size_t d = j > i ? j - i : i - j;
+      if (d > bw) bw = d;
+    }
+  f->n = A->n_rows;
+  f->bw = bw;
+  f->band = xcalloc(f->n * (2 * bw + 1), sizeof(double));
+  for (size_t i = 0; i < A->n_rows; ++i)
+    for (size_t k = A->rowptr[i]; k < A->rowptr[i + 1]; ++k) BAND(f, i, A->cols[k]) += A->vals[k];
+  for (size_t k = 0; k < f->n; ++k) {
+    const double piv = BAND(f, k, k);
+    if (!(fabs(piv) > 0.0)) return fail(ENUM, "sparse_factorize: numerically singular pivot");
+    const size_t iend = k + bw + 1 < f->n ? k + bw + 1 : f->n;
+    for (size_t i = k + 1; i < iend; ++i) {
+      const double l = BAND(f, i, k) / piv;
+      if (l == 0.0) continue;
+      BAND(f, i, k) = l;
+      for (size_t j = k + 1; j < iend; ++j) BAND(f, i, j) -= l * BAND(f, k, j);
+    }
+  }
+  return 0;
+}
+
+static void band_solve(const band_t* f, double* x) {
+  for (size_t i = 0; i < f->n; ++i) {
+    const size_t j0 = i > f->bw ? i - f->bw : 0;
+    double s = x[i];
+    for (size_t j = j0; j < i; ++j) s -= BAND(f, i, j) * x[j];
+    x[i] = s;
+  }
+  for (size_t ii = f->n; ii-- > 0;) {
+    const size_t j1 = ii + f->bw + 1 < f->n ? ii + f->bw + 1 : f->n;
+    double s = x[ii];
+    for (size_t j = ii + 1; j < j1; ++j) s -= BAND(f, ii, j) * x[j];
+    x[ii] = s / BAND(f, ii, ii);
+  }
+}
+
+/* assemble_forward (forward.cpp:39-81), solve_unit_pole (:83-98) and
+ * evaluate_response_and_jacobian (:100-172) */
+int orc_response_jacobian(orc_problem* p, const int64_t* nodes, uint64_t n_nodes, const int64_t* a, const int64_t* b,
+                          const int64_t* m, const int64_t* n, const double* k, uint64_t n_cfg, const double* model,
+                          double* J, double* g) {
+  if (!p->mixed) return fail(EINV, "orc_response_jacobian: not a mixed problem");
+  const mesh_t* me = &p->mesh;
+  double scale = 0.0;
+  for (size_t i = 0; i < 2 * me->nv; ++i)
+    if (fabs(me->v[i]) > scale) scale = fabs(me->v[i]);
+  for (uint64_t e = 0; e < n_nodes; ++e)
+    if (nodes[e] < 0 || (size_t)nodes[e] >= me->nv || fabs(me->v[2 * nodes[e] + 1]) > 1e-9 * scale)
+      return fail(EINV, "evaluate_response_and_jacobian: survey electrode is not a mesh node");
+  for (uint64_t i = 0; i < n_cfg; ++i)
+    if (a[i] < 0 || (uint64_t)a[i] >= n_nodes || m[i] < 0 || (uint64_t)m[i] >= n_nodes || n[i] < 0 ||
+        (uint64_t)n[i] >= n_nodes || (b[i] != -1 && (b[i] < 0 || (uint64_t)b[i] >= n_nodes)))
+      return fail(EINV, "attach_electrode_positions: electrode index out of range");
+  /* grounded nodes: vertices of FAR boundary edges (forward.cpp:44-56) */
+  long long* n2f = xcalloc(me->nv, sizeof(long long));
+  for (size_t bi = 0; bi < me->nb; ++bi)
+    if (me->btag[bi] == 1) {
+      n2f[me->edges[2 * me->bedge[bi]]] = -1;
+      n2f[me->edges[2 * me->bedge[bi] + 1]] = -1;
+    }
+  size_t nf = 0;
+  for (size_t v = 0; v < me->nv; ++v)
+    if (n2f[v] == 0) n2f[v] = (long long)nf++;
+    else n2f[v] = -1;
+  /* cell geometry (forward.cpp:17-36) */
+  double* area = xmalloc(me->nc * sizeof(double));
+  double* grad = xmalloc(6 * me->nc * sizeof(double));
+  for (size_t c = 0; c < me->nc; ++c) {
+    const double* p0 = me->v + 2 * me->cells[3 * c];
+    const double* p1 = me->v + 2 * me->cells[3 * c + 1];
+    const double* p2 = me->v + 2 * me->cells[3 * c + 2];
+    area[c] = signed_area(p0, p1, p2);
+    const double inv2a = 1.0 / (2.0 * area[c]);
+    double* gr = grad + 6 * c;
+    gr[0] = -(p2[1] - p1[1]) * inv2a;
+    gr[1] = (p2[0] - p1[0]) * inv2a;
+    gr[2] = -(p0[1] - p2[1]) * inv2a;
+    gr[3] = (p0[0] - p2[0]) * inv2a;
+    gr[4] = -(p1[1] - p0[1]) * inv2a;
+    gr[5] = (p1[0] - p0[0]) * inv2a;
+  }
+  /* stiffness triplets (forward.cpp:58-78) */
+  triplet* t = xmalloc(9 * me->nc * sizeof(triplet));
+  size_t nt = 0;
+  for (size_t c = 0; c < me->nc; ++c) {
+    const double sigma = exp(model[c]);
+    const double* gr = grad + 6 * c;
+    for (int i = 0; i < 3; ++i) {
+      const long long fi = n2f[me->cells[3 * c + i]];
+      if (fi < 0) continue;
+      for (int j = 0; j < 3; ++j) {
+        const long long fj = n2f[me->cells[3 * c + j]];
+        if (fj < 0) continue;
+        t[nt++] = (triplet){(size_t)fi, (size_t)fj,
+                            sigma * area[c] * (gr[2 * i] * gr[2 * j] + gr[2 * i + 1] * gr[2 * j + 1])};
+      }
+    }
+  }
+  csr Kst;
+  int rc = from_triplets(nf, nf, t, nt, &Kst);
+  free(t);
+  band_t f = {0, 0, NULL};
+  if (!rc) rc = band_factor(&Kst, &f);
+  csr_free(&Kst);
+  /* used electrodes, pole solves and cellwise gradients (forward.cpp:115-143) */
+  char* used = xcalloc(n_nodes, 1);
+  for (uint64_t i = 0; i < n_cfg; ++i) {
+    used[a[i]] = used[m[i]] = used[n[i]] = 1;
+    if (b[i] != -1) used[b[i]] = 1;
+  }
+  double* gx = xcalloc(n_nodes * me->nc, sizeof(double));
+  double* gz = xcalloc(n_nodes * me->nc, sizeof(double));
+  double* rhs = xmalloc((nf ? nf : 1) * sizeof(double));
+  double* u = xmalloc(me->nv * sizeof(double));
+  for (uint64_t e = 0; e < n_nodes && !rc; ++e) {
+    if (!used[e]) continue;
+    const long long fr = n2f[nodes[e]];
+    if (fr < 0) {
+      rc = fail(EINV, "solve_unit_pole: electrode sits on the grounded boundary");
+      break;
+    }
+    memset(rhs, 0, nf * sizeof(double));
+    rhs[fr] = 1.0;
+    band_solve(&f, rhs);
+    for (size_t v = 0; v < me->nv; ++v) u[v] = n2f[v] >= 0 ? rhs[n2f[v]] : 0.0;
+    for (size_t c = 0; c < me->nc; ++c) {
+      double sx = 0.0, sz = 0.0;
+      for (int i = 0; i < 3; ++i) {
+        sx += u[me->cells[3 * c + i]] * grad[6 * c + 2 * i];
+        sz += u[me->cells[3 * c + i]] * grad[6 * c + 2 * i + 1];
+      }
+      gx[e * me->nc + c] = sx;
+      gz[e * me->nc + c] = sz;
+    }
+  }
+  /* J rows and response (forward.cpp:145-171) */
+  for (uint64_t i = 0; i < n_cfg && !rc; ++i) {
+    double gi = 0.0;
+    for (size_t c = 0; c < me->nc; ++c) {
+      double tx = gx[a[i] * me->nc + c], tz = gz[a[i] * me->nc + c];
+      if (b[i] != -1) {
+        tx -= gx[b[i] * me->nc + c];
+        tz -= gz[b[i] * me->nc + c];
+      }
+      const double rx = gx[m[i] * me->nc + c] - gx[n[i] * me->nc + c];
+      const double rz = gz[m[i] * me->nc + c] - gz[n[i] * me->nc + c];
+      const double term = k[i] * exp(model[c]) * area[c] * (tx * rx + tz * rz);
+      gi += term;
+      J[i * me->nc + c] = -term;
+    }
+    g[i] = gi;
+    if (!isfinite(gi)) rc = fail(ENUM, "evaluate_response_and_jacobian: non-finite response");
+  }
+  free(f.band);
+  free(n2f);
+  free(area);
+  free(grad);
+  free(used);
+  free(gx);
+  free(gz);
+  free(rhs);
+  free(u);
+  return rc;
+}

@@ -107,6 +107,15 @@ class Oracle:
         if rc:
             self.err(rc)
 
+    def geometric_factor(self, a, b, m, n, dim=2) -> float:
+        fn = self.L.orc_geometric_factor
+        arr = lambda v: (C.c_double * 3)(*v)
+        fn.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.POINTER(C.c_double)]
+        k = C.c_double()
+        bb = arr(b) if b is not None else None
+        self.check(fn(arr(a), bb, arr(m), arr(n), dim, C.byref(k)))
+        return k.value
+
     def dense_cholesky(self, Cm: np.ndarray) -> np.ndarray:
         Cm = np.ascontiguousarray(Cm, dtype=np.float64)
         out = np.zeros_like(Cm)
@@ -212,6 +221,20 @@ class Problem:
             self.m = J.shape[0]
         self.beta = beta
         return dict(t_H=t[0], t_C=t[1], t_chol=t[2])
+
+    def response_jacobian(self, nodes, cfgs, model):
+        """evaluate_response_and_jacobian (forward.cpp:100-172): (g, J)."""
+        fn = self.o.L.orc_response_jacobian
+        fn.argtypes = [C.c_void_p, _i64p, _u64, _i64p, _i64p, _i64p, _i64p, _dp, _u64, _dp, _dp, _dp]
+        nodes = np.ascontiguousarray(nodes, dtype=np.int64)
+        cols = [np.ascontiguousarray(cfgs[k], dtype=np.int64) for k in ("a", "b", "m", "n")]
+        kk = np.ascontiguousarray(cfgs["k"], dtype=np.float64)
+        nc = len(kk)
+        J = np.zeros((nc, self.N))
+        g = np.zeros(nc)
+        self.o.check(fn(self.h, nodes, len(nodes), *cols, kk, nc, np.ascontiguousarray(model, dtype=np.float64),
+                        J.ravel(), g))
+        return g, J
 
     def sample_gnstep(self, J: np.ndarray, beta: float, k_cols: int, k_rows: int, k_iters: int) -> dict:
         """Bounded CPU timing sample (reference library only); see orc_api.h."""

@@ -99,6 +99,16 @@ int orc_minres(const orc_problem* p, const double* b, const double* x0, double t
 int orc_sample_gnstep(orc_problem* p, const double* J, uint64_t m, double beta, uint64_t k_cols,
                       uint64_t k_rows, uint64_t k_iters, double out[4]);
 
+/* ERT forward model on the mixed problem's mesh: evaluate_response_and_jacobian
+ * (forward.cpp:100-172) with Mesh::electrode_nodes = nodes, configs (a, b, m, n, k)
+ * (b = -1: pole at infinity).  J is n_cfg x N row-major. */
+int orc_response_jacobian(orc_problem* p, const int64_t* nodes, uint64_t n_nodes, const int64_t* a,
+                          const int64_t* b, const int64_t* m, const int64_t* n, const double* k, uint64_t n_cfg,
+                          const double* model, double* J, double* g);
+/* geometric_factor (survey.cpp:22-46); b == NULL: pole at infinity. */
+int orc_geometric_factor(const double a[3], const double* b, const double m[3], const double n[3], int dim,
+                         double* k);
+
 /* Dense Cholesky (linalg.cpp:88-105): returns 2 on a non-positive pivot. */
 int orc_dense_cholesky(uint64_t n, const double* C, double* L);
 

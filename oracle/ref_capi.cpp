@@ -11,6 +11,8 @@
 
 #include "ertinv/amg.hpp"
 #include "ertinv/fem_mixed.hpp"
+#include "ertinv/forward.hpp"
+#include "ertinv/survey.hpp"
 #include "ertinv/inversion.hpp"
 #include "ertinv/linalg.hpp"
 #include "ertinv/mesh.hpp"
@@ -367,6 +369,38 @@ int orc_sample_gnstep(orc_problem* p, const double* J, uint64_t m, double beta, 
                       [&pc](std::span<const double> v) { return pc.apply(v); }, b, x0, 1e-300, k_iters);
     const double tm = std::chrono::duration<double>(Clock::now() - t0).count();
     out[3] = tm / static_cast<double>(std::max<std::size_t>(res.second.iterations, 1));
+  });
+}
+
+int orc_response_jacobian(orc_problem* p, const int64_t* nodes, uint64_t n_nodes, const int64_t* a, const int64_t* b,
+                          const int64_t* m, const int64_t* n, const double* k, uint64_t n_cfg, const double* model,
+                          double* J, double* g) {
+  return guard([&] {
+    if (!p->mixed) throw std::invalid_argument("orc_response_jacobian: not a mixed problem");
+    p->mesh.electrode_nodes.assign(nodes, nodes + n_nodes);
+    Survey survey;
+    for (uint64_t e = 0; e < n_nodes; ++e) survey.electrode_positions.push_back(p->mesh.vertices[nodes[e]][0]);
+    for (uint64_t i = 0; i < n_cfg; ++i) {
+      ElectrodeConfig c;
+      c.a = static_cast<std::size_t>(a[i]);
+      c.b = static_cast<std::ptrdiff_t>(b[i]);
+      c.m = static_cast<std::size_t>(m[i]);
+      c.n = static_cast<std::size_t>(n[i]);
+      c.k = k[i];
+      survey.configs.push_back(c);
+    }
+    const ModelVector mv(model, model + p->mesh.n_cells());
+    const ResponseJacobian rj = evaluate_response_and_jacobian(p->mesh, mv, survey);
+    std::memcpy(J, rj.J.values.data(), rj.J.values.size() * sizeof(double));
+    std::memcpy(g, rj.g.data(), rj.g.size() * sizeof(double));
+  });
+}
+
+int orc_geometric_factor(const double a[3], const double* b, const double m[3], const double n[3], int dim, double* k) {
+  return guard([&] {
+    std::optional<std::array<double, 3>> bb;
+    if (b) bb = std::array<double, 3>{b[0], b[1], b[2]};
+    *k = geometric_factor({a[0], a[1], a[2]}, bb, {m[0], m[1], m[2]}, {n[0], n[1], n[2]}, dim);
   });
 }
 

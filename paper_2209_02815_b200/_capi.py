@@ -71,8 +71,20 @@ EXPORTED = [
     "gnw_set_jacobian", "gnw_apply_operator", "gnw_precondition", "gnw_amg_apply",
     "gnw_get_woodbury", "gnw_assemble_rhs", "gnw_minres_solve", "gnw_export_csr",
     "gnw_export_mesh", "gnw_dense_cholesky", "gnw_get_stats", "gnw_event_record",
-    "gnw_event_elapsed", "gnw_profile_kernel",
+    "gnw_event_elapsed", "gnw_profile_kernel", "gnw_set_electrodes", "gnw_response_jacobian",
+    "gnw_geometric_factor",
 ]
+
+
+class ErtConfig(C.Structure):
+    """ElectrodeConfig, survey.hpp:15-21 (b = -1: pole at infinity)."""
+
+    _fields_ = [("a", C.c_int64), ("b", C.c_int64), ("m", C.c_int64), ("n", C.c_int64), ("k", C.c_double)]
+
+
+class ErtStats(C.Structure):
+    _fields_ = [("t_assemble", C.c_double), ("t_amg", C.c_double), ("t_solve", C.c_double),
+                ("t_jacobian", C.c_double), ("pcg_iterations", C.c_uint64)]
 
 KERNELS = {"row_gemv": 0, "saddle": 1, "combine_prec": 2, "finish_prec": 3, "vcycle": 4,
            "update": 5, "dgemm": 6, "iteration": 7}
@@ -115,6 +127,9 @@ def load() -> C.CDLL:
     L.gnw_event_record.argtypes = [vp, i32]
     L.gnw_event_elapsed.argtypes = [vp, i32, i32, C.POINTER(dbl)]
     L.gnw_profile_kernel.argtypes = [vp, i32, i32, C.POINTER(dbl), C.POINTER(dbl)]
+    L.gnw_set_electrodes.argtypes = [vp, vp, u64]
+    L.gnw_response_jacobian.argtypes = [vp, vp, C.POINTER(ErtConfig), u64, vp, vp, dbl, C.POINTER(ErtStats)]
+    L.gnw_geometric_factor.argtypes = [vp, vp, vp, vp, i32, C.POINTER(dbl)]
     for name in EXPORTED:
         fn = getattr(L, name)
         if name not in ("gnw_last_error", "gnw_version", "gnw_destroy"):

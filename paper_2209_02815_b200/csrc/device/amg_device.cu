@@ -1,0 +1,217 @@
+// amg_device.cu -- device SA-AMG hierarchy and V-cycle orchestration (amg.cpp:90-111).
+#include "amg_device.cuh"
+
+#include <algorithm>
+#include <cstdlib>
+
+namespace gnw {
+
+void DeviceMemory::release_all() {
+  for (void* p : ptrs) cudaFree(p);
+  ptrs.clear();
+  bytes = 0;
+}
+
+DCsr upload_csr(DeviceMemory& mem, const host::Csr& A, cudaStream_t s) {
+  DCsr d;
+  if (A.nnz() > 0x7fffffffLL || A.n_rows > 0x7fffffffLL) throw std::invalid_argument("matrix too large for int32 indices");
+  d.n_rows = static_cast<int>(A.n_rows);
+  d.n_cols = static_cast<int>(A.n_cols);
+  d.nnz = static_cast<int>(A.nnz());
+  std::vector<int> rp(A.rowptr.size());
+  for (size_t i = 0; i < rp.size(); ++i) rp[i] = static_cast<int>(A.rowptr[i]);
+  d.rowptr = mem.alloc<int>(rp.size());
+  d.cols = mem.alloc<int>(A.cols.size());
+  d.vals = mem.alloc<double>(A.vals.size());
+  GNW_CUDA_CHECK(cudaMemcpyAsync(d.rowptr, rp.data(), rp.size() * sizeof(int), cudaMemcpyHostToDevice, s));
+  if (A.nnz()) {
+    GNW_CUDA_CHECK(cudaMemcpyAsync(d.cols, A.cols.data(), A.cols.size() * sizeof(int), cudaMemcpyHostToDevice, s));
+    GNW_CUDA_CHECK(cudaMemcpyAsync(d.vals, A.vals.data(), A.vals.size() * sizeof(double), cudaMemcpyHostToDevice, s));
+  }
+  GNW_CUDA_CHECK(cudaStreamSynchronize(s));  // host vectors are temporaries
+  return d;
+}
+
+void DeviceAmg::reset() {
+  bmem_.reset();
+  bmem_b_ = 0;
+  lv_.clear();
+  mem_.release_all();
+}
+
+void DeviceAmg::upload(const host::AmgHierarchy& h, cudaStream_t s) {
+  reset();
+  const double omega = h.options.jacobi_damping;
+  const size_t L = h.levels.size();
+  vr_.assign(L, nullptr);
+  ve_.assign(L, nullptr);
+  vres_.assign(L, nullptr);
+  vx_.assign(L, nullptr);
+  for (size_t l = 0; l < L; ++l) {
+    const host::AmgLevel& H = h.levels[l];
+    DLevel d;
+    d.n = static_cast<int>(H.A.n_rows);
+    if (l + 1 < L) {
+      d.A = upload_csr(mem_, H.A, s);
+      d.P = upload_csr(mem_, H.P, s);
+      d.R = upload_csr(mem_, host::transpose(H.P), s);
+      // warp-per-row kernels once rows carry more than ~24 entries (C2: levels >= 2)
+      constexpr double kWide = 24.0;
+      d.wideA = H.A.nnz() > kWide * static_cast<double>(H.A.n_rows);
+      d.wideP = H.P.nnz() > kWide * static_cast<double>(H.P.n_rows);
+      d.wideR = H.P.nnz() > kWide * static_cast<double>(H.P.n_cols);
+      std::vector<double> wd(H.inv_diag.size());
+      for (size_t i = 0; i < wd.size(); ++i) wd[i] = omega * H.inv_diag[i];  // amg.cpp:98 (omega*inv_diag)*r
+      d.wd = mem_.alloc<double>(wd.size());
+      GNW_CUDA_CHECK(cudaMemcpyAsync(d.wd, wd.data(), wd.size() * sizeof(double), cudaMemcpyHostToDevice, s));
+      GNW_CUDA_CHECK(cudaStreamSynchronize(s));
+      vres_[l] = mem_.alloc<double>(d.n);
+      vx_[l] = mem_.alloc<double>(d.n);
+    }
+    if (l > 0) {
+      vr_[l] = mem_.alloc<double>(d.n);
+      ve_[l] = mem_.alloc<double>(d.n);
+    }
+    lv_.push_back(d);
+  }
+  nc_ = static_cast<int>(h.nc);
+  {  // fused tail candidates: trailing levels with <= 600k nonzeros each
+    constexpr int64_t kTailNnz = 600000;
+    const int Li = static_cast<int>(L);
+    int l0 = Li - 1;
+    while (l0 > 0 && h.levels[l0 - 1].A.nnz() <= kTailNnz && (Li - 1 - (l0 - 1)) <= kMaxTail) --l0;
+    tail_l0_ = l0;
+    if (const char* e = std::getenv("GNW_TAIL_CLUSTER")) tail_cluster = std::atoi(e);
+  }
+  const std::vector<double> inv = host::cholesky_inverse(h.nc, h.coarse_chol);
+  coarse_inv_ = mem_.alloc<double>(inv.size());
+  coarse_L_ = mem_.alloc<double>(h.coarse_chol.size());
+  GNW_CUDA_CHECK(cudaMemcpyAsync(coarse_inv_, inv.data(), inv.size() * sizeof(double), cudaMemcpyHostToDevice, s));
+  GNW_CUDA_CHECK(cudaMemcpyAsync(coarse_L_, h.coarse_chol.data(), h.coarse_chol.size() * sizeof(double),
+                                 cudaMemcpyHostToDevice, s));
+  GNW_CUDA_CHECK(cudaStreamSynchronize(s));
+}
+
+// Level l as launched: the reference-order (thread-per-row) kernels everywhere in
+// exact mode, warp-per-row kernels on wide levels otherwise.
+DLevel DeviceAmg::level(int l, int exact) const {
+  DLevel d = lv_[l];
+  if (exact) d.wideA = d.wideP = d.wideR = 0;
+  return d;
+}
+
+// amg.cpp:90-111, one symmetric V-cycle; level 0 input may be a ring slot.
+void DeviceAmg::vcycle(VSel r0, double* out0, const MinresState* st, int exact, cudaStream_t s) {
+  const int L = static_cast<int>(lv_.size());
+  auto coarse = [&](VSel r, double* x) {
+    if (exact)
+      coarse_cholesky(coarse_L_, nc_, r, x, st, 1, 1, s);
+    else
+      coarse_inverse(coarse_inv_, nc_, r, x, st, 1, s);
+  };
+  if (L == 1) {
+    coarse(r0, out0);
+    return;
+  }
+  // levels [tail_l0_, L) run fused in one cluster launch when enabled (vcycle_tail.cu)
+  const int l0 = (tail_cluster > 0) ? tail_l0_ : L;
+  for (int l = 0; l < std::min(l0, L - 1); ++l) {
+    const VSel rl = l == 0 ? r0 : vfixed(vr_[l]);
+    const DLevel lev = level(l, exact);
+    vc_down(lev, rl, vres_[l], st, s);
+    vc_restrict(lev, vres_[l], vr_[l + 1], s);
+  }
+  if (l0 < L) {
+    TailArgs a;
+    a.nlev = L - 1 - l0;
+    for (int k = 0; k < a.nlev; ++k) {
+      const DLevel d = level(l0 + k, exact);
+      TailLevel& t = a.lv[k];
+      t.A = d.A;
+      t.P = d.P;
+      t.R = d.R;
+      t.wd = d.wd;
+      t.n = d.n;
+      t.wideA = d.wideA;
+      t.wideP = d.wideP;
+      t.wideR = d.wideR;
+      a.res[k] = vres_[l0 + k];
+      a.x[k] = vx_[l0 + k];
+    }
+    for (int k = 0; k <= a.nlev; ++k) {
+      a.r[k] = vr_[l0 + k];
+      a.e[k] = ve_[l0 + k];
+    }
+    a.Ainv = coarse_inv_;
+    a.Lc = coarse_L_;
+    a.nc = nc_;
+    a.exact = exact;
+    vcycle_tail(a, l0 == 0 ? r0 : vfixed(vr_[l0]), l0 == 0 ? out0 : ve_[l0], st, tail_cluster, s);
+  } else {
+    coarse(vfixed(vr_[L - 1]), ve_[L - 1]);
+  }
+  for (int l = std::min(l0, L - 1) - 1; l >= 0; --l) {
+    const VSel rl = l == 0 ? r0 : vfixed(vr_[l]);
+    const DLevel lev = level(l, exact);
+    vc_up1(lev, rl, ve_[l + 1], vx_[l], st, s);
+    vc_up2(lev, rl, vx_[l], l == 0 ? out0 : ve_[l], st, s);
+  }
+}
+
+// Persistent work arrays of the batched V-cycle (b interleaved columns).
+void DeviceAmg::ensure_batch(int b) {
+  if (bmem_ && bmem_b_ >= b) return;
+  bmem_.reset();
+  bmem_ = std::make_unique<DeviceMemory>();
+  const int L = static_cast<int>(lv_.size());
+  mr_.assign(L, nullptr);
+  me_.assign(L, nullptr);
+  mres_.assign(L, nullptr);
+  mx_.assign(L, nullptr);
+  for (int l = 0; l < L; ++l) {
+    const size_t nl = static_cast<size_t>(lv_[l].n) * b;
+    if (l > 0) {
+      mr_[l] = bmem_->alloc<double>(nl);
+      me_[l] = bmem_->alloc<double>(nl);
+    }
+    if (l + 1 < L) {
+      mres_[l] = bmem_->alloc<double>(nl);
+      mx_[l] = bmem_->alloc<double>(nl);
+    }
+  }
+  bR0_ = bmem_->alloc<double>(static_cast<size_t>(n()) * b);
+  bX0_ = bmem_->alloc<double>(static_cast<size_t>(n()) * b);
+  bmem_b_ = b;
+}
+
+// Multi-RHS V-cycle over b interleaved columns: r0/out0 are n x b.
+void DeviceAmg::vcycle_batch(const double* r0, int b, double* out0, int exact, const MinresState* st_plain,
+                             cudaStream_t s) {
+  const int L = static_cast<int>(lv_.size());
+  ensure_batch(b);
+  auto coarse = [&](const double* r, double* x) {
+    if (exact)
+      coarse_cholesky(coarse_L_, nc_, vfixed(const_cast<double*>(r)), x, st_plain, b, b, s);
+    else
+      mcoarse_inverse(coarse_inv_, nc_, r, x, b, s);
+  };
+  if (L == 1) {
+    coarse(r0, out0);
+    return;
+  }
+  for (int l = 0; l < L - 1; ++l) {
+    const double* rl = l == 0 ? r0 : mr_[l];
+    const DLevel lev = level(l, exact);
+    mvc_down(lev, rl, b, mres_[l], b, s);
+    mvc_restrict(lev, mres_[l], mr_[l + 1], b, s);
+  }
+  coarse(mr_[L - 1], me_[L - 1]);
+  for (int l = L - 2; l >= 0; --l) {
+    const double* rl = l == 0 ? r0 : mr_[l];
+    const DLevel lev = level(l, exact);
+    mvc_up1(lev, rl, b, me_[l + 1], mx_[l], b, s);
+    mvc_up2(lev, rl, b, mx_[l], l == 0 ? out0 : me_[l], b, b, s);
+  }
+}
+
+}  // namespace gnw

@@ -1,0 +1,79 @@
+// amg_device.cuh -- a device-resident SA-AMG hierarchy (amg.hpp:25-42) and its
+// V-cycles (amg.cpp:90-111): single right-hand side (MINRES loop, graph-safe:
+// level-0 input may be a device ring slot) and batched (b interleaved columns,
+// per column bit-identical to the single-RHS cycle).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../host/setup.hpp"
+#include "kernels.cuh"
+
+namespace gnw {
+
+struct DeviceError : std::runtime_error {
+  DeviceError(const char* expr, cudaError_t e, const char* file, int line)
+      : std::runtime_error(std::string("CUDA error ") + cudaGetErrorString(e) + " in " + expr + " (" + file + ":" +
+                           std::to_string(line) + ")") {}
+  explicit DeviceError(const std::string& s) : std::runtime_error(s) {}
+};
+
+// Device allocations with byte accounting; freed together.
+struct DeviceMemory {
+  std::vector<void*> ptrs;
+  size_t bytes = 0;
+  template <class T>
+  T* alloc(size_t count) {
+    void* p = nullptr;
+    const size_t nb = std::max<size_t>(count, 1) * sizeof(T);
+    GNW_CUDA_CHECK(cudaMalloc(&p, nb));
+    ptrs.push_back(p);
+    bytes += nb;
+    return static_cast<T*>(p);
+  }
+  void release_all();
+  ~DeviceMemory() { release_all(); }
+};
+
+DCsr upload_csr(DeviceMemory& mem, const host::Csr& A, cudaStream_t s);
+
+class DeviceAmg {
+ public:
+  void upload(const host::AmgHierarchy& h, cudaStream_t s);
+  void reset();
+  bool empty() const { return lv_.empty(); }
+  int n() const { return lv_.empty() ? 0 : lv_[0].n; }
+  size_t bytes() const { return mem_.bytes + (bmem_ ? bmem_->bytes : 0); }
+
+  // z = B r, one V-cycle (exact = the reference's thread-per-row order and Cholesky coarse solve)
+  void vcycle(VSel r0, double* out0, const MinresState* st, int exact, cudaStream_t s);
+  // b columns interleaved: r0 / out0 are n x b (ld = b)
+  void vcycle_batch(const double* r0, int b, double* out0, int exact, const MinresState* st_plain, cudaStream_t s);
+  void ensure_batch(int b);
+  int batch_capacity() const { return bmem_b_; }
+  double* batch_in() const { return bR0_; }
+  double* batch_out() const { return bX0_; }
+
+  int tail_cluster = 0;  // fused coarse tail (vcycle_tail.cu); 0 = off (env GNW_TAIL_CLUSTER)
+
+ private:
+  DLevel level(int l, int exact) const;
+  DeviceMemory mem_;
+  std::vector<DLevel> lv_;
+  double* coarse_inv_ = nullptr;
+  double* coarse_L_ = nullptr;
+  int nc_ = 0;
+  int tail_l0_ = 0;
+  std::vector<double*> vr_, ve_, vres_, vx_;
+  std::unique_ptr<DeviceMemory> bmem_;
+  int bmem_b_ = 0;
+  std::vector<double*> mr_, me_, mres_, mx_;
+  double *bR0_ = nullptr, *bX0_ = nullptr;
+};
+
+}  // namespace gnw

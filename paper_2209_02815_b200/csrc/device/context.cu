@@ -17,33 +17,7 @@ namespace gnw {
 
 uint64_t launch_count();
 
-void DeviceMemory::release_all() {
-  for (void* p : ptrs) cudaFree(p);
-  ptrs.clear();
-  bytes = 0;
-}
-
 namespace {
-
-DCsr upload_csr(DeviceMemory& mem, const host::Csr& A, cudaStream_t s) {
-  DCsr d;
-  d.n_rows = static_cast<int>(A.n_rows);
-  d.n_cols = static_cast<int>(A.n_cols);
-  d.nnz = static_cast<int>(A.nnz());
-  if (A.nnz() > 0x7fffffffLL || A.n_rows > 0x7fffffffLL) throw std::invalid_argument("matrix too large for int32 indices");
-  std::vector<int> rp(A.rowptr.size());
-  for (size_t i = 0; i < rp.size(); ++i) rp[i] = static_cast<int>(A.rowptr[i]);
-  d.rowptr = mem.alloc<int>(rp.size());
-  d.cols = mem.alloc<int>(A.cols.size());
-  d.vals = mem.alloc<double>(A.vals.size());
-  GNW_CUDA_CHECK(cudaMemcpyAsync(d.rowptr, rp.data(), rp.size() * sizeof(int), cudaMemcpyHostToDevice, s));
-  if (A.nnz()) {
-    GNW_CUDA_CHECK(cudaMemcpyAsync(d.cols, A.cols.data(), A.cols.size() * sizeof(int), cudaMemcpyHostToDevice, s));
-    GNW_CUDA_CHECK(cudaMemcpyAsync(d.vals, A.vals.data(), A.vals.size() * sizeof(double), cudaMemcpyHostToDevice, s));
-  }
-  GNW_CUDA_CHECK(cudaStreamSynchronize(s));  // host vectors are temporaries
-  return d;
-}
 
 template <class T>
 void h2d(T* dst, const T* src, size_t n, cudaStream_t s) {
@@ -94,7 +68,9 @@ Context::~Context() {
   for (auto& e : mev_)
     if (e) cudaEventDestroy(e);
   jmem_.reset();
-  bmem_.reset();
+  damg_.reset();
+  fwd_amg_.reset();
+  emem_.reset();
   mem_.release_all();
   if (h_st_) cudaFreeHost(h_st_);
   if (stream_) cudaStreamDestroy(stream_);
@@ -135,8 +111,9 @@ void Context::assemble(const double* vertices, int64_t nv, const int64_t* cells,
   if (device_ >= 0) {
     GNW_CUDA_CHECK(cudaSetDevice(device_));
     jmem_.reset();
-    bmem_.reset();
-    bmem_b_ = 0;
+    damg_.reset();
+    fwd_amg_.reset();
+    emem_.reset();
     jm_m_ = -1;
     dJ_ = nullptr;
     dq_ = nullptr;
@@ -179,8 +156,9 @@ void Context::assemble_amg_csr(int64_t n, const int64_t* rowptr, const int64_t* 
   if (device_ >= 0) {
     GNW_CUDA_CHECK(cudaSetDevice(device_));
     jmem_.reset();
-    bmem_.reset();
-    bmem_b_ = 0;
+    damg_.reset();
+    fwd_amg_.reset();
+    emem_.reset();
     jm_m_ = -1;
     dJ_ = nullptr;
     dq_ = nullptr;
@@ -247,55 +225,7 @@ void Context::upload_structure() {
 }
 
 void Context::upload_hierarchy() {
-  const cudaStream_t s = stream_;
-  const double omega = amg_.options.jacobi_damping;
-  lv_.clear();
-  vr_.assign(amg_.levels.size(), nullptr);
-  ve_.assign(amg_.levels.size(), nullptr);
-  vres_.assign(amg_.levels.size(), nullptr);
-  vx_.assign(amg_.levels.size(), nullptr);
-  for (size_t l = 0; l < amg_.levels.size(); ++l) {
-    const host::AmgLevel& L = amg_.levels[l];
-    DLevel d;
-    d.n = static_cast<int>(L.A.n_rows);
-    const bool last = (l + 1 == amg_.levels.size());
-    if (!last) {
-      d.A = upload_csr(mem_, L.A, s);
-      d.P = upload_csr(mem_, L.P, s);
-      d.R = upload_csr(mem_, host::transpose(L.P), s);
-      // warp-per-row kernels once rows carry more than ~24 entries (C2: levels >= 2)
-      constexpr double kWide = 24.0;
-      d.wideA = L.A.nnz() > kWide * static_cast<double>(L.A.n_rows);
-      d.wideP = L.P.nnz() > kWide * static_cast<double>(L.P.n_rows);
-      d.wideR = L.P.nnz() > kWide * static_cast<double>(L.P.n_cols);
-      std::vector<double> wd(L.inv_diag.size());
-      for (size_t i = 0; i < wd.size(); ++i) wd[i] = omega * L.inv_diag[i];  // amg.cpp:98 (omega*inv_diag)*r
-      d.wd = mem_.alloc<double>(wd.size());
-      h2d(d.wd, wd.data(), wd.size(), s);
-      sync();
-      vres_[l] = mem_.alloc<double>(d.n);
-      vx_[l] = mem_.alloc<double>(d.n);
-    }
-    if (l > 0) {
-      vr_[l] = mem_.alloc<double>(d.n);
-      ve_[l] = mem_.alloc<double>(d.n);
-    }
-    lv_.push_back(d);
-  }
-  nc_ = static_cast<int>(amg_.nc);
-  {  // fused tail: the trailing levels with <= 600k nonzeros each (C1: the whole cycle; C2: levels 2..9)
-    constexpr int64_t kTailNnz = 600000;
-    const int L = static_cast<int>(amg_.levels.size());
-    int l0 = L - 1;
-    while (l0 > 0 && amg_.levels[l0 - 1].A.nnz() <= kTailNnz && (L - 1 - (l0 - 1)) <= kMaxTail) --l0;
-    tail_l0_ = l0;
-    if (const char* e = std::getenv("GNW_TAIL_CLUSTER")) tail_cluster_ = std::atoi(e);
-  }
-  const std::vector<double> inv = host::cholesky_inverse(amg_.nc, amg_.coarse_chol);
-  coarse_inv_ = mem_.alloc<double>(inv.size());
-  coarse_L_ = mem_.alloc<double>(amg_.coarse_chol.size());
-  h2d(coarse_inv_, inv.data(), inv.size(), s);
-  h2d(coarse_L_, amg_.coarse_chol.data(), amg_.coarse_chol.size(), s);
+  damg_.upload(amg_, stream_);
   svc_ = mem_.alloc<double>(std::max<int64_t>(N_, 1));
   sync();
 }
@@ -303,129 +233,7 @@ void Context::upload_hierarchy() {
 // ----------------------------------------------------------------- V-cycle
 // amg.cpp:90-111, one symmetric V-cycle; level 0 input may be a ring slot.
 void Context::vcycle(VSel r0, double* out0, const MinresState* st) {
-  const cudaStream_t s = stream_;
-  const int L = static_cast<int>(lv_.size());
-  auto coarse = [&](VSel r, double* x) {
-    if (coarse_mode == 1)
-      coarse_cholesky(coarse_L_, nc_, r, x, st, 1, 1, s);
-    else
-      coarse_inverse(coarse_inv_, nc_, r, x, st, 1, s);
-  };
-  if (L == 1) {
-    coarse(r0, out0);
-    return;
-  }
-  // levels [tail_l0_, L) run fused in one cluster launch (vcycle_tail.cu)
-  const int l0 = (tail_cluster_ > 0) ? tail_l0_ : L;
-  for (int l = 0; l < std::min(l0, L - 1); ++l) {
-    const VSel rl = l == 0 ? r0 : vfixed(vr_[l]);
-    const DLevel lev = level(l);
-    vc_down(lev, rl, vres_[l], st, s);
-    vc_restrict(lev, vres_[l], vr_[l + 1], s);
-  }
-  if (l0 < L) {
-    TailArgs a;
-    a.nlev = L - 1 - l0;
-    for (int k = 0; k < a.nlev; ++k) {
-      const DLevel d = level(l0 + k);
-      TailLevel& t = a.lv[k];
-      t.A = d.A;
-      t.P = d.P;
-      t.R = d.R;
-      t.wd = d.wd;
-      t.n = d.n;
-      t.wideA = d.wideA;
-      t.wideP = d.wideP;
-      t.wideR = d.wideR;
-      a.res[k] = vres_[l0 + k];
-      a.x[k] = vx_[l0 + k];
-    }
-    for (int k = 0; k <= a.nlev; ++k) {
-      a.r[k] = vr_[l0 + k];
-      a.e[k] = ve_[l0 + k];
-    }
-    a.Ainv = coarse_inv_;
-    a.Lc = coarse_L_;
-    a.nc = nc_;
-    a.exact = coarse_mode == 1;
-    vcycle_tail(a, l0 == 0 ? r0 : vfixed(vr_[l0]), l0 == 0 ? out0 : ve_[l0], st, tail_cluster_, s);
-  } else {
-    coarse(vfixed(vr_[L - 1]), ve_[L - 1]);
-  }
-  for (int l = std::min(l0, L - 1) - 1; l >= 0; --l) {
-    const VSel rl = l == 0 ? r0 : vfixed(vr_[l]);
-    const DLevel lev = level(l);
-    vc_up1(lev, rl, ve_[l + 1], vx_[l], st, s);
-    vc_up2(lev, rl, vx_[l], l == 0 ? out0 : ve_[l], st, s);
-  }
-}
-
-// Level l as launched: the reference-order (thread-per-row) kernels everywhere in
-// exact mode, warp-per-row kernels on wide levels otherwise.
-DLevel Context::level(int l) const {
-  DLevel d = lv_[l];
-  if (coarse_mode == 1) d.wideA = d.wideP = d.wideR = 0;
-  return d;
-}
-
-// Persistent work arrays of the batched V-cycle (b interleaved columns).
-void Context::ensure_batch(int b) {
-  if (bmem_ && bmem_b_ >= b) return;
-  bmem_.reset();
-  bmem_ = std::make_unique<DeviceMemory>();
-  const int L = static_cast<int>(lv_.size());
-  mr_.assign(L, nullptr);
-  me_.assign(L, nullptr);
-  mres_.assign(L, nullptr);
-  mx_.assign(L, nullptr);
-  for (int l = 0; l < L; ++l) {
-    const size_t nl = static_cast<size_t>(lv_[l].n) * b;
-    if (l > 0) {
-      mr_[l] = bmem_->alloc<double>(nl);
-      me_[l] = bmem_->alloc<double>(nl);
-    }
-    if (l + 1 < L) {
-      mres_[l] = bmem_->alloc<double>(nl);
-      mx_[l] = bmem_->alloc<double>(nl);
-    }
-  }
-  bR0_ = bmem_->alloc<double>(static_cast<size_t>(N_) * b);
-  bX0_ = bmem_->alloc<double>(static_cast<size_t>(N_) * b);
-  bmem_b_ = b;
-}
-
-// Multi-RHS V-cycle over b interleaved columns: r0/out0 are N x b.
-void Context::vcycle_batch(const double* r0, int b, double* out0) {
-  const cudaStream_t s = stream_;
-  const int L = static_cast<int>(lv_.size());
-  ensure_batch(b);
-  std::vector<double*>& mr = mr_;
-  std::vector<double*>& me = me_;
-  std::vector<double*>& mres = mres_;
-  std::vector<double*>& mx = mx_;
-  auto coarse = [&](const double* r, double* x) {
-    if (coarse_mode == 1)
-      coarse_cholesky(coarse_L_, nc_, vfixed(const_cast<double*>(r)), x, st_plain_, b, b, s);
-    else
-      mcoarse_inverse(coarse_inv_, nc_, r, x, b, s);
-  };
-  if (L == 1) {
-    coarse(r0, out0);
-  } else {
-    for (int l = 0; l < L - 1; ++l) {
-      const double* rl = l == 0 ? r0 : mr[l];
-      const DLevel lev = level(l);
-      mvc_down(lev, rl, b, mres[l], b, s);
-      mvc_restrict(lev, mres[l], mr[l + 1], b, s);
-    }
-    coarse(mr[L - 1], me[L - 1]);
-    for (int l = L - 2; l >= 0; --l) {
-      const double* rl = l == 0 ? r0 : mr[l];
-      const DLevel lev = level(l);
-      mvc_up1(lev, rl, b, me[l + 1], mx[l], b, s);
-      mvc_up2(lev, rl, b, mx[l], l == 0 ? out0 : me[l], b, b, s);
-    }
-  }
+  damg_.vcycle(r0, out0, st, coarse_mode == 1, stream_);
 }
 
 // ------------------------------------------------------------ stage helpers
@@ -535,7 +343,7 @@ void Context::set_jacobian(const double* J, int64_t m, int64_t n_cells, double b
   GNW_CUDA_CHECK(cudaEventRecord(ev[0], s));
   // H = S_hat^-1 J^T by batched V-cycles (inversion.cpp:107-114); stored as Ht (m x N)
   {
-    int b = bmem_b_;
+    int b = damg_.batch_capacity();
     if (b < ((m + 31) / 32) * 32 && b < 512) {
       size_t free_b = 0, total_b = 0;
       cudaMemGetInfo(&free_b, &total_b);
@@ -543,13 +351,13 @@ void Context::set_jacobian(const double* J, int64_t m, int64_t n_cells, double b
       int64_t bmax = static_cast<int64_t>(0.5 * static_cast<double>(free_b) / per_col);
       bmax = std::max<int64_t>(32, std::min<int64_t>(bmax, 512) / 32 * 32);
       b = static_cast<int>(std::min<int64_t>(((m + 31) / 32) * 32, bmax));
-      ensure_batch(b);
+      damg_.ensure_batch(b);
     }
     for (int64_t i0 = 0; i0 < m; i0 += b) {
       const int bb = static_cast<int>(std::min<int64_t>(b, m - i0));
-      transpose_rows_to_batch(dJ_, N_, ldj_, static_cast<int>(i0), bb, bR0_, s);
-      vcycle_batch(bR0_, bb, bX0_);
-      transpose_batch_to_rows(bX0_, N_, ldh_, static_cast<int>(i0), bb, dHt_, s);
+      transpose_rows_to_batch(dJ_, N_, ldj_, static_cast<int>(i0), bb, damg_.batch_in(), s);
+      damg_.vcycle_batch(damg_.batch_in(), bb, damg_.batch_out(), coarse_mode == 1, st_plain_, s);
+      transpose_batch_to_rows(damg_.batch_out(), N_, ldh_, static_cast<int>(i0), bb, dHt_, s);
     }
     GNW_CUDA_CHECK(cudaEventRecord(ev[1], s));
   }

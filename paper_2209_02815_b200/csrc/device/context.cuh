@@ -8,40 +8,23 @@
 #include <string>
 #include <vector>
 
+#include "../host/ert.hpp"
 #include "../host/setup.hpp"
+#include "amg_device.cuh"
 #include "kernels.cuh"
 
 namespace gnw {
-
-struct DeviceError : std::runtime_error {
-  DeviceError(const char* expr, cudaError_t e, const char* file, int line)
-      : std::runtime_error(std::string("CUDA error ") + cudaGetErrorString(e) + " in " + expr + " (" + file + ":" +
-                           std::to_string(line) + ")") {}
-  explicit DeviceError(const std::string& s) : std::runtime_error(s) {}
-};
-
-// Device allocation owned by the context (bytes tracked for gnw_info).
-struct DeviceMemory {
-  std::vector<void*> ptrs;
-  size_t bytes = 0;
-  template <class T>
-  T* alloc(size_t count) {
-    void* p = nullptr;
-    const size_t nb = std::max<size_t>(count, 1) * sizeof(T);
-    GNW_CUDA_CHECK(cudaMalloc(&p, nb));
-    ptrs.push_back(p);
-    bytes += nb;
-    return static_cast<T*>(p);
-  }
-  void release_all();
-  ~DeviceMemory() { release_all(); }
-};
 
 struct MinresResult {
   std::vector<double> hist_e, hist_p;
   uint64_t iterations = 0;
   bool converged = false;
   double true_rel = 0.0;
+};
+
+struct ErtTimings {
+  double t_assemble = 0.0, t_amg = 0.0, t_solve = 0.0, t_jacobian = 0.0;
+  uint64_t pcg_iterations = 0;
 };
 
 class Context {
@@ -80,6 +63,11 @@ class Context {
   void profile_kernel(int kernel, int reps, double* seconds, double* algorithmic);
   uint64_t last_iterations = 0;
 
+  // ERT forward model (forward.cpp:39-172) on the assembled mesh
+  void set_electrodes(const int64_t* nodes, int64_t n);
+  void response_jacobian(const double* mdl, const host::ErtConfig* cfgs, int64_t n_cfg, double* J_out, double* g_out,
+                         double tol, ErtTimings* t);
+
   // structure
   const host::Mesh& mesh() const { return mesh_; }
   const host::Csr& Q() const { return Q_; }
@@ -92,7 +80,9 @@ class Context {
   int64_t N() const { return N_; }
   int64_t m() const { return m_; }
   double beta() const { return beta_; }
-  size_t device_bytes() const { return mem_.bytes + (jmem_ ? jmem_->bytes : 0); }
+  size_t device_bytes() const {
+    return mem_.bytes + (jmem_ ? jmem_->bytes : 0) + damg_.bytes() + fwd_amg_.bytes() + (emem_ ? emem_->bytes : 0);
+  }
 
   double t_minres = 0.0, t_rhs = 0.0;
   uint64_t launches = 0, setup_launches = 0;
@@ -103,9 +93,6 @@ class Context {
   void upload_structure();
   void upload_hierarchy();
   void vcycle(VSel r0, double* out0, const MinresState* st);
-  void vcycle_batch(const double* r0, int b, double* out0);
-  DLevel level(int l) const;
-  void ensure_batch(int b);
   void operator_into(VSel x, int scaled, VSel y, MinresState* st, int loop, bool fused = false);
   void precondition_into(VSel y, VSel yv2, VSel z, MinresState* st, int loop, VSel vcur, VSel vprev,
                          bool fused = false);
@@ -121,8 +108,9 @@ class Context {
   int device_ = -1;
   cudaStream_t stream_ = nullptr;
   int sm_count_ = 148;
-  DeviceMemory mem_;                      // structure + hierarchy + work vectors
+  DeviceMemory mem_;                      // structure + work vectors
   std::unique_ptr<DeviceMemory> jmem_;    // Jacobian-dependent buffers
+  DeviceAmg damg_;                        // SA-AMG of S_hat on the device
 
   bool assembled_ = false, mixed_ = false;
   host::Mesh mesh_;
@@ -133,18 +121,7 @@ class Context {
   // device structure
   OperatorArgs op_{};
   PrecArgs pa_{};
-  std::vector<DLevel> lv_;
-  double* coarse_inv_ = nullptr;
-  double* coarse_L_ = nullptr;
-  int nc_ = 0;
-  std::vector<double*> vr_, ve_, vres_, vx_;  // single-RHS V-cycle work per level
-  double* svc_ = nullptr;                     // V-cycle output (s)
-  int tail_l0_ = 0;        // first level of the fused V-cycle tail
-  int tail_cluster_ = 0;   // CTAs in the tail cluster (0: off; env GNW_TAIL_CLUSTER)
-  std::unique_ptr<DeviceMemory> bmem_;        // batched V-cycle work (persists across set_jacobian)
-  int bmem_b_ = 0;
-  std::vector<double*> mr_, me_, mres_, mx_;
-  double *bR0_ = nullptr, *bX0_ = nullptr;
+  double* svc_ = nullptr;  // V-cycle output (s)
 
   // Jacobian / Woodbury
   int64_t m_ = 0;
@@ -162,7 +139,7 @@ class Context {
   double* Z_[2] = {};
   double* Vk_[3] = {};  // V_[k] + K (cell part), V-cycle input ring
   double *opart_ = nullptr, *cpart_ = nullptr, *fpart_ = nullptr, *upart_ = nullptr, *rpart_ = nullptr;
-  unsigned* counters_ = nullptr;  // 8 counters
+  unsigned* counters_ = nullptr;  // 16 counters
   MinresState* st_ = nullptr;     // loop state
   MinresState* st_plain_ = nullptr;
   MinresState* h_st_ = nullptr;   // pinned host mirror
@@ -191,6 +168,12 @@ class Context {
   cudaGraphExec_t graph_exec_ = nullptr;
   uint64_t graph_nodes_ = 0;
   int n_comb_blocks_ = 0;
+
+  // ERT forward model state
+  std::vector<int64_t> electrodes_;
+  host::ForwardStructure fwd_;      // free-node map, stiffness pattern, per-entry contributions
+  DeviceAmg fwd_amg_;               // SA-AMG of the P1 stiffness (rebuilt per model)
+  std::unique_ptr<DeviceMemory> emem_;
 };
 
 }  // namespace gnw

@@ -5,6 +5,7 @@
 // reference's exception text.
 #include <cstring>
 #include <string>
+#include <vector>
 
 #include "../../../include/gnw.h"
 #include "context.cuh"
@@ -245,6 +246,26 @@ gnw_status gnw_export_mesh(const gnw_ctx* ctx, int64_t* cells, int64_t* edges, i
 
 gnw_status gnw_dense_cholesky(gnw_ctx* ctx, uint64_t n, const double* C, double* L) {
   return guard([&] { ctx_of(ctx).dense_cholesky(static_cast<int64_t>(n), C, L); });
+}
+
+gnw_status gnw_set_electrodes(gnw_ctx* ctx, const int64_t* nodes, uint64_t n) {
+  return guard([&] { ctx_of(ctx).set_electrodes(nodes, static_cast<int64_t>(n)); });
+}
+
+gnw_status gnw_response_jacobian(gnw_ctx* ctx, const double* m, const gnw_ert_config* cfgs, uint64_t n_cfg, double* J,
+                                 double* g, double tol, gnw_ert_stats* stats) {
+  return guard([&] {
+    std::vector<gnw::host::ErtConfig> c(n_cfg);
+    for (uint64_t i = 0; i < n_cfg; ++i) c[i] = {cfgs[i].a, cfgs[i].b, cfgs[i].m, cfgs[i].n, cfgs[i].k};
+    gnw::ErtTimings t;
+    ctx_of(ctx).response_jacobian(m, c.data(), static_cast<int64_t>(n_cfg), J, g, tol, &t);
+    if (stats) *stats = {t.t_assemble, t.t_amg, t.t_solve, t.t_jacobian, t.pcg_iterations};
+  });
+}
+
+gnw_status gnw_geometric_factor(const double a[3], const double* b, const double m[3], const double n[3], int dim,
+                                double* k) {
+  return guard([&] { *k = gnw::host::geometric_factor(a, b, m, n, dim); });
 }
 
 gnw_status gnw_event_record(gnw_ctx* ctx, int slot) {

@@ -203,6 +203,32 @@ class Context:
         A.check(self.L.gnw_profile_kernel(self.h, A.KERNELS[name], reps, C.byref(sec), C.byref(alg)))
         return sec.value, alg.value
 
+    # ------------------------------------------------------------ ERT (C4/C5)
+    def set_electrodes(self, nodes):
+        """Mesh::electrode_nodes (mesh.hpp:32) of the assembled mesh."""
+        nodes = np.ascontiguousarray(nodes, dtype=np.int64)
+        A.check(self.L.gnw_set_electrodes(self.h, nodes.ctypes.data, len(nodes)))
+        self.n_electrodes = len(nodes)
+
+    def response_jacobian(self, model, cfgs, tol: float = 1e-14, J_out=None, g_out=None):
+        """evaluate_response_and_jacobian (forward.cpp:100-172) -> (g, J, stats).
+
+        ``cfgs``: dict of arrays a, b, m, n, k (b = -1: pole at infinity)."""
+        nc = len(cfgs["k"])
+        arr = (A.ErtConfig * nc)(*[A.ErtConfig(int(cfgs["a"][i]), int(cfgs["b"][i]), int(cfgs["m"][i]),
+                                               int(cfgs["n"][i]), float(cfgs["k"][i])) for i in range(nc)])
+        model = self._in(model)
+        if self.device_pointers:
+            import torch
+            J = J_out if J_out is not None else torch.empty((nc, self.N), dtype=torch.float64, device="cuda")
+            g = g_out if g_out is not None else torch.empty(nc, dtype=torch.float64, device="cuda")
+        else:
+            J = J_out if J_out is not None else np.zeros((nc, self.N))
+            g = g_out if g_out is not None else np.zeros(nc)
+        st = A.ErtStats()
+        A.check(self.L.gnw_response_jacobian(self.h, _dptr(model), arr, nc, _dptr(J), _dptr(g), tol, C.byref(st)))
+        return g, J, {f: getattr(st, f) for f, _ in A.ErtStats._fields_}
+
     def woodbury_factors(self):
         """(H, L): H = S_hat^-1 J^T (N x m, h_hat layout) and the capacitance Cholesky factor."""
         H = np.zeros((self.N, self.m))
@@ -242,6 +268,15 @@ class Context:
 # ---------------------------------------------------------------------------
 # Reference-shaped facade (inversion.hpp / minres.hpp names)
 # ---------------------------------------------------------------------------
+def geometric_factor(a, b, m, n, dim: int = 2) -> float:
+    """geometric_factor (survey.cpp:22-46); b=None: electrode at infinity."""
+    L = A.load()
+    arr = lambda v: (C.c_double * 3)(*v)
+    k = C.c_double()
+    A.check(L.gnw_geometric_factor(arr(a), arr(b) if b is not None else None, arr(m), arr(n), dim, C.byref(k)))
+    return k.value
+
+
 def amg_setup(ctx: Context, rowptr, cols, vals, opts: A.AmgOptions | None = None) -> Context:
     return ctx.assemble_amg_csr(rowptr, cols, vals, opts)
 

@@ -147,6 +147,89 @@ class GnStepInputs:
     dg: np.ndarray
 
 
+@dataclasses.dataclass(frozen=True)
+class ErtConfigSpec:
+    """BASELINE C4/C5: unit square n x n, n_ele equispaced top-edge (z = 0) electrodes."""
+
+    name: str
+    index: int
+    n: int
+    n_ele: int
+    first: int   # node index of electrode 0 on the z = 0 row
+    step: int    # node spacing between electrodes
+    alpha: float
+    coarse_threshold: int = 64
+
+
+ERT_CONFIGS = {
+    "C4": ErtConfigSpec("C4", 3, 256, 32, 4, 8, 1e-2),
+    "C5": ErtConfigSpec("C5", 4, 1024, 64, 8, 16, 1e-3, coarse_threshold=1024),
+}
+
+
+def ert_survey(n_ele: int, positions) -> dict:
+    """Adjacent-pair dipole-dipole survey (builder's rule): sources (e, e+1),
+    readings (k, k+1) sharing no electrode with the source; pairs k in {e-1, e, e+1} are
+    dropped, and for the two edge sources also the next pair inward, so every source has
+    n_ele - 4 readings (C4: 31 x 28 = 868, C5: 63 x 60 = 3780).  k = geometric_factor
+    (survey.cpp:22-46) with the finite return electrode B, 2-D."""
+    from .solver import geometric_factor
+
+    pos = lambda e: (float(positions[e]), 0.0, 0.0)
+    npairs = n_ele - 1
+    out = {"a": [], "b": [], "m": [], "n": [], "k": []}
+    for e in range(npairs):
+        drop = {k for k in (e - 1, e, e + 1) if 0 <= k < npairs}
+        if e == 0:
+            drop.add(2)
+        if e == npairs - 1:
+            drop.add(npairs - 3)
+        for k in range(npairs):
+            if k in drop:
+                continue
+            out["a"].append(e)
+            out["b"].append(e + 1)
+            out["m"].append(k)
+            out["n"].append(k + 1)
+            out["k"].append(geometric_factor(pos(e), pos(e + 1), pos(k), pos(k + 1), 2))
+    return {key: np.array(v, dtype=np.float64 if key == "k" else np.int64) for key, v in out.items()}
+
+
+def conductivity_model(mesh: Mesh, config_index: int, corr_len: float = 0.1, n_features: int = 512) -> np.ndarray:
+    """log sigma at cell centroids: a seeded Gaussian random field (random Fourier features,
+    correlation length 0.1, unit variance) plus two disc inclusions (sigma x10 at
+    (0.3, 0.25), sigma x0.1 at (0.7, 0.35), radius 0.1)."""
+    z = gaussian(seed_for(config_index, 4), 3 * n_features)
+    w = z[: 2 * n_features].reshape(n_features, 2) / corr_len
+    phase = 2.0 * np.pi * ((splitmix64(seed_for(config_index, 4), n_features, offset=10 ** 9) >> np.uint64(11))
+                           .astype(np.float64) * 2.0 ** -53)
+    cent = mesh.vertices[mesh.cells].mean(axis=1)
+    field = np.sqrt(2.0 / n_features) * np.cos(cent @ w.T + phase).sum(axis=1)
+    d1 = np.hypot(cent[:, 0] - 0.3, cent[:, 1] - 0.25) < 0.1
+    d2 = np.hypot(cent[:, 0] - 0.7, cent[:, 1] - 0.35) < 0.1
+    field = field + np.log(10.0) * d1 + np.log(0.1) * d2
+    return np.ascontiguousarray(field)
+
+
+@dataclasses.dataclass
+class ErtInputs:
+    mesh: Mesh
+    electrodes: np.ndarray  # node ids on z = 0
+    survey: dict
+    model: np.ndarray       # log sigma (J evaluated here)
+    noise: np.ndarray       # N(0,1) per reading: g_obs = g (1 + 0.01 noise)
+
+
+def ert_inputs(name: str) -> ErtInputs:
+    cfg = ERT_CONFIGS[name]
+    mesh = unit_square_mesh(cfg.n)
+    nodes = np.array([cfg.first + cfg.step * e for e in range(cfg.n_ele)], dtype=np.int64)  # row j = 0
+    survey = ert_survey(cfg.n_ele, mesh.vertices[nodes, 0])
+    model = conductivity_model(mesh, cfg.index)
+    noise = gaussian(seed_for(cfg.index, 5), len(survey["k"]))
+    return ErtInputs(mesh, nodes, survey, model, noise)
+
+
 def gnstep_inputs(n: int, m: int, config_index: int) -> GnStepInputs:
     mesh = unit_square_mesh(n)
     n_cells = mesh.n_cells
