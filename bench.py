@@ -154,7 +154,7 @@ def c2_reference_record():
         return None
 
 
-def cpu_sample(cfg, inp, alpha, iterations, k_cols=16, k_rows=16, k_iters=10):
+def cpu_sample(cfg, inp, alpha, iterations, k_cols=16, k_rows=16, k_iters=10, label="C2"):
     """Bounded sample of the reference on this host, extrapolated to one full GN-step solve."""
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
     import orc  # CPU baseline leg only
@@ -167,7 +167,7 @@ def cpu_sample(cfg, inp, alpha, iterations, k_cols=16, k_rows=16, k_iters=10):
     s = p.sample_gnstep(inp.J, alpha, k_cols, k_rows, k_iters)
     wall = time.time() - t0
     t_est = s["t_col"] * cfg.m + s["t_row"] * cfg.m + s["t_chol"] + s["t_iter"] * iterations
-    sample = (f"reference (oracle/_ref, -O3 -DNDEBUG) on C2 alpha={alpha:g}: {k_cols} H columns (V-cycles), "
+    sample = (f"reference (oracle/_ref, -O3 -DNDEBUG) on {label} alpha={alpha:g}: {k_cols} H columns (V-cycles), "
               f"{k_rows} capacitance rows (matmul), full {cfg.m}x{cfg.m} Cholesky, {k_iters} MINRES iterations "
               f"({wall:.1f} s of CPU); per-unit times x (m={cfg.m} columns, m rows, {iterations} iterations) "
               f"-> t_norm = {t_est:.1f} s")
@@ -204,6 +204,56 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
+class _Cfg:
+    def __init__(self, **kw):
+        self.__dict__.update(kw)
+
+
+class _Inputs:
+    pass
+
+
+def make_problem(name, ctx, W, AmgOptions, torch):
+    """Assemble the context and return (cfg, inputs, ert_info).  C1-C3: synthetic J and the
+    reference's random-RHS pattern.  C4/C5: J and g from the device ERT forward model at the
+    GRF log-conductivity (build time reported as t_J, outside t_norm like inversion.cpp:224),
+    rhs = assemble_gn_rhs(m, 0, g, g (1 + 0.01 eps))."""
+    inp = _Inputs()
+    inp.J_d = None
+    if name in W.ERT_CONFIGS:
+        ec = W.ERT_CONFIGS[name]
+        e = W.ert_inputs(name)
+        inp.mesh = e.mesh
+        ctx.assemble(e.mesh, AmgOptions(coarse_threshold=ec.coarse_threshold))
+        ctx.set_electrodes(e.electrodes)
+        ctx.use_device_pointers(True)
+        model_d = torch.from_numpy(e.model).cuda()
+        ctx.response_jacobian(model_d, e.survey)  # warm-up (module load, AMG)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        g_d, J_d, st = ctx.response_jacobian(model_d, e.survey)
+        torch.cuda.synchronize()
+        t_J = time.perf_counter() - t0
+        ctx.use_device_pointers(False)
+        g = g_d.cpu().numpy()
+        inp.J_d = J_d
+        inp.J = J_d.cpu().numpy()
+        inp.rhs_m, inp.rhs_mref = e.model, np.zeros(e.mesh.n_cells)
+        inp.rhs_g, inp.rhs_gobs = g, g * (1.0 + 0.01 * e.noise)
+        m = len(g)
+        cfg = _Cfg(n=ec.n, m=m, alphas=(ec.alpha,), coarse_threshold=ec.coarse_threshold, index=ec.index)
+        ert = {"source": "device ERT forward model (gnw_response_jacobian)", "t_J_s": t_J,
+               "electrodes": len(e.electrodes), "measurements": m, **{k: v for k, v in st.items()}}
+        return cfg, inp, ert
+    cfg = W.CONFIGS[name]
+    g = W.gnstep_inputs(cfg.n, cfg.m, cfg.index)
+    inp.mesh, inp.J = g.mesh, g.J
+    inp.rhs_m, inp.rhs_mref = g.dm, np.zeros(g.mesh.n_cells)
+    inp.rhs_g, inp.rhs_gobs = g.dg, np.zeros(cfg.m)
+    ctx.assemble(g.mesh, AmgOptions(coarse_threshold=cfg.coarse_threshold))
+    return cfg, inp, None
+
+
 def run_gnw(args):
     import torch
 
@@ -214,14 +264,11 @@ def run_gnw(args):
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     from paper_2209_02815_b200 import AmgOptions, Context, workload as W
 
-    cfg = W.CONFIGS[args.config]
-    inp = W.gnstep_inputs(cfg.n, cfg.m, cfg.index)
+    tol = 1e-8
+    ctx = Context(local)
+    cfg, inp, ert = make_problem(args.config, ctx, W, AmgOptions, torch)
     K, N = W.mixed_sizes(cfg.n)
     alphas = list(cfg.alphas)
-    tol = 1e-8
-
-    ctx = Context(local)
-    ctx.assemble(inp.mesh, AmgOptions(coarse_threshold=cfg.coarse_threshold))
     info = ctx.info()
 
     def barrier():
@@ -235,11 +282,11 @@ def run_gnw(args):
 
     # ---------------------------------------------------------- device-resident arm
     ctx.use_device_pointers(True)
-    J_d = torch.from_numpy(inp.J).cuda()
-    dm_d = torch.from_numpy(inp.dm).cuda()
-    dg_d = torch.from_numpy(inp.dg).cuda()
-    zN = torch.zeros(N, dtype=torch.float64, device="cuda")
-    zm = torch.zeros(cfg.m, dtype=torch.float64, device="cuda")
+    J_d = inp.J_d if inp.J_d is not None else torch.from_numpy(inp.J).cuda()
+    dm_d = torch.from_numpy(inp.rhs_m).cuda()
+    dg_d = torch.from_numpy(inp.rhs_g).cuda()
+    zN = torch.from_numpy(inp.rhs_mref).cuda()
+    zm = torch.from_numpy(inp.rhs_gobs).cuda()
 
     def solve_dev(alpha):
         tm = ctx.set_jacobian(J_d, alpha)
@@ -272,10 +319,10 @@ def run_gnw(args):
     # ---------------------------------------------------------------- e2e arm
     ctx.use_device_pointers(False)
     J_h = torch.from_numpy(inp.J).pin_memory().numpy()
-    dm_h = torch.from_numpy(inp.dm).pin_memory().numpy()
-    dg_h = torch.from_numpy(inp.dg).pin_memory().numpy()
-    zN_h = np.zeros(N)
-    zm_h = np.zeros(cfg.m)
+    dm_h = torch.from_numpy(inp.rhs_m).pin_memory().numpy()
+    dg_h = torch.from_numpy(inp.rhs_g).pin_memory().numpy()
+    zN_h = torch.from_numpy(inp.rhs_mref).pin_memory().numpy()
+    zm_h = torch.from_numpy(inp.rhs_gobs).pin_memory().numpy()
 
     def solve_host(alpha):
         ctx.set_jacobian(J_h, alpha)
@@ -327,11 +374,12 @@ def run_gnw(args):
     # ---------------------------------------------------------- CPU baseline
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
-        rec = c2_reference_record()
-        it_ref = {r["alpha"]: r["iterations"] for r in rec["runs"]}.get(1e-2) if rec else None
-        it_use = it_ref or next(s["iterations"] for s in per_step if s["alpha"] == 1e-2)
+        rec = c2_reference_record() if args.config == "C2" else None
+        a_cpu = 1e-2 if 1e-2 in alphas else alphas[0]
+        it_ref = {r["alpha"]: r["iterations"] for r in rec["runs"]}.get(a_cpu) if rec else None
+        it_use = it_ref or next(s["iterations"] for s in per_step if s["alpha"] == a_cpu)
         try:
-            v, t_est, s, sample, kind = cpu_sample(cfg, inp, 1e-2, it_use)
+            v, t_est, s, sample, kind = cpu_sample(cfg, inp, a_cpu, it_use, label=args.config)
             cpu = {"value": v, "unit": UNIT, "cores": 1, "kind": kind, "sample": sample}
         except Exception as e:  # reported, never silently replaced
             cpu = {"value": None, "unit": UNIT, "cores": 1, "kind": "reference", "sample": f"failed: {e}"}
@@ -340,13 +388,14 @@ def run_gnw(args):
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": 1e3 * elapsed / args.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded C2 bundle)",
-            "config": {"workload": f"C2: unit square n={cfg.n} (N={N} cells, K={K} edges), m={cfg.m}, "
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": f"synthetic (seeded {args.config} bundle)",
+            "config": {"workload": f"{args.config}: unit square n={cfg.n} (N={N} cells, K={K} edges), m={cfg.m}, "
                                    f"alpha sweep {alphas}, MINRES tol {tol}; one step = one full GN-step solve",
                        "mesh_n": cfg.n, "m": cfg.m, "alphas": alphas, "tol": tol,
                        "parallelism": f"replicas x{ws}",
                        "l2": "no flush: per-solve inputs (J 1.07 GB + H 1.07 GB) exceed the 126 MB L2",
-                       "amg_levels": info["n_levels"], "coarse_n": info["coarse_n"]},
+                       "amg_levels": info["n_levels"], "coarse_n": info["coarse_n"],
+                       "jacobian": ert if ert else "synthetic U diag(10^(-4k/m)) V^T (workload.py)"},
             "roofline": {"bound": "hbm", "kernel": "k_" + dom, "achieved": kern[dom]["GBps"], "peak": hbm_peak,
                          "unit": "GB/s", "frac": kern[dom]["frac"], "traffic": traffic,
                          "peak_source": peak_src,

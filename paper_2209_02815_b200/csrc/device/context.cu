@@ -42,9 +42,17 @@ Context::Context(int device) : device_(device) {
   sm_count_ = prop.multiProcessorCount;
   if (const char* e = std::getenv("GNW_PAD")) pad_ = std::max(0LL, std::atoll(e) / 2 * 2);
   if (const char* e = std::getenv("GNW_NO_GRAPH")) no_graph_ = std::atoi(e) != 0;
+  if (const char* e = std::getenv("GNW_FORK_VCYCLE")) fork_ = std::atoi(e) != 0;
+  if (const char* e = std::getenv("GNW_RG_RESERVE")) rg_reserve_ = std::max(0, std::atoi(e));
   // A blocking stream: ordered with the legacy default stream, so device-pointer
   // callers (e.g. torch on its default stream) need no extra synchronisation.
   GNW_CUDA_CHECK(cudaStreamCreateWithFlags(&stream_, cudaStreamDefault));
+  {
+    int lo = 0, hi = 0;  // the latency-bound V-cycle branch gets the higher priority
+    GNW_CUDA_CHECK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    GNW_CUDA_CHECK(cudaStreamCreateWithPriority(&side_, cudaStreamNonBlocking, hi));
+    for (auto& e : fork_ev_) GNW_CUDA_CHECK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  }
   for (auto& e : mev_) GNW_CUDA_CHECK(cudaEventCreate(&e));
   st_ = mem_.alloc<MinresState>(1);
   st_plain_ = mem_.alloc<MinresState>(1);
@@ -67,12 +75,16 @@ Context::~Context() {
     if (e) cudaEventDestroy(e);
   for (auto& e : mev_)
     if (e) cudaEventDestroy(e);
+  for (auto& e : fork_ev_)
+    if (e) cudaEventDestroy(e);
+  if (side_) cudaStreamSynchronize(side_);
   jmem_.reset();
   damg_.reset();
   fwd_amg_.reset();
   emem_.reset();
   mem_.release_all();
   if (h_st_) cudaFreeHost(h_st_);
+  if (side_) cudaStreamDestroy(side_);
   if (stream_) cudaStreamDestroy(stream_);
 }
 
@@ -219,7 +231,7 @@ void Context::upload_structure() {
   fpart_ = mem_.alloc<double>(nb * 3);
   upart_ = mem_.alloc<double>(nb * 3);
   rpart_ = mem_.alloc<double>(nb * 3);
-  plan_ = row_gemv_plan(N_, 1);  // re-planned for the row count by set_jacobian
+  plan_ = plan_h_ = row_gemv_plan(N_, 1);  // re-planned for the row count by set_jacobian
   n_comb_blocks_ = combine_blocks(K_, N_);
   cpart_ = mem_.alloc<double>(3 * (static_cast<size_t>(n_comb_blocks_) + 16));  // one triple per combine block
 }
@@ -232,8 +244,8 @@ void Context::upload_hierarchy() {
 
 // ----------------------------------------------------------------- V-cycle
 // amg.cpp:90-111, one symmetric V-cycle; level 0 input may be a ring slot.
-void Context::vcycle(VSel r0, double* out0, const MinresState* st) {
-  damg_.vcycle(r0, out0, st, coarse_mode == 1, stream_);
+void Context::vcycle(VSel r0, double* out0, const MinresState* st, cudaStream_t s) {
+  damg_.vcycle(r0, out0, st, coarse_mode == 1, s ? s : stream_);
 }
 
 // ------------------------------------------------------------ stage helpers
@@ -287,6 +299,7 @@ void Context::set_jacobian(const double* J, int64_t m, int64_t n_cells, double b
     DeviceMemory& jm = *jmem_;
     u_ = jm.alloc<double>(m);
     plan_ = row_gemv_plan(N_, static_cast<int>(m));
+    plan_h_ = row_gemv_plan(N_, static_cast<int>(m), fork_ ? rg_reserve_ : 0);  // nchunks <= plan_'s
     gpart_ = jm.alloc<double>(static_cast<size_t>(plan_.nchunks) * m);
     ldh_ = N_ + pad_;
     jown_ = want_owned ? jm.alloc<double>(static_cast<size_t>(m) * ldh_) : nullptr;
@@ -432,10 +445,22 @@ void Context::precondition_into(VSel y, VSel yv2, VSel z, MinresState* st, int l
     pa.J = dJ_;
     pa.q = dq_;
   }
-  combine_precondition(pa, loop ? vfixed(az_) : y, vcur, vprev, y, z, loop, st, nullptr, cpart_, tpart_,
-                       counters_ + 2, t_, plan_, stream_);
-  vcycle(yv2, svc_, st);
+  const VSel az = loop ? vfixed(az_) : y;
+  combine_elem(pa, az, vcur, vprev, y, z, loop, st, cpart_, stream_);
+  // s = B y2 and t = H^T y2 both read only y2: the V-cycle (latency-bound, few
+  // CTAs on its coarse levels) runs on side_ beside the bandwidth-bound GEMV.
+  const bool fork = fork_ && pa.m > 0;
+  if (fork) {
+    GNW_CUDA_CHECK(cudaEventRecord(fork_ev_[0], stream_));
+    GNW_CUDA_CHECK(cudaStreamWaitEvent(side_, fork_ev_[0], 0));
+    vcycle(yv2, svc_, st, side_);
+    GNW_CUDA_CHECK(cudaEventRecord(fork_ev_[1], side_));
+  }
+  if (pa.m > 0)  // t = H^T v2 (matvec_transpose(h_hat, y2), inversion.cpp:82)
+    row_gemv(pa.Ht, pa.m, pa.N, pa.ldh, y, pa.K, 0, st, tpart_, counters_ + 2, t_, plan_h_, stream_);
+  if (!fork) vcycle(yv2, svc_, st);
   capacitance_solve(pa, t_, t2_, stream_);
+  if (fork) GNW_CUDA_CHECK(cudaStreamWaitEvent(stream_, fork_ev_[1], 0));
   finish_precondition(pa, svc_, t2_, y, z, loop, st, cpart_, n_comb_blocks_, fpart_, counters_ + 3, stream_);
 }
 

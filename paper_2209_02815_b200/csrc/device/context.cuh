@@ -92,7 +92,7 @@ class Context {
   void require_mixed() const;
   void upload_structure();
   void upload_hierarchy();
-  void vcycle(VSel r0, double* out0, const MinresState* st);
+  void vcycle(VSel r0, double* out0, const MinresState* st, cudaStream_t s = nullptr);
   void operator_into(VSel x, int scaled, VSel y, MinresState* st, int loop, bool fused = false);
   void precondition_into(VSel y, VSel yv2, VSel z, MinresState* st, int loop, VSel vcur, VSel vprev,
                          bool fused = false);
@@ -107,6 +107,11 @@ class Context {
 
   int device_ = -1;
   cudaStream_t stream_ = nullptr;
+  // The V-cycle runs on a second stream (a parallel graph branch) beside the
+  // H^T v row GEMV it does not depend on; env GNW_FORK_VCYCLE=0 serialises it.
+  cudaStream_t side_ = nullptr;
+  cudaEvent_t fork_ev_[2] = {};
+  bool fork_ = true;
   int sm_count_ = 148;
   DeviceMemory mem_;                      // structure + work vectors
   std::unique_ptr<DeviceMemory> jmem_;    // Jacobian-dependent buffers
@@ -129,7 +134,9 @@ class Context {
   double *dJ_ = nullptr, *dHt_ = nullptr, *dC_ = nullptr, *dL_ = nullptr, *dCinv_ = nullptr, *dY_ = nullptr;
   double *u_ = nullptr, *t_ = nullptr, *t2_ = nullptr;
   double *gpart_ = nullptr, *tpart_ = nullptr;
-  RowGemv plan_{};
+  RowGemv plan_{};    // J x (nothing runs beside it)
+  RowGemv plan_h_{};  // H^T y (leaves CTA slots for the forked V-cycle)
+  int rg_reserve_ = 2;  // env GNW_RG_RESERVE
 
   // MINRES vectors
   double *b_ = nullptr, *x_ = nullptr, *r_ = nullptr, *az_ = nullptr, *tmp_ = nullptr, *tmp2_ = nullptr;

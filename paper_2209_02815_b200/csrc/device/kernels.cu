@@ -66,8 +66,9 @@ __global__ void __launch_bounds__(kTpb) k_vc_down(DCsr A, const double* __restri
   if (i >= A.n_rows) return;
   double s = 0.0;
   const int k1 = A.rowptr[i + 1];
+#pragma unroll 4
   for (int k = A.rowptr[i]; k < k1; ++k) {
-    const int c = A.cols[k];
+    const int c = __ldg(&A.cols[k]);
     s = s + ldg(&A.vals[k]) * (ldg(&wd[c]) * r[c]);
   }
   resid[i] = r[i] + (-1.0 * s);
@@ -81,7 +82,8 @@ __global__ void __launch_bounds__(kTpb) k_vc_restrict(DCsr R, const double* __re
   if (a >= R.n_rows) return;
   double s = 0.0;
   const int k1 = R.rowptr[a + 1];
-  for (int k = R.rowptr[a]; k < k1; ++k) s = s + ldg(&R.vals[k]) * resid[R.cols[k]];
+#pragma unroll 4
+  for (int k = R.rowptr[a]; k < k1; ++k) s = s + ldg(&R.vals[k]) * resid[__ldg(&R.cols[k])];
   rc[a] = s;
 }
 
@@ -95,7 +97,8 @@ __global__ void __launch_bounds__(kTpb) k_vc_up1(DCsr P, const double* __restric
   if (i >= P.n_rows) return;
   double s = 0.0;
   const int k1 = P.rowptr[i + 1];
-  for (int k = P.rowptr[i]; k < k1; ++k) s = s + ldg(&P.vals[k]) * ec[P.cols[k]];
+#pragma unroll 4
+  for (int k = P.rowptr[i]; k < k1; ++k) s = s + ldg(&P.vals[k]) * ec[__ldg(&P.cols[k])];
   x[i] = ldg(&wd[i]) * r[i] + 1.0 * s;
 }
 
@@ -109,7 +112,8 @@ __global__ void __launch_bounds__(kTpb) k_vc_up2(DCsr A, const double* __restric
   if (i >= A.n_rows) return;
   double s = 0.0;
   const int k1 = A.rowptr[i + 1];
-  for (int k = A.rowptr[i]; k < k1; ++k) s = s + ldg(&A.vals[k]) * x[A.cols[k]];
+#pragma unroll 4
+  for (int k = A.rowptr[i]; k < k1; ++k) s = s + ldg(&A.vals[k]) * x[__ldg(&A.cols[k])];
   const double res = r[i] + (-1.0 * s);
   out[i] = x[i] + ldg(&wd[i]) * res;
 }
@@ -334,36 +338,27 @@ void transpose_batch_to_rows(const double* X, long long cols, long long ld, int 
 // ======================================================================
 // Row GEMV with chunked columns: out[i] = sum_c A[i, c] x[c] (deterministic)
 // ======================================================================
-// Column chunks sized so the grid is a multiple of the SM count (148 on B200):
-// every SM streams the same number of bytes (no partial last wave).
-// 2-D grid: (column chunk) x (group of 32 rows).  Short-lived CTAs (one 32-row x
-// chunk tile each, ~14 waves at C2) keep every SM streaming to the end.
-RowGemv row_gemv_plan(long long N, int m) {
-  RowGemv p;
-  p.ngroups = std::max(1, (m + kRowsPerCta - 1) / kRowsPerCta);
-  const long long ctas = 148LL * 8;
-  long long chunk = (N * p.ngroups + ctas - 1) / ctas;
-  chunk = std::max<long long>(64, (chunk + 63) / 64 * 64);
-  chunk = std::min<long long>(chunk, 4096);
-  p.chunk = static_cast<int>(chunk);
-  p.nchunks = static_cast<int>((N + chunk - 1) / chunk);
-  return p;
-}
+// One wave, no tail: the grid is (column spans) x (groups of 32 rows) with
+// spans x groups = SMs x resident CTAs per SM, each CTA streaming one contiguous
+// column span of its 32 rows.  (A 2-D grid of short tiles left a 1.6-wave tail at
+// C2 -- 78% of HBM bandwidth; one full wave has no tail.)  x is read through L1:
+// the 8 warps of a CTA share each x line.
 
-// R row segments A[row_r, c0 : c0+len] dotted with the smem vector xs, one warp;
-// R independent rows keep R x 2 x 16-byte loads in flight per lane.
+// R row segments A[row_r, 0 : len] dotted with x[0 : len], one warp, lanes take
+// 2-column steps; R independent rows keep R x 2 x 16-byte loads in flight per lane.
 template <int R>
 __device__ __forceinline__ void warp_rows_dot(const double* __restrict__ a, long long ld, int nrows,
-                                              const double* __restrict__ xs, int len, bool vec_ok, int lane,
-                                              double (&out)[R]) {
+                                              const double* __restrict__ x, int scaled, double sc, int len,
+                                              bool vec_ok, int lane, double (&out)[R]) {
   double acc[R];
 #pragma unroll
   for (int r = 0; r < R; ++r) acc[r] = 0.0;
+  auto xv = [&](int t) { return scaled ? __ldg(x + t) * sc : __ldg(x + t); };
   if (vec_ok) {
     const int len2 = len & ~1;
 #pragma unroll 2
     for (int t = lane * 2; t < len2; t += 64) {
-      const double x0 = xs[t], x1 = xs[t + 1];
+      const double x0 = xv(t), x1 = xv(t + 1);
       double2 v[R];
 #pragma unroll
       for (int r = 0; r < R; ++r)
@@ -374,49 +369,50 @@ __device__ __forceinline__ void warp_rows_dot(const double* __restrict__ a, long
         acc[r] = acc[r] + v[r].y * x1;
       }
     }
-    if ((len & 1) && lane == 0)
+    if ((len & 1) && lane == 0) {
+      const double xl = xv(len - 1);
 #pragma unroll
       for (int r = 0; r < R; ++r)
-        if (r < nrows) acc[r] = acc[r] + __ldg(a + r * ld + len - 1) * xs[len - 1];
+        if (r < nrows) acc[r] = acc[r] + __ldg(a + r * ld + len - 1) * xl;
+    }
   } else {
-    for (int t = lane; t < len; t += 32)
+    for (int t = lane; t < len; t += 32) {
+      const double xt = xv(t);
 #pragma unroll
       for (int r = 0; r < R; ++r)
-        if (r < nrows) acc[r] = acc[r] + __ldg(a + r * ld + t) * xs[t];
+        if (r < nrows) acc[r] = acc[r] + __ldg(a + r * ld + t) * xt;
+    }
   }
   warp_reduce<R>(acc);
 #pragma unroll
   for (int r = 0; r < R; ++r) out[r] = acc[r];
 }
 
-
 __global__ void __launch_bounds__(kTpb) k_row_gemv(const double* __restrict__ A, int m, long long N, long long ld, VSel xs,
                                                    long long xoff, int scaled, const MinresState* st,
                                                    double* __restrict__ partial, unsigned* counter,
-                                                   double* __restrict__ out, int chunk) {
+                                                   double* __restrict__ out, int span) {
   griddep_wait();
-  extern __shared__ double xsm[];
   const double* __restrict__ x = vsel(xs, st) + xoff;
   const double sc = scaled ? st->inv_gamma : 1.0;
-  const long long c0 = static_cast<long long>(blockIdx.x) * chunk;
-  const int len = static_cast<int>(min(static_cast<long long>(chunk), N - c0));
-  for (int t = threadIdx.x; t < len; t += blockDim.x) xsm[t] = scaled ? x[c0 + t] * sc : x[c0 + t];
-  __syncthreads();
+  const long long c0 = static_cast<long long>(blockIdx.x) * span;
+  const int len = static_cast<int>(min(static_cast<long long>(span), N - c0));
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const bool vec_ok = ((ld & 1) == 0);
+  const bool vec_ok = ((ld & 1) == 0);  // span is even, so every row segment starts 16-byte aligned
   {
     const int row = blockIdx.y * kRowsPerCta + warp * kRowsPerWarp;  // 8 warps x 4 rows
     if (row < m) {
       double d[kRowsPerWarp];
       const int nr = min(kRowsPerWarp, m - row);
-      warp_rows_dot<kRowsPerWarp>(A + static_cast<long long>(row) * ld + c0, ld, nr, xsm, len, vec_ok, lane, d);
+      warp_rows_dot<kRowsPerWarp>(A + static_cast<long long>(row) * ld + c0, ld, nr, x + c0, scaled, sc, len, vec_ok,
+                                  lane, d);
       if (lane == 0)
 #pragma unroll
         for (int r = 0; r < kRowsPerWarp; ++r)
           if (r < nr) partial[static_cast<long long>(blockIdx.x) * m + row + r] = d[r];
     }
   }
-  // last block reduces over chunks in index order
+  // last block reduces over spans in index order
   __shared__ bool am_last;
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -428,17 +424,40 @@ __global__ void __launch_bounds__(kTpb) k_row_gemv(const double* __restrict__ A,
   __threadfence();
   for (int row = threadIdx.x; row < m; row += blockDim.x) {
     double s = 0.0;
+    // unrolled: the partial loads are independent, so 8 L2 round trips overlap
+#pragma unroll 8
     for (unsigned b = 0; b < gridDim.x; ++b) s += __ldcg(&partial[static_cast<long long>(b) * m + row]);
     out[row] = s;
   }
   if (threadIdx.x == 0) *counter = 0u;
 }
 
+RowGemv row_gemv_plan(long long N, int m, int reserve) {
+  static int sms = 0, occ = 0;  // SMs, resident k_row_gemv CTAs per SM
+  if (sms == 0) {
+    int dev = 0;
+    sms = 148;
+    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_row_gemv, kTpb, 0) != cudaSuccess || occ < 1) occ = 4;
+    cudaGetLastError();
+  }
+  // reserve: CTA slots per SM left free for a concurrent graph branch (the V-cycle)
+  const int slots = sms * std::max(1, occ - reserve);
+  RowGemv p;
+  p.ngroups = std::max(1, (m + kRowsPerCta - 1) / kRowsPerCta);
+  const long long spans = std::max(1, slots / p.ngroups);
+  long long span = (N + spans - 1) / spans;
+  span = std::max<long long>(64, (span + 63) / 64 * 64);
+  p.chunk = static_cast<int>(span);
+  p.nchunks = static_cast<int>((N + span - 1) / span);
+  return p;
+}
+
 void row_gemv(const double* A, int m, long long N, long long ld, VSel x, long long x_off, int scaled,
               const MinresState* st, double* partial, unsigned* counter, double* out, const RowGemv& plan,
               cudaStream_t s) {
   const dim3 grid(plan.nchunks, (m + kRowsPerCta - 1) / kRowsPerCta);
-  GNW_LAUNCH(launch_k(k_row_gemv, grid, kTpb, plan.chunk * sizeof(double), s, A, m, N, ld, x, x_off, scaled, st, partial, counter, out,
+  GNW_LAUNCH(launch_k(k_row_gemv, grid, kTpb, 0, s, A, m, N, ld, x, x_off, scaled, st, partial, counter, out,
                                                              plan.chunk));
   check_launch("row_gemv");
 }
@@ -566,11 +585,16 @@ __global__ void __launch_bounds__(kTpb) k_combine_elem(PrecArgs pa, VSel azs, VS
 
 int combine_blocks(long long K, long long N) { return static_cast<int>(grid_for(K + N)); }
 
+void combine_elem(const PrecArgs& pa, VSel az, VSel vcur, VSel vprev, VSel vnext, VSel znext, int loop,
+                  MinresState* st, double* dots_part, cudaStream_t s) {
+  GNW_LAUNCH(launch_k(k_combine_elem, combine_blocks(pa.K, pa.N), kTpb, 0, s, pa, az, vcur, vprev, vnext, znext, loop, st, dots_part));
+  check_launch("combine_elem");
+}
+
 void combine_precondition(const PrecArgs& pa, VSel az, VSel vcur, VSel vprev, VSel vnext, VSel znext, int loop,
                           MinresState* st, double* /*vcopy*/, double* dots_part, double* t_part,
                           unsigned* counter, double* t_out, const RowGemv& plan, cudaStream_t s) {
-  GNW_LAUNCH(launch_k(k_combine_elem, combine_blocks(pa.K, pa.N), kTpb, 0, s, pa, az, vcur, vprev, vnext, znext, loop, st, dots_part));
-  check_launch("combine_elem");
+  combine_elem(pa, az, vcur, vprev, vnext, znext, loop, st, dots_part, s);
   if (pa.m > 0)  // t = H^T v2 (matvec_transpose(h_hat, y2), inversion.cpp:82): row GEMV over Ht
     row_gemv(pa.Ht, pa.m, pa.N, pa.ldh, vnext, pa.K, 0, st, t_part, counter, t_out, plan, s);
 }

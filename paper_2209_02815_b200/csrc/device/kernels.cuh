@@ -106,7 +106,7 @@ struct OperatorArgs {
 struct RowGemv {
   int chunk = 0, nchunks = 0, ngroups = 0;
 };
-RowGemv row_gemv_plan(long long N, int m);
+RowGemv row_gemv_plan(long long N, int m, int reserve = 0);
 // number of blocks of the elementwise combine kernel (dots partials)
 int combine_blocks(long long K, long long N);
 void row_gemv(const double* A, int m, long long N, long long ld, VSel x, long long x_off, int scaled,
@@ -138,6 +138,9 @@ struct PrecArgs {
 // v_next = Az + c1 v_cur + c2 v_prev (combine, minres.cpp:76-77) or, when
 // !loop, v_next = y (plain preconditioner input); z1 = qinv * v1; partial
 // dots; t = Ht v2 (row GEMV) reduced by the last block into t_out.
+// the element part of combine_precondition (v_next, z_next edge part, dots) alone
+void combine_elem(const PrecArgs& pa, VSel az, VSel vcur, VSel vprev, VSel vnext, VSel znext, int loop,
+                  MinresState* st, double* dots_part, cudaStream_t s);
 void combine_precondition(const PrecArgs& pa, VSel az, VSel vcur, VSel vprev, VSel vnext, VSel znext,
                           int loop, MinresState* st, double* vcopy, double* dots_part,
                           double* t_part, unsigned* counter, double* t_out, const RowGemv& plan,

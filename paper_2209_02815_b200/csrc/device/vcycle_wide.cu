@@ -36,7 +36,9 @@ template <class F>
 __device__ __forceinline__ double warp_row(const DCsr& A, int i, int lane, F f) {
   double acc = 0.0;
   const int k1 = A.rowptr[i + 1];
-  for (int k = A.rowptr[i] + lane; k < k1; k += 32) acc = acc + __ldg(&A.vals[k]) * f(A.cols[k]);
+  // unrolled so several (index -> value) load chains are in flight per lane
+#pragma unroll 4
+  for (int k = A.rowptr[i] + lane; k < k1; k += 32) acc = acc + __ldg(&A.vals[k]) * f(__ldg(&A.cols[k]));
   double v[1] = {acc};
   warp_reduce<1>(v);
   return v[0];
