@@ -213,6 +213,9 @@ class _Inputs:
     pass
 
 
+LARGE_J_BYTES = 8e9  # above this J stays on the device until the e2e arm needs a host copy
+
+
 def make_problem(name, ctx, W, AmgOptions, torch):
     """Assemble the context and return (cfg, inputs, ert_info).  C1-C3: synthetic J and the
     reference's random-RHS pattern.  C4/C5: J and g from the device ERT forward model at the
@@ -237,7 +240,7 @@ def make_problem(name, ctx, W, AmgOptions, torch):
         ctx.use_device_pointers(False)
         g = g_d.cpu().numpy()
         inp.J_d = J_d
-        inp.J = J_d.cpu().numpy()
+        inp.J = J_d.cpu().numpy() if J_d.numel() * 8 <= LARGE_J_BYTES else None
         inp.rhs_m, inp.rhs_mref = e.model, np.zeros(e.mesh.n_cells)
         inp.rhs_g, inp.rhs_gobs = g, g * (1.0 + 0.01 * e.noise)
         m = len(g)
@@ -246,11 +249,22 @@ def make_problem(name, ctx, W, AmgOptions, torch):
                "electrodes": len(e.electrodes), "measurements": m, **{k: v for k, v in st.items()}}
         return cfg, inp, ert
     cfg = W.CONFIGS[name]
-    g = W.gnstep_inputs(cfg.n, cfg.m, cfg.index)
-    inp.mesh, inp.J = g.mesh, g.J
-    inp.rhs_m, inp.rhs_mref = g.dm, np.zeros(g.mesh.n_cells)
-    inp.rhs_g, inp.rhs_gobs = g.dg, np.zeros(cfg.m)
-    ctx.assemble(g.mesh, AmgOptions(coarse_threshold=cfg.coarse_threshold))
+    K, N = W.mixed_sizes(cfg.n)
+    if 8 * cfg.m * N > LARGE_J_BYTES:
+        # C3: J (68.7 GB) is generated on the device; the host sees
+        # it only as the e2e arm's pinned input
+        inp.mesh = W.unit_square_mesh(cfg.n)
+        inp.J = None
+        inp.J_d = W.synthetic_jacobian_device(cfg.m, N, cfg.index, "cuda")
+        torch.cuda.synchronize()
+        inp.rhs_m = W.gaussian(W.seed_for(cfg.index, 2), N)
+        inp.rhs_g = W.gaussian(W.seed_for(cfg.index, 3), cfg.m)
+    else:
+        g = W.gnstep_inputs(cfg.n, cfg.m, cfg.index)
+        inp.mesh, inp.J = g.mesh, g.J
+        inp.rhs_m, inp.rhs_g = g.dm, g.dg
+    inp.rhs_mref, inp.rhs_gobs = np.zeros(N), np.zeros(cfg.m)
+    ctx.assemble(inp.mesh, AmgOptions(coarse_threshold=cfg.coarse_threshold))
     return cfg, inp, None
 
 
@@ -316,31 +330,6 @@ def run_gnw(args):
     barrier()
     value, elapsed = replica_throughput(elapsed, args.steps, ws)
 
-    # ---------------------------------------------------------------- e2e arm
-    ctx.use_device_pointers(False)
-    J_h = torch.from_numpy(inp.J).pin_memory().numpy()
-    dm_h = torch.from_numpy(inp.rhs_m).pin_memory().numpy()
-    dg_h = torch.from_numpy(inp.rhs_g).pin_memory().numpy()
-    zN_h = torch.from_numpy(inp.rhs_mref).pin_memory().numpy()
-    zm_h = torch.from_numpy(inp.rhs_gobs).pin_memory().numpy()
-
-    def solve_host(alpha):
-        ctx.set_jacobian(J_h, alpha)
-        b = ctx.assemble_rhs(dm_h, zN_h, dg_h, zm_h)
-        x, rep = ctx.minres(b, tol=tol)
-        return x, rep
-
-    solve_host(alphas[0])
-    barrier()
-    ctx.event_record(2)
-    for k in range(args.steps):
-        x_h, rep_h = solve_host(alphas[k % len(alphas)])
-    ctx.event_record(3)
-    e2e_elapsed = max_over_ranks(ctx.event_elapsed(2, 3))
-    barrier()
-    h2d = 8 * (cfg.m * N + 3 * N + 2 * cfg.m) + 8 * 2 * (K + N)  # J, m, m_ref, g, g_obs, then b, x0
-    d2h = 8 * (K + N) * 2 + 8 * 2 * (rep_h.iterations + 1)        # rhs, x, residual histories
-
     # --------------------------------------------------------------- roofline
     hbm_peak, peak_src = peaks()
     ctx.use_device_pointers(True)
@@ -367,13 +356,52 @@ def run_gnw(args):
     traffic = None
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
-            traffic = json.load(f).get(dom)
+            tj = json.load(f)
+        if tj.get("config") == args.config:  # captured on that workload only
+            traffic = tj["per_launch"].get(dom)
     except Exception:
         pass
 
+    # ---------------------------------------------------------------- e2e arm
+    ctx.use_device_pointers(False)
+    if inp.J is None:  # large configs: J lives on the device; one pinned host copy, then free it
+        J_pin = torch.empty(tuple(J_d.shape), dtype=torch.float64, pin_memory=True)
+        J_pin.copy_(J_d)
+        del J_d
+        inp.J_d = None
+        torch.cuda.empty_cache()
+        J_h = J_pin.numpy()
+    else:
+        J_h = torch.from_numpy(inp.J).pin_memory().numpy()
+    dm_h = torch.from_numpy(inp.rhs_m).pin_memory().numpy()
+    dg_h = torch.from_numpy(inp.rhs_g).pin_memory().numpy()
+    zN_h = torch.from_numpy(inp.rhs_mref).pin_memory().numpy()
+    zm_h = torch.from_numpy(inp.rhs_gobs).pin_memory().numpy()
+
+    def solve_host(alpha):
+        ctx.set_jacobian(J_h, alpha)
+        b = ctx.assemble_rhs(dm_h, zN_h, dg_h, zm_h)
+        x, rep = ctx.minres(b, tol=tol)
+        return x, rep
+
+    solve_host(alphas[0])
+    barrier()
+    ctx.event_record(2)
+    for k in range(args.steps):
+        x_h, rep_h = solve_host(alphas[k % len(alphas)])
+    ctx.event_record(3)
+    e2e_elapsed = max_over_ranks(ctx.event_elapsed(2, 3))
+    barrier()
+    h2d = 8 * (cfg.m * N + 3 * N + 2 * cfg.m) + 8 * 2 * (K + N)  # J, m, m_ref, g, g_obs, then b, x0
+    d2h = 8 * (K + N) * 2 + 8 * 2 * (rep_h.iterations + 1)        # rhs, x, residual histories
+
     # ---------------------------------------------------------- CPU baseline
     cpu = None
-    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline and 8 * cfg.m * N > LARGE_J_BYTES:
+        cpu = {"value": None, "unit": UNIT, "cores": 1, "kind": "reference",
+               "sample": f"not run: the reference holds J and H on the host ({16 * cfg.m * N / 1e9:.0f} GB), "
+                         f"beside the e2e arm's pinned J (SURVEY.md 8(c): C3/C5 full m infeasible on the host)"}
+    elif rank == 0 and ws == 1 and not args.no_cpu_baseline:
         rec = c2_reference_record() if args.config == "C2" else None
         a_cpu = 1e-2 if 1e-2 in alphas else alphas[0]
         it_ref = {r["alpha"]: r["iterations"] for r in rec["runs"]}.get(a_cpu) if rec else None
@@ -393,7 +421,7 @@ def run_gnw(args):
                                    f"alpha sweep {alphas}, MINRES tol {tol}; one step = one full GN-step solve",
                        "mesh_n": cfg.n, "m": cfg.m, "alphas": alphas, "tol": tol,
                        "parallelism": f"replicas x{ws}",
-                       "l2": "no flush: per-solve inputs (J 1.07 GB + H 1.07 GB) exceed the 126 MB L2",
+                       "l2": f"no flush: per-solve inputs (J {8 * cfg.m * N / 1e9:.2f} GB + H {8 * cfg.m * N / 1e9:.2f} GB) exceed the 126 MB L2",
                        "amg_levels": info["n_levels"], "coarse_n": info["coarse_n"],
                        "jacobian": ert if ert else "synthetic U diag(10^(-4k/m)) V^T (workload.py)"},
             "roofline": {"bound": "hbm", "kernel": "k_" + dom, "achieved": kern[dom]["GBps"], "peak": hbm_peak,

@@ -26,6 +26,50 @@ namespace gnw {
 
 namespace {
 
+// Column sweeps (J^T u, H t): loads in flight per thread.  One thread per column walks all m
+// rows.  Batch = loads in flight per thread: 8 keeps k_finish_prec at 32 registers (8 CTAs
+// per SM) for small m; at large m the t staging (30 KB smem at m = 3780) caps residency at
+// 6-7 CTAs per SM anyway and a batch of 16 carries the bytes in flight (C5 shapes:
+// 5.96 -> 7.08 TB/s; C2 with 16: 6.31 -> 6.05 TB/s, hence the switch).
+constexpr int kSweepBatchWideM = 1024;
+
+// Eight strided 8-byte loads issued back to back as one asm statement, so all eight
+// results are live at once (ptxas would otherwise interleave them with the add chain and
+// keep only ~4 in flight).
+__device__ __forceinline__ void ld8_strided(double* v, const double* p, long long stride_bytes) {
+  asm volatile(
+      "{\n\t.reg .u64 a;\n\t"
+      "mov.u64 a, %8;\n\t"
+      "ld.global.nc.f64 %0, [a];\n\tadd.u64 a, a, %9;\n\t"
+      "ld.global.nc.f64 %1, [a];\n\tadd.u64 a, a, %9;\n\t"
+      "ld.global.nc.f64 %2, [a];\n\tadd.u64 a, a, %9;\n\t"
+      "ld.global.nc.f64 %3, [a];\n\tadd.u64 a, a, %9;\n\t"
+      "ld.global.nc.f64 %4, [a];\n\tadd.u64 a, a, %9;\n\t"
+      "ld.global.nc.f64 %5, [a];\n\tadd.u64 a, a, %9;\n\t"
+      "ld.global.nc.f64 %6, [a];\n\tadd.u64 a, a, %9;\n\t"
+      "ld.global.nc.f64 %7, [a];\n\t}"
+      : "=d"(v[0]), "=d"(v[1]), "=d"(v[2]), "=d"(v[3]), "=d"(v[4]), "=d"(v[5]), "=d"(v[6]), "=d"(v[7])
+      : "l"(p), "l"(stride_bytes));
+}
+
+// sum_{i < m} p[i * ld] * s[i], accumulated in ascending i (the reference's matvec order):
+// the loads of a batch are issued before its sequential adds, so every thread keeps
+// kSweepBatch 8-byte loads in flight.
+template <int B>
+__device__ __forceinline__ double col_dot(const double* __restrict__ p, long long ld, const double* s, int m) {
+  static_assert(B % 8 == 0, "batch is a multiple of 8");
+  double acc = 0.0;
+  int i = 0;
+  for (; i + B <= m; i += B) {
+    double v[B];
+#pragma unroll
+    for (int k = 0; k < B; k += 8) ld8_strided(v + k, p + static_cast<long long>(i + k) * ld, ld * 8);
+#pragma unroll
+    for (int k = 0; k < B; ++k) acc = acc + v[k] * s[i + k];
+  }
+  for (; i < m; ++i) acc = acc + __ldg(p + static_cast<long long>(i) * ld) * s[i];
+  return acc;
+}
 constexpr int kTpb = 256;
 constexpr int kRowsPerWarp = 4;                           // row GEMV: rows per warp
 constexpr int kRowsPerCta = kRowsPerWarp * (kTpb / 32);  // row GEMV: rows per CTA
@@ -511,10 +555,7 @@ __global__ void __launch_bounds__(kTpb) k_saddle(OperatorArgs op, VSel xs, int s
       if (op.m > 0 && op.q != nullptr) {  // fused: J^T (J zhat2) = J^T (t' * ig) ~ q * ig (Woodbury identity J z2 = t')
         o = o + *op.neg_inv_beta * (op.q[c] * sc);
       } else if (op.m > 0) {  // matvec_transpose(J, J dm), linalg.cpp:45-54
-        double jt = 0.0;
-        const double* __restrict__ Jc = op.J + c;
-#pragma unroll 8
-        for (int i = 0; i < op.m; ++i) jt = jt + __ldg(Jc + static_cast<long long>(i) * op.ldj) * usm[i];
+        const double jt = col_dot<8>(op.J + c, op.ldj, usm, op.m);
         o = o + *op.neg_inv_beta * jt;  // axpy(-1.0 / beta, jtjdm, out2)
       }
       y[op.K + c] = o;
@@ -621,6 +662,7 @@ void capacitance_solve(const PrecArgs& pa, const double* t, double* t2, cudaStre
   check_launch("capacitance_solve");
 }
 
+template <int B>
 __global__ void __launch_bounds__(kTpb) k_finish_prec(PrecArgs pa, const double* __restrict__ svc,
                                                       const double* __restrict__ t2, VSel vns, VSel zns, int loop,
                                                       MinresState* st, const double* __restrict__ dots_edge,
@@ -652,8 +694,7 @@ __global__ void __launch_bounds__(kTpb) k_finish_prec(PrecArgs pa, const double*
         }
         pa.q[c] = qq;
       } else {
-#pragma unroll 8
-        for (int q = 0; q < pa.m; ++q) w = w + __ldg(Hc + static_cast<long long>(q) * pa.ldh) * tsm[q];
+        w = col_dot<B>(Hc, pa.ldh, tsm, pa.m);
       }
       z = z + *pa.neg_inv_beta * w;
     }
@@ -705,8 +746,9 @@ __global__ void __launch_bounds__(kTpb) k_finish_prec(PrecArgs pa, const double*
 void finish_precondition(const PrecArgs& pa, const double* svc, const double* t2, VSel vnext, VSel znext, int loop,
                          MinresState* st, const double* dots_edge, int n_edge_blocks, double* part,
                          unsigned* counter, cudaStream_t s) {
-  GNW_LAUNCH(launch_k(k_finish_prec, grid_for(pa.N), kTpb, std::max(pa.m, 1) * sizeof(double), s, 
-      pa, svc, t2, vnext, znext, loop, st, dots_edge, n_edge_blocks, part, counter));
+  GNW_LAUNCH(launch_k(pa.m >= kSweepBatchWideM ? k_finish_prec<16> : k_finish_prec<8>, grid_for(pa.N), kTpb,
+                      std::max(pa.m, 1) * sizeof(double), s, pa, svc, t2, vnext, znext, loop, st, dots_edge,
+                      n_edge_blocks, part, counter));
   check_launch("finish_precondition");
 }
 

@@ -17,14 +17,22 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--config", default="C2")
 ap.add_argument("--reps", type=int, default=3)
 ap.add_argument("--kernels", default="row_gemv,saddle,combine_prec,finish_prec,vcycle,update")
+ap.add_argument("--n", type=int, default=0, help="override: mesh n (J generated on the device)")
+ap.add_argument("--m", type=int, default=0, help="override: rows of J")
+ap.add_argument("--coarse-threshold", type=int, default=64)
 args = ap.parse_args()
 
-cfg = W.CONFIGS[args.config]
-inp = W.gnstep_inputs(cfg.n, cfg.m, cfg.index)
 ctx = Context(0)
-ctx.assemble(inp.mesh, AmgOptions(coarse_threshold=cfg.coarse_threshold))
+if args.n:  # e.g. C5 shapes: --n 1024 --m 3780 --coarse-threshold 1024
+    mesh = W.unit_square_mesh(args.n)
+    ctx.assemble(mesh, AmgOptions(coarse_threshold=args.coarse_threshold))
+    J = W.synthetic_jacobian_device(args.m, mesh.n_cells, 9, "cuda")
+else:
+    cfg = W.CONFIGS[args.config]
+    inp = W.gnstep_inputs(cfg.n, cfg.m, cfg.index)
+    ctx.assemble(inp.mesh, AmgOptions(coarse_threshold=cfg.coarse_threshold))
+    J = torch.from_numpy(inp.J).cuda()
 ctx.use_device_pointers(True)
-J = torch.from_numpy(inp.J).cuda()
 ctx.set_jacobian(J, 1e-2)
 names = args.kernels.split(",")
 for nm in names:  # warm-up (module load) outside the profiled range
