@@ -35,6 +35,8 @@ DCsr upload_csr(DeviceMemory& mem, const host::Csr& A, cudaStream_t s) {
 void DeviceAmg::reset() {
   bmem_.reset();
   bmem_b_ = 0;
+  collapse_l_ = -1;
+  collapse_M_ = nullptr;
   lv_.clear();
   mem_.release_all();
 }
@@ -90,6 +92,67 @@ void DeviceAmg::upload(const host::AmgHierarchy& h, cudaStream_t s) {
   GNW_CUDA_CHECK(cudaMemcpyAsync(coarse_L_, h.coarse_chol.data(), h.coarse_chol.size() * sizeof(double),
                                  cudaMemcpyHostToDevice, s));
   GNW_CUDA_CHECK(cudaStreamSynchronize(s));
+  build_collapse(s);
+}
+
+// Collapsed coarse tail.  Below some level the V-cycle is a small LINEAR map of that
+// level's residual (Jacobi smoothing, Galerkin restriction, coarse solve, prolongation --
+// amg.cpp:90-111 is linear in r), but it costs ~4 dependent launches per level.  At C2
+// levels 4..9 (1147 -> 171 rows) are 21 launches; the map itself is one 1147 x 1147 matrix
+// (10.5 MB, L2-resident) applied by one warp-per-row launch.  M is formed once per
+// hierarchy by running the sub-cycle on the unit vectors.  Default mode only: the exact
+// mode keeps the reference's level-by-level order.  Env GNW_VC_COLLAPSE=0 disables it.
+void DeviceAmg::build_collapse(cudaStream_t s) {
+  constexpr int kCollapseMax = 2048;
+  collapse_l_ = -1;
+  collapse_M_ = nullptr;
+  if (const char* e = std::getenv("GNW_VC_COLLAPSE"))
+    if (std::atoi(e) == 0) return;
+  const int L = static_cast<int>(lv_.size());
+  int lc = -1;
+  for (int l = 1; l < L - 1; ++l)
+    if (lv_[l].n <= kCollapseMax) {
+      lc = l;
+      break;
+    }
+  if (lc < 0) return;
+  const int n = lv_[lc].n;
+  DeviceMemory tmp;
+  double* I = tmp.alloc<double>(static_cast<size_t>(n) * n);
+  double* MT = tmp.alloc<double>(static_cast<size_t>(n) * n);
+  identity_rows(I, n, s);
+  for (int j = 0; j < n; ++j)  // row j of MT = sub-cycle(e_j) = column j of M
+    cycle_levels(lc, vfixed(I + static_cast<size_t>(j) * n), MT + static_cast<size_t>(j) * n, nullptr, 0, false, s);
+  collapse_M_ = mem_.alloc<double>(static_cast<size_t>(n) * n);
+  transpose_square(MT, collapse_M_, n, s);
+  GNW_CUDA_CHECK(cudaStreamSynchronize(s));
+  collapse_l_ = lc;
+}
+
+void DeviceAmg::cycle_levels(int l0, VSel r, double* out, const MinresState* st, int exact, bool collapse,
+                             cudaStream_t s) {
+  const int L = static_cast<int>(lv_.size());
+  const int stop = (collapse && collapse_l_ > l0) ? collapse_l_ : L - 1;
+  auto at = [&](int l) { return l == l0 ? r : vfixed(vr_[l]); };
+  for (int l = l0; l < stop; ++l) {
+    const DLevel lev = level(l, exact);
+    vc_down(lev, at(l), vres_[l], st, s);
+    vc_restrict(lev, vres_[l], vr_[l + 1], s);
+  }
+  double* e_stop = stop == l0 ? out : ve_[stop];
+  if (stop == L - 1) {
+    if (exact)
+      coarse_cholesky(coarse_L_, nc_, at(stop), e_stop, st, 1, 1, s);
+    else
+      coarse_inverse(coarse_inv_, nc_, at(stop), e_stop, st, 1, s);
+  } else {
+    coarse_inverse(collapse_M_, lv_[stop].n, at(stop), e_stop, st, 1, s);
+  }
+  for (int l = stop - 1; l >= l0; --l) {
+    const DLevel lev = level(l, exact);
+    vc_up1(lev, at(l), ve_[l + 1], vx_[l], st, s);
+    vc_up2(lev, at(l), vx_[l], l == l0 ? out : ve_[l], st, s);
+  }
 }
 
 // Level l as launched: the reference-order (thread-per-row) kernels everywhere in
@@ -103,6 +166,7 @@ DLevel DeviceAmg::level(int l, int exact) const {
 // amg.cpp:90-111, one symmetric V-cycle; level 0 input may be a ring slot.
 void DeviceAmg::vcycle(VSel r0, double* out0, const MinresState* st, int exact, cudaStream_t s) {
   const int L = static_cast<int>(lv_.size());
+  if (tail_cluster <= 0 && L > 1) return cycle_levels(0, r0, out0, st, exact, !exact && collapse_l_ > 0, s);
   auto coarse = [&](VSel r, double* x) {
     if (exact)
       coarse_cholesky(coarse_L_, nc_, r, x, st, 1, 1, s);
@@ -199,14 +263,18 @@ void DeviceAmg::vcycle_batch(const double* r0, int b, double* out0, int exact, c
     coarse(r0, out0);
     return;
   }
-  for (int l = 0; l < L - 1; ++l) {
+  const int stop = (!exact && collapse_l_ > 0) ? collapse_l_ : L - 1;  // as in cycle_levels
+  for (int l = 0; l < stop; ++l) {
     const double* rl = l == 0 ? r0 : mr_[l];
     const DLevel lev = level(l, exact);
     mvc_down(lev, rl, b, mres_[l], b, s);
     mvc_restrict(lev, mres_[l], mr_[l + 1], b, s);
   }
-  coarse(mr_[L - 1], me_[L - 1]);
-  for (int l = L - 2; l >= 0; --l) {
+  if (stop == L - 1)
+    coarse(mr_[L - 1], me_[L - 1]);
+  else
+    dense_emul_batch(collapse_M_, lv_[stop].n, mr_[stop], me_[stop], b, s);
+  for (int l = stop - 1; l >= 0; --l) {
     const double* rl = l == 0 ? r0 : mr_[l];
     const DLevel lev = level(l, exact);
     mvc_up1(lev, rl, b, me_[l + 1], mx_[l], b, s);

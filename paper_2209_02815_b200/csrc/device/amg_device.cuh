@@ -60,9 +60,16 @@ class DeviceAmg {
   double* batch_out() const { return bX0_; }
 
   int tail_cluster = 0;  // fused coarse tail (vcycle_tail.cu); 0 = off (env GNW_TAIL_CLUSTER)
+  int collapse_level() const { return collapse_l_; }
 
  private:
   DLevel level(int l, int exact) const;
+  // Levels [l0, L) of the cycle: r / out live at level l0.  With `collapse`, the levels from
+  // collapse_l_ down are replaced by the dense operator collapse_M_ (default mode only).
+  void cycle_levels(int l0, VSel r, double* out, const MinresState* st, int exact, bool collapse, cudaStream_t s);
+  void build_collapse(cudaStream_t s);
+  int collapse_l_ = -1;           // first level with n <= kCollapseMax above the coarsest, or -1
+  double* collapse_M_ = nullptr;  // n x n row-major: column j = the sub-cycle applied to e_j
   DeviceMemory mem_;
   std::vector<DLevel> lv_;
   double* coarse_inv_ = nullptr;

@@ -80,6 +80,10 @@ void mvc_up1(const DLevel& L, const double* r, int ldr, const double* ec, double
 void mvc_up2(const DLevel& L, const double* r, int ldr, const double* x, double* out, int ldo, int b,
              cudaStream_t s);
 void mcoarse_inverse(const double* Ainv, int n, const double* r, double* x, int b, cudaStream_t s);
+// collapsed coarse tail (amg_device.cu): batched dense apply, bit-identical per column to coarse_inverse
+void dense_emul_batch(const double* M, int n, const double* X, double* Y, int b, cudaStream_t s);
+void identity_rows(double* I, int n, cudaStream_t s);
+void transpose_square(const double* A, double* T, int n, cudaStream_t s);
 
 // rows [r0, r0+b) of a row-major (rows x cols) matrix -> cols x b interleaved
 void transpose_rows_to_batch(const double* A, long long cols, long long ld, int r0, int b, double* X,

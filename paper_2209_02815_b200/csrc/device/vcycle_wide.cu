@@ -156,6 +156,41 @@ __global__ void __launch_bounds__(256) k_mvce_up2(DCsr A, const double* __restri
   out[static_cast<long long>(i) * ldo + q] = x[static_cast<long long>(i) * b + q] + __ldg(&wd[i]) * res;
 }
 
+// ------------------------------------------------------- collapsed coarse tail
+// Y[:, q] = M X[:, q] for b interleaved columns, one thread per (row, column): the 32
+// register partials replay k_coarse_inverse's lane partition (lane l sums j = l, l+32, ...)
+// and its xor butterfly, so each column is bit-identical to the single-RHS dense apply.
+__global__ void __launch_bounds__(256) k_dense_emul_batch(const double* __restrict__ M, int n,
+                                                          const double* __restrict__ X, double* __restrict__ Y,
+                                                          int b) {
+  griddep_wait();
+  const int i = blockIdx.x * 8 + threadIdx.y;
+  const int q = blockIdx.y * 32 + threadIdx.x;
+  if (i >= n || q >= b) return;
+  double p[32];
+#pragma unroll
+  for (int l = 0; l < 32; ++l) p[l] = 0.0;
+  const double* __restrict__ Mi = M + static_cast<long long>(i) * n;
+  for (int g = 0; g < n; g += 32) {
+#pragma unroll
+    for (int l = 0; l < 32; ++l) {
+      const int j = g + l;
+      if (j < n) p[l] = p[l] + __ldg(&Mi[j]) * X[static_cast<long long>(j) * b + q];
+    }
+  }
+  Y[static_cast<long long>(i) * b + q] = tree32(p);
+}
+
+__global__ void k_identity_rows(double* __restrict__ I, int n) {
+  const long long k = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (k < static_cast<long long>(n) * n) I[k] = (k / n == k % n) ? 1.0 : 0.0;
+}
+
+__global__ void k_transpose_square(const double* __restrict__ A, double* __restrict__ T, int n) {
+  const long long k = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (k < static_cast<long long>(n) * n) T[k] = A[(k % n) * n + k / n];
+}
+
 // ------------------------------------------------------------------ launchers
 static unsigned wgrid(int rows) { return static_cast<unsigned>((rows + kRowsPerBlock - 1) / kRowsPerBlock); }
 
@@ -195,6 +230,22 @@ void mvce_up2(const DLevel& L, const double* r, int ldr, const double* x, double
   dim3 grid((L.n + 7) / 8, (b + 31) / 32), block(32, 8);
   GNW_LAUNCH(launch_k(k_mvce_up2, grid, block, 0, s, L.A, L.wd, r, ldr, x, out, ldo, b));
   note_launch("mvce_up2");
+}
+
+void dense_emul_batch(const double* M, int n, const double* X, double* Y, int b, cudaStream_t s) {
+  dim3 grid((n + 7) / 8, (b + 31) / 32), block(32, 8);
+  GNW_LAUNCH(launch_k(k_dense_emul_batch, grid, block, 0, s, M, n, X, Y, b));
+  note_launch("dense_emul_batch");
+}
+void identity_rows(double* I, int n, cudaStream_t s) {
+  const long long t = static_cast<long long>(n) * n;
+  k_identity_rows<<<static_cast<unsigned>((t + 255) / 256), 256, 0, s>>>(I, n);
+  note_launch("identity_rows");
+}
+void transpose_square(const double* A, double* T, int n, cudaStream_t s) {
+  const long long t = static_cast<long long>(n) * n;
+  k_transpose_square<<<static_cast<unsigned>((t + 255) / 256), 256, 0, s>>>(A, T, n);
+  note_launch("transpose_square");
 }
 
 }  // namespace gnw
