@@ -136,7 +136,7 @@ class Context {
   double *gpart_ = nullptr, *tpart_ = nullptr;
   RowGemv plan_{};    // J x (nothing runs beside it)
   RowGemv plan_h_{};  // H^T y (leaves CTA slots for the forked V-cycle)
-  int rg_reserve_ = 2;  // env GNW_RG_RESERVE
+  int rg_reserve_ = 1;  // env GNW_RG_RESERVE (C2 sweep: 0: 0.919, 1: 0.859, 2: 0.863 ms/iteration)
 
   // MINRES vectors
   double *b_ = nullptr, *x_ = nullptr, *r_ = nullptr, *az_ = nullptr, *tmp_ = nullptr, *tmp2_ = nullptr;
