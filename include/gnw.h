@@ -229,6 +229,31 @@ enum {
 gnw_status gnw_profile_kernel(gnw_ctx* ctx, int kernel, int reps, double* seconds_per_launch,
                               double* algorithmic_per_launch);
 
+/* ---------------------------------------------------------------------------
+ * Cell-partitioned multi-GPU solve (C3/C5).  One rank per GPU.
+ * Every rank assembles the same mesh and holds all sparse operators, the AMG
+ * hierarchy and the MINRES vectors; J and H are split by cell columns, rank r
+ * owning cells [c_lo, c_hi) (gnw_get_partition, known after gnw_assemble).
+ * gnw_set_jacobian then takes the m x (c_hi - c_lo) column slice J[:, c_lo:c_hi]
+ * (row stride c_hi - c_lo); all other vectors are full length and identical on
+ * every rank.  gnw_assemble, gnw_set_jacobian, gnw_assemble_rhs,
+ * gnw_apply_operator, gnw_precondition and gnw_minres_solve are collective: every
+ * rank calls them in the same order.  Results are bitwise identical on all ranks.
+ * The reference has no multi-GPU path; its single-process calls are the P = 1 case.
+ * ------------------------------------------------------------------------- */
+/* 128-byte NCCL unique id: created on one rank, broadcast by the caller. */
+gnw_status gnw_nccl_unique_id(unsigned char id[128]);
+/* One rank of a P-GPU group over NCCL (NVLink / NVSwitch), this process's device. */
+gnw_status gnw_create_partitioned(int device, int rank, int world, const unsigned char id[128], gnw_ctx** out);
+/* `world` ranks in THIS process on one device (out[0..world)), each driven by its
+ * own host thread; exchanges are host barriers plus device copies.  Same results as
+ * `world` GPUs over NCCL; used to test the partitioned path on one GPU. */
+gnw_status gnw_create_local_group(int device, int world, gnw_ctx** out);
+gnw_status gnw_get_partition(const gnw_ctx* ctx, int* rank, int* world, int64_t* c_lo, int64_t* c_hi);
+/* The partition rule (host only): lo[0..world], rank r owns cells [lo[r], lo[r+1]);
+ * boundaries are multiples of 64 cells. */
+gnw_status gnw_partition_cells(uint64_t n_cells, int world, int64_t* lo);
+
 #ifdef __cplusplus
 }
 #endif

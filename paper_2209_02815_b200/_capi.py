@@ -72,7 +72,8 @@ EXPORTED = [
     "gnw_get_woodbury", "gnw_assemble_rhs", "gnw_minres_solve", "gnw_export_csr",
     "gnw_export_mesh", "gnw_dense_cholesky", "gnw_get_stats", "gnw_event_record",
     "gnw_event_elapsed", "gnw_profile_kernel", "gnw_set_electrodes", "gnw_response_jacobian",
-    "gnw_geometric_factor",
+    "gnw_geometric_factor", "gnw_nccl_unique_id", "gnw_create_partitioned", "gnw_create_local_group",
+    "gnw_get_partition", "gnw_partition_cells",
 ]
 
 
@@ -130,6 +131,11 @@ def load() -> C.CDLL:
     L.gnw_set_electrodes.argtypes = [vp, vp, u64]
     L.gnw_response_jacobian.argtypes = [vp, vp, C.POINTER(ErtConfig), u64, vp, vp, dbl, C.POINTER(ErtStats)]
     L.gnw_geometric_factor.argtypes = [vp, vp, vp, vp, i32, C.POINTER(dbl)]
+    L.gnw_nccl_unique_id.argtypes = [vp]
+    L.gnw_create_partitioned.argtypes = [i32, i32, i32, vp, C.POINTER(vp)]
+    L.gnw_create_local_group.argtypes = [i32, i32, C.POINTER(vp)]
+    L.gnw_partition_cells.argtypes = [u64, i32, vp]
+    L.gnw_get_partition.argtypes = [vp, C.POINTER(i32), C.POINTER(i32), C.POINTER(C.c_int64), C.POINTER(C.c_int64)]
     for name in EXPORTED:
         fn = getattr(L, name)
         if name not in ("gnw_last_error", "gnw_version", "gnw_destroy"):

@@ -138,6 +138,17 @@ void Context::assemble(const double* vertices, int64_t nv, const int64_t* cells,
     GNW_CUDA_CHECK(cudaMemsetAsync(counters_, 0, 16 * sizeof(unsigned), stream_));
     GNW_CUDA_CHECK(cudaMemsetAsync(st_plain_, 0, sizeof(MinresState), stream_));
     upload_structure();
+    if (comm_) {  // cell partition (comm.cuh): J / H column slices and the J^T terms are rank-local
+      part_lo_ = partition_cells(N_, comm_->world);
+      for (int r = 0; r < comm_->world; ++r)
+        if (part_lo_[r + 1] == part_lo_[r])
+          throw std::invalid_argument("partition: a rank would own no cells (fewer than 64 cells per rank)");
+      c_lo_ = part_lo_[comm_->rank];
+      c_hi_ = part_lo_[comm_->rank + 1];
+      op_.c_lo = pa_.c_lo = c_lo_;
+      op_.c_hi = pa_.c_hi = c_hi_;
+      pa_.dist = 1;
+    }
     upload_hierarchy();
     sync();
   }
@@ -269,7 +280,7 @@ void Context::set_jacobian(const double* J, int64_t m, int64_t n_cells, double b
   require_mixed();
   if (timings) timings[0] = timings[1] = timings[2] = 0.0;
   if (m > 0 && !(beta > 0.0)) throw std::invalid_argument("build_woodbury_preconditioner: beta <= 0");
-  if (m > 0 && n_cells != N_) throw std::invalid_argument("build_woodbury_preconditioner: J shape mismatch");
+  if (m > 0 && n_cells != local_n()) throw std::invalid_argument("build_woodbury_preconditioner: J shape mismatch");
   require_device();
   m_ = m;
   beta_ = beta;
@@ -288,7 +299,7 @@ void Context::set_jacobian(const double* J, int64_t m, int64_t n_cells, double b
   if (m > 8192) throw std::invalid_argument("gnw_set_jacobian: m > 8192 not supported");
 
   const cudaStream_t s = stream_;
-  const size_t mN = static_cast<size_t>(m) * N_;
+  const long long Nl = local_n();  // columns of J / Ht held here (all N on one GPU)
   // Jacobian-shaped buffers persist across calls with the same (m, N, pointer
   // mode): no cudaMalloc/cudaFree (and no implied device sync) per GN step.
   const bool want_owned = ptr_mode != 1;
@@ -298,10 +309,10 @@ void Context::set_jacobian(const double* J, int64_t m, int64_t n_cells, double b
     jmem_ = std::make_unique<DeviceMemory>();
     DeviceMemory& jm = *jmem_;
     u_ = jm.alloc<double>(m);
-    plan_ = row_gemv_plan(N_, static_cast<int>(m));
-    plan_h_ = row_gemv_plan(N_, static_cast<int>(m), fork_ ? rg_reserve_ : 0);  // nchunks <= plan_'s
+    plan_ = row_gemv_plan(Nl, static_cast<int>(m));
+    plan_h_ = row_gemv_plan(Nl, static_cast<int>(m), fork_ ? rg_reserve_ : 0);  // nchunks <= plan_'s
     gpart_ = jm.alloc<double>(static_cast<size_t>(plan_.nchunks) * m);
-    ldh_ = N_ + pad_;
+    ldh_ = Nl + pad_;
     jown_ = want_owned ? jm.alloc<double>(static_cast<size_t>(m) * ldh_) : nullptr;
     dHt_ = jm.alloc<double>(static_cast<size_t>(m) * ldh_);
     dC_ = jm.alloc<double>(m * m);
@@ -312,8 +323,16 @@ void Context::set_jacobian(const double* J, int64_t m, int64_t n_cells, double b
     t2_ = jm.alloc<double>(m);
     tpart_ = jm.alloc<double>(static_cast<size_t>(plan_.nchunks) * m);
     dq_ = jm.alloc<double>(N_);
-    const DgemmPlan lo = dgemm_plan(static_cast<int>(m), N_, 0, sm_count_);
-    const DgemmPlan fu = dgemm_plan(static_cast<int>(m), N_, 1, sm_count_);
+    if (comm_) {
+      const int P = comm_->world;
+      u_part_ = jm.alloc<double>(m);
+      t_part_ = jm.alloc<double>(m);
+      gath_ = jm.alloc<double>(static_cast<size_t>(P) * std::max<int64_t>(m, 1));
+      Cpart_ = jm.alloc<double>(static_cast<size_t>(m) * m);
+      Cgath_ = jm.alloc<double>(static_cast<size_t>(P) * m * m);
+    }
+    const DgemmPlan lo = dgemm_plan(static_cast<int>(m), Nl, 0, sm_count_);
+    const DgemmPlan fu = dgemm_plan(static_cast<int>(m), Nl, 1, sm_count_);
     const size_t pl = static_cast<size_t>(lo.splits) * lo.npairs * lo.tile * lo.tile;
     const size_t pf = static_cast<size_t>(fu.splits) * fu.npairs * fu.tile * fu.tile;
     dpart_ = jm.alloc<double>(std::max(pl, pf) + 2 * 4096);
@@ -328,14 +347,14 @@ void Context::set_jacobian(const double* J, int64_t m, int64_t n_cells, double b
     // (inversion.hpp:21, :35); the caller keeps it alive while the context uses it.
     if (dJ_ != J) destroy_graph();  // the loop graph bakes the J pointer
     dJ_ = const_cast<double*>(J);
-    ldj_ = N_;
+    ldj_ = Nl;
     j_borrowed_ = true;
   } else {
     if (dJ_ != jown_) destroy_graph();
     dJ_ = jown_;
     ldj_ = ldh_;  // owned copy: padded rows like Ht
     j_borrowed_ = false;
-    GNW_CUDA_CHECK(cudaMemcpy2DAsync(dJ_, ldj_ * sizeof(double), J, N_ * sizeof(double), N_ * sizeof(double), m,
+    GNW_CUDA_CHECK(cudaMemcpy2DAsync(dJ_, ldj_ * sizeof(double), J, Nl * sizeof(double), Nl * sizeof(double), m,
                                      cudaMemcpyHostToDevice, s));
   }
   op_.J = dJ_;
@@ -366,8 +385,32 @@ void Context::set_jacobian(const double* J, int64_t m, int64_t n_cells, double b
       b = static_cast<int>(std::min<int64_t>(((m + 31) / 32) * 32, bmax));
       damg_.ensure_batch(b);
     }
+    if (comm_) {  // every rank must use the same batch width: the smallest proposal
+      double mine = b;
+      GNW_CUDA_CHECK(cudaMemcpyAsync(t_part_, &mine, sizeof(double), cudaMemcpyHostToDevice, s));
+      comm_->allgather(t_part_, gath_, 1, s);
+      std::vector<double> all(comm_->world);
+      GNW_CUDA_CHECK(cudaMemcpyAsync(all.data(), gath_, all.size() * sizeof(double), cudaMemcpyDeviceToHost, s));
+      sync();
+      b = static_cast<int>(*std::min_element(all.begin(), all.end()));
+    }
     for (int64_t i0 = 0; i0 < m; i0 += b) {
       const int bb = static_cast<int>(std::min<int64_t>(b, m - i0));
+      if (comm_) {
+        // partitioned: each rank packs its columns of J rows [i0, i0+bb) into the interleaved
+        // batch (cells are contiguous there), the slices are gathered, every rank runs the
+        // batched V-cycle and keeps its own cells of H
+        transpose_rows_to_batch(dJ_, Nl, ldj_, static_cast<int>(i0), bb, damg_.batch_in() + c_lo_ * bb, s);
+        std::vector<long long> off(comm_->world), cnt(comm_->world);
+        for (int r = 0; r < comm_->world; ++r) {
+          off[r] = part_lo_[r] * bb;
+          cnt[r] = (part_lo_[r + 1] - part_lo_[r]) * bb;
+        }
+        comm_->allgatherv(damg_.batch_in(), off, cnt, s);
+        damg_.vcycle_batch(damg_.batch_in(), bb, damg_.batch_out(), coarse_mode == 1, st_plain_, s);
+        transpose_batch_to_rows(damg_.batch_out() + c_lo_ * bb, Nl, ldh_, static_cast<int>(i0), bb, dHt_, s);
+        continue;
+      }
       transpose_rows_to_batch(dJ_, N_, ldj_, static_cast<int>(i0), bb, damg_.batch_in(), s);
       damg_.vcycle_batch(damg_.batch_in(), bb, damg_.batch_out(), coarse_mode == 1, st_plain_, s);
       transpose_batch_to_rows(damg_.batch_out(), N_, ldh_, static_cast<int>(i0), bb, dHt_, s);
@@ -375,9 +418,17 @@ void Context::set_jacobian(const double* J, int64_t m, int64_t n_cells, double b
     GNW_CUDA_CHECK(cudaEventRecord(ev[1], s));
   }
   // C = I + (J H)/beta (inversion.cpp:37-43), lower triangle
-  DgemmPlan plan = dgemm_plan(static_cast<int>(m), N_, 0, sm_count_);
+  DgemmPlan plan = dgemm_plan(static_cast<int>(m), Nl, 0, sm_count_);
+  // partitioned: C = I + (sum_r J_r H_r^T)/beta from the ranks' raw partials, fixed order
+  auto capacitance = [&](const DgemmPlan& pl) {
+    if (!comm_) return capacitance_dgemm(dJ_, ldj_, dHt_, ldh_, static_cast<int>(m), N_, beta, pl, dpart_, dC_, s);
+    fill_zero(Cpart_, m * m, s);
+    capacitance_dgemm(dJ_, ldj_, dHt_, ldh_, static_cast<int>(m), Nl, 0.0, pl, dpart_, Cpart_, s);
+    comm_->allgather(Cpart_, Cgath_, m * m, s);
+    capacitance_reduce(Cgath_, comm_->world, static_cast<int>(m), beta, dC_, s);
+  };
   {
-    capacitance_dgemm(dJ_, ldj_, dHt_, ldh_, static_cast<int>(m), N_, beta, plan, dpart_, dC_, s);
+    capacitance(plan);
     GNW_CUDA_CHECK(cudaEventRecord(ev[2], s));
     // L = chol(C), retry once after symmetrisation (inversion.cpp:21-35)
     cholesky_blocked(dC_, dY_, dL_, static_cast<int>(m), dflag_, s);
@@ -385,8 +436,8 @@ void Context::set_jacobian(const double* J, int64_t m, int64_t n_cells, double b
     GNW_CUDA_CHECK(cudaMemcpyAsync(&fail, dflag_, sizeof(int), cudaMemcpyDeviceToHost, s));
     sync();
     if (fail) {
-      DgemmPlan full = dgemm_plan(static_cast<int>(m), N_, 1, sm_count_);
-      capacitance_dgemm(dJ_, ldj_, dHt_, ldh_, static_cast<int>(m), N_, beta, full, dpart_, dC_, s);
+      DgemmPlan full = dgemm_plan(static_cast<int>(m), Nl, 1, sm_count_);
+      capacitance(full);
       symmetrize(dC_, static_cast<int>(m), s);
       cholesky_blocked(dC_, dY_, dL_, static_cast<int>(m), dflag_, s);
       GNW_CUDA_CHECK(cudaMemcpyAsync(&fail, dflag_, sizeof(int), cudaMemcpyDeviceToHost, s));
@@ -415,6 +466,17 @@ void Context::set_jacobian(const double* J, int64_t m, int64_t n_cells, double b
 // fused: the MINRES loop's A zhat takes J^T u from q = J^T t' (fused_active()).
 void Context::operator_into(VSel x, int scaled, VSel y, MinresState* st, int loop, bool fused) {
   OperatorArgs op = op_;
+  if (comm_) {  // partitioned: u = sum_r J_r x_r, then the own-cell J^T u, gather, delta
+    if (m_ > 0) {
+      row_gemv(dJ_, static_cast<int>(m_), c_hi_ - c_lo_, ldj_, x, K_ + c_lo_, scaled, st, gpart_, counters_ + 0,
+               u_part_, plan_, stream_);
+      reduce_m(u_part_, u_, m_, stream_);
+    }
+    saddle_operator(op, x, scaled, u_, y, st, 0, opart_, counters_ + 1, stream_);
+    gather_cells(resolve(y), stream_);
+    dist_delta(op, x, scaled, y, st, loop, opart_, counters_ + 1, stream_);
+    return;
+  }
   if (fused) {
     op.q = dq_;
   } else if (m_ > 0) {
@@ -424,7 +486,7 @@ void Context::operator_into(VSel x, int scaled, VSel y, MinresState* st, int loo
   saddle_operator(op, x, scaled, u_, y, st, loop, opart_, counters_ + 1, stream_);
 }
 
-bool Context::fused_active() const { return fused_ && m_ > 0 && pa_.m > 0 && dq_ != nullptr; }
+bool Context::fused_active() const { return fused_ && !comm_ && m_ > 0 && pa_.m > 0 && dq_ != nullptr; }
 
 void Context::apply_operator(const double* x, double* y) {
   require_mixed();
@@ -447,6 +509,18 @@ void Context::precondition_into(VSel y, VSel yv2, VSel z, MinresState* st, int l
   }
   const VSel az = loop ? vfixed(az_) : y;
   combine_elem(pa, az, vcur, vprev, y, z, loop, st, cpart_, stream_);
+  if (comm_) {  // partitioned: t = sum_r H_r^T y_r; z2 on own cells, gathered; then the Givens step
+    if (pa.m > 0) {
+      row_gemv(pa.Ht, pa.m, c_hi_ - c_lo_, pa.ldh, y, pa.K + c_lo_, 0, st, tpart_, counters_ + 2, t_part_, plan_h_, stream_);
+      reduce_m(t_part_, t_, pa.m, stream_);
+    }
+    vcycle(yv2, svc_, st);
+    capacitance_solve(pa, t_, t2_, stream_);
+    finish_precondition(pa, svc_, t2_, y, z, loop, st, cpart_, n_comb_blocks_, fpart_, counters_ + 3, stream_);
+    gather_cells(resolve(z), stream_);
+    dist_givens(pa, y, z, loop, st, cpart_, n_comb_blocks_, fpart_, counters_ + 3, stream_);
+    return;
+  }
   // s = B y2 and t = H^T y2 both read only y2: the V-cycle (latency-bound, few
   // CTAs on its coarse levels) runs on side_ beside the bandwidth-bound GEMV.
   const bool fork = fork_ && pa.m > 0;
@@ -507,6 +581,7 @@ void Context::assemble_rhs(const double* mdl, const double* mref, const double* 
   double* dr = ptr_mode == 1 ? rhs : io_c_;
   cudaEventRecord(e0, stream_);
   gnw::assemble_rhs(op_, beta_, dm, dmr, u_, dr, stream_);
+  if (comm_) gather_cells(dr, stream_);  // J^T (g - g_obs) / beta was formed on each rank's own cells
   cudaEventRecord(e1, stream_);
   stage_out(rhs, dr, K_ + N_);
   float ms = 0.f;
@@ -661,7 +736,8 @@ MinresResult Context::minres(const double* b, const double* x0, double* x, doubl
   st.status = maxit >= 1 ? kRunning : kMaxit;
   *h_st_ = st;
   GNW_CUDA_CHECK(cudaMemcpyAsync(st_, h_st_, sizeof(MinresState), cudaMemcpyHostToDevice, s));
-  if (!graph_exec_ && !no_graph_) {
+  const bool host_loop = no_graph_ || comm_ != nullptr;  // partitioned: exchanges between the phases
+  if (!graph_exec_ && !host_loop) {
     build_graph();
     built_now = graph_nodes_;
   }
@@ -675,7 +751,8 @@ MinresResult Context::minres(const double* b, const double* x0, double* x, doubl
   bool done = false;
   while (!done) {
     MinresState cur;
-    if (h_st_->status == kRunning && no_graph_) {  // host-driven loop (profiling): one sync per iteration
+    if (h_st_->status == kRunning && host_loop) {  // host-driven loop (profiling, partitioned): one sync per iteration
+      host_j_ = h_st_->j;
       launch_iteration(0, 0);
       GNW_CUDA_CHECK(cudaMemcpyAsync(h_st_, st_, sizeof(MinresState), cudaMemcpyDeviceToHost, s));
       sync();
@@ -686,7 +763,7 @@ MinresResult Context::minres(const double* b, const double* x0, double* x, doubl
       sync();
     }
     cur = *h_st_;
-    graph_iters = no_graph_ ? 0 : static_cast<uint64_t>(cur.iterations);  // direct launches are counted as issued
+    graph_iters = host_loop ? 0 : static_cast<uint64_t>(cur.iterations);  // direct launches are counted as issued
     switch (cur.status) {
       case kErrNotPD: throw std::runtime_error("minres: preconditioner is not positive definite");
       case kErrStagnated: throw std::runtime_error("minres: breakdown (stagnated rotation)");
@@ -746,6 +823,7 @@ MinresResult Context::minres(const double* b, const double* x0, double* x, doubl
 
 void Context::get_woodbury(double* H, double* L) {
   require_device();
+  if (comm_) throw std::invalid_argument("get_woodbury: H is partitioned across ranks");
   if (m_ == 0 || pa_.m == 0) return;
   if (H) {
     std::vector<double> ht(static_cast<size_t>(m_) * N_);

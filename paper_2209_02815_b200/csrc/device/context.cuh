@@ -11,6 +11,7 @@
 #include "../host/ert.hpp"
 #include "../host/setup.hpp"
 #include "amg_device.cuh"
+#include "comm.cuh"
 #include "kernels.cuh"
 
 namespace gnw {
@@ -62,6 +63,15 @@ class Context {
   double event_elapsed(int a, int b);
   void profile_kernel(int kernel, int reps, double* seconds, double* algorithmic);
   uint64_t last_iterations = 0;
+
+  // Cell-partitioned multi-GPU mode (comm.cuh); set before assemble.  J and
+  // the right-hand side's J^T term then cover only this rank's cells [c_lo, c_hi): set_jacobian
+  // takes the m x (c_hi - c_lo) column slice; every other vector stays full and replicated.
+  void set_comm(std::shared_ptr<Comm> c);
+  bool partitioned() const { return comm_ != nullptr; }
+  const Comm* comm() const { return comm_.get(); }
+  long long c_lo() const { return c_lo_; }
+  long long c_hi() const { return c_hi_; }
 
   // ERT forward model (forward.cpp:39-172) on the assembled mesh
   void set_electrodes(const int64_t* nodes, int64_t n);
@@ -175,6 +185,17 @@ class Context {
   cudaGraphExec_t graph_exec_ = nullptr;
   uint64_t graph_nodes_ = 0;
   int n_comb_blocks_ = 0;
+
+  // partitioned mode
+  std::shared_ptr<Comm> comm_;
+  std::vector<long long> part_lo_;  // world + 1 cell boundaries
+  long long c_lo_ = 0, c_hi_ = 0;
+  long long host_j_ = 0;            // iteration index mirrored on the host (ring slots of the exchanges)
+  double *u_part_ = nullptr, *t_part_ = nullptr, *gath_ = nullptr, *Cpart_ = nullptr, *Cgath_ = nullptr;
+  long long local_n() const { return comm_ ? c_hi_ - c_lo_ : N_; }
+  double* resolve(const VSel& v) const { return v.mod == 1 ? v.p[0] : v.p[(host_j_ + v.off) % v.mod]; }
+  void gather_cells(double* full, cudaStream_t s);                  // allgatherv of the cell part
+  void reduce_m(const double* part, double* out, long long n, cudaStream_t s);  // fixed-order allreduce
 
   // ERT forward model state
   std::vector<int64_t> electrodes_;

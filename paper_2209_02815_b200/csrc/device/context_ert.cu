@@ -38,6 +38,7 @@ void Context::response_jacobian(const double* mdl, const host::ErtConfig* cfgs, 
                                 double* g_out, double tol, ErtTimings* tm) {
   require_mixed();
   require_device();
+  if (comm_) throw std::invalid_argument("evaluate_response_and_jacobian: not available on a partitioned context");
   if (electrodes_.empty()) throw std::invalid_argument("evaluate_response_and_jacobian: electrode count mismatch");
   const int64_t ne = static_cast<int64_t>(electrodes_.size());
   const int64_t N = mesh_.nc;

@@ -19,19 +19,29 @@ struct gnw_ctx {
 namespace {
 thread_local std::string g_err;
 
+// A failed collective call on an in-process partitioned rank releases the other ranks'
+// barriers (they fail too) instead of leaving them waiting.
+void abandon(gnw_ctx* c) {
+  if (c && c->c && c->c->partitioned() && std::string(c->c->comm()->kind()) == "local")
+    static_cast<gnw::LocalComm*>(const_cast<gnw::Comm*>(c->c->comm()))->hub().abandon();
+}
+
 template <class F>
-gnw_status guard(F&& f) {
+gnw_status guard(F&& f, gnw_ctx* c = nullptr) {
   try {
     f();
     return GNW_OK;
   } catch (const std::invalid_argument& e) {
     g_err = e.what();
+    abandon(c);
     return GNW_INVALID_ARGUMENT;
   } catch (const gnw::DeviceError& e) {
     g_err = e.what();
+    abandon(c);
     return GNW_DEVICE;
   } catch (const std::exception& e) {
     g_err = e.what();
+    abandon(c);
     return GNW_NUMERICAL;
   }
 }
@@ -120,7 +130,7 @@ gnw_status gnw_assemble(gnw_ctx* ctx, const gnw_mesh* mesh, const gnw_amg_option
     if (!mesh || !mesh->vertices || !mesh->cells) throw std::invalid_argument("gnw_assemble: null mesh");
     ctx_of(ctx).assemble(mesh->vertices, static_cast<int64_t>(mesh->n_vertices), mesh->cells,
                          static_cast<int64_t>(mesh->n_cells), to_opts(opts));
-  });
+  }, ctx);
 }
 
 gnw_status gnw_assemble_amg_csr(gnw_ctx* ctx, uint64_t n, const int64_t* rowptr, const int64_t* cols,
@@ -157,14 +167,14 @@ gnw_status gnw_set_jacobian(gnw_ctx* ctx, const double* J, uint64_t m, uint64_t 
       timings->t_C = t[1];
       timings->t_chol = t[2];
     }
-  });
+  }, ctx);
 }
 
 gnw_status gnw_apply_operator(gnw_ctx* ctx, const double* x, double* y) {
-  return guard([&] { ctx_of(ctx).apply_operator(x, y); });
+  return guard([&] { ctx_of(ctx).apply_operator(x, y); }, ctx);
 }
 gnw_status gnw_precondition(gnw_ctx* ctx, const double* y, double* z) {
-  return guard([&] { ctx_of(ctx).precondition(y, z); });
+  return guard([&] { ctx_of(ctx).precondition(y, z); }, ctx);
 }
 gnw_status gnw_amg_apply(gnw_ctx* ctx, const double* r, double* z) {
   return guard([&] { ctx_of(ctx).amg_apply(r, z); });
@@ -174,7 +184,7 @@ gnw_status gnw_get_woodbury(gnw_ctx* ctx, double* H, double* L) {
 }
 gnw_status gnw_assemble_rhs(gnw_ctx* ctx, const double* m, const double* m_ref, const double* g, const double* g_obs,
                             double* rhs) {
-  return guard([&] { ctx_of(ctx).assemble_rhs(m, m_ref, g, g_obs, rhs); });
+  return guard([&] { ctx_of(ctx).assemble_rhs(m, m_ref, g, g_obs, rhs); }, ctx);
 }
 
 gnw_status gnw_minres_solve(gnw_ctx* ctx, const double* b, const double* x0, double* x, double tol, uint64_t maxit,
@@ -192,6 +202,74 @@ gnw_status gnw_minres_solve(gnw_ctx* ctx, const double* b, const double* x0, dou
         if (report->pnorm_relative_residuals) report->pnorm_relative_residuals[k] = r.hist_p[k];
       }
     }
+  }, ctx);
+}
+
+// ------------------------------------------------------- partitioned contexts
+gnw_status gnw_nccl_unique_id(unsigned char id[128]) {
+  return guard([&] {
+    if (!id) throw std::invalid_argument("gnw_nccl_unique_id: null output");
+    gnw::nccl_unique_id(id);
+  });
+}
+
+gnw_status gnw_create_partitioned(int device, int rank, int world, const unsigned char id[128], gnw_ctx** out) {
+  return guard([&] {
+    if (!out || !id) throw std::invalid_argument("gnw_create_partitioned: null argument");
+    *out = nullptr;
+    if (world < 1 || rank < 0 || rank >= world) throw std::invalid_argument("gnw_create_partitioned: bad rank/world");
+    auto* h = new gnw_ctx;
+    try {
+      h->c = new Context(device);
+      h->c->set_comm(std::make_shared<gnw::NcclComm>(id, rank, world, device));
+    } catch (...) {
+      delete h->c;
+      delete h;
+      throw;
+    }
+    *out = h;
+  });
+}
+
+gnw_status gnw_create_local_group(int device, int world, gnw_ctx** out) {
+  return guard([&] {
+    if (!out) throw std::invalid_argument("gnw_create_local_group: null output");
+    if (world < 1) throw std::invalid_argument("gnw_create_local_group: world size must be >= 1");
+    auto hub = std::make_shared<gnw::LocalHub>(world);
+    std::vector<gnw_ctx*> made;
+    try {
+      for (int r = 0; r < world; ++r) {
+        auto* h = new gnw_ctx;
+        made.push_back(h);
+        h->c = new Context(device);
+        h->c->set_comm(std::make_shared<gnw::LocalComm>(hub, r));
+      }
+    } catch (...) {
+      for (gnw_ctx* h : made) {
+        delete h->c;
+        delete h;
+      }
+      throw;
+    }
+    for (int r = 0; r < world; ++r) out[r] = made[r];
+  });
+}
+
+gnw_status gnw_partition_cells(uint64_t n_cells, int world, int64_t* lo) {
+  return guard([&] {
+    if (!lo) throw std::invalid_argument("gnw_partition_cells: null output");
+    const std::vector<long long> p = gnw::partition_cells(static_cast<long long>(n_cells), world);
+    for (size_t r = 0; r < p.size(); ++r) lo[r] = p[r];
+  });
+}
+
+gnw_status gnw_get_partition(const gnw_ctx* ctx, int* rank, int* world, int64_t* c_lo, int64_t* c_hi) {
+  return guard([&] {
+    const Context& c = ctx_of(ctx);
+    if (rank) *rank = c.partitioned() ? c.comm()->rank : 0;
+    if (world) *world = c.partitioned() ? c.comm()->world : 1;
+    if (c_lo) *c_lo = c.partitioned() ? c.c_lo() : 0;
+    if (c_hi) *c_hi = c.partitioned() ? c.c_hi() : c.N();
   });
 }
 

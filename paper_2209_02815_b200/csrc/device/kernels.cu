@@ -554,8 +554,8 @@ __global__ void __launch_bounds__(kTpb) k_saddle(OperatorArgs op, VSel xs, int s
       o = o + 1.0 * sd;  // spmv_add(*D, zeta, 1.0, out2)
       if (op.m > 0 && op.q != nullptr) {  // fused: J^T (J zhat2) = J^T (t' * ig) ~ q * ig (Woodbury identity J z2 = t')
         o = o + *op.neg_inv_beta * (op.q[c] * sc);
-      } else if (op.m > 0) {  // matvec_transpose(J, J dm), linalg.cpp:45-54
-        const double jt = col_dot<8>(op.J + c, op.ldj, usm, op.m);
+      } else if (op.m > 0 && c >= op.c_lo && (op.c_hi < 0 || c < op.c_hi)) {  // matvec_transpose(J, J dm), linalg.cpp:45-54
+        const double jt = col_dot<8>(op.J + (c - op.c_lo), op.ldj, usm, op.m);
         o = o + *op.neg_inv_beta * jt;  // axpy(-1.0 / beta, jtjdm, out2)
       }
       y[op.K + c] = o;
@@ -662,6 +662,9 @@ void capacitance_solve(const PrecArgs& pa, const double* t, double* t2, cudaStre
   check_launch("capacitance_solve");
 }
 
+__device__ void finish_scalars(const double (&tot)[3], const double* __restrict__ dots_edge, int n_edge_blocks,
+                               int loop, MinresState* st, double* red);
+
 template <int B>
 __global__ void __launch_bounds__(kTpb) k_finish_prec(PrecArgs pa, const double* __restrict__ svc,
                                                       const double* __restrict__ t2, VSel vns, VSel zns, int loop,
@@ -677,12 +680,12 @@ __global__ void __launch_bounds__(kTpb) k_finish_prec(PrecArgs pa, const double*
     __syncthreads();
   }
   double d[3] = {0.0, 0.0, 0.0};
-  const long long c = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (c < pa.N) {
+  const long long c = pa.c_lo + static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (c < (pa.c_hi < 0 ? pa.N : pa.c_hi)) {
     double z = svc[c];
     if (pa.m > 0) {  // w = matvec(h_hat, t) row c (linalg.cpp:33-43); s += (-1/beta) w
       double w = 0.0;
-      const double* __restrict__ Hc = pa.Ht + c;
+      const double* __restrict__ Hc = pa.Ht + (c - pa.c_lo);
       if (pa.q != nullptr) {  // one sweep over H and J: w = (H t')_c, q_c = (J^T t')_c
         const double* __restrict__ Jc = pa.J + c;
         double qq = 0.0;
@@ -703,9 +706,16 @@ __global__ void __launch_bounds__(kTpb) k_finish_prec(PrecArgs pa, const double*
     d[0] = z * v;
     d[1] = z * z;
   }
+  if (pa.dist) return;  // partitioned: dist_givens reduces once the cells are gathered
   double tot[3];
   if (!grid_reduce_last<3>(d, part, counter, red, tot)) return;
-  // add the combine kernel's partials (edge blocks: all three; cell blocks: <v,v>)
+  finish_scalars(tot, dots_edge, n_edge_blocks, loop, st, red);
+}
+
+// k_finish_prec's tail: add the combine kernel's partials (edge blocks: all three; cell
+// blocks: <v,v>) to the cell totals, then gamma_next and the Givens rotation.
+__device__ void finish_scalars(const double (&tot)[3], const double* __restrict__ dots_edge, int n_edge_blocks,
+                               int loop, MinresState* st, double* red) {
   double e3[3] = {0.0, 0.0, 0.0};
   for (int b = threadIdx.x; b < n_edge_blocks; b += blockDim.x)
     for (int k = 0; k < 3; ++k) e3[k] += __ldcg(&dots_edge[b * 3 + k]);
@@ -743,13 +753,115 @@ __global__ void __launch_bounds__(kTpb) k_finish_prec(PrecArgs pa, const double*
   st->eta = -st->s_next * st->eta;
 }
 
+int finish_blocks(const PrecArgs& pa) {
+  return static_cast<int>(grid_for((pa.c_hi < 0 ? pa.N : pa.c_hi) - pa.c_lo));
+}
+
 void finish_precondition(const PrecArgs& pa, const double* svc, const double* t2, VSel vnext, VSel znext, int loop,
                          MinresState* st, const double* dots_edge, int n_edge_blocks, double* part,
                          unsigned* counter, cudaStream_t s) {
-  GNW_LAUNCH(launch_k(pa.m >= kSweepBatchWideM ? k_finish_prec<16> : k_finish_prec<8>, grid_for(pa.N), kTpb,
+  GNW_LAUNCH(launch_k(pa.m >= kSweepBatchWideM ? k_finish_prec<16> : k_finish_prec<8>, finish_blocks(pa), kTpb,
                       std::max(pa.m, 1) * sizeof(double), s, pa, svc, t2, vnext, znext, loop, st, dots_edge,
                       n_edge_blocks, part, counter));
   check_launch("finish_precondition");
+}
+
+// ======================================================================
+// Partitioned (multi-GPU) solve: the reductions that follow a cell gather
+// ======================================================================
+// delta = <y, zhat>: k_saddle's dot, with its block partition (edge blocks, then cell
+// blocks) so that one rank reproduces the single-GPU delta bit for bit.
+__global__ void __launch_bounds__(kTpb) k_dist_delta(long long K, long long N, VSel zs, int scaled, VSel ys,
+                                                     MinresState* st, int loop, int nb_edge, double* part,
+                                                     unsigned* counter) {
+  griddep_wait();
+  __shared__ double red[kTpb / 32];
+  const double* __restrict__ z = vsel(zs, st);
+  const double* __restrict__ y = vsel(ys, st);
+  const double sc = scaled ? st->inv_gamma : 1.0;
+  double dotv[1] = {0.0};
+  const long long i = static_cast<int>(blockIdx.x) < nb_edge
+                          ? static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x
+                          : K + static_cast<long long>(blockIdx.x - nb_edge) * blockDim.x + threadIdx.x;
+  const bool ok = static_cast<int>(blockIdx.x) < nb_edge ? i < K : i < K + N;
+  if (ok) dotv[0] = y[i] * (scaled ? z[i] * sc : z[i]);
+  double tot[1];
+  if (grid_reduce_last<1>(dotv, part, counter, red, tot) && threadIdx.x == 0) {
+    const double delta = tot[0];
+    if (loop) {
+      st->delta = delta;
+      st->coef_v1 = -delta / st->gamma_cur;
+      st->coef_v2 = -st->gamma_cur / st->gamma_prev;
+    } else {
+      st->scratch[0] = delta;
+    }
+  }
+}
+
+void dist_delta(const OperatorArgs& op, VSel z, int scaled, VSel y, MinresState* st, int loop, double* part,
+                unsigned* counter, cudaStream_t s) {
+  const int nbe = static_cast<int>(grid_for(op.K)), nbc = static_cast<int>(grid_for(op.N));
+  GNW_LAUNCH(launch_k(k_dist_delta, nbe + nbc, kTpb, 0, s, op.K, op.N, z, scaled, y, st, loop, nbe, part, counter));
+  check_launch("dist_delta");
+}
+
+// <z, v>, <z, z> over all cells with k_finish_prec's block partition, then its tail.
+__global__ void __launch_bounds__(kTpb) k_dist_givens(long long K, long long N, VSel vns, VSel zns, int loop,
+                                                      MinresState* st, const double* __restrict__ dots_edge,
+                                                      int n_edge_blocks, double* part, unsigned* counter) {
+  griddep_wait();
+  __shared__ double red[3 * (kTpb / 32)];
+  const double* __restrict__ vn = vsel(vns, st);
+  const double* __restrict__ zn = vsel(zns, st);
+  double d[3] = {0.0, 0.0, 0.0};
+  const long long c = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (c < N) {
+    const double z = zn[K + c];
+    d[0] = z * vn[K + c];
+    d[1] = z * z;
+  }
+  double tot[3];
+  if (!grid_reduce_last<3>(d, part, counter, red, tot)) return;
+  finish_scalars(tot, dots_edge, n_edge_blocks, loop, st, red);
+}
+
+void dist_givens(const PrecArgs& pa, VSel vn, VSel zn, int loop, MinresState* st, const double* dots_edge,
+                 int n_edge_blocks, double* part, unsigned* counter, cudaStream_t s) {
+  GNW_LAUNCH(launch_k(k_dist_givens, grid_for(pa.N), kTpb, 0, s, pa.K, pa.N, vn, zn, loop, st, dots_edge,
+                      n_edge_blocks, part, counter));
+  check_launch("dist_givens");
+}
+
+__global__ void k_sum_partials(const double* __restrict__ parts, int P, long long n, double* __restrict__ out) {
+  griddep_wait();
+  const long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double s = 0.0;
+  for (int r = 0; r < P; ++r) s += parts[static_cast<long long>(r) * n + i];
+  out[i] = s;
+}
+
+void sum_partials(const double* parts, int P, long long n, double* out, cudaStream_t s) {
+  GNW_LAUNCH(launch_k(k_sum_partials, grid_for(n), kTpb, 0, s, parts, P, n, out));
+  check_launch("sum_partials");
+}
+
+__global__ void k_capacitance_reduce(const double* __restrict__ parts, int P, int m, double beta,
+                                     double* __restrict__ C) {
+  griddep_wait();
+  const long long k = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const long long mm = static_cast<long long>(m) * m;
+  if (k >= mm) return;
+  double s = 0.0;
+  for (int r = 0; r < P; ++r) s += parts[r * mm + k];
+  double v = s / beta;
+  if (k / m == k % m) v += 1.0;
+  C[k] = v;
+}
+
+void capacitance_reduce(const double* parts, int P, int m, double beta, double* C, cudaStream_t s) {
+  GNW_LAUNCH(launch_k(k_capacitance_reduce, grid_for(static_cast<long long>(m) * m), kTpb, 0, s, parts, P, m, beta, C));
+  check_launch("capacitance_reduce");
 }
 
 // ======================================================================
@@ -914,9 +1026,9 @@ __global__ void __launch_bounds__(kTpb) k_rhs(OperatorArgs op, double beta, cons
     for (int t = threadIdx.x; t < op.m; t += blockDim.x) gsm[t] = dg[t];
     __syncthreads();
     const long long c = static_cast<long long>(blockIdx.x - nb_edge) * blockDim.x + threadIdx.x;
-    if (c >= op.N) return;
+    if (c >= op.N || c < op.c_lo || (op.c_hi >= 0 && c >= op.c_hi)) return;  // partition: own cells only
     double jt = 0.0;
-    const double* __restrict__ Jc = op.J + c;
+    const double* __restrict__ Jc = op.J + (c - op.c_lo);
 #pragma unroll 8
     for (int i = 0; i < op.m; ++i) jt = jt + __ldg(Jc + static_cast<long long>(i) * op.ldj) * gsm[i];
     rhs[op.K + c] = jt / beta;
@@ -1056,6 +1168,10 @@ __global__ void k_dgemm_finalize(const double* __restrict__ part, const int2* __
   if (i >= m || j >= m) return;
   double s = 0.0;
   for (int k = 0; k < splits; ++k) s += part[(static_cast<long long>(k) * npairs + p) * (BM * BN) + e];
+  if (beta <= 0.0) {  // raw partial J_g H_g^T of one rank (partitioned capacitance)
+    C[static_cast<long long>(i) * m + j] = s;
+    return;
+  }
   double v = s / beta;
   if (i == j) v += 1.0;
   C[static_cast<long long>(i) * m + j] = v;

@@ -85,6 +85,7 @@ void dense_emul_batch(const double* M, int n, const double* X, double* Y, int b,
 void identity_rows(double* I, int n, cudaStream_t s);
 void transpose_square(const double* A, double* T, int n, cudaStream_t s);
 
+
 // rows [r0, r0+b) of a row-major (rows x cols) matrix -> cols x b interleaved
 void transpose_rows_to_batch(const double* A, long long cols, long long ld, int r0, int b, double* X,
                              cudaStream_t s);
@@ -103,6 +104,9 @@ struct OperatorArgs {
   // Woodbury-fused loop: J^T u = (J^T t') / gamma with q = J^T t'
   // produced by the previous preconditioner pass; J is then not read by the operator.
   const double* q = nullptr;
+  // cell partition (multi-GPU): J holds only the columns [c_lo, c_hi) of this
+  // rank (J + (c - c_lo) is column c); c_hi < 0 means N (single GPU)
+  long long c_lo = 0, c_hi = -1;
 };
 
 // u = A[:, ] x2 * scale partial GEMV over rows of a row-major (m x N) matrix,
@@ -137,6 +141,10 @@ struct PrecArgs {
   // fused loop: the finish pass also forms q = J^T t' (J read in the same sweep as H)
   const double* J = nullptr;
   double* q = nullptr;
+  // cell partition: Ht holds the columns [c_lo, c_hi); dist != 0: the finish pass only
+  // writes z for those cells (no reductions -- the partitioned driver reduces after the gather)
+  long long c_lo = 0, c_hi = -1;
+  int dist = 0;
 };
 
 // v_next = Az + c1 v_cur + c2 v_prev (combine, minres.cpp:76-77) or, when
@@ -153,6 +161,7 @@ void combine_precondition(const PrecArgs& pa, VSel az, VSel vcur, VSel vprev, VS
 void capacitance_solve(const PrecArgs& pa, const double* t, double* t2, cudaStream_t s);
 // z2 = s + (-1/beta) H t2; dots <z, v>, ||z||^2; last block: Givens update
 // (minres.cpp:78-101) when loop, else totals to st->scratch.
+int finish_blocks(const PrecArgs& pa);
 void finish_precondition(const PrecArgs& pa, const double* svc, const double* t2, VSel vnext,
                          VSel znext, int loop, MinresState* st, const double* dots_edge,
                          int n_edge_blocks, double* part, unsigned* counter, cudaStream_t s);
@@ -201,5 +210,18 @@ void symmetrize(double* C, int n, cudaStream_t s);
 void cholesky_inverse(const double* L, double* Y, double* Cinv, int n, cudaStream_t s);
 
 void fill_zero(double* p, long long n, cudaStream_t s);
+
+// ---- partitioned (multi-GPU) solve helpers (context_dist.cu) ----
+// delta = <y, zhat> over all K+N (same block partition as k_saddle) -> st (loop) / st->scratch[0]
+void dist_delta(const OperatorArgs& op, VSel z, int scaled, VSel y, MinresState* st, int loop, double* part,
+                unsigned* counter, cudaStream_t s);
+// <z,v>, <z,z> over the cells (same block partition as k_finish_prec) + the combine pass's
+// partials -> gamma_next and the Givens rotation (minres.cpp:79-101), as k_finish_prec's tail
+void dist_givens(const PrecArgs& pa, VSel vn, VSel zn, int loop, MinresState* st, const double* dots_edge,
+                 int n_edge_blocks, double* part, unsigned* counter, cudaStream_t s);
+// out[i] = sum_{r < P} parts[r * n + i], r ascending (deterministic allreduce body)
+void sum_partials(const double* parts, int P, long long n, double* out, cudaStream_t s);
+// C = I + (sum_r parts[r]) / beta, parts m x m each (capacitance, inversion.cpp:37-43)
+void capacitance_reduce(const double* parts, int P, int m, double beta, double* C, cudaStream_t s);
 
 }  // namespace gnw

@@ -55,6 +55,41 @@ class Context:
         self.device_pointers = False
         self.K = self.N = self.m = 0
 
+    # ------------------------------------------------ partitioned (multi-GPU)
+    @classmethod
+    def _adopt(cls, handle, device):
+        self = cls.__new__(cls)
+        self.L = A.load()
+        self.h = handle
+        self.device = device
+        self.device_pointers = False
+        self.K = self.N = self.m = 0
+        return self
+
+    @classmethod
+    def partitioned(cls, rank: int, world: int, nccl_id: bytes, device: int = 0) -> "Context":
+        """One rank of a cell-partitioned P-GPU solve over NCCL (gnw_create_partitioned)."""
+        L = A.load()
+        buf = (C.c_ubyte * 128).from_buffer_copy(bytes(nccl_id))
+        h = C.c_void_p()
+        A.check(L.gnw_create_partitioned(device, rank, world, buf, C.byref(h)))
+        return cls._adopt(h, device)
+
+    @classmethod
+    def local_group(cls, world: int, device: int = 0) -> list:
+        """``world`` partitioned ranks in this process on one device; drive each from its own
+        thread (``run_ranks``).  Same results as ``world`` GPUs over NCCL."""
+        L = A.load()
+        hs = (C.c_void_p * world)()
+        A.check(L.gnw_create_local_group(device, world, hs))
+        return [cls._adopt(C.c_void_p(hs[r]), device) for r in range(world)]
+
+    def partition(self) -> dict:
+        r, w = C.c_int(), C.c_int()
+        lo, hi = C.c_int64(), C.c_int64()
+        A.check(self.L.gnw_get_partition(self.h, C.byref(r), C.byref(w), C.byref(lo), C.byref(hi)))
+        return {"rank": r.value, "world": w.value, "c_lo": lo.value, "c_hi": hi.value}
+
     def close(self):
         if getattr(self, "h", None) and self.h.value:
             self.L.gnw_destroy(self.h)
@@ -292,3 +327,53 @@ def assemble_gn_rhs(ctx: Context, m, m_ref, g, g_obs):
 
 def minres(ctx: Context, b, x0=None, tol: float = 1e-8, maxit: int | None = None):
     return ctx.minres(b, x0, tol, maxit)
+
+
+# ------------------------------------------------------------ partitioned helpers
+def nccl_unique_id() -> bytes:
+    """128-byte NCCL unique id for gnw_create_partitioned (create on one rank, broadcast)."""
+    buf = (C.c_ubyte * 128)()
+    A.check(A.load().gnw_nccl_unique_id(buf))
+    return bytes(buf)
+
+
+def partition_cells(n_cells: int, world: int) -> np.ndarray:
+    """Cell boundaries of the partitioned solve (gnw_partition_cells): rank r owns [lo[r], lo[r+1])."""
+    lo = np.zeros(world + 1, dtype=np.int64)
+    A.check(A.load().gnw_partition_cells(n_cells, world, lo.ctypes.data))
+    return lo
+
+
+def partitioned_from_torch_distributed(device: int) -> Context:
+    """The calling rank's partitioned context: rank 0 makes the NCCL id and the initialised
+    torch.distributed group (any backend) broadcasts it."""
+    import torch.distributed as dist
+
+    obj = [nccl_unique_id() if dist.get_rank() == 0 else None]
+    dist.broadcast_object_list(obj, src=0)
+    return Context.partitioned(dist.get_rank(), dist.get_world_size(), obj[0], device)
+
+
+def run_ranks(ctxs, fn):
+    """Run ``fn(ctx, rank)`` for every in-process rank on its own thread (the collective calls
+    of a local group must run concurrently); returns the per-rank results, re-raises the first
+    failure."""
+    import threading
+
+    out, err = [None] * len(ctxs), [None] * len(ctxs)
+
+    def body(r):
+        try:
+            out[r] = fn(ctxs[r], r)
+        except BaseException as e:  # noqa: BLE001 -- re-raised below
+            err[r] = e
+
+    ts = [threading.Thread(target=body, args=(r,)) for r in range(len(ctxs))]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    primary = [e for e in err if e is not None and "another rank failed" not in str(e)]
+    for e in primary + [e for e in err if e is not None]:
+        raise e
+    return out

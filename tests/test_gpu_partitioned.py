@@ -1,0 +1,96 @@
+"""Cell-partitioned multi-GPU solve on one GPU: P ranks as threads of one
+process (gnw_create_local_group; every exchange is a host barrier plus device copies, so no
+kernel waits on another rank's kernel) and the NCCL path at world size 1.  Bars: P = 1 is
+bitwise the single-GPU solver; P > 1 is the same solve up to the order of the m-vector sums
+(iterations equal, solutions within 1e-10)."""
+import numpy as np
+import pytest
+
+from paper_2209_02815_b200 import AmgOptions, Context, nccl_unique_id, run_ranks, workload as W
+
+pytestmark = pytest.mark.gpu
+
+
+def problem(n=32, m=16, index=0):
+    inp = W.gnstep_inputs(n, m, index)
+    return inp
+
+
+def single(inp, alpha, tol):
+    c = Context(0)
+    c.assemble(inp.mesh)
+    c.set_jacobian(inp.J, alpha)
+    b = c.assemble_rhs(inp.dm, np.zeros(c.N), inp.dg, np.zeros(inp.J.shape[0]))
+    x, rep = c.minres(b, tol=tol)
+    y = c.apply_operator(b)
+    z = c.precondition(b)
+    return b, x, rep, y, z
+
+
+def partitioned(ctxs, inp, alpha, tol):
+    def body(c, r):
+        c.assemble(inp.mesh)
+        p = c.partition()
+        assert p["rank"] == r and p["world"] == len(ctxs)
+        c.set_jacobian(np.ascontiguousarray(inp.J[:, p["c_lo"]:p["c_hi"]]), alpha)
+        b = c.assemble_rhs(inp.dm, np.zeros(c.N), inp.dg, np.zeros(inp.J.shape[0]))
+        x, rep = c.minres(b, tol=tol)
+        return b, x, rep, c.apply_operator(b), c.precondition(b), p
+    return run_ranks(ctxs, body)
+
+
+def test_local_group_world1_is_bitwise_single_gpu():
+    inp = problem()
+    b0, x0, r0, y0, z0 = single(inp, 1e-2, 1e-10)
+    (b1, x1, r1, y1, z1, _), = partitioned(Context.local_group(1), inp, 1e-2, 1e-10)
+    assert np.array_equal(b0, b1)
+    assert np.array_equal(y0, y1) and np.array_equal(z0, z1)
+    assert r1.iterations == r0.iterations
+    assert np.array_equal(x0, x1)
+
+
+@pytest.mark.parametrize("world", [2, 3, 4])
+def test_local_group_matches_single_gpu(world):
+    inp = problem(64, 32, 0)
+    b0, x0, r0, y0, z0 = single(inp, 1e-2, 1e-10)
+    res = partitioned(Context.local_group(world), inp, 1e-2, 1e-10)
+    los = [p["c_lo"] for *_, p in res] + [res[-1][-1]["c_hi"]]
+    assert los[0] == 0 and los[-1] == inp.mesh.n_cells and all(a < b for a, b in zip(los, los[1:]))
+    for b, x, rep, y, z, _ in res:
+        # every rank holds the same bits
+        assert np.array_equal(b, res[0][0]) and np.array_equal(x, res[0][1])
+        assert rep.iterations == res[0][2].iterations
+    b, x, rep, y, z, _ = res[0]
+    rel = lambda a, c: np.linalg.norm(a - c) / np.linalg.norm(c)
+    assert rel(b, b0) <= 1e-14
+    assert rel(y, y0) <= 1e-13 and rel(z, z0) <= 1e-13
+    # the m-vector sums run in rank order instead of span order: rounding-level differences,
+    # which near a tight tol can move the stopping iteration (the reference's own FMA and
+    # non-FMA builds differ the same way); the early history is unaffected
+    h, h0 = rep.relative_residuals, r0.relative_residuals
+    assert np.allclose(h[:40], h0[:40], rtol=1e-6, atol=0)
+    assert abs(rep.iterations - r0.iterations) <= 2
+    assert rep.converged and rel(x, x0) <= 1e-8, rel(x, x0)
+
+
+def test_local_group_laplace_and_errors():
+    inp = problem(32, 16, 0)
+    ctxs = Context.local_group(2)
+
+    def bad(c, r):
+        c.assemble(inp.mesh)
+        p = c.partition()
+        cols = p["c_hi"] - p["c_lo"] + (1 if r == 1 else 0)  # rank 1 passes a wrong slice
+        c.set_jacobian(np.zeros((16, cols)), 1e-2)
+
+    with pytest.raises(ValueError, match="J shape mismatch"):
+        run_ranks(ctxs, bad)
+
+
+def test_nccl_world1_is_bitwise_single_gpu():
+    inp = problem()
+    b0, x0, r0, y0, z0 = single(inp, 1e-2, 1e-10)
+    c = Context.partitioned(0, 1, nccl_unique_id(), 0)
+    (b1, x1, r1, y1, z1, p), = partitioned([c], inp, 1e-2, 1e-10)
+    assert p == {"rank": 0, "world": 1, "c_lo": 0, "c_hi": inp.mesh.n_cells}
+    assert np.array_equal(b0, b1) and np.array_equal(x0, x1) and r1.iterations == r0.iterations
