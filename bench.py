@@ -451,6 +451,110 @@ def run_gnw(args):
         torch.distributed.destroy_process_group()
 
 
+def run_partitioned(args):
+    """--partitioned: ONE GN-step solve split over N GPUs by cell columns (SURVEY 8(e), C3/C5
+    scale; `scaling` strong).  Every rank builds its J column slice on its device (distributed
+    CholeskyQR2), the ranks exchange through NCCL inside libgnw (gnw_create_partitioned)."""
+    import torch
+
+    ws, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    if ws > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_2209_02815_b200 import (AmgOptions, Context, nccl_unique_id, partitioned_from_torch_distributed,
+                                       workload as W)
+
+    tol = 1e-8
+    cfg = W.CONFIGS[args.config]
+    K, N = W.mixed_sizes(cfg.n)
+    ctx = partitioned_from_torch_distributed(local) if ws > 1 else Context.partitioned(0, 1, nccl_unique_id(), local)
+    mesh = W.unit_square_mesh(cfg.n)
+    ctx.assemble(mesh, AmgOptions(coarse_threshold=cfg.coarse_threshold))
+    part = ctx.partition()
+    allreduce = (lambda t: torch.distributed.all_reduce(t)) if ws > 1 else None
+    J_d = W.synthetic_jacobian_slice(cfg.m, N, cfg.index, part["c_lo"], part["c_hi"], "cuda", allreduce=allreduce)
+    dm = W.gaussian(W.seed_for(cfg.index, 2), N)
+    dg = W.gaussian(W.seed_for(cfg.index, 3), cfg.m)
+    alphas = list(cfg.alphas)
+
+    def barrier():
+        torch.cuda.synchronize()
+        if ws > 1:
+            torch.distributed.barrier()
+        torch.cuda.synchronize()
+
+    ctx.use_device_pointers(True)
+    dm_d, dg_d = torch.from_numpy(dm).cuda(), torch.from_numpy(dg).cuda()
+    zN, zm = torch.zeros(N, dtype=torch.float64, device="cuda"), torch.zeros(cfg.m, dtype=torch.float64, device="cuda")
+
+    def solve(alpha):
+        tm = ctx.set_jacobian(J_d, alpha)
+        b = ctx.assemble_rhs(dm_d, zN, dg_d, zm)
+        x, rep = ctx.minres(b, tol=tol)
+        return tm, rep, ctx.stats()
+
+    clk = ClockSampler(local).__enter__()
+    for k in range(args.warmup):
+        solve(alphas[k % len(alphas)])
+    barrier()
+    clk.mark()
+    ctx.event_record(0)
+    phases = []
+    for k in range(args.steps):
+        a = alphas[k % len(alphas)]
+        tm, rep, st = solve(a)
+        phases.append(dict(alpha=a, iterations=rep.iterations, converged=rep.converged,
+                           true_rel=rep.true_relative_residual, t_minres=st["t_minres"], **tm))
+    ctx.event_record(1)
+    clk.mark()
+    elapsed = max_over_ranks_dist(ctx.event_elapsed(0, 1), ws)
+    barrier()
+    # e2e: host buffers through the C-ABI (this rank's J slice and the full vectors)
+    ctx.use_device_pointers(False)
+    J_h = torch.empty(tuple(J_d.shape), dtype=torch.float64, pin_memory=True)
+    J_h.copy_(J_d)
+    del J_d
+    torch.cuda.empty_cache()
+    J_h = J_h.numpy()
+
+    def solve_host(alpha):
+        ctx.set_jacobian(J_h, alpha)
+        b = ctx.assemble_rhs(dm, np.zeros(N), dg, np.zeros(cfg.m))
+        return ctx.minres(b, tol=tol)
+
+    solve_host(alphas[0])
+    barrier()
+    ctx.event_record(2)
+    for k in range(args.steps):
+        x_h, rep_h = solve_host(alphas[k % len(alphas)])
+    ctx.event_record(3)
+    e2e_el = max_over_ranks_dist(ctx.event_elapsed(2, 3), ws)
+    if rank == 0:
+        w = part["c_hi"] - part["c_lo"]
+        line = {
+            "metric": METRIC, "value": args.steps / elapsed, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": 1e3 * elapsed / args.steps, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": f"synthetic (seeded {args.config} bundle, J slices generated per rank on the device)",
+            "config": {"workload": f"{args.config}: unit square n={cfg.n} (N={N}, K={K}), m={cfg.m}, one GN-step "
+                                   f"solve split over {ws} GPUs by cell columns", "mesh_n": cfg.n, "m": cfg.m,
+                       "alphas": alphas, "tol": tol, "parallelism": f"cell-partitioned x{ws} (NCCL)",
+                       "rank0_cells": [part["c_lo"], part["c_hi"]],
+                       "l2": f"no flush: per-rank J+H slices ({16 * cfg.m * w / 1e9:.2f} GB) exceed the L2"},
+            "roofline": None, "cpu_baseline": None,
+            "e2e": {"value": args.steps / e2e_el, "unit": UNIT,
+                    "h2d_bytes_per_step": 8 * (cfg.m * w + 3 * N + 2 * cfg.m) + 16 * (K + N),
+                    "d2h_bytes_per_step": 16 * (K + N) + 16 * (rep_h.iterations + 1)},
+            "gpu_launches": None, "clocks": clk.summary(), "phases": phases,
+        }
+        print(json.dumps(line), flush=True)
+    clk.__exit__(None, None, None)
+    ctx.close()
+    if ws > 1:
+        torch.distributed.destroy_process_group()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -459,11 +563,15 @@ def main():
     ap.add_argument("--config", default="C2")
     ap.add_argument("--impl", default="gnw", choices=["gnw", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--partitioned", action="store_true",
+                    help="split ONE solve over the N GPUs by cell columns (C3-scale; NCCL inside libgnw)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
     if args.impl == "reference":
         run_reference(args)
+    elif args.partitioned:
+        run_partitioned(args)
     else:
         run_gnw(args)
 

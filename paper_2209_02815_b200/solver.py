@@ -344,14 +344,22 @@ def partition_cells(n_cells: int, world: int) -> np.ndarray:
     return lo
 
 
-def partitioned_from_torch_distributed(device: int) -> Context:
-    """The calling rank's partitioned context: rank 0 makes the NCCL id and the initialised
-    torch.distributed group (any backend) broadcasts it."""
+def shared_nccl_id() -> bytes:
+    """Rank 0's NCCL unique id, broadcast over the initialised torch.distributed group (any
+    backend, e.g. gloo for the bootstrap)."""
     import torch.distributed as dist
 
     obj = [nccl_unique_id() if dist.get_rank() == 0 else None]
     dist.broadcast_object_list(obj, src=0)
-    return Context.partitioned(dist.get_rank(), dist.get_world_size(), obj[0], device)
+    return obj[0]
+
+
+def partitioned_from_torch_distributed(device: int) -> Context:
+    """The calling rank's partitioned context (one rank per GPU, NCCL)."""
+    import torch.distributed as dist
+
+    nid = shared_nccl_id()
+    return Context.partitioned(dist.get_rank(), dist.get_world_size(), nid, device)
 
 
 def run_ranks(ctxs, fn):
