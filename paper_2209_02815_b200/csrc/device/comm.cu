@@ -76,6 +76,19 @@ void LocalComm::allgather(const double* in, double* out, long long n, cudaStream
   hub_->barrier();
 }
 
+void LocalComm::alltoallv(const std::vector<const double*>& send, const std::vector<long long>&,
+                          const std::vector<double*>& recv, const std::vector<long long>& rcnt, cudaStream_t s) {
+  GNW_CUDA_CHECK(cudaStreamSynchronize(s));
+  for (int q = 0; q < world; ++q) hub_->table()[rank][q] = send[q];
+  hub_->barrier();
+  for (int q = 0; q < world; ++q)
+    if (rcnt[q] > 0)
+      GNW_CUDA_CHECK(cudaMemcpyAsync(recv[q], hub_->table()[q][rank], rcnt[q] * sizeof(double),
+                                     cudaMemcpyDeviceToDevice, s));
+  GNW_CUDA_CHECK(cudaStreamSynchronize(s));
+  hub_->barrier();
+}
+
 // ------------------------------------------------------------------- NCCL
 namespace {
 struct NcclApi {
@@ -86,6 +99,8 @@ struct NcclApi {
   ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
   ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
   ncclResult_t (*Broadcast)(const void*, void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*Send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
   ncclResult_t (*GroupStart)() = nullptr;
   ncclResult_t (*GroupEnd)() = nullptr;
   const char* (*GetErrorString)(ncclResult_t) = nullptr;
@@ -106,10 +121,12 @@ const NcclApi& nccl() {
     a.CommDestroy = reinterpret_cast<decltype(a.CommDestroy)>(sym("ncclCommDestroy"));
     a.AllGather = reinterpret_cast<decltype(a.AllGather)>(sym("ncclAllGather"));
     a.Broadcast = reinterpret_cast<decltype(a.Broadcast)>(sym("ncclBroadcast"));
+    a.Send = reinterpret_cast<decltype(a.Send)>(sym("ncclSend"));
+    a.Recv = reinterpret_cast<decltype(a.Recv)>(sym("ncclRecv"));
     a.GroupStart = reinterpret_cast<decltype(a.GroupStart)>(sym("ncclGroupStart"));
     a.GroupEnd = reinterpret_cast<decltype(a.GroupEnd)>(sym("ncclGroupEnd"));
     a.GetErrorString = reinterpret_cast<decltype(a.GetErrorString)>(sym("ncclGetErrorString"));
-    a.ok = a.GetUniqueId && a.CommInitRank && a.CommDestroy && a.AllGather && a.Broadcast && a.GroupStart &&
+    a.ok = a.GetUniqueId && a.CommInitRank && a.CommDestroy && a.AllGather && a.Broadcast && a.Send && a.Recv && a.GroupStart &&
            a.GroupEnd && a.GetErrorString;
     if (!a.ok) a.why = "libnccl.so.2 lacks a required symbol";
     return a;
@@ -174,6 +191,24 @@ void NcclComm::allgather(const double* in, double* out, long long n, cudaStream_
   const NcclApi& a = nccl_or_throw();
   nccl_check(a.AllGather(in, out, static_cast<size_t>(n), ncclDouble, static_cast<ncclComm_t>(comm_), s),
              "ncclAllGather");
+}
+
+void NcclComm::alltoallv(const std::vector<const double*>& send, const std::vector<long long>& scnt,
+                         const std::vector<double*>& recv, const std::vector<long long>& rcnt, cudaStream_t s) {
+  const NcclApi& a = nccl_or_throw();
+  if (rcnt[rank] > 0)  // own chunk: a device copy
+    GNW_CUDA_CHECK(cudaMemcpyAsync(recv[rank], send[rank], rcnt[rank] * sizeof(double), cudaMemcpyDeviceToDevice, s));
+  nccl_check(a.GroupStart(), "ncclGroupStart");
+  for (int q = 0; q < world; ++q) {
+    if (q == rank) continue;
+    if (scnt[q] > 0)
+      nccl_check(a.Send(send[q], static_cast<size_t>(scnt[q]), ncclDouble, q, static_cast<ncclComm_t>(comm_), s),
+                 "ncclSend");
+    if (rcnt[q] > 0)
+      nccl_check(a.Recv(recv[q], static_cast<size_t>(rcnt[q]), ncclDouble, q, static_cast<ncclComm_t>(comm_), s),
+                 "ncclRecv");
+  }
+  nccl_check(a.GroupEnd(), "ncclGroupEnd");
 }
 
 }  // namespace gnw

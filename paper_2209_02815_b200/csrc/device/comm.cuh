@@ -45,6 +45,9 @@ class Comm {
                           cudaStream_t s) = 0;
   // out[r * n, (r + 1) * n) = rank r's in[0, n)
   virtual void allgather(const double* in, double* out, long long n, cudaStream_t s) = 0;
+  // personalised exchange: send[q] (scnt[q] doubles) goes to rank q, recv[q] (rcnt[q]) comes from q
+  virtual void alltoallv(const std::vector<const double*>& send, const std::vector<long long>& scnt,
+                         const std::vector<double*>& recv, const std::vector<long long>& rcnt, cudaStream_t s) = 0;
   virtual const char* kind() const = 0;
 };
 
@@ -57,6 +60,7 @@ class LocalHub {
   void barrier();
   void abandon();  // a rank failed: wake and fail the others instead of hanging
   std::vector<const double*>& ptrs() { return ptr_; }
+  std::vector<std::vector<const double*>>& table() { return table_; }  // [from][to] send pointers
 
  private:
   int world_;
@@ -66,6 +70,7 @@ class LocalHub {
   long long generation_ = 0;
   bool broken_ = false;
   std::vector<const double*> ptr_;
+  std::vector<std::vector<const double*>> table_ = std::vector<std::vector<const double*>>(world_, std::vector<const double*>(world_));
 };
 
 class LocalComm final : public Comm {
@@ -75,6 +80,8 @@ class LocalComm final : public Comm {
   void allgatherv(double* buf, const std::vector<long long>& off, const std::vector<long long>& cnt,
                   cudaStream_t s) override;
   void allgather(const double* in, double* out, long long n, cudaStream_t s) override;
+  void alltoallv(const std::vector<const double*>& send, const std::vector<long long>& scnt,
+                 const std::vector<double*>& recv, const std::vector<long long>& rcnt, cudaStream_t s) override;
   const char* kind() const override { return "local"; }
   LocalHub& hub() { return *hub_; }
 
@@ -90,6 +97,8 @@ class NcclComm final : public Comm {
   void allgatherv(double* buf, const std::vector<long long>& off, const std::vector<long long>& cnt,
                   cudaStream_t s) override;
   void allgather(const double* in, double* out, long long n, cudaStream_t s) override;
+  void alltoallv(const std::vector<const double*>& send, const std::vector<long long>& scnt,
+                 const std::vector<double*>& recv, const std::vector<long long>& rcnt, cudaStream_t s) override;
   const char* kind() const override { return "nccl"; }
 
  private:

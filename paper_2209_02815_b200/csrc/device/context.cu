@@ -397,19 +397,8 @@ void Context::set_jacobian(const double* J, int64_t m, int64_t n_cells, double b
     for (int64_t i0 = 0; i0 < m; i0 += b) {
       const int bb = static_cast<int>(std::min<int64_t>(b, m - i0));
       if (comm_) {
-        // partitioned: each rank packs its columns of J rows [i0, i0+bb) into the interleaved
-        // batch (cells are contiguous there), the slices are gathered, every rank runs the
-        // batched V-cycle and keeps its own cells of H
-        transpose_rows_to_batch(dJ_, Nl, ldj_, static_cast<int>(i0), bb, damg_.batch_in() + c_lo_ * bb, s);
-        std::vector<long long> off(comm_->world), cnt(comm_->world);
-        for (int r = 0; r < comm_->world; ++r) {
-          off[r] = part_lo_[r] * bb;
-          cnt[r] = (part_lo_[r + 1] - part_lo_[r]) * bb;
-        }
-        comm_->allgatherv(damg_.batch_in(), off, cnt, s);
-        damg_.vcycle_batch(damg_.batch_in(), bb, damg_.batch_out(), coarse_mode == 1, st_plain_, s);
-        transpose_batch_to_rows(damg_.batch_out() + c_lo_ * bb, Nl, ldh_, static_cast<int>(i0), bb, dHt_, s);
-        continue;
+        build_h_partitioned(b);
+        break;
       }
       transpose_rows_to_batch(dJ_, N_, ldj_, static_cast<int>(i0), bb, damg_.batch_in(), s);
       damg_.vcycle_batch(damg_.batch_in(), bb, damg_.batch_out(), coarse_mode == 1, st_plain_, s);

@@ -196,6 +196,10 @@ class Context {
   double* resolve(const VSel& v) const { return v.mod == 1 ? v.p[0] : v.p[(host_j_ + v.off) % v.mod]; }
   void gather_cells(double* full, cudaStream_t s);                  // allgatherv of the cell part
   void reduce_m(const double* part, double* out, long long n, cudaStream_t s);  // fixed-order allreduce
+  void build_h_partitioned(int b);  // H = B J^T with the column batches spread over the ranks
+  std::unique_ptr<DeviceMemory> a2a_mem_;
+  double *a2a_a_ = nullptr, *a2a_b_ = nullptr;
+  size_t a2a_na_ = 0, a2a_nb_ = 0;
 
   // ERT forward model state
   std::vector<int64_t> electrodes_;
