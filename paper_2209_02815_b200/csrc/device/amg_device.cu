@@ -248,7 +248,12 @@ void DeviceAmg::ensure_batch(int b) {
   bmem_b_ = b;
 }
 
-// Multi-RHS V-cycle over b interleaved columns: r0/out0 are n x b.
+// Multi-RHS V-cycle over b interleaved columns: r0/out0 are n x b.  Every level uses the
+// thread-per-(row, column) kernels with the reference's sequential row sums (coalesced over
+// the columns, few registers).  In exact mode that makes each column of H bit-identical to
+// the reference's amg_apply; in the default mode it agrees with the loop's single-RHS cycle
+// (warp-per-row on wide levels, dense collapsed tail) to rounding.  (A 32-partial emulation
+// of the warp lanes kept the two bitwise equal but ran the C2 setup at 1/3 of its roofline.)
 void DeviceAmg::vcycle_batch(const double* r0, int b, double* out0, int exact, const MinresState* st_plain,
                              cudaStream_t s) {
   const int L = static_cast<int>(lv_.size());
@@ -266,17 +271,17 @@ void DeviceAmg::vcycle_batch(const double* r0, int b, double* out0, int exact, c
   const int stop = (!exact && collapse_l_ > 0) ? collapse_l_ : L - 1;  // as in cycle_levels
   for (int l = 0; l < stop; ++l) {
     const double* rl = l == 0 ? r0 : mr_[l];
-    const DLevel lev = level(l, exact);
+    const DLevel lev = level(l, 1);  // sequential row order on every level (see below)
     mvc_down(lev, rl, b, mres_[l], b, s);
     mvc_restrict(lev, mres_[l], mr_[l + 1], b, s);
   }
   if (stop == L - 1)
     coarse(mr_[L - 1], me_[L - 1]);
   else
-    dense_emul_batch(collapse_M_, lv_[stop].n, mr_[stop], me_[stop], b, s);
+    dense_seq_batch(collapse_M_, lv_[stop].n, mr_[stop], me_[stop], b, s);
   for (int l = stop - 1; l >= 0; --l) {
     const double* rl = l == 0 ? r0 : mr_[l];
-    const DLevel lev = level(l, exact);
+    const DLevel lev = level(l, 1);
     mvc_up1(lev, rl, b, me_[l + 1], mx_[l], b, s);
     mvc_up2(lev, rl, b, mx_[l], l == 0 ? out0 : me_[l], b, b, s);
   }

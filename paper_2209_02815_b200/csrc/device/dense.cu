@@ -34,6 +34,7 @@ __global__ void __launch_bounds__(PT) k_chol_panel(double* __restrict__ W, doubl
                                                    int* fail) {
   griddep_wait();
   __shared__ double colk[PW];
+  __shared__ double lcol[PW];  // L[p + t][k] of the diagonal-block rows, divided once per step
   __shared__ int bad;
   if (*fail) return;
   const int w = min(PW, n - p);
@@ -65,6 +66,10 @@ __global__ void __launch_bounds__(PT) k_chol_panel(double* __restrict__ W, doubl
     }
     const double ljj = sqrt(d);
     const int k = p + c;
+    // the panel rows' L[j][k] = W[j][k] / L[k][k]: one division each, shared by every row
+    // below (the same operands, so the same bits as dividing in every thread)
+    if (diag && t < w && t > c) lcol[t] = colk[t] / ljj;
+    __syncthreads();
     if (!valid) continue;
     if (i == k) {
       if (writer) L[static_cast<long long>(i) * n + i] = ljj;
@@ -79,7 +84,7 @@ __global__ void __launch_bounds__(PT) k_chol_panel(double* __restrict__ W, doubl
         if (cj <= c || cj >= w) continue;
         const int j = p + cj;
         if (j > i) continue;
-        const double ljk = colk[cj] / ljj;  // == L[j][k], bit for bit
+        const double ljk = lcol[cj];  // == L[j][k], bit for bit
         row[cj] = row[cj] - lik * ljk;
       }
     }

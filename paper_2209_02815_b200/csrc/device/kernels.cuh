@@ -82,6 +82,8 @@ void mvc_up2(const DLevel& L, const double* r, int ldr, const double* x, double*
 void mcoarse_inverse(const double* Ainv, int n, const double* r, double* x, int b, cudaStream_t s);
 // collapsed coarse tail (amg_device.cu): batched dense apply, bit-identical per column to coarse_inverse
 void dense_emul_batch(const double* M, int n, const double* X, double* Y, int b, cudaStream_t s);
+// batched dense apply in sequential order (the batched V-cycle's collapsed tail)
+void dense_seq_batch(const double* M, int n, const double* X, double* Y, int b, cudaStream_t s);
 void identity_rows(double* I, int n, cudaStream_t s);
 void transpose_square(const double* A, double* T, int n, cudaStream_t s);
 

@@ -181,6 +181,21 @@ __global__ void __launch_bounds__(256) k_dense_emul_batch(const double* __restri
   Y[static_cast<long long>(i) * b + q] = tree32(p);
 }
 
+// Y[:, q] = M X[:, q], one thread per (row, column), j ascending (sequential order):
+// X loads coalesced over the columns, M rows broadcast within a warp; ~20 registers.
+__global__ void __launch_bounds__(256) k_dense_seq_batch(const double* __restrict__ M, int n,
+                                                         const double* __restrict__ X, double* __restrict__ Y, int b) {
+  griddep_wait();
+  const int i = blockIdx.x * 8 + threadIdx.y;
+  const int q = blockIdx.y * 32 + threadIdx.x;
+  if (i >= n || q >= b) return;
+  const double* __restrict__ Mi = M + static_cast<long long>(i) * n;
+  double acc = 0.0;
+#pragma unroll 8
+  for (int j = 0; j < n; ++j) acc = acc + __ldg(&Mi[j]) * X[static_cast<long long>(j) * b + q];
+  Y[static_cast<long long>(i) * b + q] = acc;
+}
+
 __global__ void k_identity_rows(double* __restrict__ I, int n) {
   const long long k = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (k < static_cast<long long>(n) * n) I[k] = (k / n == k % n) ? 1.0 : 0.0;
@@ -236,6 +251,11 @@ void dense_emul_batch(const double* M, int n, const double* X, double* Y, int b,
   dim3 grid((n + 7) / 8, (b + 31) / 32), block(32, 8);
   GNW_LAUNCH(launch_k(k_dense_emul_batch, grid, block, 0, s, M, n, X, Y, b));
   note_launch("dense_emul_batch");
+}
+void dense_seq_batch(const double* M, int n, const double* X, double* Y, int b, cudaStream_t s) {
+  dim3 grid((n + 7) / 8, (b + 31) / 32), block(32, 8);
+  GNW_LAUNCH(launch_k(k_dense_seq_batch, grid, block, 0, s, M, n, X, Y, b));
+  note_launch("dense_seq_batch");
 }
 void identity_rows(double* I, int n, cudaStream_t s) {
   const long long t = static_cast<long long>(n) * n;
