@@ -224,7 +224,9 @@ enum {
   GNW_K_VCYCLE = 4,        /* one single-RHS V-cycle (all its kernels) */
   GNW_K_UPDATE = 5,        /* w/u/x/r recurrences */
   GNW_K_DGEMM = 6,         /* capacitance DGEMM (DMMA), flops */
-  GNW_K_ITERATION = 7      /* one full MINRES iteration (graph body, replayed by the kernels) */
+  GNW_K_ITERATION = 7,     /* one full MINRES iteration (graph body, replayed by the kernels) */
+  GNW_K_BODY = 8           /* the loop body captured once and replayed without loop control;
+                              env GNW_EXP_SKIP (bit mask) leaves parts out, for attribution only */
 };
 gnw_status gnw_profile_kernel(gnw_ctx* ctx, int kernel, int reps, double* seconds_per_launch,
                               double* algorithmic_per_launch);

@@ -88,7 +88,7 @@ class ErtStats(C.Structure):
                 ("t_jacobian", C.c_double), ("pcg_iterations", C.c_uint64)]
 
 KERNELS = {"row_gemv": 0, "saddle": 1, "combine_prec": 2, "finish_prec": 3, "vcycle": 4,
-           "update": 5, "dgemm": 6, "iteration": 7}
+           "update": 5, "dgemm": 6, "iteration": 7, "body": 8}
 
 _lib = None
 

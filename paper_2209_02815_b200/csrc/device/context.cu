@@ -468,11 +468,11 @@ void Context::operator_into(VSel x, int scaled, VSel y, MinresState* st, int loo
   }
   if (fused) {
     op.q = dq_;
-  } else if (m_ > 0) {
+  } else if (m_ > 0 && !(exp_skip_ & 1)) {
     VSel xs = x;  // J acts on the cell part
     row_gemv(dJ_, static_cast<int>(m_), N_, ldj_, xs, K_, scaled, st, gpart_, counters_ + 0, u_, plan_, stream_);
   }
-  saddle_operator(op, x, scaled, u_, y, st, loop, opart_, counters_ + 1, stream_);
+  if (!(exp_skip_ & 2)) saddle_operator(op, x, scaled, u_, y, st, loop, opart_, counters_ + 1, stream_);
 }
 
 bool Context::fused_active() const { return fused_ && !comm_ && m_ > 0 && pa_.m > 0 && dq_ != nullptr; }
@@ -497,7 +497,7 @@ void Context::precondition_into(VSel y, VSel yv2, VSel z, MinresState* st, int l
     pa.q = dq_;
   }
   const VSel az = loop ? vfixed(az_) : y;
-  combine_elem(pa, az, vcur, vprev, y, z, loop, st, cpart_, stream_);
+  if (!(exp_skip_ & 4)) combine_elem(pa, az, vcur, vprev, y, z, loop, st, cpart_, stream_);
   if (comm_) {  // partitioned: t = sum_r H_r^T y_r; z2 on own cells, gathered; then the Givens step
     if (pa.m > 0) {
       row_gemv(pa.Ht, pa.m, c_hi_ - c_lo_, pa.ldh, y, pa.K + c_lo_, 0, st, tpart_, counters_ + 2, t_part_, plan_h_, stream_);
@@ -516,15 +516,15 @@ void Context::precondition_into(VSel y, VSel yv2, VSel z, MinresState* st, int l
   if (fork) {
     GNW_CUDA_CHECK(cudaEventRecord(fork_ev_[0], stream_));
     GNW_CUDA_CHECK(cudaStreamWaitEvent(side_, fork_ev_[0], 0));
-    vcycle(yv2, svc_, st, side_);
+    if (!(exp_skip_ & 16)) vcycle(yv2, svc_, st, side_);
     GNW_CUDA_CHECK(cudaEventRecord(fork_ev_[1], side_));
   }
-  if (pa.m > 0)  // t = H^T v2 (matvec_transpose(h_hat, y2), inversion.cpp:82)
+  if (pa.m > 0 && !(exp_skip_ & 8))  // t = H^T v2 (matvec_transpose(h_hat, y2), inversion.cpp:82)
     row_gemv(pa.Ht, pa.m, pa.N, pa.ldh, y, pa.K, 0, st, tpart_, counters_ + 2, t_, plan_h_, stream_);
-  if (!fork) vcycle(yv2, svc_, st);
-  capacitance_solve(pa, t_, t2_, stream_);
+  if (!fork && !(exp_skip_ & 16)) vcycle(yv2, svc_, st);
+  if (!(exp_skip_ & 32)) capacitance_solve(pa, t_, t2_, stream_);
   if (fork) GNW_CUDA_CHECK(cudaStreamWaitEvent(stream_, fork_ev_[1], 0));
-  finish_precondition(pa, svc_, t2_, y, z, loop, st, cpart_, n_comb_blocks_, fpart_, counters_ + 3, stream_);
+  if (!(exp_skip_ & 64)) finish_precondition(pa, svc_, t2_, y, z, loop, st, cpart_, n_comb_blocks_, fpart_, counters_ + 3, stream_);
 }
 
 void Context::precondition(const double* y, double* z) {
@@ -589,9 +589,10 @@ void Context::launch_iteration(unsigned long long cond_handle, int use_cond) {
   operator_into(ring2(Z_, 0), 1, vfixed(az_), st_, 1, fu);                  // Az = A zhat, delta
   precondition_into(ring3(V_, 2), ring3(Vk_, 2), ring2(Z_, 1), st_, 1,       // v_next, z_next = P^-1 v_next,
                     ring3(V_, 1), ring3(V_, 0), fu);                         // gamma_next, Givens
-  minres_update(K_ + N_, ring2(Z_, 0), vfixed(az_), ring3(W_, 0), ring3(W_, 1), ring3(W_, 2), ring3(U_, 0),
-                ring3(U_, 1), ring3(U_, 2), x_, r_, st_, hist_e_, hist_p_, hist_cap_, upart_, counters_ + 4,
-                cond_handle, use_cond, stream_);
+  if (!(exp_skip_ & 128))
+    minres_update(K_ + N_, ring2(Z_, 0), vfixed(az_), ring3(W_, 0), ring3(W_, 1), ring3(W_, 2), ring3(U_, 0),
+                  ring3(U_, 1), ring3(U_, 2), x_, r_, st_, hist_e_, hist_p_, hist_cap_, upart_, counters_ + 4,
+                  cond_handle, use_cond, stream_);
 }
 
 void Context::build_graph() {
@@ -873,6 +874,7 @@ void Context::profile_kernel(int kernel, int reps, double* seconds, double* algo
     case 5: alg = 96 * (K + N); break;
     case 6: alg = 2.0 * m * m * N; break;
     case 7:
+    case 8:
       alg = 16 * m * N + 16 * hm * N + (12 * nnzQ + 4 * (K + 1)) + 2 * (12 * nnzD + 4 * (N + 1)) + bv +
             8 * (20 * (K + N) + K);
       break;
@@ -884,6 +886,40 @@ void Context::profile_kernel(int kernel, int reps, double* seconds, double* algo
     return;
   }
   if ((kernel == 0 || kernel == 6) && m_ == 0) throw std::invalid_argument("gnw_profile_kernel: no Jacobian set");
+  if (kernel == 8) {  // one loop-body graph (no loop control) replayed; env GNW_EXP_SKIP drops parts of it
+    if (comm_ || hist_cap_ == 0) throw std::invalid_argument("gnw_profile_kernel: run minres first (single GPU)");
+    const char* e = std::getenv("GNW_EXP_SKIP");
+    exp_skip_ = e ? std::atoi(e) : 0;
+    cudaGraph_t g = nullptr;
+    cudaGraphExec_t ge = nullptr;
+    try {
+      GNW_CUDA_CHECK(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+      launch_iteration(0, 2);
+      GNW_CUDA_CHECK(cudaStreamEndCapture(s, &g));
+      GNW_CUDA_CHECK(cudaGraphInstantiate(&ge, g, 0));
+    } catch (...) {
+      exp_skip_ = 0;
+      throw;
+    }
+    exp_skip_ = 0;
+    GNW_CUDA_CHECK(cudaGraphLaunch(ge, s));
+    sync();
+    cudaEvent_t a0, a1;
+    GNW_CUDA_CHECK(cudaEventCreate(&a0));
+    GNW_CUDA_CHECK(cudaEventCreate(&a1));
+    GNW_CUDA_CHECK(cudaEventRecord(a0, s));
+    for (int r = 0; r < reps; ++r) GNW_CUDA_CHECK(cudaGraphLaunch(ge, s));
+    GNW_CUDA_CHECK(cudaEventRecord(a1, s));
+    sync();
+    float ms = 0.f;
+    GNW_CUDA_CHECK(cudaEventElapsedTime(&ms, a0, a1));
+    cudaEventDestroy(a0);
+    cudaEventDestroy(a1);
+    cudaGraphExecDestroy(ge);
+    cudaGraphDestroy(g);
+    *seconds = ms * 1e-3 / reps;
+    return;
+  }
   const int64_t n = K_ + N_;
   fill_zero(io_a_, n, s);
   fill_zero(io_b_, n, s);

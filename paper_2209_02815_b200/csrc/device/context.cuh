@@ -146,6 +146,7 @@ class Context {
   double *gpart_ = nullptr, *tpart_ = nullptr;
   RowGemv plan_{};    // J x (nothing runs beside it)
   RowGemv plan_h_{};  // H^T y (leaves CTA slots for the forked V-cycle)
+  int exp_skip_ = 0;     // profiling only (profile_kernel "body"): bit mask of iteration parts left out
   int rg_reserve_ = 1;  // env GNW_RG_RESERVE (C2 sweep: 0: 0.919, 1: 0.859, 2: 0.863 ms/iteration)
 
   // MINRES vectors
