@@ -194,6 +194,35 @@ gnw_status gnw_set_electrodes(gnw_ctx* ctx, const int64_t* nodes, uint64_t n);
  * residual of the batched PCG pole solves (the reference factorises exactly). */
 gnw_status gnw_response_jacobian(gnw_ctx* ctx, const double* m, const gnw_ert_config* cfgs, uint64_t n_cfg,
                                  double* J, double* g, double tol, gnw_ert_stats* stats);
+/* gauss_newton (inversion.hpp:66-105, inversion.cpp:187-292) for the iterative algorithms:
+ * each outer step evaluates g and J at m (gnw_response_jacobian; the electrodes come from
+ * gnw_set_electrodes), builds the Woodbury (or Laplace) preconditioner, assembles the rhs
+ * and solves with MINRES from x0 = 0, then m += x[K:].  GnAlgorithm::kDirect (sparse LU)
+ * is out of scope. */
+typedef struct gnw_gn_config {
+  double beta;                  /* GnConfig::beta (> 0) */
+  uint64_t max_outer_steps;     /* GnConfig::max_outer_steps */
+  double minres_tol;            /* GnConfig::minres_tol */
+  uint64_t minres_maxit;        /* 0 -> 2 (K + N) */
+  int32_t algorithm;            /* GNW_PC_WOODBURY (kWoodburyMinres) or GNW_PC_LAPLACE (kLaplaceMinres) */
+  double misfit_reduction_tol;  /* 0 disables the early exit */
+  double forward_tol;           /* pole-solve PCG tolerance (0 -> 1e-14) */
+} gnw_gn_config;
+
+typedef struct gnw_gn_step {    /* GnStepReport (inversion.hpp:77-87) */
+  double misfit;
+  uint64_t minres_iters;
+  int32_t converged;
+  double euclid_relative_residual;
+  double pnorm_relative_residual;
+  double t_H, t_C, t_chol, t_norm;
+  double t_forward;             /* evaluate_response_and_jacobian of the step (not in t_norm) */
+} gnw_gn_step;
+
+gnw_status gnw_gauss_newton(gnw_ctx* ctx, const double* m0, const double* m_ref, const gnw_ert_config* cfgs,
+                            uint64_t n_cfg, const double* g_obs, const gnw_gn_config* config, double* m_out,
+                            gnw_gn_step* steps, uint64_t steps_cap, uint64_t* n_steps, double* final_misfit);
+
 /* geometric_factor (survey.hpp:33-37, survey.cpp:22-46); b == NULL: pole at infinity. */
 gnw_status gnw_geometric_factor(const double a[3], const double* b, const double m[3], const double n[3], int dim,
                                 double* k);

@@ -236,6 +236,68 @@ class Problem:
                         J.ravel(), g))
         return g, J
 
+    def gauss_newton(self, nodes, cfgs, g_obs, m_ref, m0, beta=0.1, max_outer_steps=2, minres_tol=1e-7,
+                     minres_maxit=0, algorithm="woodbury", misfit_reduction_tol=0.0):
+        """gauss_newton (inversion.cpp:187-292) for the iterative algorithms, composed from this
+        oracle's own pieces in the reference's order: misfit = norm2(g - g_obs) (:225-226),
+        preconditioner (:244-256), rhs (:259-260), MINRES from x0 = 0 (:261-265), m += x[K:]
+        (:275-278), optional early exit (:280-283), final misfit (:286-291)."""
+        K, N = self.K, self.N
+        maxit = minres_maxit if minres_maxit > 0 else 2 * (K + N)
+        m = np.array(m0, dtype=np.float64)
+        g_obs = np.asarray(g_obs, dtype=np.float64)
+        steps = []
+
+        def misfit(gv):
+            d = gv - g_obs
+            s = 0.0
+            for v in d:  # norm2: sequential dot (linalg.cpp:9-22)
+                s += v * v
+            return float(np.sqrt(s))
+
+        for step in range(max_outer_steps):
+            g, J = self.response_jacobian(nodes, cfgs, m)
+            sr = dict(misfit=misfit(g))
+            self.set_jacobian(J, beta, laplace_pc=(algorithm == "laplace"))
+            b = self.assemble_rhs(m, m_ref, g, g_obs)
+            x, rep = self.minres(b, np.zeros(K + N), tol=minres_tol, maxit=maxit)
+            sr.update(minres_iters=rep["iterations"], converged=rep["converged"],
+                      euclid_relative_residual=rep["true_relative_residual"],
+                      pnorm_relative_residual=float(rep["pnorm_relative_residuals"][-1]))
+            delta = x[K:]
+            if not np.all(np.isfinite(delta)):
+                raise RuntimeError("gauss_newton: non-finite model update")
+            m = m + delta
+            steps.append(sr)
+            if misfit_reduction_tol > 0.0 and step > 0:
+                if sr["misfit"] > (1.0 - misfit_reduction_tol) * steps[-2]["misfit"]:
+                    break
+        g, _ = self.response_jacobian(nodes, cfgs, m)
+        return m, dict(steps=steps, final_misfit=misfit(g))
+
+    def gauss_newton_reference(self, nodes, cfgs, g_obs, m_ref, m0, beta=0.1, max_outer_steps=2, minres_tol=1e-7,
+                               minres_maxit=0, algorithm="woodbury", misfit_reduction_tol=0.0):
+        """The unmodified reference gauss_newton (oracle/_ref only), same return shape."""
+        fn = self.o.L.orc_gauss_newton
+        fn.argtypes = [C.c_void_p, _i64p, _u64, _i64p, _i64p, _i64p, _i64p, _dp, _u64, _dp, _dp, _dp, C.c_double,
+                       _u64, C.c_double, _u64, C.c_int, C.c_double, _dp, _dp, _u64, C.POINTER(_u64),
+                       C.POINTER(C.c_double)]
+        nodes = np.ascontiguousarray(nodes, dtype=np.int64)
+        cols = [np.ascontiguousarray(cfgs[k], dtype=np.int64) for k in ("a", "b", "m", "n")]
+        kk = np.ascontiguousarray(cfgs["k"], dtype=np.float64)
+        f = lambda a: np.ascontiguousarray(a, dtype=np.float64)
+        m_out = np.zeros(self.N)
+        cap = max(1, max_outer_steps)
+        st = np.zeros(5 * cap)
+        ns, fin = _u64(), C.c_double()
+        self.o.check(fn(self.h, nodes, len(nodes), *cols, kk, len(kk), f(g_obs), f(m_ref), f(m0), beta,
+                        max_outer_steps, minres_tol, minres_maxit, 1 if algorithm == "laplace" else 0,
+                        misfit_reduction_tol, m_out, st, cap, C.byref(ns), C.byref(fin)))
+        steps = [dict(misfit=st[5 * i], minres_iters=int(st[5 * i + 1]), converged=bool(st[5 * i + 2]),
+                      euclid_relative_residual=st[5 * i + 3], pnorm_relative_residual=st[5 * i + 4])
+                 for i in range(ns.value)]
+        return m_out, dict(steps=steps, final_misfit=fin.value)
+
     def sample_gnstep(self, J: np.ndarray, beta: float, k_cols: int, k_rows: int, k_iters: int) -> dict:
         """Bounded CPU timing sample (reference library only); see orc_api.h."""
         fn = self.o.L.orc_sample_gnstep

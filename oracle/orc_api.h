@@ -105,6 +105,14 @@ int orc_sample_gnstep(orc_problem* p, const double* J, uint64_t m, double beta, 
 int orc_response_jacobian(orc_problem* p, const int64_t* nodes, uint64_t n_nodes, const int64_t* a,
                           const int64_t* b, const int64_t* m, const int64_t* n, const double* k, uint64_t n_cfg,
                           const double* model, double* J, double* g);
+/* gauss_newton (inversion.cpp:187-292), reference library only (the restatement composes it
+ * in orc.py from the functions above).  algorithm: 0 kWoodburyMinres, 1 kLaplaceMinres.
+ * steps: n_steps x {misfit, minres_iters, converged, euclid rel. residual, pnorm rel. residual}. */
+int orc_gauss_newton(orc_problem* p, const int64_t* nodes, uint64_t n_nodes, const int64_t* a, const int64_t* b,
+                     const int64_t* m, const int64_t* n, const double* k, uint64_t n_cfg, const double* g_obs,
+                     const double* m_ref, const double* m0, double beta, uint64_t max_outer_steps, double minres_tol,
+                     uint64_t minres_maxit, int algorithm, double misfit_reduction_tol, double* m_out,
+                     double* steps, uint64_t steps_cap, uint64_t* n_steps, double* final_misfit);
 /* geometric_factor (survey.cpp:22-46); b == NULL: pole at infinity. */
 int orc_geometric_factor(const double a[3], const double* b, const double m[3], const double n[3], int dim,
                          double* k);

@@ -396,6 +396,55 @@ int orc_response_jacobian(orc_problem* p, const int64_t* nodes, uint64_t n_nodes
   });
 }
 
+int orc_gauss_newton(orc_problem* p, const int64_t* nodes, uint64_t n_nodes, const int64_t* a, const int64_t* b,
+                     const int64_t* m, const int64_t* n, const double* k, uint64_t n_cfg, const double* g_obs,
+                     const double* m_ref, const double* m0, double beta, uint64_t max_outer_steps, double minres_tol,
+                     uint64_t minres_maxit, int algorithm, double misfit_reduction_tol, double* m_out,
+                     double* steps, uint64_t steps_cap, uint64_t* n_steps, double* final_misfit) {
+  return guard([&] {
+    if (!p->mixed) throw std::invalid_argument("orc_gauss_newton: not a mixed problem");
+    p->mesh.electrode_nodes.assign(nodes, nodes + n_nodes);
+    Survey survey;
+    for (uint64_t e = 0; e < n_nodes; ++e) survey.electrode_positions.push_back(p->mesh.vertices[nodes[e]][0]);
+    for (uint64_t i = 0; i < n_cfg; ++i) {
+      ElectrodeConfig c;
+      c.a = static_cast<std::size_t>(a[i]);
+      c.b = static_cast<std::ptrdiff_t>(b[i]);
+      c.m = static_cast<std::size_t>(m[i]);
+      c.n = static_cast<std::size_t>(n[i]);
+      c.k = k[i];
+      survey.configs.push_back(c);
+    }
+    const std::size_t N = p->mesh.n_cells();
+    GnProblem prob;
+    prob.mesh = &p->mesh;
+    prob.survey = &survey;
+    prob.g_obs.assign(g_obs, g_obs + n_cfg);
+    prob.m_ref.assign(m_ref, m_ref + N);
+    prob.m0.assign(m0, m0 + N);
+    GnConfig cfg;
+    cfg.beta = beta;
+    cfg.max_outer_steps = max_outer_steps;
+    cfg.minres_tol = minres_tol;
+    cfg.minres_maxit = minres_maxit;
+    cfg.algorithm = algorithm == 1 ? GnAlgorithm::kLaplaceMinres : GnAlgorithm::kWoodburyMinres;
+    cfg.misfit_reduction_tol = misfit_reduction_tol;
+    auto [mv, rep] = gauss_newton(prob, cfg);  // inversion.cpp:187-292, unmodified
+    std::memcpy(m_out, mv.data(), N * sizeof(double));
+    *n_steps = rep.steps.size();
+    *final_misfit = rep.final_misfit;
+    for (std::size_t i = 0; i < std::min<std::size_t>(steps_cap, rep.steps.size()); ++i) {
+      const GnStepReport& q = rep.steps[i];
+      double* o = steps + 5 * i;
+      o[0] = q.misfit;
+      o[1] = static_cast<double>(q.minres_iters);
+      o[2] = q.converged ? 1.0 : 0.0;
+      o[3] = q.euclid_relative_residual;
+      o[4] = q.pnorm_relative_residual;
+    }
+  });
+}
+
 int orc_geometric_factor(const double a[3], const double* b, const double m[3], const double n[3], int dim, double* k) {
   return guard([&] {
     std::optional<std::array<double, 3>> bb;

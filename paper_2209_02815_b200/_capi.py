@@ -73,7 +73,7 @@ EXPORTED = [
     "gnw_export_mesh", "gnw_dense_cholesky", "gnw_get_stats", "gnw_event_record",
     "gnw_event_elapsed", "gnw_profile_kernel", "gnw_set_electrodes", "gnw_response_jacobian",
     "gnw_geometric_factor", "gnw_nccl_unique_id", "gnw_create_partitioned", "gnw_create_local_group",
-    "gnw_get_partition", "gnw_partition_cells",
+    "gnw_get_partition", "gnw_partition_cells", "gnw_gauss_newton",
 ]
 
 
@@ -86,6 +86,23 @@ class ErtConfig(C.Structure):
 class ErtStats(C.Structure):
     _fields_ = [("t_assemble", C.c_double), ("t_amg", C.c_double), ("t_solve", C.c_double),
                 ("t_jacobian", C.c_double), ("pcg_iterations", C.c_uint64)]
+
+class GnConfig(C.Structure):
+    """GnConfig (inversion.hpp:66-75)."""
+
+    _fields_ = [("beta", C.c_double), ("max_outer_steps", C.c_uint64), ("minres_tol", C.c_double),
+                ("minres_maxit", C.c_uint64), ("algorithm", C.c_int32), ("misfit_reduction_tol", C.c_double),
+                ("forward_tol", C.c_double)]
+
+
+class GnStep(C.Structure):
+    """GnStepReport (inversion.hpp:77-87) + t_forward."""
+
+    _fields_ = [("misfit", C.c_double), ("minres_iters", C.c_uint64), ("converged", C.c_int32),
+                ("euclid_relative_residual", C.c_double), ("pnorm_relative_residual", C.c_double),
+                ("t_H", C.c_double), ("t_C", C.c_double), ("t_chol", C.c_double), ("t_norm", C.c_double),
+                ("t_forward", C.c_double)]
+
 
 KERNELS = {"row_gemv": 0, "saddle": 1, "combine_prec": 2, "finish_prec": 3, "vcycle": 4,
            "update": 5, "dgemm": 6, "iteration": 7, "body": 8}
@@ -135,6 +152,8 @@ def load() -> C.CDLL:
     L.gnw_create_partitioned.argtypes = [i32, i32, i32, vp, C.POINTER(vp)]
     L.gnw_create_local_group.argtypes = [i32, i32, C.POINTER(vp)]
     L.gnw_partition_cells.argtypes = [u64, i32, vp]
+    L.gnw_gauss_newton.argtypes = [vp, vp, vp, C.POINTER(ErtConfig), u64, vp, C.POINTER(GnConfig), vp,
+                                   C.POINTER(GnStep), u64, C.POINTER(u64), C.POINTER(dbl)]
     L.gnw_get_partition.argtypes = [vp, C.POINTER(i32), C.POINTER(i32), C.POINTER(C.c_int64), C.POINTER(C.c_int64)]
     for name in EXPORTED:
         fn = getattr(L, name)

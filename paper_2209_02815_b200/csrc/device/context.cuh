@@ -23,6 +23,29 @@ struct MinresResult {
   double true_rel = 0.0;
 };
 
+// GnConfig / GnStepReport / GnReport (inversion.hpp:66-95)
+struct GnConfig {
+  double beta = 0.1;
+  uint64_t max_outer_steps = 2;
+  double minres_tol = 1e-7;
+  uint64_t minres_maxit = 0;  // 0 -> 2 (K + N)
+  int laplace = 0;            // GnAlgorithm::kLaplaceMinres instead of kWoodburyMinres
+  double misfit_reduction_tol = 0.0;
+  double forward_tol = 1e-14;  // batched PCG of the pole solves (the reference factorises exactly)
+};
+struct GnStepReport {
+  double misfit = 0.0;
+  uint64_t minres_iters = 0;
+  bool converged = true;
+  double euclid_relative_residual = 0.0, pnorm_relative_residual = 0.0;
+  double t_H = 0.0, t_C = 0.0, t_chol = 0.0, t_norm = 0.0;
+  double t_forward = 0.0;  // evaluate_response_and_jacobian (outside t_norm, as the reference)
+};
+struct GnResult {
+  std::vector<GnStepReport> steps;
+  double final_misfit = 0.0;
+};
+
 struct ErtTimings {
   double t_assemble = 0.0, t_amg = 0.0, t_solve = 0.0, t_jacobian = 0.0;
   uint64_t pcg_iterations = 0;
@@ -77,6 +100,11 @@ class Context {
   void set_electrodes(const int64_t* nodes, int64_t n);
   void response_jacobian(const double* mdl, const host::ErtConfig* cfgs, int64_t n_cfg, double* J_out, double* g_out,
                          double tol, ErtTimings* t);
+
+  // gauss_newton (inversion.cpp:187-292), iterative algorithms, on the device: forward
+  // response + J, Woodbury (or Laplace) preconditioner, rhs, MINRES, model update.
+  GnResult gauss_newton(const double* m0, const double* m_ref, const host::ErtConfig* cfgs, int64_t n_cfg,
+                        const double* g_obs, const GnConfig& cfg, double* m_out);
 
   // structure
   const host::Mesh& mesh() const { return mesh_; }

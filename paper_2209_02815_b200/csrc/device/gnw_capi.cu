@@ -341,6 +341,35 @@ gnw_status gnw_response_jacobian(gnw_ctx* ctx, const double* m, const gnw_ert_co
   });
 }
 
+gnw_status gnw_gauss_newton(gnw_ctx* ctx, const double* m0, const double* m_ref, const gnw_ert_config* cfgs,
+                            uint64_t n_cfg, const double* g_obs, const gnw_gn_config* config, double* m_out,
+                            gnw_gn_step* steps, uint64_t steps_cap, uint64_t* n_steps, double* final_misfit) {
+  return guard([&] {
+    if (!config || !m0 || !m_ref || !cfgs || !g_obs) throw std::invalid_argument("gauss_newton: null argument");
+    if (config->algorithm != GNW_PC_WOODBURY && config->algorithm != GNW_PC_LAPLACE)
+      throw std::invalid_argument("gauss_newton: only the iterative algorithms (Woodbury / Laplace MINRES)");
+    gnw::GnConfig c;
+    c.beta = config->beta;
+    c.max_outer_steps = config->max_outer_steps;
+    c.minres_tol = config->minres_tol;
+    c.minres_maxit = config->minres_maxit;
+    c.laplace = config->algorithm == GNW_PC_LAPLACE;
+    c.misfit_reduction_tol = config->misfit_reduction_tol;
+    if (config->forward_tol > 0.0) c.forward_tol = config->forward_tol;
+    std::vector<gnw::host::ErtConfig> e(n_cfg);
+    for (uint64_t i = 0; i < n_cfg; ++i) e[i] = {cfgs[i].a, cfgs[i].b, cfgs[i].m, cfgs[i].n, cfgs[i].k};
+    const gnw::GnResult r =
+        ctx_of(ctx).gauss_newton(m0, m_ref, e.data(), static_cast<int64_t>(n_cfg), g_obs, c, m_out);
+    if (n_steps) *n_steps = r.steps.size();
+    if (final_misfit) *final_misfit = r.final_misfit;
+    for (uint64_t k = 0; steps && k < std::min<uint64_t>(steps_cap, r.steps.size()); ++k) {
+      const gnw::GnStepReport& q = r.steps[k];
+      steps[k] = {q.misfit, q.minres_iters, q.converged ? 1 : 0, q.euclid_relative_residual,
+                  q.pnorm_relative_residual, q.t_H, q.t_C, q.t_chol, q.t_norm, q.t_forward};
+    }
+  });
+}
+
 gnw_status gnw_geometric_factor(const double a[3], const double* b, const double m[3], const double n[3], int dim,
                                 double* k) {
   return guard([&] { *k = gnw::host::geometric_factor(a, b, m, n, dim); });

@@ -264,6 +264,28 @@ class Context:
         A.check(self.L.gnw_response_jacobian(self.h, _dptr(model), arr, nc, _dptr(J), _dptr(g), tol, C.byref(st)))
         return g, J, {f: getattr(st, f) for f, _ in A.ErtStats._fields_}
 
+    def gauss_newton(self, m0, m_ref, cfgs, g_obs, beta: float = 0.1, max_outer_steps: int = 2,
+                     minres_tol: float = 1e-7, minres_maxit: int = 0, algorithm: str = "woodbury",
+                     misfit_reduction_tol: float = 0.0, forward_tol: float = 1e-14):
+        """gauss_newton (inversion.cpp:187-292), kWoodburyMinres / kLaplaceMinres -> (m, report).
+
+        ``cfgs`` as for ``response_jacobian``; the electrodes come from ``set_electrodes``."""
+        nc = len(cfgs["k"])
+        arr = (A.ErtConfig * nc)(*[A.ErtConfig(int(cfgs["a"][i]), int(cfgs["b"][i]), int(cfgs["m"][i]),
+                                               int(cfgs["n"][i]), float(cfgs["k"][i])) for i in range(nc)])
+        alg = {"woodbury": 0, "laplace": 1}[algorithm]
+        cfg = A.GnConfig(beta, max_outer_steps, minres_tol, minres_maxit, alg, misfit_reduction_tol, forward_tol)
+        m0, m_ref, g_obs = self._in(m0), self._in(m_ref), self._in(g_obs)
+        m_out = self._out(self.N, like=m0 if self.device_pointers else None)
+        cap = max(1, max_outer_steps)
+        steps = (A.GnStep * cap)()
+        n_steps, fin = C.c_uint64(), C.c_double()
+        A.check(self.L.gnw_gauss_newton(self.h, _dptr(m0), _dptr(m_ref), arr, nc, _dptr(g_obs), C.byref(cfg),
+                                        _dptr(m_out), steps, cap, C.byref(n_steps), C.byref(fin)))
+        rep = {"steps": [{f: getattr(steps[k], f) for f, _ in A.GnStep._fields_} for k in range(n_steps.value)],
+               "final_misfit": fin.value}
+        return m_out, rep
+
     def woodbury_factors(self):
         """(H, L): H = S_hat^-1 J^T (N x m, h_hat layout) and the capacitance Cholesky factor."""
         H = np.zeros((self.N, self.m))
