@@ -113,6 +113,20 @@ int orc_gauss_newton(orc_problem* p, const int64_t* nodes, uint64_t n_nodes, con
                      const double* m_ref, const double* m0, double beta, uint64_t max_outer_steps, double minres_tol,
                      uint64_t minres_maxit, int algorithm, double misfit_reduction_tol, double* m_out,
                      double* steps, uint64_t steps_cap, uint64_t* n_steps, double* final_misfit);
+/* The reference's file formats (reference library only): mesh JSON (mesh.cpp:331-383),
+ * survey CSV (survey.cpp:81-116), model JSON (kind 0) / observations CSV (kind 1)
+ * (forward.cpp:174-219), result JSON (inversion.cpp:294-317; steps: 9 doubles each).
+ * Readers: call with NULL arrays for the counts first. */
+int orc_io_write_mesh(orc_problem* p, const int64_t* electrodes, uint64_t ne, const char* path);
+int orc_io_read_mesh(const char* path, uint64_t* nv, uint64_t* nc, uint64_t* ne, double* vertices, int64_t* cells,
+                     int64_t* electrodes);
+int orc_io_write_survey(const int64_t* a, const int64_t* b, const int64_t* m, const int64_t* n, const double* k,
+                        uint64_t count, const char* path);
+int orc_io_read_survey(const char* path, uint64_t* count, int64_t* a, int64_t* b, int64_t* m, int64_t* n, double* k);
+int orc_io_write_vector(int kind, const double* v, uint64_t count, const char* path);
+int orc_io_read_vector(int kind, const char* path, uint64_t* count, double* v);
+int orc_io_write_result(const double* m, uint64_t N, const double* steps, uint64_t n_steps, double final_misfit,
+                        uint64_t K, uint64_t M, const char* path);
 /* geometric_factor (survey.cpp:22-46); b == NULL: pole at infinity. */
 int orc_geometric_factor(const double a[3], const double* b, const double m[3], const double n[3], int dim,
                          double* k);

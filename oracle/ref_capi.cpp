@@ -445,6 +445,110 @@ int orc_gauss_newton(orc_problem* p, const int64_t* nodes, uint64_t n_nodes, con
   });
 }
 
+/* ---- the reference's file formats (used to pin paper_2209_02815_b200/io.py) ---- */
+int orc_io_write_mesh(orc_problem* p, const int64_t* electrodes, uint64_t ne, const char* path) {
+  return guard([&] {
+    p->mesh.electrode_nodes.assign(electrodes, electrodes + ne);
+    write_mesh_json(p->mesh, path);
+  });
+}
+
+int orc_io_read_mesh(const char* path, uint64_t* nv, uint64_t* nc, uint64_t* ne, double* vertices, int64_t* cells,
+                     int64_t* electrodes) {
+  return guard([&] {
+    const Mesh m = read_mesh_json(path);
+    *nv = m.vertices.size();
+    *nc = m.cells.size();
+    *ne = m.electrode_nodes.size();
+    if (vertices)
+      for (std::size_t i = 0; i < m.vertices.size(); ++i) {
+        vertices[2 * i] = m.vertices[i][0];
+        vertices[2 * i + 1] = m.vertices[i][1];
+      }
+    if (cells)
+      for (std::size_t c = 0; c < m.cells.size(); ++c)
+        for (int k = 0; k < 3; ++k) cells[3 * c + k] = static_cast<int64_t>(m.cells[c][k]);
+    if (electrodes)
+      for (std::size_t e = 0; e < m.electrode_nodes.size(); ++e) electrodes[e] = static_cast<int64_t>(m.electrode_nodes[e]);
+  });
+}
+
+int orc_io_write_survey(const int64_t* a, const int64_t* b, const int64_t* m, const int64_t* n, const double* k,
+                        uint64_t count, const char* path) {
+  return guard([&] {
+    Survey s;
+    for (uint64_t i = 0; i < count; ++i) {
+      ElectrodeConfig c;
+      c.a = static_cast<std::size_t>(a[i]);
+      c.b = static_cast<std::ptrdiff_t>(b[i]);
+      c.m = static_cast<std::size_t>(m[i]);
+      c.n = static_cast<std::size_t>(n[i]);
+      c.k = k[i];
+      s.configs.push_back(c);
+    }
+    write_survey_csv(s, path);
+  });
+}
+
+int orc_io_read_survey(const char* path, uint64_t* count, int64_t* a, int64_t* b, int64_t* m, int64_t* n, double* k) {
+  return guard([&] {
+    const Survey s = read_survey_csv(path);
+    *count = s.configs.size();
+    if (a)
+      for (std::size_t i = 0; i < s.configs.size(); ++i) {
+        a[i] = static_cast<int64_t>(s.configs[i].a);
+        b[i] = static_cast<int64_t>(s.configs[i].b);
+        m[i] = static_cast<int64_t>(s.configs[i].m);
+        n[i] = static_cast<int64_t>(s.configs[i].n);
+        k[i] = s.configs[i].k;
+      }
+  });
+}
+
+int orc_io_write_vector(int kind, const double* v, uint64_t count, const char* path) {
+  return guard([&] {
+    const Vector x(v, v + count);
+    if (kind == 0)
+      write_model_json(x, path);
+    else
+      write_observations_csv(x, path);
+  });
+}
+
+int orc_io_read_vector(int kind, const char* path, uint64_t* count, double* v) {
+  return guard([&] {
+    const Vector x = kind == 0 ? read_model_json(path) : read_observations_csv(path);
+    *count = x.size();
+    if (v) std::memcpy(v, x.data(), x.size() * sizeof(double));
+  });
+}
+
+int orc_io_write_result(const double* m, uint64_t N, const double* steps, uint64_t n_steps, double final_misfit,
+                        uint64_t K, uint64_t M, const char* path) {
+  return guard([&] {
+    GnReport r;
+    for (uint64_t i = 0; i < n_steps; ++i) {
+      const double* q = steps + 9 * i;
+      GnStepReport s;
+      s.misfit = q[0];
+      s.minres_iters = static_cast<std::size_t>(q[1]);
+      s.converged = q[2] != 0.0;
+      s.euclid_relative_residual = q[3];
+      s.pnorm_relative_residual = q[4];
+      s.t_H = q[5];
+      s.t_C = q[6];
+      s.t_chol = q[7];
+      s.t_norm = q[8];
+      r.steps.push_back(s);
+    }
+    r.final_misfit = final_misfit;
+    r.n_flux_dofs = K;
+    r.n_cell_dofs = N;
+    r.n_measurements = M;
+    write_result_json(ModelVector(m, m + N), r, path);
+  });
+}
+
 int orc_geometric_factor(const double a[3], const double* b, const double m[3], const double n[3], int dim, double* k) {
   return guard([&] {
     std::optional<std::array<double, 3>> bb;
