@@ -52,6 +52,33 @@ __device__ __forceinline__ void ld8_strided(double* v, const double* p, long lon
       : "l"(p), "l"(stride_bytes));
 }
 
+// Sixteen at once: ptxas may schedule adds between two 8-load statements (the adds wait for
+// the first eight), so a 16-deep batch needs one statement.
+__device__ __forceinline__ void ld16_strided(double* v, const double* p, long long stride_bytes) {
+  asm volatile(
+      "{\n\t.reg .u64 a;\n\t"
+      "mov.u64 a, %16;\n\t"
+      "ld.global.nc.f64 %0, [a];\n\tadd.u64 a, a, %17;\n\t"
+      "ld.global.nc.f64 %1, [a];\n\tadd.u64 a, a, %17;\n\t"
+      "ld.global.nc.f64 %2, [a];\n\tadd.u64 a, a, %17;\n\t"
+      "ld.global.nc.f64 %3, [a];\n\tadd.u64 a, a, %17;\n\t"
+      "ld.global.nc.f64 %4, [a];\n\tadd.u64 a, a, %17;\n\t"
+      "ld.global.nc.f64 %5, [a];\n\tadd.u64 a, a, %17;\n\t"
+      "ld.global.nc.f64 %6, [a];\n\tadd.u64 a, a, %17;\n\t"
+      "ld.global.nc.f64 %7, [a];\n\tadd.u64 a, a, %17;\n\t"
+      "ld.global.nc.f64 %8, [a];\n\tadd.u64 a, a, %17;\n\t"
+      "ld.global.nc.f64 %9, [a];\n\tadd.u64 a, a, %17;\n\t"
+      "ld.global.nc.f64 %10, [a];\n\tadd.u64 a, a, %17;\n\t"
+      "ld.global.nc.f64 %11, [a];\n\tadd.u64 a, a, %17;\n\t"
+      "ld.global.nc.f64 %12, [a];\n\tadd.u64 a, a, %17;\n\t"
+      "ld.global.nc.f64 %13, [a];\n\tadd.u64 a, a, %17;\n\t"
+      "ld.global.nc.f64 %14, [a];\n\tadd.u64 a, a, %17;\n\t"
+      "ld.global.nc.f64 %15, [a];\n\t}"
+      : "=d"(v[0]), "=d"(v[1]), "=d"(v[2]), "=d"(v[3]), "=d"(v[4]), "=d"(v[5]), "=d"(v[6]), "=d"(v[7]),
+        "=d"(v[8]), "=d"(v[9]), "=d"(v[10]), "=d"(v[11]), "=d"(v[12]), "=d"(v[13]), "=d"(v[14]), "=d"(v[15])
+      : "l"(p), "l"(stride_bytes));
+}
+
 // sum_{i < m} p[i * ld] * s[i], accumulated in ascending i (the reference's matvec order):
 // the loads of a batch are issued before its sequential adds, so every thread keeps
 // kSweepBatch 8-byte loads in flight.
@@ -62,8 +89,13 @@ __device__ __forceinline__ double col_dot(const double* __restrict__ p, long lon
   int i = 0;
   for (; i + B <= m; i += B) {
     double v[B];
+    if constexpr (B % 16 == 0) {
 #pragma unroll
-    for (int k = 0; k < B; k += 8) ld8_strided(v + k, p + static_cast<long long>(i + k) * ld, ld * 8);
+      for (int k = 0; k < B; k += 16) ld16_strided(v + k, p + static_cast<long long>(i + k) * ld, ld * 8);
+    } else {
+#pragma unroll
+      for (int k = 0; k < B; k += 8) ld8_strided(v + k, p + static_cast<long long>(i + k) * ld, ld * 8);
+    }
 #pragma unroll
     for (int k = 0; k < B; ++k) acc = acc + v[k] * s[i + k];
   }
@@ -509,7 +541,10 @@ void row_gemv(const double* A, int m, long long N, long long ld, VSel x, long lo
 // ======================================================================
 // Saddle operator  y = [Q x1 + D^T x2 ; D x1 - (1/beta) J^T (J x2)]
 // ======================================================================
-__global__ void __launch_bounds__(kTpb) k_saddle(OperatorArgs op, VSel xs, int scaled, const double* __restrict__ u,
+// B = 16 (m >= 1024): the register budget of 5 CTAs per SM lets ptxas keep the 16 loads of a
+// batch in flight (with the default budget it interleaves them with the add chain at 32 registers)
+template <int B>
+__global__ void __launch_bounds__(kTpb, B >= 16 ? 5 : 8) k_saddle(OperatorArgs op, VSel xs, int scaled, const double* __restrict__ u,
                                                  VSel ys, MinresState* st, int loop, int nb_edge,
                                                  double* part, unsigned* counter) {
   griddep_wait();
@@ -555,7 +590,7 @@ __global__ void __launch_bounds__(kTpb) k_saddle(OperatorArgs op, VSel xs, int s
       if (op.m > 0 && op.q != nullptr) {  // fused: J^T (J zhat2) = J^T (t' * ig) ~ q * ig (Woodbury identity J z2 = t')
         o = o + *op.neg_inv_beta * (op.q[c] * sc);
       } else if (op.m > 0 && c >= op.c_lo && (op.c_hi < 0 || c < op.c_hi)) {  // matvec_transpose(J, J dm), linalg.cpp:45-54
-        const double jt = col_dot<8>(op.J + (c - op.c_lo), op.ldj, usm, op.m);
+        const double jt = col_dot<B>(op.J + (c - op.c_lo), op.ldj, usm, op.m);
         o = o + *op.neg_inv_beta * jt;  // axpy(-1.0 / beta, jtjdm, out2)
       }
       y[op.K + c] = o;
@@ -578,7 +613,7 @@ __global__ void __launch_bounds__(kTpb) k_saddle(OperatorArgs op, VSel xs, int s
 void saddle_operator(const OperatorArgs& op, VSel x, int scaled, const double* u, VSel y, MinresState* st,
                      int loop, double* partial, unsigned* counter, cudaStream_t s) {
   const int nbe = static_cast<int>(grid_for(op.K)), nbc = static_cast<int>(grid_for(op.N));
-  GNW_LAUNCH(launch_k(k_saddle, nbe + nbc, kTpb, std::max(op.m, 1) * sizeof(double), s, op, x, scaled, u, y, st, loop, nbe,
+  GNW_LAUNCH(launch_k(op.m >= kSweepBatchWideM ? k_saddle<16> : k_saddle<8>, nbe + nbc, kTpb, std::max(op.m, 1) * sizeof(double), s, op, x, scaled, u, y, st, loop, nbe,
                                                                        partial, counter));
   check_launch("saddle_operator");
 }

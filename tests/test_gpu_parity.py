@@ -111,6 +111,30 @@ def test_operator_precondition_rhs(c1, gpu_ctx_factory, n, m):
     assert np.array_equal(b, bref)  # assemble_gn_rhs is bit-exact (reference op order)
 
 
+def test_operator_precondition_wide_m(oracle, gpu_ctx_factory):
+    """m >= 1024 takes the 16-deep column-sweep kernels (k_saddle<16>, k_finish_prec<16>) and
+    a multi-row-group row GEMV; C3/C5-shaped m on a small mesh."""
+    n, m = 24, 1100
+    mesh = W.unit_square_mesh(n)
+    J = W.synthetic_jacobian(m, mesh.n_cells, 7)
+    prob = orc.Problem.mixed(oracle, mesh)
+    ctx = gpu_ctx_factory(mesh, exact=False)
+    beta = 1e-2
+    ctx.set_jacobian(J, beta)
+    prob.set_jacobian(J, beta)
+    x = W.gaussian(5, prob.K + prob.N)
+    assert rel(ctx.apply_operator(x), prob.apply_operator(x)) <= 1e-13
+    assert rel(ctx.precondition(x), prob.precondition(x)) <= 1e-10
+    dg = W.gaussian(6, m)
+    b = ctx.assemble_rhs(W.gaussian(7, prob.N), np.zeros(prob.N), dg, np.zeros(m))
+    bref = prob.assemble_rhs(W.gaussian(7, prob.N), np.zeros(prob.N), dg, np.zeros(m))
+    assert np.array_equal(b, bref)
+    xs, rep = ctx.minres(b, tol=1e-10)
+    xr, rr = prob.minres(bref, tol=1e-10)
+    assert abs(rep.iterations - rr["iterations"]) <= 1
+    assert rel(xs, xr) <= 1e-8
+
+
 def test_operator_without_J_bitwise(c1, gpu_ctx_factory):
     mesh, inp, prob = c1[16]
     ctx = gpu_ctx_factory(mesh)
