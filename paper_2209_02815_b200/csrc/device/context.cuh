@@ -175,7 +175,7 @@ class Context {
   RowGemv plan_{};    // J x (nothing runs beside it)
   RowGemv plan_h_{};  // H^T y (leaves CTA slots for the forked V-cycle)
   int exp_skip_ = 0;     // profiling only (profile_kernel "body"): bit mask of iteration parts left out
-  int rg_reserve_ = 1;  // env GNW_RG_RESERVE (C2 sweep: 0: 0.919, 1: 0.859, 2: 0.863 ms/iteration)
+  int rg_reserve_ = 2;  // env GNW_RG_RESERVE; of 4 resident k_row_gemv CTAs per SM (C2 sweep: 0: 0.895, 1: 0.862, 2: 0.847, 3: 0.950 ms/iteration)
 
   // MINRES vectors
   double *b_ = nullptr, *x_ = nullptr, *r_ = nullptr, *az_ = nullptr, *tmp_ = nullptr, *tmp2_ = nullptr;
