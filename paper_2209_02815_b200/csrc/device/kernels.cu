@@ -638,30 +638,46 @@ __global__ void __launch_bounds__(kTpb) k_combine_elem(PrecArgs pa, VSel azs, VS
   const double* __restrict__ vc = loop ? vsel(vcs, st) : nullptr;
   const double* __restrict__ vp = loop ? vsel(vps, st) : nullptr;
   double d[3] = {0.0, 0.0, 0.0};  // <z, v>, <z, z>, <v, v>
-  const long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (i < pa.K + pa.N) {
+  const long long n = pa.K + pa.N;
+  // two consecutive elements per thread, 16-byte loads (all vectors are separate allocations)
+  const long long i0 = 2 * (static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x);
+  auto one = [&](long long i, double a, double b, double c) {
     double v;
     if (loop) {
-      v = az[i] + c1 * vc[i];  // combine: ca*a + cb*b + cc*c, ca = 1
-      v = v + c2 * vp[i];
-      vn[i] = v;
+      v = a + c1 * b;  // combine: ca*a + cb*b + cc*c, ca = 1
+      v = v + c2 * c;
     } else {
-      v = az[i];
+      v = a;
     }
     if (i < pa.K) {
       const double z = __ldg(&pa.qinv[i]) * v;
       zn[i] = z;
-      d[0] = z * v;
-      d[1] = z * z;
+      d[0] = d[0] + z * v;
+      d[1] = d[1] + z * z;
     }
-    d[2] = v * v;
+    d[2] = d[2] + v * v;
+    return v;
+  };
+  if (i0 + 1 < n) {
+    const double2 a = *reinterpret_cast<const double2*>(az + i0);
+    double2 b = make_double2(0.0, 0.0), c = make_double2(0.0, 0.0);
+    if (loop) {
+      b = *reinterpret_cast<const double2*>(vc + i0);
+      c = *reinterpret_cast<const double2*>(vp + i0);
+    }
+    const double v0 = one(i0, a.x, b.x, c.x);
+    const double v1 = one(i0 + 1, a.y, b.y, c.y);
+    if (loop) *reinterpret_cast<double2*>(vn + i0) = make_double2(v0, v1);
+  } else if (i0 < n) {
+    const double v0 = one(i0, az[i0], loop ? vc[i0] : 0.0, loop ? vp[i0] : 0.0);
+    if (loop) vn[i0] = v0;
   }
   block_reduce<3>(d, red);
   if (threadIdx.x == 0)
     for (int k = 0; k < 3; ++k) dots_part[blockIdx.x * 3 + k] = d[k];
 }
 
-int combine_blocks(long long K, long long N) { return static_cast<int>(grid_for(K + N)); }
+int combine_blocks(long long K, long long N) { return static_cast<int>(grid_for((K + N + 1) / 2)); }
 
 void combine_elem(const PrecArgs& pa, VSel az, VSel vcur, VSel vprev, VSel vnext, VSel znext, int loop,
                   MinresState* st, double* dots_part, cudaStream_t s) {
@@ -927,21 +943,39 @@ __global__ void __launch_bounds__(kTpb) k_minres_update(long long n, VSel zs, VS
   const double ig = st->inv_gamma, na3 = -st->alpha3, na2 = -st->alpha2, ia = st->inv_alpha1;
   const double tau = st->tau, ntau = -tau;
   double rr[1] = {0.0};
-  for (long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
-       i += static_cast<long long>(gridDim.x) * blockDim.x) {
-    const double zh = z[i] * ig;
-    double w = zh + na3 * wp[i];
-    w = w + na2 * wc[i];
+  // minres.cpp:93-106 per element; pairs of elements with 16-byte loads/stores
+  auto elem = [&](double zv, double wpv, double wcv, double azv, double upv, double ucv, double xv, double rv,
+                  double& wo, double& uo, double& xo, double& ro) {
+    const double zh = zv * ig;
+    double w = zh + na3 * wpv;
+    w = w + na2 * wcv;
     w = w * ia;
-    double uu = az[i] + na3 * up[i];
-    uu = uu + na2 * uc[i];
+    double uu = azv + na3 * upv;
+    uu = uu + na2 * ucv;
     uu = uu * ia;
-    wn[i] = w;
-    un[i] = uu;
-    x[i] = x[i] + tau * w;
-    const double ri = r[i] + ntau * uu;
-    r[i] = ri;
-    rr[0] = rr[0] + ri * ri;
+    wo = w;
+    uo = uu;
+    xo = xv + tau * w;
+    ro = rv + ntau * uu;
+    rr[0] = rr[0] + ro * ro;
+  };
+  const long long np = n / 2;
+  auto ld2 = [](const double* p, long long k) { return *reinterpret_cast<const double2*>(p + 2 * k); };
+  for (long long k = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; k < np;
+       k += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const double2 zv = ld2(z, k), wpv = ld2(wp, k), wcv = ld2(wc, k), azv = ld2(az, k), upv = ld2(up, k),
+                  ucv = ld2(uc, k), xv = ld2(x, k), rv = ld2(r, k);
+    double2 wo, uo, xo, ro;
+    elem(zv.x, wpv.x, wcv.x, azv.x, upv.x, ucv.x, xv.x, rv.x, wo.x, uo.x, xo.x, ro.x);
+    elem(zv.y, wpv.y, wcv.y, azv.y, upv.y, ucv.y, xv.y, rv.y, wo.y, uo.y, xo.y, ro.y);
+    *reinterpret_cast<double2*>(wn + 2 * k) = wo;
+    *reinterpret_cast<double2*>(un + 2 * k) = uo;
+    *reinterpret_cast<double2*>(x + 2 * k) = xo;
+    *reinterpret_cast<double2*>(r + 2 * k) = ro;
+  }
+  if ((n & 1) && blockIdx.x == 0 && threadIdx.x == 0) {
+    const long long i = n - 1;
+    elem(z[i], wp[i], wc[i], az[i], up[i], uc[i], x[i], r[i], wn[i], un[i], x[i], r[i]);
   }
   double tot[1];
   if (!grid_reduce_last<1>(rr, part, counter, red, tot) || threadIdx.x != 0 || use_cond == 2) return;
@@ -974,7 +1008,7 @@ __global__ void __launch_bounds__(kTpb) k_minres_update(long long n, VSel zs, VS
 void minres_update(long long n, VSel z, VSel az, VSel wprev, VSel wcur, VSel wnext, VSel uprev, VSel ucur, VSel unext,
                    double* x, double* r, MinresState* st, double* hist_e, double* hist_p, long long hist_cap,
                    double* part, unsigned* counter, unsigned long long cond_handle, int use_cond, cudaStream_t s) {
-  const unsigned grid = std::min<unsigned>(grid_for(n), 148u * 8u);
+  const unsigned grid = std::min<unsigned>(grid_for((n + 1) / 2), 148u * 8u);
   GNW_LAUNCH(launch_k(k_minres_update, grid, kTpb, 0, s, n, z, az, wprev, wcur, wnext, uprev, ucur, unext, x, r, st, hist_e, hist_p,
                                         hist_cap, part, counter,
                                         static_cast<cudaGraphConditionalHandle>(cond_handle), use_cond));
