@@ -163,13 +163,21 @@ __global__ void __launch_bounds__(1024) k_trinv_block(const double* __restrict__
   const int i = p + r;
   const int j = blockIdx.x * 32 + jc;      // global column
   const bool act = i < n && j <= i;
-  double s = 0.0;
-  if (act) {
-    s = (i == j) ? 1.0 : 0.0;
-    // rows k < p of Y were written by earlier launches: read-only here
-#pragma unroll 8
-    for (int k = j; k < p; ++k)
-      s = s - __ldg(&L[static_cast<long long>(i) * n + k]) * __ldg(&Y[static_cast<long long>(k) * n + j]);
+  // s = [i == j] - sum_{k < p} L[i][k] Y[k][j], k ascending.  Rows k < p of Y were written by
+  // earlier launches.  The sum runs over 32 x 32 shared-memory tiles of L and Y (one global
+  // load of each per thread per tile) instead of p dependent L2 loads per thread; Y[k][j] = 0
+  // for k < j, so starting every column of the chunk at the chunk's first column only adds
+  // exact zeros and leaves the rounding unchanged.
+  __shared__ double Ls[32][33], Ys[32][33];
+  double s = (act && i == j) ? 1.0 : 0.0;
+  for (int k0 = blockIdx.x * 32; k0 < p; k0 += 32) {
+    const int kk = min(32, p - k0);
+    Ls[r][jc] = (i < n && jc < kk) ? __ldg(&L[static_cast<long long>(i) * n + k0 + jc]) : 0.0;
+    Ys[r][jc] = (r < kk && j < n) ? __ldg(&Y[static_cast<long long>(k0 + r) * n + j]) : 0.0;
+    __syncthreads();
+    if (act)
+      for (int t = 0; t < kk; ++t) s = s - Ls[r][t] * Ys[t][jc];
+    __syncthreads();
   }
   const int w = min(32, n - p);
   for (int rr = 0; rr < w; ++rr) {

@@ -181,8 +181,8 @@ __global__ void __launch_bounds__(256) k_dense_emul_batch(const double* __restri
   Y[static_cast<long long>(i) * b + q] = tree32(p);
 }
 
-// Y[:, q] = M X[:, q], one thread per (row, column), j ascending (sequential order):
-// X loads coalesced over the columns, M rows broadcast within a warp; ~20 registers.
+// Y[:, q] = M X[:, q], one thread per (row, column): X loads coalesced over the columns,
+// M rows broadcast within a warp.
 __global__ void __launch_bounds__(256) k_dense_seq_batch(const double* __restrict__ M, int n,
                                                          const double* __restrict__ X, double* __restrict__ Y, int b) {
   griddep_wait();
@@ -190,10 +190,17 @@ __global__ void __launch_bounds__(256) k_dense_seq_batch(const double* __restric
   const int q = blockIdx.y * 32 + threadIdx.x;
   if (i >= n || q >= b) return;
   const double* __restrict__ Mi = M + static_cast<long long>(i) * n;
-  double acc = 0.0;
-#pragma unroll 8
-  for (int j = 0; j < n; ++j) acc = acc + __ldg(&Mi[j]) * X[static_cast<long long>(j) * b + q];
-  Y[static_cast<long long>(i) * b + q] = acc;
+  // four interleaved partial sums (default mode only; four loads in flight per thread)
+  double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+  int j = 0;
+  for (; j + 4 <= n; j += 4) {
+    a0 = a0 + __ldg(&Mi[j]) * X[static_cast<long long>(j) * b + q];
+    a1 = a1 + __ldg(&Mi[j + 1]) * X[static_cast<long long>(j + 1) * b + q];
+    a2 = a2 + __ldg(&Mi[j + 2]) * X[static_cast<long long>(j + 2) * b + q];
+    a3 = a3 + __ldg(&Mi[j + 3]) * X[static_cast<long long>(j + 3) * b + q];
+  }
+  for (; j < n; ++j) a0 = a0 + __ldg(&Mi[j]) * X[static_cast<long long>(j) * b + q];
+  Y[static_cast<long long>(i) * b + q] = (a0 + a1) + (a2 + a3);
 }
 
 __global__ void k_identity_rows(double* __restrict__ I, int n) {
