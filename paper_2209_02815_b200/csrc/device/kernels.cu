@@ -325,21 +325,18 @@ __global__ void __launch_bounds__(256) k_mvc_up2(DCsr A, const double* __restric
 }
 
 void mvc_down(const DLevel& L, const double* r, int ldr, double* resid, int b, cudaStream_t s) {
-  if (L.wideA) return mvce_down(L, r, ldr, resid, b, s);
   if (b % 2 == 0 && ldr % 2 == 0) return mvc2_down(L, r, ldr, resid, b, s);
   dim3 grid((L.n + 7) / 8, (b + 31) / 32), block(32, 8);
   GNW_LAUNCH(launch_k(k_mvc_down, grid, block, 0, s, L.A, L.wd, r, ldr, resid, b));
   check_launch("mvc_down");
 }
 void mvc_restrict(const DLevel& L, const double* resid, double* rc, int b, cudaStream_t s) {
-  if (L.wideR) return mvce_restrict(L, resid, rc, b, s);
   if (b % 2 == 0) return mvc2_restrict(L, resid, rc, b, s);
   dim3 grid((L.R.n_rows + 7) / 8, (b + 31) / 32), block(32, 8);
   GNW_LAUNCH(launch_k(k_mvc_restrict, grid, block, 0, s, L.R, resid, rc, b));
   check_launch("mvc_restrict");
 }
 void mvc_up1(const DLevel& L, const double* r, int ldr, const double* ec, double* x, int b, cudaStream_t s) {
-  if (L.wideP) return mvce_up1(L, r, ldr, ec, x, b, s);
   if (b % 2 == 0 && ldr % 2 == 0) return mvc2_up1(L, r, ldr, ec, x, b, s);
   dim3 grid((L.n + 7) / 8, (b + 31) / 32), block(32, 8);
   GNW_LAUNCH(launch_k(k_mvc_up1, grid, block, 0, s, L.P, L.wd, r, ldr, ec, x, b));
@@ -347,7 +344,6 @@ void mvc_up1(const DLevel& L, const double* r, int ldr, const double* ec, double
 }
 void mvc_up2(const DLevel& L, const double* r, int ldr, const double* x, double* out, int ldo, int b,
              cudaStream_t s) {
-  if (L.wideA) return mvce_up2(L, r, ldr, x, out, ldo, b, s);
   if (b % 2 == 0 && ldr % 2 == 0 && ldo % 2 == 0) return mvc2_up2(L, r, ldr, x, out, ldo, b, s);
   dim3 grid((L.n + 7) / 8, (b + 31) / 32), block(32, 8);
   GNW_LAUNCH(launch_k(k_mvc_up2, grid, block, 0, s, L.A, L.wd, r, ldr, x, out, ldo, b));

@@ -46,11 +46,6 @@ void vcw_down(const DLevel& L, VSel r, double* resid, const MinresState* st, cud
 void vcw_restrict(const DLevel& L, const double* resid, double* rc, cudaStream_t s);
 void vcw_up1(const DLevel& L, VSel r, const double* ec, double* x, const MinresState* st, cudaStream_t s);
 void vcw_up2(const DLevel& L, VSel r, const double* x, double* out, const MinresState* st, cudaStream_t s);
-void mvce_down(const DLevel& L, const double* r, int ldr, double* resid, int b, cudaStream_t s);
-void mvce_restrict(const DLevel& L, const double* resid, double* rc, int b, cudaStream_t s);
-void mvce_up1(const DLevel& L, const double* r, int ldr, const double* ec, double* x, int b, cudaStream_t s);
-void mvce_up2(const DLevel& L, const double* r, int ldr, const double* x, double* out, int ldo, int b,
-              cudaStream_t s);
 
 // narrow-level batched kernels, 2 columns per thread (vcycle_batch.cu); even b only
 void mvc2_down(const DLevel& L, const double* r, int ldr, double* resid, int b, cudaStream_t s);
@@ -80,8 +75,6 @@ void mvc_up1(const DLevel& L, const double* r, int ldr, const double* ec, double
 void mvc_up2(const DLevel& L, const double* r, int ldr, const double* x, double* out, int ldo, int b,
              cudaStream_t s);
 void mcoarse_inverse(const double* Ainv, int n, const double* r, double* x, int b, cudaStream_t s);
-// collapsed coarse tail (amg_device.cu): batched dense apply, bit-identical per column to coarse_inverse
-void dense_emul_batch(const double* M, int n, const double* X, double* Y, int b, cudaStream_t s);
 // batched dense apply in sequential order (the batched V-cycle's collapsed tail)
 void dense_seq_batch(const double* M, int n, const double* X, double* Y, int b, cudaStream_t s);
 void identity_rows(double* I, int n, cudaStream_t s);

@@ -23,15 +23,6 @@ void note_launch(const char* what);
 
 namespace {
 
-__device__ __forceinline__ double tree32(double (&p)[32]) {
-  // lane 0's view of the xor butterfly: own + partner at offsets 16, 8, 4, 2, 1
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1)
-#pragma unroll
-    for (int l = 0; l < o; ++l) p[l] = p[l] + p[l + o];
-  return p[0];
-}
-
 template <class F>
 __device__ __forceinline__ double warp_row(const DCsr& A, int i, int lane, F f) {
   double acc = 0.0;
@@ -42,24 +33,6 @@ __device__ __forceinline__ double warp_row(const DCsr& A, int i, int lane, F f) 
   double v[1] = {acc};
   warp_reduce<1>(v);
   return v[0];
-}
-
-// One pass over the row in groups of 32 consecutive entries; entry k feeds the
-// partial of lane class (k - k0) % 32 -- the same per-class order as warp_row.
-template <class F>
-__device__ __forceinline__ double emul_row(const DCsr& A, int i, F f) {
-  double p[32];
-#pragma unroll
-  for (int l = 0; l < 32; ++l) p[l] = 0.0;
-  const int k0 = A.rowptr[i], k1 = A.rowptr[i + 1];
-  for (int g = k0; g < k1; g += 32) {
-#pragma unroll
-    for (int l = 0; l < 32; ++l) {
-      const int k = g + l;
-      if (k < k1) p[l] = p[l] + __ldg(&A.vals[k]) * f(A.cols[k]);
-    }
-  }
-  return tree32(p);
 }
 
 constexpr int kRowsPerBlock = 8;  // 8 warps, one row each
@@ -111,76 +84,7 @@ __global__ void __launch_bounds__(256) k_vcw_up2(DCsr A, const double* __restric
   }
 }
 
-// ---------------------------------------------------------------- multi RHS
-__global__ void __launch_bounds__(256) k_mvce_down(DCsr A, const double* __restrict__ wd,
-                                                   const double* __restrict__ r, int ldr,
-                                                   double* __restrict__ resid, int b) {
-  griddep_wait();
-  const int i = blockIdx.x * 8 + threadIdx.y;
-  const int q = blockIdx.y * 32 + threadIdx.x;
-  if (i >= A.n_rows || q >= b) return;
-  const double s = emul_row(A, i, [&](int c) { return __ldg(&wd[c]) * r[static_cast<long long>(c) * ldr + q]; });
-  resid[static_cast<long long>(i) * b + q] = r[static_cast<long long>(i) * ldr + q] + (-1.0 * s);
-}
-
-__global__ void __launch_bounds__(256) k_mvce_restrict(DCsr R, const double* __restrict__ resid,
-                                                       double* __restrict__ rc, int b) {
-  griddep_wait();
-  const int a = blockIdx.x * 8 + threadIdx.y;
-  const int q = blockIdx.y * 32 + threadIdx.x;
-  if (a >= R.n_rows || q >= b) return;
-  rc[static_cast<long long>(a) * b + q] = emul_row(R, a, [&](int c) { return resid[static_cast<long long>(c) * b + q]; });
-}
-
-__global__ void __launch_bounds__(256) k_mvce_up1(DCsr P, const double* __restrict__ wd,
-                                                  const double* __restrict__ r, int ldr,
-                                                  const double* __restrict__ ec, double* __restrict__ x, int b) {
-  griddep_wait();
-  const int i = blockIdx.x * 8 + threadIdx.y;
-  const int q = blockIdx.y * 32 + threadIdx.x;
-  if (i >= P.n_rows || q >= b) return;
-  const double s = emul_row(P, i, [&](int c) { return ec[static_cast<long long>(c) * b + q]; });
-  x[static_cast<long long>(i) * b + q] = __ldg(&wd[i]) * r[static_cast<long long>(i) * ldr + q] + 1.0 * s;
-}
-
-__global__ void __launch_bounds__(256) k_mvce_up2(DCsr A, const double* __restrict__ wd,
-                                                  const double* __restrict__ r, int ldr,
-                                                  const double* __restrict__ x, double* __restrict__ out,
-                                                  int ldo, int b) {
-  griddep_wait();
-  const int i = blockIdx.x * 8 + threadIdx.y;
-  const int q = blockIdx.y * 32 + threadIdx.x;
-  if (i >= A.n_rows || q >= b) return;
-  const double s = emul_row(A, i, [&](int c) { return x[static_cast<long long>(c) * b + q]; });
-  const double res = r[static_cast<long long>(i) * ldr + q] + (-1.0 * s);
-  out[static_cast<long long>(i) * ldo + q] = x[static_cast<long long>(i) * b + q] + __ldg(&wd[i]) * res;
-}
-
 // ------------------------------------------------------- collapsed coarse tail
-// Y[:, q] = M X[:, q] for b interleaved columns, one thread per (row, column): the 32
-// register partials replay k_coarse_inverse's lane partition (lane l sums j = l, l+32, ...)
-// and its xor butterfly, so each column is bit-identical to the single-RHS dense apply.
-__global__ void __launch_bounds__(256) k_dense_emul_batch(const double* __restrict__ M, int n,
-                                                          const double* __restrict__ X, double* __restrict__ Y,
-                                                          int b) {
-  griddep_wait();
-  const int i = blockIdx.x * 8 + threadIdx.y;
-  const int q = blockIdx.y * 32 + threadIdx.x;
-  if (i >= n || q >= b) return;
-  double p[32];
-#pragma unroll
-  for (int l = 0; l < 32; ++l) p[l] = 0.0;
-  const double* __restrict__ Mi = M + static_cast<long long>(i) * n;
-  for (int g = 0; g < n; g += 32) {
-#pragma unroll
-    for (int l = 0; l < 32; ++l) {
-      const int j = g + l;
-      if (j < n) p[l] = p[l] + __ldg(&Mi[j]) * X[static_cast<long long>(j) * b + q];
-    }
-  }
-  Y[static_cast<long long>(i) * b + q] = tree32(p);
-}
-
 // Y[:, q] = M X[:, q], one thread per (row, column): X loads coalesced over the columns,
 // M rows broadcast within a warp.
 __global__ void __launch_bounds__(256) k_dense_seq_batch(const double* __restrict__ M, int n,
@@ -231,33 +135,6 @@ void vcw_up1(const DLevel& L, VSel r, const double* ec, double* x, const MinresS
 void vcw_up2(const DLevel& L, VSel r, const double* x, double* out, const MinresState* st, cudaStream_t s) {
   GNW_LAUNCH(launch_k(k_vcw_up2, wgrid(L.n), 256, 0, s, L.A, L.wd, r, x, out, st));
   note_launch("vcw_up2");
-}
-void mvce_down(const DLevel& L, const double* r, int ldr, double* resid, int b, cudaStream_t s) {
-  dim3 grid((L.n + 7) / 8, (b + 31) / 32), block(32, 8);
-  GNW_LAUNCH(launch_k(k_mvce_down, grid, block, 0, s, L.A, L.wd, r, ldr, resid, b));
-  note_launch("mvce_down");
-}
-void mvce_restrict(const DLevel& L, const double* resid, double* rc, int b, cudaStream_t s) {
-  dim3 grid((L.R.n_rows + 7) / 8, (b + 31) / 32), block(32, 8);
-  GNW_LAUNCH(launch_k(k_mvce_restrict, grid, block, 0, s, L.R, resid, rc, b));
-  note_launch("mvce_restrict");
-}
-void mvce_up1(const DLevel& L, const double* r, int ldr, const double* ec, double* x, int b, cudaStream_t s) {
-  dim3 grid((L.n + 7) / 8, (b + 31) / 32), block(32, 8);
-  GNW_LAUNCH(launch_k(k_mvce_up1, grid, block, 0, s, L.P, L.wd, r, ldr, ec, x, b));
-  note_launch("mvce_up1");
-}
-void mvce_up2(const DLevel& L, const double* r, int ldr, const double* x, double* out, int ldo, int b,
-              cudaStream_t s) {
-  dim3 grid((L.n + 7) / 8, (b + 31) / 32), block(32, 8);
-  GNW_LAUNCH(launch_k(k_mvce_up2, grid, block, 0, s, L.A, L.wd, r, ldr, x, out, ldo, b));
-  note_launch("mvce_up2");
-}
-
-void dense_emul_batch(const double* M, int n, const double* X, double* Y, int b, cudaStream_t s) {
-  dim3 grid((n + 7) / 8, (b + 31) / 32), block(32, 8);
-  GNW_LAUNCH(launch_k(k_dense_emul_batch, grid, block, 0, s, M, n, X, Y, b));
-  note_launch("dense_emul_batch");
 }
 void dense_seq_batch(const double* M, int n, const double* X, double* Y, int b, cudaStream_t s) {
   dim3 grid((n + 7) / 8, (b + 31) / 32), block(32, 8);
