@@ -14,7 +14,9 @@ per solve) are far larger than the 126 MB L2, so no L2 flush is needed between s
 * value  -- device-resident inputs (torch CUDA tensors, device-pointer mode), timed with CUDA
             events on the library's stream; whole-job throughput (N replicas, max over ranks).
 * e2e    -- the same solves through the C-ABI with HOST buffers (pinned): J, m, m_ref, g, g_obs
-            copied H2D every step inside the timed region; rhs and x copied back D2H.
+            copied H2D every step inside the timed region; rhs and x copied back D2H.  Step k+1's
+            J (1.07 GB) is staged with gnw_prefetch_jacobian during step k's MINRES (copy stream);
+            step 0 copies its own J, so every step's input transfer is inside the timed region.
 * roofline -- the dominant per-iteration kernel measured in isolation with CUDA events
             (gnw_profile_kernel), algorithmic bytes per SURVEY.md 8(d); peak = MEASURED_PEAKS.json.
 * cpu_baseline -- the unmodified reference (oracle/_ref) on this host, 1 core (the reference is
@@ -378,17 +380,23 @@ def run_gnw(args):
     zN_h = torch.from_numpy(inp.rhs_mref).pin_memory().numpy()
     zm_h = torch.from_numpy(inp.rhs_gobs).pin_memory().numpy()
 
-    def solve_host(alpha):
-        ctx.set_jacobian(J_h, alpha)
-        b = ctx.assemble_rhs(dm_h, zN_h, dg_h, zm_h)
-        x, rep = ctx.minres(b, tol=tol)
+    b_h = torch.empty(K + N, dtype=torch.float64, pin_memory=True).numpy()   # rhs (D2H, then H2D)
+    x0_h = torch.zeros(K + N, dtype=torch.float64, pin_memory=True).numpy()
+    x_h = torch.empty(K + N, dtype=torch.float64, pin_memory=True).numpy()   # solution (D2H)
+
+    def solve_host(alpha, prefetch_next):
+        ctx.set_jacobian(J_h, alpha)  # takes the staged copy when the previous step prefetched it
+        b = ctx.assemble_rhs(dm_h, zN_h, dg_h, zm_h, out=b_h)
+        if prefetch_next:  # the next step's J crosses PCIe during this step's MINRES
+            ctx.prefetch_jacobian(J_h)
+        x, rep = ctx.minres(b, x0=x0_h, tol=tol, out=x_h)
         return x, rep
 
-    solve_host(alphas[0])
+    solve_host(alphas[0], False)  # nothing staged when the timed region opens: step 0 copies J itself
     barrier()
     ctx.event_record(2)
     for k in range(args.steps):
-        x_h, rep_h = solve_host(alphas[k % len(alphas)])
+        x_h, rep_h = solve_host(alphas[k % len(alphas)], k + 1 < args.steps)
     ctx.event_record(3)
     e2e_elapsed = max_over_ranks(ctx.event_elapsed(2, 3))
     barrier()

@@ -147,6 +147,12 @@ gnw_status gnw_get_info(const gnw_ctx* ctx, gnw_info* info);
 
 gnw_status gnw_set_jacobian(gnw_ctx* ctx, const double* J, uint64_t m, uint64_t n_cells,
                             double beta, gnw_timings* timings);
+/* Pipelining aid for consecutive GN steps (no reference analogue: the reference
+ * holds J in host memory).  Host-pointer mode only.  Starts the host->device copy
+ * of the NEXT step's J (m x n_cells row-major, ideally pinned) on a copy stream, so
+ * it overlaps the current solve; the next gnw_set_jacobian with the same pointer and
+ * shape takes the staged bytes instead of copying.  J must stay unchanged until then. */
+gnw_status gnw_prefetch_jacobian(gnw_ctx* ctx, const double* J, uint64_t m, uint64_t n_cells);
 
 gnw_status gnw_apply_operator(gnw_ctx* ctx, const double* x, double* y);
 gnw_status gnw_precondition(gnw_ctx* ctx, const double* y, double* z);

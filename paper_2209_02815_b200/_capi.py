@@ -68,7 +68,7 @@ class Stats(C.Structure):
 EXPORTED = [
     "gnw_last_error", "gnw_version", "gnw_create", "gnw_destroy", "gnw_set_pointer_mode",
     "gnw_set_coarse_mode", "gnw_set_preconditioner", "gnw_set_loop_mode", "gnw_assemble", "gnw_assemble_amg_csr", "gnw_get_info",
-    "gnw_set_jacobian", "gnw_apply_operator", "gnw_precondition", "gnw_amg_apply",
+    "gnw_set_jacobian", "gnw_prefetch_jacobian", "gnw_apply_operator", "gnw_precondition", "gnw_amg_apply",
     "gnw_get_woodbury", "gnw_assemble_rhs", "gnw_minres_solve", "gnw_export_csr",
     "gnw_export_mesh", "gnw_dense_cholesky", "gnw_get_stats", "gnw_event_record",
     "gnw_event_elapsed", "gnw_profile_kernel", "gnw_set_electrodes", "gnw_response_jacobian",
@@ -132,6 +132,7 @@ def load() -> C.CDLL:
     L.gnw_assemble_amg_csr.argtypes = [vp, u64, vp, vp, vp, C.POINTER(AmgOptions)]
     L.gnw_get_info.argtypes = [vp, C.POINTER(Info)]
     L.gnw_set_jacobian.argtypes = [vp, vp, u64, u64, dbl, C.POINTER(Timings)]
+    L.gnw_prefetch_jacobian.argtypes = [vp, vp, u64, u64]
     L.gnw_apply_operator.argtypes = [vp, vp, vp]
     L.gnw_precondition.argtypes = [vp, vp, vp]
     L.gnw_amg_apply.argtypes = [vp, vp, vp]

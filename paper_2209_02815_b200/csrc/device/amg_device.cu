@@ -62,6 +62,9 @@ void DeviceAmg::upload(const host::AmgHierarchy& h, cudaStream_t s) {
       d.wideA = H.A.nnz() > kWide * static_cast<double>(H.A.n_rows);
       d.wideP = H.P.nnz() > kWide * static_cast<double>(H.P.n_rows);
       d.wideR = H.P.nnz() > kWide * static_cast<double>(H.P.n_cols);
+      d.gA = vc_group_lanes(H.A.nnz(), H.A.n_rows);
+      d.gP = vc_group_lanes(H.P.nnz(), H.P.n_rows);
+      d.gR = vc_group_lanes(H.P.nnz(), H.P.n_cols);
       std::vector<double> wd(H.inv_diag.size());
       for (size_t i = 0; i < wd.size(); ++i) wd[i] = omega * H.inv_diag[i];  // amg.cpp:98 (omega*inv_diag)*r
       d.wd = mem_.alloc<double>(wd.size());
@@ -159,7 +162,10 @@ void DeviceAmg::cycle_levels(int l0, VSel r, double* out, const MinresState* st,
 // exact mode, warp-per-row kernels on wide levels otherwise.
 DLevel DeviceAmg::level(int l, int exact) const {
   DLevel d = lv_[l];
-  if (exact) d.wideA = d.wideP = d.wideR = 0;
+  if (exact) {
+    d.wideA = d.wideP = d.wideR = 0;
+    d.gA = d.gP = d.gR = 1;
+  }
   return d;
 }
 

@@ -54,6 +54,9 @@ Context::Context(int device) : device_(device) {
     for (auto& e : fork_ev_) GNW_CUDA_CHECK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   }
   for (auto& e : mev_) GNW_CUDA_CHECK(cudaEventCreate(&e));
+  // host->device staging of the next Jacobian (prefetch_jacobian) runs on its own stream
+  GNW_CUDA_CHECK(cudaStreamCreateWithFlags(&copy_, cudaStreamNonBlocking));
+  for (auto& e : stage_ev_) GNW_CUDA_CHECK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   st_ = mem_.alloc<MinresState>(1);
   st_plain_ = mem_.alloc<MinresState>(1);
   counters_ = mem_.alloc<unsigned>(16);
@@ -78,6 +81,10 @@ Context::~Context() {
   for (auto& e : fork_ev_)
     if (e) cudaEventDestroy(e);
   if (side_) cudaStreamSynchronize(side_);
+  if (copy_) cudaStreamSynchronize(copy_);
+  for (auto& e : stage_ev_)
+    if (e) cudaEventDestroy(e);
+  stage_mem_.reset();
   jmem_.reset();
   damg_.reset();
   fwd_amg_.reset();
@@ -85,6 +92,7 @@ Context::~Context() {
   mem_.release_all();
   if (h_st_) cudaFreeHost(h_st_);
   if (side_) cudaStreamDestroy(side_);
+  if (copy_) cudaStreamDestroy(copy_);
   if (stream_) cudaStreamDestroy(stream_);
 }
 
@@ -354,8 +362,20 @@ void Context::set_jacobian(const double* J, int64_t m, int64_t n_cells, double b
     dJ_ = jown_;
     ldj_ = ldh_;  // owned copy: padded rows like Ht
     j_borrowed_ = false;
-    GNW_CUDA_CHECK(cudaMemcpy2DAsync(dJ_, ldj_ * sizeof(double), J, Nl * sizeof(double), Nl * sizeof(double), m,
-                                     cudaMemcpyHostToDevice, s));
+    if (staged_src_ == J && staged_m_ == m && staged_n_ == Nl && staged_ld_ == ldj_) {
+      issue_stage();  // no-op unless no solve ran since the prefetch
+      // prefetch_jacobian already moved these bytes over PCIe beside the previous solve:
+      // one device copy (2 x 8 m N bytes of HBM traffic) instead of the host transfer
+      GNW_CUDA_CHECK(cudaStreamWaitEvent(s, stage_ev_[0], 0));
+      GNW_CUDA_CHECK(cudaMemcpyAsync(dJ_, jstage_, static_cast<size_t>(m) * ldj_ * sizeof(double),
+                                     cudaMemcpyDeviceToDevice, s));
+      GNW_CUDA_CHECK(cudaEventRecord(stage_ev_[1], s));  // the staging buffer is free again
+    } else {
+      GNW_CUDA_CHECK(cudaMemcpy2DAsync(dJ_, ldj_ * sizeof(double), J, Nl * sizeof(double), Nl * sizeof(double), m,
+                                       cudaMemcpyHostToDevice, s));
+    }
+    staged_src_ = nullptr;
+    stage_deferred_ = false;
   }
   op_.J = dJ_;
   op_.ldj = ldj_;
@@ -449,6 +469,50 @@ void Context::set_jacobian(const double* J, int64_t m, int64_t n_cells, double b
   pa_.Ht = dHt_;
   pa_.Cinv = dCinv_;
   pa_.Lc = dL_;
+}
+
+// Starts the host->device transfer of the NEXT step's Jacobian on the copy stream, into a
+// staging buffer, so it overlaps whatever the context runs meanwhile (the current step's
+// MINRES).  The next set_jacobian with the same host pointer and shape waits for it on the
+// device and takes the staged bytes; any other set_jacobian drops the stage.  The caller
+// keeps the host array unchanged until then (pinned memory gives the overlap; pageable
+// memory makes the copy synchronous, still correct).  Host-pointer mode only.
+void Context::prefetch_jacobian(const double* J, int64_t m, int64_t n_cells) {
+  require_mixed();
+  require_device();
+  if (ptr_mode == 1) throw std::invalid_argument("gnw_prefetch_jacobian: host-pointer mode only");
+  if (J == nullptr || m <= 0 || m > 8192) throw std::invalid_argument("gnw_prefetch_jacobian: bad J");
+  if (n_cells != local_n()) throw std::invalid_argument("gnw_prefetch_jacobian: J shape mismatch");
+  const long long Nl = local_n();
+  const long long ld = Nl + pad_;  // the owned copy's padded row stride (set_jacobian)
+  const size_t need = static_cast<size_t>(m) * ld;
+  if (!stage_mem_ || stage_cap_ < need) {
+    GNW_CUDA_CHECK(cudaStreamSynchronize(copy_));
+    sync();  // a pending consume of the old buffer
+    stage_mem_.reset();
+    stage_mem_ = std::make_unique<DeviceMemory>();
+    jstage_ = stage_mem_->alloc<double>(need);
+    stage_cap_ = need;
+    GNW_CUDA_CHECK(cudaEventRecord(stage_ev_[1], stream_));
+  }
+  staged_src_ = J;
+  staged_m_ = m;
+  staged_n_ = Nl;
+  staged_ld_ = ld;
+  stage_deferred_ = true;
+}
+
+// The staged copy is issued once the next MINRES has its own inputs on the device (or by
+// set_jacobian if no solve comes first): host->device copies share the copy engine, so a
+// 1 GB transfer queued ahead of minres's b / x0 uploads would hold the solve back.
+void Context::issue_stage() {
+  if (!stage_deferred_) return;
+  stage_deferred_ = false;
+  // the previous stage must have been consumed (device-side order, no host wait)
+  GNW_CUDA_CHECK(cudaStreamWaitEvent(copy_, stage_ev_[1], 0));
+  GNW_CUDA_CHECK(cudaMemcpy2DAsync(jstage_, staged_ld_ * sizeof(double), staged_src_, staged_n_ * sizeof(double),
+                                   staged_n_ * sizeof(double), staged_m_, cudaMemcpyHostToDevice, copy_));
+  GNW_CUDA_CHECK(cudaEventRecord(stage_ev_[0], copy_));
 }
 
 // --------------------------------------------------------------- operator
@@ -666,6 +730,7 @@ MinresResult Context::minres(const double* b, const double* x0, double* x, doubl
   operator_into(vfixed(x_), 0, vfixed(az_), st_plain_, 0);
   residual(n, b_, az_, r_, st_plain_, 1, rpart_, counters_ + 5, s);
   MinresState ps = read_plain();
+  issue_stage();  // b and x0 are on the device now: a prefetched J may take the copy engine
   const double bnorm = std::sqrt(ps.scratch[5]);
   auto finish = [&]() {
     GNW_CUDA_CHECK(cudaEventRecord(e1, s));

@@ -75,6 +75,8 @@ class Context {
   void assemble_amg_csr(int64_t n, const int64_t* rowptr, const int64_t* cols, const double* vals,
                         const host::AmgOptions& o);
   void set_jacobian(const double* J, int64_t m, int64_t n_cells, double beta, double timings[3]);
+  // async H2D of the next step's J beside the current solve (host-pointer mode)
+  void prefetch_jacobian(const double* J, int64_t m, int64_t n_cells);
   void apply_operator(const double* x, double* y);
   void precondition(const double* y, double* z);
   void amg_apply(const double* r, double* z);
@@ -119,7 +121,7 @@ class Context {
   int64_t m() const { return m_; }
   double beta() const { return beta_; }
   size_t device_bytes() const {
-    return mem_.bytes + (jmem_ ? jmem_->bytes : 0) + damg_.bytes() + fwd_amg_.bytes() + (emem_ ? emem_->bytes : 0);
+    return mem_.bytes + (jmem_ ? jmem_->bytes : 0) + (stage_mem_ ? stage_mem_->bytes : 0) + damg_.bytes() + fwd_amg_.bytes() + (emem_ ? emem_->bytes : 0);
   }
 
   double t_minres = 0.0, t_rhs = 0.0;
@@ -203,6 +205,16 @@ class Context {
   int64_t jm_m_ = -1;          // shape of the persistent Jacobian buffers
   bool jm_owned_ = false;
   double* jown_ = nullptr;     // owned copy of J (host-pointer mode)
+  cudaStream_t copy_ = nullptr;            // prefetch_jacobian's host->device stream
+  cudaEvent_t stage_ev_[2] = {};           // [0] staged bytes landed, [1] staging buffer consumed
+  std::unique_ptr<DeviceMemory> stage_mem_;
+  double* jstage_ = nullptr;
+  size_t stage_cap_ = 0;
+  const double* staged_src_ = nullptr;     // host J of the pending stage (nullptr: none)
+  int64_t staged_m_ = -1;
+  long long staged_n_ = -1, staged_ld_ = -1;
+  bool stage_deferred_ = false;            // requested, not yet issued (issue_stage)
+  void issue_stage();
   double* dpart_ = nullptr;    // DGEMM split-K partials
   double* dnib_ = nullptr;     // device scalar -1/beta
   double* dq_ = nullptr;       // q = J^T t' (fused loop), N

@@ -157,6 +157,10 @@ gnw_status gnw_get_info(const gnw_ctx* ctx, gnw_info* info) {
   });
 }
 
+gnw_status gnw_prefetch_jacobian(gnw_ctx* ctx, const double* J, uint64_t m, uint64_t n_cells) {
+  return guard([&] { ctx_of(ctx).prefetch_jacobian(J, static_cast<int64_t>(m), static_cast<int64_t>(n_cells)); });
+}
+
 gnw_status gnw_set_jacobian(gnw_ctx* ctx, const double* J, uint64_t m, uint64_t n_cells, double beta,
                             gnw_timings* timings) {
   return guard([&] {

@@ -232,22 +232,22 @@ __global__ void k_coarse_cholesky(const double* __restrict__ L, int n, VSel rs, 
 void note_launch(const char* what) { check_launch(what); }
 
 void vc_down(const DLevel& L, VSel r, double* resid, const MinresState* st, cudaStream_t s) {
-  if (L.wideA) return vcw_down(L, r, resid, st, s);
+  if (L.gA > 1) return vcg_down(L, r, resid, st, s);
   GNW_LAUNCH(launch_k(k_vc_down, grid_for(L.n), kTpb, 0, s, L.A, L.wd, r, resid, st));
   check_launch("vc_down");
 }
 void vc_restrict(const DLevel& L, const double* resid, double* rc, cudaStream_t s) {
-  if (L.wideR) return vcw_restrict(L, resid, rc, s);
+  if (L.gR > 1) return vcg_restrict(L, resid, rc, s);
   GNW_LAUNCH(launch_k(k_vc_restrict, grid_for(L.R.n_rows), kTpb, 0, s, L.R, resid, rc));
   check_launch("vc_restrict");
 }
 void vc_up1(const DLevel& L, VSel r, const double* ec, double* x, const MinresState* st, cudaStream_t s) {
-  if (L.wideP) return vcw_up1(L, r, ec, x, st, s);
+  if (L.gP > 1) return vcg_up1(L, r, ec, x, st, s);
   GNW_LAUNCH(launch_k(k_vc_up1, grid_for(L.n), kTpb, 0, s, L.P, L.wd, r, ec, x, st));
   check_launch("vc_up1");
 }
 void vc_up2(const DLevel& L, VSel r, const double* x, double* out, const MinresState* st, cudaStream_t s) {
-  if (L.wideA) return vcw_up2(L, r, x, out, st, s);
+  if (L.gA > 1) return vcg_up2(L, r, x, out, st, s);
   GNW_LAUNCH(launch_k(k_vc_up2, grid_for(L.n), kTpb, 0, s, L.A, L.wd, r, x, out, st));
   check_launch("vc_up2");
 }

@@ -15,8 +15,11 @@ struct DLevel {
   DCsr A, P, R;
   double* wd = nullptr;  // omega * inv_diag (rounded exactly as amg.cpp:98)
   int n = 0;             // rows of A
-  // warp-per-row kernels (vcycle_wide.cu) for matrices with many entries per row
+  // warp-per-row flags of the fused cluster tail (vcycle_tail.cu)
   int wideA = 0, wideP = 0, wideR = 0;
+  // lanes per row of the single-RHS kernels (vcycle_wide.cu): 1 = thread-per-row in the
+  // reference order (kernels.cu), 2..32 = a G-lane group per row
+  int gA = 1, gP = 1, gR = 1;
 };
 
 // Fused coarse tail of the single-RHS V-cycle (vcycle_tail.cu): levels l0..L-1
@@ -41,11 +44,13 @@ struct TailArgs {
 };
 void vcycle_tail(const TailArgs& a, VSel rin, double* out, const MinresState* st, int cluster, cudaStream_t s);
 
-// wide-level kernels (vcycle_wide.cu)
-void vcw_down(const DLevel& L, VSel r, double* resid, const MinresState* st, cudaStream_t s);
-void vcw_restrict(const DLevel& L, const double* resid, double* rc, cudaStream_t s);
-void vcw_up1(const DLevel& L, VSel r, const double* ec, double* x, const MinresState* st, cudaStream_t s);
-void vcw_up2(const DLevel& L, VSel r, const double* x, double* out, const MinresState* st, cudaStream_t s);
+// G-lanes-per-row kernels (vcycle_wide.cu), G = DLevel::gA / gR / gP
+void vcg_down(const DLevel& L, VSel r, double* resid, const MinresState* st, cudaStream_t s);
+void vcg_restrict(const DLevel& L, const double* resid, double* rc, cudaStream_t s);
+void vcg_up1(const DLevel& L, VSel r, const double* ec, double* x, const MinresState* st, cudaStream_t s);
+void vcg_up2(const DLevel& L, VSel r, const double* x, double* out, const MinresState* st, cudaStream_t s);
+// lanes per row for a matrix with `nnz` entries over `rows` rows (env GNW_VC_T tunes it)
+int vc_group_lanes(long long nnz, long long rows);
 
 // narrow-level batched kernels, 2 columns per thread (vcycle_batch.cu); even b only
 void mvc2_down(const DLevel& L, const double* r, int ldr, double* resid, int b, cudaStream_t s);

@@ -1,19 +1,22 @@
-// vcycle_wide.cu -- V-cycle kernels for WIDE levels (many nonzeros per row).
+// vcycle_wide.cu -- V-cycle kernels for levels with several nonzeros per row.
 //
 // Thread-per-row CSR (kernels.cu) reproduces the reference's sequential row sums
-// bit for bit, but on the coarse SA-AMG levels rows hold 25..400 entries and
-// only a few hundred rows exist (C2: 5541 x 72, 1147 x 150, then 396..171 dense
-// rows), so one thread walking a row serialises hundreds of dependent loads.
-// Here a warp owns a row: lane l accumulates the entries k = start + l,
-// start + l + 32, ... in order, then the lanes combine through the xor
-// butterfly (16, 8, 4, 2, 1).  That order is deterministic but not the
-// reference's; GNW_COARSE_CHOLESKY ("exact") mode never uses these kernels.
+// bit for bit, but a thread walking a row of 10..400 entries serialises its
+// dependent loads and its loads are strided across the warp (C3, ncu cold-cache:
+// level 1 of the hierarchy, 13 entries per row, ran at 3.9 TB/s; warp-per-row on
+// level 2, 26 per row, at 1.5 TB/s because 6 of 32 lanes idled and every warp
+// carried a whole row's latency chain for 26 entries).  Here a group of G lanes
+// (G = 2..32, picked per matrix from its mean row length, DLevel::gA/gP/gR) owns
+// a row: lane j accumulates the entries k = start + j, start + j + G, ... in
+// order, then the group combines through the xor butterfly (G/2, ..., 1).
+// That order is deterministic but not the reference's; GNW_COARSE_CHOLESKY
+// ("exact") mode never uses these kernels.
 //
 // The multi-RHS kernels (H = S^-1 J^T, b interleaved columns) run one thread per
-// (row, column) and EMULATE the same lane partition and butterfly with 32
-// register partials, so every column of a batched V-cycle is bit-identical to
-// the single-RHS V-cycle of the MINRES loop.
+// (row, column) in the reference's sequential order (kernels.cu, vcycle_batch.cu).
 #include <cuda_runtime.h>
+
+#include <cstdlib>
 
 #include "kernels.cuh"
 
@@ -23,64 +26,80 @@ void note_launch(const char* what);
 
 namespace {
 
-template <class F>
-__device__ __forceinline__ double warp_row(const DCsr& A, int i, int lane, F f) {
+// G lanes own a row (G = 2..32, a power of two): lane j of the group accumulates the entries
+// k = start + j, start + j + G, ... in order, then the group combines through the xor
+// butterfly (G/2, ..., 1).  G = 32 is the warp-per-row order.  Rows outside the matrix
+// still join the shuffles (full mask) with a zero partial.
+template <int G, class F>
+__device__ __forceinline__ double group_row(const DCsr& A, int i, int sub, bool valid, F f) {
   double acc = 0.0;
-  const int k1 = A.rowptr[i + 1];
-  // unrolled so several (index -> value) load chains are in flight per lane
+  if (valid) {
+    const int k1 = A.rowptr[i + 1];
+    // unrolled so several (index -> value) load chains are in flight per lane
 #pragma unroll 4
-  for (int k = A.rowptr[i] + lane; k < k1; k += 32) acc = acc + __ldg(&A.vals[k]) * f(__ldg(&A.cols[k]));
-  double v[1] = {acc};
-  warp_reduce<1>(v);
-  return v[0];
+    for (int k = A.rowptr[i] + sub; k < k1; k += G) acc = acc + __ldg(&A.vals[k]) * f(__ldg(&A.cols[k]));
+  }
+#pragma unroll
+  for (int o = G / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  return acc;
 }
 
-constexpr int kRowsPerBlock = 8;  // 8 warps, one row each
+constexpr int kGroupTpb = 256;
+
+template <int G>
+struct GroupIdx {
+  int i, sub;
+  __device__ GroupIdx() : i(blockIdx.x * (kGroupTpb / G) + threadIdx.x / G), sub(threadIdx.x % G) {}
+};
 
 }  // namespace
 
 // --------------------------------------------------------------- single RHS
-__global__ void __launch_bounds__(256) k_vcw_down(DCsr A, const double* __restrict__ wd, VSel rs,
-                                                  double* __restrict__ resid, const MinresState* st) {
+template <int G>
+__global__ void __launch_bounds__(kGroupTpb) k_vcg_down(DCsr A, const double* __restrict__ wd, VSel rs,
+                                                        double* __restrict__ resid, const MinresState* st) {
   griddep_wait();
   const double* __restrict__ r = vsel(rs, st);
-  const int i = blockIdx.x * kRowsPerBlock + (threadIdx.x >> 5), lane = threadIdx.x & 31;
-  if (i >= A.n_rows) return;
-  const double s = warp_row(A, i, lane, [&](int c) { return __ldg(&wd[c]) * r[c]; });
-  if (lane == 0) resid[i] = r[i] + (-1.0 * s);
+  const GroupIdx<G> g;
+  const bool ok = g.i < A.n_rows;
+  const double s = group_row<G>(A, g.i, g.sub, ok, [&](int c) { return __ldg(&wd[c]) * r[c]; });
+  if (ok && g.sub == 0) resid[g.i] = r[g.i] + (-1.0 * s);
 }
 
-__global__ void __launch_bounds__(256) k_vcw_restrict(DCsr R, const double* __restrict__ resid,
-                                                      double* __restrict__ rc) {
+template <int G>
+__global__ void __launch_bounds__(kGroupTpb) k_vcg_restrict(DCsr R, const double* __restrict__ resid,
+                                                            double* __restrict__ rc) {
   griddep_wait();
-  const int a = blockIdx.x * kRowsPerBlock + (threadIdx.x >> 5), lane = threadIdx.x & 31;
-  if (a >= R.n_rows) return;
-  const double s = warp_row(R, a, lane, [&](int c) { return resid[c]; });
-  if (lane == 0) rc[a] = s;
+  const GroupIdx<G> g;
+  const bool ok = g.i < R.n_rows;
+  const double s = group_row<G>(R, g.i, g.sub, ok, [&](int c) { return resid[c]; });
+  if (ok && g.sub == 0) rc[g.i] = s;
 }
 
-__global__ void __launch_bounds__(256) k_vcw_up1(DCsr P, const double* __restrict__ wd, VSel rs,
-                                                 const double* __restrict__ ec, double* __restrict__ x,
-                                                 const MinresState* st) {
-  griddep_wait();
-  const double* __restrict__ r = vsel(rs, st);
-  const int i = blockIdx.x * kRowsPerBlock + (threadIdx.x >> 5), lane = threadIdx.x & 31;
-  if (i >= P.n_rows) return;
-  const double s = warp_row(P, i, lane, [&](int c) { return ec[c]; });
-  if (lane == 0) x[i] = __ldg(&wd[i]) * r[i] + 1.0 * s;
-}
-
-__global__ void __launch_bounds__(256) k_vcw_up2(DCsr A, const double* __restrict__ wd, VSel rs,
-                                                 const double* __restrict__ x, double* __restrict__ out,
-                                                 const MinresState* st) {
+template <int G>
+__global__ void __launch_bounds__(kGroupTpb) k_vcg_up1(DCsr P, const double* __restrict__ wd, VSel rs,
+                                                       const double* __restrict__ ec, double* __restrict__ x,
+                                                       const MinresState* st) {
   griddep_wait();
   const double* __restrict__ r = vsel(rs, st);
-  const int i = blockIdx.x * kRowsPerBlock + (threadIdx.x >> 5), lane = threadIdx.x & 31;
-  if (i >= A.n_rows) return;
-  const double s = warp_row(A, i, lane, [&](int c) { return x[c]; });
-  if (lane == 0) {
-    const double res = r[i] + (-1.0 * s);
-    out[i] = x[i] + __ldg(&wd[i]) * res;
+  const GroupIdx<G> g;
+  const bool ok = g.i < P.n_rows;
+  const double s = group_row<G>(P, g.i, g.sub, ok, [&](int c) { return ec[c]; });
+  if (ok && g.sub == 0) x[g.i] = __ldg(&wd[g.i]) * r[g.i] + 1.0 * s;
+}
+
+template <int G>
+__global__ void __launch_bounds__(kGroupTpb) k_vcg_up2(DCsr A, const double* __restrict__ wd, VSel rs,
+                                                       const double* __restrict__ x, double* __restrict__ out,
+                                                       const MinresState* st) {
+  griddep_wait();
+  const double* __restrict__ r = vsel(rs, st);
+  const GroupIdx<G> g;
+  const bool ok = g.i < A.n_rows;
+  const double s = group_row<G>(A, g.i, g.sub, ok, [&](int c) { return x[c]; });
+  if (ok && g.sub == 0) {
+    const double res = r[g.i] + (-1.0 * s);
+    out[g.i] = x[g.i] + __ldg(&wd[g.i]) * res;
   }
 }
 
@@ -118,23 +137,51 @@ __global__ void k_transpose_square(const double* __restrict__ A, double* __restr
 }
 
 // ------------------------------------------------------------------ launchers
-static unsigned wgrid(int rows) { return static_cast<unsigned>((rows + kRowsPerBlock - 1) / kRowsPerBlock); }
+// G = the largest power of two <= (mean entries per row) / T, in [1, 32]; T = 4 by default
+// (C3 hierarchy: 4 -> 1, 10 -> 2, 13 -> 2, 26 -> 4, 72 -> 16, 150+ -> 32; standalone V-cycle
+// T = 2 / 3 / 4 / 6: C3 0.951 / 0.906 / 0.856 / 0.872 ms, C5 0.294 / 0.287 / 0.285 / 0.300 ms,
+// C2 0.105 / 0.108 / 0.109 / 0.118 ms; warp-per-row on every level >= 24 per row: 1.04 / 0.40 / 0.12).
+int vc_group_lanes(long long nnz, long long rows) {
+  static const double T = [] {
+    const char* e = std::getenv("GNW_VC_T");
+    return e ? std::atof(e) : 4.0;
+  }();
+  if (rows <= 0) return 1;
+  const double per = static_cast<double>(nnz) / static_cast<double>(rows) / T;
+  int g = 1;
+  while (g < 32 && 2 * g <= per) g *= 2;
+  return g;
+}
 
-void vcw_down(const DLevel& L, VSel r, double* resid, const MinresState* st, cudaStream_t s) {
-  GNW_LAUNCH(launch_k(k_vcw_down, wgrid(L.n), 256, 0, s, L.A, L.wd, r, resid, st));
-  note_launch("vcw_down");
+static unsigned ggrid(int rows, int G) {
+  const int per = kGroupTpb / G;
+  return static_cast<unsigned>((rows + per - 1) / per);
 }
-void vcw_restrict(const DLevel& L, const double* resid, double* rc, cudaStream_t s) {
-  GNW_LAUNCH(launch_k(k_vcw_restrict, wgrid(L.R.n_rows), 256, 0, s, L.R, resid, rc));
-  note_launch("vcw_restrict");
+
+#define GNW_G_DISPATCH(G, KERNEL, ROWS, ...)                                                         \
+  switch (G) {                                                                                       \
+    case 2: GNW_LAUNCH(launch_k(KERNEL<2>, ggrid(ROWS, 2), kGroupTpb, 0, __VA_ARGS__)); break;     \
+    case 4: GNW_LAUNCH(launch_k(KERNEL<4>, ggrid(ROWS, 4), kGroupTpb, 0, __VA_ARGS__)); break;     \
+    case 8: GNW_LAUNCH(launch_k(KERNEL<8>, ggrid(ROWS, 8), kGroupTpb, 0, __VA_ARGS__)); break;     \
+    case 16: GNW_LAUNCH(launch_k(KERNEL<16>, ggrid(ROWS, 16), kGroupTpb, 0, __VA_ARGS__)); break;  \
+    default: GNW_LAUNCH(launch_k(KERNEL<32>, ggrid(ROWS, 32), kGroupTpb, 0, __VA_ARGS__)); break;  \
+  }
+
+void vcg_down(const DLevel& L, VSel r, double* resid, const MinresState* st, cudaStream_t s) {
+  GNW_G_DISPATCH(L.gA, k_vcg_down, L.n, s, L.A, L.wd, r, resid, st);
+  note_launch("vcg_down");
 }
-void vcw_up1(const DLevel& L, VSel r, const double* ec, double* x, const MinresState* st, cudaStream_t s) {
-  GNW_LAUNCH(launch_k(k_vcw_up1, wgrid(L.n), 256, 0, s, L.P, L.wd, r, ec, x, st));
-  note_launch("vcw_up1");
+void vcg_restrict(const DLevel& L, const double* resid, double* rc, cudaStream_t s) {
+  GNW_G_DISPATCH(L.gR, k_vcg_restrict, L.R.n_rows, s, L.R, resid, rc);
+  note_launch("vcg_restrict");
 }
-void vcw_up2(const DLevel& L, VSel r, const double* x, double* out, const MinresState* st, cudaStream_t s) {
-  GNW_LAUNCH(launch_k(k_vcw_up2, wgrid(L.n), 256, 0, s, L.A, L.wd, r, x, out, st));
-  note_launch("vcw_up2");
+void vcg_up1(const DLevel& L, VSel r, const double* ec, double* x, const MinresState* st, cudaStream_t s) {
+  GNW_G_DISPATCH(L.gP, k_vcg_up1, L.n, s, L.P, L.wd, r, ec, x, st);
+  note_launch("vcg_up1");
+}
+void vcg_up2(const DLevel& L, VSel r, const double* x, double* out, const MinresState* st, cudaStream_t s) {
+  GNW_G_DISPATCH(L.gA, k_vcg_up2, L.n, s, L.A, L.wd, r, x, out, st);
+  note_launch("vcg_up2");
 }
 void dense_seq_batch(const double* M, int n, const double* X, double* Y, int b, cudaStream_t s) {
   dim3 grid((n + 7) / 8, (b + 31) / 32), block(32, 8);

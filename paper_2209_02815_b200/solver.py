@@ -166,6 +166,17 @@ class Context:
         self.beta = beta
         return {"t_H": t.t_H, "t_C": t.t_C, "t_chol": t.t_chol}
 
+    def prefetch_jacobian(self, J) -> None:
+        """Start the host->device copy of the NEXT step's J beside the current solve
+        (host-pointer mode; pinned J overlaps).  The next set_jacobian(J, ...) with the same
+        array takes the staged copy.  J must not change in between."""
+        if self.device_pointers:
+            raise ValueError("gnw_prefetch_jacobian: host-pointer mode only")
+        if not (isinstance(J, np.ndarray) and J.dtype == np.float64 and J.flags.c_contiguous):
+            raise ValueError("gnw_prefetch_jacobian: J must be a C-contiguous float64 array (it is read later)")
+        m, n = J.shape
+        A.check(self.L.gnw_prefetch_jacobian(self.h, _dptr(J), m, n))
+
     # ----------------------------------------------------------------- applies
     def _out(self, n, like=None):
         if self.device_pointers:
@@ -197,15 +208,24 @@ class Context:
         A.check(self.L.gnw_amg_apply(self.h, _dptr(r), _dptr(z)))
         return z
 
-    def assemble_rhs(self, m, m_ref, g, g_obs):
-        """assemble_gn_rhs (inversion.cpp:126-146)."""
+    def _check_out(self, out, n):
+        if self.device_pointers or not (isinstance(out, np.ndarray) and out.dtype == np.float64
+                                        and out.flags.c_contiguous and out.shape == (n,)):
+            raise ValueError("out must be a C-contiguous float64 host array of the result's length")
+        return out
+
+    def assemble_rhs(self, m, m_ref, g, g_obs, out=None):
+        """assemble_gn_rhs (inversion.cpp:126-146).  ``out``: optional host array (e.g. pinned)
+        that receives the rhs."""
         m, m_ref, g, g_obs = (self._in(a) for a in (m, m_ref, g, g_obs))
-        out = self._out(self.K + self.N, m)
+        out = self._out(self.K + self.N, m) if out is None else self._check_out(out, self.K + self.N)
         A.check(self.L.gnw_assemble_rhs(self.h, _dptr(m), _dptr(m_ref), _dptr(g), _dptr(g_obs), _dptr(out)))
         return out
 
-    def minres(self, b, x0=None, tol: float = 1e-8, maxit: int | None = None, hist_cap: int = 1 << 16):
-        """minres(op.apply, pc.apply, b, x0, tol, maxit) (minres.cpp:20-155)."""
+    def minres(self, b, x0=None, tol: float = 1e-8, maxit: int | None = None, hist_cap: int = 1 << 16,
+               out=None):
+        """minres(op.apply, pc.apply, b, x0, tol, maxit) (minres.cpp:20-155).  ``out``: optional
+        host array (e.g. pinned) that receives x."""
         n = self.K + self.N
         b = self._in(b)
         if x0 is None:
@@ -215,7 +235,7 @@ class Context:
         else:
             x0 = self._in(x0)
         maxit = 2 * n if maxit is None else int(maxit)
-        x = self._out(n, b)
+        x = self._out(n, b) if out is None else self._check_out(out, n)
         he = np.zeros(hist_cap)
         hp = np.zeros(hist_cap)
         rep = A.Report(0, 0, 0.0, 0, he.ctypes.data, hp.ctypes.data, hist_cap)

@@ -235,3 +235,31 @@ def test_amg_csr_poisson(oracle, gpu_ctx_factory):
     prob = orc.Problem.amg_csr(oracle, rowptr, cols, vals, orc.AmgOpts.make(coarse_threshold=16))
     r = W.gaussian(11, n * n)
     assert np.array_equal(ctx.amg_apply(r), prob.amg_apply(r))
+
+
+def test_prefetch_jacobian_same_bits(c1, gpu_ctx_factory):
+    """gnw_prefetch_jacobian: a staged J gives bit-identical Woodbury factors and solves; a
+    different array (or a changed shape) drops the stage instead of using stale bytes."""
+    mesh, inp, prob = c1[64]
+    ctx = gpu_ctx_factory(mesh)
+    J = np.ascontiguousarray(inp.J)
+    b = prob.assemble_rhs(inp.dm, np.zeros(prob.N), inp.dg, np.zeros(J.shape[0]))
+    ctx.set_jacobian(J, 1e-2)
+    H0, L0 = ctx.woodbury_factors()
+    x0, r0 = ctx.minres(b, tol=1e-10)
+    ctx.prefetch_jacobian(J)
+    ctx.set_jacobian(J, 1e-2)
+    H1, L1 = ctx.woodbury_factors()
+    x1, r1 = ctx.minres(b, tol=1e-10)
+    assert np.array_equal(H0, H1) and np.array_equal(L0, L1)
+    assert r0.iterations == r1.iterations and np.array_equal(x0, x1)
+    # stage J, then set a different Jacobian: the stage is not used
+    J2 = np.ascontiguousarray(2.0 * J)
+    ctx.prefetch_jacobian(J)
+    ctx.set_jacobian(J2, 1e-2)
+    H2, _ = ctx.woodbury_factors()
+    ctx.set_jacobian(J2, 1e-2)
+    H3, _ = ctx.woodbury_factors()
+    assert np.array_equal(H2, H3) and np.array_equal(H2, 2.0 * H0)
+    with pytest.raises(ValueError, match="shape mismatch"):
+        ctx.prefetch_jacobian(np.ascontiguousarray(J[:, :-2]))
