@@ -12,7 +12,9 @@
 //   k_chol_panel  : columns [p, p+w) of the rows i >= p.  One thread per row holds
 //                   the row's w panel entries in registers; each CTA also carries the
 //                   32 diagonal-block rows (redundantly), whose column k is published
-//                   through shared memory once per step.
+//                   through shared memory once per step.  (A variant that factored the
+//                   diagonal block in warp 0 first, fully unrolled, ran 2x slower: its
+//                   17k-instruction body stalled on instruction fetch.)
 //   k_chol_update : W[i][j] -= L[i][k] L[j][k], k = p .. p+w-1 in order, for the
 //                   trailing lower triangle (32 x 32 tiles, panel columns in smem).
 #include <cuda_runtime.h>
@@ -157,9 +159,8 @@ void cholesky_blocked(const double* C, double* W, double* L, int n, int* fail, c
 __global__ void __launch_bounds__(1024) k_trinv_block(const double* __restrict__ L, double* __restrict__ Y, int n,
                                                       int p) {
   griddep_wait();
-  __shared__ double yr[32][33];
-  const int r = threadIdx.y;               // row within block
-  const int jc = threadIdx.x;              // column within chunk
+  const int r = threadIdx.x;               // row within block (a warp holds one column's 32 rows)
+  const int jc = threadIdx.y;              // column within chunk
   const int i = p + r;
   const int j = blockIdx.x * 32 + jc;      // global column
   const bool act = i < n && j <= i;
@@ -172,22 +173,28 @@ __global__ void __launch_bounds__(1024) k_trinv_block(const double* __restrict__
   double s = (act && i == j) ? 1.0 : 0.0;
   for (int k0 = blockIdx.x * 32; k0 < p; k0 += 32) {
     const int kk = min(32, p - k0);
-    Ls[r][jc] = (i < n && jc < kk) ? __ldg(&L[static_cast<long long>(i) * n + k0 + jc]) : 0.0;
-    Ys[r][jc] = (r < kk && j < n) ? __ldg(&Y[static_cast<long long>(k0 + r) * n + j]) : 0.0;
+    Ls[jc][r] = (p + jc < n && r < kk) ? __ldg(&L[static_cast<long long>(p + jc) * n + k0 + r]) : 0.0;
+    Ys[jc][r] = (jc < kk && blockIdx.x * 32 + r < n) ? __ldg(&Y[static_cast<long long>(k0 + jc) * n + blockIdx.x * 32 + r]) : 0.0;
     __syncthreads();
     if (act)
       for (int t = 0; t < kk; ++t) s = s - Ls[r][t] * Ys[t][jc];
     __syncthreads();
   }
+  // the 32 x 32 diagonal block, row by row: within a column only the warp's own lanes
+  // interact, so the quotient of row rr reaches the rows below by shuffle (no CTA barrier)
   const int w = min(32, n - p);
+  // the diagonal block L[p + r][p + rr] staged once (the per-step load of L[i][p + rr] was
+  // 32 lines per warp instruction in this column-per-warp layout)
+  Ls[jc][r] = (p + jc < n && r < w) ? L[static_cast<long long>(p + jc) * n + p + r] : 1.0;
+  __syncthreads();
   for (int rr = 0; rr < w; ++rr) {
+    double y = 0.0;
     if (r == rr) {
-      const double y = act ? s / L[static_cast<long long>(i) * n + i] : 0.0;
-      yr[rr][jc] = y;
+      y = act ? s / Ls[r][r] : 0.0;
       if (i < n && j < n) Y[static_cast<long long>(i) * n + j] = act ? y : 0.0;
     }
-    __syncthreads();
-    if (r > rr && act && j <= p + rr) s = s - L[static_cast<long long>(i) * n + p + rr] * yr[rr][jc];
+    y = __shfl_sync(0xffffffffu, y, rr);
+    if (r > rr && act && j <= p + rr) s = s - Ls[r][rr] * y;
   }
 }
 

@@ -9,6 +9,9 @@
 // of several entries are in flight together (level 0 carries 4-5 entries per row).
 #include <cuda_runtime.h>
 
+#include <algorithm>
+#include <cstdlib>
+
 #include "kernels.cuh"
 
 namespace gnw {
@@ -20,110 +23,168 @@ __device__ __forceinline__ double2 ld2(const double* p) { return *reinterpret_ca
 __device__ __forceinline__ void st2(double* p, double2 v) { *reinterpret_cast<double2*>(p) = v; }
 }  // namespace
 
+// V double2 vectors (2V consecutive columns) per thread.  V = 2 doubles the bytes each
+// thread has in flight behind one (row pointer -> column index -> gather) latency chain:
+// the level-0 kernels were long-scoreboard bound at 3.4 TB/s with V = 1 (C2, ncu).
+template <int V>
 __global__ void __launch_bounds__(256) k_mvc2_down(DCsr A, const double* __restrict__ wd,
                                                    const double* __restrict__ r, int ldr,
                                                    double* __restrict__ resid, int b) {
   griddep_wait();
   const int i = blockIdx.x * 8 + threadIdx.y;
-  const int q = 2 * (blockIdx.y * 32 + threadIdx.x);
+  const int q = 2 * V * (blockIdx.y * 32 + threadIdx.x);
   if (i >= A.n_rows || q >= b) return;
-  double sx = 0.0, sy = 0.0;
+  double sx[V], sy[V];
+#pragma unroll
+  for (int v = 0; v < V; ++v) sx[v] = sy[v] = 0.0;
   const int k0 = A.rowptr[i], k1 = A.rowptr[i + 1];
 #pragma unroll 4
   for (int k = k0; k < k1; ++k) {
     const int c = __ldg(&A.cols[k]);
     const double a = __ldg(&A.vals[k]), w = __ldg(&wd[c]);
-    const double2 x = ld2(r + static_cast<long long>(c) * ldr + q);
-    sx = sx + a * (w * x.x);
-    sy = sy + a * (w * x.y);
+#pragma unroll
+    for (int v = 0; v < V; ++v) {
+      const double2 x = ld2(r + static_cast<long long>(c) * ldr + q + 2 * v);
+      sx[v] = sx[v] + a * (w * x.x);
+      sy[v] = sy[v] + a * (w * x.y);
+    }
   }
-  const double2 ri = ld2(r + static_cast<long long>(i) * ldr + q);
-  st2(resid + static_cast<long long>(i) * b + q, make_double2(ri.x + (-1.0 * sx), ri.y + (-1.0 * sy)));
+#pragma unroll
+  for (int v = 0; v < V; ++v) {
+    const double2 ri = ld2(r + static_cast<long long>(i) * ldr + q + 2 * v);
+    st2(resid + static_cast<long long>(i) * b + q + 2 * v, make_double2(ri.x + (-1.0 * sx[v]), ri.y + (-1.0 * sy[v])));
+  }
 }
 
+template <int V>
 __global__ void __launch_bounds__(256) k_mvc2_restrict(DCsr R, const double* __restrict__ resid,
                                                        double* __restrict__ rc, int b) {
   griddep_wait();
   const int a = blockIdx.x * 8 + threadIdx.y;
-  const int q = 2 * (blockIdx.y * 32 + threadIdx.x);
+  const int q = 2 * V * (blockIdx.y * 32 + threadIdx.x);
   if (a >= R.n_rows || q >= b) return;
-  double sx = 0.0, sy = 0.0;
+  double sx[V], sy[V];
+#pragma unroll
+  for (int v = 0; v < V; ++v) sx[v] = sy[v] = 0.0;
   const int k0 = R.rowptr[a], k1 = R.rowptr[a + 1];
 #pragma unroll 4
   for (int k = k0; k < k1; ++k) {
     const int c = __ldg(&R.cols[k]);
-    const double v = __ldg(&R.vals[k]);
-    const double2 x = ld2(resid + static_cast<long long>(c) * b + q);
-    sx = sx + v * x.x;
-    sy = sy + v * x.y;
+    const double val = __ldg(&R.vals[k]);
+#pragma unroll
+    for (int v = 0; v < V; ++v) {
+      const double2 x = ld2(resid + static_cast<long long>(c) * b + q + 2 * v);
+      sx[v] = sx[v] + val * x.x;
+      sy[v] = sy[v] + val * x.y;
+    }
   }
-  st2(rc + static_cast<long long>(a) * b + q, make_double2(sx, sy));
+#pragma unroll
+  for (int v = 0; v < V; ++v) st2(rc + static_cast<long long>(a) * b + q + 2 * v, make_double2(sx[v], sy[v]));
 }
 
+template <int V>
 __global__ void __launch_bounds__(256) k_mvc2_up1(DCsr P, const double* __restrict__ wd,
                                                   const double* __restrict__ r, int ldr,
                                                   const double* __restrict__ ec, double* __restrict__ x, int b) {
   griddep_wait();
   const int i = blockIdx.x * 8 + threadIdx.y;
-  const int q = 2 * (blockIdx.y * 32 + threadIdx.x);
+  const int q = 2 * V * (blockIdx.y * 32 + threadIdx.x);
   if (i >= P.n_rows || q >= b) return;
-  double sx = 0.0, sy = 0.0;
+  double sx[V], sy[V];
+#pragma unroll
+  for (int v = 0; v < V; ++v) sx[v] = sy[v] = 0.0;
   const int k0 = P.rowptr[i], k1 = P.rowptr[i + 1];
 #pragma unroll 4
   for (int k = k0; k < k1; ++k) {
     const int c = __ldg(&P.cols[k]);
-    const double v = __ldg(&P.vals[k]);
-    const double2 e = ld2(ec + static_cast<long long>(c) * b + q);
-    sx = sx + v * e.x;
-    sy = sy + v * e.y;
+    const double val = __ldg(&P.vals[k]);
+#pragma unroll
+    for (int v = 0; v < V; ++v) {
+      const double2 e = ld2(ec + static_cast<long long>(c) * b + q + 2 * v);
+      sx[v] = sx[v] + val * e.x;
+      sy[v] = sy[v] + val * e.y;
+    }
   }
   const double w = __ldg(&wd[i]);
-  const double2 ri = ld2(r + static_cast<long long>(i) * ldr + q);
-  st2(x + static_cast<long long>(i) * b + q, make_double2(w * ri.x + 1.0 * sx, w * ri.y + 1.0 * sy));
+#pragma unroll
+  for (int v = 0; v < V; ++v) {
+    const double2 ri = ld2(r + static_cast<long long>(i) * ldr + q + 2 * v);
+    st2(x + static_cast<long long>(i) * b + q + 2 * v, make_double2(w * ri.x + 1.0 * sx[v], w * ri.y + 1.0 * sy[v]));
+  }
 }
 
+template <int V>
 __global__ void __launch_bounds__(256) k_mvc2_up2(DCsr A, const double* __restrict__ wd,
                                                   const double* __restrict__ r, int ldr,
                                                   const double* __restrict__ x, double* __restrict__ out,
                                                   int ldo, int b) {
   griddep_wait();
   const int i = blockIdx.x * 8 + threadIdx.y;
-  const int q = 2 * (blockIdx.y * 32 + threadIdx.x);
+  const int q = 2 * V * (blockIdx.y * 32 + threadIdx.x);
   if (i >= A.n_rows || q >= b) return;
-  double sx = 0.0, sy = 0.0;
+  double sx[V], sy[V];
+#pragma unroll
+  for (int v = 0; v < V; ++v) sx[v] = sy[v] = 0.0;
   const int k0 = A.rowptr[i], k1 = A.rowptr[i + 1];
 #pragma unroll 4
   for (int k = k0; k < k1; ++k) {
     const int c = __ldg(&A.cols[k]);
     const double a = __ldg(&A.vals[k]);
-    const double2 xv = ld2(x + static_cast<long long>(c) * b + q);
-    sx = sx + a * xv.x;
-    sy = sy + a * xv.y;
+#pragma unroll
+    for (int v = 0; v < V; ++v) {
+      const double2 xv = ld2(x + static_cast<long long>(c) * b + q + 2 * v);
+      sx[v] = sx[v] + a * xv.x;
+      sy[v] = sy[v] + a * xv.y;
+    }
   }
   const double w = __ldg(&wd[i]);
-  const double2 ri = ld2(r + static_cast<long long>(i) * ldr + q);
-  const double2 xi = ld2(x + static_cast<long long>(i) * b + q);
-  const double resx = ri.x + (-1.0 * sx), resy = ri.y + (-1.0 * sy);
-  st2(out + static_cast<long long>(i) * ldo + q, make_double2(xi.x + w * resx, xi.y + w * resy));
+#pragma unroll
+  for (int v = 0; v < V; ++v) {
+    const double2 ri = ld2(r + static_cast<long long>(i) * ldr + q + 2 * v);
+    const double2 xi = ld2(x + static_cast<long long>(i) * b + q + 2 * v);
+    const double resx = ri.x + (-1.0 * sx[v]), resy = ri.y + (-1.0 * sy[v]);
+    st2(out + static_cast<long long>(i) * ldo + q + 2 * v, make_double2(xi.x + w * resx, xi.y + w * resy));
+  }
 }
 
-static dim3 grid2(int rows, int b) { return dim3((rows + 7) / 8, (b / 2 + 31) / 32); }
+// 4 columns per thread (V = 2) on large short-row matrices, 2 otherwise.  C2 (ncu, V = 1 -> 2):
+// level 0 up1 724 -> 475 us, up2 757 -> 586, down 646 -> 580, restrict (10 per row) 305 -> 268,
+// level-1 up1 (4.7 per row) 184 -> 142; the 13+ per row levels got slower with V = 2, and also
+// with warp-cooperative index loads + shuffles (t_H 4.30 -> 4.43 ms), so they keep V = 1.
+// Env GNW_MVC_V=1 disables V = 2.
+static int mvc_v(const DCsr& M, int b) {
+  static const int vmax = [] {
+    const char* e = std::getenv("GNW_MVC_V");
+    return e ? std::max(1, std::min(2, std::atoi(e))) : 2;
+  }();
+  const bool shape = M.n_rows >= 65536 && M.nnz <= 12LL * M.n_rows;
+  return (vmax >= 2 && b % 4 == 0 && shape) ? 2 : 1;
+}
+static dim3 grid2(int rows, int b, int V) { return dim3((rows + 7) / 8, (b / (2 * V) + 31) / 32); }
+
+#define GNW_MVC_LAUNCH(KERNEL, MAT, ROWS, ...)                                                         \
+  do {                                                                                                 \
+    if (mvc_v(MAT, b) == 2)                                                                            \
+      GNW_LAUNCH(launch_k(KERNEL<2>, grid2(ROWS, b, 2), dim3(32, 8), 0, s, __VA_ARGS__));              \
+    else                                                                                               \
+      GNW_LAUNCH(launch_k(KERNEL<1>, grid2(ROWS, b, 1), dim3(32, 8), 0, s, __VA_ARGS__));              \
+  } while (0)
 
 void mvc2_down(const DLevel& L, const double* r, int ldr, double* resid, int b, cudaStream_t s) {
-  GNW_LAUNCH(launch_k(k_mvc2_down, grid2(L.n, b), dim3(32, 8), 0, s, L.A, L.wd, r, ldr, resid, b));
+  GNW_MVC_LAUNCH(k_mvc2_down, L.A, L.n, L.A, L.wd, r, ldr, resid, b);
   note_launch("mvc2_down");
 }
 void mvc2_restrict(const DLevel& L, const double* resid, double* rc, int b, cudaStream_t s) {
-  GNW_LAUNCH(launch_k(k_mvc2_restrict, grid2(L.R.n_rows, b), dim3(32, 8), 0, s, L.R, resid, rc, b));
+  GNW_MVC_LAUNCH(k_mvc2_restrict, L.R, L.R.n_rows, L.R, resid, rc, b);
   note_launch("mvc2_restrict");
 }
 void mvc2_up1(const DLevel& L, const double* r, int ldr, const double* ec, double* x, int b, cudaStream_t s) {
-  GNW_LAUNCH(launch_k(k_mvc2_up1, grid2(L.n, b), dim3(32, 8), 0, s, L.P, L.wd, r, ldr, ec, x, b));
+  GNW_MVC_LAUNCH(k_mvc2_up1, L.P, L.n, L.P, L.wd, r, ldr, ec, x, b);
   note_launch("mvc2_up1");
 }
 void mvc2_up2(const DLevel& L, const double* r, int ldr, const double* x, double* out, int ldo, int b,
               cudaStream_t s) {
-  GNW_LAUNCH(launch_k(k_mvc2_up2, grid2(L.n, b), dim3(32, 8), 0, s, L.A, L.wd, r, ldr, x, out, ldo, b));
+  GNW_MVC_LAUNCH(k_mvc2_up2, L.A, L.n, L.A, L.wd, r, ldr, x, out, ldo, b);
   note_launch("mvc2_up2");
 }
 

@@ -69,8 +69,12 @@ def test_local_group_matches_single_gpu(world):
     # non-FMA builds differ the same way); the early history is unaffected
     h, h0 = rep.relative_residuals, r0.relative_residuals
     assert np.allclose(h[:40], h0[:40], rtol=1e-6, atol=0)
-    assert abs(rep.iterations - r0.iterations) <= 2
+    assert abs(rep.iterations - r0.iterations) <= 3  # tol 1e-10 sits near the stagnation floor
     assert rep.converged and rel(x, x0) <= 1e-8, rel(x, x0)
+    # at the benchmark tolerance the counts agree within the north star's +-1
+    _, _, r8, _, _ = single(inp, 1e-2, 1e-8)
+    res8 = partitioned(Context.local_group(world), inp, 1e-2, 1e-8)
+    assert abs(res8[0][2].iterations - r8.iterations) <= 1
 
 
 def test_local_group_laplace_and_errors():
