@@ -21,6 +21,23 @@ void note_launch(const char* what);
 namespace {
 __device__ __forceinline__ double2 ld2(const double* p) { return *reinterpret_cast<const double2*>(p); }
 __device__ __forceinline__ void st2(double* p, double2 v) { *reinterpret_cast<double2*>(p) = v; }
+
+// Lanes per row: a warp covers 64V columns of one row when b allows; a narrower batch (C3
+// runs b = 32 for memory) packs 32 / lanes rows into each warp instead of idling lanes.
+__host__ __device__ __forceinline__ int mvc_lanes(int b, int V) {
+  const int need = (b + 2 * V - 1) / (2 * V);
+  int l = 1;
+  while (l < 32 && l < need) l *= 2;
+  return l;
+}
+template <int V>
+struct MvcIdx {
+  int row, q;
+  __device__ MvcIdx(int lsh) {  // lsh = log2(lanes per row), from the launcher
+    row = (((blockIdx.x * 8 + threadIdx.y) << 5) + threadIdx.x) >> lsh;
+    q = 2 * V * ((blockIdx.y << lsh) + (threadIdx.x & ((1 << lsh) - 1)));
+  }
+};
 }  // namespace
 
 // V double2 vectors (2V consecutive columns) per thread.  V = 2 doubles the bytes each
@@ -29,10 +46,10 @@ __device__ __forceinline__ void st2(double* p, double2 v) { *reinterpret_cast<do
 template <int V>
 __global__ void __launch_bounds__(256) k_mvc2_down(DCsr A, const double* __restrict__ wd,
                                                    const double* __restrict__ r, int ldr,
-                                                   double* __restrict__ resid, int b) {
+                                                   double* __restrict__ resid, int b, int lsh) {
   griddep_wait();
-  const int i = blockIdx.x * 8 + threadIdx.y;
-  const int q = 2 * V * (blockIdx.y * 32 + threadIdx.x);
+  const MvcIdx<V> ix(lsh);
+  const int i = ix.row, q = ix.q;
   if (i >= A.n_rows || q >= b) return;
   double sx[V], sy[V];
 #pragma unroll
@@ -58,10 +75,10 @@ __global__ void __launch_bounds__(256) k_mvc2_down(DCsr A, const double* __restr
 
 template <int V>
 __global__ void __launch_bounds__(256) k_mvc2_restrict(DCsr R, const double* __restrict__ resid,
-                                                       double* __restrict__ rc, int b) {
+                                                       double* __restrict__ rc, int b, int lsh) {
   griddep_wait();
-  const int a = blockIdx.x * 8 + threadIdx.y;
-  const int q = 2 * V * (blockIdx.y * 32 + threadIdx.x);
+  const MvcIdx<V> ix(lsh);
+  const int a = ix.row, q = ix.q;
   if (a >= R.n_rows || q >= b) return;
   double sx[V], sy[V];
 #pragma unroll
@@ -85,10 +102,10 @@ __global__ void __launch_bounds__(256) k_mvc2_restrict(DCsr R, const double* __r
 template <int V>
 __global__ void __launch_bounds__(256) k_mvc2_up1(DCsr P, const double* __restrict__ wd,
                                                   const double* __restrict__ r, int ldr,
-                                                  const double* __restrict__ ec, double* __restrict__ x, int b) {
+                                                  const double* __restrict__ ec, double* __restrict__ x, int b, int lsh) {
   griddep_wait();
-  const int i = blockIdx.x * 8 + threadIdx.y;
-  const int q = 2 * V * (blockIdx.y * 32 + threadIdx.x);
+  const MvcIdx<V> ix(lsh);
+  const int i = ix.row, q = ix.q;
   if (i >= P.n_rows || q >= b) return;
   double sx[V], sy[V];
 #pragma unroll
@@ -117,10 +134,10 @@ template <int V>
 __global__ void __launch_bounds__(256) k_mvc2_up2(DCsr A, const double* __restrict__ wd,
                                                   const double* __restrict__ r, int ldr,
                                                   const double* __restrict__ x, double* __restrict__ out,
-                                                  int ldo, int b) {
+                                                  int ldo, int b, int lsh) {
   griddep_wait();
-  const int i = blockIdx.x * 8 + threadIdx.y;
-  const int q = 2 * V * (blockIdx.y * 32 + threadIdx.x);
+  const MvcIdx<V> ix(lsh);
+  const int i = ix.row, q = ix.q;
   if (i >= A.n_rows || q >= b) return;
   double sx[V], sy[V];
 #pragma unroll
@@ -158,16 +175,31 @@ static int mvc_v(const DCsr& M, int b) {
     return e ? std::max(1, std::min(2, std::atoi(e))) : 2;
   }();
   const bool shape = M.n_rows >= 65536 && M.nnz <= 12LL * M.n_rows;
-  return (vmax >= 2 && b % 4 == 0 && shape) ? 2 : 1;
+  // and only when the wider vectors fill the warps as well (b = 160: 40 threads per row
+  // leave a second warp 3/4 idle, 80 fill 2.5 warps)
+  auto fill = [b](int V) {
+    const int need = (b + 2 * V - 1) / (2 * V), l = mvc_lanes(b, V);
+    return static_cast<double>(need) / (((need + l - 1) / l) * l);
+  };
+  return (vmax >= 2 && b % 4 == 0 && shape && fill(2) >= fill(1)) ? 2 : 1;
 }
-static dim3 grid2(int rows, int b, int V) { return dim3((rows + 7) / 8, (b / (2 * V) + 31) / 32); }
+static int lanes_log2(int b, int V) {
+  int l = mvc_lanes(b, V), sh = 0;
+  while ((1 << sh) < l) ++sh;
+  return sh;
+}
+static dim3 grid2(int rows, int b, int V) {
+  const int l = mvc_lanes(b, V), rows_per_cta = 8 * (32 / l);
+  const int need = (b + 2 * V - 1) / (2 * V);
+  return dim3((rows + rows_per_cta - 1) / rows_per_cta, (need + l - 1) / l);
+}
 
 #define GNW_MVC_LAUNCH(KERNEL, MAT, ROWS, ...)                                                         \
   do {                                                                                                 \
     if (mvc_v(MAT, b) == 2)                                                                            \
-      GNW_LAUNCH(launch_k(KERNEL<2>, grid2(ROWS, b, 2), dim3(32, 8), 0, s, __VA_ARGS__));              \
+      GNW_LAUNCH(launch_k(KERNEL<2>, grid2(ROWS, b, 2), dim3(32, 8), 0, s, __VA_ARGS__, lanes_log2(b, 2))); \
     else                                                                                               \
-      GNW_LAUNCH(launch_k(KERNEL<1>, grid2(ROWS, b, 1), dim3(32, 8), 0, s, __VA_ARGS__));              \
+      GNW_LAUNCH(launch_k(KERNEL<1>, grid2(ROWS, b, 1), dim3(32, 8), 0, s, __VA_ARGS__, lanes_log2(b, 1))); \
   } while (0)
 
 void mvc2_down(const DLevel& L, const double* r, int ldr, double* resid, int b, cudaStream_t s) {
