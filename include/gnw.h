@@ -187,10 +187,12 @@ typedef struct gnw_ert_config {
 
 typedef struct gnw_ert_stats {
   double t_assemble;  /* host: P1 stiffness values (assemble_forward, forward.cpp:58-80) */
-  double t_amg;       /* host: amg_setup of the stiffness + upload */
+  double t_amg;       /* preconditioner setup: device geometric MG (structured unit-square
+                         meshes) or host amg_setup of the stiffness + upload */
   double t_solve;     /* device: batched PCG unit-pole solves (solve_unit_pole, forward.cpp:83-98) */
   double t_jacobian;  /* device: gradients, J rows and g (forward.cpp:122-167) */
   uint64_t pcg_iterations;
+  uint64_t gmg_levels;  /* 0: SA-AMG preconditioner, else geometric MG levels */
 } gnw_ert_stats;
 
 /* Mesh::electrode_nodes for the assembled mesh; nodes must lie on z = 0. */

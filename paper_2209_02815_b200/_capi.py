@@ -85,7 +85,8 @@ class ErtConfig(C.Structure):
 
 class ErtStats(C.Structure):
     _fields_ = [("t_assemble", C.c_double), ("t_amg", C.c_double), ("t_solve", C.c_double),
-                ("t_jacobian", C.c_double), ("pcg_iterations", C.c_uint64)]
+                ("t_jacobian", C.c_double), ("pcg_iterations", C.c_uint64),
+                ("gmg_levels", C.c_uint64)]
 
 class GnConfig(C.Structure):
     """GnConfig (inversion.hpp:66-75)."""

@@ -88,6 +88,7 @@ Context::~Context() {
   jmem_.reset();
   damg_.reset();
   fwd_amg_.reset();
+  ews_.reset();
   emem_.reset();
   mem_.release_all();
   if (h_st_) cudaFreeHost(h_st_);
@@ -134,6 +135,9 @@ void Context::assemble(const double* vertices, int64_t nv, const int64_t* cells,
     damg_.reset();
     fwd_amg_.reset();
     emem_.reset();
+    ews_.reset();
+    ews_b_ = -1;
+    fwd_gmg_n_ = -1;
     jm_m_ = -1;
     dJ_ = nullptr;
     dq_ = nullptr;
@@ -190,6 +194,9 @@ void Context::assemble_amg_csr(int64_t n, const int64_t* rowptr, const int64_t* 
     damg_.reset();
     fwd_amg_.reset();
     emem_.reset();
+    ews_.reset();
+    ews_b_ = -1;
+    fwd_gmg_n_ = -1;
     jm_m_ = -1;
     dJ_ = nullptr;
     dq_ = nullptr;

@@ -12,6 +12,8 @@
 #include "../host/setup.hpp"
 #include "amg_device.cuh"
 #include "comm.cuh"
+#include "ert_gmg.cuh"
+#include "ert_kernels.cuh"
 #include "kernels.cuh"
 
 namespace gnw {
@@ -49,6 +51,7 @@ struct GnResult {
 struct ErtTimings {
   double t_assemble = 0.0, t_amg = 0.0, t_solve = 0.0, t_jacobian = 0.0;
   uint64_t pcg_iterations = 0;
+  uint64_t gmg_levels = 0;  // 0: SA-AMG preconditioner (host setup), else geometric MG levels
 };
 
 class Context {
@@ -121,7 +124,7 @@ class Context {
   int64_t m() const { return m_; }
   double beta() const { return beta_; }
   size_t device_bytes() const {
-    return mem_.bytes + (jmem_ ? jmem_->bytes : 0) + (stage_mem_ ? stage_mem_->bytes : 0) + damg_.bytes() + fwd_amg_.bytes() + (emem_ ? emem_->bytes : 0);
+    return mem_.bytes + (jmem_ ? jmem_->bytes : 0) + (stage_mem_ ? stage_mem_->bytes : 0) + damg_.bytes() + fwd_amg_.bytes() + fwd_gmg_.bytes() + (emem_ ? emem_->bytes : 0);
   }
 
   double t_minres = 0.0, t_rhs = 0.0;
@@ -246,7 +249,22 @@ class Context {
   std::vector<int64_t> electrodes_;
   host::ForwardStructure fwd_;      // free-node map, stiffness pattern, per-entry contributions
   DeviceAmg fwd_amg_;               // SA-AMG of the P1 stiffness (rebuilt per model)
-  std::unique_ptr<DeviceMemory> emem_;
+  ErtGmg fwd_gmg_;                  // geometric MG of the same operator (structured meshes)
+  int fwd_gmg_n_ = -1;              // ErtGmg::structured_n of the mesh (-1: not checked yet)
+  std::unique_ptr<DeviceMemory> emem_;  // mesh-only forward structure on the device (per mesh)
+  DCsr ek_{};                           // stiffness pattern (values re-uploaded per model)
+  int64_t *ecells_ = nullptr, *en2f_ = nullptr;
+  double *egrad_ = nullptr, *earea_ = nullptr;
+  std::unique_ptr<DeviceMemory> ews_;   // response_jacobian work buffers
+  struct {
+    double *X, *R, *Z, *P, *AP, *sc, *part, *m, *gx, *gz, *gpart, *J, *g;
+    int *active, *col;
+    int64_t* unit;
+    ErtCfgDev* cfg;
+  } ew_{};
+  int ews_b_ = -1;
+  int64_t ews_ncfg_ = -1;
+  bool ews_own_ = false;
 };
 
 }  // namespace gnw

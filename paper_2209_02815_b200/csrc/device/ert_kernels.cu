@@ -5,6 +5,9 @@
 // with the response g_i = sum_c of the same terms.
 #include <cuda_runtime.h>
 
+#include <stdexcept>
+#include <string>
+
 #include "ert_kernels.cuh"
 
 namespace gnw {
@@ -129,7 +132,10 @@ __global__ void __launch_bounds__(256) k_cell_grad(const int64_t* __restrict__ c
   }
 }
 
-// J rows and response partials (forward.cpp:145-167).  grid = (cell chunks of 256, config groups of 32)
+// J rows and response partials (forward.cpp:145-167).  grid = (config groups of 32, cell chunks
+// of 256): the config groups of one cell chunk run back to back, so the chunk's gradient
+// columns are re-read from L2, not DRAM (the other order re-streamed gx/gz, 2 GB at C5, once
+// per group: 42 ms for the 63 GB J).
 __global__ void __launch_bounds__(256) k_jacobian(const ErtCfgDev* __restrict__ cfg, int n_cfg,
                                                   const int* __restrict__ col_of_electrode, const double* __restrict__ gx,
                                                   const double* __restrict__ gz, const double* __restrict__ mdl,
@@ -137,23 +143,33 @@ __global__ void __launch_bounds__(256) k_jacobian(const ErtCfgDev* __restrict__ 
                                                   long long ldj, double* __restrict__ gpart) {
   griddep_wait();
   __shared__ double red[8][33];
-  const long long c = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const long long c = static_cast<long long>(blockIdx.y) * blockDim.x + threadIdx.x;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const bool ok = c < nc;
   const double sa = ok ? exp(mdl[c]) : 0.0;
   const double ar = ok ? area[c] : 0.0;
+  // surveys list the readings of one source together: the source gradient t is reloaded
+  // only when (a, b) changes (uniform across the block), halving the gradient loads
+  int pa = -2, pb = -2;
+  double tx = 0.0, tz = 0.0;
   for (int k = 0; k < 32; ++k) {
-    const int i = blockIdx.y * 32 + k;
+    const int i = blockIdx.x * 32 + k;
     if (i >= n_cfg) break;  // uniform across the block
     const ErtCfgDev cf = cfg[i];
     double term = 0.0;
     if (ok) {
-      const long long a = col_of_electrode[cf.a], mm = col_of_electrode[cf.m], nn = col_of_electrode[cf.n];
-      double tx = gx[a * nc + c], tz = gz[a * nc + c];
-      if (cf.b >= 0) {
-        const long long bb = col_of_electrode[cf.b];
-        tx = tx - gx[bb * nc + c];
-        tz = tz - gz[bb * nc + c];
+      const long long mm = col_of_electrode[cf.m], nn = col_of_electrode[cf.n];
+      if (cf.a != pa || cf.b != pb) {
+        const long long a = col_of_electrode[cf.a];
+        tx = gx[a * nc + c];
+        tz = gz[a * nc + c];
+        if (cf.b >= 0) {
+          const long long bb = col_of_electrode[cf.b];
+          tx = tx - gx[bb * nc + c];
+          tz = tz - gz[bb * nc + c];
+        }
+        pa = cf.a;
+        pb = cf.b;
       }
       const double rx = gx[mm * nc + c] - gx[nn * nc + c];
       const double rz = gz[mm * nc + c] - gz[nn * nc + c];
@@ -166,11 +182,11 @@ __global__ void __launch_bounds__(256) k_jacobian(const ErtCfgDev* __restrict__ 
   }
   __syncthreads();
   if (threadIdx.x < 32) {
-    const int i = blockIdx.y * 32 + threadIdx.x;
+    const int i = blockIdx.x * 32 + threadIdx.x;
     if (i < n_cfg) {
       double s = 0.0;
       for (int w = 0; w < 8; ++w) s += red[w][threadIdx.x];
-      gpart[static_cast<long long>(blockIdx.x) * n_cfg + i] = s;
+      gpart[static_cast<long long>(blockIdx.y) * n_cfg + i] = s;
     }
   }
 }
@@ -187,6 +203,16 @@ __global__ void k_response_reduce(const double* __restrict__ gpart, int nchunks,
 }
 
 // ------------------------------------------------------------------ launchers
+__global__ void k_unit_columns(double* __restrict__ R, const int64_t* __restrict__ unit, int b) {
+  const int q = blockIdx.x * blockDim.x + threadIdx.x;
+  if (q < b) R[unit[q] * b + q] = 1.0;
+}
+void unit_columns(double* R, const int64_t* unit, long long nf, int b, cudaStream_t s) {
+  const cudaError_t e = cudaMemsetAsync(R, 0, static_cast<size_t>(nf) * b * sizeof(double), s);
+  if (e != cudaSuccess) throw std::runtime_error(std::string("unit_columns: ") + cudaGetErrorString(e));
+  k_unit_columns<<<cdiv(b, 64), 64, 0, s>>>(R, unit, b);
+  note_launch("unit_columns");
+}
 void spmm(const DCsr& A, const double* X, double* Y, int b, cudaStream_t s) {
   GNW_LAUNCH(launch_k(k_spmm, dim3(cdiv(A.n_rows, 8), cdiv(b, 32)), dim3(32, 8), 0, s, A, X, Y, b));
   note_launch("spmm");
@@ -219,7 +245,7 @@ void jacobian(const ErtCfgDev* cfg, int n_cfg, const int* col_of_electrode, cons
               const double* mdl, const double* area, long long nc, double* J, long long ldj, double* gpart, double* g,
               cudaStream_t s) {
   const int nch = jacobian_chunks(nc);
-  GNW_LAUNCH(launch_k(k_jacobian, dim3(nch, cdiv(n_cfg, 32)), kT, 0, s, cfg, n_cfg, col_of_electrode, gx, gz, mdl,
+  GNW_LAUNCH(launch_k(k_jacobian, dim3(cdiv(n_cfg, 32), nch), kT, 0, s, cfg, n_cfg, col_of_electrode, gx, gz, mdl,
                       area, nc, J, ldj, gpart));
   note_launch("jacobian");
   GNW_LAUNCH(launch_k(k_response_reduce, cdiv(static_cast<long long>(n_cfg) * 32, kT), kT, 0, s, gpart, nch, n_cfg, g));

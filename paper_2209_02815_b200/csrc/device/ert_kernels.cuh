@@ -13,6 +13,8 @@ struct ErtCfgDev {  // ElectrodeConfig, survey.hpp:15-21 (b < 0: pole at infinit
   double k;
 };
 
+// R = 0 except R[unit[q] * b + q] = 1 (the unit-pole right-hand sides, free x b interleaved)
+void unit_columns(double* R, const int64_t* unit, long long nf, int b, cudaStream_t s);
 void spmm(const DCsr& A, const double* X, double* Y, int b, cudaStream_t s);
 int col_dots_chunks(long long n);
 void col_dots(const double* X, const double* Y, long long n, int b, double* part, unsigned* counter, double* out,

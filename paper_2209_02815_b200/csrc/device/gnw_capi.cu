@@ -341,7 +341,7 @@ gnw_status gnw_response_jacobian(gnw_ctx* ctx, const double* m, const gnw_ert_co
     for (uint64_t i = 0; i < n_cfg; ++i) c[i] = {cfgs[i].a, cfgs[i].b, cfgs[i].m, cfgs[i].n, cfgs[i].k};
     gnw::ErtTimings t;
     ctx_of(ctx).response_jacobian(m, c.data(), static_cast<int64_t>(n_cfg), J, g, tol, &t);
-    if (stats) *stats = {t.t_assemble, t.t_amg, t.t_solve, t.t_jacobian, t.pcg_iterations};
+    if (stats) *stats = {t.t_assemble, t.t_amg, t.t_solve, t.t_jacobian, t.pcg_iterations, t.gmg_levels};
   });
 }
 

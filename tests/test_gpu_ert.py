@@ -104,3 +104,31 @@ def test_c4_gn_step_against_restatement_reduced():
     assert rep.converged and rr["converged"]
     assert abs(rep.iterations - rr["iterations"]) <= 1
     assert rel(x, xr) <= 1e-6
+
+
+def test_geometric_mg_and_amg_preconditioners_agree(monkeypatch):
+    """Structured unit-square meshes precondition the pole solves with the device geometric MG
+    (ert_gmg.cu); GNW_ERT_PC=amg selects the host SA-AMG.  Both converge to the same g and J."""
+    mesh, nodes, sv, model = small_case(64, 16, 2, 4)
+    c = gpu_ert(mesh, nodes)
+    g, J, st = c.response_jacobian(model, sv, tol=1e-13)
+    assert st["gmg_levels"] == 3  # 64, 32, 16
+    monkeypatch.setenv("GNW_ERT_PC", "amg")
+    ga, Ja, sta = c.response_jacobian(model, sv, tol=1e-13)
+    assert sta["gmg_levels"] == 0
+    assert rel(g, ga) <= 1e-10 and rel(J, Ja) <= 1e-9
+    assert st["pcg_iterations"] < sta["pcg_iterations"]
+
+
+def test_unstructured_cell_order_falls_back_to_amg():
+    """A mesh whose cells are not in make_unit_square_mesh order keeps the SA-AMG path and the
+    same physics (g is invariant to the cell numbering; J's columns follow the cells)."""
+    mesh, nodes, sv, model = small_case(32, 8, 2, 4)
+    perm = np.random.default_rng(5).permutation(mesh.n_cells)
+    pm = W.Mesh(mesh.vertices, np.ascontiguousarray(mesh.cells[perm]))
+    c0, c1 = gpu_ert(mesh, nodes), gpu_ert(pm, nodes)
+    g0, J0, st0 = c0.response_jacobian(model, sv, tol=1e-13)
+    g1, J1, st1 = c1.response_jacobian(np.ascontiguousarray(model[perm]), sv, tol=1e-13)
+    assert st0["gmg_levels"] == 2 and st1["gmg_levels"] == 0
+    assert rel(g1, g0) <= 1e-10
+    assert rel(J1, J0[:, perm]) <= 1e-9
