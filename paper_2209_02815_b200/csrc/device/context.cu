@@ -483,7 +483,8 @@ void Context::set_jacobian(const double* J, int64_t m, int64_t n_cells, double b
 // MINRES).  The next set_jacobian with the same host pointer and shape waits for it on the
 // device and takes the staged bytes; any other set_jacobian drops the stage.  The caller
 // keeps the host array unchanged until then (pinned memory gives the overlap; pageable
-// memory makes the copy synchronous, still correct).  Host-pointer mode only.
+// memory makes the copy synchronous, still correct).  Host-pointer mode only.  When a second
+// J-sized buffer does not fit beside the solve's working set, nothing is staged.
 void Context::prefetch_jacobian(const double* J, int64_t m, int64_t n_cells) {
   require_mixed();
   require_device();
@@ -497,6 +498,16 @@ void Context::prefetch_jacobian(const double* J, int64_t m, int64_t n_cells) {
     GNW_CUDA_CHECK(cudaStreamSynchronize(copy_));
     sync();  // a pending consume of the old buffer
     stage_mem_.reset();
+    stage_cap_ = 0;
+    // A second J-sized buffer must leave room for the solve (C3/C5: J + H already take
+    // 127-137 GB); without it the prefetch is a no-op and set_jacobian copies as usual.
+    size_t free_b = 0, total_b = 0;
+    GNW_CUDA_CHECK(cudaMemGetInfo(&free_b, &total_b));
+    if (need * sizeof(double) + (size_t{4} << 30) > free_b) {
+      staged_src_ = nullptr;
+      stage_deferred_ = false;
+      return;
+    }
     stage_mem_ = std::make_unique<DeviceMemory>();
     jstage_ = stage_mem_->alloc<double>(need);
     stage_cap_ = need;
