@@ -355,54 +355,84 @@ void mcoarse_inverse(const double* Ainv, int n, const double* r, double* x, int 
   check_launch("mcoarse_inverse");
 }
 
-// rows [r0, r0+b) of A (row-major, `cols` columns) -> X[c * b + q]
-__global__ void k_transpose_rows_to_batch(const double* __restrict__ A, long long cols, long long ld, int r0, int b,
-                                          double* __restrict__ X) {
+// rows [r0, r0+b) of A (row-major, `cols` columns) -> X[c * b + q]; and back.  Tiles of
+// 32 rows (q) x 64 columns (c): the row side moves 16-byte pairs (512 B per warp row), so
+// every thread has 4 x 16 B in flight on that side (the 32 x 32 tiles with 8-byte accesses
+// ran at 4.6-4.8 TB/s).  `vec` = both the row stride and the tile start are even.
+__global__ void __launch_bounds__(256) k_transpose_rows_to_batch(const double* __restrict__ A, long long cols,
+                                                                 long long ld, int r0, int b,
+                                                                 double* __restrict__ X) {
   griddep_wait();
-  __shared__ double tile[32][33];
-  const long long c0 = static_cast<long long>(blockIdx.x) * 32;
+  __shared__ double tile[32][65];
+  const long long c0 = static_cast<long long>(blockIdx.x) * 64;
   const int q0 = blockIdx.y * 32;
+  const bool vec = (ld & 1) == 0;
+#pragma unroll
   for (int y = threadIdx.y; y < 32; y += 8) {
     const int q = q0 + y;
-    const long long c = c0 + threadIdx.x;
-    tile[y][threadIdx.x] = (q < b && c < cols) ? A[static_cast<long long>(r0 + q) * ld + c] : 0.0;
+    const long long c = c0 + 2 * threadIdx.x;
+    double2 v = make_double2(0.0, 0.0);
+    if (q < b) {
+      const double* row = A + static_cast<long long>(r0 + q) * ld;
+      if (vec && c + 1 < cols) {
+        v = __ldg(reinterpret_cast<const double2*>(row + c));
+      } else {
+        if (c < cols) v.x = __ldg(row + c);
+        if (c + 1 < cols) v.y = __ldg(row + c + 1);
+      }
+    }
+    tile[y][2 * threadIdx.x] = v.x;
+    tile[y][2 * threadIdx.x + 1] = v.y;
   }
   __syncthreads();
-  for (int y = threadIdx.y; y < 32; y += 8) {
+#pragma unroll
+  for (int y = threadIdx.y; y < 64; y += 8) {
     const long long c = c0 + y;
     const int q = q0 + threadIdx.x;
     if (c < cols && q < b) X[c * b + q] = tile[threadIdx.x][y];
   }
 }
 
-__global__ void k_transpose_batch_to_rows(const double* __restrict__ X, long long cols, long long ld, int r0, int b,
-                                          double* __restrict__ A) {
+__global__ void __launch_bounds__(256) k_transpose_batch_to_rows(const double* __restrict__ X, long long cols,
+                                                                 long long ld, int r0, int b,
+                                                                 double* __restrict__ A) {
   griddep_wait();
-  __shared__ double tile[32][33];
-  const long long c0 = static_cast<long long>(blockIdx.x) * 32;
+  __shared__ double tile[32][65];
+  const long long c0 = static_cast<long long>(blockIdx.x) * 64;
   const int q0 = blockIdx.y * 32;
-  for (int y = threadIdx.y; y < 32; y += 8) {
+  const bool vec = (ld & 1) == 0;
+#pragma unroll
+  for (int y = threadIdx.y; y < 64; y += 8) {
     const long long c = c0 + y;
     const int q = q0 + threadIdx.x;
-    tile[y][threadIdx.x] = (c < cols && q < b) ? X[c * b + q] : 0.0;
+    tile[threadIdx.x][y] = (c < cols && q < b) ? X[c * b + q] : 0.0;
   }
   __syncthreads();
+#pragma unroll
   for (int y = threadIdx.y; y < 32; y += 8) {
     const int q = q0 + y;
-    const long long c = c0 + threadIdx.x;
-    if (q < b && c < cols) A[static_cast<long long>(r0 + q) * ld + c] = tile[threadIdx.x][y];
+    const long long c = c0 + 2 * threadIdx.x;
+    if (q >= b) continue;
+    double* row = A + static_cast<long long>(r0 + q) * ld;
+    const double2 v = make_double2(tile[y][2 * threadIdx.x], tile[y][2 * threadIdx.x + 1]);
+    if (vec && c + 1 < cols) {
+      *reinterpret_cast<double2*>(row + c) = v;
+    } else {
+      if (c < cols) row[c] = v.x;
+      if (c + 1 < cols) row[c + 1] = v.y;
+    }
   }
 }
 
 void transpose_rows_to_batch(const double* A, long long cols, long long ld, int r0, int b, double* X,
                              cudaStream_t s) {
-  dim3 grid(static_cast<unsigned>((cols + 31) / 32), (b + 31) / 32), block(32, 8);
+  dim3 grid(static_cast<unsigned>((cols + 63) / 64), (b + 31) / 32), block(32, 8);
   GNW_LAUNCH(launch_k(k_transpose_rows_to_batch, grid, block, 0, s, A, cols, ld, r0, b, X));
   check_launch("transpose_rows_to_batch");
 }
 void transpose_batch_to_rows(const double* X, long long cols, long long ld, int r0, int b, double* A,
                              cudaStream_t s) {
-  dim3 grid(static_cast<unsigned>((cols + 31) / 32), (b + 31) / 32), block(32, 8);
+  dim3 grid(static_cast<unsigned>((cols + 63) / 64), (b + 31) / 32), block(32, 8);
   GNW_LAUNCH(launch_k(k_transpose_batch_to_rows, grid, block, 0, s, X, cols, ld, r0, b, A));
   check_launch("transpose_batch_to_rows");
 }
