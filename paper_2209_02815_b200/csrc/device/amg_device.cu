@@ -260,8 +260,8 @@ void DeviceAmg::ensure_batch(int b) {
 // the reference's amg_apply; in the default mode it agrees with the loop's single-RHS cycle
 // (warp-per-row on wide levels, dense collapsed tail) to rounding.  (A 32-partial emulation
 // of the warp lanes kept the two bitwise equal but ran the C2 setup at 1/3 of its roofline.)
-void DeviceAmg::vcycle_batch(const double* r0, int b, double* out0, int exact, const MinresState* st_plain,
-                             cudaStream_t s) {
+bool DeviceAmg::vcycle_batch(const double* r0, int b, double* out0, int exact, const MinresState* st_plain,
+                             cudaStream_t s, double* ht, long long ldh) {
   const int L = static_cast<int>(lv_.size());
   ensure_batch(b);
   auto coarse = [&](const double* r, double* x) {
@@ -272,7 +272,7 @@ void DeviceAmg::vcycle_batch(const double* r0, int b, double* out0, int exact, c
   };
   if (L == 1) {
     coarse(r0, out0);
-    return;
+    return false;
   }
   const int stop = (!exact && collapse_l_ > 0) ? collapse_l_ : L - 1;  // as in cycle_levels
   for (int l = 0; l < stop; ++l) {
@@ -285,12 +285,17 @@ void DeviceAmg::vcycle_batch(const double* r0, int b, double* out0, int exact, c
     coarse(mr_[L - 1], me_[L - 1]);
   else
     dense_seq_batch(collapse_M_, lv_[stop].n, mr_[stop], me_[stop], b, s);
+  bool to_rows = false;
   for (int l = stop - 1; l >= 0; --l) {
     const double* rl = l == 0 ? r0 : mr_[l];
     const DLevel lev = level(l, 1);
     mvc_up1(lev, rl, b, me_[l + 1], mx_[l], b, s);
-    mvc_up2(lev, rl, b, mx_[l], l == 0 ? out0 : me_[l], b, b, s);
+    if (l == 0 && ht != nullptr && mvc2_up2_rows(lev, rl, b, mx_[l], ht, ldh, b, s))
+      to_rows = true;
+    else
+      mvc_up2(lev, rl, b, mx_[l], l == 0 ? out0 : me_[l], b, b, s);
   }
+  return to_rows;
 }
 
 }  // namespace gnw

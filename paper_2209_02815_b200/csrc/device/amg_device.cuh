@@ -53,7 +53,10 @@ class DeviceAmg {
   // z = B r, one V-cycle (exact = the reference's thread-per-row order and Cholesky coarse solve)
   void vcycle(VSel r0, double* out0, const MinresState* st, int exact, cudaStream_t s);
   // b columns interleaved: r0 / out0 are n x b (ld = b)
-  void vcycle_batch(const double* r0, int b, double* out0, int exact, const MinresState* st_plain, cudaStream_t s);
+  // With ht != nullptr the result may instead be stored transposed into Ht rows
+  // (ht[q * ldh + i], see mvc2_up2_rows); returns true when it was (out0 untouched).
+  bool vcycle_batch(const double* r0, int b, double* out0, int exact, const MinresState* st_plain, cudaStream_t s,
+                    double* ht = nullptr, long long ldh = 0);
   void ensure_batch(int b);
   int batch_capacity() const { return bmem_b_; }
   double* batch_in() const { return bR0_; }

@@ -428,8 +428,9 @@ void Context::set_jacobian(const double* J, int64_t m, int64_t n_cells, double b
         break;
       }
       transpose_rows_to_batch(dJ_, N_, ldj_, static_cast<int>(i0), bb, damg_.batch_in(), s);
-      damg_.vcycle_batch(damg_.batch_in(), bb, damg_.batch_out(), coarse_mode == 1, st_plain_, s);
-      transpose_batch_to_rows(damg_.batch_out(), N_, ldh_, static_cast<int>(i0), bb, dHt_, s);
+      if (!damg_.vcycle_batch(damg_.batch_in(), bb, damg_.batch_out(), coarse_mode == 1, st_plain_, s,
+                              dHt_ + i0 * ldh_, ldh_))
+        transpose_batch_to_rows(damg_.batch_out(), N_, ldh_, static_cast<int>(i0), bb, dHt_, s);
     }
     GNW_CUDA_CHECK(cudaEventRecord(ev[1], s));
   }

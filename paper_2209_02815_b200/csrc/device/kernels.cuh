@@ -58,6 +58,10 @@ void mvc2_restrict(const DLevel& L, const double* resid, double* rc, int b, cuda
 void mvc2_up1(const DLevel& L, const double* r, int ldr, const double* ec, double* x, int b, cudaStream_t s);
 void mvc2_up2(const DLevel& L, const double* r, int ldr, const double* x, double* out, int ldo, int b,
               cudaStream_t s);
+// level-0 up2 storing straight into rows of Ht (ht = &Ht[r0 * ldh], column i = fine row);
+// false when the shape does not fit (V = 2, 32 lanes per row, n % 8 == 0) -- nothing launched
+bool mvc2_up2_rows(const DLevel& L, const double* r, int ldr, const double* x, double* ht, long long ldh, int b,
+                   cudaStream_t s);
 
 // ------------------------------------------------------------------ V-cycle
 // Single right-hand side (amg.cpp:90-111); `r` may be a ring slot (level 0).

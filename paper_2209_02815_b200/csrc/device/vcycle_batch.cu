@@ -164,6 +164,60 @@ __global__ void __launch_bounds__(256) k_mvc2_up2(DCsr A, const double* __restri
   }
 }
 
+// Level-0 up2 of the Woodbury setup with the batch -> rows transpose fused into its store:
+// out(i, q) goes straight to Ht[(r0 + q) * ldh + i] instead of an n x b buffer that a second
+// kernel transposes (saves a write and a read of n x b doubles, 2.1 GB at C2).  The CTA's
+// 8 rows x 128 columns are staged in shared memory, then each column's 8 consecutive rows
+// leave as one 64-byte run (two 16-byte stores per thread).  V = 2, one row per warp.
+__global__ void __launch_bounds__(256) k_mvc2_up2_rows(DCsr A, const double* __restrict__ wd,
+                                                       const double* __restrict__ r, int ldr,
+                                                       const double* __restrict__ x, double* __restrict__ ht,
+                                                       long long ldh, int b) {
+  griddep_wait();
+  __shared__ __align__(16) double tile[8][129];
+  const int ty = threadIdx.y, lane = threadIdx.x;
+  const int i0 = blockIdx.x * 8, i = i0 + ty;
+  const int qb = blockIdx.y * 128, q = qb + 4 * lane;
+  const bool ok = i < A.n_rows && q < b;
+  double sx[2] = {0.0, 0.0}, sy[2] = {0.0, 0.0};
+  if (ok) {
+    const int k0 = A.rowptr[i], k1 = A.rowptr[i + 1];
+#pragma unroll 4
+    for (int k = k0; k < k1; ++k) {
+      const int c = __ldg(&A.cols[k]);
+      const double a = __ldg(&A.vals[k]);
+#pragma unroll
+      for (int v = 0; v < 2; ++v) {
+        const double2 xv = ld2(x + static_cast<long long>(c) * b + q + 2 * v);
+        sx[v] = sx[v] + a * xv.x;
+        sy[v] = sy[v] + a * xv.y;
+      }
+    }
+    const double w = __ldg(&wd[i]);
+#pragma unroll
+    for (int v = 0; v < 2; ++v) {
+      const double2 ri = ld2(r + static_cast<long long>(i) * ldr + q + 2 * v);
+      const double2 xi = ld2(x + static_cast<long long>(i) * b + q + 2 * v);
+      const double resx = ri.x + (-1.0 * sx[v]), resy = ri.y + (-1.0 * sy[v]);
+      tile[ty][4 * lane + 2 * v] = xi.x + w * resx;
+      tile[ty][4 * lane + 2 * v + 1] = xi.y + w * resy;
+    }
+  }
+  __syncthreads();
+  // 128 columns x 2 halves of 4 rows: thread t writes rows 4h..4h+3 of column t / 2
+  const int t = ty * 32 + lane, cq = t >> 1, h = t & 1;
+  const int qq = qb + cq;
+  if (qq >= b) return;
+  double* dst = ht + static_cast<long long>(qq) * ldh + i0 + 4 * h;
+  const int rows = min(4, A.n_rows - (i0 + 4 * h));
+  if (rows == 4) {
+    st2(dst, make_double2(tile[4 * h][cq], tile[4 * h + 1][cq]));
+    st2(dst + 2, make_double2(tile[4 * h + 2][cq], tile[4 * h + 3][cq]));
+  } else {
+    for (int rr = 0; rr < rows; ++rr) dst[rr] = tile[4 * h + rr][cq];
+  }
+}
+
 // 4 columns per thread (V = 2) on large short-row matrices, 2 otherwise.  C2 (ncu, V = 1 -> 2):
 // level 0 up1 724 -> 475 us, up2 757 -> 586, down 646 -> 580, restrict (10 per row) 305 -> 268,
 // level-1 up1 (4.7 per row) 184 -> 142; the 13+ per row levels got slower with V = 2, and also
@@ -214,6 +268,15 @@ void mvc2_up1(const DLevel& L, const double* r, int ldr, const double* ec, doubl
   GNW_MVC_LAUNCH(k_mvc2_up1, L.P, L.n, L.P, L.wd, r, ldr, ec, x, b);
   note_launch("mvc2_up1");
 }
+bool mvc2_up2_rows(const DLevel& L, const double* r, int ldr, const double* x, double* ht, long long ldh, int b,
+                   cudaStream_t s) {
+  if (ldr % 2 != 0 || ldh % 2 != 0 || L.n % 8 != 0 || mvc_v(L.A, b) != 2 || mvc_lanes(b, 2) != 32) return false;
+  const dim3 grid((L.n + 7) / 8, (b + 127) / 128);
+  GNW_LAUNCH(launch_k(k_mvc2_up2_rows, grid, dim3(32, 8), 0, s, L.A, L.wd, r, ldr, x, ht, ldh, b));
+  note_launch("mvc2_up2_rows");
+  return true;
+}
+
 void mvc2_up2(const DLevel& L, const double* r, int ldr, const double* x, double* out, int ldo, int b,
               cudaStream_t s) {
   GNW_MVC_LAUNCH(k_mvc2_up2, L.A, L.n, L.A, L.wd, r, ldr, x, out, ldo, b);

@@ -81,6 +81,24 @@ def test_woodbury_H_bitwise_and_L(c1, gpu_ctx_factory, n, m):
     assert set(tg) == {"t_H", "t_C", "t_chol"}
 
 
+@pytest.mark.parametrize("m", [128, 228, 132])
+def test_woodbury_H_bitwise_wide_batch(oracle, gpu_ctx_factory, m):
+    """A mesh and batch large enough for the 4-column batched kernels (>= 65536 rows) and the
+    level-0 store straight into Ht rows (full column groups: m = 128; a partial last group:
+    228; 132 keeps 2 columns per thread and the separate transpose): H stays bit-identical to the
+    reference's amg_apply column by column (exact coarse mode)."""
+    n = 256  # 131072 cells (default AmgOptions work here, SURVEY 8(c))
+    mesh = W.unit_square_mesh(n)
+    J = np.random.default_rng(5).standard_normal((m, mesh.n_cells))
+    ctx = gpu_ctx_factory(mesh, exact=True)
+    ctx.set_jacobian(J, 1e-2)
+    H, _ = ctx.woodbury_factors()
+    prob = orc.Problem.mixed(oracle, mesh)
+    prob.set_jacobian(J, 1e-2)
+    Href = prob.H()
+    assert np.array_equal(H, Href), f"H max diff {np.max(np.abs(H - Href))}"
+
+
 def test_device_cholesky_bitwise(oracle, gpu_ctx_factory):
     mesh = W.unit_square_mesh(4)
     ctx = gpu_ctx_factory(mesh)
