@@ -41,6 +41,8 @@ struct DeviceMemory {
 };
 
 DCsr upload_csr(DeviceMemory& mem, const host::Csr& A, cudaStream_t s);
+// sparse_matmul on the device, bit-identical to host::spgemm (spgemm.cu)
+host::Csr device_spgemm(const host::Csr& A, const host::Csr& B, cudaStream_t s);
 
 class DeviceAmg {
  public:

@@ -9,6 +9,8 @@
 #include "context.cuh"
 
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
@@ -117,11 +119,44 @@ void Context::destroy_graph() {
 void Context::assemble(const double* vertices, int64_t nv, const int64_t* cells, int64_t nc,
                        const host::AmgOptions& o) {
   destroy_graph();
+  // Env GNW_DEVICE_SPGEMM=1: the setup's sparse products run on this context's device
+  // (spgemm.cu, bit-identical to the host / reference sparse_matmul).  Off by default: the
+  // products themselves take 3-40 ms on the B200 against 60-600 ms on 16 host cores, but
+  // the host hierarchy around them makes every product a pageable upload + download
+  // (n = 2048: 9.2 s setup against 7.5 s on the host).  A device-resident setup is next.
+  struct HookGuard {
+    explicit HookGuard(Context* c) {
+      const char* e = std::getenv("GNW_DEVICE_SPGEMM");
+      const char* mn = std::getenv("GNW_SPGEMM_MIN");  // products below which the host is used
+      const int64_t min_products = mn ? std::atoll(mn) : (int64_t{1} << 20);
+      if (c->has_device() && e && std::atoi(e) != 0)
+        host::set_spgemm_hook(
+            [](const host::Csr& A, const host::Csr& B, void* u) {
+              Context* cx = static_cast<Context*>(u);
+              GNW_CUDA_CHECK(cudaSetDevice(cx->device_));
+              return device_spgemm(A, B, cx->stream_);
+            },
+            c, min_products);
+    }
+    ~HookGuard() { host::set_spgemm_hook(nullptr, nullptr, 0); }
+  } hook_guard(this);
+  const auto t0 = std::chrono::steady_clock::now();
   mesh_ = host::finalize_mesh(vertices, nv, cells, nc);  // mesh.cpp:85-154
+  const auto t1 = std::chrono::steady_clock::now();
   Q_ = host::assemble_Q(mesh_);                          // fem_mixed.cpp:29-68
+  const auto t1q = std::chrono::steady_clock::now();
   D_ = host::assemble_D(mesh_);                          // fem_mixed.cpp:70-82
+  const auto t1d = std::chrono::steady_clock::now();
   S_ = host::lumped_schur(Q_, D_);                       // fem_mixed.cpp:84-94
+  const auto t2 = std::chrono::steady_clock::now();
   amg_ = host::amg_setup(S_, o);                         // amg.cpp:115-187
+  if (const char* e = std::getenv("GNW_SETUP_TIMING"))
+    if (std::atoi(e) != 0)
+      std::fprintf(stderr, "[gnw setup] finalize_mesh %.1f ms, assemble Q %.1f ms, D %.1f ms, S_hat %.1f ms\n",
+                   std::chrono::duration<double, std::milli>(t1 - t0).count(),
+                   std::chrono::duration<double, std::milli>(t1q - t1).count(),
+                   std::chrono::duration<double, std::milli>(t1d - t1q).count(),
+                   std::chrono::duration<double, std::milli>(t2 - t1d).count());
   K_ = mesh_.ne;
   N_ = mesh_.nc;
   mixed_ = true;

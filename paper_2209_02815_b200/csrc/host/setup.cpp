@@ -4,6 +4,10 @@
 
 #include <omp.h>
 
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
+
 #include <algorithm>
 #include <cmath>
 #include <numeric>
@@ -239,8 +243,25 @@ Csr transpose(const Csr& A) {
 
 // sparse_matmul, sparse.cpp:118-154.  Row-parallel; each row accumulates in the
 // reference's (A entry, B entry) order and emits sorted columns.
+namespace {
+thread_local SpgemmHook t_spgemm_hook = nullptr;
+thread_local void* t_spgemm_user = nullptr;
+thread_local int64_t t_spgemm_min = 0;
+}  // namespace
+
+void set_spgemm_hook(SpgemmHook fn, void* user, int64_t min_products) {
+  t_spgemm_hook = fn;
+  t_spgemm_user = user;
+  t_spgemm_min = min_products;
+}
+
 Csr spgemm(const Csr& A, const Csr& B) {
   if (A.n_cols != B.n_rows) throw std::invalid_argument("sparse_matmul: dimension mismatch");
+  if (t_spgemm_hook != nullptr) {
+    int64_t products = 0;
+    for (int64_t k = 0; k < A.nnz(); ++k) products += B.rowptr[A.cols[k] + 1] - B.rowptr[A.cols[k]];
+    if (products >= t_spgemm_min) return t_spgemm_hook(A, B, t_spgemm_user);
+  }
   Csr C;
   C.n_rows = A.n_rows;
   C.n_cols = B.n_cols;
@@ -427,8 +448,30 @@ std::vector<int64_t> aggregate(const Csr& A, const AmgOptions& o, int64_t& n_agg
 
 }  // namespace
 
+namespace {
+// env GNW_SETUP_TIMING=1: per-phase wall times of the host setup on stderr
+bool setup_timing() {
+  static const bool on = [] {
+    const char* e = std::getenv("GNW_SETUP_TIMING");
+    return e != nullptr && std::atoi(e) != 0;
+  }();
+  return on;
+}
+struct PhaseTimer {
+  std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now();
+  void lap(const char* what, long long level = -1) {
+    if (!setup_timing()) return;
+    const auto t1 = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[gnw setup] %-24s level %2lld  %8.1f ms\n", what, level,
+                 std::chrono::duration<double, std::milli>(t1 - t0).count());
+    t0 = t1;
+  }
+};
+}  // namespace
+
 // amg_setup, amg.cpp:115-187
 AmgHierarchy amg_setup(const Csr& S, const AmgOptions& o) {
+  PhaseTimer pt;
   if (S.n_rows != S.n_cols) throw std::invalid_argument("amg_setup: matrix not square");
   double max_abs = 0.0;
   for (double v : S.vals) max_abs = std::max(max_abs, std::abs(v));
@@ -439,7 +482,10 @@ AmgHierarchy amg_setup(const Csr& S, const AmgOptions& o) {
   Csr cur = S;
   while (static_cast<int64_t>(h.levels.size()) + 1 < o.max_levels && cur.n_rows > o.coarse_threshold) {
     int64_t n_agg = 0;
+    const long long lev = static_cast<long long>(h.levels.size());
+    pt.lap("(level start)", lev);
     const std::vector<int64_t> agg = aggregate(cur, o, n_agg);
+    pt.lap("aggregate", lev);
     if (n_agg >= cur.n_rows) break;
     // tentative prolongator, amg.cpp:70-79 (one entry per row, no duplicates)
     std::vector<int64_t> count(n_agg, 0);
@@ -480,7 +526,9 @@ AmgHierarchy amg_setup(const Csr& S, const AmgOptions& o) {
     }
     std::vector<double> scaled = inverse_diagonal(F);
     for (double& v : scaled) v *= o.prolongation_damping;
+    pt.lap("tentative + filtered", lev);
     const Csr AT = spgemm(scale_rows(F, scaled), T);
+    pt.lap("spgemm A_F T", lev);
     // P = T - AT through triplets (amg.cpp:168-177): per row, T's single entry
     // and AT's entries merged by column; duplicates (<= 2) summed from 0.0.
     Csr P;
@@ -529,7 +577,9 @@ AmgHierarchy amg_setup(const Csr& S, const AmgOptions& o) {
         }
       }
     }
+    pt.lap("P merge", lev);
     Csr coarse = spgemm(transpose(P), spgemm(cur, P));  // Galerkin, amg.cpp:179
+    pt.lap("galerkin P^T A P", lev);
     h.levels.push_back({std::move(cur), std::move(P), std::move(inv_diag)});
     cur = std::move(coarse);
   }
@@ -541,6 +591,7 @@ AmgHierarchy amg_setup(const Csr& S, const AmgOptions& o) {
   h.levels.push_back({std::move(cur), Csr{}, std::move(inv_last)});
   h.coarse_chol = dense_cholesky(nc, dense);
   h.nc = nc;
+  pt.lap("coarse cholesky", static_cast<long long>(h.levels.size()) - 1);
   return h;
 }
 

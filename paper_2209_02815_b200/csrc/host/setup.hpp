@@ -65,6 +65,11 @@ Csr assemble_Q(const Mesh& mesh);
 Csr assemble_D(const Mesh& mesh);
 Csr transpose(const Csr& A);
 Csr spgemm(const Csr& A, const Csr& B);
+/// Optional device implementation of spgemm for the calling thread (same result bit for bit;
+/// set by a device context around its setup, nullptr = host).  Used for products with at
+/// least `min_products` scalar products.
+using SpgemmHook = Csr (*)(const Csr& A, const Csr& B, void* user);
+void set_spgemm_hook(SpgemmHook fn, void* user, int64_t min_products);
 Csr scale_rows(const Csr& A, const std::vector<double>& s);
 std::vector<double> diagonal(const Csr& A);
 double symmetry_error(const Csr& A);
