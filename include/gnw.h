@@ -128,13 +128,18 @@ void gnw_destroy(gnw_ctx* ctx);
 gnw_status gnw_set_pointer_mode(gnw_ctx* ctx, int mode);
 gnw_status gnw_set_coarse_mode(gnw_ctx* ctx, int mode);
 gnw_status gnw_set_preconditioner(gnw_ctx* ctx, int kind);
-/* MINRES loop schedule.  GNW_LOOP_REFERENCE (default) evaluates A zhat exactly as
+/* MINRES loop schedule.  GNW_LOOP_REFERENCE evaluates A zhat exactly as
  * SaddleOperator::apply does (J zhat2, then J^T u: two sweeps over J).
- * GNW_LOOP_FUSED uses the Woodbury identity J P22^-1 v2 = C^-1 H^T v2 = t': the
- * preconditioner's sweep over H also forms q = J^T t', and the next operator
+ * GNW_LOOP_FUSED uses the Woodbury identity J P22^-1 v2 = C^-1 H^T v2 = t':
+ * the preconditioner's sweep over H also forms q = J^T t', and the next operator
  * takes J^T u = q / gamma, so J is swept once per iteration instead of twice.
- * Same operator in exact arithmetic; rounding differs. */
-enum { GNW_LOOP_REFERENCE = 0, GNW_LOOP_FUSED = 1 };
+ * Same operator in exact arithmetic; rounding differs.  If a true-residual
+ * check (minres.cpp:108-120) fails in fused mode, the solve restarts from the current
+ * x on the reference schedule (gnw_stats.loop_restarts counts these).  Partitioned
+ * contexts and the Laplace-only preconditioner always run the reference schedule.
+ * GNW_LOOP_AUTO (default): fused for solves with tol >= 1e-8, the reference schedule
+ * below (where the fused rounding can move the stopping iteration by more than one). */
+enum { GNW_LOOP_REFERENCE = 0, GNW_LOOP_FUSED = 1, GNW_LOOP_AUTO = 2 };
 gnw_status gnw_set_loop_mode(gnw_ctx* ctx, int mode);
 
 gnw_status gnw_assemble(gnw_ctx* ctx, const gnw_mesh* mesh, const gnw_amg_options* opts);
@@ -241,6 +246,8 @@ typedef struct gnw_stats {
   double t_rhs;
   uint64_t kernel_launches; /* kernels launched by the last solve (graph nodes x iterations) */
   uint64_t setup_kernel_launches;
+  uint64_t loop_restarts;   /* fused-loop solves restarted on the reference schedule (lifetime) */
+  uint64_t fused_iterations; /* of the last solve's iterations, run on the fused schedule */
 } gnw_stats;
 gnw_status gnw_get_stats(const gnw_ctx* ctx, gnw_stats* stats);
 
@@ -261,9 +268,12 @@ enum {
   GNW_K_VCYCLE = 4,        /* one single-RHS V-cycle (all its kernels) */
   GNW_K_UPDATE = 5,        /* w/u/x/r recurrences */
   GNW_K_DGEMM = 6,         /* capacitance DGEMM (DMMA), flops */
-  GNW_K_ITERATION = 7,     /* one full MINRES iteration (graph body, replayed by the kernels) */
-  GNW_K_BODY = 8           /* the loop body captured once and replayed without loop control;
+  GNW_K_ITERATION = 7,     /* one full MINRES iteration of the last solve (t_minres / iterations; bytes of
+                              the schedule it ran: GNW_LOOP_FUSED iterations skip one sweep over J) */
+  GNW_K_BODY = 8,          /* the loop body captured once and replayed without loop control;
                               env GNW_EXP_SKIP (bit mask) leaves parts out, for attribution only */
+  GNW_K_SADDLE_FUSED = 9,  /* saddle operator taking J^T u = q from the preconditioner sweep (fused) */
+  GNW_K_FINISH_FUSED = 10  /* finish_prec that also forms q = J^T t' (fused: sweeps H and J) */
 };
 gnw_status gnw_profile_kernel(gnw_ctx* ctx, int kernel, int reps, double* seconds_per_launch,
                               double* algorithmic_per_launch);

@@ -44,6 +44,7 @@ Context::Context(int device) : device_(device) {
   sm_count_ = prop.multiProcessorCount;
   if (const char* e = std::getenv("GNW_PAD")) pad_ = std::max(0LL, std::atoll(e) / 2 * 2);
   if (const char* e = std::getenv("GNW_NO_GRAPH")) no_graph_ = std::atoi(e) != 0;
+  if (const char* e = std::getenv("GNW_LOOP_MODE")) fused_ = std::min(2, std::max(0, std::atoi(e)));  // gnw.h GNW_LOOP_*
   if (const char* e = std::getenv("GNW_FORK_VCYCLE")) fork_ = std::atoi(e) != 0;
   if (const char* e = std::getenv("GNW_RG_RESERVE")) rg_reserve_ = std::max(0, std::atoi(e));
   // A blocking stream: ordered with the legacy default stream, so device-pointer
@@ -109,10 +110,13 @@ void Context::require_mixed() const {
 }
 
 void Context::destroy_graph() {
-  if (graph_exec_) cudaGraphExecDestroy(graph_exec_);
-  if (graph_) cudaGraphDestroy(graph_);
-  graph_exec_ = nullptr;
-  graph_ = nullptr;
+  for (int k = 0; k < 2; ++k) {
+    if (graph_exec_[k]) cudaGraphExecDestroy(graph_exec_[k]);
+    if (graph_[k]) cudaGraphDestroy(graph_[k]);
+    graph_exec_[k] = nullptr;
+    graph_[k] = nullptr;
+    graph_nodes_[k] = 0;
+  }
 }
 
 // ---------------------------------------------------------------- assembly
@@ -593,7 +597,7 @@ void Context::operator_into(VSel x, int scaled, VSel y, MinresState* st, int loo
   if (!(exp_skip_ & 2)) saddle_operator(op, x, scaled, u_, y, st, loop, opart_, counters_ + 1, stream_);
 }
 
-bool Context::fused_active() const { return fused_ && !comm_ && m_ > 0 && pa_.m > 0 && dq_ != nullptr; }
+bool Context::fused_active() const { return fused_ && !fused_off_ && !comm_ && m_ > 0 && pa_.m > 0 && dq_ != nullptr; }
 
 void Context::apply_operator(const double* x, double* y) {
   require_mixed();
@@ -714,7 +718,11 @@ void Context::launch_iteration(unsigned long long cond_handle, int use_cond) {
 }
 
 void Context::build_graph() {
-  destroy_graph();
+  const int slot = fused_active() ? 1 : 0;
+  if (graph_exec_[slot]) cudaGraphExecDestroy(graph_exec_[slot]);
+  if (graph_[slot]) cudaGraphDestroy(graph_[slot]);
+  graph_exec_[slot] = nullptr;
+  graph_[slot] = nullptr;
   cudaGraph_t g;
   GNW_CUDA_CHECK(cudaGraphCreate(&g, 0));
   cudaGraphConditionalHandle h;
@@ -741,9 +749,9 @@ void Context::build_graph() {
     throw;
   }
   GNW_CUDA_CHECK(cudaStreamEndCapture(stream_, &body));
-  graph_nodes_ = launch_count() - l0;
-  GNW_CUDA_CHECK(cudaGraphInstantiate(&graph_exec_, g, 0));
-  graph_ = g;
+  graph_nodes_[slot] = launch_count() - l0;
+  GNW_CUDA_CHECK(cudaGraphInstantiate(&graph_exec_[slot], g, 0));
+  graph_[slot] = g;
 }
 
 MinresResult Context::minres(const double* b, const double* x0, double* x, double tol, uint64_t maxit) {
@@ -754,7 +762,8 @@ MinresResult Context::minres(const double* b, const double* x0, double* x, doubl
   const cudaStream_t s = stream_;
   MinresResult res;
   const uint64_t l0 = launch_count();
-  uint64_t graph_iters = 0;
+  uint64_t graph_launched = 0;  // kernels run inside loop-graph launches
+  uint64_t fused_iters = 0;     // iterations run on the fused schedule
   uint64_t built_now = 0;
 
   const long long cap = static_cast<long long>(std::min<uint64_t>(maxit, 4u << 20)) + 1;
@@ -794,7 +803,7 @@ MinresResult Context::minres(const double* b, const double* x0, double* x, doubl
     t_minres = ms * 1e-3;
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
-    launches = launch_count() - l0 - built_now + graph_iters * graph_nodes_;
+    launches = launch_count() - l0 - built_now + graph_launched;
     stage_out(x, x_, n);
   };
   if (bnorm == 0.0) {  // minres.cpp:32-39
@@ -804,14 +813,27 @@ MinresResult Context::minres(const double* b, const double* x0, double* x, doubl
     finish();
     return res;
   }
-  // z = P^-1 r, gamma_1 (minres.cpp:44-47)
-  precondition_into(vfixed(r_), vfixed(r_ + K_), vfixed(Z_[1]), st_plain_, 0, vfixed(r_), vfixed(r_),
-                    fused_active());
-  ps = read_plain();
-  const double gamma_sq0 = ps.scratch[0];
-  if (gamma_sq0 < 0.0) throw std::runtime_error("minres: preconditioner is not positive definite");
-  const double gamma1 = std::sqrt(gamma_sq0);
-  const double rel0 = std::sqrt(ps.scratch[4]) / bnorm;  // residual kernel's ||r||^2 (scratch[4] untouched since)
+  fused_off_ = (fused_ == 2 && tol < kAutoFusedTol);  // auto: tight tolerances keep the reference schedule
+  // One MINRES cycle from r_ (minres.cpp:44-63) with iteration index j0: z = P^-1 r,
+  // gamma_1, and the initial ring vectors v_prev = 0, v_cur = r, w = u = 0 in the slots
+  // iteration j0 reads.  Returns gamma_1 (the cycle's), or throws like the reference.
+  auto start_cycle = [&](long long j0, double* gamma_out, double* rel_out) {
+    double* zc = Z_[j0 % 2];
+    precondition_into(vfixed(r_), vfixed(r_ + K_), vfixed(zc), st_plain_, 0, vfixed(r_), vfixed(r_),
+                      fused_active());
+    const MinresState q = read_plain();
+    if (q.scratch[0] < 0.0) throw std::runtime_error("minres: preconditioner is not positive definite");
+    *gamma_out = std::sqrt(q.scratch[0]);
+    *rel_out = std::sqrt(q.scratch[4]) / bnorm;  // residual kernel's ||r||^2 (scratch[4] untouched since)
+    fill_zero(V_[j0 % 3], n, s);
+    GNW_CUDA_CHECK(cudaMemcpyAsync(V_[(j0 + 1) % 3], r_, n * sizeof(double), cudaMemcpyDeviceToDevice, s));
+    for (long long k = j0; k < j0 + 2; ++k) {
+      fill_zero(W_[k % 3], n, s);
+      fill_zero(U_[k % 3], n, s);
+    }
+  };
+  double gamma1 = 0.0, rel0 = 0.0;
+  start_cycle(1, &gamma1, &rel0);
   res.hist_e.push_back(rel0);
   res.hist_p.push_back(1.0);
   if (rel0 <= tol) {
@@ -821,13 +843,6 @@ MinresResult Context::minres(const double* b, const double* x0, double* x, doubl
     return res;
   }
   if (gamma1 == 0.0) throw std::runtime_error("minres: breakdown (zero preconditioned residual, nonzero residual)");
-  // initial vectors (minres.cpp:60-63): v_prev = V[1] = 0, v_cur = V[2] = r, w/u = 0
-  fill_zero(V_[1], n, s);
-  GNW_CUDA_CHECK(cudaMemcpyAsync(V_[2], r_, n * sizeof(double), cudaMemcpyDeviceToDevice, s));
-  for (int k = 1; k < 3; ++k) {
-    fill_zero(W_[k], n, s);
-    fill_zero(U_[k], n, s);
-  }
   MinresState st;
   std::memset(&st, 0, sizeof st);
   st.gamma_prev = 1.0;
@@ -846,10 +861,15 @@ MinresResult Context::minres(const double* b, const double* x0, double* x, doubl
   *h_st_ = st;
   GNW_CUDA_CHECK(cudaMemcpyAsync(st_, h_st_, sizeof(MinresState), cudaMemcpyHostToDevice, s));
   const bool host_loop = no_graph_ || comm_ != nullptr;  // partitioned: exchanges between the phases
-  if (!graph_exec_ && !host_loop) {
-    build_graph();
-    built_now = graph_nodes_;
-  }
+  auto ensure_graph = [&]() -> cudaGraphExec_t {
+    const int slot = fused_active() ? 1 : 0;
+    if (!graph_exec_[slot]) {
+      build_graph();
+      built_now += graph_nodes_[slot];
+    }
+    return graph_exec_[slot];
+  };
+  if (!host_loop) ensure_graph();
   std::vector<std::pair<uint64_t, double>> overrides;  // verified residuals replace recurred ones
   auto true_residual_rel = [&](double* rout) {
     operator_into(vfixed(x_), 0, vfixed(tmp2_), st_plain_, 0);
@@ -862,17 +882,22 @@ MinresResult Context::minres(const double* b, const double* x0, double* x, doubl
     MinresState cur;
     if (h_st_->status == kRunning && host_loop) {  // host-driven loop (profiling, partitioned): one sync per iteration
       host_j_ = h_st_->j;
+      if (fused_active()) ++fused_iters;
       launch_iteration(0, 0);
       GNW_CUDA_CHECK(cudaMemcpyAsync(h_st_, st_, sizeof(MinresState), cudaMemcpyDeviceToHost, s));
       sync();
       if (h_st_->status == kRunning) continue;
     } else if (h_st_->status == kRunning) {
-      GNW_CUDA_CHECK(cudaGraphLaunch(graph_exec_, s));
+      const long long it0 = h_st_->iterations;
+      const cudaGraphExec_t ge = ensure_graph();
+      const uint64_t nodes = graph_nodes_[fused_active() ? 1 : 0];
+      GNW_CUDA_CHECK(cudaGraphLaunch(ge, s));
       GNW_CUDA_CHECK(cudaMemcpyAsync(h_st_, st_, sizeof(MinresState), cudaMemcpyDeviceToHost, s));
       sync();
+      graph_launched += static_cast<uint64_t>(h_st_->iterations - it0) * nodes;  // direct launches count as issued
+      if (fused_active()) fused_iters += static_cast<uint64_t>(h_st_->iterations - it0);
     }
     cur = *h_st_;
-    graph_iters = host_loop ? 0 : static_cast<uint64_t>(cur.iterations);  // direct launches are counted as issued
     switch (cur.status) {
       case kErrNotPD: throw std::runtime_error("minres: preconditioner is not positive definite");
       case kErrStagnated: throw std::runtime_error("minres: breakdown (stagnated rotation)");
@@ -883,6 +908,29 @@ MinresResult Context::minres(const double* b, const double* x0, double* x, doubl
           res.converged = true;
           res.true_rel = rel_true;
           done = true;
+          break;
+        }
+        if (fused_active()) {
+          // The fused schedule's A zhat comes from the Woodbury identity, whose rounding
+          // grows like 1/beta; when that drift keeps the true residual above 10 tol, the
+          // solve restarts from x on the reference schedule (r = b - A x is in r_).
+          fused_off_ = true;
+          ++loop_restarts;
+          const long long j0 = cur.j + 1;
+          double g1 = 0.0, rr = 0.0;
+          start_cycle(j0, &g1, &rr);
+          if (g1 == 0.0) throw std::runtime_error("minres: breakdown (zero preconditioned residual, nonzero residual)");
+          MinresState st2 = cur;  // keeps gamma1, bnorm, tol, exhausted_tol, maxit, iterations
+          st2.gamma_prev = 1.0;
+          st2.gamma_cur = g1;
+          st2.c_prev = st2.c_cur = 1.0;
+          st2.s_prev = st2.s_cur = 0.0;
+          st2.eta = g1;
+          st2.inv_gamma = 1.0 / g1;
+          st2.j = j0;
+          st2.status = j0 > st2.maxit ? kMaxit : kRunning;
+          *h_st_ = st2;
+          GNW_CUDA_CHECK(cudaMemcpyAsync(st_, h_st_, sizeof(MinresState), cudaMemcpyHostToDevice, s));
           break;
         }
         if (cur.gamma_next <= cur.exhausted_tol) {
@@ -915,6 +963,7 @@ MinresResult Context::minres(const double* b, const double* x0, double* x, doubl
   }
   res.iterations = static_cast<uint64_t>(h_st_->iterations);
   last_iterations = res.iterations;
+  last_fused_iters_ = std::min<uint64_t>(fused_iters, res.iterations);
   const uint64_t nh = std::min<uint64_t>(res.iterations + 1, static_cast<uint64_t>(hist_cap_));
   std::vector<double> he(nh), hp(nh);
   GNW_CUDA_CHECK(cudaMemcpyAsync(he.data(), hist_e_, nh * sizeof(double), cudaMemcpyDeviceToHost, s));
@@ -992,6 +1041,10 @@ void Context::profile_kernel(int kernel, int reps, double* seconds, double* algo
     case 4: alg = bv; break;
     case 5: alg = 96 * (K + N); break;
     case 6: alg = 2.0 * m * m * N; break;
+    case 9: alg = (12 * nnzQ + 4 * (K + 1)) + (12 * nnzD + 4 * (K + 1)) + (12 * nnzD + 4 * (N + 1)) + 8 * N +
+                  16 * (K + N);
+      break;
+    case 10: alg = 16 * hm * N + 32 * N + 8 * hm; break;
     case 7:
     case 8:
       alg = 16 * m * N + 16 * hm * N + (12 * nnzQ + 4 * (K + 1)) + 2 * (12 * nnzD + 4 * (N + 1)) + bv +
@@ -999,7 +1052,11 @@ void Context::profile_kernel(int kernel, int reps, double* seconds, double* algo
       break;
     default: throw std::invalid_argument("gnw_profile_kernel: unknown kernel");
   }
+  if (kernel == 7 && last_iterations)  // fused iterations skip the J zhat2 sweep (GNW_LOOP_FUSED)
+    alg -= 8 * m * N * static_cast<double>(last_fused_iters_) / static_cast<double>(last_iterations);
   *algorithmic = alg;
+  if ((kernel == 9 || kernel == 10) && !(m_ > 0 && pa_.m > 0 && dq_))
+    throw std::invalid_argument("gnw_profile_kernel: the fused kernels need a Woodbury Jacobian");
   if (kernel == 7) {
     *seconds = last_iterations ? t_minres / static_cast<double>(last_iterations) : 0.0;
     return;
@@ -1069,6 +1126,20 @@ void Context::profile_kernel(int kernel, int reps, double* seconds, double* algo
                       vfixed(io_a_), vfixed(io_c_), io_d_, tmp_, st_plain_, nullptr, nullptr, 0, upart_, counters_ + 4,
                       0, 2, s);
         break;
+      case 9: {
+        OperatorArgs op = op_;
+        op.q = dq_;
+        saddle_operator(op, vfixed(io_a_), 0, u_, vfixed(io_b_), st_plain_, 0, opart_, counters_ + 1, s);
+        break;
+      }
+      case 10: {
+        PrecArgs pa = pa_;
+        pa.J = dJ_;
+        pa.q = dq_;
+        finish_precondition(pa, svc_, t2_, vfixed(io_a_), vfixed(io_b_), 0, st_plain_, cpart_, n_comb_blocks_, fpart_,
+                            counters_ + 3, s);
+        break;
+      }
       case 6: capacitance_dgemm(dJ_, ldj_, dHt_ ? dHt_ : dJ_, dHt_ ? ldh_ : ldj_, static_cast<int>(m_), N_, beta_, plan, part, dC_ ? dC_ : io_d_, s); break;
     }
   };

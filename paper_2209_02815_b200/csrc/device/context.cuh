@@ -64,11 +64,11 @@ class Context {
   int coarse_mode = 0;
   int pc_laplace = 0;  // GnAlgorithm::kLaplaceMinres (inversion.cpp:251-256)
   // Woodbury-fused MINRES loop: J^T u from the preconditioner sweep
-  void set_fused(int on) {
-    if ((on != 0) != (fused_ != 0)) destroy_graph();
-    fused_ = on != 0;
-  }
+  // 0 reference schedule, 1 fused, 2 auto: fused when the solve's tol >= kAutoFusedTol
+  static constexpr double kAutoFusedTol = 1e-8;
+  void set_fused(int mode) { fused_ = mode; }
   int fused() const { return fused_; }
+  uint64_t loop_restarts = 0;  // fused-loop solves restarted on the reference schedule
   void set_coarse(int mode) {
     if (mode != coarse_mode) destroy_graph();  // the loop graph bakes the kernel choice
     coarse_mode = mode;
@@ -91,6 +91,7 @@ class Context {
   double event_elapsed(int a, int b);
   void profile_kernel(int kernel, int reps, double* seconds, double* algorithmic);
   uint64_t last_iterations = 0;
+  uint64_t last_fused_iters_ = 0;  // of last_iterations, run on the fused schedule
 
   // Cell-partitioned multi-GPU mode (comm.cuh); set before assemble.  J and
   // the right-hand side's J^T term then cover only this rank's cells [c_lo, c_hi): set_jacobian
@@ -223,11 +224,13 @@ class Context {
   double* dq_ = nullptr;       // q = J^T t' (fused loop), N
   long long ldh_ = 0, ldj_ = 0;  // row strides of Ht / J on device
   long long pad_ = 64;           // row padding (doubles) of owned m x N matrices (env GNW_PAD)
-  int fused_ = 0;
+  int fused_ = 2;
   bool j_borrowed_ = false;  // device-pointer J referenced, not copied (SaddleOperator holds a pointer)
-  cudaGraph_t graph_ = nullptr;
-  cudaGraphExec_t graph_exec_ = nullptr;
-  uint64_t graph_nodes_ = 0;
+  // loop graphs per schedule: [0] reference, [1] fused (built on first use)
+  cudaGraph_t graph_[2] = {};
+  cudaGraphExec_t graph_exec_[2] = {};
+  uint64_t graph_nodes_[2] = {};
+  bool fused_off_ = false;  // this solve restarted on the reference schedule (minres)
   int n_comb_blocks_ = 0;
 
   // partitioned mode

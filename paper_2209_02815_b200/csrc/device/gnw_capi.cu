@@ -120,7 +120,7 @@ gnw_status gnw_set_preconditioner(gnw_ctx* ctx, int kind) {
 
 gnw_status gnw_set_loop_mode(gnw_ctx* ctx, int mode) {
   return guard([&] {
-    if (mode != GNW_LOOP_REFERENCE && mode != GNW_LOOP_FUSED) throw std::invalid_argument("gnw_set_loop_mode: bad mode");
+    if (mode != GNW_LOOP_REFERENCE && mode != GNW_LOOP_FUSED && mode != GNW_LOOP_AUTO) throw std::invalid_argument("gnw_set_loop_mode: bad mode");
     ctx_of(ctx).set_fused(mode);
   });
 }
@@ -398,6 +398,8 @@ gnw_status gnw_get_stats(const gnw_ctx* ctx, gnw_stats* stats) {
     stats->t_rhs = c.t_rhs;
     stats->kernel_launches = c.launches;
     stats->setup_kernel_launches = c.setup_launches;
+    stats->loop_restarts = c.loop_restarts;
+    stats->fused_iterations = c.last_fused_iters_;
   });
 }
 

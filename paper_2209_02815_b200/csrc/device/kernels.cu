@@ -102,6 +102,43 @@ __device__ __forceinline__ double col_dot(const double* __restrict__ p, long lon
   for (; i < m; ++i) acc = acc + __ldg(p + static_cast<long long>(i) * ld) * s[i];
   return acc;
 }
+// Two column dots over the same s in one sweep (fused loop: w = (H t')_c and q_c = (J^T t')_c),
+// each in ascending i; the batch's loads of both columns are issued before the adds.
+template <int B>
+__device__ __forceinline__ void col_dot2(const double* __restrict__ p, long long ldp, const double* __restrict__ r,
+                                         long long ldr, const double* s, int m, double& accp, double& accr) {
+  static_assert(B % 8 == 0, "batch is a multiple of 8");
+  double ap = 0.0, ar = 0.0;
+  int i = 0;
+  for (; i + B <= m; i += B) {
+    double v[B], w[B];
+    if constexpr (B % 16 == 0) {
+#pragma unroll
+      for (int k = 0; k < B; k += 16) {
+        ld16_strided(v + k, p + static_cast<long long>(i + k) * ldp, ldp * 8);
+        ld16_strided(w + k, r + static_cast<long long>(i + k) * ldr, ldr * 8);
+      }
+    } else {
+#pragma unroll
+      for (int k = 0; k < B; k += 8) {
+        ld8_strided(v + k, p + static_cast<long long>(i + k) * ldp, ldp * 8);
+        ld8_strided(w + k, r + static_cast<long long>(i + k) * ldr, ldr * 8);
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < B; ++k) {
+      ap = ap + v[k] * s[i + k];
+      ar = ar + w[k] * s[i + k];
+    }
+  }
+  for (; i < m; ++i) {
+    ap = ap + __ldg(p + static_cast<long long>(i) * ldp) * s[i];
+    ar = ar + __ldg(r + static_cast<long long>(i) * ldr) * s[i];
+  }
+  accp = ap;
+  accr = ar;
+}
+
 constexpr int kTpb = 256;
 constexpr int kRowsPerWarp = 4;                           // row GEMV: rows per warp
 constexpr int kRowsPerCta = kRowsPerWarp * (kTpb / 32);  // row GEMV: rows per CTA
@@ -766,14 +803,8 @@ __global__ void __launch_bounds__(kTpb) k_finish_prec(PrecArgs pa, const double*
       double w = 0.0;
       const double* __restrict__ Hc = pa.Ht + (c - pa.c_lo);
       if (pa.q != nullptr) {  // one sweep over H and J: w = (H t')_c, q_c = (J^T t')_c
-        const double* __restrict__ Jc = pa.J + c;
         double qq = 0.0;
-#pragma unroll 8
-        for (int q = 0; q < pa.m; ++q) {
-          const double tq = tsm[q];
-          w = w + __ldg(Hc + static_cast<long long>(q) * pa.ldh) * tq;
-          qq = qq + __ldg(Jc + static_cast<long long>(q) * pa.ldj) * tq;
-        }
+        col_dot2<8>(Hc, pa.ldh, pa.J + c, pa.ldj, tsm, pa.m, w, qq);  // 16 loads in flight (32 at B = 16 spill residency)
         pa.q[c] = qq;
       } else {
         w = col_dot<B>(Hc, pa.ldh, tsm, pa.m);

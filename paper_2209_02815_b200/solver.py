@@ -106,9 +106,13 @@ class Context:
         A.check(self.L.gnw_set_pointer_mode(self.h, A.GNW_DEVICE_POINTERS if on else A.GNW_HOST_POINTERS))
         self.device_pointers = on
 
-    def set_loop_mode(self, fused: bool):
-        """GNW_LOOP_FUSED: one sweep over J per MINRES iteration (Woodbury identity); see gnw.h."""
-        A.check(self.L.gnw_set_loop_mode(self.h, 1 if fused else 0))
+    def set_loop_mode(self, mode):
+        """MINRES loop schedule (gnw.h): False / "reference" = SaddleOperator::apply's two sweeps
+        over J; True / "fused" = one sweep (Woodbury identity); "auto" (the default) = fused
+        for tol >= 1e-8, reference below."""
+        modes = {False: A.GNW_LOOP_REFERENCE, True: A.GNW_LOOP_FUSED, "reference": A.GNW_LOOP_REFERENCE,
+                 "fused": A.GNW_LOOP_FUSED, "auto": A.GNW_LOOP_AUTO}
+        A.check(self.L.gnw_set_loop_mode(self.h, modes[mode]))
 
     def set_coarse_mode(self, exact: bool):
         A.check(self.L.gnw_set_coarse_mode(self.h, A.GNW_COARSE_CHOLESKY if exact else A.GNW_COARSE_INVERSE))

@@ -18,6 +18,7 @@ def problem(n=32, m=16, index=0):
 
 def single(inp, alpha, tol):
     c = Context(0)
+    c.set_loop_mode(False)  # partitioned contexts run the reference schedule
     c.assemble(inp.mesh)
     c.set_jacobian(inp.J, alpha)
     b = c.assemble_rhs(inp.dm, np.zeros(c.N), inp.dg, np.zeros(inp.J.shape[0]))

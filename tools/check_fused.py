@@ -42,18 +42,19 @@ for a in cfg.alphas:
         ctx.set_jacobian(J, a)
         b = ctx.assemble_rhs(dm, zN, dg, zm)
         for tol in (1e-8, 1e-12):
-            mi = 400 if tol < 1e-9 else None  # tol 1e-12 can stagnate above tol at small alpha
-            ctx.minres(b, tol=tol, maxit=mi)  # warm
+            ctx.minres(b, tol=tol)  # warm
             torch.cuda.synchronize()
+            r0 = ctx.stats()["loop_restarts"]
             t0 = time.perf_counter()
-            x, rep = ctx.minres(b, tol=tol, maxit=mi)
+            x, rep = ctx.minres(b, tol=tol)
             torch.cuda.synchronize()
             dt = time.perf_counter() - t0
+            rep.restarts = ctx.stats()["loop_restarts"] - r0
             out[(fused, tol)] = (x.cpu().numpy(), rep, dt)
     for tol in (1e-8, 1e-12):
         xr, rr, tr = out[(False, tol)]
         xf, rf, tf = out[(True, tol)]
         d = np.linalg.norm(xr - xf) / np.linalg.norm(xr)
         print(f"alpha={a:g} tol={tol:g}: ref-loop {rr.iterations} it {1e3 * tr:.1f} ms true {rr.true_relative_residual:.2e} | "
-              f"fused {rf.iterations} it {1e3 * tf:.1f} ms true {rf.true_relative_residual:.2e} | rel diff {d:.2e}"
+              f"fused {rf.iterations} it ({rf.restarts} restarts) {1e3 * tf:.1f} ms true {rf.true_relative_residual:.2e} | rel diff {d:.2e}"
               + (f" | reference {ref[a]}" if tol == 1e-8 and a in ref else ""), flush=True)
