@@ -159,7 +159,8 @@ def c2_reference_record():
 # CUDA kernel behind each gnw_profile_kernel name
 KERNEL_NAMES = {"row_gemv": "k_row_gemv", "saddle": "k_saddle", "saddle_fused": "k_saddle (q from the finish sweep)",
                 "finish_prec": "k_finish_prec", "finish_fused": "k_finish_prec (+ q = J^T t')",
-                "vcycle": "V-cycle", "update": "k_minres_update"}
+                "vcycle": "V-cycle", "update": "k_minres_update", "col_sweep": "k_col_sweep (q = J^T t')",
+                "finish_lean": "k_finish_prec (w = B q)"}
 
 
 def cpu_sample(cfg, inp, alpha, iterations, k_cols=16, k_rows=16, k_iters=10, label="C2"):
@@ -346,12 +347,16 @@ def run_gnw(args):
     ctx.set_jacobian(J_d, 1e-2)
     b = ctx.assemble_rhs(dm_d, zN, dg_d, zm)
     ctx.minres(b, tol=tol)
-    fused = ctx.stats()["fused_iterations"] > 0  # GNW_LOOP_AUTO runs tol 1e-8 on the fused schedule
+    fused = ctx.stats()["fused_iterations"] > 0  # GNW_LOOP_AUTO runs tol 1e-8 on the fused/lean schedule
+    lean = fused and ctx.loop_schedule() == "lean"
     kern = {}
     # launches per MINRES iteration: k_row_gemv runs twice (J zhat2 and, inside
     # combine_prec, H^T v2); everything else once.  The fused schedule drops the J zhat2
     # GEMV and the saddle's J^T u sweep; its finish sweep reads H and J (q = J^T t').
-    if fused:
+    if lean:  # H t' = B (J^T t'): a column sweep over J and a second V-cycle replace the H t sweep
+        per_iter = {"row_gemv": 1, "saddle_fused": 1, "combine_prec": 1, "col_sweep": 1, "finish_lean": 1,
+                    "vcycle": 2, "update": 1}
+    elif fused:
         per_iter = {"row_gemv": 1, "saddle_fused": 1, "combine_prec": 1, "finish_fused": 1, "vcycle": 1, "update": 1}
     else:
         per_iter = {"row_gemv": 2, "saddle": 1, "combine_prec": 1, "finish_prec": 1, "vcycle": 1, "update": 1}
@@ -362,9 +367,11 @@ def run_gnw(args):
     it_sec, it_bytes = ctx.profile_kernel("iteration")
     dg_sec, dg_flops = ctx.profile_kernel("dgemm", reps=5)
     # share of one iteration per kernel KIND (k_row_gemv: its own J pass + the H^T pass of combine_prec)
-    sad, fin = ("saddle_fused", "finish_fused") if fused else ("saddle", "finish_prec")
+    sad, fin = ("saddle_fused", "finish_lean" if lean else "finish_fused") if fused else ("saddle", "finish_prec")
     kind_ms = {"row_gemv": per_iter["row_gemv"] * kern["row_gemv"]["ms"], sad: kern[sad]["ms"],
-               fin: kern[fin]["ms"], "vcycle": kern["vcycle"]["ms"], "update": kern["update"]["ms"]}
+               fin: kern[fin]["ms"], "vcycle": per_iter["vcycle"] * kern["vcycle"]["ms"], "update": kern["update"]["ms"]}
+    if lean:
+        kind_ms["col_sweep"] = kern["col_sweep"]["ms"]
     dom = max(kind_ms, key=kind_ms.get)
     for k, v in kind_ms.items():
         kern[k]["iteration_share"] = v / (it_sec * 1e3) if it_sec else None
@@ -448,7 +455,7 @@ def run_gnw(args):
                        "amg_levels": info["n_levels"], "coarse_n": info["coarse_n"],
                        "jacobian": ert if ert else "synthetic U diag(10^(-4k/m)) V^T (workload.py)"},
             "roofline": {"bound": "hbm", "kernel": KERNEL_NAMES.get(dom, "k_" + dom),
-                         "loop_schedule": "fused (GNW_LOOP_AUTO at tol >= 1e-8)" if fused else "reference", "achieved": kern[dom]["GBps"], "peak": hbm_peak,
+                         "loop_schedule": ctx.loop_schedule() + (" (GNW_LOOP_AUTO at tol >= 1e-8)" if fused else ""), "achieved": kern[dom]["GBps"], "peak": hbm_peak,
                          "unit": "GB/s", "frac": kern[dom]["frac"], "traffic": traffic,
                          "peak_source": peak_src,
                          "algorithmic_bytes_per_launch": kern[dom]["GB"] * 1e9,

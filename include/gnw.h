@@ -137,9 +137,14 @@ gnw_status gnw_set_preconditioner(gnw_ctx* ctx, int kind);
  * check (minres.cpp:108-120) fails in fused mode, the solve restarts from the current
  * x on the reference schedule (gnw_stats.loop_restarts counts these).  Partitioned
  * contexts and the Laplace-only preconditioner always run the reference schedule.
- * GNW_LOOP_AUTO (default): fused for solves with tol >= 1e-8, the reference schedule
- * below (where the fused rounding can move the stopping iteration by more than one). */
-enum { GNW_LOOP_REFERENCE = 0, GNW_LOOP_FUSED = 1, GNW_LOOP_AUTO = 2 };
+ * GNW_LOOP_LEAN goes one step further: since H = B J^T and the V-cycle B is linear,
+ * H t' = B (J^T t'); the preconditioner forms q = J^T t' by one sweep over J and applies a
+ * second V-cycle to it, so H is swept once per iteration (H^T v2) and J once (q): two dense
+ * sweeps instead of four, for one extra V-cycle.
+ * GNW_LOOP_AUTO (default): for solves with tol >= 1e-8, lean when a sweep over J moves more
+ * bytes than two V-cycles (else fused); the reference schedule below 1e-8 (where the
+ * identity's rounding can move the stopping iteration by more than one). */
+enum { GNW_LOOP_REFERENCE = 0, GNW_LOOP_FUSED = 1, GNW_LOOP_AUTO = 2, GNW_LOOP_LEAN = 3 };
 gnw_status gnw_set_loop_mode(gnw_ctx* ctx, int mode);
 
 gnw_status gnw_assemble(gnw_ctx* ctx, const gnw_mesh* mesh, const gnw_amg_options* opts);
@@ -247,7 +252,8 @@ typedef struct gnw_stats {
   uint64_t kernel_launches; /* kernels launched by the last solve (graph nodes x iterations) */
   uint64_t setup_kernel_launches;
   uint64_t loop_restarts;   /* fused-loop solves restarted on the reference schedule (lifetime) */
-  uint64_t fused_iterations; /* of the last solve's iterations, run on the fused schedule */
+  uint64_t fused_iterations; /* of the last solve's iterations, run on the fused or lean schedule */
+  uint64_t lean_iterations;  /* of those, on the lean schedule */
 } gnw_stats;
 gnw_status gnw_get_stats(const gnw_ctx* ctx, gnw_stats* stats);
 
@@ -273,7 +279,9 @@ enum {
   GNW_K_BODY = 8,          /* the loop body captured once and replayed without loop control;
                               env GNW_EXP_SKIP (bit mask) leaves parts out, for attribution only */
   GNW_K_SADDLE_FUSED = 9,  /* saddle operator taking J^T u = q from the preconditioner sweep (fused) */
-  GNW_K_FINISH_FUSED = 10  /* finish_prec that also forms q = J^T t' (fused: sweeps H and J) */
+  GNW_K_FINISH_FUSED = 10, /* finish_prec that also forms q = J^T t' (fused: sweeps H and J) */
+  GNW_K_COL_SWEEP = 11,    /* q = J^T t' alone (lean schedule) */
+  GNW_K_FINISH_LEAN = 12   /* finish_prec taking H t' = B q from the second V-cycle (lean, no sweep) */
 };
 gnw_status gnw_profile_kernel(gnw_ctx* ctx, int kernel, int reps, double* seconds_per_launch,
                               double* algorithmic_per_launch);

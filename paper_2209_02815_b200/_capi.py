@@ -17,7 +17,7 @@ LIB_PATH = os.path.join(HERE, "libgnw.so")
 GNW_OK, GNW_INVALID_ARGUMENT, GNW_NUMERICAL, GNW_DEVICE = 0, 1, 2, 3
 GNW_HOST_POINTERS, GNW_DEVICE_POINTERS = 0, 1
 GNW_COARSE_INVERSE, GNW_COARSE_CHOLESKY = 0, 1
-GNW_LOOP_REFERENCE, GNW_LOOP_FUSED, GNW_LOOP_AUTO = 0, 1, 2
+GNW_LOOP_REFERENCE, GNW_LOOP_FUSED, GNW_LOOP_AUTO, GNW_LOOP_LEAN = 0, 1, 2, 3
 
 
 class GnwDeviceError(RuntimeError):
@@ -63,7 +63,8 @@ class Info(C.Structure):
 class Stats(C.Structure):
     _fields_ = [("t_minres", C.c_double), ("t_rhs", C.c_double),
                 ("kernel_launches", C.c_uint64), ("setup_kernel_launches", C.c_uint64),
-                ("loop_restarts", C.c_uint64), ("fused_iterations", C.c_uint64)]
+                ("loop_restarts", C.c_uint64), ("fused_iterations", C.c_uint64),
+                ("lean_iterations", C.c_uint64)]
 
 
 # every symbol include/gnw.h declares (checked by tests/test_capi_symbols.py)
@@ -108,7 +109,8 @@ class GnStep(C.Structure):
 
 
 KERNELS = {"row_gemv": 0, "saddle": 1, "combine_prec": 2, "finish_prec": 3, "vcycle": 4,
-           "update": 5, "dgemm": 6, "iteration": 7, "body": 8, "saddle_fused": 9, "finish_fused": 10}
+           "update": 5, "dgemm": 6, "iteration": 7, "body": 8, "saddle_fused": 9, "finish_fused": 10,
+           "col_sweep": 11, "finish_lean": 12}
 
 _lib = None
 

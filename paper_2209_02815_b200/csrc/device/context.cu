@@ -44,7 +44,9 @@ Context::Context(int device) : device_(device) {
   sm_count_ = prop.multiProcessorCount;
   if (const char* e = std::getenv("GNW_PAD")) pad_ = std::max(0LL, std::atoll(e) / 2 * 2);
   if (const char* e = std::getenv("GNW_NO_GRAPH")) no_graph_ = std::atoi(e) != 0;
-  if (const char* e = std::getenv("GNW_LOOP_MODE")) fused_ = std::min(2, std::max(0, std::atoi(e)));  // gnw.h GNW_LOOP_*
+  if (const char* e = std::getenv("GNW_LOOP_MODE")) fused_ = std::min(3, std::max(0, std::atoi(e)));  // gnw.h GNW_LOOP_*
+  if (const char* e = std::getenv("GNW_CINV_REFINE")) cinv_refine_ = std::atoi(e) != 0;
+  if (const char* e = std::getenv("GNW_AUTO_SCHED")) auto_sched_ = std::min(2, std::max(0, std::atoi(e)));
   if (const char* e = std::getenv("GNW_FORK_VCYCLE")) fork_ = std::atoi(e) != 0;
   if (const char* e = std::getenv("GNW_RG_RESERVE")) rg_reserve_ = std::max(0, std::atoi(e));
   // A blocking stream: ordered with the legacy default stream, so device-pointer
@@ -110,7 +112,7 @@ void Context::require_mixed() const {
 }
 
 void Context::destroy_graph() {
-  for (int k = 0; k < 2; ++k) {
+  for (int k = 0; k < 3; ++k) {
     if (graph_exec_[k]) cudaGraphExecDestroy(graph_exec_[k]);
     if (graph_[k]) cudaGraphDestroy(graph_[k]);
     graph_exec_[k] = nullptr;
@@ -377,6 +379,8 @@ void Context::set_jacobian(const double* J, int64_t m, int64_t n_cells, double b
     t2_ = jm.alloc<double>(m);
     tpart_ = jm.alloc<double>(static_cast<size_t>(plan_.nchunks) * m);
     dq_ = jm.alloc<double>(N_);
+    bq_ = jm.alloc<double>(N_);
+    cres_ = jm.alloc<double>(m);
     if (comm_) {
       const int P = comm_->world;
       u_part_ = jm.alloc<double>(m);
@@ -501,6 +505,7 @@ void Context::set_jacobian(const double* J, int64_t m, int64_t n_cells, double b
       if (fail) throw std::runtime_error("dense_cholesky: matrix not positive definite");
     }
     cholesky_inverse(dL_, dY_, dCinv_, static_cast<int>(m), s);
+    if (!fail) mirror_lower(dC_, static_cast<int>(m), s);  // full C for the fused loops' refinement
     GNW_CUDA_CHECK(cudaEventRecord(ev[3], s));
     sync();
   }
@@ -597,7 +602,15 @@ void Context::operator_into(VSel x, int scaled, VSel y, MinresState* st, int loo
   if (!(exp_skip_ & 2)) saddle_operator(op, x, scaled, u_, y, st, loop, opart_, counters_ + 1, stream_);
 }
 
-bool Context::fused_active() const { return fused_ && !fused_off_ && !comm_ && m_ > 0 && pa_.m > 0 && dq_ != nullptr; }
+int Context::loop_sched() const {
+  if (!fused_ || fused_off_ || comm_ || m_ == 0 || pa_.m == 0 || dq_ == nullptr) return 0;
+  if (fused_ != 2) return fused_ == 1 ? 1 : 2;
+  if (auto_sched_) return auto_sched_;
+  // auto: lean trades one dense sweep (8 m N bytes) for a second, serialised V-cycle, which
+  // runs well below the HBM roofline on small levels (latency-bound): lean when the sweep
+  // outweighs two V-cycles' bytes (C2-C5; C1 stays fused)
+  return 8.0 * static_cast<double>(m_) * static_cast<double>(N_) > 2.0 * vcycle_bytes() ? 2 : 1;
+}
 
 void Context::apply_operator(const double* x, double* y) {
   require_mixed();
@@ -611,12 +624,16 @@ void Context::apply_operator(const double* x, double* y) {
 
 // z = P^-1 y.  In the loop, y = v_next is formed on the fly from Az, v_cur, v_prev.
 void Context::precondition_into(VSel y, VSel yv2, VSel z, MinresState* st, int loop, VSel vcur, VSel vprev,
-                                bool fused) {
+                                int sched) {
   pa_.exact = coarse_mode;
   PrecArgs pa = pa_;
-  if (fused) {  // the finish sweep also forms q = J^T t' for the next operator
+  if (sched == 1) {  // fused: the finish sweep also forms q = J^T t' for the next operator
     pa.J = dJ_;
     pa.q = dq_;
+  }
+  if (sched != 0 && cinv_refine_) {
+    pa.Cfull = dC_;
+    pa.cres = cres_;
   }
   const VSel az = loop ? vfixed(az_) : y;
   if (!(exp_skip_ & 4)) combine_elem(pa, az, vcur, vprev, y, z, loop, st, cpart_, stream_);
@@ -645,7 +662,16 @@ void Context::precondition_into(VSel y, VSel yv2, VSel z, MinresState* st, int l
     row_gemv(pa.Ht, pa.m, pa.N, pa.ldh, y, pa.K, 0, st, tpart_, counters_ + 2, t_, plan_h_, stream_);
   if (!fork && !(exp_skip_ & 16)) vcycle(yv2, svc_, st);
   if (!(exp_skip_ & 32)) capacitance_solve(pa, t_, t2_, stream_);
-  if (fork) GNW_CUDA_CHECK(cudaStreamWaitEvent(stream_, fork_ev_[1], 0));
+  if (sched == 2) {
+    // lean: H t' = B J^T t' (B linear, H = B J^T), so the finish step needs no sweep over
+    // H: q = J^T t' (also the next operator's J^T u, up to 1 / gamma) and a second V-cycle
+    col_sweep(dJ_, ldj_, t2_, pa.m, N_, dq_, stream_);
+    if (fork) GNW_CUDA_CHECK(cudaStreamWaitEvent(stream_, fork_ev_[1], 0));
+    vcycle(vfixed(dq_), bq_, st);
+    pa.bq = bq_;
+  } else if (fork) {
+    GNW_CUDA_CHECK(cudaStreamWaitEvent(stream_, fork_ev_[1], 0));
+  }
   if (!(exp_skip_ & 64)) finish_precondition(pa, svc_, t2_, y, z, loop, st, cpart_, n_comb_blocks_, fpart_, counters_ + 3, stream_);
 }
 
@@ -707,10 +733,10 @@ void Context::assemble_rhs(const double* mdl, const double* mref, const double* 
 // device from st_->j.  Captured once into the conditional-WHILE graph body, or
 // launched per iteration by the host in GNW_NO_GRAPH (profiling) mode.
 void Context::launch_iteration(unsigned long long cond_handle, int use_cond) {
-  const bool fu = fused_active();
-  operator_into(ring2(Z_, 0), 1, vfixed(az_), st_, 1, fu);                  // Az = A zhat, delta
+  const int sc = loop_sched();
+  operator_into(ring2(Z_, 0), 1, vfixed(az_), st_, 1, sc != 0);             // Az = A zhat, delta
   precondition_into(ring3(V_, 2), ring3(Vk_, 2), ring2(Z_, 1), st_, 1,       // v_next, z_next = P^-1 v_next,
-                    ring3(V_, 1), ring3(V_, 0), fu);                         // gamma_next, Givens
+                    ring3(V_, 1), ring3(V_, 0), sc);                         // gamma_next, Givens
   if (!(exp_skip_ & 128))
     minres_update(K_ + N_, ring2(Z_, 0), vfixed(az_), ring3(W_, 0), ring3(W_, 1), ring3(W_, 2), ring3(U_, 0),
                   ring3(U_, 1), ring3(U_, 2), x_, r_, st_, hist_e_, hist_p_, hist_cap_, upart_, counters_ + 4,
@@ -718,7 +744,7 @@ void Context::launch_iteration(unsigned long long cond_handle, int use_cond) {
 }
 
 void Context::build_graph() {
-  const int slot = fused_active() ? 1 : 0;
+  const int slot = loop_sched();
   if (graph_exec_[slot]) cudaGraphExecDestroy(graph_exec_[slot]);
   if (graph_[slot]) cudaGraphDestroy(graph_[slot]);
   graph_exec_[slot] = nullptr;
@@ -763,7 +789,7 @@ MinresResult Context::minres(const double* b, const double* x0, double* x, doubl
   MinresResult res;
   const uint64_t l0 = launch_count();
   uint64_t graph_launched = 0;  // kernels run inside loop-graph launches
-  uint64_t fused_iters = 0;     // iterations run on the fused schedule
+  uint64_t sched_iters[3] = {0, 0, 0};  // iterations run per loop schedule
   uint64_t built_now = 0;
 
   const long long cap = static_cast<long long>(std::min<uint64_t>(maxit, 4u << 20)) + 1;
@@ -820,7 +846,7 @@ MinresResult Context::minres(const double* b, const double* x0, double* x, doubl
   auto start_cycle = [&](long long j0, double* gamma_out, double* rel_out) {
     double* zc = Z_[j0 % 2];
     precondition_into(vfixed(r_), vfixed(r_ + K_), vfixed(zc), st_plain_, 0, vfixed(r_), vfixed(r_),
-                      fused_active());
+                      loop_sched());
     const MinresState q = read_plain();
     if (q.scratch[0] < 0.0) throw std::runtime_error("minres: preconditioner is not positive definite");
     *gamma_out = std::sqrt(q.scratch[0]);
@@ -862,7 +888,7 @@ MinresResult Context::minres(const double* b, const double* x0, double* x, doubl
   GNW_CUDA_CHECK(cudaMemcpyAsync(st_, h_st_, sizeof(MinresState), cudaMemcpyHostToDevice, s));
   const bool host_loop = no_graph_ || comm_ != nullptr;  // partitioned: exchanges between the phases
   auto ensure_graph = [&]() -> cudaGraphExec_t {
-    const int slot = fused_active() ? 1 : 0;
+    const int slot = loop_sched();
     if (!graph_exec_[slot]) {
       build_graph();
       built_now += graph_nodes_[slot];
@@ -882,7 +908,7 @@ MinresResult Context::minres(const double* b, const double* x0, double* x, doubl
     MinresState cur;
     if (h_st_->status == kRunning && host_loop) {  // host-driven loop (profiling, partitioned): one sync per iteration
       host_j_ = h_st_->j;
-      if (fused_active()) ++fused_iters;
+      ++sched_iters[loop_sched()];
       launch_iteration(0, 0);
       GNW_CUDA_CHECK(cudaMemcpyAsync(h_st_, st_, sizeof(MinresState), cudaMemcpyDeviceToHost, s));
       sync();
@@ -890,12 +916,12 @@ MinresResult Context::minres(const double* b, const double* x0, double* x, doubl
     } else if (h_st_->status == kRunning) {
       const long long it0 = h_st_->iterations;
       const cudaGraphExec_t ge = ensure_graph();
-      const uint64_t nodes = graph_nodes_[fused_active() ? 1 : 0];
+      const uint64_t nodes = graph_nodes_[loop_sched()];
       GNW_CUDA_CHECK(cudaGraphLaunch(ge, s));
       GNW_CUDA_CHECK(cudaMemcpyAsync(h_st_, st_, sizeof(MinresState), cudaMemcpyDeviceToHost, s));
       sync();
       graph_launched += static_cast<uint64_t>(h_st_->iterations - it0) * nodes;  // direct launches count as issued
-      if (fused_active()) fused_iters += static_cast<uint64_t>(h_st_->iterations - it0);
+      sched_iters[loop_sched()] += static_cast<uint64_t>(h_st_->iterations - it0);
     }
     cur = *h_st_;
     switch (cur.status) {
@@ -963,7 +989,8 @@ MinresResult Context::minres(const double* b, const double* x0, double* x, doubl
   }
   res.iterations = static_cast<uint64_t>(h_st_->iterations);
   last_iterations = res.iterations;
-  last_fused_iters_ = std::min<uint64_t>(fused_iters, res.iterations);
+  for (int k = 0; k < 3; ++k) last_sched_iters_[k] = std::min<uint64_t>(sched_iters[k], res.iterations);
+  last_fused_iters_ = last_sched_iters_[1] + last_sched_iters_[2];
   const uint64_t nh = std::min<uint64_t>(res.iterations + 1, static_cast<uint64_t>(hist_cap_));
   std::vector<double> he(nh), hp(nh);
   GNW_CUDA_CHECK(cudaMemcpyAsync(he.data(), hist_e_, nh * sizeof(double), cudaMemcpyDeviceToHost, s));
@@ -1010,6 +1037,19 @@ double Context::event_elapsed(int a, int b) {
   return ms * 1e-3;
 }
 
+// B_V, the algorithmic bytes of one single-RHS V-cycle
+double Context::vcycle_bytes() const {
+  double bv = 0.0;
+  const size_t L = amg_.levels.size();
+  for (size_t l = 0; l + 1 < L; ++l) {
+    const double n = static_cast<double>(amg_.levels[l].A.n_rows);
+    const double nA = static_cast<double>(amg_.levels[l].A.nnz()), nP = static_cast<double>(amg_.levels[l].P.nnz());
+    bv += 2 * (12 * nA + 4 * (n + 1)) + 2 * (12 * nP + 4 * (n + 1)) + 16 * n + 48 * n;
+  }
+  const double nl = static_cast<double>(amg_.nc);
+  return bv + 8 * nl * nl + 32 * nl;
+}
+
 // Algorithmic traffic per launch (SURVEY.md 8(d) conventions) and isolated timing.
 void Context::profile_kernel(int kernel, int reps, double* seconds, double* algorithmic) {
   require_mixed();
@@ -1018,17 +1058,7 @@ void Context::profile_kernel(int kernel, int reps, double* seconds, double* algo
   const cudaStream_t s = stream_;
   const double K = static_cast<double>(K_), N = static_cast<double>(N_), m = static_cast<double>(m_);
   const double nnzQ = static_cast<double>(Q_.nnz()), nnzD = static_cast<double>(D_.nnz());
-  double bv = 0.0;  // B_V
-  {
-    const size_t L = amg_.levels.size();
-    for (size_t l = 0; l + 1 < L; ++l) {
-      const double n = static_cast<double>(amg_.levels[l].A.n_rows);
-      const double nA = static_cast<double>(amg_.levels[l].A.nnz()), nP = static_cast<double>(amg_.levels[l].P.nnz());
-      bv += 2 * (12 * nA + 4 * (n + 1)) + 2 * (12 * nP + 4 * (n + 1)) + 16 * n + 48 * n;
-    }
-    const double nl = static_cast<double>(amg_.nc);
-    bv += 8 * nl * nl + 32 * nl;
-  }
+  const double bv = vcycle_bytes();  // B_V
   const double hm = (pa_.m > 0) ? m : 0.0;  // H present (Woodbury)
   double alg = 0.0;
   switch (kernel) {
@@ -1045,6 +1075,8 @@ void Context::profile_kernel(int kernel, int reps, double* seconds, double* algo
                   16 * (K + N);
       break;
     case 10: alg = 16 * hm * N + 32 * N + 8 * hm; break;
+    case 11: alg = 8 * m * N + 8 * N + 8 * m; break;
+    case 12: alg = 32 * N; break;
     case 7:
     case 8:
       alg = 16 * m * N + 16 * hm * N + (12 * nnzQ + 4 * (K + 1)) + 2 * (12 * nnzD + 4 * (N + 1)) + bv +
@@ -1052,10 +1084,13 @@ void Context::profile_kernel(int kernel, int reps, double* seconds, double* algo
       break;
     default: throw std::invalid_argument("gnw_profile_kernel: unknown kernel");
   }
-  if (kernel == 7 && last_iterations)  // fused iterations skip the J zhat2 sweep (GNW_LOOP_FUSED)
-    alg -= 8 * m * N * static_cast<double>(last_fused_iters_) / static_cast<double>(last_iterations);
+  if (kernel == 7 && last_iterations) {  // schedules: fused skips the J zhat2 sweep; lean also the
+    const double it = static_cast<double>(last_iterations);  // H t sweep, for a second V-cycle
+    alg -= 8 * m * N * static_cast<double>(last_sched_iters_[1]) / it;
+    alg -= (16 * m * N - bv) * static_cast<double>(last_sched_iters_[2]) / it;
+  }
   *algorithmic = alg;
-  if ((kernel == 9 || kernel == 10) && !(m_ > 0 && pa_.m > 0 && dq_))
+  if (kernel >= 9 && kernel <= 12 && !(m_ > 0 && pa_.m > 0 && dq_))
     throw std::invalid_argument("gnw_profile_kernel: the fused kernels need a Woodbury Jacobian");
   if (kernel == 7) {
     *seconds = last_iterations ? t_minres / static_cast<double>(last_iterations) : 0.0;
@@ -1136,6 +1171,14 @@ void Context::profile_kernel(int kernel, int reps, double* seconds, double* algo
         PrecArgs pa = pa_;
         pa.J = dJ_;
         pa.q = dq_;
+        finish_precondition(pa, svc_, t2_, vfixed(io_a_), vfixed(io_b_), 0, st_plain_, cpart_, n_comb_blocks_, fpart_,
+                            counters_ + 3, s);
+        break;
+      }
+      case 11: col_sweep(dJ_, ldj_, t2_, static_cast<int>(m_), N_, dq_, s); break;
+      case 12: {
+        PrecArgs pa = pa_;
+        pa.bq = bq_;
         finish_precondition(pa, svc_, t2_, vfixed(io_a_), vfixed(io_b_), 0, st_plain_, cpart_, n_comb_blocks_, fpart_,
                             counters_ + 3, s);
         break;

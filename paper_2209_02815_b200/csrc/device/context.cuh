@@ -64,8 +64,11 @@ class Context {
   int coarse_mode = 0;
   int pc_laplace = 0;  // GnAlgorithm::kLaplaceMinres (inversion.cpp:251-256)
   // Woodbury-fused MINRES loop: J^T u from the preconditioner sweep
-  // 0 reference schedule, 1 fused, 2 auto: fused when the solve's tol >= kAutoFusedTol
+  // loop modes (gnw.h GNW_LOOP_*): 0 reference, 1 fused, 2 auto, 3 lean.  auto runs
+  // auto_sched_ when the solve's tol >= kAutoFusedTol, the reference schedule below.
   static constexpr double kAutoFusedTol = 1e-8;
+  int auto_sched_ = 0;  // schedule auto picks: 0 by sweep vs V-cycle bytes, 1 fused, 2 lean (env GNW_AUTO_SCHED)
+  double vcycle_bytes() const;
   void set_fused(int mode) { fused_ = mode; }
   int fused() const { return fused_; }
   uint64_t loop_restarts = 0;  // fused-loop solves restarted on the reference schedule
@@ -91,7 +94,8 @@ class Context {
   double event_elapsed(int a, int b);
   void profile_kernel(int kernel, int reps, double* seconds, double* algorithmic);
   uint64_t last_iterations = 0;
-  uint64_t last_fused_iters_ = 0;  // of last_iterations, run on the fused schedule
+  uint64_t last_fused_iters_ = 0;  // of last_iterations, run on the fused or lean schedule
+  uint64_t last_sched_iters_[3] = {0, 0, 0};  // of last_iterations, per schedule (reference, fused, lean)
 
   // Cell-partitioned multi-GPU mode (comm.cuh); set before assemble.  J and
   // the right-hand side's J^T term then cover only this rank's cells [c_lo, c_hi): set_jacobian
@@ -138,9 +142,11 @@ class Context {
   void upload_hierarchy();
   void vcycle(VSel r0, double* out0, const MinresState* st, cudaStream_t s = nullptr);
   void operator_into(VSel x, int scaled, VSel y, MinresState* st, int loop, bool fused = false);
+  // the current solve's loop schedule: 0 reference, 1 fused (3 dense sweeps), 2 lean (2 sweeps)
+  int loop_sched() const;
   void precondition_into(VSel y, VSel yv2, VSel z, MinresState* st, int loop, VSel vcur, VSel vprev,
-                         bool fused = false);
-  bool fused_active() const;
+                         int sched = 0);
+  bool fused_active() const { return loop_sched() != 0; }
   void build_graph();
   void launch_iteration(unsigned long long cond_handle, int use_cond);
   bool no_graph_ = false;  // env GNW_NO_GRAPH=1: host-driven loop (for ncu; kernels in conditional graphs are not listed)
@@ -222,14 +228,17 @@ class Context {
   double* dpart_ = nullptr;    // DGEMM split-K partials
   double* dnib_ = nullptr;     // device scalar -1/beta
   double* dq_ = nullptr;       // q = J^T t' (fused loop), N
+  double* bq_ = nullptr;       // B q (lean loop), N
+  double* cres_ = nullptr;     // m scratch: capacitance refinement residual
+  bool cinv_refine_ = true;    // fused/lean: refine t2 = C^-1 t once (env GNW_CINV_REFINE=0 disables)
   long long ldh_ = 0, ldj_ = 0;  // row strides of Ht / J on device
   long long pad_ = 64;           // row padding (doubles) of owned m x N matrices (env GNW_PAD)
   int fused_ = 2;
   bool j_borrowed_ = false;  // device-pointer J referenced, not copied (SaddleOperator holds a pointer)
-  // loop graphs per schedule: [0] reference, [1] fused (built on first use)
-  cudaGraph_t graph_[2] = {};
-  cudaGraphExec_t graph_exec_[2] = {};
-  uint64_t graph_nodes_[2] = {};
+  // loop graphs per schedule: [0] reference, [1] fused, [2] lean (built on first use)
+  cudaGraph_t graph_[3] = {};
+  cudaGraphExec_t graph_exec_[3] = {};
+  uint64_t graph_nodes_[3] = {};
   bool fused_off_ = false;  // this solve restarted on the reference schedule (minres)
   int n_comb_blocks_ = 0;
 

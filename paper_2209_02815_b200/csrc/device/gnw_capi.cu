@@ -120,7 +120,8 @@ gnw_status gnw_set_preconditioner(gnw_ctx* ctx, int kind) {
 
 gnw_status gnw_set_loop_mode(gnw_ctx* ctx, int mode) {
   return guard([&] {
-    if (mode != GNW_LOOP_REFERENCE && mode != GNW_LOOP_FUSED && mode != GNW_LOOP_AUTO) throw std::invalid_argument("gnw_set_loop_mode: bad mode");
+    if (mode != GNW_LOOP_REFERENCE && mode != GNW_LOOP_FUSED && mode != GNW_LOOP_AUTO &&
+        mode != GNW_LOOP_LEAN) throw std::invalid_argument("gnw_set_loop_mode: bad mode");
     ctx_of(ctx).set_fused(mode);
   });
 }
@@ -400,6 +401,7 @@ gnw_status gnw_get_stats(const gnw_ctx* ctx, gnw_stats* stats) {
     stats->setup_kernel_launches = c.setup_launches;
     stats->loop_restarts = c.loop_restarts;
     stats->fused_iterations = c.last_fused_iters_;
+    stats->lean_iterations = c.last_sched_iters_[2];
   });
 }
 

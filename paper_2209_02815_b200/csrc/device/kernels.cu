@@ -768,14 +768,63 @@ __global__ void k_cinv_apply(const double* __restrict__ Cinv, const double* __re
   if (lane == 0) t2[w] = acc[0];
 }
 
+// r = t - C t2 (warp per row, C full and symmetric)
+__global__ void k_cap_residual(const double* __restrict__ C, const double* __restrict__ t,
+                               const double* __restrict__ t2, double* __restrict__ r, int m) {
+  griddep_wait();
+  const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (w >= m) return;
+  double acc[1] = {0.0};
+  for (int j = lane; j < m; j += 32) acc[0] = acc[0] + __ldg(&C[static_cast<long long>(w) * m + j]) * t2[j];
+  warp_reduce<1>(acc);
+  if (lane == 0) r[w] = t[w] - acc[0];
+}
+
+// t2 += Cinv r (warp per row)
+__global__ void k_cinv_refine(const double* __restrict__ Cinv, const double* __restrict__ r, double* __restrict__ t2,
+                              int m) {
+  griddep_wait();
+  const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (w >= m) return;
+  double acc[1] = {0.0};
+  for (int j = lane; j < m; j += 32) acc[0] = acc[0] + __ldg(&Cinv[static_cast<long long>(w) * m + j]) * r[j];
+  warp_reduce<1>(acc);
+  if (lane == 0) t2[w] = t2[w] + acc[0];
+}
+
 void capacitance_solve(const PrecArgs& pa, const double* t, double* t2, cudaStream_t s) {
   if (pa.m == 0) return;
   if (pa.exact) {
     GNW_LAUNCH(launch_k(k_coarse_cholesky, 1, 64, 0, s, pa.Lc, pa.m, vfixed(const_cast<double*>(t)), t2, nullptr, 1, 1));
   } else {
-    GNW_LAUNCH(launch_k(k_cinv_apply, grid_for(static_cast<long long>(pa.m) * 32), kTpb, 0, s, pa.Cinv, t, t2, pa.m));
+    const unsigned g = grid_for(static_cast<long long>(pa.m) * 32);
+    GNW_LAUNCH(launch_k(k_cinv_apply, g, kTpb, 0, s, pa.Cinv, t, t2, pa.m));
+    if (pa.Cfull && pa.cres) {
+      // one step of iterative refinement: the fused/lean loops use J z2 = t2 = C^-1 t, which
+      // holds only as far as C t2 = t does; the explicit inverse alone leaves a residual
+      // ~ eps kappa(C) |t|, refinement brings it to ~ eps |C| |t2| (backward stable)
+      check_launch("capacitance_solve");
+      GNW_LAUNCH(launch_k(k_cap_residual, g, kTpb, 0, s, pa.Cfull, t, const_cast<const double*>(t2), pa.cres, pa.m));
+      check_launch("capacitance_solve");
+      GNW_LAUNCH(launch_k(k_cinv_refine, g, kTpb, 0, s, pa.Cinv, const_cast<const double*>(pa.cres), t2, pa.m));
+    }
   }
   check_launch("capacitance_solve");
+}
+
+// upper triangle of C from its lower triangle (the capacitance DGEMM computes the lower tiles)
+__global__ void k_mirror_lower(double* C, int n) {
+  griddep_wait();
+  const long long t = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (t >= static_cast<long long>(n) * n) return;
+  const int i = static_cast<int>(t / n), j = static_cast<int>(t % n);
+  if (j <= i) return;
+  C[static_cast<long long>(i) * n + j] = C[static_cast<long long>(j) * n + i];
+}
+
+void mirror_lower(double* C, int n, cudaStream_t s) {
+  GNW_LAUNCH(launch_k(k_mirror_lower, grid_for(static_cast<long long>(n) * n), kTpb, 0, s, C, n));
+  check_launch("mirror_lower");
 }
 
 __device__ void finish_scalars(const double (&tot)[3], const double* __restrict__ dots_edge, int n_edge_blocks,
@@ -791,7 +840,7 @@ __global__ void __launch_bounds__(kTpb) k_finish_prec(PrecArgs pa, const double*
   __shared__ double red[3 * (kTpb / 32)];
   const double* __restrict__ vn = vsel(vns, st);
   double* __restrict__ zn = vsel(zns, st);
-  if (pa.m > 0) {
+  if (pa.m > 0 && pa.bq == nullptr) {
     for (int t = threadIdx.x; t < pa.m; t += blockDim.x) tsm[t] = t2[t];
     __syncthreads();
   }
@@ -802,7 +851,9 @@ __global__ void __launch_bounds__(kTpb) k_finish_prec(PrecArgs pa, const double*
     if (pa.m > 0) {  // w = matvec(h_hat, t) row c (linalg.cpp:33-43); s += (-1/beta) w
       double w = 0.0;
       const double* __restrict__ Hc = pa.Ht + (c - pa.c_lo);
-      if (pa.q != nullptr) {  // one sweep over H and J: w = (H t')_c, q_c = (J^T t')_c
+      if (pa.bq != nullptr) {  // lean loop: H t' = B (J^T t'), already applied
+        w = pa.bq[c];
+      } else if (pa.q != nullptr) {  // one sweep over H and J: w = (H t')_c, q_c = (J^T t')_c
         double qq = 0.0;
         col_dot2<8>(Hc, pa.ldh, pa.J + c, pa.ldj, tsm, pa.m, w, qq);  // 16 loads in flight (32 at B = 16 spill residency)
         pa.q[c] = qq;
@@ -863,6 +914,30 @@ __device__ void finish_scalars(const double (&tot)[3], const double* __restrict_
   st->eta = -st->s_next * st->eta;
 }
 
+template <int B>
+__global__ void __launch_bounds__(kTpb) k_col_sweep(const double* __restrict__ A, long long ld,
+                                                    const double* __restrict__ t, int m, long long n,
+                                                    double* __restrict__ q) {
+  griddep_wait();
+  extern __shared__ double tsm[];
+  for (int i = threadIdx.x; i < m; i += blockDim.x) tsm[i] = t[i];
+  __syncthreads();
+  const long long c = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (c < n) q[c] = col_dot<B>(A + c, ld, tsm, m);
+}
+
+void col_sweep(const double* A, long long ld, const double* t, int m, long long n, double* q, cudaStream_t s) {
+  static const bool once = [] {  // t staged in shared memory: m <= 8192 doubles
+    cudaFuncSetAttribute(k_col_sweep<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 8192 * 8);
+    cudaFuncSetAttribute(k_col_sweep<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 8192 * 8);
+    return true;
+  }();
+  (void)once;
+  GNW_LAUNCH(launch_k(m >= kSweepBatchWideM ? k_col_sweep<16> : k_col_sweep<8>, grid_for(n), kTpb,
+                      std::max(m, 1) * sizeof(double), s, A, ld, t, m, n, q));
+  check_launch("col_sweep");
+}
+
 int finish_blocks(const PrecArgs& pa) {
   return static_cast<int>(grid_for((pa.c_hi < 0 ? pa.N : pa.c_hi) - pa.c_lo));
 }
@@ -870,6 +945,12 @@ int finish_blocks(const PrecArgs& pa) {
 void finish_precondition(const PrecArgs& pa, const double* svc, const double* t2, VSel vnext, VSel znext, int loop,
                          MinresState* st, const double* dots_edge, int n_edge_blocks, double* part,
                          unsigned* counter, cudaStream_t s) {
+  static const bool once = [] {  // t staged in shared memory: m <= 8192 doubles
+    cudaFuncSetAttribute(k_finish_prec<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 8192 * 8);
+    cudaFuncSetAttribute(k_finish_prec<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 8192 * 8);
+    return true;
+  }();
+  (void)once;
   GNW_LAUNCH(launch_k(pa.m >= kSweepBatchWideM ? k_finish_prec<16> : k_finish_prec<8>, finish_blocks(pa), kTpb,
                       std::max(pa.m, 1) * sizeof(double), s, pa, svc, t2, vnext, znext, loop, st, dots_edge,
                       n_edge_blocks, part, counter));

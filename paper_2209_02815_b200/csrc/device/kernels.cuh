@@ -145,6 +145,11 @@ struct PrecArgs {
   // fused loop: the finish pass also forms q = J^T t' (J read in the same sweep as H)
   const double* J = nullptr;
   double* q = nullptr;
+  // fused/lean loops: t2 = C^-1 t refined once against the full C (cres: m scratch)
+  const double* Cfull = nullptr;
+  double* cres = nullptr;
+  // lean loop: w = (H t')_c arrives as bq = B (J^T t') from a second V-cycle (no sweep here)
+  const double* bq = nullptr;
   // cell partition: Ht holds the columns [c_lo, c_hi); dist != 0: the finish pass only
   // writes z for those cells (no reductions -- the partitioned driver reduces after the gather)
   long long c_lo = 0, c_hi = -1;
@@ -161,6 +166,10 @@ void combine_precondition(const PrecArgs& pa, VSel az, VSel vcur, VSel vprev, VS
                           int loop, MinresState* st, double* vcopy, double* dots_part,
                           double* t_part, unsigned* counter, double* t_out, const RowGemv& plan,
                           cudaStream_t s);
+// q_c = sum_i A[i * ld + c] t[i] in ascending i for c < n (column sweep, lean loop's J^T t')
+void col_sweep(const double* A, long long ld, const double* t, int m, long long n, double* q, cudaStream_t s);
+// upper triangle of C := its lower triangle
+void mirror_lower(double* C, int n, cudaStream_t s);
 // t2 = C^-1 t (inverse apply) or the exact cholesky_solve (exact mode)
 void capacitance_solve(const PrecArgs& pa, const double* t, double* t2, cudaStream_t s);
 // z2 = s + (-1/beta) H t2; dots <z, v>, ||z||^2; last block: Givens update

@@ -111,8 +111,15 @@ class Context:
         over J; True / "fused" = one sweep (Woodbury identity); "auto" (the default) = fused
         for tol >= 1e-8, reference below."""
         modes = {False: A.GNW_LOOP_REFERENCE, True: A.GNW_LOOP_FUSED, "reference": A.GNW_LOOP_REFERENCE,
-                 "fused": A.GNW_LOOP_FUSED, "auto": A.GNW_LOOP_AUTO}
+                 "fused": A.GNW_LOOP_FUSED, "auto": A.GNW_LOOP_AUTO, "lean": A.GNW_LOOP_LEAN}
         A.check(self.L.gnw_set_loop_mode(self.h, modes[mode]))
+
+    def loop_schedule(self) -> str:
+        """The schedule most of the last solve's iterations ran: "reference", "fused" or "lean"."""
+        st = self.stats()
+        if st["lean_iterations"] > 0:
+            return "lean"
+        return "fused" if st["fused_iterations"] > 0 else "reference"
 
     def set_coarse_mode(self, exact: bool):
         A.check(self.L.gnw_set_coarse_mode(self.h, A.GNW_COARSE_CHOLESKY if exact else A.GNW_COARSE_INVERSE))

@@ -27,7 +27,9 @@ def oracle_gn(oracle, mesh, nodes, sv, g_obs, m0, **kw):
 
 
 @pytest.mark.parametrize("algorithm,mode,tol", [("woodbury", "reference", 1e-10), ("woodbury", "auto", 1e-10),
-                                                ("woodbury", "fused", 1e-8), ("laplace", "auto", 1e-10)])
+                                                ("woodbury", "fused", 1e-8), ("woodbury", "lean", 1e-8),
+                                                ("woodbury", "lean", 1e-10), ("woodbury", "fused", 1e-10),
+                                                ("laplace", "auto", 1e-10)])
 def test_gauss_newton_matches_reference(oracle, algorithm, mode, tol):
     mesh, nodes, sv, m_true, m0 = gn_case()
     p = orc.Problem.mixed(oracle, mesh)

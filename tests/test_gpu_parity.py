@@ -162,12 +162,12 @@ def test_operator_without_J_bitwise(c1, gpu_ctx_factory):
     assert np.array_equal(ctx.apply_operator(x), prob.apply_operator(x))
 
 
-@pytest.mark.parametrize("fused", [False, True], ids=["reference-schedule", "fused-schedule"])
+@pytest.mark.parametrize("mode", ["reference", "fused", "lean"])
 @pytest.mark.parametrize("alpha", [1e-4, 1e-2, 1.0])
-def test_minres_c1_parity(c1, gpu_ctx_factory, alpha, fused):
+def test_minres_c1_parity(c1, gpu_ctx_factory, alpha, mode):
     mesh, inp, prob = c1[64]
     ctx = gpu_ctx_factory(mesh)
-    ctx.set_loop_mode(fused)
+    ctx.set_loop_mode(mode)
     ctx.set_jacobian(inp.J, alpha)
     prob.set_jacobian(inp.J, alpha)
     b = prob.assemble_rhs(inp.dm, np.zeros(prob.N), inp.dg, np.zeros(inp.J.shape[0]))
@@ -183,7 +183,8 @@ def test_minres_c1_parity(c1, gpu_ctx_factory, alpha, fused):
     x12, rep12 = ctx.minres(b, tol=1e-12)
     xr12, rr12 = prob.minres(b, tol=1e-12)
     restarted = ctx.stats()["loop_restarts"] - r0
-    assert restarted == 0 or fused
+    assert restarted == 0 or mode != "reference"
+    assert ctx.loop_schedule() == mode or restarted
     assert rep12.converged and rep12.true_relative_residual <= 1e-11
     if not restarted:
         assert abs(rep12.iterations - rr12["iterations"]) <= 1
@@ -192,14 +193,15 @@ def test_minres_c1_parity(c1, gpu_ctx_factory, alpha, fused):
     assert rel(x, xr12) <= 1e-5 and rel(xr, xr12) <= 1e-5
 
 
-def test_fused_schedule_restarts_on_identity_drift(c1, gpu_ctx_factory):
-    """GNW_LOOP_FUSED takes J zhat2 from the Woodbury identity C^-1 H^T v2; its rounding
+@pytest.mark.parametrize("mode", ["fused", "lean"])
+def test_fused_schedule_restarts_on_identity_drift(c1, gpu_ctx_factory, mode):
+    """GNW_LOOP_FUSED and GNW_LOOP_LEAN take J zhat2 from the Woodbury identity C^-1 H^T v2; its rounding
     grows like 1/beta.  A tolerance below that drift fails the true-residual check
     (minres.cpp:108-120); the solve then restarts from x on the reference schedule and
     still converges to the oracle's solution.  maxit caps the total like the reference."""
     mesh, inp, prob = c1[64]
     ctx = gpu_ctx_factory(mesh)
-    ctx.set_loop_mode(True)
+    ctx.set_loop_mode(mode)
     alpha = 1e-6  # drift ~ eps / beta: above tol 1e-12
     ctx.set_jacobian(inp.J, alpha)
     prob.set_jacobian(inp.J, alpha)
@@ -207,7 +209,7 @@ def test_fused_schedule_restarts_on_identity_drift(c1, gpu_ctx_factory):
     xr, rr = prob.minres(b, tol=1e-12)
     r0 = ctx.stats()["loop_restarts"]
     x, rep = ctx.minres(b, tol=1e-12)
-    print(f"fused: {rep.iterations} it, {ctx.stats()['loop_restarts'] - r0} restarts; oracle {rr['iterations']} it")
+    print(f"{mode}: {rep.iterations} it, {ctx.stats()['loop_restarts'] - r0} restarts; oracle {rr['iterations']} it")
     assert rep.converged and rep.true_relative_residual <= 1e-11
     assert rel(x, xr) <= 1e-8
     assert len(rep.relative_residuals) == rep.iterations + 1

@@ -1,7 +1,8 @@
-"""Reference-schedule vs fused MINRES loop on a config: iterations, residuals, timings,
-and the distance between the two solutions (tol 1e-8 and 1e-12).
+"""MINRES loop schedules side by side on a config (gnw.h GNW_LOOP_*): iterations, restarts,
+true residuals, timings, and each schedule's distance from the reference schedule's solution
+(tol 1e-8 and 1e-12).
 
-    python tools/check_fused.py [--config C2]
+    python tools/check_fused.py [--config C2] [--modes reference,fused,lean] [--n N --m M]
 """
 import argparse
 import json
@@ -18,6 +19,8 @@ from paper_2209_02815_b200 import AmgOptions, Context, workload as W  # noqa: E4
 
 ap = argparse.ArgumentParser()
 ap.add_argument("--config", default="C2")
+ap.add_argument("--modes", default="reference,fused,lean")
+ap.add_argument("--tols", default="1e-8,1e-12")
 args = ap.parse_args()
 cfg = W.CONFIGS[args.config]
 inp = W.gnstep_inputs(cfg.n, cfg.m, cfg.index)
@@ -35,13 +38,15 @@ dm = torch.from_numpy(inp.dm).cuda()
 dg = torch.from_numpy(inp.dg).cuda()
 zN = torch.zeros(inp.mesh.n_cells, dtype=torch.float64, device="cuda")
 zm = torch.zeros(cfg.m, dtype=torch.float64, device="cuda")
+modes = args.modes.split(",")
+tols = [float(t) for t in args.tols.split(",")]
 for a in cfg.alphas:
     out = {}
-    for fused in (False, True):
-        ctx.set_loop_mode(fused)
+    for mode in modes:
+        ctx.set_loop_mode(mode)
         ctx.set_jacobian(J, a)
         b = ctx.assemble_rhs(dm, zN, dg, zm)
-        for tol in (1e-8, 1e-12):
+        for tol in tols:
             ctx.minres(b, tol=tol)  # warm
             torch.cuda.synchronize()
             r0 = ctx.stats()["loop_restarts"]
@@ -49,12 +54,14 @@ for a in cfg.alphas:
             x, rep = ctx.minres(b, tol=tol)
             torch.cuda.synchronize()
             dt = time.perf_counter() - t0
-            rep.restarts = ctx.stats()["loop_restarts"] - r0
-            out[(fused, tol)] = (x.cpu().numpy(), rep, dt)
-    for tol in (1e-8, 1e-12):
-        xr, rr, tr = out[(False, tol)]
-        xf, rf, tf = out[(True, tol)]
-        d = np.linalg.norm(xr - xf) / np.linalg.norm(xr)
-        print(f"alpha={a:g} tol={tol:g}: ref-loop {rr.iterations} it {1e3 * tr:.1f} ms true {rr.true_relative_residual:.2e} | "
-              f"fused {rf.iterations} it ({rf.restarts} restarts) {1e3 * tf:.1f} ms true {rf.true_relative_residual:.2e} | rel diff {d:.2e}"
-              + (f" | reference {ref[a]}" if tol == 1e-8 and a in ref else ""), flush=True)
+            out[(mode, tol)] = (x.cpu().numpy(), rep, dt, ctx.stats()["loop_restarts"] - r0)
+    for tol in tols:
+        xr = out[(modes[0], tol)][0]
+        parts = []
+        for mode in modes:
+            x, rep, dt, rs = out[(mode, tol)]
+            d = np.linalg.norm(x - xr) / np.linalg.norm(xr)
+            parts.append(f"{mode} {rep.iterations} it ({rs} rs) {1e3 * dt:.1f} ms "
+                         f"{1e3 * dt / max(rep.iterations, 1):.3f} ms/it true {rep.true_relative_residual:.2e} d {d:.1e}")
+        print(f"alpha={a:g} tol={tol:g}: " + " | ".join(parts)
+              + (f" | reference run {ref[a]}" if tol == 1e-8 and a in ref else ""), flush=True)
