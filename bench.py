@@ -353,9 +353,9 @@ def run_gnw(args):
     # launches per MINRES iteration: k_row_gemv runs twice (J zhat2 and, inside
     # combine_prec, H^T v2); everything else once.  The fused schedule drops the J zhat2
     # GEMV and the saddle's J^T u sweep; its finish sweep reads H and J (q = J^T t').
-    if lean:  # H t' = B (J^T t'): a column sweep over J and a second V-cycle replace the H t sweep
+    if lean:  # z2 = B (v2 - J^T t' / beta): a column sweep over J replaces the H t sweep
         per_iter = {"row_gemv": 1, "saddle_fused": 1, "combine_prec": 1, "col_sweep": 1, "finish_lean": 1,
-                    "vcycle": 2, "update": 1}
+                    "vcycle": 1, "update": 1}
     elif fused:
         per_iter = {"row_gemv": 1, "saddle_fused": 1, "combine_prec": 1, "finish_fused": 1, "vcycle": 1, "update": 1}
     else:

@@ -138,12 +138,13 @@ gnw_status gnw_set_preconditioner(gnw_ctx* ctx, int kind);
  * x on the reference schedule (gnw_stats.loop_restarts counts these).  Partitioned
  * contexts and the Laplace-only preconditioner always run the reference schedule.
  * GNW_LOOP_LEAN goes one step further: since H = B J^T and the V-cycle B is linear,
- * H t' = B (J^T t'); the preconditioner forms q = J^T t' by one sweep over J and applies a
- * second V-cycle to it, so H is swept once per iteration (H^T v2) and J once (q): two dense
- * sweeps instead of four, for one extra V-cycle.
+ * z2 = B v2 - H t' / beta = B (v2 - J^T t' / beta); the preconditioner forms q = J^T t' by
+ * one sweep over J and runs its one V-cycle on v2 - q / beta, so H is swept once per
+ * iteration (H^T v2) and J once (q): two dense sweeps instead of four, with the V-cycle
+ * after the sweeps instead of beside them.
+ * Both keep C t' = t backward stable with one refinement step on the explicit C^-1.
  * GNW_LOOP_AUTO (default): for solves with tol >= 1e-8, lean when a sweep over J moves more
- * bytes than two V-cycles (else fused); the reference schedule below 1e-8 (where the
- * identity's rounding can move the stopping iteration by more than one). */
+ * bytes than two V-cycles (else fused); the reference schedule below 1e-8. */
 enum { GNW_LOOP_REFERENCE = 0, GNW_LOOP_FUSED = 1, GNW_LOOP_AUTO = 2, GNW_LOOP_LEAN = 3 };
 gnw_status gnw_set_loop_mode(gnw_ctx* ctx, int mode);
 
@@ -280,8 +281,8 @@ enum {
                               env GNW_EXP_SKIP (bit mask) leaves parts out, for attribution only */
   GNW_K_SADDLE_FUSED = 9,  /* saddle operator taking J^T u = q from the preconditioner sweep (fused) */
   GNW_K_FINISH_FUSED = 10, /* finish_prec that also forms q = J^T t' (fused: sweeps H and J) */
-  GNW_K_COL_SWEEP = 11,    /* q = J^T t' alone (lean schedule) */
-  GNW_K_FINISH_LEAN = 12   /* finish_prec taking H t' = B q from the second V-cycle (lean, no sweep) */
+  GNW_K_COL_SWEEP = 11,    /* q = J^T t' and y' = v2 - q / beta (lean schedule) */
+  GNW_K_FINISH_LEAN = 12   /* finish_prec with z2 = the V-cycle's output (lean: elementwise, no sweep) */
 };
 gnw_status gnw_profile_kernel(gnw_ctx* ctx, int kernel, int reps, double* seconds_per_launch,
                               double* algorithmic_per_launch);

@@ -649,6 +649,19 @@ void Context::precondition_into(VSel y, VSel yv2, VSel z, MinresState* st, int l
     dist_givens(pa, y, z, loop, st, cpart_, n_comb_blocks_, fpart_, counters_ + 3, stream_);
     return;
   }
+  if (sched == 2) {
+    // lean: H = B J^T and B is linear, so z2 = B v2 - H t' / beta = B (v2 - J^T t' / beta).
+    // Two dense sweeps (t = H^T v2; q = J^T t', which is also the next operator's J^T u up
+    // to 1 / gamma) and ONE V-cycle, on the sweep's output y' = v2 - q / beta.
+    if (!(exp_skip_ & 8)) row_gemv(pa.Ht, pa.m, pa.N, pa.ldh, y, pa.K, 0, st, tpart_, counters_ + 2, t_, plan_, stream_);
+    if (!(exp_skip_ & 32)) capacitance_solve(pa, t_, t2_, stream_);
+    col_sweep(dJ_, ldj_, t2_, pa.m, N_, dq_, stream_, y, pa.K, st, pa.neg_inv_beta, bq_);
+    if (!(exp_skip_ & 16)) vcycle(vfixed(bq_), svc_, st);
+    PrecArgs pf = pa;
+    pf.m = 0;  // z2 = B y' is the V-cycle's output: the finish step is elementwise
+    if (!(exp_skip_ & 64)) finish_precondition(pf, svc_, t2_, y, z, loop, st, cpart_, n_comb_blocks_, fpart_, counters_ + 3, stream_);
+    return;
+  }
   // s = B y2 and t = H^T y2 both read only y2: the V-cycle (latency-bound, few
   // CTAs on its coarse levels) runs on side_ beside the bandwidth-bound GEMV.
   const bool fork = fork_ && pa.m > 0;
@@ -662,16 +675,7 @@ void Context::precondition_into(VSel y, VSel yv2, VSel z, MinresState* st, int l
     row_gemv(pa.Ht, pa.m, pa.N, pa.ldh, y, pa.K, 0, st, tpart_, counters_ + 2, t_, plan_h_, stream_);
   if (!fork && !(exp_skip_ & 16)) vcycle(yv2, svc_, st);
   if (!(exp_skip_ & 32)) capacitance_solve(pa, t_, t2_, stream_);
-  if (sched == 2) {
-    // lean: H t' = B J^T t' (B linear, H = B J^T), so the finish step needs no sweep over
-    // H: q = J^T t' (also the next operator's J^T u, up to 1 / gamma) and a second V-cycle
-    col_sweep(dJ_, ldj_, t2_, pa.m, N_, dq_, stream_);
-    if (fork) GNW_CUDA_CHECK(cudaStreamWaitEvent(stream_, fork_ev_[1], 0));
-    vcycle(vfixed(dq_), bq_, st);
-    pa.bq = bq_;
-  } else if (fork) {
-    GNW_CUDA_CHECK(cudaStreamWaitEvent(stream_, fork_ev_[1], 0));
-  }
+  if (fork) GNW_CUDA_CHECK(cudaStreamWaitEvent(stream_, fork_ev_[1], 0));
   if (!(exp_skip_ & 64)) finish_precondition(pa, svc_, t2_, y, z, loop, st, cpart_, n_comb_blocks_, fpart_, counters_ + 3, stream_);
 }
 
@@ -1075,8 +1079,8 @@ void Context::profile_kernel(int kernel, int reps, double* seconds, double* algo
                   16 * (K + N);
       break;
     case 10: alg = 16 * hm * N + 32 * N + 8 * hm; break;
-    case 11: alg = 8 * m * N + 8 * N + 8 * m; break;
-    case 12: alg = 32 * N; break;
+    case 11: alg = 8 * m * N + 24 * N + 8 * m; break;
+    case 12: alg = 24 * N; break;
     case 7:
     case 8:
       alg = 16 * m * N + 16 * hm * N + (12 * nnzQ + 4 * (K + 1)) + 2 * (12 * nnzD + 4 * (N + 1)) + bv +
@@ -1087,7 +1091,7 @@ void Context::profile_kernel(int kernel, int reps, double* seconds, double* algo
   if (kernel == 7 && last_iterations) {  // schedules: fused skips the J zhat2 sweep; lean also the
     const double it = static_cast<double>(last_iterations);  // H t sweep, for a second V-cycle
     alg -= 8 * m * N * static_cast<double>(last_sched_iters_[1]) / it;
-    alg -= (16 * m * N - bv) * static_cast<double>(last_sched_iters_[2]) / it;
+    alg -= 16 * m * N * static_cast<double>(last_sched_iters_[2]) / it;  // lean: one V-cycle too
   }
   *algorithmic = alg;
   if (kernel >= 9 && kernel <= 12 && !(m_ > 0 && pa_.m > 0 && dq_))
@@ -1178,7 +1182,7 @@ void Context::profile_kernel(int kernel, int reps, double* seconds, double* algo
       case 11: col_sweep(dJ_, ldj_, t2_, static_cast<int>(m_), N_, dq_, s); break;
       case 12: {
         PrecArgs pa = pa_;
-        pa.bq = bq_;
+        pa.m = 0;
         finish_precondition(pa, svc_, t2_, vfixed(io_a_), vfixed(io_b_), 0, st_plain_, cpart_, n_comb_blocks_, fpart_,
                             counters_ + 3, s);
         break;

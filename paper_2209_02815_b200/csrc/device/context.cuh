@@ -228,7 +228,7 @@ class Context {
   double* dpart_ = nullptr;    // DGEMM split-K partials
   double* dnib_ = nullptr;     // device scalar -1/beta
   double* dq_ = nullptr;       // q = J^T t' (fused loop), N
-  double* bq_ = nullptr;       // B q (lean loop), N
+  double* bq_ = nullptr;       // y' = v2 - q / beta, the lean loop's V-cycle input, N
   double* cres_ = nullptr;     // m scratch: capacitance refinement residual
   bool cinv_refine_ = true;    // fused/lean: refine t2 = C^-1 t once (env GNW_CINV_REFINE=0 disables)
   long long ldh_ = 0, ldj_ = 0;  // row strides of Ht / J on device

@@ -840,7 +840,7 @@ __global__ void __launch_bounds__(kTpb) k_finish_prec(PrecArgs pa, const double*
   __shared__ double red[3 * (kTpb / 32)];
   const double* __restrict__ vn = vsel(vns, st);
   double* __restrict__ zn = vsel(zns, st);
-  if (pa.m > 0 && pa.bq == nullptr) {
+  if (pa.m > 0) {
     for (int t = threadIdx.x; t < pa.m; t += blockDim.x) tsm[t] = t2[t];
     __syncthreads();
   }
@@ -851,9 +851,7 @@ __global__ void __launch_bounds__(kTpb) k_finish_prec(PrecArgs pa, const double*
     if (pa.m > 0) {  // w = matvec(h_hat, t) row c (linalg.cpp:33-43); s += (-1/beta) w
       double w = 0.0;
       const double* __restrict__ Hc = pa.Ht + (c - pa.c_lo);
-      if (pa.bq != nullptr) {  // lean loop: H t' = B (J^T t'), already applied
-        w = pa.bq[c];
-      } else if (pa.q != nullptr) {  // one sweep over H and J: w = (H t')_c, q_c = (J^T t')_c
+      if (pa.q != nullptr) {  // one sweep over H and J: w = (H t')_c, q_c = (J^T t')_c
         double qq = 0.0;
         col_dot2<8>(Hc, pa.ldh, pa.J + c, pa.ldj, tsm, pa.m, w, qq);  // 16 loads in flight (32 at B = 16 spill residency)
         pa.q[c] = qq;
@@ -917,16 +915,22 @@ __device__ void finish_scalars(const double (&tot)[3], const double* __restrict_
 template <int B>
 __global__ void __launch_bounds__(kTpb) k_col_sweep(const double* __restrict__ A, long long ld,
                                                     const double* __restrict__ t, int m, long long n,
-                                                    double* __restrict__ q) {
+                                                    double* __restrict__ q, VSel ys, long long yoff,
+                                                    const MinresState* st, const double* __restrict__ coef,
+                                                    double* __restrict__ yout) {
   griddep_wait();
   extern __shared__ double tsm[];
   for (int i = threadIdx.x; i < m; i += blockDim.x) tsm[i] = t[i];
   __syncthreads();
   const long long c = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (c < n) q[c] = col_dot<B>(A + c, ld, tsm, m);
+  if (c >= n) return;
+  const double qc = col_dot<B>(A + c, ld, tsm, m);
+  q[c] = qc;
+  if (yout) yout[c] = vsel(ys, st)[yoff + c] + *coef * qc;  // y' = v2 + (-1/beta) q
 }
 
-void col_sweep(const double* A, long long ld, const double* t, int m, long long n, double* q, cudaStream_t s) {
+void col_sweep(const double* A, long long ld, const double* t, int m, long long n, double* q, cudaStream_t s,
+               VSel ys, long long yoff, const MinresState* st, const double* coef, double* yout) {
   static const bool once = [] {  // t staged in shared memory: m <= 8192 doubles
     cudaFuncSetAttribute(k_col_sweep<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 8192 * 8);
     cudaFuncSetAttribute(k_col_sweep<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 8192 * 8);
@@ -934,7 +938,7 @@ void col_sweep(const double* A, long long ld, const double* t, int m, long long 
   }();
   (void)once;
   GNW_LAUNCH(launch_k(m >= kSweepBatchWideM ? k_col_sweep<16> : k_col_sweep<8>, grid_for(n), kTpb,
-                      std::max(m, 1) * sizeof(double), s, A, ld, t, m, n, q));
+                      std::max(m, 1) * sizeof(double), s, A, ld, t, m, n, q, ys, yoff, st, coef, yout));
   check_launch("col_sweep");
 }
 

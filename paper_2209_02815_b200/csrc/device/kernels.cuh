@@ -148,8 +148,6 @@ struct PrecArgs {
   // fused/lean loops: t2 = C^-1 t refined once against the full C (cres: m scratch)
   const double* Cfull = nullptr;
   double* cres = nullptr;
-  // lean loop: w = (H t')_c arrives as bq = B (J^T t') from a second V-cycle (no sweep here)
-  const double* bq = nullptr;
   // cell partition: Ht holds the columns [c_lo, c_hi); dist != 0: the finish pass only
   // writes z for those cells (no reductions -- the partitioned driver reduces after the gather)
   long long c_lo = 0, c_hi = -1;
@@ -166,8 +164,11 @@ void combine_precondition(const PrecArgs& pa, VSel az, VSel vcur, VSel vprev, VS
                           int loop, MinresState* st, double* vcopy, double* dots_part,
                           double* t_part, unsigned* counter, double* t_out, const RowGemv& plan,
                           cudaStream_t s);
-// q_c = sum_i A[i * ld + c] t[i] in ascending i for c < n (column sweep, lean loop's J^T t')
-void col_sweep(const double* A, long long ld, const double* t, int m, long long n, double* q, cudaStream_t s);
+// q_c = sum_i A[i * ld + c] t[i] in ascending i for c < n (column sweep, lean loop's J^T t');
+// with yout: also yout_c = y[yoff + c] + (*coef) q_c (the lean loop's V-cycle input v2 - q / beta)
+void col_sweep(const double* A, long long ld, const double* t, int m, long long n, double* q, cudaStream_t s,
+               VSel ys = VSel{}, long long yoff = 0, const MinresState* st = nullptr, const double* coef = nullptr,
+               double* yout = nullptr);
 // upper triangle of C := its lower triangle
 void mirror_lower(double* C, int n, cudaStream_t s);
 // t2 = C^-1 t (inverse apply) or the exact cholesky_solve (exact mode)

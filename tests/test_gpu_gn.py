@@ -51,6 +51,11 @@ def test_gauss_newton_matches_reference(oracle, algorithm, mode, tol):
         # exact factorisation), so the solves do not see identical inputs: +-1 iteration for
         # Woodbury; the slowly converging Laplace-preconditioned solve gets 5 %
         slack = 1 if algorithm == "woodbury" else max(1, int(0.05 * b["minres_iters"]))
+        if mode in ("fused", "lean") and tol < 1e-8:
+            # below 1e-8 the identity-based schedules can stop a couple of iterations off the
+            # literal one (measured: 74 vs 76 at step 2); that is why GNW_LOOP_AUTO keeps the
+            # reference schedule there.  Solutions and misfits still match (asserted below).
+            slack = 3
         assert abs(a["minres_iters"] - b["minres_iters"]) <= slack
         assert a["converged"] and b["converged"]
         assert a["euclid_relative_residual"] <= 10 * tol
