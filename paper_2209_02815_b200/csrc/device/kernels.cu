@@ -831,7 +831,7 @@ __device__ void finish_scalars(const double (&tot)[3], const double* __restrict_
                                int loop, MinresState* st, double* red);
 
 template <int B>
-__global__ void __launch_bounds__(kTpb) k_finish_prec(PrecArgs pa, const double* __restrict__ svc,
+__global__ void __launch_bounds__(kTpb, B >= 16 ? 5 : 8) k_finish_prec(PrecArgs pa, const double* __restrict__ svc,
                                                       const double* __restrict__ t2, VSel vns, VSel zns, int loop,
                                                       MinresState* st, const double* __restrict__ dots_edge,
                                                       int n_edge_blocks, double* part, unsigned* counter) {
@@ -913,7 +913,7 @@ __device__ void finish_scalars(const double (&tot)[3], const double* __restrict_
 }
 
 template <int B>
-__global__ void __launch_bounds__(kTpb) k_col_sweep(const double* __restrict__ A, long long ld,
+__global__ void __launch_bounds__(kTpb, B >= 16 ? 5 : 8) k_col_sweep(const double* __restrict__ A, long long ld,
                                                     const double* __restrict__ t, int m, long long n,
                                                     double* __restrict__ q, VSel ys, long long yoff,
                                                     const MinresState* st, const double* __restrict__ coef,
@@ -937,7 +937,11 @@ void col_sweep(const double* A, long long ld, const double* t, int m, long long 
     return true;
   }();
   (void)once;
-  GNW_LAUNCH(launch_k(m >= kSweepBatchWideM ? k_col_sweep<16> : k_col_sweep<8>, grid_for(n), kTpb,
+  static const int wide_m = [] {  // env GNW_COL_SWEEP_WIDE_M: batch-16 threshold (experiments)
+    const char* e = std::getenv("GNW_COL_SWEEP_WIDE_M");
+    return e ? std::atoi(e) : kSweepBatchWideM;
+  }();
+  GNW_LAUNCH(launch_k(m >= wide_m ? k_col_sweep<16> : k_col_sweep<8>, grid_for(n), kTpb,
                       std::max(m, 1) * sizeof(double), s, A, ld, t, m, n, q, ys, yoff, st, coef, yout));
   check_launch("col_sweep");
 }
