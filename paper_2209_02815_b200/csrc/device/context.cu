@@ -655,7 +655,7 @@ void Context::precondition_into(VSel y, VSel yv2, VSel z, MinresState* st, int l
     // to 1 / gamma) and ONE V-cycle, on the sweep's output y' = v2 - q / beta.
     if (!(exp_skip_ & 8)) row_gemv(pa.Ht, pa.m, pa.N, pa.ldh, y, pa.K, 0, st, tpart_, counters_ + 2, t_, plan_, stream_);
     if (!(exp_skip_ & 32)) capacitance_solve(pa, t_, t2_, stream_);
-    col_sweep(dJ_, ldj_, t2_, pa.m, N_, dq_, stream_, y, pa.K, st, pa.neg_inv_beta, bq_);
+    if (!(exp_skip_ & 256)) col_sweep(dJ_, ldj_, t2_, pa.m, N_, dq_, stream_, y, pa.K, st, pa.neg_inv_beta, bq_);
     if (!(exp_skip_ & 16)) vcycle(vfixed(bq_), svc_, st);
     PrecArgs pf = pa;
     pf.m = 0;  // z2 = B y' is the V-cycle's output: the finish step is elementwise

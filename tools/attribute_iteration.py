@@ -10,7 +10,7 @@ import subprocess
 import sys
 
 PARTS = {"J row GEMV": 1, "saddle (J^T u)": 2, "combine elem": 4, "H^T y GEMV": 8, "V-cycle": 16,
-         "C^-1 apply": 32, "finish (H t)": 64, "update": 128}
+         "C^-1 apply": 32, "finish (H t)": 64, "update": 128, "col sweep (lean)": 256}
 
 if len(sys.argv) > 1 and sys.argv[1] == "--child":
     sys.path.insert(0, os.getcwd())
@@ -45,4 +45,4 @@ print(f"{args.config}: loop iteration {it:.4f} ms; replayed body {full:.4f} ms")
 for name, bit in PARTS.items():
     t, _ = run(bit)
     print(f"  without {name:16s} {t:.4f} ms  (part costs {full - t:+.4f} ms)")
-print(f"  everything skipped {run(255)[0]:.4f} ms (graph launch floor)")
+print(f"  everything skipped {run(511)[0]:.4f} ms (graph launch floor)")
