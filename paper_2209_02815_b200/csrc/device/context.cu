@@ -417,9 +417,13 @@ void Context::set_jacobian(const double* J, int64_t m, int64_t n_cells, double b
       // prefetch_jacobian already moved these bytes over PCIe beside the previous solve:
       // one device copy (2 x 8 m N bytes of HBM traffic) instead of the host transfer
       GNW_CUDA_CHECK(cudaStreamWaitEvent(s, stage_ev_[0], 0));
-      GNW_CUDA_CHECK(cudaMemcpyAsync(dJ_, jstage_, static_cast<size_t>(m) * ldj_ * sizeof(double),
+      GNW_CUDA_CHECK(cudaMemcpyAsync(dJ_, jstage_, static_cast<size_t>(staged_rows_) * ldj_ * sizeof(double),
                                      cudaMemcpyDeviceToDevice, s));
       GNW_CUDA_CHECK(cudaEventRecord(stage_ev_[1], s));  // the staging buffer is free again
+      if (staged_rows_ < m)  // partial stage (C3/C5): the remaining rows cross PCIe now
+        GNW_CUDA_CHECK(cudaMemcpy2DAsync(dJ_ + static_cast<size_t>(staged_rows_) * ldj_, ldj_ * sizeof(double),
+                                         J + static_cast<size_t>(staged_rows_) * Nl, Nl * sizeof(double),
+                                         Nl * sizeof(double), m - staged_rows_, cudaMemcpyHostToDevice, s));
     } else {
       GNW_CUDA_CHECK(cudaMemcpy2DAsync(dJ_, ldj_ * sizeof(double), J, Nl * sizeof(double), Nl * sizeof(double), m,
                                        cudaMemcpyHostToDevice, s));
@@ -538,28 +542,35 @@ void Context::prefetch_jacobian(const double* J, int64_t m, int64_t n_cells) {
   if (n_cells != local_n()) throw std::invalid_argument("gnw_prefetch_jacobian: J shape mismatch");
   const long long Nl = local_n();
   const long long ld = Nl + pad_;  // the owned copy's padded row stride (set_jacobian)
-  const size_t need = static_cast<size_t>(m) * ld;
-  if (!stage_mem_ || stage_cap_ < need) {
+  // Stage as many leading rows of J as fit beside the solve: all of them at C1/C2/C4; at
+  // C3/C5 (J + H already take 127-137 GB of the 179) the rows that fit in what is left, and
+  // set_jacobian copies only the remainder over PCIe.
+  int64_t rows = m;
+  if (!stage_mem_ || stage_cap_ < static_cast<size_t>(m) * ld) {
     GNW_CUDA_CHECK(cudaStreamSynchronize(copy_));
     sync();  // a pending consume of the old buffer
     stage_mem_.reset();
     stage_cap_ = 0;
-    // A second J-sized buffer must leave room for the solve (C3/C5: J + H already take
-    // 127-137 GB); without it the prefetch is a no-op and set_jacobian copies as usual.
     size_t free_b = 0, total_b = 0;
     GNW_CUDA_CHECK(cudaMemGetInfo(&free_b, &total_b));
-    if (need * sizeof(double) + (size_t{4} << 30) > free_b) {
+    const size_t margin = size_t{4} << 30;
+    const size_t row_b = static_cast<size_t>(ld) * sizeof(double);
+    rows = free_b > margin ? std::min<int64_t>(m, static_cast<int64_t>((free_b - margin) / row_b)) : 0;
+    if (const char* e = std::getenv("GNW_STAGE_ROWS_MAX")) rows = std::min<int64_t>(rows, std::atoll(e));  // tests
+    if (rows < std::max<int64_t>(1, m / 16)) {  // too little to matter: set_jacobian copies as usual
       staged_src_ = nullptr;
       stage_deferred_ = false;
       return;
     }
     stage_mem_ = std::make_unique<DeviceMemory>();
-    jstage_ = stage_mem_->alloc<double>(need);
-    stage_cap_ = need;
+    jstage_ = stage_mem_->alloc<double>(static_cast<size_t>(rows) * ld);
+    stage_cap_ = static_cast<size_t>(rows) * ld;
     GNW_CUDA_CHECK(cudaEventRecord(stage_ev_[1], stream_));
   }
+  rows = std::min<int64_t>(m, static_cast<int64_t>(stage_cap_ / static_cast<size_t>(ld)));
   staged_src_ = J;
   staged_m_ = m;
+  staged_rows_ = rows;
   staged_n_ = Nl;
   staged_ld_ = ld;
   stage_deferred_ = true;
@@ -574,7 +585,7 @@ void Context::issue_stage() {
   // the previous stage must have been consumed (device-side order, no host wait)
   GNW_CUDA_CHECK(cudaStreamWaitEvent(copy_, stage_ev_[1], 0));
   GNW_CUDA_CHECK(cudaMemcpy2DAsync(jstage_, staged_ld_ * sizeof(double), staged_src_, staged_n_ * sizeof(double),
-                                   staged_n_ * sizeof(double), staged_m_, cudaMemcpyHostToDevice, copy_));
+                                   staged_n_ * sizeof(double), staged_rows_, cudaMemcpyHostToDevice, copy_));
   GNW_CUDA_CHECK(cudaEventRecord(stage_ev_[0], copy_));
 }
 

@@ -222,6 +222,7 @@ class Context {
   size_t stage_cap_ = 0;
   const double* staged_src_ = nullptr;     // host J of the pending stage (nullptr: none)
   int64_t staged_m_ = -1;
+  int64_t staged_rows_ = 0;                // leading rows of J staged (< m when only part fits)
   long long staged_n_ = -1, staged_ld_ = -1;
   bool stage_deferred_ = false;            // requested, not yet issued (issue_stage)
   void issue_stage();

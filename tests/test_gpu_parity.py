@@ -300,6 +300,7 @@ def test_prefetch_jacobian_same_bits(c1, gpu_ctx_factory):
     mesh, inp, prob = c1[64]
     ctx = gpu_ctx_factory(mesh)
     J = np.ascontiguousarray(inp.J)
+    prob.set_jacobian(J, 1e-2)
     b = prob.assemble_rhs(inp.dm, np.zeros(prob.N), inp.dg, np.zeros(J.shape[0]))
     ctx.set_jacobian(J, 1e-2)
     H0, L0 = ctx.woodbury_factors()
@@ -320,3 +321,27 @@ def test_prefetch_jacobian_same_bits(c1, gpu_ctx_factory):
     assert np.array_equal(H2, H3) and np.array_equal(H2, 2.0 * H0)
     with pytest.raises(ValueError, match="shape mismatch"):
         ctx.prefetch_jacobian(np.ascontiguousarray(J[:, :-2]))
+
+
+def test_prefetch_jacobian_partial_stage_same_bits(c1, monkeypatch):
+    """C3/C5 stage only the leading rows of J that fit beside the solve; set_jacobian then
+    copies the rest over PCIe.  Forced here with GNW_STAGE_ROWS_MAX: the same bits."""
+    from paper_2209_02815_b200 import Context
+    mesh, inp, prob = c1[64]
+    monkeypatch.setenv("GNW_STAGE_ROWS_MAX", "13")  # of m = 32 rows
+    ctx = Context(0)
+    ctx.assemble(mesh)
+    J = np.ascontiguousarray(inp.J)
+    prob.set_jacobian(J, 1e-2)
+    b = prob.assemble_rhs(inp.dm, np.zeros(prob.N), inp.dg, np.zeros(J.shape[0]))
+    ctx.set_jacobian(J, 1e-2)
+    H0, L0 = ctx.woodbury_factors()
+    x0, r0 = ctx.minres(b, tol=1e-10)
+    ctx.prefetch_jacobian(J)
+    x0b, _ = ctx.minres(b, tol=1e-10)  # the staged rows cross PCIe beside this solve
+    ctx.set_jacobian(J, 1e-2)
+    H1, L1 = ctx.woodbury_factors()
+    x1, r1 = ctx.minres(b, tol=1e-10)
+    assert np.array_equal(H0, H1) and np.array_equal(L0, L1)
+    assert r0.iterations == r1.iterations and np.array_equal(x0, x1) and np.array_equal(x0, x0b)
+    ctx.close()
