@@ -140,8 +140,6 @@ __device__ __forceinline__ void col_dot2(const double* __restrict__ p, long long
 }
 
 constexpr int kTpb = 256;
-constexpr int kRowsPerWarp = 4;                           // row GEMV: rows per warp
-constexpr int kRowsPerCta = kRowsPerWarp * (kTpb / 32);  // row GEMV: rows per CTA
 
 inline unsigned grid_for(long long n, int tpb = kTpb) {
   return static_cast<unsigned>((n + tpb - 1) / tpb);
@@ -485,7 +483,7 @@ void transpose_batch_to_rows(const double* X, long long cols, long long ld, int 
 
 // R row segments A[row_r, 0 : len] dotted with x[0 : len], one warp, lanes take
 // 2-column steps; R independent rows keep R x 2 x 16-byte loads in flight per lane.
-template <int R>
+template <int R, int U = 4>
 __device__ __forceinline__ void warp_rows_dot(const double* __restrict__ a, long long ld, int nrows,
                                               const double* __restrict__ x, int scaled, double sc, int len,
                                               bool vec_ok, int lane, double (&out)[R]) {
@@ -495,7 +493,7 @@ __device__ __forceinline__ void warp_rows_dot(const double* __restrict__ a, long
   auto xv = [&](int t) { return scaled ? __ldg(x + t) * sc : __ldg(x + t); };
   if (vec_ok) {
     const int len2 = len & ~1;
-#pragma unroll 4
+#pragma unroll U
     for (int t = lane * 2; t < len2; t += 64) {
       const double x0 = xv(t), x1 = xv(t + 1);
       double2 v[R];
@@ -529,7 +527,10 @@ __device__ __forceinline__ void warp_rows_dot(const double* __restrict__ a, long
 
 // Register budget of 4 CTAs per SM: with it ptxas keeps the unrolled 16-byte row loads in
 // flight (64 registers; C2 0.173 -> 0.165 ms); at the default budget it interleaves them.
-__global__ void __launch_bounds__(kTpb, 4) k_row_gemv(const double* __restrict__ A, int m, long long N, long long ld, VSel xs,
+// R rows per warp (8 warps): R = 4 below m = 1024; R = 8 (64 rows per CTA) at large m, where
+// the one-wave plan otherwise rounds 119 row groups x 4 spans = 476 of 592 CTA slots (C5).
+template <int R, int U, int MINB>
+__global__ void __launch_bounds__(kTpb, MINB) k_row_gemv(const double* __restrict__ A, int m, long long N, long long ld, VSel xs,
                                                    long long xoff, int scaled, const MinresState* st,
                                                    double* __restrict__ partial, unsigned* counter,
                                                    double* __restrict__ out, int span) {
@@ -541,15 +542,14 @@ __global__ void __launch_bounds__(kTpb, 4) k_row_gemv(const double* __restrict__
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const bool vec_ok = ((ld & 1) == 0);  // span is even, so every row segment starts 16-byte aligned
   {
-    const int row = blockIdx.y * kRowsPerCta + warp * kRowsPerWarp;  // 8 warps x 4 rows
+    const int row = blockIdx.y * (R * (kTpb / 32)) + warp * R;
     if (row < m) {
-      double d[kRowsPerWarp];
-      const int nr = min(kRowsPerWarp, m - row);
-      warp_rows_dot<kRowsPerWarp>(A + static_cast<long long>(row) * ld + c0, ld, nr, x + c0, scaled, sc, len, vec_ok,
-                                  lane, d);
+      double d[R];
+      const int nr = min(R, m - row);
+      warp_rows_dot<R, U>(A + static_cast<long long>(row) * ld + c0, ld, nr, x + c0, scaled, sc, len, vec_ok, lane, d);
       if (lane == 0)
 #pragma unroll
-        for (int r = 0; r < kRowsPerWarp; ++r)
+        for (int r = 0; r < R; ++r)
           if (r < nr) partial[static_cast<long long>(blockIdx.x) * m + row + r] = d[r];
     }
   }
@@ -573,19 +573,30 @@ __global__ void __launch_bounds__(kTpb, 4) k_row_gemv(const double* __restrict__
   if (threadIdx.x == 0) *counter = 0u;
 }
 
+static int g_rg_wide_m = [] {  // env GNW_RG_WIDE_M: m from which the 8-rows-per-warp variant runs
+  const char* e = std::getenv("GNW_RG_WIDE_M");
+  return e ? std::atoi(e) : 1024;
+}();
+static inline bool rg_wide(int m) { return m >= g_rg_wide_m; }
+#define K_ROW_GEMV_NARROW k_row_gemv<4, 4, 4>
+#define K_ROW_GEMV_WIDE k_row_gemv<8, 2, 3>
+
 RowGemv row_gemv_plan(long long N, int m, int reserve) {
-  static int sms = 0, occ = 0;  // SMs, resident k_row_gemv CTAs per SM
+  static int sms = 0, occ = 0, occw = 0;  // SMs, resident k_row_gemv CTAs per SM (narrow, wide)
   if (sms == 0) {
     int dev = 0;
     sms = 148;
     if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_row_gemv, kTpb, 0) != cudaSuccess || occ < 1) occ = 4;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, K_ROW_GEMV_NARROW, kTpb, 0) != cudaSuccess || occ < 1) occ = 4;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occw, K_ROW_GEMV_WIDE, kTpb, 0) != cudaSuccess || occw < 1) occw = 3;
     cudaGetLastError();
   }
+  const bool wide = rg_wide(m);
+  const int rows_cta = (wide ? 8 : 4) * (kTpb / 32);
   // reserve: CTA slots per SM left free for a concurrent graph branch (the V-cycle)
-  const int slots = sms * std::max(1, occ - reserve);
+  const int slots = sms * std::max(1, (wide ? occw : occ) - reserve);
   RowGemv p;
-  p.ngroups = std::max(1, (m + kRowsPerCta - 1) / kRowsPerCta);
+  p.ngroups = std::max(1, (m + rows_cta - 1) / rows_cta);
   const long long spans = std::max(1, slots / p.ngroups);
   long long span = (N + spans - 1) / spans;
   span = std::max<long long>(64, (span + 63) / 64 * 64);
@@ -597,9 +608,11 @@ RowGemv row_gemv_plan(long long N, int m, int reserve) {
 void row_gemv(const double* A, int m, long long N, long long ld, VSel x, long long x_off, int scaled,
               const MinresState* st, double* partial, unsigned* counter, double* out, const RowGemv& plan,
               cudaStream_t s) {
-  const dim3 grid(plan.nchunks, (m + kRowsPerCta - 1) / kRowsPerCta);
-  GNW_LAUNCH(launch_k(k_row_gemv, grid, kTpb, 0, s, A, m, N, ld, x, x_off, scaled, st, partial, counter, out,
-                                                             plan.chunk));
+  const bool wide = rg_wide(m);
+  const int rows_cta = (wide ? 8 : 4) * (kTpb / 32);
+  const dim3 grid(plan.nchunks, (m + rows_cta - 1) / rows_cta);
+  GNW_LAUNCH(launch_k(wide ? K_ROW_GEMV_WIDE : K_ROW_GEMV_NARROW, grid, kTpb, 0, s, A, m, N, ld, x, x_off, scaled, st,
+                      partial, counter, out, plan.chunk));
   check_launch("row_gemv");
 }
 
