@@ -32,6 +32,35 @@ DCsr upload_csr(DeviceMemory& mem, const host::Csr& A, cudaStream_t s) {
   return d;
 }
 
+DSell upload_sell(DeviceMemory& mem, const host::Csr& A, cudaStream_t s) {
+  DSell d;
+  int64_t w = 0;
+  for (int64_t r = 0; r < A.n_rows; ++r) w = std::max(w, A.rowptr[r + 1] - A.rowptr[r]);
+  if (A.n_rows == 0 || w == 0 || w > kSellMaxWidth || A.n_rows > 0x7fffffffLL) return d;
+  const int64_t slices = (A.n_rows + 31) / 32;
+  const size_t len = static_cast<size_t>(slices * 32 * w);
+  std::vector<int> cols(len, -1);
+  std::vector<double> vals(len, 0.0);
+  for (int64_t r = 0; r < A.n_rows; ++r) {
+    const int64_t base = (r / 32) * 32 * w + (r % 32);
+    for (int64_t k = A.rowptr[r]; k < A.rowptr[r + 1]; ++k) {
+      const int64_t j = k - A.rowptr[r];
+      cols[static_cast<size_t>(base + 32 * j)] = A.cols[static_cast<size_t>(k)];
+      vals[static_cast<size_t>(base + 32 * j)] = A.vals[static_cast<size_t>(k)];
+    }
+  }
+  int* dc = mem.alloc<int>(len);
+  double* dv = mem.alloc<double>(len);
+  GNW_CUDA_CHECK(cudaMemcpyAsync(dc, cols.data(), len * sizeof(int), cudaMemcpyHostToDevice, s));
+  GNW_CUDA_CHECK(cudaMemcpyAsync(dv, vals.data(), len * sizeof(double), cudaMemcpyHostToDevice, s));
+  GNW_CUDA_CHECK(cudaStreamSynchronize(s));  // host vectors are temporaries
+  d.n_rows = static_cast<int>(A.n_rows);
+  d.width = static_cast<int>(w);
+  d.cols = dc;
+  d.vals = dv;
+  return d;
+}
+
 void DeviceAmg::reset() {
   bmem_.reset();
   bmem_b_ = 0;
@@ -56,7 +85,13 @@ void DeviceAmg::upload(const host::AmgHierarchy& h, cudaStream_t s) {
     if (l + 1 < L) {
       d.A = upload_csr(mem_, H.A, s);
       d.P = upload_csr(mem_, H.P, s);
-      d.R = upload_csr(mem_, host::transpose(H.P), s);
+      const host::Csr Rt = host::transpose(H.P);
+      d.R = upload_csr(mem_, Rt, s);
+      if (!std::getenv("GNW_VC_CSR")) {  // experiment switch: CSR thread-per-row kernels
+        d.As = upload_sell(mem_, H.A, s);
+        d.Ps = upload_sell(mem_, H.P, s);
+        d.Rs = upload_sell(mem_, Rt, s);
+      }
       // warp-per-row kernels once rows carry more than ~24 entries (C2: levels >= 2)
       constexpr double kWide = 24.0;
       d.wideA = H.A.nnz() > kWide * static_cast<double>(H.A.n_rows);

@@ -41,6 +41,8 @@ struct DeviceMemory {
 };
 
 DCsr upload_csr(DeviceMemory& mem, const host::Csr& A, cudaStream_t s);
+// SELL-32 copy of A (common.cuh); width 0 (nothing allocated) if a row exceeds kSellMaxWidth
+DSell upload_sell(DeviceMemory& mem, const host::Csr& A, cudaStream_t s);
 // sparse_matmul on the device, bit-identical to host::spgemm (spgemm.cu)
 host::Csr device_spgemm(const host::Csr& A, const host::Csr& B, cudaStream_t s);
 

@@ -115,6 +115,96 @@ struct DCsr {
   double* vals = nullptr;
 };
 
+// Device sliced-ELL copy of a CSR matrix (SELL-32): rows in slices of 32, each slice stores
+// `width` entries per row column-major, entry k of row r at
+// (r / 32) * 32 * width + k * 32 + r % 32.  A warp's k-th loads of cols/vals are then one
+// contiguous 128 B / 256 B segment, and every entry load of a row is independent of the
+// others (no rowptr -> cols -> x chain per entry).  Entries keep the CSR order of their row;
+// padding has col = -1 and is skipped, so a row sum adds exactly the CSR terms in the CSR
+// order (bit-identical to the CSR loop).  width = 0: not built (row longer than kSellMaxWidth).
+constexpr int kSellMaxWidth = 8;
+struct DSell {
+  int n_rows = 0, width = 0;
+  const int* cols = nullptr;
+  const double* vals = nullptr;
+};
+
+// sum_k vals[k] * (x[off + cols[k]] * sc)  (sc applied only when scaled), in CSR order
+template <int W>
+__device__ __forceinline__ double sell_row_w(const DSell& A, long long row, const double* __restrict__ x,
+                                             long long off, bool scaled, double sc) {
+  const long long base = (row >> 5) * 32LL * W + (row & 31);
+  int c[W];
+  double v[W];
+#pragma unroll
+  for (int k = 0; k < W; ++k) {
+    c[k] = __ldg(A.cols + base + 32 * k);
+    v[k] = __ldg(A.vals + base + 32 * k);
+  }
+#pragma unroll
+  for (int k = 0; k < W; ++k) {
+    const double xv = c[k] >= 0 ? x[off + c[k]] : 0.0;
+    v[k] = v[k] * (scaled ? xv * sc : xv);  // --fmad=false: same rounding as the CSR loop
+  }
+  double s = 0.0;
+#pragma unroll
+  for (int k = 0; k < W; ++k)
+    if (c[k] >= 0) s = s + v[k];
+  return s;
+}
+
+// the two halves of sell_row_w, so that the entry loads of several matrices (and of the
+// MINRES state) are all in flight before the first gather
+template <int W>
+__device__ __forceinline__ void sell_load(const DSell& A, long long row, int (&c)[W], double (&v)[W]) {
+  const long long base = (row >> 5) * 32LL * W + (row & 31);
+#pragma unroll
+  for (int k = 0; k < W; ++k) {
+    c[k] = __ldg(A.cols + base + 32 * k);
+    v[k] = __ldg(A.vals + base + 32 * k);
+  }
+}
+template <int W>
+__device__ __forceinline__ double sell_finish(const int (&c)[W], double (&v)[W], const double* __restrict__ x,
+                                              long long off, bool scaled, double sc) {
+#pragma unroll
+  for (int k = 0; k < W; ++k) {
+    const double xv = c[k] >= 0 ? x[off + c[k]] : 0.0;
+    v[k] = v[k] * (scaled ? xv * sc : xv);
+  }
+  double s = 0.0;
+#pragma unroll
+  for (int k = 0; k < W; ++k)
+    if (c[k] >= 0) s = s + v[k];
+  return s;
+}
+
+// sell_finish with the multiplicand of entry (row, c) given by f(c)
+template <int W, class F>
+__device__ __forceinline__ double sell_finish_f(const int (&c)[W], double (&v)[W], F f) {
+#pragma unroll
+  for (int k = 0; k < W; ++k) v[k] = v[k] * (c[k] >= 0 ? f(c[k]) : 0.0);
+  double s = 0.0;
+#pragma unroll
+  for (int k = 0; k < W; ++k)
+    if (c[k] >= 0) s = s + v[k];
+  return s;
+}
+
+__device__ __forceinline__ double sell_row(const DSell& A, long long row, const double* __restrict__ x, long long off,
+                                           bool scaled, double sc) {
+  switch (A.width) {
+    case 1: return sell_row_w<1>(A, row, x, off, scaled, sc);
+    case 2: return sell_row_w<2>(A, row, x, off, scaled, sc);
+    case 3: return sell_row_w<3>(A, row, x, off, scaled, sc);
+    case 4: return sell_row_w<4>(A, row, x, off, scaled, sc);
+    case 5: return sell_row_w<5>(A, row, x, off, scaled, sc);
+    case 6: return sell_row_w<6>(A, row, x, off, scaled, sc);
+    case 7: return sell_row_w<7>(A, row, x, off, scaled, sc);
+    default: return sell_row_w<8>(A, row, x, off, scaled, sc);
+  }
+}
+
 // ---------------------------------------------------------------- reductions
 // Deterministic block reduction: warp xor-tree, then warps in index order.
 template <int NV>
@@ -169,9 +259,23 @@ __device__ bool grid_reduce_last(double (&v)[NV], double* part, unsigned int* co
   double acc[NV];
 #pragma unroll
   for (int k = 0; k < NV; ++k) acc[k] = 0.0;
-  for (int b = threadIdx.x; b < (int)gridDim.x; b += blockDim.x)
+  // U strided partials per thread loaded at once, then added in the same order as the plain
+  // strided loop (same bits): the last block no longer pays one L2 round trip per partial
+  // while every other SM idles (k_saddle at n = 1024: 20488 blocks -> 80 round trips)
+  constexpr int U = NV >= 3 ? 2 : 8;  // NV = 3 kernels run at 32 registers
+  const int G = static_cast<int>(gridDim.x), bs = static_cast<int>(blockDim.x);
+  for (int b0 = threadIdx.x; b0 < G; b0 += U * bs) {
+    double t[U][NV];
 #pragma unroll
-    for (int k = 0; k < NV; ++k) acc[k] += __ldcg(&part[b * NV + k]);
+    for (int j = 0; j < U; ++j)
+#pragma unroll
+      for (int k = 0; k < NV; ++k) t[j][k] = b0 + j * bs < G ? __ldcg(&part[(b0 + j * bs) * NV + k]) : 0.0;
+#pragma unroll
+    for (int j = 0; j < U; ++j)
+      if (b0 + j * bs < G)
+#pragma unroll
+        for (int k = 0; k < NV; ++k) acc[k] += t[j][k];
+  }
   block_reduce<NV>(acc, smem);
 #pragma unroll
   for (int k = 0; k < NV; ++k) out[k] = acc[k];

@@ -261,7 +261,15 @@ void Context::upload_structure() {
   op_ = OperatorArgs{};
   op_.Q = upload_csr(mem_, Q_, s);
   op_.D = upload_csr(mem_, D_, s);
-  op_.Dt = upload_csr(mem_, host::transpose(D_), s);
+  {
+    const host::Csr Dt = host::transpose(D_);
+    op_.Dt = upload_csr(mem_, Dt, s);
+    if (!std::getenv("GNW_SADDLE_CSR")) {  // experiment switch: the CSR loops of round 1
+      op_.Qs = upload_sell(mem_, Q_, s);
+      op_.Ds = upload_sell(mem_, D_, s);
+      op_.Dts = upload_sell(mem_, Dt, s);
+    }
+  }
   op_.K = K_;
   op_.N = N_;
   dnib_ = mem_.alloc<double>(1);

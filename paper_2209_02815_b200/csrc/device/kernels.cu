@@ -264,25 +264,114 @@ __global__ void k_coarse_cholesky(const double* __restrict__ L, int n, VSel rs, 
   }
 }
 
+// The same four level kernels on the SELL-32 copies (common.cuh): every entry load of a row
+// is issued at once and coalesced across the warp; the row sums add the same terms in the
+// same order as the CSR loops above (bit-identical).
+template <int W>
+__global__ void __launch_bounds__(kTpb) k_vcs_down(DSell A, const double* __restrict__ wd, VSel rs,
+                                                   double* __restrict__ resid, const MinresState* st) {
+  griddep_wait();
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= A.n_rows) return;
+  int c[W];
+  double v[W];
+  sell_load<W>(A, i, c, v);
+  const double* __restrict__ r = vsel(rs, st);
+  const double s = sell_finish_f<W>(c, v, [&](int j) { return ldg(&wd[j]) * r[j]; });
+  resid[i] = r[i] + (-1.0 * s);
+}
+
+template <int W>
+__global__ void __launch_bounds__(kTpb) k_vcs_restrict(DSell R, const double* __restrict__ resid,
+                                                       double* __restrict__ rc) {
+  griddep_wait();
+  const int a = blockIdx.x * blockDim.x + threadIdx.x;
+  if (a >= R.n_rows) return;
+  int c[W];
+  double v[W];
+  sell_load<W>(R, a, c, v);
+  rc[a] = sell_finish_f<W>(c, v, [&](int j) { return resid[j]; });
+}
+
+template <int W>
+__global__ void __launch_bounds__(kTpb) k_vcs_up1(DSell P, const double* __restrict__ wd, VSel rs,
+                                                  const double* __restrict__ ec, double* __restrict__ x,
+                                                  const MinresState* st) {
+  griddep_wait();
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= P.n_rows) return;
+  int c[W];
+  double v[W];
+  sell_load<W>(P, i, c, v);
+  const double* __restrict__ r = vsel(rs, st);
+  const double s = sell_finish_f<W>(c, v, [&](int j) { return ec[j]; });
+  x[i] = ldg(&wd[i]) * r[i] + 1.0 * s;
+}
+
+template <int W>
+__global__ void __launch_bounds__(kTpb) k_vcs_up2(DSell A, const double* __restrict__ wd, VSel rs,
+                                                  const double* __restrict__ x, double* __restrict__ out,
+                                                  const MinresState* st) {
+  griddep_wait();
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= A.n_rows) return;
+  int c[W];
+  double v[W];
+  sell_load<W>(A, i, c, v);
+  const double* __restrict__ r = vsel(rs, st);
+  const double s = sell_finish_f<W>(c, v, [&](int j) { return x[j]; });
+  const double res = r[i] + (-1.0 * s);
+  out[i] = x[i] + ldg(&wd[i]) * res;
+}
+
+#define GNW_SELL_SWITCH(width, KER, ...)          \
+  switch (width) {                                \
+    case 1: KER(1, __VA_ARGS__); break;           \
+    case 2: KER(2, __VA_ARGS__); break;           \
+    case 3: KER(3, __VA_ARGS__); break;           \
+    case 4: KER(4, __VA_ARGS__); break;           \
+    case 5: KER(5, __VA_ARGS__); break;           \
+    case 6: KER(6, __VA_ARGS__); break;           \
+    case 7: KER(7, __VA_ARGS__); break;           \
+    default: KER(8, __VA_ARGS__); break;          \
+  }
+#define GNW_VCS_LAUNCH(W, ker, n, ...) GNW_LAUNCH(launch_k(ker<W>, grid_for(n), kTpb, 0, __VA_ARGS__))
+
 void note_launch(const char* what) { check_launch(what); }
 
 void vc_down(const DLevel& L, VSel r, double* resid, const MinresState* st, cudaStream_t s) {
   if (L.gA > 1) return vcg_down(L, r, resid, st, s);
+  if (L.As.width > 0) {
+    GNW_SELL_SWITCH(L.As.width, GNW_VCS_LAUNCH, k_vcs_down, L.n, s, L.As, L.wd, r, resid, st);
+    return check_launch("vcs_down");
+  }
   GNW_LAUNCH(launch_k(k_vc_down, grid_for(L.n), kTpb, 0, s, L.A, L.wd, r, resid, st));
   check_launch("vc_down");
 }
 void vc_restrict(const DLevel& L, const double* resid, double* rc, cudaStream_t s) {
   if (L.gR > 1) return vcg_restrict(L, resid, rc, s);
+  if (L.Rs.width > 0) {
+    GNW_SELL_SWITCH(L.Rs.width, GNW_VCS_LAUNCH, k_vcs_restrict, L.R.n_rows, s, L.Rs, resid, rc);
+    return check_launch("vcs_restrict");
+  }
   GNW_LAUNCH(launch_k(k_vc_restrict, grid_for(L.R.n_rows), kTpb, 0, s, L.R, resid, rc));
   check_launch("vc_restrict");
 }
 void vc_up1(const DLevel& L, VSel r, const double* ec, double* x, const MinresState* st, cudaStream_t s) {
   if (L.gP > 1) return vcg_up1(L, r, ec, x, st, s);
+  if (L.Ps.width > 0) {
+    GNW_SELL_SWITCH(L.Ps.width, GNW_VCS_LAUNCH, k_vcs_up1, L.n, s, L.Ps, L.wd, r, ec, x, st);
+    return check_launch("vcs_up1");
+  }
   GNW_LAUNCH(launch_k(k_vc_up1, grid_for(L.n), kTpb, 0, s, L.P, L.wd, r, ec, x, st));
   check_launch("vc_up1");
 }
 void vc_up2(const DLevel& L, VSel r, const double* x, double* out, const MinresState* st, cudaStream_t s) {
   if (L.gA > 1) return vcg_up2(L, r, x, out, st, s);
+  if (L.As.width > 0) {
+    GNW_SELL_SWITCH(L.As.width, GNW_VCS_LAUNCH, k_vcs_up2, L.n, s, L.As, L.wd, r, x, out, st);
+    return check_launch("vcs_up2");
+  }
   GNW_LAUNCH(launch_k(k_vc_up2, grid_for(L.n), kTpb, 0, s, L.A, L.wd, r, x, out, st));
   check_launch("vc_up2");
 }
@@ -622,28 +711,44 @@ void row_gemv(const double* A, int m, long long N, long long ld, VSel x, long lo
 // B = 16 (m >= 1024): the register budget of 5 CTAs per SM lets ptxas keep the 16 loads of a
 // batch in flight (with the default budget it interleaves them with the add chain at 32 registers)
 template <int B>
-__global__ void __launch_bounds__(kTpb, B >= 16 ? 5 : 8) k_saddle(OperatorArgs op, VSel xs, int scaled, const double* __restrict__ u,
+__global__ void __launch_bounds__(kTpb, B >= 16 ? 5 : 6) k_saddle(OperatorArgs op, VSel xs, int scaled, const double* __restrict__ u,
                                                  VSel ys, MinresState* st, int loop, int nb_edge,
                                                  double* part, unsigned* counter) {
   griddep_wait();
   extern __shared__ double usm[];
   __shared__ double red[kTpb / 32];
-  const double* __restrict__ z = vsel(xs, st);
-  double* __restrict__ y = vsel(ys, st);
-  const double sc = scaled ? st->inv_gamma : 1.0;
   double dotv[1] = {0.0};
   if (static_cast<int>(blockIdx.x) < nb_edge) {
     const long long e = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+    // unit-square RT0 rows (5 Q entries, 2 D^T entries; boundary rows padded): every entry
+    // load of the row is issued before the state load that selects z
+    const bool fast = e < op.K && op.Qs.width == 5 && op.Dts.width == 2;
+    int cq[5], ct[2];
+    double vq[5], vt[2];
+    if (fast) {
+      sell_load<5>(op.Qs, e, cq, vq);
+      sell_load<2>(op.Dts, e, ct, vt);
+    }
+    const double* __restrict__ z = vsel(xs, st);
+    double* __restrict__ y = vsel(ys, st);
+    const double sc = scaled ? st->inv_gamma : 1.0;
     if (e < op.K) {
-      double sq = 0.0;
-      for (int k = op.Q.rowptr[e]; k < op.Q.rowptr[e + 1]; ++k) {
-        const int c = op.Q.cols[k];
-        sq = sq + __ldg(&op.Q.vals[k]) * (scaled ? z[c] * sc : z[c]);
-      }
-      double sd = 0.0;
-      for (int k = op.Dt.rowptr[e]; k < op.Dt.rowptr[e + 1]; ++k) {
-        const long long c = op.K + op.Dt.cols[k];
-        sd = sd + __ldg(&op.Dt.vals[k]) * (scaled ? z[c] * sc : z[c]);
+      double sq = 0.0, sd = 0.0;
+      if (fast) {
+        sq = sell_finish<5>(cq, vq, z, 0, scaled, sc);
+        sd = sell_finish<2>(ct, vt, z, op.K, scaled, sc);
+      } else if (op.Qs.width > 0 && op.Dts.width > 0) {  // SELL-32: independent, coalesced entry loads
+        sq = sell_row(op.Qs, e, z, 0, scaled, sc);
+        sd = sell_row(op.Dts, e, z, op.K, scaled, sc);
+      } else {
+        for (int k = op.Q.rowptr[e]; k < op.Q.rowptr[e + 1]; ++k) {
+          const int c = op.Q.cols[k];
+          sq = sq + __ldg(&op.Q.vals[k]) * (scaled ? z[c] * sc : z[c]);
+        }
+        for (int k = op.Dt.rowptr[e]; k < op.Dt.rowptr[e + 1]; ++k) {
+          const long long c = op.K + op.Dt.cols[k];
+          sd = sd + __ldg(&op.Dt.vals[k]) * (scaled ? z[c] * sc : z[c]);
+        }
       }
       double o = 0.0;
       o = o + 1.0 * sq;  // spmv_add(*Q, zeta, 1.0, out1)
@@ -652,16 +757,29 @@ __global__ void __launch_bounds__(kTpb, B >= 16 ? 5 : 8) k_saddle(OperatorArgs o
       dotv[0] = o * (scaled ? z[e] * sc : z[e]);
     }
   } else {
-    if (op.m > 0) {
+    const long long c = static_cast<long long>(blockIdx.x - nb_edge) * blockDim.x + threadIdx.x;
+    const bool fast = c < op.N && op.Ds.width == 3;
+    int cd[3];
+    double vd[3];
+    if (fast) sell_load<3>(op.Ds, c, cd, vd);
+    const double* __restrict__ z = vsel(xs, st);
+    double* __restrict__ y = vsel(ys, st);
+    const double sc = scaled ? st->inv_gamma : 1.0;
+    if (op.m > 0 && op.q == nullptr) {  // the fused/lean loops read q instead of J^T (J zhat2)
       for (int t = threadIdx.x; t < op.m; t += blockDim.x) usm[t] = u[t];
       __syncthreads();
     }
-    const long long c = static_cast<long long>(blockIdx.x - nb_edge) * blockDim.x + threadIdx.x;
     if (c < op.N) {
       double sd = 0.0;
-      for (int k = op.D.rowptr[c]; k < op.D.rowptr[c + 1]; ++k) {
-        const int e = op.D.cols[k];
-        sd = sd + __ldg(&op.D.vals[k]) * (scaled ? z[e] * sc : z[e]);
+      if (fast) {
+        sd = sell_finish<3>(cd, vd, z, 0, scaled, sc);
+      } else if (op.Ds.width > 0) {
+        sd = sell_row(op.Ds, c, z, 0, scaled, sc);
+      } else {
+        for (int k = op.D.rowptr[c]; k < op.D.rowptr[c + 1]; ++k) {
+          const int e = op.D.cols[k];
+          sd = sd + __ldg(&op.D.vals[k]) * (scaled ? z[e] * sc : z[e]);
+        }
       }
       double o = 0.0;
       o = o + 1.0 * sd;  // spmv_add(*D, zeta, 1.0, out2)

@@ -20,6 +20,8 @@ struct DLevel {
   // lanes per row of the single-RHS kernels (vcycle_wide.cu): 1 = thread-per-row in the
   // reference order (kernels.cu), 2..32 = a G-lane group per row
   int gA = 1, gP = 1, gR = 1;
+  // SELL-32 copies for the thread-per-row kernels (same order, coalesced; width 0: CSR)
+  DSell As, Ps, Rs;
 };
 
 // Fused coarse tail of the single-RHS V-cycle (vcycle_tail.cu): levels l0..L-1
@@ -100,6 +102,7 @@ void transpose_batch_to_rows(const double* X, long long cols, long long ld, int 
 // ---------------------------------------------------------------- operator
 struct OperatorArgs {
   DCsr Q, D, Dt;       // Dt = D^T (rows = edges, columns = cells ascending)
+  DSell Qs, Ds, Dts;   // SELL-32 copies read by k_saddle (width 0: CSR loops)
   const double* J = nullptr;  // m x N row-major (nullptr: no low-rank term)
   int m = 0;
   long long K = 0, N = 0;
