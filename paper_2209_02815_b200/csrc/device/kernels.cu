@@ -244,6 +244,35 @@ __global__ void k_coarse_inverse(const double* __restrict__ Ainv, int n, VSel rs
   if (lane == 0) x[static_cast<long long>(i) * nrhs + q] = acc[0];
 }
 
+// Single right-hand side (the MINRES V-cycle's coarse / collapsed-tail apply, C2: n = 1147):
+// one warp per row with four independent accumulators, so each lane keeps four loads of the
+// row in flight instead of one dependent add chain of n / 32 L2 round trips (14 us at C2 with
+// one warp per SM).  Deterministic; not the reference order (the reference solves with the
+// Cholesky factor, k_coarse_cholesky, in exact mode).
+__global__ void k_coarse_inverse1(const double* __restrict__ Ainv, int n, VSel rs, double* __restrict__ x,
+                                  const MinresState* st) {
+  griddep_wait();
+  const double* __restrict__ r = vsel(rs, st);
+  const long long i = (static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (i >= n) return;
+  const double* __restrict__ row = Ainv + i * n;
+  double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+  int j = lane;
+  for (; j + 96 < n; j += 128) {
+    const double m0 = ldg(&row[j]), m1 = ldg(&row[j + 32]), m2 = ldg(&row[j + 64]), m3 = ldg(&row[j + 96]);
+    const double r0 = r[j], r1 = r[j + 32], r2 = r[j + 64], r3 = r[j + 96];
+    a0 = a0 + m0 * r0;
+    a1 = a1 + m1 * r1;
+    a2 = a2 + m2 * r2;
+    a3 = a3 + m3 * r3;
+  }
+  for (; j < n; j += 32) a0 = a0 + ldg(&row[j]) * r[j];
+  double acc[1] = {(a0 + a1) + (a2 + a3)};
+  warp_reduce<1>(acc);
+  if (lane == 0) x[i] = acc[0];
+}
+
 // cholesky_solve (linalg.cpp:107-123) replayed exactly, one thread per rhs column
 __global__ void k_coarse_cholesky(const double* __restrict__ L, int n, VSel rs, double* __restrict__ x,
                                   const MinresState* st, int nrhs, int ld) {
@@ -378,6 +407,10 @@ void vc_up2(const DLevel& L, VSel r, const double* x, double* out, const MinresS
 void coarse_inverse(const double* Ainv, int n, VSel r, double* x, const MinresState* st, int nrhs,
                     cudaStream_t s) {
   const long long threads = static_cast<long long>(n) * nrhs * 32;
+  if (nrhs == 1) {
+    GNW_LAUNCH(launch_k(k_coarse_inverse1, grid_for(threads, 128), 128, 0, s, Ainv, n, r, x, st));
+    return check_launch("coarse_inverse1");
+  }
   GNW_LAUNCH(launch_k(k_coarse_inverse, grid_for(threads), kTpb, 0, s, Ainv, n, r, x, st, nrhs));
   check_launch("coarse_inverse");
 }
