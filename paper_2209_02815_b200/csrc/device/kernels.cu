@@ -744,7 +744,7 @@ void row_gemv(const double* A, int m, long long N, long long ld, VSel x, long lo
 // B = 16 (m >= 1024): the register budget of 5 CTAs per SM lets ptxas keep the 16 loads of a
 // batch in flight (with the default budget it interleaves them with the add chain at 32 registers)
 template <int B>
-__global__ void __launch_bounds__(kTpb, B >= 16 ? 5 : 6) k_saddle(OperatorArgs op, VSel xs, int scaled, const double* __restrict__ u,
+__global__ void __launch_bounds__(kTpb, B >= 16 ? 5 : 8) k_saddle(OperatorArgs op, VSel xs, int scaled, const double* __restrict__ u,
                                                  VSel ys, MinresState* st, int loop, int nb_edge,
                                                  double* part, unsigned* counter) {
   griddep_wait();
