@@ -842,7 +842,7 @@ __global__ void __launch_bounds__(kTpb, B >= 16 ? 5 : 8) k_saddle(OperatorArgs o
 void saddle_operator(const OperatorArgs& op, VSel x, int scaled, const double* u, VSel y, MinresState* st,
                      int loop, double* partial, unsigned* counter, cudaStream_t s) {
   const int nbe = static_cast<int>(grid_for(op.K)), nbc = static_cast<int>(grid_for(op.N));
-  GNW_LAUNCH(launch_k(op.m >= kSweepBatchWideM ? k_saddle<16> : k_saddle<8>, nbe + nbc, kTpb, std::max(op.m, 1) * sizeof(double), s, op, x, scaled, u, y, st, loop, nbe,
+  GNW_LAUNCH(launch_k((op.m >= kSweepBatchWideM && op.q == nullptr) ? k_saddle<16> : k_saddle<8>, nbe + nbc, kTpb, op.q != nullptr ? 0 : std::max(op.m, 1) * sizeof(double), s, op, x, scaled, u, y, st, loop, nbe,
                                                                        partial, counter));
   check_launch("saddle_operator");
 }
