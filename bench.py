@@ -175,76 +175,150 @@ def cpu_sample(cfg, inp, alpha, iterations, k_cols=16, k_rows=16, k_iters=10, la
     t0 = time.time()
     s = p.sample_gnstep(inp.J, alpha, k_cols, k_rows, k_iters)
     wall = time.time() - t0
-    t_est = s["t_col"] * cfg.m + s["t_row"] * cfg.m + s["t_chol"] + s["t_iter"] * iterations
+    t_est = s["t_col"] * cfg.m + s["t_row"] * cfg.m + s["t_chol"] + s["t_minres0"] + s["t_iter"] * iterations
     sample = (f"reference (oracle/_ref, -O3 -DNDEBUG) on {label} alpha={alpha:g}: {k_cols} H columns (V-cycles), "
-              f"{k_rows} capacitance rows (matmul), full {cfg.m}x{cfg.m} Cholesky, {k_iters} MINRES iterations "
+              f"{k_rows} capacitance rows (matmul), full {cfg.m}x{cfg.m} Cholesky, MINRES runs of {k_iters} and "
+              f"{2 * k_iters} iterations (per-iteration cost and minres's fixed start-up separated) "
               f"({wall:.1f} s of CPU); per-unit times x (m={cfg.m} columns, m rows, {iterations} iterations) "
               f"-> t_norm = {t_est:.1f} s")
     return 1.0 / t_est, t_est, s, sample, o.kind
 
 
-_REF_JOB = None  # (cfg, inputs) shared with the forked reference workers
+def host_info() -> dict:
+    """The host the CPU legs ran on: logical CPUs, CPU model, memory."""
+    model = "unknown"
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name"):
+                    model = ln.split(":", 1)[1].strip()
+                    break
+    except Exception:
+        pass
+    mem = None
+    try:
+        import psutil
+        mem = round(psutil.virtual_memory().total / 2**30, 1)
+    except Exception:
+        pass
+    return {"nproc": os.cpu_count(), "cpu_model": model, "mem_gib": mem}
+
+
+def reference_iterations(config: str) -> dict:
+    """Per-alpha MINRES iteration counts of the reference's OWN full solves at tol 1e-8 on the
+    seeded bundle of `config` (committed fixtures, tests/golden/).  Empty when none exist."""
+    if config == "C2":
+        rec = c2_reference_record()
+        return {r["alpha"]: r["iterations"] for r in rec["runs"]} if rec else {}
+    return {}
 
 
 def _ref_worker(job):
-    cfg, inp = _REF_JOB
-    alpha, iters, kc, kr, ki, label = job
+    """One reference process (spawned, so the reference library is loaded by a fresh
+    interpreter): loads the shared bundle, runs the bounded sample or a full solve."""
+    path, n, m, thr, alpha, iters, kc, kr, ki, label, full = job
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import orc  # CPU baseline leg only
+    from paper_2209_02815_b200 import workload as W
+
+    d = np.load(path)
+    inp = _Inputs()
+    inp.mesh, inp.J, inp.dm, inp.dg = W.unit_square_mesh(n), d["J"], d["dm"], d["dg"]
+    cfg = _Cfg(n=n, m=m, coarse_threshold=thr)
+    if full:  # the whole t_norm measured: set_jacobian + assemble_gn_rhs + minres (inversion.cpp:242-271)
+        o = orc.Oracle("reference")
+        p = orc.Problem.mixed(o, inp.mesh, orc.AmgOpts.make(coarse_threshold=thr))
+        t0 = time.time()
+        p.set_jacobian(inp.J, alpha)
+        b = p.assemble_rhs(inp.dm, np.zeros(p.N), inp.dg, np.zeros(m))
+        x, rep = p.minres(b, tol=1e-8)
+        t = time.time() - t0
+        return t, (f"reference (oracle/_ref, -O3 -DNDEBUG) on {label} alpha={alpha:g}: one full GN-step solve "
+                   f"measured ({rep['iterations']} MINRES iterations, t_norm {t:.3f} s)"), o.kind
     v, t_est, s, sample, kind = cpu_sample(cfg, inp, alpha, iters, k_cols=kc, k_rows=kr, k_iters=ki, label=label)
     return t_est, sample, kind
 
 
-def ref_processes():
-    """Independent reference processes the host can run at once: one per core, capped by
-    memory (a C2 sample holds J, a J-sized H and the hierarchy: ~3 GB)."""
+def ref_processes(job_bytes: float):
+    """Independent reference processes the host can run at once: one per logical CPU, capped
+    by memory (a C2 sample holds J, a J-sized H and the hierarchy: ~3 GB).  Returns
+    (processes, memory_capped)."""
     n = os.cpu_count() or 1
+    capped = False
     try:
         import psutil
-        n = min(n, max(1, int(0.6 * psutil.virtual_memory().available / 3.2e9)))
+        by_mem = max(1, int(0.6 * psutil.virtual_memory().available / job_bytes))
+        capped = by_mem < n
+        n = min(n, by_mem)
     except Exception:
         pass
-    return max(1, n)
+    return max(1, n), capped
 
 
-def cpu_sample_parallel(cfg, inp, alpha, iterations, procs, k_cols, k_rows, k_iters, label):
-    """The reference is single-threaded: to use every host core the same bounded
-    sample runs as `procs` independent processes at once (one solve each); throughput is the
-    sum of their solves/s, each extrapolated from its own timings under the shared load."""
+def cpu_sample_parallel(path, cfg, alpha, iterations, procs, k_cols, k_rows, k_iters, label, full):
+    """The reference is single-threaded: to use every host core the same job runs as
+    `procs` independent spawned processes at once (one solve each); throughput is the sum of
+    their solves/s, each measured (or extrapolated from its own timings) under the shared load."""
     import multiprocessing as mp
 
-    global _REF_JOB
-    _REF_JOB = (cfg, inp)
-    job = (alpha, iterations, k_cols, k_rows, k_iters, label)
-    with mp.get_context("fork").Pool(procs) as pool:
+    job = (path, cfg.n, cfg.m, cfg.coarse_threshold, alpha, iterations, k_cols, k_rows, k_iters, label, full)
+    with mp.get_context("spawn").Pool(procs) as pool:
         res = pool.map(_ref_worker, [job] * procs)
     ts = [r[0] for r in res]
     value = sum(1.0 / t for t in ts)
     sample = (f"{procs} concurrent single-threaded reference processes, each: {res[0][1]}; "
-              f"per-process t_norm {min(ts):.1f}-{max(ts):.1f} s; value = sum of 1 / t_norm")
+              f"per-process t_norm {min(ts):.2f}-{max(ts):.2f} s; value = sum of 1 / t_norm")
     return value, ts, sample, res[0][2]
 
 
+def full_solve_record(config: str):
+    """A full reference solve timed on a GPU box's host (tools/ref_full_solve.py), used to check
+    the bounded sample's extrapolation: the model-to-measured ratio."""
+    try:
+        with open(os.path.join(ROOT, "profiles", f"ref_full_solve_{config}.json")) as f:
+            return json.load(f)
+    except Exception:
+        return None
+
+
 def run_reference(args):
-    """--impl reference: the reference's own CPU implementation, bounded samples per step, on
-    every host core (independent single-threaded solves in parallel)."""
+    """--impl reference: the reference's own CPU implementation on every host core.  C1: full
+    solves, measured.  C2: bounded samples per process (H columns, capacitance rows, Cholesky,
+    MINRES iterations) extrapolated with the reference's own iteration counts."""
     ws, rank, local = dist_env()
     if rank != 0:
         return
+    import tempfile
+
     from paper_2209_02815_b200 import workload as W
 
+    if args.config not in W.CONFIGS or args.config == "C3":
+        print(json.dumps({"impl": "reference", "unavailable": f"{args.config}: the reference would hold J and H "
+                          "(> 100 GB) on the host; SURVEY 8(c) reports the m=32 proxy instead"}), flush=True)
+        return
     cfg = W.CONFIGS[args.config]
     inp = W.gnstep_inputs(cfg.n, cfg.m, cfg.index)
-    rec = c2_reference_record()
-    iters = {r["alpha"]: r["iterations"] for r in rec["runs"]} if rec else {}
+    full = 8 * cfg.m * inp.mesh.n_cells < 64e6  # C1: a whole solve takes ~0.1 s -- measure it
+    iters = reference_iterations(args.config)
     alphas = list(cfg.alphas)
-    procs = ref_processes()
+    if not full and any(a not in iters for a in alphas):
+        raise RuntimeError(f"no reference iteration counts recorded for {args.config} (tests/golden)")
+    procs, capped = ref_processes(3.2e9 if not full else 0.2e9)
+    fd, path = tempfile.mkstemp(suffix=".npz", dir="/dev/shm" if os.path.isdir("/dev/shm") else None)
+    os.close(fd)
+    np.savez(path, J=inp.J, dm=inp.dm, dg=inp.dg)
     t_total, last = 0.0, None
-    for k in range(args.warmup + args.steps):
-        a = alphas[k % len(alphas)]
-        v, ts, sample, kind = cpu_sample_parallel(cfg, inp, a, iters.get(a, 88), procs, 8, 8, 4, args.config)
-        if k >= args.warmup:
-            t_total += 1.0 / v  # seconds per solve of the whole host
-            last = (sample, kind)
+    try:
+        for k in range(args.warmup + args.steps):
+            a = alphas[k % len(alphas)]
+            v, ts, sample, kind = cpu_sample_parallel(path, cfg, a, iters.get(a), procs, 8, 8, 4, args.config, full)
+            if k >= args.warmup:
+                t_total += 1.0 / v  # seconds per solve of the whole host
+                last = (sample, kind)
+    finally:
+        os.unlink(path)
     value = args.steps / t_total
+    rec = full_solve_record(args.config)
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t_total / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
@@ -254,7 +328,11 @@ def run_reference(args):
                                    f"one step = one full GN-step solve",
                        "mesh_n": cfg.n, "m": cfg.m, "alphas": alphas, "tol": 1e-8,
                        "parallelism": f"{procs} independent single-threaded reference processes"},
-            "cpu_baseline": {"value": value, "unit": UNIT, "cores": procs, "kind": last[1], "sample": last[0]},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": procs, "kind": last[1], "sample": last[0],
+                             "measured": "full solves" if full else "bounded samples, extrapolated",
+                             "host": host_info(), "memory_capped": capped,
+                             "iterations_source": "measured" if full else "tests/golden/c2_reference.json (reference runs)",
+                             "full_solve_check": rec},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -321,6 +399,17 @@ def make_problem(name, ctx, W, AmgOptions, torch):
     inp.rhs_mref, inp.rhs_gobs = np.zeros(N), np.zeros(cfg.m)
     ctx.assemble(inp.mesh, AmgOptions(coarse_threshold=cfg.coarse_threshold))
     return cfg, inp, None
+
+
+def dgemm_summary(sec: float, flops: float, m: int, N: int) -> dict:
+    """C = I + J H / beta: algorithmic 2 m^2 N flops, but C is symmetric and only the
+    lower-triangle 128 x 128 tiles run (kernels.cu k_dgemm_nt), so the roofline fraction is the
+    EXECUTED tile flops over the DMMA peak (128 flop/clk/SM x 148 SMs x 1.965 GHz)."""
+    tiles = -(-m // 128)
+    executed = tiles * (tiles + 1) // 2 * 128 * 128 * 2.0 * N
+    return {"ms": sec * 1e3, "algorithmic_TFLOPs": flops / sec / 1e12, "executed_TFLOPs": executed / sec / 1e12,
+            "frac_of_dmma_peak": executed / sec / 1e12 / 37.2, "dmma_peak_tflops": 37.2,
+            "note": "frac = executed lower-triangle tile flops / DMMA peak; algorithmic = 2 m^2 N / t"}
 
 
 def run_gnw(args):
@@ -396,9 +485,10 @@ def run_gnw(args):
     fused = ctx.stats()["fused_iterations"] > 0  # GNW_LOOP_AUTO runs tol 1e-8 on the fused/lean schedule
     lean = fused and ctx.loop_schedule() == "lean"
     kern = {}
-    # launches per MINRES iteration: k_row_gemv runs twice (J zhat2 and, inside
-    # combine_prec, H^T v2); everything else once.  The fused schedule drops the J zhat2
-    # GEMV and the saddle's J^T u sweep; its finish sweep reads H and J (q = J^T t').
+    # launches per MINRES iteration.  Reference schedule: k_row_gemv runs twice (J zhat2, and
+    # H^T v2 inside combine_prec).  The fused and lean schedules launch NO J zhat2 GEMV (u comes
+    # from t' by the Woodbury identity): their one k_row_gemv is the H^T v2 pass inside
+    # combine_prec, profiled alone as "row_gemv" (same kernel, same bytes) to attribute it.
     if lean:  # z2 = B (v2 - J^T t' / beta): a column sweep over J replaces the H t sweep
         per_iter = {"row_gemv": 1, "saddle_fused": 1, "combine_prec": 1, "col_sweep": 1, "finish_lean": 1,
                     "vcycle": 1, "update": 1}
@@ -406,10 +496,17 @@ def run_gnw(args):
         per_iter = {"row_gemv": 1, "saddle_fused": 1, "combine_prec": 1, "finish_fused": 1, "vcycle": 1, "update": 1}
     else:
         per_iter = {"row_gemv": 2, "saddle": 1, "combine_prec": 1, "finish_prec": 1, "vcycle": 1, "update": 1}
+    notes = {"row_gemv": ("J zhat2 and H^T v2 (the latter inside combine_prec)" if not fused else
+                          "H^T v2 only -- the k_row_gemv inside combine_prec, profiled alone; no J zhat2 GEMV runs"),
+             "combine_prec": "k_combine_elem + the H^T v2 k_row_gemv (not an extra sweep)",
+             "vcycle": "B y' (y' = v2 - q / beta) after the column sweep" if lean else "B v2 beside H^T v2",
+             "update": "standalone timing: its 0.13 GB working set is partly L2-resident; see iteration"}
     for name in per_iter:
         sec, byt = ctx.profile_kernel(name, reps=20)
         kern[name] = {"ms": sec * 1e3, "GB": byt / 1e9, "GBps": byt / sec / 1e9, "frac": byt / sec / 1e9 / hbm_peak,
                       "launches_per_iteration": per_iter[name]}
+        if name in notes:
+            kern[name]["note"] = notes[name]
     it_sec, it_bytes = ctx.profile_kernel("iteration")
     dg_sec, dg_flops = ctx.profile_kernel("dgemm", reps=5)
     # share of one iteration per kernel KIND (k_row_gemv: its own J pass + the H^T pass of combine_prec)
@@ -478,13 +575,14 @@ def run_gnw(args):
                "sample": f"not run: the reference holds J and H on the host ({16 * cfg.m * N / 1e9:.0f} GB), "
                          f"beside the e2e arm's pinned J (SURVEY.md 8(c): C3/C5 full m infeasible on the host)"}
     elif rank == 0 and ws == 1 and not args.no_cpu_baseline:
-        rec = c2_reference_record() if args.config == "C2" else None
         a_cpu = 1e-2 if 1e-2 in alphas else alphas[0]
-        it_ref = {r["alpha"]: r["iterations"] for r in rec["runs"]}.get(a_cpu) if rec else None
-        it_use = it_ref or next(s["iterations"] for s in per_step if s["alpha"] == a_cpu)
+        # the reference's own iteration count where a reference run is recorded, else the GPU's
+        # (iterations match within +-1: tests/test_gpu_golden.py)
+        it_use = reference_iterations(args.config).get(a_cpu) or next(
+            s["iterations"] for s in per_step if s["alpha"] == a_cpu)
         try:
             v, t_est, s, sample, kind = cpu_sample(cfg, inp, a_cpu, it_use, label=args.config)
-            cpu = {"value": v, "unit": UNIT, "cores": 1, "kind": kind, "sample": sample}
+            cpu = {"value": v, "unit": UNIT, "cores": 1, "kind": kind, "sample": sample, "host": host_info()}
         except Exception as e:  # reported, never silently replaced
             cpu = {"value": None, "unit": UNIT, "cores": 1, "kind": "reference", "sample": f"failed: {e}"}
 
@@ -511,9 +609,7 @@ def run_gnw(args):
                                        "GBps": it_bytes / it_sec / 1e9 if it_sec else None,
                                        "frac": it_bytes / it_sec / 1e9 / hbm_peak if it_sec else None},
                          "kernels": kern,
-                         "dgemm": {"ms": dg_sec * 1e3, "TFLOPs": dg_flops / dg_sec / 1e12,
-                                   "frac_of_dmma_peak": dg_flops / dg_sec / 1e12 / 37.2,
-                                   "note": "algorithmic 2 m^2 N; lower-triangle tiles only are executed"}},
+                         "dgemm": dgemm_summary(dg_sec, dg_flops, cfg.m, N)},
             "cpu_baseline": cpu,
             "e2e": {"value": ws * args.steps / e2e_elapsed, "unit": UNIT, "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h, "iterations": e2e_iters,

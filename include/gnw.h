@@ -118,6 +118,8 @@ typedef struct gnw_info {
   uint64_t m;            /* rows of J (0: Laplace-only) */
   double beta;
   uint64_t device_bytes; /* device memory held by the context */
+  int64_t collapse_level; /* first V-cycle level replaced by its dense collapsed map (-1: none) */
+  int64_t persist_level;  /* first level of the persistent small-level tail launch (-1: off) */
 } gnw_info;
 
 const char* gnw_last_error(void);
@@ -174,6 +176,11 @@ gnw_status gnw_assemble_rhs(gnw_ctx* ctx, const double* m, const double* m_ref,
                             const double* g, const double* g_obs, double* rhs);
 gnw_status gnw_minres_solve(gnw_ctx* ctx, const double* b, const double* x0, double* x,
                             double tol, uint64_t maxit, gnw_report* report);
+/* The full residual histories of the last gnw_minres_solve (MinresReport::relative_residuals
+ * and ::pnorm_relative_residuals, minres.hpp:15-16), for callers whose report capacity was
+ * smaller than n_hist: copies min(cap, n_hist) entries; *n_hist = the full length. */
+gnw_status gnw_minres_history(const gnw_ctx* ctx, double* relative_residuals,
+                              double* pnorm_relative_residuals, uint64_t cap, uint64_t* n_hist);
 
 /* Structure export for bit-exact parity checks (host arrays).  which: 0=Q 1=D
  * 2=S_hat 3=A_level 4=P_level; NULL arrays query sizes only. */

@@ -13,6 +13,7 @@
 // Errors are rethrown with the reference's exception types and message texts.
 #pragma once
 
+#include <algorithm>
 #include <cstdint>
 #include <stdexcept>
 #include <string>
@@ -108,7 +109,9 @@ class GnStepSolver {
   std::vector<double> minres(const std::vector<double>& b, const std::vector<double>& x0, double tol,
                              std::size_t maxit, MinresReport* report = nullptr) {
     std::vector<double> x(b.size());
-    std::vector<double> he(maxit + 1), hp(maxit + 1);
+    // histories: a small first buffer (not maxit + 1 -- 2 (K + N) is 42M at C3), the rest
+    // fetched after the solve only when the run was longer
+    std::vector<double> he(std::min<std::size_t>(maxit, 4095) + 1), hp(he.size());
     gnw_report r{};
     r.relative_residuals = he.data();
     r.pnorm_relative_residuals = hp.data();
@@ -118,6 +121,11 @@ class GnStepSolver {
       report->iterations = r.iterations;
       report->converged = r.converged != 0;
       report->true_relative_residual = r.true_relative_residual;
+      if (r.n_hist > he.size()) {
+        he.resize(r.n_hist);
+        hp.resize(r.n_hist);
+        throw_on(gnw_minres_history(ctx_, he.data(), hp.data(), he.size(), nullptr));
+      }
       const std::size_t nh = std::min<std::size_t>(r.n_hist, he.size());
       report->relative_residuals.assign(he.begin(), he.begin() + static_cast<std::ptrdiff_t>(nh));
       report->pnorm_relative_residuals.assign(hp.begin(), hp.begin() + static_cast<std::ptrdiff_t>(nh));

@@ -303,9 +303,9 @@ class Problem:
         fn = self.o.L.orc_sample_gnstep
         fn.argtypes = [C.c_void_p, C.c_void_p, _u64, C.c_double, _u64, _u64, _u64, _dp]
         J = np.ascontiguousarray(J, dtype=np.float64)
-        out = np.zeros(4)
+        out = np.zeros(5)
         self.o.check(fn(self.h, J.ctypes.data, J.shape[0], beta, k_cols, k_rows, k_iters, out))
-        return dict(t_col=out[0], t_row=out[1], t_chol=out[2], t_iter=out[3])
+        return dict(t_col=out[0], t_row=out[1], t_chol=out[2], t_iter=out[3], t_minres0=out[4])
 
     def H(self) -> np.ndarray:
         out = np.zeros(self.N * self.m)

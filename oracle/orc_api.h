@@ -95,9 +95,10 @@ int orc_minres(const orc_problem* p, const double* b, const double* x0, double t
                double* hist_pnorm, uint64_t hist_cap);
 
 /* Bounded timing sample of one GN-step solve (reference library only; see
- * ref_capi.cpp): out = {s per H column, s per C row, s Cholesky, s per MINRES iteration}. */
+ * ref_capi.cpp): out = {s per H column, s per C row, s Cholesky, s per MINRES iteration,
+ * s of minres's fixed start-up (r0 = b - A x0, first preconditioner application)}. */
 int orc_sample_gnstep(orc_problem* p, const double* J, uint64_t m, double beta, uint64_t k_cols,
-                      uint64_t k_rows, uint64_t k_iters, double out[4]);
+                      uint64_t k_rows, uint64_t k_iters, double out[5]);
 
 /* ERT forward model on the mixed problem's mesh: evaluate_response_and_jacobian
  * (forward.cpp:100-172) with Mesh::electrode_nodes = nodes, configs (a, b, m, n, k)

@@ -57,7 +57,7 @@ class Info(C.Structure):
     _fields_ = [("K", C.c_uint64), ("N", C.c_uint64), ("n_vertices", C.c_uint64),
                 ("n_edges", C.c_uint64), ("n_boundary_edges", C.c_uint64), ("n_levels", C.c_uint64),
                 ("coarse_n", C.c_uint64), ("m", C.c_uint64), ("beta", C.c_double),
-                ("device_bytes", C.c_uint64)]
+                ("device_bytes", C.c_uint64), ("collapse_level", C.c_int64), ("persist_level", C.c_int64)]
 
 
 class Stats(C.Structure):
@@ -72,7 +72,7 @@ EXPORTED = [
     "gnw_last_error", "gnw_version", "gnw_create", "gnw_destroy", "gnw_set_pointer_mode",
     "gnw_set_coarse_mode", "gnw_set_preconditioner", "gnw_set_loop_mode", "gnw_assemble", "gnw_assemble_amg_csr", "gnw_get_info",
     "gnw_set_jacobian", "gnw_prefetch_jacobian", "gnw_apply_operator", "gnw_precondition", "gnw_amg_apply",
-    "gnw_get_woodbury", "gnw_assemble_rhs", "gnw_minres_solve", "gnw_export_csr",
+    "gnw_get_woodbury", "gnw_assemble_rhs", "gnw_minres_solve", "gnw_minres_history", "gnw_export_csr",
     "gnw_export_mesh", "gnw_dense_cholesky", "gnw_get_stats", "gnw_event_record",
     "gnw_event_elapsed", "gnw_profile_kernel", "gnw_set_electrodes", "gnw_response_jacobian",
     "gnw_geometric_factor", "gnw_nccl_unique_id", "gnw_create_partitioned", "gnw_create_local_group",
@@ -144,6 +144,7 @@ def load() -> C.CDLL:
     L.gnw_get_woodbury.argtypes = [vp, vp, vp]
     L.gnw_assemble_rhs.argtypes = [vp, vp, vp, vp, vp, vp]
     L.gnw_minres_solve.argtypes = [vp, vp, vp, vp, dbl, u64, C.POINTER(Report)]
+    L.gnw_minres_history.argtypes = [vp, vp, vp, u64, C.POINTER(u64)]
     L.gnw_export_csr.argtypes = [vp, i32, u64, C.POINTER(u64), C.POINTER(u64), C.POINTER(u64), vp, vp, vp]
     L.gnw_export_mesh.argtypes = [vp, vp, vp, vp, vp, vp, vp]
     L.gnw_dense_cholesky.argtypes = [vp, u64, vp, vp]

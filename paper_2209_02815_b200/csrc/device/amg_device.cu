@@ -66,6 +66,8 @@ void DeviceAmg::reset() {
   bmem_b_ = 0;
   collapse_l_ = -1;
   collapse_M_ = nullptr;
+  persist_l_ = -1;
+  persist_dense_ = false;
   lv_.clear();
   mem_.release_all();
 }
@@ -92,11 +94,6 @@ void DeviceAmg::upload(const host::AmgHierarchy& h, cudaStream_t s) {
         d.Ps = upload_sell(mem_, H.P, s);
         d.Rs = upload_sell(mem_, Rt, s);
       }
-      // warp-per-row kernels once rows carry more than ~24 entries (C2: levels >= 2)
-      constexpr double kWide = 24.0;
-      d.wideA = H.A.nnz() > kWide * static_cast<double>(H.A.n_rows);
-      d.wideP = H.P.nnz() > kWide * static_cast<double>(H.P.n_rows);
-      d.wideR = H.P.nnz() > kWide * static_cast<double>(H.P.n_cols);
       d.gA = vc_group_lanes(H.A.nnz(), H.A.n_rows);
       d.gP = vc_group_lanes(H.P.nnz(), H.P.n_rows);
       d.gR = vc_group_lanes(H.P.nnz(), H.P.n_cols);
@@ -115,14 +112,6 @@ void DeviceAmg::upload(const host::AmgHierarchy& h, cudaStream_t s) {
     lv_.push_back(d);
   }
   nc_ = static_cast<int>(h.nc);
-  {  // fused tail candidates: trailing levels with <= 600k nonzeros each
-    constexpr int64_t kTailNnz = 600000;
-    const int Li = static_cast<int>(L);
-    int l0 = Li - 1;
-    while (l0 > 0 && h.levels[l0 - 1].A.nnz() <= kTailNnz && (Li - 1 - (l0 - 1)) <= kMaxTail) --l0;
-    tail_l0_ = l0;
-    if (const char* e = std::getenv("GNW_TAIL_CLUSTER")) tail_cluster = std::atoi(e);
-  }
   const std::vector<double> inv = host::cholesky_inverse(h.nc, h.coarse_chol);
   coarse_inv_ = mem_.alloc<double>(inv.size());
   coarse_L_ = mem_.alloc<double>(h.coarse_chol.size());
@@ -131,6 +120,51 @@ void DeviceAmg::upload(const host::AmgHierarchy& h, cudaStream_t s) {
                                  cudaMemcpyHostToDevice, s));
   GNW_CUDA_CHECK(cudaStreamSynchronize(s));
   build_collapse(s);
+  build_persist(s);
+}
+
+// The persistent small-level tail: from the first level with at most GNW_VC_PERSIST_ROWS rows
+// (default 65536; C2: level 2 of 10, 22 057 rows) down to the dense level -- the collapsed
+// operator, or the coarsest explicit inverse -- and back up.  Default (non-exact) mode only.
+void DeviceAmg::build_persist(cudaStream_t s) {
+  persist_l_ = -1;
+  persist_dense_ = false;
+  persist_ = PersistTail{};
+  int rows_max = 65536;
+  if (const char* e = std::getenv("GNW_VC_PERSIST_ROWS")) rows_max = std::atoi(e);
+  const int L = static_cast<int>(lv_.size());
+  if (rows_max <= 0 || L < 2) return;
+  const int stop = collapse_l_ > 0 ? collapse_l_ : L - 1;  // the dense level
+  int lp = stop;
+  while (lp > 0 && lv_[lp - 1].n <= rows_max && stop - (lp - 1) <= kMaxPersist) --lp;
+  PersistTail t;
+  t.nlev = stop - lp;
+  for (int k = 0; k < t.nlev; ++k) {
+    const DLevel& d = lv_[lp + k];
+    PersistLevel& p = t.lv[k];
+    p.A = d.A;
+    p.P = d.P;
+    p.R = d.R;
+    p.wd = d.wd;
+    p.n = d.n;
+    p.gA = d.gA;
+    p.gP = d.gP;
+    p.gR = d.gR;
+    p.r = vr_[lp + k];
+    p.res = vres_[lp + k];
+    p.x = vx_[lp + k];
+    p.e = ve_[lp + k];
+  }
+  t.M = stop == L - 1 && collapse_l_ <= 0 ? coarse_inv_ : collapse_M_;
+  t.nM = lv_[stop].n;
+  t.rM = vr_[stop];
+  t.eM = ve_[stop];
+  t.bar = mem_.alloc<unsigned>(2);
+  GNW_CUDA_CHECK(cudaMemsetAsync(t.bar, 0, 2 * sizeof(unsigned), s));
+  GNW_CUDA_CHECK(cudaStreamSynchronize(s));
+  persist_ = t;
+  persist_l_ = lp;
+  persist_dense_ = true;
 }
 
 // Collapsed coarse tail.  Below some level the V-cycle is a small LINEAR map of that
@@ -198,7 +232,6 @@ void DeviceAmg::cycle_levels(int l0, VSel r, double* out, const MinresState* st,
 DLevel DeviceAmg::level(int l, int exact) const {
   DLevel d = lv_[l];
   if (exact) {
-    d.wideA = d.wideP = d.wideR = 0;
     d.gA = d.gP = d.gR = 1;
   }
   return d;
@@ -206,61 +239,28 @@ DLevel DeviceAmg::level(int l, int exact) const {
 
 // amg.cpp:90-111, one symmetric V-cycle; level 0 input may be a ring slot.
 void DeviceAmg::vcycle(VSel r0, double* out0, const MinresState* st, int exact, cudaStream_t s) {
-  const int L = static_cast<int>(lv_.size());
-  if (tail_cluster <= 0 && L > 1) return cycle_levels(0, r0, out0, st, exact, !exact && collapse_l_ > 0, s);
-  auto coarse = [&](VSel r, double* x) {
+  if (lv_.size() == 1) {
     if (exact)
-      coarse_cholesky(coarse_L_, nc_, r, x, st, 1, 1, s);
+      coarse_cholesky(coarse_L_, nc_, r0, out0, st, 1, 1, s);
     else
-      coarse_inverse(coarse_inv_, nc_, r, x, st, 1, s);
-  };
-  if (L == 1) {
-    coarse(r0, out0);
+      coarse_inverse(coarse_inv_, nc_, r0, out0, st, 1, s);
     return;
   }
-  // levels [tail_l0_, L) run fused in one cluster launch when enabled (vcycle_tail.cu)
-  const int l0 = (tail_cluster > 0) ? tail_l0_ : L;
-  for (int l = 0; l < std::min(l0, L - 1); ++l) {
-    const VSel rl = l == 0 ? r0 : vfixed(vr_[l]);
-    const DLevel lev = level(l, exact);
-    vc_down(lev, rl, vres_[l], st, s);
-    vc_restrict(lev, vres_[l], vr_[l + 1], s);
-  }
-  if (l0 < L) {
-    TailArgs a;
-    a.nlev = L - 1 - l0;
-    for (int k = 0; k < a.nlev; ++k) {
-      const DLevel d = level(l0 + k, exact);
-      TailLevel& t = a.lv[k];
-      t.A = d.A;
-      t.P = d.P;
-      t.R = d.R;
-      t.wd = d.wd;
-      t.n = d.n;
-      t.wideA = d.wideA;
-      t.wideP = d.wideP;
-      t.wideR = d.wideR;
-      a.res[k] = vres_[l0 + k];
-      a.x[k] = vx_[l0 + k];
+  if (!exact && persist_l_ >= 0) {  // kernels down to persist_l_, then the persistent tail
+    auto at = [&](int l) { return l == 0 ? r0 : vfixed(vr_[l]); };
+    const int lp = persist_l_;
+    for (int l = 0; l < lp; ++l) {
+      vc_down(lv_[l], at(l), vres_[l], st, s);
+      vc_restrict(lv_[l], vres_[l], vr_[l + 1], s);
     }
-    for (int k = 0; k <= a.nlev; ++k) {
-      a.r[k] = vr_[l0 + k];
-      a.e[k] = ve_[l0 + k];
+    vcycle_persist(persist_, at(lp), lp == 0 ? out0 : ve_[lp], st, s);
+    for (int l = lp - 1; l >= 0; --l) {
+      vc_up1(lv_[l], at(l), ve_[l + 1], vx_[l], st, s);
+      vc_up2(lv_[l], at(l), vx_[l], l == 0 ? out0 : ve_[l], st, s);
     }
-    a.Ainv = coarse_inv_;
-    a.Lc = coarse_L_;
-    a.nc = nc_;
-    a.exact = exact;
-    vcycle_tail(a, l0 == 0 ? r0 : vfixed(vr_[l0]), l0 == 0 ? out0 : ve_[l0], st, tail_cluster, s);
-  } else {
-    coarse(vfixed(vr_[L - 1]), ve_[L - 1]);
+    return;
   }
-  for (int l = std::min(l0, L - 1) - 1; l >= 0; --l) {
-    const VSel rl = l == 0 ? r0 : vfixed(vr_[l]);
-    const DLevel lev = level(l, exact);
-    vc_up1(lev, rl, ve_[l + 1], vx_[l], st, s);
-    vc_up2(lev, rl, vx_[l], l == 0 ? out0 : ve_[l], st, s);
-  }
+  cycle_levels(0, r0, out0, st, exact, !exact && collapse_l_ > 0, s);
 }
 
 // Persistent work arrays of the batched V-cycle (b interleaved columns).

@@ -16,6 +16,8 @@
 namespace gnw {
 
 constexpr int kWarp = 32;
+// largest m whose m-vector is staged in shared memory by the dense sweeps (gnw_set_jacobian cap)
+constexpr int kMaxStageM = 8192;
 
 // Programmatic dependent launch: every kernel starts with griddep_wait(), so a
 // launch may be issued (and its CTAs made resident) while its predecessor on the
@@ -28,6 +30,10 @@ __device__ __forceinline__ void griddep_wait() {
 }
 
 extern bool g_pdl;  // launch with programmatic stream serialization (env GNW_PDL, default on)
+
+// Opts `fn` in to `bytes` of dynamic shared memory on the CURRENT device, once per
+// (kernel, device) pair; thread-safe (kernels.cu).  Throws on failure.
+void smem_optin(const void* fn, int bytes);
 
 template <typename... KArgs, typename... Args>
 inline cudaError_t launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,

@@ -59,6 +59,7 @@ Context::Context(int device) : device_(device) {
     for (auto& e : fork_ev_) GNW_CUDA_CHECK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   }
   for (auto& e : mev_) GNW_CUDA_CHECK(cudaEventCreate(&e));
+  for (auto& e : rhs_ev_) GNW_CUDA_CHECK(cudaEventCreate(&e));
   // host->device staging of the next Jacobian (prefetch_jacobian) runs on its own stream
   GNW_CUDA_CHECK(cudaStreamCreateWithFlags(&copy_, cudaStreamNonBlocking));
   for (auto& e : stage_ev_) GNW_CUDA_CHECK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
@@ -80,6 +81,8 @@ Context::~Context() {
   for (auto& e : events_)
     if (e) cudaEventDestroy(e);
   for (auto& e : jev_)
+    if (e) cudaEventDestroy(e);
+  for (auto& e : rhs_ev_)
     if (e) cudaEventDestroy(e);
   for (auto& e : mev_)
     if (e) cudaEventDestroy(e);
@@ -360,7 +363,7 @@ void Context::set_jacobian(const double* J, int64_t m, int64_t n_cells, double b
     pa_.Ht = pa_.Cinv = pa_.Lc = nullptr;
     return;
   }
-  if (m > 8192) throw std::invalid_argument("gnw_set_jacobian: m > 8192 not supported");
+  if (m > kMaxStageM) throw std::invalid_argument("gnw_set_jacobian: m > 8192 not supported");
 
   const cudaStream_t s = stream_;
   const long long Nl = local_n();  // columns of J / Ht held here (all N on one GPU)
@@ -546,7 +549,7 @@ void Context::prefetch_jacobian(const double* J, int64_t m, int64_t n_cells) {
   require_mixed();
   require_device();
   if (ptr_mode == 1) throw std::invalid_argument("gnw_prefetch_jacobian: host-pointer mode only");
-  if (J == nullptr || m <= 0 || m > 8192) throw std::invalid_argument("gnw_prefetch_jacobian: bad J");
+  if (J == nullptr || m <= 0 || m > kMaxStageM) throw std::invalid_argument("gnw_prefetch_jacobian: bad J");
   if (n_cells != local_n()) throw std::invalid_argument("gnw_prefetch_jacobian: J shape mismatch");
   const long long Nl = local_n();
   const long long ld = Nl + pad_;  // the owned copy's padded row stride (set_jacobian)
@@ -554,17 +557,22 @@ void Context::prefetch_jacobian(const double* J, int64_t m, int64_t n_cells) {
   // C3/C5 (J + H already take 127-137 GB of the 179) the rows that fit in what is left, and
   // set_jacobian copies only the remainder over PCIe.
   int64_t rows = m;
-  if (!stage_mem_ || stage_cap_ < static_cast<size_t>(m) * ld) {
+  // (re)size only when the shape changes: a partial stage (C3/C5) keeps its buffer across
+  // steps instead of re-entering this branch (device sync + a tens-of-GB free/malloc) each call
+  if (stage_key_m_ != m || stage_key_ld_ != ld) {
     GNW_CUDA_CHECK(cudaStreamSynchronize(copy_));
     sync();  // a pending consume of the old buffer
     stage_mem_.reset();
     stage_cap_ = 0;
+    stage_key_m_ = stage_key_ld_ = -1;
     size_t free_b = 0, total_b = 0;
     GNW_CUDA_CHECK(cudaMemGetInfo(&free_b, &total_b));
     const size_t margin = size_t{4} << 30;
     const size_t row_b = static_cast<size_t>(ld) * sizeof(double);
     rows = free_b > margin ? std::min<int64_t>(m, static_cast<int64_t>((free_b - margin) / row_b)) : 0;
     if (const char* e = std::getenv("GNW_STAGE_ROWS_MAX")) rows = std::min<int64_t>(rows, std::atoll(e));  // tests
+    stage_key_m_ = m;
+    stage_key_ld_ = ld;
     if (rows < std::max<int64_t>(1, m / 16)) {  // too little to matter: set_jacobian copies as usual
       staged_src_ = nullptr;
       stage_deferred_ = false;
@@ -574,6 +582,11 @@ void Context::prefetch_jacobian(const double* J, int64_t m, int64_t n_cells) {
     jstage_ = stage_mem_->alloc<double>(static_cast<size_t>(rows) * ld);
     stage_cap_ = static_cast<size_t>(rows) * ld;
     GNW_CUDA_CHECK(cudaEventRecord(stage_ev_[1], stream_));
+  }
+  if (stage_cap_ == 0) {  // this shape stages nothing (decided above on an earlier call)
+    staged_src_ = nullptr;
+    stage_deferred_ = false;
+    return;
   }
   rows = std::min<int64_t>(m, static_cast<int64_t>(stage_cap_ / static_cast<size_t>(ld)));
   staged_src_ = J;
@@ -722,33 +735,27 @@ void Context::assemble_rhs(const double* mdl, const double* mref, const double* 
   require_mixed();
   require_device();
   if (m_ == 0) throw std::invalid_argument("assemble_gn_rhs: shape mismatch");
-  std::vector<double> dg(m_);
-  std::vector<double> hg(m_), hgo(m_);
-  if (ptr_mode == 1) {
-    GNW_CUDA_CHECK(cudaMemcpy(hg.data(), g, m_ * sizeof(double), cudaMemcpyDeviceToHost));
-    GNW_CUDA_CHECK(cudaMemcpy(hgo.data(), gobs, m_ * sizeof(double), cudaMemcpyDeviceToHost));
-  } else {
-    std::memcpy(hg.data(), g, m_ * sizeof(double));
-    std::memcpy(hgo.data(), gobs, m_ * sizeof(double));
+  // g - g_obs is formed inside the rhs kernel (same subtraction as inversion.cpp:137-138):
+  // no device -> host round trip and no host sync before the launch
+  const double* dgv = g;
+  const double* dgo = gobs;
+  if (ptr_mode != 1) {
+    h2d(t_, g, m_, stream_);
+    h2d(t2_, gobs, m_, stream_);
+    dgv = t_;
+    dgo = t2_;
   }
-  for (int64_t i = 0; i < m_; ++i) dg[i] = hg[i] - hgo[i];  // inversion.cpp:137-138
-  cudaEvent_t e0, e1;
-  cudaEventCreate(&e0);
-  cudaEventCreate(&e1);
   double* dm = stage_in(mdl, N_, io_a_);
   double* dmr = stage_in(mref, N_, io_b_);
-  h2d(u_, dg.data(), m_, stream_);
   double* dr = ptr_mode == 1 ? rhs : io_c_;
-  cudaEventRecord(e0, stream_);
-  gnw::assemble_rhs(op_, beta_, dm, dmr, u_, dr, stream_);
+  GNW_CUDA_CHECK(cudaEventRecord(rhs_ev_[0], stream_));
+  gnw::assemble_rhs(op_, beta_, dm, dmr, dgv, dgo, dr, stream_);
   if (comm_) gather_cells(dr, stream_);  // J^T (g - g_obs) / beta was formed on each rank's own cells
-  cudaEventRecord(e1, stream_);
+  GNW_CUDA_CHECK(cudaEventRecord(rhs_ev_[1], stream_));
   stage_out(rhs, dr, K_ + N_);
   float ms = 0.f;
-  cudaEventElapsedTime(&ms, e0, e1);
+  GNW_CUDA_CHECK(cudaEventElapsedTime(&ms, rhs_ev_[0], rhs_ev_[1]));
   t_rhs = ms * 1e-3;
-  cudaEventDestroy(e0);
-  cudaEventDestroy(e1);
 }
 
 // ------------------------------------------------------------------ MINRES

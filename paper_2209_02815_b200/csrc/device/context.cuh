@@ -60,6 +60,8 @@ class Context {
   ~Context();
 
   bool has_device() const { return device_ >= 0; }
+  int vc_collapse_level() const { return damg_.collapse_level(); }
+  int vc_persist_level() const { return damg_.persist_level(); }
   int ptr_mode = 0;
   int coarse_mode = 0;
   int pc_laplace = 0;  // GnAlgorithm::kLaplaceMinres (inversion.cpp:251-256)
@@ -212,6 +214,7 @@ class Context {
   cudaEvent_t events_[16] = {};
   cudaEvent_t jev_[4] = {};    // set_jacobian phase timers
   cudaEvent_t mev_[2] = {};    // minres timers
+  cudaEvent_t rhs_ev_[2] = {};  // assemble_rhs timers
   int64_t jm_m_ = -1;          // shape of the persistent Jacobian buffers
   bool jm_owned_ = false;
   double* jown_ = nullptr;     // owned copy of J (host-pointer mode)
@@ -220,6 +223,8 @@ class Context {
   std::unique_ptr<DeviceMemory> stage_mem_;
   double* jstage_ = nullptr;
   size_t stage_cap_ = 0;
+  int64_t stage_key_m_ = -1;               // (m, row stride) the stage buffer was sized for
+  long long stage_key_ld_ = -1;
   const double* staged_src_ = nullptr;     // host J of the pending stage (nullptr: none)
   int64_t staged_m_ = -1;
   int64_t staged_rows_ = 0;                // leading rows of J staged (< m when only part fits)

@@ -14,6 +14,7 @@ using gnw::Context;
 
 struct gnw_ctx {
   Context* c = nullptr;
+  std::vector<double> hist_e, hist_p;  // residual histories of the last gnw_minres_solve
 };
 
 namespace {
@@ -155,6 +156,8 @@ gnw_status gnw_get_info(const gnw_ctx* ctx, gnw_info* info) {
     info->m = c.m();
     info->beta = c.beta();
     info->device_bytes = c.device_bytes();
+    info->collapse_level = c.has_device() ? c.vc_collapse_level() : -1;
+    info->persist_level = c.has_device() ? c.vc_persist_level() : -1;
   });
 }
 
@@ -196,6 +199,8 @@ gnw_status gnw_minres_solve(gnw_ctx* ctx, const double* b, const double* x0, dou
                             gnw_report* report) {
   return guard([&] {
     gnw::MinresResult r = ctx_of(ctx).minres(b, x0, x, tol, maxit);
+    ctx->hist_e = r.hist_e;
+    ctx->hist_p = r.hist_p;
     if (report) {
       report->iterations = r.iterations;
       report->converged = r.converged ? 1 : 0;
@@ -208,6 +213,18 @@ gnw_status gnw_minres_solve(gnw_ctx* ctx, const double* b, const double* x0, dou
       }
     }
   }, ctx);
+}
+
+gnw_status gnw_minres_history(const gnw_ctx* ctx, double* relative_residuals, double* pnorm_relative_residuals,
+                              uint64_t cap, uint64_t* n_hist) {
+  return guard([&] {
+    ctx_of(ctx);
+    const uint64_t n = ctx->hist_e.size();
+    if (n_hist) *n_hist = n;
+    const uint64_t h = std::min<uint64_t>(cap, n);
+    if (relative_residuals && h) std::memcpy(relative_residuals, ctx->hist_e.data(), h * sizeof(double));
+    if (pnorm_relative_residuals && h) std::memcpy(pnorm_relative_residuals, ctx->hist_p.data(), h * sizeof(double));
+  });
 }
 
 // ------------------------------------------------------- partitioned contexts

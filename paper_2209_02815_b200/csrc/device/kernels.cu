@@ -18,6 +18,8 @@
 #include <cmath>
 #include <cstdlib>
 #include <stdexcept>
+#include <mutex>
+#include <set>
 #include <string>
 
 #include "kernels.cuh"
@@ -158,6 +160,18 @@ __device__ __forceinline__ double ldg(const double* p) { return __ldg(p); }
 }  // namespace
 
 uint64_t launch_count() { return g_launches.load(std::memory_order_relaxed); }
+
+void smem_optin(const void* fn, int bytes) {
+  static std::mutex mu;
+  static std::set<std::pair<const void*, int>> done;  // (kernel, device)
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lock(mu);
+  if (e == cudaSuccess && done.count({fn, dev})) return;
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e != cudaSuccess) throw std::runtime_error(std::string("kernel launch failed: ") + cudaGetErrorString(e));
+  done.insert({fn, dev});
+}
 
 bool g_pdl = [] {
   const char* e = std::getenv("GNW_PDL");
@@ -841,6 +855,9 @@ __global__ void __launch_bounds__(kTpb, B >= 16 ? 5 : 8) k_saddle(OperatorArgs o
 
 void saddle_operator(const OperatorArgs& op, VSel x, int scaled, const double* u, VSel y, MinresState* st,
                      int loop, double* partial, unsigned* counter, cudaStream_t s) {
+  // u staged in shared memory for the J^T u column dot: m <= kMaxStageM doubles
+  smem_optin(reinterpret_cast<const void*>(k_saddle<8>), kMaxStageM * 8);
+  smem_optin(reinterpret_cast<const void*>(k_saddle<16>), kMaxStageM * 8);
   const int nbe = static_cast<int>(grid_for(op.K)), nbc = static_cast<int>(grid_for(op.N));
   GNW_LAUNCH(launch_k((op.m >= kSweepBatchWideM && op.q == nullptr) ? k_saddle<16> : k_saddle<8>, nbe + nbc, kTpb, op.q != nullptr ? 0 : std::max(op.m, 1) * sizeof(double), s, op, x, scaled, u, y, st, loop, nbe,
                                                                        partial, counter));
@@ -1095,12 +1112,9 @@ __global__ void __launch_bounds__(kTpb, B >= 16 ? 5 : 8) k_col_sweep(const doubl
 
 void col_sweep(const double* A, long long ld, const double* t, int m, long long n, double* q, cudaStream_t s,
                VSel ys, long long yoff, const MinresState* st, const double* coef, double* yout) {
-  static const bool once = [] {  // t staged in shared memory: m <= 8192 doubles
-    cudaFuncSetAttribute(k_col_sweep<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 8192 * 8);
-    cudaFuncSetAttribute(k_col_sweep<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 8192 * 8);
-    return true;
-  }();
-  (void)once;
+  // t staged in shared memory: m <= kMaxStageM doubles
+  smem_optin(reinterpret_cast<const void*>(k_col_sweep<8>), kMaxStageM * 8);
+  smem_optin(reinterpret_cast<const void*>(k_col_sweep<16>), kMaxStageM * 8);
   static const int wide_m = [] {  // env GNW_COL_SWEEP_WIDE_M: batch-16 threshold (experiments)
     const char* e = std::getenv("GNW_COL_SWEEP_WIDE_M");
     return e ? std::atoi(e) : kSweepBatchWideM;
@@ -1117,12 +1131,8 @@ int finish_blocks(const PrecArgs& pa) {
 void finish_precondition(const PrecArgs& pa, const double* svc, const double* t2, VSel vnext, VSel znext, int loop,
                          MinresState* st, const double* dots_edge, int n_edge_blocks, double* part,
                          unsigned* counter, cudaStream_t s) {
-  static const bool once = [] {  // t staged in shared memory: m <= 8192 doubles
-    cudaFuncSetAttribute(k_finish_prec<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 8192 * 8);
-    cudaFuncSetAttribute(k_finish_prec<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 8192 * 8);
-    return true;
-  }();
-  (void)once;
+  smem_optin(reinterpret_cast<const void*>(k_finish_prec<8>), kMaxStageM * 8);
+  smem_optin(reinterpret_cast<const void*>(k_finish_prec<16>), kMaxStageM * 8);
   GNW_LAUNCH(launch_k(pa.m >= kSweepBatchWideM ? k_finish_prec<16> : k_finish_prec<8>, finish_blocks(pa), kTpb,
                       std::max(pa.m, 1) * sizeof(double), s, pa, svc, t2, vnext, znext, loop, st, dots_edge,
                       n_edge_blocks, part, counter));
@@ -1390,8 +1400,9 @@ void dot(long long n, const double* a, const double* b, double* out, double* par
 
 // rhs = [-D^T (m - m_ref); J^T (g - g_obs) / beta]   inversion.cpp:126-146
 __global__ void __launch_bounds__(kTpb) k_rhs(OperatorArgs op, double beta, const double* __restrict__ mdl,
-                                              const double* __restrict__ mref, const double* __restrict__ dg,
-                                              double* __restrict__ rhs, int nb_edge) {
+                                              const double* __restrict__ mref, const double* __restrict__ g,
+                                              const double* __restrict__ gobs, double* __restrict__ rhs,
+                                              int nb_edge) {
   griddep_wait();
   extern __shared__ double gsm[];
   if (static_cast<int>(blockIdx.x) < nb_edge) {
@@ -1404,7 +1415,7 @@ __global__ void __launch_bounds__(kTpb) k_rhs(OperatorArgs op, double beta, cons
     }
     rhs[e] = -s;
   } else {
-    for (int t = threadIdx.x; t < op.m; t += blockDim.x) gsm[t] = dg[t];
+    for (int t = threadIdx.x; t < op.m; t += blockDim.x) gsm[t] = g[t] - gobs[t];  // inversion.cpp:137-138
     __syncthreads();
     const long long c = static_cast<long long>(blockIdx.x - nb_edge) * blockDim.x + threadIdx.x;
     if (c >= op.N || c < op.c_lo || (op.c_hi >= 0 && c >= op.c_hi)) return;  // partition: own cells only
@@ -1416,10 +1427,12 @@ __global__ void __launch_bounds__(kTpb) k_rhs(OperatorArgs op, double beta, cons
   }
 }
 
-void assemble_rhs(const OperatorArgs& op, double beta, const double* mdl, const double* mref, const double* dg,
-                  double* rhs, cudaStream_t s) {
+void assemble_rhs(const OperatorArgs& op, double beta, const double* mdl, const double* mref, const double* g,
+                  const double* gobs, double* rhs, cudaStream_t s) {
   const int nbe = static_cast<int>(grid_for(op.K)), nbc = static_cast<int>(grid_for(op.N));
-  GNW_LAUNCH(launch_k(k_rhs, nbe + nbc, kTpb, std::max(op.m, 1) * sizeof(double), s, op, beta, mdl, mref, dg, rhs, nbe));
+  smem_optin(reinterpret_cast<const void*>(k_rhs), kMaxStageM * 8);
+  GNW_LAUNCH(launch_k(k_rhs, nbe + nbc, kTpb, std::max(op.m, 1) * sizeof(double), s, op, beta, mdl, mref, g, gobs,
+                      rhs, nbe));
   check_launch("assemble_rhs");
 }
 
@@ -1600,11 +1613,7 @@ void capacitance_dgemm(const double* J, long long ldj, const double* Ht, long lo
       if (plan.full || j <= i) hp[np++] = make_int2(i, j);
   int2* dpairs = reinterpret_cast<int2*>(part + static_cast<long long>(plan.splits) * plan.npairs * dg::BM * dg::BN);
   cudaMemcpyAsync(dpairs, hp, np * sizeof(int2), cudaMemcpyHostToDevice, s);
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaFuncSetAttribute(k_dgemm_nt, cudaFuncAttributeMaxDynamicSharedMemorySize, dg::SMEM);
-    attr_set = true;
-  }
+  smem_optin(reinterpret_cast<const void*>(k_dgemm_nt), dg::SMEM);
   dim3 grid(plan.npairs, plan.splits);
   GNW_LAUNCH(launch_k(k_dgemm_nt, grid, 256, dg::SMEM, s, J, ldj, Ht, ldh, m, N, plan.kchunk, dpairs, plan.npairs, part));
   check_launch("dgemm_nt");

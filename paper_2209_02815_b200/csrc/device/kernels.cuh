@@ -15,8 +15,6 @@ struct DLevel {
   DCsr A, P, R;
   double* wd = nullptr;  // omega * inv_diag (rounded exactly as amg.cpp:98)
   int n = 0;             // rows of A
-  // warp-per-row flags of the fused cluster tail (vcycle_tail.cu)
-  int wideA = 0, wideP = 0, wideR = 0;
   // lanes per row of the single-RHS kernels (vcycle_wide.cu): 1 = thread-per-row in the
   // reference order (kernels.cu), 2..32 = a G-lane group per row
   int gA = 1, gP = 1, gR = 1;
@@ -24,27 +22,26 @@ struct DLevel {
   DSell As, Ps, Rs;
 };
 
-// Fused coarse tail of the single-RHS V-cycle (vcycle_tail.cu): levels l0..L-1
-// in one cluster launch.  Index k of the arrays is level l0 + k.
-constexpr int kMaxTail = 14;
-struct TailLevel {
+// The small levels of the single-RHS V-cycle plus its dense level in ONE persistent cooperative
+// launch with grid barriers between the phases (vcycle_persist.cu); bit-identical to the kernel
+// chain.  Level k of lv[] is hierarchy level l0 + k; its input r (level l0: the launch argument)
+// and output e; the dense operator M (n_M x n_M) maps rM to eM.
+constexpr int kMaxPersist = 6;
+struct PersistLevel {
   DCsr A, P, R;
   const double* wd = nullptr;
-  int n = 0;
-  int wideA = 0, wideP = 0, wideR = 0;
+  int n = 0, gA = 1, gP = 1, gR = 1;
+  double *r = nullptr, *res = nullptr, *x = nullptr, *e = nullptr;
 };
-struct TailArgs {
-  int nlev = 0;  // non-coarsest tail levels; level l0 + nlev is the coarsest
-  TailLevel lv[kMaxTail];
-  const double* Ainv = nullptr;  // coarsest explicit inverse
-  const double* Lc = nullptr;    // coarsest Cholesky factor (exact mode)
-  int nc = 0, exact = 0;
-  double* r[kMaxTail + 1] = {};
-  double* e[kMaxTail + 1] = {};
-  double* res[kMaxTail] = {};
-  double* x[kMaxTail] = {};
+struct PersistTail {
+  int nlev = 0;
+  PersistLevel lv[kMaxPersist];
+  const double* M = nullptr;
+  int nM = 0;
+  double *rM = nullptr, *eM = nullptr;
+  unsigned* bar = nullptr;  // 2 words, zero-initialised: grid barrier
 };
-void vcycle_tail(const TailArgs& a, VSel rin, double* out, const MinresState* st, int cluster, cudaStream_t s);
+void vcycle_persist(const PersistTail& t, VSel r, double* out, const MinresState* st, cudaStream_t s);
 
 // G-lanes-per-row kernels (vcycle_wide.cu), G = DLevel::gA / gR / gP
 void vcg_down(const DLevel& L, VSel r, double* resid, const MinresState* st, cudaStream_t s);
@@ -200,8 +197,9 @@ void dot(long long n, const double* a, const double* b, double* out, double* par
          cudaStream_t s);
 
 // rhs = [-D^T (m - m_ref); J^T (g - g_obs) / beta]  (inversion.cpp:126-146)
-void assemble_rhs(const OperatorArgs& op, double beta, const double* mdl, const double* mref,
-                  const double* dg, double* rhs, cudaStream_t s);
+// rhs = [-D^T (mdl - mref); J^T (g - gobs) / beta]  (assemble_gn_rhs, inversion.cpp:126-146)
+void assemble_rhs(const OperatorArgs& op, double beta, const double* mdl, const double* mref, const double* g,
+                  const double* gobs, double* rhs, cudaStream_t s);
 
 // ------------------------------------------------------------- dense / DMMA
 // C = I + (J Ht^T) / beta, lower triangle (or full) by split-K FP64 DMMA.

@@ -153,6 +153,49 @@ def test_operator_precondition_wide_m(oracle, gpu_ctx_factory):
     assert rel(xs, xr) <= 1e-8
 
 
+@pytest.mark.parametrize("mode", ["fused", "lean"])
+def test_wide_m_fused_and_lean_schedules(oracle, gpu_ctx_factory, mode):
+    """m >= 1024 on the schedules the C3/C5 benches run (tol 1e-8, GNW_LOOP_AUTO picks them):
+    k_saddle<8> with q in place of J^T u (no shared-memory stage) and k_col_sweep<16>."""
+    n, m = 24, 1100
+    mesh = W.unit_square_mesh(n)
+    J = W.synthetic_jacobian(m, mesh.n_cells, 7)
+    prob = orc.Problem.mixed(oracle, mesh)
+    ctx = gpu_ctx_factory(mesh, exact=False)
+    beta = 1e-2
+    ctx.set_loop_mode(mode)
+    ctx.set_jacobian(J, beta)
+    prob.set_jacobian(J, beta)
+    dg = W.gaussian(6, m)
+    b = prob.assemble_rhs(W.gaussian(7, prob.N), np.zeros(prob.N), dg, np.zeros(m))
+    xs, rep = ctx.minres(b, tol=1e-8)
+    assert ctx.loop_schedule() == mode and ctx.stats()["loop_restarts"] == 0
+    xr, rr = prob.minres(b, tol=1e-8)
+    assert rep.converged and abs(rep.iterations - rr["iterations"]) <= 1
+    xr12, _ = prob.minres(b, tol=1e-12)
+    assert rel(xs, xr12) <= 1e-6 and rel(xr, xr12) <= 1e-6
+
+
+def test_m_above_6144_launches(oracle, gpu_ctx_factory):
+    """set_jacobian accepts m <= 8192: the J^T u stage of k_saddle needs > 48 KB of shared
+    memory above m = 6144 (opted in per device, kernels.cu smem_optin)."""
+    n, m = 8, 6200
+    mesh = W.unit_square_mesh(n)
+    rng = np.random.default_rng(3)
+    J = rng.standard_normal((m, mesh.n_cells)) / np.sqrt(m * mesh.n_cells)
+    prob = orc.Problem.mixed(oracle, mesh)
+    ctx = gpu_ctx_factory(mesh, exact=False)
+    ctx.set_loop_mode("reference")
+    ctx.set_jacobian(J, 1.0)
+    prob.set_jacobian(J, 1.0)
+    x = W.gaussian(5, prob.K + prob.N)
+    assert rel(ctx.apply_operator(x), prob.apply_operator(x)) <= 1e-13
+    b = prob.assemble_rhs(W.gaussian(7, prob.N), np.zeros(prob.N), W.gaussian(6, m), np.zeros(m))
+    xs, rep = ctx.minres(b, tol=1e-10)
+    xr, rr = prob.minres(b, tol=1e-10)
+    assert abs(rep.iterations - rr["iterations"]) <= 1 and rel(xs, xr) <= 1e-7
+
+
 def test_operator_without_J_bitwise(c1, gpu_ctx_factory):
     mesh, inp, prob = c1[16]
     ctx = gpu_ctx_factory(mesh)
