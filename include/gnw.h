@@ -119,7 +119,6 @@ typedef struct gnw_info {
   double beta;
   uint64_t device_bytes; /* device memory held by the context */
   int64_t collapse_level; /* first V-cycle level replaced by its dense collapsed map (-1: none) */
-  int64_t persist_level;  /* first level of the persistent small-level tail launch (-1: off) */
 } gnw_info;
 
 const char* gnw_last_error(void);

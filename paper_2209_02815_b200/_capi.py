@@ -57,7 +57,7 @@ class Info(C.Structure):
     _fields_ = [("K", C.c_uint64), ("N", C.c_uint64), ("n_vertices", C.c_uint64),
                 ("n_edges", C.c_uint64), ("n_boundary_edges", C.c_uint64), ("n_levels", C.c_uint64),
                 ("coarse_n", C.c_uint64), ("m", C.c_uint64), ("beta", C.c_double),
-                ("device_bytes", C.c_uint64), ("collapse_level", C.c_int64), ("persist_level", C.c_int64)]
+                ("device_bytes", C.c_uint64), ("collapse_level", C.c_int64)]
 
 
 class Stats(C.Structure):

@@ -66,8 +66,6 @@ void DeviceAmg::reset() {
   bmem_b_ = 0;
   collapse_l_ = -1;
   collapse_M_ = nullptr;
-  persist_l_ = -1;
-  persist_dense_ = false;
   lv_.clear();
   mem_.release_all();
 }
@@ -76,6 +74,19 @@ void DeviceAmg::upload(const host::AmgHierarchy& h, cudaStream_t s) {
   reset();
   const double omega = h.options.jacobi_damping;
   const size_t L = h.levels.size();
+  // the dense tail starts at the collapse level (build_collapse's rule) or the coarsest level;
+  // the levels above it get the fused operators (env GNW_VC_FUSED=0: the four-pass levels)
+  const char* fe = std::getenv("GNW_VC_FUSED");
+  const bool fused_on = !(fe && std::atoi(fe) == 0);
+  int stop = static_cast<int>(L) - 1;
+  for (int l = 1; l + 1 < static_cast<int>(L); ++l)
+    if (h.levels[l].A.n_rows <= kCollapseMax) {
+      stop = l;
+      break;
+    }
+  if (const char* e = std::getenv("GNW_VC_COLLAPSE"))
+    if (std::atoi(e) == 0) stop = static_cast<int>(L) - 1;
+  fused_ = false;
   vr_.assign(L, nullptr);
   ve_.assign(L, nullptr);
   vres_.assign(L, nullptr);
@@ -102,6 +113,16 @@ void DeviceAmg::upload(const host::AmgHierarchy& h, cudaStream_t s) {
       d.wd = mem_.alloc<double>(wd.size());
       GNW_CUDA_CHECK(cudaMemcpyAsync(d.wd, wd.data(), wd.size() * sizeof(double), cudaMemcpyHostToDevice, s));
       GNW_CUDA_CHECK(cudaStreamSynchronize(s));
+      if (fused_on && static_cast<int>(l) < stop) {
+        fused_ = true;  // levels above the dense tail (vcycle_fused.cu)
+        const host::FusedCycleOps f = host::fused_cycle_ops(H.A, H.P, wd);
+        d.S = upload_csr(mem_, f.S, s);
+        d.T = upload_csr(mem_, f.T, s);
+        d.Tt = upload_csr(mem_, f.Tt, s);
+        d.gS = vc_group_lanes(f.S.nnz() + f.T.nnz(), f.S.n_rows);
+        d.gTt = vc_group_lanes(f.Tt.nnz(), f.Tt.n_rows);
+        d.fused = 1;
+      }
       vres_[l] = mem_.alloc<double>(d.n);
       vx_[l] = mem_.alloc<double>(d.n);
     }
@@ -120,51 +141,6 @@ void DeviceAmg::upload(const host::AmgHierarchy& h, cudaStream_t s) {
                                  cudaMemcpyHostToDevice, s));
   GNW_CUDA_CHECK(cudaStreamSynchronize(s));
   build_collapse(s);
-  build_persist(s);
-}
-
-// The persistent small-level tail: from the first level with at most GNW_VC_PERSIST_ROWS rows
-// (default 65536; C2: level 2 of 10, 22 057 rows) down to the dense level -- the collapsed
-// operator, or the coarsest explicit inverse -- and back up.  Default (non-exact) mode only.
-void DeviceAmg::build_persist(cudaStream_t s) {
-  persist_l_ = -1;
-  persist_dense_ = false;
-  persist_ = PersistTail{};
-  int rows_max = 65536;
-  if (const char* e = std::getenv("GNW_VC_PERSIST_ROWS")) rows_max = std::atoi(e);
-  const int L = static_cast<int>(lv_.size());
-  if (rows_max <= 0 || L < 2) return;
-  const int stop = collapse_l_ > 0 ? collapse_l_ : L - 1;  // the dense level
-  int lp = stop;
-  while (lp > 0 && lv_[lp - 1].n <= rows_max && stop - (lp - 1) <= kMaxPersist) --lp;
-  PersistTail t;
-  t.nlev = stop - lp;
-  for (int k = 0; k < t.nlev; ++k) {
-    const DLevel& d = lv_[lp + k];
-    PersistLevel& p = t.lv[k];
-    p.A = d.A;
-    p.P = d.P;
-    p.R = d.R;
-    p.wd = d.wd;
-    p.n = d.n;
-    p.gA = d.gA;
-    p.gP = d.gP;
-    p.gR = d.gR;
-    p.r = vr_[lp + k];
-    p.res = vres_[lp + k];
-    p.x = vx_[lp + k];
-    p.e = ve_[lp + k];
-  }
-  t.M = stop == L - 1 && collapse_l_ <= 0 ? coarse_inv_ : collapse_M_;
-  t.nM = lv_[stop].n;
-  t.rM = vr_[stop];
-  t.eM = ve_[stop];
-  t.bar = mem_.alloc<unsigned>(2);
-  GNW_CUDA_CHECK(cudaMemsetAsync(t.bar, 0, 2 * sizeof(unsigned), s));
-  GNW_CUDA_CHECK(cudaStreamSynchronize(s));
-  persist_ = t;
-  persist_l_ = lp;
-  persist_dense_ = true;
 }
 
 // Collapsed coarse tail.  Below some level the V-cycle is a small LINEAR map of that
@@ -175,7 +151,6 @@ void DeviceAmg::build_persist(cudaStream_t s) {
 // hierarchy by running the sub-cycle on the unit vectors.  Default mode only: the exact
 // mode keeps the reference's level-by-level order.  Env GNW_VC_COLLAPSE=0 disables it.
 void DeviceAmg::build_collapse(cudaStream_t s) {
-  constexpr int kCollapseMax = 2048;
   collapse_l_ = -1;
   collapse_M_ = nullptr;
   if (const char* e = std::getenv("GNW_VC_COLLAPSE"))
@@ -246,18 +221,14 @@ void DeviceAmg::vcycle(VSel r0, double* out0, const MinresState* st, int exact, 
       coarse_inverse(coarse_inv_, nc_, r0, out0, st, 1, s);
     return;
   }
-  if (!exact && persist_l_ >= 0) {  // kernels down to persist_l_, then the persistent tail
+  if (!exact && fused_) {  // one pass per level each way (vcycle_fused.cu)
+    const int L = static_cast<int>(lv_.size());
+    const int stop = collapse_l_ > 0 ? collapse_l_ : L - 1;
     auto at = [&](int l) { return l == 0 ? r0 : vfixed(vr_[l]); };
-    const int lp = persist_l_;
-    for (int l = 0; l < lp; ++l) {
-      vc_down(lv_[l], at(l), vres_[l], st, s);
-      vc_restrict(lv_[l], vres_[l], vr_[l + 1], s);
-    }
-    vcycle_persist(persist_, at(lp), lp == 0 ? out0 : ve_[lp], st, s);
-    for (int l = lp - 1; l >= 0; --l) {
-      vc_up1(lv_[l], at(l), ve_[l + 1], vx_[l], st, s);
-      vc_up2(lv_[l], at(l), vx_[l], l == 0 ? out0 : ve_[l], st, s);
-    }
+    for (int l = 0; l < stop; ++l) vcf_restrict(lv_[l], at(l), vr_[l + 1], st, s);
+    coarse_inverse(stop == L - 1 && collapse_l_ <= 0 ? coarse_inv_ : collapse_M_, lv_[stop].n, at(stop),
+                   stop == 0 ? out0 : ve_[stop], st, 1, s);
+    for (int l = stop - 1; l >= 0; --l) vcf_up(lv_[l], at(l), ve_[l + 1], l == 0 ? out0 : ve_[l], st, s);
     return;
   }
   cycle_levels(0, r0, out0, st, exact, !exact && collapse_l_ > 0, s);
@@ -310,6 +281,18 @@ bool DeviceAmg::vcycle_batch(const double* r0, int b, double* out0, int exact, c
     return false;
   }
   const int stop = (!exact && collapse_l_ > 0) ? collapse_l_ : L - 1;  // as in cycle_levels
+  if (!exact && fused_) {  // one pass per level each way (vcycle_fused.cu)
+    for (int l = 0; l < stop; ++l) mvcf_restrict(lv_[l], l == 0 ? r0 : mr_[l], mr_[l + 1], b, s);
+    if (stop == L - 1)
+      coarse(mr_[L - 1], me_[L - 1]);
+    else
+      dense_seq_batch(collapse_M_, lv_[stop].n, mr_[stop], me_[stop], b, s);
+    bool rows = false;
+    for (int l = stop - 1; l >= 0; --l)
+      rows = mvcf_up(lv_[l], l == 0 ? r0 : mr_[l], me_[l + 1], l == 0 ? out0 : me_[l], b, l == 0 ? ht : nullptr,
+                     ldh, s);
+    return rows;
+  }
   for (int l = 0; l < stop; ++l) {
     const double* rl = l == 0 ? r0 : mr_[l];
     const DLevel lev = level(l, 1);  // sequential row order on every level (see below)

@@ -67,7 +67,8 @@ class DeviceAmg {
   double* batch_out() const { return bX0_; }
 
   int collapse_level() const { return collapse_l_; }
-  int persist_level() const { return persist_.nlev > 0 || persist_dense_ ? persist_l_ : -1; }
+  bool fused() const { return fused_; }
+  static constexpr int kCollapseMax = 2048;  // dense collapsed tail from the first level this small
 
  private:
   DLevel level(int l, int exact) const;
@@ -75,12 +76,8 @@ class DeviceAmg {
   // collapse_l_ down are replaced by the dense operator collapse_M_ (default mode only).
   void cycle_levels(int l0, VSel r, double* out, const MinresState* st, int exact, bool collapse, cudaStream_t s);
   void build_collapse(cudaStream_t s);
-  void build_persist(cudaStream_t s);
-  // levels [persist_l_, collapse level) and the dense level as one persistent launch
-  // (vcycle_persist.cu); persist_l_ = -1: off (env GNW_VC_PERSIST_ROWS=0)
-  int persist_l_ = -1;
-  bool persist_dense_ = false;
-  PersistTail persist_{};
+
+  bool fused_ = false;             // fused per-level operators built (vcycle_fused.cu)
   int collapse_l_ = -1;           // first level with n <= kCollapseMax above the coarsest, or -1
   double* collapse_M_ = nullptr;  // n x n row-major: column j = the sub-cycle applied to e_j
   DeviceMemory mem_;

@@ -193,19 +193,12 @@ void Context::assemble(const double* vertices, int64_t nv, const int64_t* cells,
     dflag_ = mem_.alloc<int>(4);
     GNW_CUDA_CHECK(cudaMemsetAsync(counters_, 0, 16 * sizeof(unsigned), stream_));
     GNW_CUDA_CHECK(cudaMemsetAsync(st_plain_, 0, sizeof(MinresState), stream_));
-    upload_structure();
-    if (comm_) {  // cell partition (comm.cuh): J / H column slices and the J^T terms are rank-local
-      part_lo_ = partition_cells(N_, comm_->world);
-      for (int r = 0; r < comm_->world; ++r)
-        if (part_lo_[r + 1] == part_lo_[r])
-          throw std::invalid_argument("partition: a rank would own no cells (fewer than 64 cells per rank)");
-      c_lo_ = part_lo_[comm_->rank];
-      c_hi_ = part_lo_[comm_->rank + 1];
-      op_.c_lo = pa_.c_lo = c_lo_;
-      op_.c_hi = pa_.c_hi = c_hi_;
-      pa_.dist = 1;
+    if (comm_) {  // row partition (context_rowpart.cu): local operators, halos, partitioned V-cycle
+      setup_rowpart();
+    } else {
+      upload_structure();
+      upload_hierarchy();
     }
-    upload_hierarchy();
     sync();
   }
 }
@@ -286,7 +279,13 @@ void Context::upload_structure() {
   pa_.K = K_;
   pa_.N = N_;
   pa_.neg_inv_beta = dnib_;
-  const int64_t n = K_ + N_;
+  alloc_vectors(K_ + N_, K_, N_);
+}
+
+// MINRES work vectors of n_alloc entries (K edge rows + N cell rows, plus ghosts when
+// partitioned) and the per-block partial buffers of the fused reductions
+void Context::alloc_vectors(long long n_alloc, long long K, long long N) {
+  const int64_t n = n_alloc;
   b_ = mem_.alloc<double>(n);
   x_ = mem_.alloc<double>(n);
   r_ = mem_.alloc<double>(n);
@@ -297,20 +296,20 @@ void Context::upload_structure() {
     V_[k] = mem_.alloc<double>(n);
     W_[k] = mem_.alloc<double>(n);
     U_[k] = mem_.alloc<double>(n);
-    Vk_[k] = V_[k] + K_;
+    Vk_[k] = V_[k] + K;
   }
   for (int k = 0; k < 2; ++k) Z_[k] = mem_.alloc<double>(n);
   io_a_ = mem_.alloc<double>(n);
   io_b_ = mem_.alloc<double>(n);
   io_c_ = mem_.alloc<double>(n);
   io_d_ = mem_.alloc<double>(n);
-  const int64_t nb = (n + 255) / 256 + 16;
+  const int64_t nb = (K + N + 255) / 256 + 16;
   opart_ = mem_.alloc<double>(nb * 3);
   fpart_ = mem_.alloc<double>(nb * 3);
   upart_ = mem_.alloc<double>(nb * 3);
   rpart_ = mem_.alloc<double>(nb * 3);
-  plan_ = plan_h_ = row_gemv_plan(N_, 1);  // re-planned for the row count by set_jacobian
-  n_comb_blocks_ = combine_blocks(K_, N_);
+  plan_ = plan_h_ = row_gemv_plan(N, 1);  // re-planned for the row count by set_jacobian
+  n_comb_blocks_ = combine_blocks(K, N);
   cpart_ = mem_.alloc<double>(3 * (static_cast<size_t>(n_comb_blocks_) + 16));  // one triple per combine block
 }
 
@@ -323,6 +322,10 @@ void Context::upload_hierarchy() {
 // ----------------------------------------------------------------- V-cycle
 // amg.cpp:90-111, one symmetric V-cycle; level 0 input may be a ring slot.
 void Context::vcycle(VSel r0, double* out0, const MinresState* st, cudaStream_t s) {
+  if (comm_) {  // the partitioned V-cycle (part_amg.cuh), one-pass levels + replicated tail
+    if (coarse_mode == 1) throw std::invalid_argument("partitioned solve: the exact coarse mode is single-GPU only");
+    return pamg_->vcycle(r0, out0, st, stream_);
+  }
   damg_.vcycle(r0, out0, st, coarse_mode == 1, s ? s : stream_);
 }
 
@@ -389,8 +392,8 @@ void Context::set_jacobian(const double* J, int64_t m, int64_t n_cells, double b
     t_ = jm.alloc<double>(m);
     t2_ = jm.alloc<double>(m);
     tpart_ = jm.alloc<double>(static_cast<size_t>(plan_.nchunks) * m);
-    dq_ = jm.alloc<double>(N_);
-    bq_ = jm.alloc<double>(N_);
+    dq_ = jm.alloc<double>(std::max<long long>(nd(), 1));
+    bq_ = jm.alloc<double>(std::max<long long>(nd(), 1));
     cres_ = jm.alloc<double>(m);
     if (comm_) {
       const int P = comm_->world;
@@ -461,7 +464,7 @@ void Context::set_jacobian(const double* J, int64_t m, int64_t n_cells, double b
   // H = S_hat^-1 J^T by batched V-cycles (inversion.cpp:107-114); stored as Ht (m x N)
   {
     int b = damg_.batch_capacity();
-    if (b < ((m + 31) / 32) * 32 && b < 512) {
+    if (!comm_ && b < ((m + 31) / 32) * 32 && b < 512) {
       size_t free_b = 0, total_b = 0;
       cudaMemGetInfo(&free_b, &total_b);
       const double per_col = 8.0 * static_cast<double>(N_) * 8.0;  // level-0 arrays x ~2 for coarser levels
@@ -470,25 +473,16 @@ void Context::set_jacobian(const double* J, int64_t m, int64_t n_cells, double b
       b = static_cast<int>(std::min<int64_t>(((m + 31) / 32) * 32, bmax));
       damg_.ensure_batch(b);
     }
-    if (comm_) {  // every rank must use the same batch width: the smallest proposal
-      double mine = b;
-      GNW_CUDA_CHECK(cudaMemcpyAsync(t_part_, &mine, sizeof(double), cudaMemcpyHostToDevice, s));
-      comm_->allgather(t_part_, gath_, 1, s);
-      std::vector<double> all(comm_->world);
-      GNW_CUDA_CHECK(cudaMemcpyAsync(all.data(), gath_, all.size() * sizeof(double), cudaMemcpyDeviceToHost, s));
-      sync();
-      b = static_cast<int>(*std::min_element(all.begin(), all.end()));
-    }
-    for (int64_t i0 = 0; i0 < m; i0 += b) {
-      const int bb = static_cast<int>(std::min<int64_t>(b, m - i0));
-      if (comm_) {
-        build_h_partitioned(b);
-        break;
+    if (comm_) {
+      build_h_rowpart();
+    } else {
+      for (int64_t i0 = 0; i0 < m; i0 += b) {
+        const int bb = static_cast<int>(std::min<int64_t>(b, m - i0));
+        transpose_rows_to_batch(dJ_, N_, ldj_, static_cast<int>(i0), bb, damg_.batch_in(), s);
+        if (!damg_.vcycle_batch(damg_.batch_in(), bb, damg_.batch_out(), coarse_mode == 1, st_plain_, s,
+                                dHt_ + i0 * ldh_, ldh_))
+          transpose_batch_to_rows(damg_.batch_out(), N_, ldh_, static_cast<int>(i0), bb, dHt_, s);
       }
-      transpose_rows_to_batch(dJ_, N_, ldj_, static_cast<int>(i0), bb, damg_.batch_in(), s);
-      if (!damg_.vcycle_batch(damg_.batch_in(), bb, damg_.batch_out(), coarse_mode == 1, st_plain_, s,
-                              dHt_ + i0 * ldh_, ldh_))
-        transpose_batch_to_rows(damg_.batch_out(), N_, ldh_, static_cast<int>(i0), bb, dHt_, s);
     }
     GNW_CUDA_CHECK(cudaEventRecord(ev[1], s));
   }
@@ -614,15 +608,18 @@ void Context::issue_stage() {
 // fused: the MINRES loop's A zhat takes J^T u from q = J^T t' (fused_active()).
 void Context::operator_into(VSel x, int scaled, VSel y, MinresState* st, int loop, bool fused) {
   OperatorArgs op = op_;
-  if (comm_) {  // partitioned: u = sum_r J_r x_r, then the own-cell J^T u, gather, delta
-    if (m_ > 0) {
-      row_gemv(dJ_, static_cast<int>(m_), c_hi_ - c_lo_, ldj_, x, K_ + c_lo_, scaled, st, gpart_, counters_ + 0,
-               u_part_, plan_, stream_);
+  if (comm_) {  // partitioned: ghosts of x, u = sum_r J_r x_r (fixed-order), own rows, delta reduced
+    exchange_saddle(resolve(x));
+    if (fused) {
+      op.q = dq_;
+    } else if (m_ > 0) {
+      row_gemv(dJ_, static_cast<int>(m_), Nl_, ldj_, x, Kl_, scaled, st, gpart_, counters_ + 0, u_part_, plan_,
+               stream_);
       reduce_m(u_part_, u_, m_, stream_);
     }
     saddle_operator(op, x, scaled, u_, y, st, 0, opart_, counters_ + 1, stream_);
-    gather_cells(resolve(y), stream_);
-    dist_delta(op, x, scaled, y, st, loop, opart_, counters_ + 1, stream_);
+    reduce_scratch(st, 0, 1);
+    if (loop) delta_coef(st, stream_);
     return;
   }
   if (fused) {
@@ -635,7 +632,7 @@ void Context::operator_into(VSel x, int scaled, VSel y, MinresState* st, int loo
 }
 
 int Context::loop_sched() const {
-  if (!fused_ || fused_off_ || comm_ || m_ == 0 || pa_.m == 0 || dq_ == nullptr) return 0;
+  if (!fused_ || fused_off_ || m_ == 0 || pa_.m == 0 || dq_ == nullptr) return 0;
   if (fused_ != 2) return fused_ == 1 ? 1 : 2;
   if (auto_sched_) return auto_sched_;
   // auto: lean trades one dense sweep (8 m N bytes) for a second, serialised V-cycle, which
@@ -647,6 +644,12 @@ int Context::loop_sched() const {
 void Context::apply_operator(const double* x, double* y) {
   require_mixed();
   require_device();
+  if (comm_) {  // global x in (own entries and ghosts read from it), global y out
+    global_to_local(global_in(x, K_ + N_, gio_a_), io_a_, true);
+    operator_into(vfixed(io_a_), 0, vfixed(io_b_), st_plain_, 0);
+    local_to_global(io_b_, gio_b_);
+    return global_out(y, gio_b_, K_ + N_);
+  }
   const size_t n = K_ + N_;
   double* dx = stage_in(x, n, io_a_);
   double* dy = ptr_mode == 1 ? y : io_b_;
@@ -669,29 +672,34 @@ void Context::precondition_into(VSel y, VSel yv2, VSel z, MinresState* st, int l
   }
   const VSel az = loop ? vfixed(az_) : y;
   if (!(exp_skip_ & 4)) combine_elem(pa, az, vcur, vprev, y, z, loop, st, cpart_, stream_);
-  if (comm_) {  // partitioned: t = sum_r H_r^T y_r; z2 on own cells, gathered; then the Givens step
-    if (pa.m > 0) {
-      row_gemv(pa.Ht, pa.m, c_hi_ - c_lo_, pa.ldh, y, pa.K + c_lo_, 0, st, tpart_, counters_ + 2, t_part_, plan_h_, stream_);
-      reduce_m(t_part_, t_, pa.m, stream_);
+  // partitioned: the m-partials of the row GEMVs and the finish kernel's dots are summed over the
+  // ranks (fixed order) before anything reads them
+  double* tdst = comm_ ? t_part_ : t_;
+  auto reduce_t = [&]() {
+    if (comm_) reduce_m(t_part_, t_, pa.m, stream_);
+  };
+  auto finish = [&](const PrecArgs& pf) {
+    finish_precondition(pf, svc_, t2_, y, z, comm_ ? 0 : loop, st, cpart_, n_comb_blocks_, fpart_, counters_ + 3,
+                        stream_);
+    if (comm_) {
+      reduce_scratch(st, 0, 3);
+      if (loop) givens_from_scratch(st, stream_);
     }
-    vcycle(yv2, svc_, st);
-    capacitance_solve(pa, t_, t2_, stream_);
-    finish_precondition(pa, svc_, t2_, y, z, loop, st, cpart_, n_comb_blocks_, fpart_, counters_ + 3, stream_);
-    gather_cells(resolve(z), stream_);
-    dist_givens(pa, y, z, loop, st, cpart_, n_comb_blocks_, fpart_, counters_ + 3, stream_);
-    return;
-  }
+  };
   if (sched == 2) {
     // lean: H = B J^T and B is linear, so z2 = B v2 - H t' / beta = B (v2 - J^T t' / beta).
     // Two dense sweeps (t = H^T v2; q = J^T t', which is also the next operator's J^T u up
     // to 1 / gamma) and ONE V-cycle, on the sweep's output y' = v2 - q / beta.
-    if (!(exp_skip_ & 8)) row_gemv(pa.Ht, pa.m, pa.N, pa.ldh, y, pa.K, 0, st, tpart_, counters_ + 2, t_, plan_, stream_);
+    if (!(exp_skip_ & 8)) {
+      row_gemv(pa.Ht, pa.m, pa.N, pa.ldh, y, pa.K, 0, st, tpart_, counters_ + 2, tdst, plan_, stream_);
+      reduce_t();
+    }
     if (!(exp_skip_ & 32)) capacitance_solve(pa, t_, t2_, stream_);
-    if (!(exp_skip_ & 256)) col_sweep(dJ_, ldj_, t2_, pa.m, N_, dq_, stream_, y, pa.K, st, pa.neg_inv_beta, bq_);
+    if (!(exp_skip_ & 256)) col_sweep(dJ_, ldj_, t2_, pa.m, pa.N, dq_, stream_, y, pa.K, st, pa.neg_inv_beta, bq_);
     if (!(exp_skip_ & 16)) vcycle(vfixed(bq_), svc_, st);
     PrecArgs pf = pa;
     pf.m = 0;  // z2 = B y' is the V-cycle's output: the finish step is elementwise
-    if (!(exp_skip_ & 64)) finish_precondition(pf, svc_, t2_, y, z, loop, st, cpart_, n_comb_blocks_, fpart_, counters_ + 3, stream_);
+    if (!(exp_skip_ & 64)) finish(pf);
     return;
   }
   // s = B y2 and t = H^T y2 both read only y2: the V-cycle (latency-bound, few
@@ -703,17 +711,26 @@ void Context::precondition_into(VSel y, VSel yv2, VSel z, MinresState* st, int l
     if (!(exp_skip_ & 16)) vcycle(yv2, svc_, st, side_);
     GNW_CUDA_CHECK(cudaEventRecord(fork_ev_[1], side_));
   }
-  if (pa.m > 0 && !(exp_skip_ & 8))  // t = H^T v2 (matvec_transpose(h_hat, y2), inversion.cpp:82)
-    row_gemv(pa.Ht, pa.m, pa.N, pa.ldh, y, pa.K, 0, st, tpart_, counters_ + 2, t_, plan_h_, stream_);
+  if (pa.m > 0 && !(exp_skip_ & 8)) {  // t = H^T v2 (matvec_transpose(h_hat, y2), inversion.cpp:82)
+    row_gemv(pa.Ht, pa.m, pa.N, pa.ldh, y, pa.K, 0, st, tpart_, counters_ + 2, tdst, plan_h_, stream_);
+    reduce_t();
+  }
   if (!fork && !(exp_skip_ & 16)) vcycle(yv2, svc_, st);
   if (!(exp_skip_ & 32)) capacitance_solve(pa, t_, t2_, stream_);
   if (fork) GNW_CUDA_CHECK(cudaStreamWaitEvent(stream_, fork_ev_[1], 0));
-  if (!(exp_skip_ & 64)) finish_precondition(pa, svc_, t2_, y, z, loop, st, cpart_, n_comb_blocks_, fpart_, counters_ + 3, stream_);
+  if (!(exp_skip_ & 64)) finish(pa);
 }
 
 void Context::precondition(const double* y, double* z) {
   require_mixed();
   require_device();
+  if (comm_) {
+    global_to_local(global_in(y, K_ + N_, gio_a_), io_a_, false);
+    precondition_into(vfixed(io_a_), vfixed(io_a_ + Kl_), vfixed(io_b_), st_plain_, 0, vfixed(io_a_), vfixed(io_a_),
+                      loop_sched());
+    local_to_global(io_b_, gio_b_);
+    return global_out(z, gio_b_, K_ + N_);
+  }
   const size_t n = K_ + N_;
   double* dy = stage_in(y, n, io_a_);
   double* dz = ptr_mode == 1 ? z : io_b_;
@@ -724,6 +741,20 @@ void Context::precondition(const double* y, double* z) {
 void Context::amg_apply(const double* r, double* z) {
   if (!assembled_) throw std::invalid_argument("amg_apply: empty hierarchy");
   require_device();
+  if (comm_) {  // the partitioned V-cycle on the own cells of a global r; global z
+    const double* g = global_in(r, N_, gio_c_);
+    GNW_CUDA_CHECK(cudaMemcpyAsync(io_a_, g + c_lo_, Nl_ * sizeof(double), cudaMemcpyDeviceToDevice, stream_));
+    vcycle(vfixed(io_a_), io_b_, st_plain_);
+    GNW_CUDA_CHECK(cudaMemcpyAsync(gio_d_ + c_lo_, io_b_, Nl_ * sizeof(double), cudaMemcpyDeviceToDevice, stream_));
+    const int P = comm_->world;
+    std::vector<long long> off(P), cnt(P);
+    for (int q = 0; q < P; ++q) {
+      off[q] = part_lo_[q];
+      cnt[q] = part_lo_[q + 1] - part_lo_[q];
+    }
+    comm_->allgatherv(gio_d_, off, cnt, stream_);
+    return global_out(z, gio_d_, N_);
+  }
   const size_t n = N_;
   double* dr = stage_in(r, n, io_a_);
   double* dz = ptr_mode == 1 ? z : io_b_;
@@ -745,14 +776,25 @@ void Context::assemble_rhs(const double* mdl, const double* mref, const double* 
     dgv = t_;
     dgo = t2_;
   }
-  double* dm = stage_in(mdl, N_, io_a_);
-  double* dmr = stage_in(mref, N_, io_b_);
-  double* dr = ptr_mode == 1 ? rhs : io_c_;
-  GNW_CUDA_CHECK(cudaEventRecord(rhs_ev_[0], stream_));
-  gnw::assemble_rhs(op_, beta_, dm, dmr, dgv, dgo, dr, stream_);
-  if (comm_) gather_cells(dr, stream_);  // J^T (g - g_obs) / beta was formed on each rank's own cells
-  GNW_CUDA_CHECK(cudaEventRecord(rhs_ev_[1], stream_));
-  stage_out(rhs, dr, K_ + N_);
+  if (comm_) {  // own edges read m - m_ref on their ghost cells too (cell layout of the local D^T)
+    const double* gm = global_in(mdl, N_, gio_c_);
+    gather_rows(cell_l2g_, n_cell_l2g_, gm, io_a_, 1, stream_);
+    const double* gr = global_in(mref, N_, gio_d_);
+    gather_rows(cell_l2g_, n_cell_l2g_, gr, io_b_, 1, stream_);
+    GNW_CUDA_CHECK(cudaEventRecord(rhs_ev_[0], stream_));
+    gnw::assemble_rhs(op_, beta_, io_a_, io_b_, dgv, dgo, io_c_, stream_);
+    GNW_CUDA_CHECK(cudaEventRecord(rhs_ev_[1], stream_));
+    local_to_global(io_c_, gio_b_);
+    global_out(rhs, gio_b_, K_ + N_);
+  } else {
+    double* dm = stage_in(mdl, N_, io_a_);
+    double* dmr = stage_in(mref, N_, io_b_);
+    double* dr = ptr_mode == 1 ? rhs : io_c_;
+    GNW_CUDA_CHECK(cudaEventRecord(rhs_ev_[0], stream_));
+    gnw::assemble_rhs(op_, beta_, dm, dmr, dgv, dgo, dr, stream_);
+    GNW_CUDA_CHECK(cudaEventRecord(rhs_ev_[1], stream_));
+    stage_out(rhs, dr, K_ + N_);
+  }
   float ms = 0.f;
   GNW_CUDA_CHECK(cudaEventElapsedTime(&ms, rhs_ev_[0], rhs_ev_[1]));
   t_rhs = ms * 1e-3;
@@ -767,10 +809,15 @@ void Context::launch_iteration(unsigned long long cond_handle, int use_cond) {
   operator_into(ring2(Z_, 0), 1, vfixed(az_), st_, 1, sc != 0);             // Az = A zhat, delta
   precondition_into(ring3(V_, 2), ring3(Vk_, 2), ring2(Z_, 1), st_, 1,       // v_next, z_next = P^-1 v_next,
                     ring3(V_, 1), ring3(V_, 0), sc);                         // gamma_next, Givens
-  if (!(exp_skip_ & 128))
-    minres_update(K_ + N_, ring2(Z_, 0), vfixed(az_), ring3(W_, 0), ring3(W_, 1), ring3(W_, 2), ring3(U_, 0),
+  if (!(exp_skip_ & 128)) {
+    minres_update(kd() + nd(), ring2(Z_, 0), vfixed(az_), ring3(W_, 0), ring3(W_, 1), ring3(W_, 2), ring3(U_, 0),
                   ring3(U_, 1), ring3(U_, 2), x_, r_, st_, hist_e_, hist_p_, hist_cap_, upart_, counters_ + 4,
-                  cond_handle, use_cond, stream_);
+                  cond_handle, comm_ ? 3 : use_cond, stream_);
+    if (comm_) {  // ||r||^2 over the ranks, then the loop-control epilogue on every rank
+      reduce_scratch(st_, 6, 1);
+      update_tail_from_scratch(st_, hist_e_, hist_p_, hist_cap_, stream_);
+    }
+  }
 }
 
 void Context::build_graph() {
@@ -814,7 +861,7 @@ MinresResult Context::minres(const double* b, const double* x0, double* x, doubl
   if (!(tol > 0.0)) throw std::invalid_argument("minres: tol must be positive");
   require_mixed();
   require_device();
-  const int64_t n = K_ + N_;
+  const int64_t n = kd() + nd();  // own rows (partitioned: b and x0 are global, taken apart below)
   const cudaStream_t s = stream_;
   MinresResult res;
   const uint64_t l0 = launch_count();
@@ -832,7 +879,10 @@ MinresResult Context::minres(const double* b, const double* x0, double* x, doubl
   cudaEvent_t e0, e1;
   GNW_CUDA_CHECK(cudaEventCreate(&e0));
   GNW_CUDA_CHECK(cudaEventCreate(&e1));
-  if (ptr_mode == 1) {
+  if (comm_) {
+    global_to_local(global_in(b, K_ + N_, gio_a_), b_, false);
+    global_to_local(global_in(x0, K_ + N_, gio_b_), x_, false);
+  } else if (ptr_mode == 1) {
     GNW_CUDA_CHECK(cudaMemcpyAsync(b_, b, n * sizeof(double), cudaMemcpyDeviceToDevice, s));
     GNW_CUDA_CHECK(cudaMemcpyAsync(x_, x0, n * sizeof(double), cudaMemcpyDeviceToDevice, s));
   } else {
@@ -848,6 +898,7 @@ MinresResult Context::minres(const double* b, const double* x0, double* x, doubl
   // r = b - A x  (and ||b||)
   operator_into(vfixed(x_), 0, vfixed(az_), st_plain_, 0);
   residual(n, b_, az_, r_, st_plain_, 1, rpart_, counters_ + 5, s);
+  if (comm_) reduce_scratch(st_plain_, 4, 2);
   MinresState ps = read_plain();
   issue_stage();  // b and x0 are on the device now: a prefetched J may take the copy engine
   const double bnorm = std::sqrt(ps.scratch[5]);
@@ -860,7 +911,12 @@ MinresResult Context::minres(const double* b, const double* x0, double* x, doubl
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
     launches = launch_count() - l0 - built_now + graph_launched;
-    stage_out(x, x_, n);
+    if (comm_) {
+      local_to_global(x_, gio_a_);
+      global_out(x, gio_a_, K_ + N_);
+    } else {
+      stage_out(x, x_, n);
+    }
   };
   if (bnorm == 0.0) {  // minres.cpp:32-39
     res.converged = (ps.scratch[4] == 0.0);
@@ -875,7 +931,7 @@ MinresResult Context::minres(const double* b, const double* x0, double* x, doubl
   // iteration j0 reads.  Returns gamma_1 (the cycle's), or throws like the reference.
   auto start_cycle = [&](long long j0, double* gamma_out, double* rel_out) {
     double* zc = Z_[j0 % 2];
-    precondition_into(vfixed(r_), vfixed(r_ + K_), vfixed(zc), st_plain_, 0, vfixed(r_), vfixed(r_),
+    precondition_into(vfixed(r_), vfixed(r_ + kd()), vfixed(zc), st_plain_, 0, vfixed(r_), vfixed(r_),
                       loop_sched());
     const MinresState q = read_plain();
     if (q.scratch[0] < 0.0) throw std::runtime_error("minres: preconditioner is not positive definite");
@@ -930,6 +986,7 @@ MinresResult Context::minres(const double* b, const double* x0, double* x, doubl
   auto true_residual_rel = [&](double* rout) {
     operator_into(vfixed(x_), 0, vfixed(tmp2_), st_plain_, 0);
     residual(n, b_, tmp2_, rout, st_plain_, 0, rpart_, counters_ + 5, s);
+    if (comm_) reduce_scratch(st_plain_, 4, 1);
     const MinresState q = read_plain();
     return std::sqrt(q.scratch[4]) / bnorm;
   };
@@ -1084,6 +1141,7 @@ double Context::vcycle_bytes() const {
 void Context::profile_kernel(int kernel, int reps, double* seconds, double* algorithmic) {
   require_mixed();
   require_device();
+  if (comm_) throw std::invalid_argument("gnw_profile_kernel: single GPU only");
   if (reps < 1) reps = 1;
   const cudaStream_t s = stream_;
   const double K = static_cast<double>(K_), N = static_cast<double>(N_), m = static_cast<double>(m_);

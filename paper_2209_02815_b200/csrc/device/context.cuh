@@ -15,6 +15,7 @@
 #include "ert_gmg.cuh"
 #include "ert_kernels.cuh"
 #include "kernels.cuh"
+#include "part_amg.cuh"
 
 namespace gnw {
 
@@ -61,7 +62,6 @@ class Context {
 
   bool has_device() const { return device_ >= 0; }
   int vc_collapse_level() const { return damg_.collapse_level(); }
-  int vc_persist_level() const { return damg_.persist_level(); }
   int ptr_mode = 0;
   int coarse_mode = 0;
   int pc_laplace = 0;  // GnAlgorithm::kLaplaceMinres (inversion.cpp:251-256)
@@ -99,14 +99,20 @@ class Context {
   uint64_t last_fused_iters_ = 0;  // of last_iterations, run on the fused or lean schedule
   uint64_t last_sched_iters_[3] = {0, 0, 0};  // of last_iterations, per schedule (reference, fused, lean)
 
-  // Cell-partitioned multi-GPU mode (comm.cuh); set before assemble.  J and
-  // the right-hand side's J^T term then cover only this rank's cells [c_lo, c_hi): set_jacobian
-  // takes the m x (c_hi - c_lo) column slice; every other vector stays full and replicated.
+  // Row-partitioned multi-GPU mode (context_rowpart.cu); set before assemble.
+  // The rank owns cells [c_lo, c_hi) (whole mesh rows) and the edges first met in them; J and
+  // H are its m x (c_hi - c_lo) column slices (set_jacobian takes that slice).  The public
+  // entry points still take and return GLOBAL vectors (every rank passes the same input and
+  // receives the full result); the solve itself runs on the owned rows with halo exchanges.
   void set_comm(std::shared_ptr<Comm> c);
   bool partitioned() const { return comm_ != nullptr; }
   const Comm* comm() const { return comm_.get(); }
   long long c_lo() const { return c_lo_; }
   long long c_hi() const { return c_hi_; }
+  long long own_edges() const { return comm_ ? Kl_ : K_; }
+  long long own_cells() const { return comm_ ? Nl_ : N_; }
+  long long ghost_entries() const { return comm_ ? nloc_ - Kl_ - Nl_ : 0; }
+  int part_levels() const { return pamg_ ? pamg_->partitioned_levels() : 0; }
 
   // ERT forward model (forward.cpp:39-172) on the assembled mesh
   void set_electrodes(const int64_t* nodes, int64_t n);
@@ -248,20 +254,37 @@ class Context {
   bool fused_off_ = false;  // this solve restarted on the reference schedule (minres)
   int n_comb_blocks_ = 0;
 
-  // partitioned mode
+  // partitioned mode (context_rowpart.cu)
   std::shared_ptr<Comm> comm_;
-  std::vector<long long> part_lo_;  // world + 1 cell boundaries
-  long long c_lo_ = 0, c_hi_ = 0;
-  long long host_j_ = 0;            // iteration index mirrored on the host (ring slots of the exchanges)
-  double *u_part_ = nullptr, *t_part_ = nullptr, *gath_ = nullptr, *Cpart_ = nullptr, *Cgath_ = nullptr;
-  long long local_n() const { return comm_ ? c_hi_ - c_lo_ : N_; }
+  std::vector<long long> part_lo_, part_e_;  // world + 1 cell / edge boundaries
+  long long c_lo_ = 0, c_hi_ = 0, e_lo_ = 0, e_hi_ = 0;
+  long long Kl_ = 0, Nl_ = 0, nloc_ = 0;     // own edges, own cells, local length with ghosts
+  long long host_j_ = 0;                     // iteration index mirrored on the host (ring slots of the exchanges)
+  long long kd() const { return comm_ ? Kl_ : K_; }  // edge / cell rows of the device vectors
+  long long nd() const { return comm_ ? Nl_ : N_; }
+  long long local_n() const { return nd(); }
   double* resolve(const VSel& v) const { return v.mod == 1 ? v.p[0] : v.p[(host_j_ + v.off) % v.mod]; }
-  void gather_cells(double* full, cudaStream_t s);                  // allgatherv of the cell part
+  void setup_rowpart();
+  void alloc_vectors(long long n_alloc, long long K, long long N);
   void reduce_m(const double* part, double* out, long long n, cudaStream_t s);  // fixed-order allreduce
-  void build_h_partitioned(int b);  // H = B J^T with the column batches spread over the ranks
-  std::unique_ptr<DeviceMemory> a2a_mem_;
-  double *a2a_a_ = nullptr, *a2a_b_ = nullptr;
-  size_t a2a_na_ = 0, a2a_nb_ = 0;
+  void reduce_scratch(MinresState* st, int k0, int cnt);  // st->scratch[k0, k0+cnt) summed over ranks
+  void exchange_saddle(double* v);                         // ghost edges and cells of a saddle vector
+  void global_to_local(const double* g, double* l, bool ghosts);
+  void local_to_global(const double* l, double* g);
+  const double* global_in(const double* p, size_t n, double* dev);
+  void global_out(double* p, const double* dev, size_t n);
+  void build_h_rowpart();
+  DeviceMemory rpmem_;
+  std::unique_ptr<DHalo> sh_;
+  std::unique_ptr<PartAmg> pamg_;
+  int *sad_l2g_ = nullptr, *cell_l2g_ = nullptr;
+  long long n_cell_l2g_ = 0;
+  double *gio_a_ = nullptr, *gio_b_ = nullptr, *gio_c_ = nullptr, *gio_d_ = nullptr, *sgath_ = nullptr;
+  double *u_part_ = nullptr, *t_part_ = nullptr, *gath_ = nullptr, *Cpart_ = nullptr, *Cgath_ = nullptr;
+  long long gath_cap_ = 0;
+  std::unique_ptr<DeviceMemory> hx_mem_;
+  double *hx_ = nullptr, *hy_ = nullptr;
+  int hx_b_ = 0;
 
   // ERT forward model state
   std::vector<int64_t> electrodes_;

@@ -157,7 +157,6 @@ gnw_status gnw_get_info(const gnw_ctx* ctx, gnw_info* info) {
     info->beta = c.beta();
     info->device_bytes = c.device_bytes();
     info->collapse_level = c.has_device() ? c.vc_collapse_level() : -1;
-    info->persist_level = c.has_device() ? c.vc_persist_level() : -1;
   });
 }
 

@@ -273,6 +273,22 @@ __global__ void k_coarse_inverse1(const double* __restrict__ Ainv, int n, VSel r
   const double* __restrict__ row = Ainv + i * n;
   double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
   int j = lane;
+  // four 128-column blocks at a time: 16 loads per lane in flight, the adds in the same order
+  for (; j + 96 + 384 < n; j += 512) {
+    double mm[16], rr[16];
+#pragma unroll
+    for (int u = 0; u < 16; ++u) {
+      mm[u] = ldg(&row[j + 32 * u]);
+      rr[u] = r[j + 32 * u];
+    }
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      a0 = a0 + mm[4 * b] * rr[4 * b];
+      a1 = a1 + mm[4 * b + 1] * rr[4 * b + 1];
+      a2 = a2 + mm[4 * b + 2] * rr[4 * b + 2];
+      a3 = a3 + mm[4 * b + 3] * rr[4 * b + 3];
+    }
+  }
   for (; j + 96 < n; j += 128) {
     const double m0 = ldg(&row[j]), m1 = ldg(&row[j + 32]), m2 = ldg(&row[j + 64]), m3 = ldg(&row[j + 96]);
     const double r0 = r[j], r1 = r[j + 32], r2 = r[j + 64], r3 = r[j + 96];
@@ -832,8 +848,8 @@ __global__ void __launch_bounds__(kTpb, B >= 16 ? 5 : 8) k_saddle(OperatorArgs o
       o = o + 1.0 * sd;  // spmv_add(*D, zeta, 1.0, out2)
       if (op.m > 0 && op.q != nullptr) {  // fused: J^T (J zhat2) = J^T (t' * ig) ~ q * ig (Woodbury identity J z2 = t')
         o = o + *op.neg_inv_beta * (op.q[c] * sc);
-      } else if (op.m > 0 && c >= op.c_lo && (op.c_hi < 0 || c < op.c_hi)) {  // matvec_transpose(J, J dm), linalg.cpp:45-54
-        const double jt = col_dot<B>(op.J + (c - op.c_lo), op.ldj, usm, op.m);
+      } else if (op.m > 0) {  // matvec_transpose(J, J dm), linalg.cpp:45-54
+        const double jt = col_dot<B>(op.J + c, op.ldj, usm, op.m);
         o = o + *op.neg_inv_beta * jt;  // axpy(-1.0 / beta, jtjdm, out2)
       }
       y[op.K + c] = o;
@@ -1010,6 +1026,7 @@ void mirror_lower(double* C, int n, cudaStream_t s) {
 
 __device__ void finish_scalars(const double (&tot)[3], const double* __restrict__ dots_edge, int n_edge_blocks,
                                int loop, MinresState* st, double* red);
+__device__ void givens_step(double gsq, double zz, double vv, MinresState* st);
 
 template <int B>
 __global__ void __launch_bounds__(kTpb, B >= 16 ? 5 : 8) k_finish_prec(PrecArgs pa, const double* __restrict__ svc,
@@ -1026,12 +1043,12 @@ __global__ void __launch_bounds__(kTpb, B >= 16 ? 5 : 8) k_finish_prec(PrecArgs 
     __syncthreads();
   }
   double d[3] = {0.0, 0.0, 0.0};
-  const long long c = pa.c_lo + static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (c < (pa.c_hi < 0 ? pa.N : pa.c_hi)) {
+  const long long c = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (c < pa.N) {
     double z = svc[c];
     if (pa.m > 0) {  // w = matvec(h_hat, t) row c (linalg.cpp:33-43); s += (-1/beta) w
       double w = 0.0;
-      const double* __restrict__ Hc = pa.Ht + (c - pa.c_lo);
+      const double* __restrict__ Hc = pa.Ht + c;
       if (pa.q != nullptr) {  // one sweep over H and J: w = (H t')_c, q_c = (J^T t')_c
         double qq = 0.0;
         col_dot2<8>(Hc, pa.ldh, pa.J + c, pa.ldj, tsm, pa.m, w, qq);  // 16 loads in flight (32 at B = 16 spill residency)
@@ -1046,7 +1063,6 @@ __global__ void __launch_bounds__(kTpb, B >= 16 ? 5 : 8) k_finish_prec(PrecArgs 
     d[0] = z * v;
     d[1] = z * z;
   }
-  if (pa.dist) return;  // partitioned: dist_givens reduces once the cells are gathered
   double tot[3];
   if (!grid_reduce_last<3>(d, part, counter, red, tot)) return;
   finish_scalars(tot, dots_edge, n_edge_blocks, loop, st, red);
@@ -1068,7 +1084,11 @@ __device__ void finish_scalars(const double (&tot)[3], const double* __restrict_
     st->scratch[2] = vv;
     return;
   }
-  // minres.cpp:79-101
+  givens_step(gsq, zz, vv, st);
+}
+
+// minres.cpp:79-101: gamma_next and the Givens rotation from <z,v>, <z,z>, <v,v>
+__device__ void givens_step(double gsq, double zz, double vv, MinresState* st) {
   if (gsq < -1e-12 * (sqrt(zz) * sqrt(vv) + 1.0)) {
     st->status = kErrNotPD;
     return;
@@ -1091,6 +1111,15 @@ __device__ void finish_scalars(const double (&tot)[3], const double* __restrict_
   st->inv_alpha1 = 1.0 / alpha1;
   st->tau = st->c_next * st->eta;
   st->eta = -st->s_next * st->eta;
+}
+
+__global__ void k_givens_from_scratch(MinresState* st) {
+  griddep_wait();
+  givens_step(st->scratch[0], st->scratch[1], st->scratch[2], st);
+}
+void givens_from_scratch(MinresState* st, cudaStream_t s) {
+  GNW_LAUNCH(launch_k(k_givens_from_scratch, 1, 1, 0, s, st));
+  check_launch("givens_from_scratch");
 }
 
 template <int B>
@@ -1125,7 +1154,7 @@ void col_sweep(const double* A, long long ld, const double* t, int m, long long 
 }
 
 int finish_blocks(const PrecArgs& pa) {
-  return static_cast<int>(grid_for((pa.c_hi < 0 ? pa.N : pa.c_hi) - pa.c_lo));
+  return static_cast<int>(grid_for(pa.N));
 }
 
 void finish_precondition(const PrecArgs& pa, const double* svc, const double* t2, VSel vnext, VSel znext, int loop,
@@ -1140,69 +1169,35 @@ void finish_precondition(const PrecArgs& pa, const double* svc, const double* t2
 }
 
 // ======================================================================
-// Partitioned (multi-GPU) solve: the reductions that follow a cell gather
+// Partitioned (multi-GPU) solve: fixed-order sums of the ranks' partials and the scalar steps
+// that follow them (context_rowpart.cu).  Every rank sums the same gathered partials in rank
+// order, so every rank holds the same bits.
 // ======================================================================
-// delta = <y, zhat>: k_saddle's dot, with its block partition (edge blocks, then cell
-// blocks) so that one rank reproduces the single-GPU delta bit for bit.
-__global__ void __launch_bounds__(kTpb) k_dist_delta(long long K, long long N, VSel zs, int scaled, VSel ys,
-                                                     MinresState* st, int loop, int nb_edge, double* part,
-                                                     unsigned* counter) {
+__global__ void k_sum_scratch(const double* __restrict__ parts, int P, int cnt, MinresState* st, int k0) {
   griddep_wait();
-  __shared__ double red[kTpb / 32];
-  const double* __restrict__ z = vsel(zs, st);
-  const double* __restrict__ y = vsel(ys, st);
-  const double sc = scaled ? st->inv_gamma : 1.0;
-  double dotv[1] = {0.0};
-  const long long i = static_cast<int>(blockIdx.x) < nb_edge
-                          ? static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x
-                          : K + static_cast<long long>(blockIdx.x - nb_edge) * blockDim.x + threadIdx.x;
-  const bool ok = static_cast<int>(blockIdx.x) < nb_edge ? i < K : i < K + N;
-  if (ok) dotv[0] = y[i] * (scaled ? z[i] * sc : z[i]);
-  double tot[1];
-  if (grid_reduce_last<1>(dotv, part, counter, red, tot) && threadIdx.x == 0) {
-    const double delta = tot[0];
-    if (loop) {
-      st->delta = delta;
-      st->coef_v1 = -delta / st->gamma_cur;
-      st->coef_v2 = -st->gamma_cur / st->gamma_prev;
-    } else {
-      st->scratch[0] = delta;
-    }
-  }
+  const int i = threadIdx.x;
+  if (i >= cnt) return;
+  double s = 0.0;
+  for (int r = 0; r < P; ++r) s += parts[r * cnt + i];
+  st->scratch[k0 + i] = s;
 }
 
-void dist_delta(const OperatorArgs& op, VSel z, int scaled, VSel y, MinresState* st, int loop, double* part,
-                unsigned* counter, cudaStream_t s) {
-  const int nbe = static_cast<int>(grid_for(op.K)), nbc = static_cast<int>(grid_for(op.N));
-  GNW_LAUNCH(launch_k(k_dist_delta, nbe + nbc, kTpb, 0, s, op.K, op.N, z, scaled, y, st, loop, nbe, part, counter));
-  check_launch("dist_delta");
+void sum_scratch(const double* parts, int P, int cnt, MinresState* st, int k0, cudaStream_t s) {
+  GNW_LAUNCH(launch_k(k_sum_scratch, 1, 32, 0, s, parts, P, cnt, st, k0));
+  check_launch("sum_scratch");
 }
 
-// <z, v>, <z, z> over all cells with k_finish_prec's block partition, then its tail.
-__global__ void __launch_bounds__(kTpb) k_dist_givens(long long K, long long N, VSel vns, VSel zns, int loop,
-                                                      MinresState* st, const double* __restrict__ dots_edge,
-                                                      int n_edge_blocks, double* part, unsigned* counter) {
+// the saddle kernel's loop epilogue from the reduced delta (scratch[0])
+__global__ void k_delta_coef(MinresState* st) {
   griddep_wait();
-  __shared__ double red[3 * (kTpb / 32)];
-  const double* __restrict__ vn = vsel(vns, st);
-  const double* __restrict__ zn = vsel(zns, st);
-  double d[3] = {0.0, 0.0, 0.0};
-  const long long c = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (c < N) {
-    const double z = zn[K + c];
-    d[0] = z * vn[K + c];
-    d[1] = z * z;
-  }
-  double tot[3];
-  if (!grid_reduce_last<3>(d, part, counter, red, tot)) return;
-  finish_scalars(tot, dots_edge, n_edge_blocks, loop, st, red);
+  const double delta = st->scratch[0];
+  st->delta = delta;
+  st->coef_v1 = -delta / st->gamma_cur;
+  st->coef_v2 = -st->gamma_cur / st->gamma_prev;
 }
-
-void dist_givens(const PrecArgs& pa, VSel vn, VSel zn, int loop, MinresState* st, const double* dots_edge,
-                 int n_edge_blocks, double* part, unsigned* counter, cudaStream_t s) {
-  GNW_LAUNCH(launch_k(k_dist_givens, grid_for(pa.N), kTpb, 0, s, pa.K, pa.N, vn, zn, loop, st, dots_edge,
-                      n_edge_blocks, part, counter));
-  check_launch("dist_givens");
+void delta_coef(MinresState* st, cudaStream_t s) {
+  GNW_LAUNCH(launch_k(k_delta_coef, 1, 1, 0, s, st));
+  check_launch("delta_coef");
 }
 
 __global__ void k_sum_partials(const double* __restrict__ parts, int P, long long n, double* __restrict__ out) {
@@ -1240,6 +1235,8 @@ void capacitance_reduce(const double* parts, int P, int m, double beta, double* 
 // ======================================================================
 // MINRES vector recurrences (minres.cpp:93-106) and loop control
 // ======================================================================
+__device__ void update_tail(double rr, MinresState* st, double* hist_e, double* hist_p, long long hist_cap);
+
 __global__ void __launch_bounds__(kTpb) k_minres_update(long long n, VSel zs, VSel azs, VSel wps, VSel wcs, VSel wns,
                                                         VSel ups, VSel ucs, VSel uns, double* __restrict__ x,
                                                         double* __restrict__ r, MinresState* st,
@@ -1249,7 +1246,7 @@ __global__ void __launch_bounds__(kTpb) k_minres_update(long long n, VSel zs, VS
   griddep_wait();
   __shared__ double red[kTpb / 32];
   if (use_cond != 2 && st->status != kRunning) {  // use_cond == 2: isolated timing, no loop control
-    if (use_cond && blockIdx.x == 0 && threadIdx.x == 0) cudaGraphSetConditional(handle, 0);
+    if (use_cond == 1 && blockIdx.x == 0 && threadIdx.x == 0) cudaGraphSetConditional(handle, 0);
     return;
   }
   const double* __restrict__ z = vsel(zs, st);
@@ -1299,8 +1296,18 @@ __global__ void __launch_bounds__(kTpb) k_minres_update(long long n, VSel zs, VS
   }
   double tot[1];
   if (!grid_reduce_last<1>(rr, part, counter, red, tot) || threadIdx.x != 0 || use_cond == 2) return;
+  if (use_cond == 3) {  // partitioned: this rank's ||r||^2 only; update_tail_from_scratch finishes
+    st->scratch[6] = tot[0];
+    return;
+  }
+  update_tail(tot[0], st, hist_e, hist_p, hist_cap);
+  if (use_cond == 1) cudaGraphSetConditional(handle, st->status == kRunning ? 1u : 0u);
+}
+
+// minres.cpp:93-148 after the vector updates: history, convergence / exhaustion, rotation, j++
+__device__ void update_tail(double rr, MinresState* st, double* hist_e, double* hist_p, long long hist_cap) {
   const long long j = st->j;
-  const double rel = sqrt(tot[0]) / st->bnorm;
+  const double rel = sqrt(rr) / st->bnorm;
   st->iterations = j;
   st->rel = rel;
   if (j < hist_cap) {
@@ -1322,7 +1329,16 @@ __global__ void __launch_bounds__(kTpb) k_minres_update(long long n, VSel zs, VS
     st->j = j + 1;
     if (j + 1 > st->maxit) st->status = kMaxit;
   }
-  if (use_cond) cudaGraphSetConditional(handle, st->status == kRunning ? 1u : 0u);
+}
+
+__global__ void k_update_tail_from_scratch(MinresState* st, double* hist_e, double* hist_p, long long hist_cap) {
+  griddep_wait();
+  if (st->status != kRunning) return;
+  update_tail(st->scratch[6], st, hist_e, hist_p, hist_cap);
+}
+void update_tail_from_scratch(MinresState* st, double* hist_e, double* hist_p, long long hist_cap, cudaStream_t s) {
+  GNW_LAUNCH(launch_k(k_update_tail_from_scratch, 1, 1, 0, s, st, hist_e, hist_p, hist_cap));
+  check_launch("update_tail_from_scratch");
 }
 
 void minres_update(long long n, VSel z, VSel az, VSel wprev, VSel wcur, VSel wnext, VSel uprev, VSel ucur, VSel unext,
@@ -1418,9 +1434,9 @@ __global__ void __launch_bounds__(kTpb) k_rhs(OperatorArgs op, double beta, cons
     for (int t = threadIdx.x; t < op.m; t += blockDim.x) gsm[t] = g[t] - gobs[t];  // inversion.cpp:137-138
     __syncthreads();
     const long long c = static_cast<long long>(blockIdx.x - nb_edge) * blockDim.x + threadIdx.x;
-    if (c >= op.N || c < op.c_lo || (op.c_hi >= 0 && c >= op.c_hi)) return;  // partition: own cells only
+    if (c >= op.N) return;
     double jt = 0.0;
-    const double* __restrict__ Jc = op.J + (c - op.c_lo);
+    const double* __restrict__ Jc = op.J + c;
 #pragma unroll 8
     for (int i = 0; i < op.m; ++i) jt = jt + __ldg(Jc + static_cast<long long>(i) * op.ldj) * gsm[i];
     rhs[op.K + c] = jt / beta;

@@ -20,28 +20,19 @@ struct DLevel {
   int gA = 1, gP = 1, gR = 1;
   // SELL-32 copies for the thread-per-row kernels (same order, coalesced; width 0: CSR)
   DSell As, Ps, Rs;
+  // default-mode one-pass-per-direction operators (vcycle_fused.cu, host::fused_cycle_ops):
+  // r_c = Tt r, e = S r + T e_c; fused = 0: not built for this level
+  DCsr S, T, Tt;
+  int gS = 1, gTt = 1, fused = 0;
 };
 
-// The small levels of the single-RHS V-cycle plus its dense level in ONE persistent cooperative
-// launch with grid barriers between the phases (vcycle_persist.cu); bit-identical to the kernel
-// chain.  Level k of lv[] is hierarchy level l0 + k; its input r (level l0: the launch argument)
-// and output e; the dense operator M (n_M x n_M) maps rM to eM.
-constexpr int kMaxPersist = 6;
-struct PersistLevel {
-  DCsr A, P, R;
-  const double* wd = nullptr;
-  int n = 0, gA = 1, gP = 1, gR = 1;
-  double *r = nullptr, *res = nullptr, *x = nullptr, *e = nullptr;
-};
-struct PersistTail {
-  int nlev = 0;
-  PersistLevel lv[kMaxPersist];
-  const double* M = nullptr;
-  int nM = 0;
-  double *rM = nullptr, *eM = nullptr;
-  unsigned* bar = nullptr;  // 2 words, zero-initialised: grid barrier
-};
-void vcycle_persist(const PersistTail& t, VSel r, double* out, const MinresState* st, cudaStream_t s);
+// one pass per level each way (vcycle_fused.cu): rc = Tt r; out = S r + T ec
+void vcf_restrict(const DLevel& L, VSel r, double* rc, const MinresState* st, cudaStream_t s);
+void vcf_up(const DLevel& L, VSel r, const double* ec, double* out, const MinresState* st, cudaStream_t s);
+void mvcf_restrict(const DLevel& L, const double* r, double* rc, int b, cudaStream_t s);
+// with ht != nullptr the result may go straight to Ht rows (returns true when it did)
+bool mvcf_up(const DLevel& L, const double* r, const double* ec, double* out, int b, double* ht, long long ldh,
+             cudaStream_t s);
 
 // G-lanes-per-row kernels (vcycle_wide.cu), G = DLevel::gA / gR / gP
 void vcg_down(const DLevel& L, VSel r, double* resid, const MinresState* st, cudaStream_t s);
@@ -108,9 +99,6 @@ struct OperatorArgs {
   // Woodbury-fused loop: J^T u = (J^T t') / gamma with q = J^T t'
   // produced by the previous preconditioner pass; J is then not read by the operator.
   const double* q = nullptr;
-  // cell partition (multi-GPU): J holds only the columns [c_lo, c_hi) of this
-  // rank (J + (c - c_lo) is column c); c_hi < 0 means N (single GPU)
-  long long c_lo = 0, c_hi = -1;
 };
 
 // u = A[:, ] x2 * scale partial GEMV over rows of a row-major (m x N) matrix,
@@ -148,10 +136,6 @@ struct PrecArgs {
   // fused/lean loops: t2 = C^-1 t refined once against the full C (cres: m scratch)
   const double* Cfull = nullptr;
   double* cres = nullptr;
-  // cell partition: Ht holds the columns [c_lo, c_hi); dist != 0: the finish pass only
-  // writes z for those cells (no reductions -- the partitioned driver reduces after the gather)
-  long long c_lo = 0, c_hi = -1;
-  int dist = 0;
 };
 
 // v_next = Az + c1 v_cur + c2 v_prev (combine, minres.cpp:76-77) or, when
@@ -226,14 +210,15 @@ void cholesky_inverse(const double* L, double* Y, double* Cinv, int n, cudaStrea
 
 void fill_zero(double* p, long long n, cudaStream_t s);
 
-// ---- partitioned (multi-GPU) solve helpers (context_dist.cu) ----
-// delta = <y, zhat> over all K+N (same block partition as k_saddle) -> st (loop) / st->scratch[0]
-void dist_delta(const OperatorArgs& op, VSel z, int scaled, VSel y, MinresState* st, int loop, double* part,
-                unsigned* counter, cudaStream_t s);
-// <z,v>, <z,z> over the cells (same block partition as k_finish_prec) + the combine pass's
-// partials -> gamma_next and the Givens rotation (minres.cpp:79-101), as k_finish_prec's tail
-void dist_givens(const PrecArgs& pa, VSel vn, VSel zn, int loop, MinresState* st, const double* dots_edge,
-                 int n_edge_blocks, double* part, unsigned* counter, cudaStream_t s);
+// ---- partitioned (multi-GPU) solve (context_rowpart.cu) ----
+// st->scratch[k0 + i] = sum over ranks r (in rank order) of parts[r * cnt + i]
+void sum_scratch(const double* parts, int P, int cnt, MinresState* st, int k0, cudaStream_t s);
+// the saddle kernel's loop epilogue (delta, v-combination coefficients) from scratch[0]
+void delta_coef(MinresState* st, cudaStream_t s);
+// the finish kernel's loop epilogue (gamma_next, Givens rotation; minres.cpp:79-101) from scratch[0..2]
+void givens_from_scratch(MinresState* st, cudaStream_t s);
+// the update kernel's epilogue (history, convergence, rotation) from scratch[6] = ||r||^2
+void update_tail_from_scratch(MinresState* st, double* hist_e, double* hist_p, long long hist_cap, cudaStream_t s);
 // out[i] = sum_{r < P} parts[r * n + i], r ascending (deterministic allreduce body)
 void sum_partials(const double* parts, int P, long long n, double* out, cudaStream_t s);
 // C = I + (sum_r parts[r]) / beta, parts m x m each (capacitance, inversion.cpp:37-43)

@@ -9,6 +9,7 @@
 #include <cstdlib>
 
 #include <algorithm>
+#include <cstdint>
 #include <cmath>
 #include <numeric>
 #include <utility>
@@ -315,6 +316,57 @@ Csr spgemm(const Csr& A, const Csr& B) {
     std::copy(cvals[ch].begin(), cvals[ch].end(), C.vals.begin() + C.rowptr[r0]);
   }
   return C;
+}
+
+FusedCycleOps fused_cycle_ops(const Csr& A, const Csr& P, const std::vector<double>& wd) {
+  if (A.n_rows != A.n_cols || P.n_rows != A.n_rows || static_cast<int64_t>(wd.size()) != A.n_rows)
+    throw std::invalid_argument("fused_cycle_ops: shape mismatch");
+  FusedCycleOps f;
+  // S = 2 Wd - Wd A Wd on A's pattern
+  f.S = A;
+#pragma omp parallel for schedule(static)
+  for (int64_t i = 0; i < A.n_rows; ++i)
+    for (int64_t k = A.rowptr[i]; k < A.rowptr[i + 1]; ++k) {
+      const int64_t j = A.cols[k];
+      const double v = -(wd[i] * A.vals[k] * wd[j]);
+      f.S.vals[k] = (i == j) ? 2.0 * wd[i] + v : v;
+    }
+  // T = P - Wd (A P), rows merged by column
+  const Csr AP = spgemm(A, P);
+  f.T.n_rows = P.n_rows;
+  f.T.n_cols = P.n_cols;
+  f.T.rowptr.assign(P.n_rows + 1, 0);
+  std::vector<int64_t> len(P.n_rows);
+#pragma omp parallel for schedule(static)
+  for (int64_t i = 0; i < P.n_rows; ++i) {  // |union of the two sorted column lists|
+    int64_t a = P.rowptr[i], b = AP.rowptr[i], n = 0;
+    while (a < P.rowptr[i + 1] || b < AP.rowptr[i + 1]) {
+      const int32_t ca = a < P.rowptr[i + 1] ? P.cols[a] : INT32_MAX;
+      const int32_t cb = b < AP.rowptr[i + 1] ? AP.cols[b] : INT32_MAX;
+      if (ca <= cb) ++a;
+      if (cb <= ca) ++b;
+      ++n;
+    }
+    len[i] = n;
+  }
+  for (int64_t i = 0; i < P.n_rows; ++i) f.T.rowptr[i + 1] = f.T.rowptr[i] + len[i];
+  f.T.cols.resize(f.T.rowptr[P.n_rows]);
+  f.T.vals.resize(f.T.rowptr[P.n_rows]);
+#pragma omp parallel for schedule(static)
+  for (int64_t i = 0; i < P.n_rows; ++i) {
+    int64_t a = P.rowptr[i], b = AP.rowptr[i], o = f.T.rowptr[i];
+    while (a < P.rowptr[i + 1] || b < AP.rowptr[i + 1]) {
+      const int32_t ca = a < P.rowptr[i + 1] ? P.cols[a] : INT32_MAX;
+      const int32_t cb = b < AP.rowptr[i + 1] ? AP.cols[b] : INT32_MAX;
+      double v = 0.0;
+      if (ca <= cb) v = P.vals[a++];
+      if (cb <= ca) v = v - wd[i] * AP.vals[b++];
+      f.T.cols[o] = std::min(ca, cb);
+      f.T.vals[o++] = v;
+    }
+  }
+  f.Tt = transpose(f.T);
+  return f;
 }
 
 Csr scale_rows(const Csr& A, const std::vector<double>& s) {  // sparse.cpp:156-163

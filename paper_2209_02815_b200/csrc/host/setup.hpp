@@ -78,6 +78,16 @@ Csr lumped_schur(const Csr& Q, const Csr& D);
 Csr from_triplets(int64_t n_rows, int64_t n_cols, std::vector<int64_t> rows,
                   std::vector<int64_t> cols, std::vector<double> vals);
 AmgHierarchy amg_setup(const Csr& S, const AmgOptions& opt);
+/// One level of the default-mode V-cycle (amg.cpp:90-111) as two sparse operators.  With
+/// Wd = omega diag(A)^-1 the level computes x1 = Wd r + P e_c, e = x1 + Wd (r - A x1) and passes
+/// r_c = P^T (r - A Wd r) down; for symmetric A that is
+///     r_c = T^T r,    e = S r + T e_c,    T = (I - Wd A) P,    S = 2 Wd - Wd A Wd,
+/// i.e. ONE pass per level on the way down and one on the way up instead of two each (the
+/// same linear map; rounding differs from the level-by-level order, which the exact mode keeps).
+struct FusedCycleOps {
+  Csr S, T, Tt;  // Tt = transpose(T): the restriction, exactly T's entries
+};
+FusedCycleOps fused_cycle_ops(const Csr& A, const Csr& P, const std::vector<double>& wd);
 /// dense_cholesky (linalg.cpp:88-105); throws std::runtime_error on failure.
 std::vector<double> dense_cholesky(int64_t n, const std::vector<double>& C);
 /// Explicit inverse L^-T L^-1 of an SPD matrix from its lower factor.

@@ -83,7 +83,9 @@ def solve_both(p, b, tag_iters):
         x, rep = p.minres(b, tol=tol)
         res[f"{tol:.0e}"] = dict(iterations=rep["iterations"], converged=rep["converged"],
                                  true_relative_residual=rep["true_relative_residual"],
-                                 t_minres=time.time() - t0, **fingerprint(x))
+                                 t_minres=time.time() - t0, **fingerprint(x),
+                                 hist_e=rep["relative_residuals"].tolist(),
+                                 hist_p=rep["pnorm_relative_residuals"].tolist())
         print(f"  {tag_iters} tol {tol:.0e}: {rep['iterations']} iterations", flush=True)
     return res
 

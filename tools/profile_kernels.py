@@ -34,6 +34,12 @@ else:
     J = torch.from_numpy(inp.J).cuda()
 ctx.use_device_pointers(True)
 ctx.set_jacobian(J, 1e-2)
+if args.n == 0:  # one solve first: "iteration" is the last solve's time per MINRES iteration
+    b = ctx.assemble_rhs(torch.from_numpy(inp.dm).cuda(), torch.zeros(inp.mesh.n_cells, dtype=torch.float64, device="cuda"),
+                         torch.from_numpy(inp.dg).cuda(), torch.zeros(cfg.m, dtype=torch.float64, device="cuda"))
+    for _ in range(2):
+        x, rep = ctx.minres(b, tol=1e-8)
+    print(f"solve: {rep.iterations} iterations, schedule {ctx.loop_schedule()}, info {ctx.info()}")
 names = args.kernels.split(",")
 for nm in names:  # warm-up (module load) outside the profiled range
     ctx.profile_kernel(nm, reps=1)
