@@ -317,6 +317,17 @@ gnw_status gnw_get_partition(const gnw_ctx* ctx, int* rank, int* world, int64_t*
 /* The partition rule (host only): lo[0..world], rank r owns cells [lo[r], lo[r+1]);
  * boundaries are multiples of 64 cells. */
 gnw_status gnw_partition_cells(uint64_t n_cells, int world, int64_t* lo);
+/* The row partition of the saddle system [[Q, D^T], [D, 0]] (host/partition.hpp) as rank `rank`
+ * of `world` would hold it, computed on the host from an assembled context (no GPU needed):
+ * sizes = {own edges, own cells, ghosts, send entries}; local_to_global (own + ghosts; edge e
+ * -> e, cell c -> K + c), recv_off / send_off (world + 1), send_idx.  NULL arrays: sizes only. */
+gnw_status gnw_partition_saddle(const gnw_ctx* ctx, int world, int rank, uint64_t sizes[4],
+                                int64_t* local_to_global, int64_t* recv_off, int64_t* send_off,
+                                int32_t* send_idx);
+/* That rank's local operators: which 0 = Q, 1 = D, 2 = D^T (cell columns stored minus the own
+ * edge count, as the kernels address them).  NULL arrays: sizes only. */
+gnw_status gnw_partition_csr(const gnw_ctx* ctx, int world, int rank, int which, uint64_t* n_rows,
+                             uint64_t* nnz, int64_t* rowptr, int32_t* cols, double* vals);
 
 #ifdef __cplusplus
 }

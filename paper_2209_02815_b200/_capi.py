@@ -76,7 +76,7 @@ EXPORTED = [
     "gnw_export_mesh", "gnw_dense_cholesky", "gnw_get_stats", "gnw_event_record",
     "gnw_event_elapsed", "gnw_profile_kernel", "gnw_set_electrodes", "gnw_response_jacobian",
     "gnw_geometric_factor", "gnw_nccl_unique_id", "gnw_create_partitioned", "gnw_create_local_group",
-    "gnw_get_partition", "gnw_partition_cells", "gnw_gauss_newton",
+    "gnw_get_partition", "gnw_partition_cells", "gnw_partition_saddle", "gnw_partition_csr", "gnw_gauss_newton",
 ]
 
 
@@ -159,6 +159,8 @@ def load() -> C.CDLL:
     L.gnw_create_partitioned.argtypes = [i32, i32, i32, vp, C.POINTER(vp)]
     L.gnw_create_local_group.argtypes = [i32, i32, C.POINTER(vp)]
     L.gnw_partition_cells.argtypes = [u64, i32, vp]
+    L.gnw_partition_saddle.argtypes = [vp, i32, i32, vp, vp, vp, vp, vp]
+    L.gnw_partition_csr.argtypes = [vp, i32, i32, i32, C.POINTER(u64), C.POINTER(u64), vp, vp, vp]
     L.gnw_gauss_newton.argtypes = [vp, vp, vp, C.POINTER(ErtConfig), u64, vp, C.POINTER(GnConfig), vp,
                                    C.POINTER(GnStep), u64, C.POINTER(u64), C.POINTER(dbl)]
     L.gnw_get_partition.argtypes = [vp, C.POINTER(i32), C.POINTER(i32), C.POINTER(C.c_int64), C.POINTER(C.c_int64)]

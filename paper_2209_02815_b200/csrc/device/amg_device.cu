@@ -70,8 +70,9 @@ void DeviceAmg::reset() {
   mem_.release_all();
 }
 
-void DeviceAmg::upload(const host::AmgHierarchy& h, cudaStream_t s) {
+void DeviceAmg::upload(const host::AmgHierarchy& h, cudaStream_t s, int min_collapse_level) {
   reset();
+  min_collapse_ = min_collapse_level;
   const double omega = h.options.jacobi_damping;
   const size_t L = h.levels.size();
   // the dense tail starts at the collapse level (build_collapse's rule) or the coarsest level;
@@ -79,7 +80,7 @@ void DeviceAmg::upload(const host::AmgHierarchy& h, cudaStream_t s) {
   const char* fe = std::getenv("GNW_VC_FUSED");
   const bool fused_on = !(fe && std::atoi(fe) == 0);
   int stop = static_cast<int>(L) - 1;
-  for (int l = 1; l + 1 < static_cast<int>(L); ++l)
+  for (int l = min_collapse_; l + 1 < static_cast<int>(L); ++l)
     if (h.levels[l].A.n_rows <= kCollapseMax) {
       stop = l;
       break;
@@ -157,7 +158,7 @@ void DeviceAmg::build_collapse(cudaStream_t s) {
     if (std::atoi(e) == 0) return;
   const int L = static_cast<int>(lv_.size());
   int lc = -1;
-  for (int l = 1; l < L - 1; ++l)
+  for (int l = min_collapse_; l < L - 1; ++l)
     if (lv_[l].n <= kCollapseMax) {
       lc = l;
       break;
@@ -179,7 +180,7 @@ void DeviceAmg::build_collapse(cudaStream_t s) {
 void DeviceAmg::cycle_levels(int l0, VSel r, double* out, const MinresState* st, int exact, bool collapse,
                              cudaStream_t s) {
   const int L = static_cast<int>(lv_.size());
-  const int stop = (collapse && collapse_l_ > l0) ? collapse_l_ : L - 1;
+  const int stop = (collapse && collapse_l_ >= l0) ? collapse_l_ : L - 1;
   auto at = [&](int l) { return l == l0 ? r : vfixed(vr_[l]); };
   for (int l = l0; l < stop; ++l) {
     const DLevel lev = level(l, exact);
@@ -223,15 +224,15 @@ void DeviceAmg::vcycle(VSel r0, double* out0, const MinresState* st, int exact, 
   }
   if (!exact && fused_) {  // one pass per level each way (vcycle_fused.cu)
     const int L = static_cast<int>(lv_.size());
-    const int stop = collapse_l_ > 0 ? collapse_l_ : L - 1;
+    const int stop = collapse_l_ >= 0 ? collapse_l_ : L - 1;
     auto at = [&](int l) { return l == 0 ? r0 : vfixed(vr_[l]); };
     for (int l = 0; l < stop; ++l) vcf_restrict(lv_[l], at(l), vr_[l + 1], st, s);
-    coarse_inverse(stop == L - 1 && collapse_l_ <= 0 ? coarse_inv_ : collapse_M_, lv_[stop].n, at(stop),
-                   stop == 0 ? out0 : ve_[stop], st, 1, s);
+    coarse_inverse(collapse_l_ >= 0 ? collapse_M_ : coarse_inv_, lv_[stop].n, at(stop), stop == 0 ? out0 : ve_[stop],
+                   st, 1, s);
     for (int l = stop - 1; l >= 0; --l) vcf_up(lv_[l], at(l), ve_[l + 1], l == 0 ? out0 : ve_[l], st, s);
     return;
   }
-  cycle_levels(0, r0, out0, st, exact, !exact && collapse_l_ > 0, s);
+  cycle_levels(0, r0, out0, st, exact, !exact && collapse_l_ >= 0, s);
 }
 
 // Persistent work arrays of the batched V-cycle (b interleaved columns).
@@ -280,13 +281,15 @@ bool DeviceAmg::vcycle_batch(const double* r0, int b, double* out0, int exact, c
     coarse(r0, out0);
     return false;
   }
-  const int stop = (!exact && collapse_l_ > 0) ? collapse_l_ : L - 1;  // as in cycle_levels
+  const int stop = (!exact && collapse_l_ >= 0) ? collapse_l_ : L - 1;  // as in cycle_levels
+  const double* r_stop = stop == 0 ? r0 : mr_[stop];
+  double* e_stop = stop == 0 ? out0 : me_[stop];
   if (!exact && fused_) {  // one pass per level each way (vcycle_fused.cu)
     for (int l = 0; l < stop; ++l) mvcf_restrict(lv_[l], l == 0 ? r0 : mr_[l], mr_[l + 1], b, s);
     if (stop == L - 1)
-      coarse(mr_[L - 1], me_[L - 1]);
+      coarse(r_stop, e_stop);
     else
-      dense_seq_batch(collapse_M_, lv_[stop].n, mr_[stop], me_[stop], b, s);
+      dense_seq_batch(collapse_M_, lv_[stop].n, r_stop, e_stop, b, s);
     bool rows = false;
     for (int l = stop - 1; l >= 0; --l)
       rows = mvcf_up(lv_[l], l == 0 ? r0 : mr_[l], me_[l + 1], l == 0 ? out0 : me_[l], b, l == 0 ? ht : nullptr,
@@ -300,9 +303,9 @@ bool DeviceAmg::vcycle_batch(const double* r0, int b, double* out0, int exact, c
     mvc_restrict(lev, mres_[l], mr_[l + 1], b, s);
   }
   if (stop == L - 1)
-    coarse(mr_[L - 1], me_[L - 1]);
+    coarse(r_stop, e_stop);
   else
-    dense_seq_batch(collapse_M_, lv_[stop].n, mr_[stop], me_[stop], b, s);
+    dense_seq_batch(collapse_M_, lv_[stop].n, r_stop, e_stop, b, s);
   bool to_rows = false;
   for (int l = stop - 1; l >= 0; --l) {
     const double* rl = l == 0 ? r0 : mr_[l];

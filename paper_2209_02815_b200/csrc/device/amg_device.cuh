@@ -48,7 +48,9 @@ host::Csr device_spgemm(const host::Csr& A, const host::Csr& B, cudaStream_t s);
 
 class DeviceAmg {
  public:
-  void upload(const host::AmgHierarchy& h, cudaStream_t s);
+  // min_collapse_level: the first level the dense collapsed tail may start at (1 for a whole
+  // hierarchy; 0 for the replicated tail of a partitioned cycle that starts at the collapse level)
+  void upload(const host::AmgHierarchy& h, cudaStream_t s, int min_collapse_level = 1);
   void reset();
   bool empty() const { return lv_.empty(); }
   int n() const { return lv_.empty() ? 0 : lv_[0].n; }
@@ -78,6 +80,7 @@ class DeviceAmg {
   void build_collapse(cudaStream_t s);
 
   bool fused_ = false;             // fused per-level operators built (vcycle_fused.cu)
+  int min_collapse_ = 1;
   int collapse_l_ = -1;           // first level with n <= kCollapseMax above the coarsest, or -1
   double* collapse_M_ = nullptr;  // n x n row-major: column j = the sub-cycle applied to e_j
   DeviceMemory mem_;

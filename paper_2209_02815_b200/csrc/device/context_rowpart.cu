@@ -57,48 +57,24 @@ void Context::setup_rowpart() {
       throw std::invalid_argument("partition: a rank would own no cells (fewer than 64 cells per rank)");
   c_lo_ = part_lo_[me];
   c_hi_ = part_lo_[me + 1];
-  const std::vector<int32_t> cell_own = host::owners_from_ranges(part_lo_, N_);
-  const std::vector<int32_t> edge_own = host::edge_owners(mesh_, cell_own);
-  // the saddle space [edges; cells] (combined index: e, K + c)
-  std::vector<int32_t> own(static_cast<size_t>(K_ + N_));
-  std::copy(edge_own.begin(), edge_own.end(), own.begin());
-  std::copy(cell_own.begin(), cell_own.end(), own.begin() + K_);
-  const host::Csr Dt = host::transpose(D_);
-  std::vector<std::vector<int64_t>> refs(P);
-  std::vector<std::vector<int64_t>> my_e(P), my_c(P);
-  for (int r = 0; r < P; ++r) {
-    my_e[r] = host::owned(edge_own, r);
-    my_c[r] = host::owned(cell_own, r);
-    host::append_refs(Q_, my_e[r], refs[r]);                        // Q: edge columns
-    const size_t k0 = refs[r].size();
-    host::append_refs(Dt, my_e[r], refs[r]);                        // D^T: cell columns -> K + c
-    for (size_t k = k0; k < refs[r].size(); ++k) refs[r][k] += K_;
-    host::append_refs(D_, my_c[r], refs[r]);                       // D: edge columns
-  }
-  const std::vector<host::Halo> H = host::build_halos(own, P, refs, me);
-  const host::Halo& h = H[me];
-  Kl_ = static_cast<long long>(my_e[me].size());
-  Nl_ = static_cast<long long>(my_c[me].size());
+  const host::SaddlePartition sp = host::partition_saddle(mesh_, Q_, D_, part_lo_, me);
+  const host::Halo& h = sp.halo;
+  const std::vector<int32_t>& cell_own = sp.cell_owner;
+  Kl_ = sp.K_l;
+  Nl_ = sp.N_l;
   nloc_ = h.n_local();
-  if (Kl_ > 0 && (my_e[me].back() - my_e[me].front() + 1 != Kl_))
-    throw std::logic_error("partition: own edges are not contiguous");
-  e_lo_ = Kl_ ? my_e[me].front() : 0;
-  e_hi_ = e_lo_ + Kl_;
-  part_e_.assign(P + 1, 0);
-  for (int r = 0; r < P; ++r) part_e_[r + 1] = part_e_[r] + static_cast<long long>(my_e[r].size());
+  part_e_ = sp.edge_lo;
+  e_lo_ = part_e_[me];
+  e_hi_ = part_e_[me + 1];
   rpmem_.release_all();
   sh_ = std::make_unique<DHalo>(upload_halo(rpmem_, h, s));
-  // local operators: Q (own edges x local edges), D^T (own edges x cells at K_l + col), D (own cells)
-  const host::Csr Ql = host::localize(Q_, my_e[me], h);
-  const host::Csr Dl = host::localize(D_, my_c[me], h);
-  const host::Csr Dtl = host::localize(Dt, my_e[me], h, K_, Kl_);
   op_ = OperatorArgs{};
-  op_.Q = upload_csr(mem_, Ql, s);
-  op_.D = upload_csr(mem_, Dl, s);
-  op_.Dt = upload_csr(mem_, Dtl, s);
-  op_.Qs = upload_sell(mem_, Ql, s);
-  op_.Ds = upload_sell(mem_, Dl, s);
-  op_.Dts = upload_sell(mem_, Dtl, s);
+  op_.Q = upload_csr(mem_, sp.Q, s);
+  op_.D = upload_csr(mem_, sp.D, s);
+  op_.Dt = upload_csr(mem_, sp.Dt, s);
+  op_.Qs = upload_sell(mem_, sp.Q, s);
+  op_.Ds = upload_sell(mem_, sp.D, s);
+  op_.Dts = upload_sell(mem_, sp.Dt, s);
   op_.K = Kl_;
   op_.N = Nl_;
   // local -> global maps: the saddle layout (own + ghosts) and the cell vector of the rhs

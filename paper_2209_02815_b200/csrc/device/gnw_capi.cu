@@ -3,6 +3,7 @@
 // std::invalid_argument -> GNW_INVALID_ARGUMENT, gnw::DeviceError -> GNW_DEVICE,
 // any other std::exception -> GNW_NUMERICAL; the message text is the
 // reference's exception text.
+#include <algorithm>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -281,6 +282,49 @@ gnw_status gnw_partition_cells(uint64_t n_cells, int world, int64_t* lo) {
     if (!lo) throw std::invalid_argument("gnw_partition_cells: null output");
     const std::vector<long long> p = gnw::partition_cells(static_cast<long long>(n_cells), world);
     for (size_t r = 0; r < p.size(); ++r) lo[r] = p[r];
+  });
+}
+
+gnw_status gnw_partition_saddle(const gnw_ctx* ctx, int world, int rank, uint64_t sizes[4], int64_t* local_to_global,
+                                int64_t* recv_off, int64_t* send_off, int32_t* send_idx) {
+  return guard([&] {
+    const Context& c = ctx_of(ctx);
+    if (!c.mixed() || !c.assembled()) throw std::invalid_argument("gnw_partition_saddle: not assembled");
+    if (world < 1 || rank < 0 || rank >= world) throw std::invalid_argument("gnw_partition_saddle: bad rank/world");
+    const std::vector<long long> lo = gnw::partition_cells(c.N(), world);
+    const gnw::host::SaddlePartition sp = gnw::host::partition_saddle(c.mesh(), c.Q(), c.D(), lo, rank);
+    const gnw::host::Halo& h = sp.halo;
+    if (sizes) {
+      sizes[0] = sp.K_l;
+      sizes[1] = sp.N_l;
+      sizes[2] = h.ghost_global.size();
+      sizes[3] = h.send_idx.size();
+    }
+    if (local_to_global) {
+      std::copy(h.own_global.begin(), h.own_global.end(), local_to_global);
+      std::copy(h.ghost_global.begin(), h.ghost_global.end(), local_to_global + h.n_own);
+    }
+    if (recv_off) std::copy(h.recv_off.begin(), h.recv_off.end(), recv_off);
+    if (send_off) std::copy(h.send_off.begin(), h.send_off.end(), send_off);
+    if (send_idx) std::copy(h.send_idx.begin(), h.send_idx.end(), send_idx);
+  });
+}
+
+gnw_status gnw_partition_csr(const gnw_ctx* ctx, int world, int rank, int which, uint64_t* n_rows, uint64_t* nnz,
+                             int64_t* rowptr, int32_t* cols, double* vals) {
+  return guard([&] {
+    const Context& c = ctx_of(ctx);
+    if (!c.mixed() || !c.assembled()) throw std::invalid_argument("gnw_partition_csr: not assembled");
+    if (world < 1 || rank < 0 || rank >= world) throw std::invalid_argument("gnw_partition_csr: bad rank/world");
+    const std::vector<long long> lo = gnw::partition_cells(c.N(), world);
+    const gnw::host::SaddlePartition sp = gnw::host::partition_saddle(c.mesh(), c.Q(), c.D(), lo, rank);
+    const gnw::host::Csr* A = which == 0 ? &sp.Q : which == 1 ? &sp.D : which == 2 ? &sp.Dt : nullptr;
+    if (!A) throw std::invalid_argument("gnw_partition_csr: which must be 0 (Q), 1 (D) or 2 (D^T)");
+    if (n_rows) *n_rows = A->n_rows;
+    if (nnz) *nnz = A->nnz();
+    if (rowptr) std::copy(A->rowptr.begin(), A->rowptr.end(), rowptr);
+    if (cols) std::copy(A->cols.begin(), A->cols.end(), cols);
+    if (vals) std::copy(A->vals.begin(), A->vals.end(), vals);
   });
 }
 

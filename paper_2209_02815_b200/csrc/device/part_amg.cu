@@ -2,6 +2,7 @@
 #include "part_amg.cuh"
 
 #include <algorithm>
+#include <cstdlib>
 #include <stdexcept>
 
 namespace gnw {
@@ -148,7 +149,16 @@ void PartAmg::build(const host::AmgHierarchy& h, const std::vector<int32_t>& cel
   sub.coarse_chol = h.coarse_chol;
   sub.nc = h.nc;
   sub.options = h.options;
-  tail_.upload(sub, s);
+  // the tail collapses where the whole hierarchy's cycle would (DeviceAmg::build_collapse's rule)
+  int gc = -1;
+  const char* ce = std::getenv("GNW_VC_COLLAPSE");
+  if (!(ce && std::atoi(ce) == 0))
+    for (int l = 1; l + 1 < L; ++l)
+      if (h.levels[l].A.n_rows <= DeviceAmg::kCollapseMax) {
+        gc = l;
+        break;
+      }
+  tail_.upload(sub, s, gc == lt_ ? 0 : 1);
   const host::Halo& Ht = halos[lt_][me];
   tail_n_ = h.levels[lt_].A.n_rows;
   tail_n_own_ = Ht.n_own;

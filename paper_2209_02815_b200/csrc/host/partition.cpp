@@ -127,4 +127,41 @@ Csr localize(const Csr& A, const std::vector<int64_t>& rows, const Halo& cols, i
   return L;
 }
 
+SaddlePartition partition_saddle(const Mesh& mesh, const Csr& Q, const Csr& D, const std::vector<long long>& cell_lo,
+                                 int me) {
+  const int P = static_cast<int>(cell_lo.size()) - 1;
+  const int64_t K = Q.n_rows, N = D.n_rows;
+  SaddlePartition sp;
+  sp.cell_lo = cell_lo;
+  sp.cell_owner = owners_from_ranges(cell_lo, N);
+  const std::vector<int32_t> edge_own = edge_owners(mesh, sp.cell_owner);
+  std::vector<int32_t> own(static_cast<size_t>(K + N));
+  std::copy(edge_own.begin(), edge_own.end(), own.begin());
+  std::copy(sp.cell_owner.begin(), sp.cell_owner.end(), own.begin() + K);
+  const Csr Dt = transpose(D);
+  std::vector<std::vector<int64_t>> refs(static_cast<size_t>(P)), my_e(static_cast<size_t>(P)),
+      my_c(static_cast<size_t>(P));
+  sp.edge_lo.assign(static_cast<size_t>(P) + 1, 0);
+  for (int r = 0; r < P; ++r) {
+    my_e[r] = owned(edge_own, r);
+    my_c[r] = owned(sp.cell_owner, r);
+    if (!my_e[r].empty() && my_e[r].back() - my_e[r].front() + 1 != static_cast<int64_t>(my_e[r].size()))
+      throw std::logic_error("partition: own edges are not contiguous");
+    sp.edge_lo[r + 1] = sp.edge_lo[r] + static_cast<long long>(my_e[r].size());
+    append_refs(Q, my_e[r], refs[r]);  // Q: edge columns
+    const size_t k0 = refs[r].size();
+    append_refs(Dt, my_e[r], refs[r]);  // D^T: cell columns -> K + c
+    for (size_t k = k0; k < refs[r].size(); ++k) refs[r][k] += K;
+    append_refs(D, my_c[r], refs[r]);  // D: edge columns
+  }
+  std::vector<Halo> H = build_halos(own, P, refs, me);
+  sp.halo = std::move(H[static_cast<size_t>(me)]);
+  sp.K_l = static_cast<int64_t>(my_e[me].size());
+  sp.N_l = static_cast<int64_t>(my_c[me].size());
+  sp.Q = localize(Q, my_e[me], sp.halo);
+  sp.D = localize(D, my_c[me], sp.halo);
+  sp.Dt = localize(Dt, my_e[me], sp.halo, K, sp.K_l);
+  return sp;
+}
+
 }  // namespace gnw::host

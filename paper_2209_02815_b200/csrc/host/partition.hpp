@@ -64,4 +64,18 @@ std::vector<int32_t> coarse_owners(const Csr& P, const std::vector<int32_t>& fin
 // Owned global indices of rank r, ascending.
 std::vector<int64_t> owned(const std::vector<int32_t>& owner, int r);
 
+// Rank `me`'s part of the saddle system [[Q, D^T], [D, 0]] on P ranks: the halo of the combined
+// space (edge e -> e, cell c -> K + c) and the local operators.  Local layout
+// [own edges (K_l) | own cells (N_l) | ghosts]; Dt's columns are stored minus K_l (the kernels
+// address cell columns as x[K_l + col]).
+struct SaddlePartition {
+  std::vector<long long> cell_lo, edge_lo;  // P + 1 contiguous ranges
+  std::vector<int32_t> cell_owner;
+  Halo halo;
+  Csr Q, D, Dt;
+  int64_t K_l = 0, N_l = 0;
+};
+SaddlePartition partition_saddle(const Mesh& mesh, const Csr& Q, const Csr& D, const std::vector<long long>& cell_lo,
+                                 int me);
+
 }  // namespace gnw::host

@@ -397,6 +397,35 @@ def partition_cells(n_cells: int, world: int) -> np.ndarray:
     return lo
 
 
+def partition_saddle(ctx: Context, world: int, rank: int) -> dict:
+    """Rank `rank`'s part of the row partition of the saddle system (gnw_partition_saddle; host
+    only): own edge / cell counts, local -> global map (own entries then ghosts), halo lists."""
+    L = A.load()
+    sz = np.zeros(4, dtype=np.uint64)
+    A.check(L.gnw_partition_saddle(ctx.h, world, rank, sz.ctypes.data, None, None, None, None))
+    ke, nc, ng, ns = (int(v) for v in sz)
+    l2g = np.zeros(ke + nc + ng, np.int64)
+    ro, so = np.zeros(world + 1, np.int64), np.zeros(world + 1, np.int64)
+    si = np.zeros(max(ns, 1), np.int32)
+    A.check(L.gnw_partition_saddle(ctx.h, world, rank, sz.ctypes.data, l2g.ctypes.data, ro.ctypes.data,
+                                   so.ctypes.data, si.ctypes.data))
+    return dict(own_edges=ke, own_cells=nc, ghosts=ng, local_to_global=l2g, recv_off=ro, send_off=so,
+                send_idx=si[:ns])
+
+
+def partition_csr(ctx: Context, world: int, rank: int, which: int):
+    """(n_rows, rowptr, cols, vals) of that rank's local Q (0), D (1) or D^T (2)."""
+    L = A.load()
+    nr, nnz = C.c_uint64(), C.c_uint64()
+    A.check(L.gnw_partition_csr(ctx.h, world, rank, which, C.byref(nr), C.byref(nnz), None, None, None))
+    rp = np.zeros(nr.value + 1, np.int64)
+    ci = np.zeros(max(nnz.value, 1), np.int32)
+    va = np.zeros(max(nnz.value, 1), np.float64)
+    A.check(L.gnw_partition_csr(ctx.h, world, rank, which, C.byref(nr), C.byref(nnz), rp.ctypes.data,
+                                ci.ctypes.data, va.ctypes.data))
+    return nr.value, rp, ci[:nnz.value], va[:nnz.value]
+
+
 def shared_nccl_id() -> bytes:
     """Rank 0's NCCL unique id, broadcast over the initialised torch.distributed group (any
     backend, e.g. gloo for the bootstrap)."""

@@ -1,81 +1,127 @@
-"""Cell-partitioned multi-GPU solve on one GPU: P ranks as threads of one
-process (gnw_create_local_group; every exchange is a host barrier plus device copies, so no
-kernel waits on another rank's kernel) and the NCCL path at world size 1.  Bars: P = 1 is
-bitwise the single-GPU solver; P > 1 is the same solve up to the order of the m-vector sums
-(iterations equal, solutions within 1e-10)."""
+"""Row-partitioned multi-GPU solve (context_rowpart.cu, part_amg.cu) on one GPU:
+P ranks as threads of one process (gnw_create_local_group; every exchange is a host barrier
+plus device copies, so no kernel waits on another rank's kernel) and the NCCL path at world 1.
+
+Each rank owns whole mesh rows of cells and the edges first met in them; MINRES vectors, the
+saddle SpMV and the fine V-cycle levels run on the owned rows with halo exchanges; the coarse
+tail of the V-cycle is replicated; dot products and the m-vector GEMVs are summed over the
+ranks in rank order.  Bars:
+* P = 1 is bitwise the single-GPU solver (same kernels, same row order, one-rank sums);
+* every rank holds the same bits for every result (fixed-order reductions);
+* the V-cycle is bitwise the single-GPU V-cycle at any P (rows sum the same terms in the
+  same order; the replicated tail is the same code on the same data);
+* P > 1 solves agree with one GPU up to the order of the cross-rank sums, and with the
+  reference's own solve on the C5 mesh (tests/golden/ref_p1024.json) at the north-star bar."""
 import numpy as np
 import pytest
 
+import refdata
 from paper_2209_02815_b200 import AmgOptions, Context, nccl_unique_id, run_ranks, workload as W
 
 pytestmark = pytest.mark.gpu
 
 
 def problem(n=32, m=16, index=0):
-    inp = W.gnstep_inputs(n, m, index)
-    return inp
+    return W.gnstep_inputs(n, m, index)
 
 
-def single(inp, alpha, tol):
+def rel(a, c):
+    return np.linalg.norm(np.asarray(a) - np.asarray(c)) / np.linalg.norm(np.asarray(c))
+
+
+def single(inp, alpha, tol, mode="reference", opts=None):
     c = Context(0)
-    c.set_loop_mode(False)  # partitioned contexts run the reference schedule
-    c.assemble(inp.mesh)
+    c.set_loop_mode(mode)
+    c.assemble(inp.mesh, opts)
     c.set_jacobian(inp.J, alpha)
     b = c.assemble_rhs(inp.dm, np.zeros(c.N), inp.dg, np.zeros(inp.J.shape[0]))
     x, rep = c.minres(b, tol=tol)
     y = c.apply_operator(b)
     z = c.precondition(b)
-    return b, x, rep, y, z
+    v = c.amg_apply(b[c.K:])
+    return b, x, rep, y, z, v
 
 
-def partitioned(ctxs, inp, alpha, tol):
+def partitioned(ctxs, inp, alpha, tol, mode="reference", opts=None):
     def body(c, r):
-        c.assemble(inp.mesh)
+        c.set_loop_mode(mode)
+        c.assemble(inp.mesh, opts)
         p = c.partition()
         assert p["rank"] == r and p["world"] == len(ctxs)
         c.set_jacobian(np.ascontiguousarray(inp.J[:, p["c_lo"]:p["c_hi"]]), alpha)
         b = c.assemble_rhs(inp.dm, np.zeros(c.N), inp.dg, np.zeros(inp.J.shape[0]))
         x, rep = c.minres(b, tol=tol)
-        return b, x, rep, c.apply_operator(b), c.precondition(b), p
+        return b, x, rep, c.apply_operator(b), c.precondition(b), c.amg_apply(b[c.K:]), p
     return run_ranks(ctxs, body)
 
 
 def test_local_group_world1_is_bitwise_single_gpu():
     inp = problem()
-    b0, x0, r0, y0, z0 = single(inp, 1e-2, 1e-10)
-    (b1, x1, r1, y1, z1, _), = partitioned(Context.local_group(1), inp, 1e-2, 1e-10)
+    b0, x0, r0, y0, z0, v0 = single(inp, 1e-2, 1e-10)
+    (b1, x1, r1, y1, z1, v1, _), = partitioned(Context.local_group(1), inp, 1e-2, 1e-10)
     assert np.array_equal(b0, b1)
+    assert np.array_equal(v0, v1)
     assert np.array_equal(y0, y1) and np.array_equal(z0, z1)
     assert r1.iterations == r0.iterations
     assert np.array_equal(x0, x1)
 
 
 @pytest.mark.parametrize("world", [2, 3, 4])
-def test_local_group_matches_single_gpu(world):
+@pytest.mark.parametrize("mode", ["reference", "lean"])
+def test_local_group_matches_single_gpu(world, mode):
     inp = problem(64, 32, 0)
-    b0, x0, r0, y0, z0 = single(inp, 1e-2, 1e-10)
-    res = partitioned(Context.local_group(world), inp, 1e-2, 1e-10)
+    b0, x0, r0, y0, z0, v0 = single(inp, 1e-2, 1e-10, mode)
+    res = partitioned(Context.local_group(world), inp, 1e-2, 1e-10, mode)
     los = [p["c_lo"] for *_, p in res] + [res[-1][-1]["c_hi"]]
     assert los[0] == 0 and los[-1] == inp.mesh.n_cells and all(a < b for a, b in zip(los, los[1:]))
-    for b, x, rep, y, z, _ in res:
-        # every rank holds the same bits
+    for b, x, rep, y, z, v, _ in res:  # every rank holds the same bits
         assert np.array_equal(b, res[0][0]) and np.array_equal(x, res[0][1])
         assert rep.iterations == res[0][2].iterations
-    b, x, rep, y, z, _ = res[0]
-    rel = lambda a, c: np.linalg.norm(a - c) / np.linalg.norm(c)
+        assert np.array_equal(z, res[0][4]) and np.array_equal(v, res[0][5])
+    b, x, rep, y, z, v, _ = res[0]
+    assert np.array_equal(v, v0)  # the partitioned V-cycle is the single-GPU V-cycle, bit for bit
     assert rel(b, b0) <= 1e-14
     assert rel(y, y0) <= 1e-13 and rel(z, z0) <= 1e-13
-    # the m-vector sums run in rank order instead of span order: rounding-level differences,
-    # which near a tight tol can move the stopping iteration (the reference's own FMA and
-    # non-FMA builds differ the same way); the early history is unaffected
     h, h0 = rep.relative_residuals, r0.relative_residuals
     assert np.allclose(h[:40], h0[:40], rtol=1e-6, atol=0)
-    assert abs(rep.iterations - r0.iterations) <= 3  # tol 1e-10 sits near the stagnation floor
+    # tol 1e-10 sits near the stagnation floor (the lean schedule's Woodbury-identity rounding
+    # grows like 1/beta): the stopping iteration moves with the rounding of the rank-order sums
+    assert abs(rep.iterations - r0.iterations) <= (3 if mode == "reference" else 6)
     assert rep.converged and rel(x, x0) <= 1e-8, rel(x, x0)
     # at the benchmark tolerance the counts agree within the north star's +-1
-    _, _, r8, _, _ = single(inp, 1e-2, 1e-8)
-    res8 = partitioned(Context.local_group(world), inp, 1e-2, 1e-8)
+    r8 = single(inp, 1e-2, 1e-8, mode)[2]
+    res8 = partitioned(Context.local_group(world), inp, 1e-2, 1e-8, mode)
     assert abs(res8[0][2].iterations - r8.iterations) <= 1
+
+
+def test_local_group_p8_c5_mesh_matches_reference():
+    """P = 8 on the BASELINE C5 mesh (n = 1024, AmgOptions threshold 1024) with the m = 32 proxy
+    J: the partitioned solve at tol 1e-12 against the reference's own solve (iterations +-1,
+    solution within 1e-8), every rank with the same bits."""
+    if not refdata.available("p1024"):
+        pytest.skip("fixture ref_p1024.json not generated")
+    ref = refdata.load("p1024")
+    inp = W.gnstep_inputs(ref["n"], ref["m"], ref["config_index"])
+    opts = AmgOptions(coarse_threshold=ref["coarse_threshold"])
+    ctxs = Context.local_group(8)
+
+    def body(c, r):
+        c.set_loop_mode("reference")
+        c.assemble(inp.mesh, opts)
+        p = c.partition()
+        c.set_jacobian(np.ascontiguousarray(inp.J[:, p["c_lo"]:p["c_hi"]]), ref["alpha"])
+        b = c.assemble_rhs(inp.dm, np.zeros(c.N), inp.dg, np.zeros(ref["m"]))
+        x, rep = c.minres(b, tol=1e-12)
+        return x, rep, c.stats()
+
+    res = run_ranks(ctxs, body)
+    x, rep, st = res[0]
+    for xr, rr, _ in res:
+        assert np.array_equal(xr, x) and rr.iterations == rep.iterations
+    r12 = ref["solves"]["1e-12"]
+    assert rep.converged and abs(rep.iterations - r12["iterations"]) <= 1, (rep.iterations, r12["iterations"])
+    d = refdata.fingerprint_rel(x, r12)
+    assert d["max"] <= 1e-8, d
 
 
 def test_local_group_laplace_and_errors():
@@ -94,8 +140,8 @@ def test_local_group_laplace_and_errors():
 
 def test_nccl_world1_is_bitwise_single_gpu():
     inp = problem()
-    b0, x0, r0, y0, z0 = single(inp, 1e-2, 1e-10)
+    b0, x0, r0, y0, z0, v0 = single(inp, 1e-2, 1e-10)
     c = Context.partitioned(0, 1, nccl_unique_id(), 0)
-    (b1, x1, r1, y1, z1, p), = partitioned([c], inp, 1e-2, 1e-10)
+    (b1, x1, r1, y1, z1, v1, p), = partitioned([c], inp, 1e-2, 1e-10)
     assert p == {"rank": 0, "world": 1, "c_lo": 0, "c_hi": inp.mesh.n_cells}
     assert np.array_equal(b0, b1) and np.array_equal(x0, x1) and r1.iterations == r0.iterations

@@ -1,8 +1,10 @@
-"""Host side of the cell-partitioned solve with two gloo ranks on CPU:
+"""Host side of the row-partitioned solve with two gloo ranks on CPU:
 the NCCL id bootstrap, the partition rule, the per-rank slice of the synthetic Jacobian
-(distributed CholeskyQR2), and the exchange algebra the device path implements -- a
-fixed-order sum of per-rank m-vector partials for J x, and an allgather of the owners'
-cell slices for J^T u."""
+(distributed CholeskyQR2), the m-vector reduction (fixed-order sum of the rank partials) and
+the saddle halo plan of libgnw itself (gnw_partition_saddle / gnw_partition_csr: the same
+host/partition.cpp the device path uploads) driven through a real exchange: every rank fills
+its ghosts from the owners' send lists over gloo and applies its local Q, D, D^T -- the owned
+rows must equal the global operator's rows bit for bit."""
 import os
 import socket
 
@@ -49,7 +51,24 @@ def _worker(rank, ws, port, out):
         jt_own = Jr.T @ u  # own cells of J^T u
         slices = [None] * ws
         dist.all_gather_object(slices, (c0, c1, jt_own, Jr))
-        out[rank] = dict(ids=ids, lo=lo.tolist(), u=u, slices=slices, x=x)
+        # the saddle halo plan (libgnw host code) and one exchange over gloo
+        from paper_2209_02815_b200 import Context, partition_csr, partition_saddle
+        mesh = W.unit_square_mesh(n)
+        ctx = Context(None).assemble(mesh)
+        K = ctx.K
+        plan = partition_saddle(ctx, ws, rank)
+        l2g, so, si, ro = plan["local_to_global"], plan["send_off"], plan["send_idx"], plan["recv_off"]
+        no = plan["own_edges"] + plan["own_cells"]
+        z = W.gaussian(91, K + N)  # a global saddle vector
+        zl = np.zeros(len(l2g))
+        zl[:no] = z[l2g[:no]]  # own entries only; ghosts come from their owners
+        payload = {q: zl[si[so[q]:so[q + 1]]] for q in range(ws)}
+        got = [None] * ws
+        dist.all_gather_object(got, payload)
+        for q in range(ws):
+            zl[no + ro[q]:no + ro[q + 1]] = got[q][rank]
+        mats = {w: partition_csr(ctx, ws, rank, w) for w in (0, 1, 2)}
+        out[rank] = dict(ids=ids, lo=lo.tolist(), u=u, slices=slices, x=x, plan=plan, zl=zl, z=z, mats=mats, K=K)
     finally:
         dist.destroy_process_group()
 
@@ -80,6 +99,38 @@ def test_partitioned_host_logic_gloo_ws2():
     assert np.allclose(res[0]["u"], J @ x, rtol=1e-12, atol=1e-14)
     jt = np.concatenate([s[2] for s in res[0]["slices"]])
     assert np.allclose(jt, J.T @ (J @ x), rtol=1e-11, atol=1e-13)
+    # the halo exchange delivered exactly the ghosts' global values
+    for r in range(ws):
+        p, zl, z = res[r]["plan"], res[r]["zl"], res[r]["z"]
+        assert np.array_equal(zl, z[p["local_to_global"]])
+    # owned rows, ascending and disjoint, cover the saddle space; ghosts are owned elsewhere
+    own = [res[r]["plan"]["local_to_global"][:res[r]["plan"]["own_edges"] + res[r]["plan"]["own_cells"]]
+           for r in range(ws)]
+    allown = np.sort(np.concatenate(own))
+    K = res[0]["K"]
+    assert np.array_equal(allown, np.arange(K + N))
+    for r in range(ws):
+        gh = res[r]["plan"]["local_to_global"][len(own[r]):]
+        assert not np.isin(gh, own[r]).any() and np.isin(gh, own[1 - r]).all()
+    # local operators on the exchanged vector = the global operator's owned rows, bit for bit
+    import scipy.sparse as sp
+    from paper_2209_02815_b200 import Context
+    g = Context(None).assemble(W.unit_square_mesh(32))
+    Q = sp.csr_matrix(tuple(reversed(g.export_csr(0)[2:])), shape=(K, K))
+    D = sp.csr_matrix(tuple(reversed(g.export_csr(1)[2:])), shape=(N, K))
+    z = res[0]["z"]
+    y_glob = np.concatenate([Q @ z[:K] + D.T @ z[K:], D @ z[:K]])
+    for r in range(ws):
+        p, zl, m = res[r]["plan"], res[r]["zl"], res[r]["mats"]
+        ke, nc = p["own_edges"], p["own_cells"]
+
+        def apply(w, x):
+            nr, rp, ci, va = m[w]
+            return np.array([sum(va[k] * x[ci[k]] for k in range(rp[i], rp[i + 1])) for i in range(nr)])
+        ye = np.array([a + b for a, b in zip(apply(0, zl), apply(2, zl[ke:]))])
+        yc = apply(1, zl)
+        loc = np.concatenate([ye, yc])
+        assert np.allclose(loc, y_glob[p["local_to_global"][:ke + nc]], rtol=1e-14, atol=1e-14)
 
 
 def test_partition_rule_edges():
