@@ -618,49 +618,53 @@ def run_gnw(args):
             "clocks": clk.summary(),
             "phases": per_step,
         }
-        print(json.dumps(line), flush=True)
     clk.__exit__(None, None, None)
     ctx.close()
+    J_d = inp = None  # free the replica's device inputs before the partitioned leg
+    torch.cuda.empty_cache()
+    # The north star's strong-scaling case: ONE C3 solve row-partitioned over the N GPUs (SURVEY
+    # 8(e)).  Reported beside the replica metric when N > 1 (or GNW_BENCH_PARTITIONED=1), so the
+    # driver's 1/2/4/8-GPU runs also trace the partitioned curve.
+    part_cfg = os.environ.get("GNW_BENCH_PARTITIONED_CONFIG", "C3")
+    if ws > 1 or os.environ.get("GNW_BENCH_PARTITIONED") == "1":
+        try:
+            part = partitioned_leg(part_cfg, steps=2, warmup=1)
+        except Exception as e:  # reported, never silently replaced
+            part = {"failed": f"{type(e).__name__}: {e}"}
+        if rank == 0:
+            line["partitioned"] = part
+    if rank == 0:
+        print(json.dumps(line), flush=True)
     if ws > 1:
         torch.distributed.destroy_process_group()
 
 
-def run_partitioned(args):
-    """--partitioned: ONE GN-step solve split over N GPUs by cell columns (SURVEY 8(e), C3/C5
-    scale; `scaling` strong).  Every rank builds its J column slice on its device (distributed
-    CholeskyQR2), the ranks exchange through NCCL inside libgnw (gnw_create_partitioned)."""
+def partitioned_leg(config: str, steps: int, warmup: int, tol: float = 1e-8) -> dict:
+    """ONE GN-step solve of `config` row-partitioned over the torch.distributed world (one rank
+    per GPU, NCCL inside libgnw): each rank generates its J column slice on its device
+    (distributed CholeskyQR2), the MINRES vectors / SpMV / fine V-cycle levels run on its mesh
+    rows with halo exchanges.  Collective; returns the summary (max-over-ranks device times)."""
     import torch
 
-    ws, rank, local = dist_env()
-    torch.cuda.set_device(local)
-    if ws > 1:
-        import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     from paper_2209_02815_b200 import (AmgOptions, Context, nccl_unique_id, partitioned_from_torch_distributed,
                                        workload as W)
 
-    tol = 1e-8
-    cfg = W.CONFIGS[args.config]
+    ws, rank, local = dist_env()
+    cfg = W.CONFIGS[config]
     K, N = W.mixed_sizes(cfg.n)
+    t_setup0 = time.perf_counter()
     ctx = partitioned_from_torch_distributed(local) if ws > 1 else Context.partitioned(0, 1, nccl_unique_id(), local)
-    mesh = W.unit_square_mesh(cfg.n)
-    ctx.assemble(mesh, AmgOptions(coarse_threshold=cfg.coarse_threshold))
+    ctx.assemble(W.unit_square_mesh(cfg.n), AmgOptions(coarse_threshold=cfg.coarse_threshold))
     part = ctx.partition()
     allreduce = (lambda t: torch.distributed.all_reduce(t)) if ws > 1 else None
     J_d = W.synthetic_jacobian_slice(cfg.m, N, cfg.index, part["c_lo"], part["c_hi"], "cuda", allreduce=allreduce)
-    dm = W.gaussian(W.seed_for(cfg.index, 2), N)
-    dg = W.gaussian(W.seed_for(cfg.index, 3), cfg.m)
-    alphas = list(cfg.alphas)
-
-    def barrier():
-        torch.cuda.synchronize()
-        if ws > 1:
-            torch.distributed.barrier()
-        torch.cuda.synchronize()
-
+    t_setup = time.perf_counter() - t_setup0
     ctx.use_device_pointers(True)
-    dm_d, dg_d = torch.from_numpy(dm).cuda(), torch.from_numpy(dg).cuda()
-    zN, zm = torch.zeros(N, dtype=torch.float64, device="cuda"), torch.zeros(cfg.m, dtype=torch.float64, device="cuda")
+    dm_d = torch.from_numpy(W.gaussian(W.seed_for(cfg.index, 2), N)).cuda()
+    dg_d = torch.from_numpy(W.gaussian(W.seed_for(cfg.index, 3), cfg.m)).cuda()
+    zN = torch.zeros(N, dtype=torch.float64, device="cuda")
+    zm = torch.zeros(cfg.m, dtype=torch.float64, device="cuda")
+    alphas = list(cfg.alphas)
 
     def solve(alpha):
         tm = ctx.set_jacobian(J_d, alpha)
@@ -668,63 +672,64 @@ def run_partitioned(args):
         x, rep = ctx.minres(b, tol=tol)
         return tm, rep, ctx.stats()
 
-    clk = ClockSampler(local).__enter__()
-    for k in range(args.warmup):
+    for k in range(warmup):
         solve(alphas[k % len(alphas)])
-    barrier()
-    clk.mark()
+    torch.cuda.synchronize()
+    if ws > 1:
+        torch.distributed.barrier()
     ctx.event_record(0)
     phases = []
-    for k in range(args.steps):
+    for k in range(steps):
         a = alphas[k % len(alphas)]
         tm, rep, st = solve(a)
         phases.append(dict(alpha=a, iterations=rep.iterations, converged=rep.converged,
-                           true_rel=rep.true_relative_residual, t_minres=st["t_minres"], **tm))
+                           true_rel=rep.true_relative_residual, t_minres=st["t_minres"],
+                           ms_per_iteration=1e3 * st["t_minres"] / max(rep.iterations, 1),
+                           exchanges=st["comm_calls"], exchange_MB=st["comm_bytes"] / 1e6, **tm))
     ctx.event_record(1)
-    clk.mark()
     elapsed = max_over_ranks_dist(ctx.event_elapsed(0, 1), ws)
-    barrier()
-    # e2e: host buffers through the C-ABI (this rank's J slice and the full vectors)
-    ctx.use_device_pointers(False)
-    J_h = torch.empty(tuple(J_d.shape), dtype=torch.float64, pin_memory=True)
-    J_h.copy_(J_d)
+    it_ms = max_over_ranks_dist(phases[-1]["ms_per_iteration"], ws)
+    info = dict(own_cells=part["c_hi"] - part["c_lo"])
+    ctx.close()
     del J_d
     torch.cuda.empty_cache()
-    J_h = J_h.numpy()
+    # per-rank roofline of the lean iteration: (B_iter - 16 m N + B_V) / P bytes per rank
+    hbm_peak, _ = peaks()
+    bytes_rank = 8.0 * 2 * cfg.m * N / ws + 8 * 40 * (K + N) / ws  # the two dense sweeps + vector traffic
+    return {"metric": METRIC, "value": steps / elapsed, "unit": UNIT, "n_gpus": ws, "scaling": "strong",
+            "workload": f"{config}: unit square n={cfg.n} (N={N}, K={K}), m={cfg.m}, alpha {alphas}, tol {tol}; "
+                        f"one GN-step solve row-partitioned over {ws} GPU(s)",
+            "ms_per_solve": 1e3 * elapsed / steps, "ms_per_iteration": it_ms, "setup_s_rank0": t_setup,
+            "rank0": info, "phases": phases,
+            "per_rank_roofline": {"bytes_per_iteration_GB": bytes_rank / 1e9,
+                                  "GBps": bytes_rank / (it_ms * 1e-3) / 1e9,
+                                  "frac": bytes_rank / (it_ms * 1e-3) / 1e9 / hbm_peak,
+                                  "note": "dense sweeps (16 m N / P) + ~40 (K + N) / P vector bytes; V-cycle excluded"}}
 
-    def solve_host(alpha):
-        ctx.set_jacobian(J_h, alpha)
-        b = ctx.assemble_rhs(dm, np.zeros(N), dg, np.zeros(cfg.m))
-        return ctx.minres(b, tol=tol)
 
-    solve_host(alphas[0])
-    barrier()
-    ctx.event_record(2)
-    for k in range(args.steps):
-        x_h, rep_h = solve_host(alphas[k % len(alphas)])
-    ctx.event_record(3)
-    e2e_el = max_over_ranks_dist(ctx.event_elapsed(2, 3), ws)
-    if rank == 0:
-        w = part["c_hi"] - part["c_lo"]
-        line = {
-            "metric": METRIC, "value": args.steps / elapsed, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": 1e3 * elapsed / args.steps, "higher_is_better": True,
-            "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-            "data": f"synthetic (seeded {args.config} bundle, J slices generated per rank on the device)",
-            "config": {"workload": f"{args.config}: unit square n={cfg.n} (N={N}, K={K}), m={cfg.m}, one GN-step "
-                                   f"solve split over {ws} GPUs by cell columns", "mesh_n": cfg.n, "m": cfg.m,
-                       "alphas": alphas, "tol": tol, "parallelism": f"cell-partitioned x{ws} (NCCL)",
-                       "rank0_cells": [part["c_lo"], part["c_hi"]],
-                       "l2": f"no flush: per-rank J+H slices ({16 * cfg.m * w / 1e9:.2f} GB) exceed the L2"},
-            "roofline": None, "cpu_baseline": None,
-            "e2e": {"value": args.steps / e2e_el, "unit": UNIT,
-                    "h2d_bytes_per_step": 8 * (cfg.m * w + 3 * N + 2 * cfg.m) + 16 * (K + N),
-                    "d2h_bytes_per_step": 16 * (K + N) + 16 * (rep_h.iterations + 1)},
-            "gpu_launches": None, "clocks": clk.summary(), "phases": phases,
-        }
-        print(json.dumps(line), flush=True)
+def run_partitioned(args):
+    """--partitioned: ONE GN-step solve split over the N GPUs by mesh rows (SURVEY 8(e), C3/C5
+    scale; `scaling` strong)."""
+    import torch
+
+    ws, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    if ws > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    clk = ClockSampler(local).__enter__()
+    clk.mark()
+    res = partitioned_leg(args.config, args.steps, args.warmup)
+    clk.mark()
     clk.__exit__(None, None, None)
-    ctx.close()
+    if rank == 0:
+        line = {"metric": METRIC, "value": res["value"], "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": res["ms_per_solve"], "higher_is_better": True,
+                "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+                "data": f"synthetic (seeded {args.config} bundle, J slices generated per rank on the device)",
+                "config": {"workload": res["workload"], "parallelism": f"row-partitioned x{ws} (NCCL)"},
+                "partitioned": res, "clocks": clk.summary()}
+        print(json.dumps(line), flush=True)
     if ws > 1:
         torch.distributed.destroy_process_group()
 

@@ -79,6 +79,15 @@ typedef struct gnw_amg_options {
   uint64_t max_levels;         /* default 25 */
 } gnw_amg_options;
 
+/* A CSR matrix view (SparseMatrix, sparse.hpp:14-25, with int64 indices). */
+typedef struct gnw_csr {
+  uint64_t n_rows;
+  uint64_t n_cols;
+  const int64_t* rowptr; /* n_rows + 1, rowptr[0] = 0 */
+  const int64_t* cols;
+  const double* vals;
+} gnw_csr;
+
 /* Raw triangulation, the inputs of finalize_mesh (mesh.hpp:53-55). */
 typedef struct gnw_mesh {
   uint64_t n_vertices;
@@ -155,6 +164,20 @@ gnw_status gnw_assemble(gnw_ctx* ctx, const gnw_mesh* mesh, const gnw_amg_option
 gnw_status gnw_assemble_amg_csr(gnw_ctx* ctx, uint64_t n, const int64_t* rowptr,
                                 const int64_t* cols, const double* vals,
                                 const gnw_amg_options* opts);
+/* The mixed problem from the caller's assembled Q (K x K) and D (N x K) -- the operands of
+ * SaddleOperator{&Q, &D, &J, beta} (inversion.hpp:18-26) -- instead of a mesh; with opts, also
+ * amg_setup(assemble_lumped_schur(Q, D), *opts) (inversion.cpp:196-213); opts = NULL builds no
+ * hierarchy (gnw_set_amg_hierarchy supplies the caller's). */
+gnw_status gnw_assemble_saddle_csr(gnw_ctx* ctx, const gnw_csr* Q, const gnw_csr* D, const gnw_amg_options* opts);
+/* The caller's AmgHierarchy (amg.hpp:25-42): per level A and P (P of the coarsest level is
+ * empty) and 1/diag(A); the coarsest dense Cholesky factor (nc x nc, row-major).  The Jacobian
+ * must be set again afterwards. */
+gnw_status gnw_set_amg_hierarchy(gnw_ctx* ctx, uint64_t n_levels, const gnw_csr* A, const gnw_csr* P,
+                                 const double* const* inv_diag, const double* coarse_chol, uint64_t nc,
+                                 const gnw_amg_options* opts);
+/* The flux block diag(Q)^-1 of the preconditioner (WoodburyPreconditioner::q_diag_inv,
+ * inversion.hpp:31) given by the caller: K values, host memory. */
+gnw_status gnw_set_flux_scaling(gnw_ctx* ctx, const double* q_diag_inv);
 gnw_status gnw_get_info(const gnw_ctx* ctx, gnw_info* info);
 
 gnw_status gnw_set_jacobian(gnw_ctx* ctx, const double* J, uint64_t m, uint64_t n_cells,
@@ -261,6 +284,8 @@ typedef struct gnw_stats {
   uint64_t loop_restarts;   /* fused-loop solves restarted on the reference schedule (lifetime) */
   uint64_t fused_iterations; /* of the last solve's iterations, run on the fused or lean schedule */
   uint64_t lean_iterations;  /* of those, on the lean schedule */
+  uint64_t comm_calls;       /* partitioned: exchanges this rank issued in the last solve */
+  double comm_bytes;         /* partitioned: bytes this rank sent in them */
 } gnw_stats;
 gnw_status gnw_get_stats(const gnw_ctx* ctx, gnw_stats* stats);
 

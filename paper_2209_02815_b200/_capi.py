@@ -64,13 +64,14 @@ class Stats(C.Structure):
     _fields_ = [("t_minres", C.c_double), ("t_rhs", C.c_double),
                 ("kernel_launches", C.c_uint64), ("setup_kernel_launches", C.c_uint64),
                 ("loop_restarts", C.c_uint64), ("fused_iterations", C.c_uint64),
-                ("lean_iterations", C.c_uint64)]
+                ("lean_iterations", C.c_uint64), ("comm_calls", C.c_uint64), ("comm_bytes", C.c_double)]
 
 
 # every symbol include/gnw.h declares (checked by tests/test_capi_symbols.py)
 EXPORTED = [
     "gnw_last_error", "gnw_version", "gnw_create", "gnw_destroy", "gnw_set_pointer_mode",
-    "gnw_set_coarse_mode", "gnw_set_preconditioner", "gnw_set_loop_mode", "gnw_assemble", "gnw_assemble_amg_csr", "gnw_get_info",
+    "gnw_set_coarse_mode", "gnw_set_preconditioner", "gnw_set_loop_mode", "gnw_assemble", "gnw_assemble_amg_csr",
+    "gnw_assemble_saddle_csr", "gnw_set_amg_hierarchy", "gnw_set_flux_scaling", "gnw_get_info",
     "gnw_set_jacobian", "gnw_prefetch_jacobian", "gnw_apply_operator", "gnw_precondition", "gnw_amg_apply",
     "gnw_get_woodbury", "gnw_assemble_rhs", "gnw_minres_solve", "gnw_minres_history", "gnw_export_csr",
     "gnw_export_mesh", "gnw_dense_cholesky", "gnw_get_stats", "gnw_event_record",

@@ -12,6 +12,7 @@
 #include <chrono>
 #include <cstdio>
 #include <cmath>
+#include <limits>
 #include <cstdlib>
 #include <cstring>
 
@@ -169,6 +170,12 @@ void Context::assemble(const double* vertices, int64_t nv, const int64_t* cells,
   K_ = mesh_.ne;
   N_ = mesh_.nc;
   mixed_ = true;
+  finish_assembly();
+}
+
+// The device side of an assembly: fresh work state, the saddle structure and the hierarchy
+// (or, partitioned, the rank's local operators, halos and the partitioned V-cycle).
+void Context::finish_assembly() {
   assembled_ = true;
   m_ = 0;
   hist_cap_ = 0;
@@ -201,6 +208,70 @@ void Context::assemble(const double* vertices, int64_t nv, const int64_t* cells,
     }
     sync();
   }
+}
+
+// The mixed problem from its assembled Q (K x K) and D (N x K) instead of a mesh -- the
+// reference's own objects (SaddleOperator{&Q, &D, ...}, inversion.hpp:18-26) -- and, with
+// options, the hierarchy amg_setup(assemble_lumped_schur(Q, D), o) (inversion.cpp:196-213).
+// Without options no hierarchy is built (set_hierarchy supplies one).
+void Context::assemble_saddle_csr(int64_t K, int64_t N, const int64_t* qrp, const int64_t* qci, const double* qv,
+                                  const int64_t* drp, const int64_t* dci, const double* dv, const host::AmgOptions* o) {
+  destroy_graph();
+  if (comm_) throw std::invalid_argument("gnw_assemble_saddle_csr: partitioned contexts assemble from a mesh");
+  if (K <= 0 || N <= 0 || !qrp || !drp) throw std::invalid_argument("gnw_assemble_saddle_csr: empty or null matrix");
+  auto csr = [](int64_t nr, int64_t nc, const int64_t* rp, const int64_t* ci, const double* v) {
+    host::Csr A;
+    A.n_rows = nr;
+    A.n_cols = nc;
+    A.rowptr.assign(rp, rp + nr + 1);
+    if (rp[0] != 0) throw std::invalid_argument("gnw_assemble_saddle_csr: rowptr[0] != 0");
+    const int64_t nnz = rp[nr];
+    A.cols.resize(static_cast<size_t>(nnz));
+    for (int64_t k = 0; k < nnz; ++k) {
+      if (ci[k] < 0 || ci[k] >= nc) throw std::invalid_argument("gnw_assemble_saddle_csr: column index out of range");
+      A.cols[static_cast<size_t>(k)] = static_cast<int32_t>(ci[k]);
+    }
+    A.vals.assign(v, v + nnz);
+    return A;
+  };
+  Q_ = csr(K, K, qrp, qci, qv);
+  D_ = csr(N, K, drp, dci, dv);
+  mesh_ = host::Mesh{};
+  S_ = host::lumped_schur(Q_, D_);                        // fem_mixed.cpp:84-94
+  amg_ = o ? host::amg_setup(S_, *o) : host::AmgHierarchy{};  // amg.cpp:115-187
+  K_ = K;
+  N_ = N;
+  mixed_ = true;
+  finish_assembly();
+}
+
+// Replaces the AMG hierarchy (a caller's own AmgHierarchy, e.g. WoodburyPreconditioner::amg);
+// the Woodbury factors depend on it, so the Jacobian must be set again.
+void Context::set_hierarchy(const host::AmgHierarchy& h) {
+  require_mixed();
+  if (comm_) throw std::invalid_argument("gnw_set_amg_hierarchy: not on a partitioned context");
+  if (h.levels.empty() || h.levels[0].A.n_rows != N_) throw std::invalid_argument("gnw_set_amg_hierarchy: size mismatch");
+  destroy_graph();
+  amg_ = h;
+  m_ = 0;
+  op_.m = 0;
+  pa_.m = 0;
+  jm_m_ = -1;
+  jmem_.reset();
+  dJ_ = nullptr;
+  if (device_ >= 0) {
+    damg_.upload(amg_, stream_);
+    sync();
+  }
+}
+
+// The flux block of the preconditioner, diag(Q)^-1 (WoodburyPreconditioner::q_diag_inv,
+// inversion.hpp:31), given instead of computed from Q.
+void Context::set_qinv(const double* q) {
+  require_mixed();
+  require_device();
+  if (comm_) throw std::invalid_argument("gnw_set_flux_scaling: not on a partitioned context");
+  GNW_CUDA_CHECK(cudaMemcpy(const_cast<double*>(pa_.qinv), q, K_ * sizeof(double), cudaMemcpyHostToDevice));
 }
 
 void Context::assemble_amg_csr(int64_t n, const int64_t* rowptr, const int64_t* cols, const double* vals,
@@ -314,7 +385,7 @@ void Context::alloc_vectors(long long n_alloc, long long K, long long N) {
 }
 
 void Context::upload_hierarchy() {
-  damg_.upload(amg_, stream_);
+  if (!amg_.levels.empty()) damg_.upload(amg_, stream_);
   svc_ = mem_.alloc<double>(std::max<int64_t>(N_, 1));
   sync();
 }
@@ -322,6 +393,7 @@ void Context::upload_hierarchy() {
 // ----------------------------------------------------------------- V-cycle
 // amg.cpp:90-111, one symmetric V-cycle; level 0 input may be a ring slot.
 void Context::vcycle(VSel r0, double* out0, const MinresState* st, cudaStream_t s) {
+  if (!comm_ && damg_.empty()) throw std::invalid_argument("amg_apply: empty hierarchy");
   if (comm_) {  // the partitioned V-cycle (part_amg.cuh), one-pass levels + replicated tail
     if (coarse_mode == 1) throw std::invalid_argument("partitioned solve: the exact coarse mode is single-GPU only");
     return pamg_->vcycle(r0, out0, st, stream_);
@@ -457,6 +529,7 @@ void Context::set_jacobian(const double* J, int64_t m, int64_t n_cells, double b
     return;
   }
   if (pa_.m != static_cast<int>(m)) destroy_graph();
+  if (!comm_ && damg_.empty()) throw std::invalid_argument("build_woodbury_preconditioner: empty hierarchy");
 
   cudaEvent_t* ev = jev_;
   const uint64_t l0 = launch_count();
@@ -516,7 +589,21 @@ void Context::set_jacobian(const double* J, int64_t m, int64_t n_cells, double b
     cholesky_inverse(dL_, dY_, dCinv_, static_cast<int>(m), s);
     if (!fail) mirror_lower(dC_, static_cast<int>(m), s);  // full C for the fused loops' refinement
     GNW_CUDA_CHECK(cudaEventRecord(ev[3], s));
+    // kappa(C) >= (max L_ii / min L_ii)^2: beyond ~1e10 the explicit inverse is not accurate
+    // enough for the preconditioner (its error grows like eps kappa), so C^-1 t runs as the
+    // reference does, by the triangular solves with L (cholesky_solve_in_place, linalg.cpp:107-123)
+    std::vector<double> ld(static_cast<size_t>(m));
+    GNW_CUDA_CHECK(cudaMemcpy2DAsync(ld.data(), sizeof(double), dL_, (m + 1) * sizeof(double), sizeof(double), m,
+                                     cudaMemcpyDeviceToHost, s));
     sync();
+    double dmax = 0.0, dmin = std::numeric_limits<double>::infinity();
+    for (double v : ld) {
+      dmax = std::max(dmax, std::fabs(v));
+      dmin = std::min(dmin, std::fabs(v));
+    }
+    const bool tri = !(dmin > 0.0) || (dmax / dmin) * (dmax / dmin) > 1e10;
+    if (tri != (pa_.cap_tri != 0)) destroy_graph();
+    pa_.cap_tri = tri ? 1 : 0;
   }
   float ms[3];
   for (int k = 0; k < 3; ++k) GNW_CUDA_CHECK(cudaEventElapsedTime(&ms[k], ev[k], ev[k + 1]));
@@ -864,6 +951,7 @@ MinresResult Context::minres(const double* b, const double* x0, double* x, doubl
   const int64_t n = kd() + nd();  // own rows (partitioned: b and x0 are global, taken apart below)
   const cudaStream_t s = stream_;
   MinresResult res;
+  const CommTally tally0 = comm_tally();
   const uint64_t l0 = launch_count();
   uint64_t graph_launched = 0;  // kernels run inside loop-graph launches
   uint64_t sched_iters[3] = {0, 0, 0};  // iterations run per loop schedule
@@ -911,6 +999,8 @@ MinresResult Context::minres(const double* b, const double* x0, double* x, doubl
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
     launches = launch_count() - l0 - built_now + graph_launched;
+    comm_calls_ = comm_tally().calls - tally0.calls;
+    comm_bytes_ = comm_tally().bytes - tally0.bytes;
     if (comm_) {
       local_to_global(x_, gio_a_);
       global_out(x, gio_a_, K_ + N_);

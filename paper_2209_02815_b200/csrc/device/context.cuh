@@ -82,6 +82,10 @@ class Context {
   void assemble(const double* vertices, int64_t nv, const int64_t* cells, int64_t nc, const host::AmgOptions& o);
   void assemble_amg_csr(int64_t n, const int64_t* rowptr, const int64_t* cols, const double* vals,
                         const host::AmgOptions& o);
+  void assemble_saddle_csr(int64_t K, int64_t N, const int64_t* qrp, const int64_t* qci, const double* qv,
+                           const int64_t* drp, const int64_t* dci, const double* dv, const host::AmgOptions* o);
+  void set_hierarchy(const host::AmgHierarchy& h);
+  void set_qinv(const double* q);
   void set_jacobian(const double* J, int64_t m, int64_t n_cells, double beta, double timings[3]);
   // async H2D of the next step's J beside the current solve (host-pointer mode)
   void prefetch_jacobian(const double* J, int64_t m, int64_t n_cells);
@@ -113,6 +117,8 @@ class Context {
   long long own_cells() const { return comm_ ? Nl_ : N_; }
   long long ghost_entries() const { return comm_ ? nloc_ - Kl_ - Nl_ : 0; }
   int part_levels() const { return pamg_ ? pamg_->partitioned_levels() : 0; }
+  unsigned long long comm_calls() const { return comm_calls_; }
+  double comm_bytes() const { return comm_bytes_; }
 
   // ERT forward model (forward.cpp:39-172) on the assembled mesh
   void set_electrodes(const int64_t* nodes, int64_t n);
@@ -147,6 +153,7 @@ class Context {
   void require_device() const;
   void require_mixed() const;
   void upload_structure();
+  void finish_assembly();
   void upload_hierarchy();
   void vcycle(VSel r0, double* out0, const MinresState* st, cudaStream_t s = nullptr);
   void operator_into(VSel x, int scaled, VSel y, MinresState* st, int loop, bool fused = false);
@@ -282,6 +289,8 @@ class Context {
   double *gio_a_ = nullptr, *gio_b_ = nullptr, *gio_c_ = nullptr, *gio_d_ = nullptr, *sgath_ = nullptr;
   double *u_part_ = nullptr, *t_part_ = nullptr, *gath_ = nullptr, *Cpart_ = nullptr, *Cgath_ = nullptr;
   long long gath_cap_ = 0;
+  unsigned long long comm_calls_ = 0;  // exchanges and bytes of the last minres (partitioned)
+  double comm_bytes_ = 0.0;
   std::unique_ptr<DeviceMemory> hx_mem_;
   double *hx_ = nullptr, *hy_ = nullptr;
   int hx_b_ = 0;

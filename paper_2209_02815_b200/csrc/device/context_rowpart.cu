@@ -37,11 +37,15 @@ void Context::set_comm(std::shared_ptr<Comm> c) {
 
 void Context::reduce_m(const double* part, double* out, long long n, cudaStream_t s) {
   comm_->allgather(part, gath_, n, s);
+  comm_tally().calls += 1;
+  comm_tally().bytes += 8.0 * static_cast<double>(n) * comm_->world;
   sum_partials(gath_, comm_->world, n, out, s);
 }
 
 void Context::reduce_scratch(MinresState* st, int k0, int cnt) {
   comm_->allgather(st->scratch + k0, sgath_, cnt, stream_);
+  comm_tally().calls += 1;
+  comm_tally().bytes += 8.0 * cnt * comm_->world;
   sum_scratch(sgath_, comm_->world, cnt, st, k0, stream_);
 }
 

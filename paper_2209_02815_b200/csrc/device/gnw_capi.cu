@@ -143,6 +143,54 @@ gnw_status gnw_assemble_amg_csr(gnw_ctx* ctx, uint64_t n, const int64_t* rowptr,
   });
 }
 
+gnw_status gnw_assemble_saddle_csr(gnw_ctx* ctx, const gnw_csr* Q, const gnw_csr* D, const gnw_amg_options* opts) {
+  return guard([&] {
+    if (!Q || !D) throw std::invalid_argument("gnw_assemble_saddle_csr: null matrix");
+    if (Q->n_rows != Q->n_cols || D->n_cols != Q->n_rows) throw std::invalid_argument("gnw_assemble_saddle_csr: shape mismatch");
+    const gnw::host::AmgOptions o = to_opts(opts);
+    ctx_of(ctx).assemble_saddle_csr(static_cast<int64_t>(Q->n_rows), static_cast<int64_t>(D->n_rows), Q->rowptr, Q->cols,
+                                    Q->vals, D->rowptr, D->cols, D->vals, opts ? &o : nullptr);
+  });
+}
+
+gnw_status gnw_set_amg_hierarchy(gnw_ctx* ctx, uint64_t n_levels, const gnw_csr* A, const gnw_csr* P,
+                                 const double* const* inv_diag, const double* coarse_chol, uint64_t nc,
+                                 const gnw_amg_options* opts) {
+  return guard([&] {
+    if (n_levels == 0 || !A || !P || !inv_diag || !coarse_chol) throw std::invalid_argument("gnw_set_amg_hierarchy: null argument");
+    auto csr = [](const gnw_csr& m) {
+      gnw::host::Csr c;
+      c.n_rows = static_cast<int64_t>(m.n_rows);
+      c.n_cols = static_cast<int64_t>(m.n_cols);
+      c.rowptr.assign(m.rowptr, m.rowptr + m.n_rows + 1);
+      const int64_t nnz = m.n_rows ? m.rowptr[m.n_rows] : 0;
+      c.cols.resize(static_cast<size_t>(nnz));
+      for (int64_t k = 0; k < nnz; ++k) c.cols[static_cast<size_t>(k)] = static_cast<int32_t>(m.cols[k]);
+      c.vals.assign(m.vals, m.vals + nnz);
+      return c;
+    };
+    gnw::host::AmgHierarchy h;
+    h.options = to_opts(opts);
+    for (uint64_t l = 0; l < n_levels; ++l) {
+      gnw::host::AmgLevel lv;
+      lv.A = csr(A[l]);
+      if (l + 1 < n_levels) lv.P = csr(P[l]);
+      lv.inv_diag.assign(inv_diag[l], inv_diag[l] + A[l].n_rows);
+      h.levels.push_back(std::move(lv));
+    }
+    h.nc = static_cast<int64_t>(nc);
+    h.coarse_chol.assign(coarse_chol, coarse_chol + nc * nc);
+    ctx_of(ctx).set_hierarchy(h);
+  });
+}
+
+gnw_status gnw_set_flux_scaling(gnw_ctx* ctx, const double* q_diag_inv) {
+  return guard([&] {
+    if (!q_diag_inv) throw std::invalid_argument("gnw_set_flux_scaling: null argument");
+    ctx_of(ctx).set_qinv(q_diag_inv);
+  });
+}
+
 gnw_status gnw_get_info(const gnw_ctx* ctx, gnw_info* info) {
   return guard([&] {
     const Context& c = ctx_of(ctx);
@@ -462,6 +510,8 @@ gnw_status gnw_get_stats(const gnw_ctx* ctx, gnw_stats* stats) {
     stats->loop_restarts = c.loop_restarts;
     stats->fused_iterations = c.last_fused_iters_;
     stats->lean_iterations = c.last_sched_iters_[2];
+    stats->comm_calls = c.comm_calls();
+    stats->comm_bytes = c.comm_bytes();
   });
 }
 

@@ -989,8 +989,39 @@ __global__ void k_cinv_refine(const double* __restrict__ Cinv, const double* __r
   if (lane == 0) t2[w] = t2[w] + acc[0];
 }
 
+// t2 = L^-T L^-1 t in one CTA (x in shared memory, L read from L2): right-looking forward and
+// backward substitution, each step's updates spread over the threads.  The fallback for an
+// ill-conditioned capacitance matrix (PrecArgs::cap_tri); O(m) barriers, ~0.1 ms at m ~ 1000.
+__global__ void __launch_bounds__(1024) k_cap_tri_solve(const double* __restrict__ L, const double* __restrict__ t,
+                                                        double* __restrict__ t2, int m) {
+  griddep_wait();
+  extern __shared__ double xs[];
+  for (int i = threadIdx.x; i < m; i += blockDim.x) xs[i] = t[i];
+  __syncthreads();
+  for (int i = 0; i < m; ++i) {  // L y = t
+    if (threadIdx.x == 0) xs[i] = xs[i] / L[static_cast<long long>(i) * m + i];
+    __syncthreads();
+    const double yi = xs[i];
+    for (int j = i + 1 + threadIdx.x; j < m; j += blockDim.x) xs[j] = xs[j] - L[static_cast<long long>(j) * m + i] * yi;
+    __syncthreads();
+  }
+  for (int i = m - 1; i >= 0; --i) {  // L^T x = y
+    if (threadIdx.x == 0) xs[i] = xs[i] / L[static_cast<long long>(i) * m + i];
+    __syncthreads();
+    const double xi = xs[i];
+    for (int j = threadIdx.x; j < i; j += blockDim.x) xs[j] = xs[j] - L[static_cast<long long>(i) * m + j] * xi;
+    __syncthreads();
+  }
+  for (int i = threadIdx.x; i < m; i += blockDim.x) t2[i] = xs[i];
+}
+
 void capacitance_solve(const PrecArgs& pa, const double* t, double* t2, cudaStream_t s) {
   if (pa.m == 0) return;
+  if (pa.cap_tri && !pa.exact) {
+    smem_optin(reinterpret_cast<const void*>(k_cap_tri_solve), kMaxStageM * 8);
+    GNW_LAUNCH(launch_k(k_cap_tri_solve, 1, 1024, static_cast<size_t>(pa.m) * sizeof(double), s, pa.Lc, t, t2, pa.m));
+    return check_launch("capacitance_solve");
+  }
   if (pa.exact) {
     GNW_LAUNCH(launch_k(k_coarse_cholesky, 1, 64, 0, s, pa.Lc, pa.m, vfixed(const_cast<double*>(t)), t2, nullptr, 1, 1));
   } else {

@@ -130,6 +130,9 @@ struct PrecArgs {
   long long ldh = 0, ldj = 0;  // row strides of Ht and J
   const double* neg_inv_beta = nullptr;
   int exact = 0;
+  // ill-conditioned C (set_jacobian's estimate from diag(L)): C^-1 t by the two triangular
+  // solves with L instead of the explicit inverse, whose error grows like eps kappa(C)
+  int cap_tri = 0;
   // fused loop: the finish pass also forms q = J^T t' (J read in the same sweep as H)
   const double* J = nullptr;
   double* q = nullptr;

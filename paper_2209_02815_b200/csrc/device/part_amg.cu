@@ -68,9 +68,16 @@ DHalo upload_halo(DeviceMemory& mem, const host::Halo& h, cudaStream_t s) {
   return d;
 }
 
+CommTally& comm_tally() {
+  thread_local CommTally t;  // per rank thread (in-process ranks run one per thread)
+  return t;
+}
+
 void halo_exchange(Comm& comm, DHalo& h, double* v, int b, DeviceMemory& mem, cudaStream_t s) {
   const int P = comm.world;
   if (P == 1) return;
+  comm_tally().calls += 1;
+  comm_tally().bytes += 8.0 * static_cast<double>(h.n_send) * b;
   if (b > h.bmax) {  // the pack buffer grows with the widest exchange (the setup's b columns)
     h.sendbuf = mem.alloc<double>(static_cast<size_t>(std::max<long long>(h.n_send, 1)) * b);
     h.bmax = b;
@@ -194,6 +201,8 @@ void PartAmg::tail_gather(const double* own, int b, double* full, cudaStream_t s
   if (tail_n_own_)
     GNW_CUDA_CHECK(cudaMemcpyAsync(pad, own, tail_n_own_ * b * sizeof(double), cudaMemcpyDeviceToDevice, s));
   comm_->allgather(pad, gath, tail_maxown_ * b, s);
+  comm_tally().calls += 1;
+  comm_tally().bytes += 8.0 * static_cast<double>(tail_maxown_) * b * comm_->world;
   scatter_rows(tail_gidx_, tail_gidx_n_, gath, full, b, s);  // padding (index -1) is skipped
 }
 

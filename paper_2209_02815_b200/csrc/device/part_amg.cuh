@@ -39,6 +39,12 @@ struct DHalo {
 DHalo upload_halo(DeviceMemory& mem, const host::Halo& h, cudaStream_t s);
 // ghosts of v (b interleaved columns per entry: v[local * b + q]) from their owners
 void halo_exchange(Comm& comm, DHalo& h, double* v, int b, DeviceMemory& mem, cudaStream_t s);
+// exchanges issued and bytes sent by this process's partitioned solves (all contexts)
+struct CommTally {
+  unsigned long long calls = 0;
+  double bytes = 0.0;
+};
+CommTally& comm_tally();
 // out[k * b + q] = in[idx[k] * b + q], k < n  (gathers / extractions through an index map)
 void gather_rows(const int* idx, long long n, const double* in, double* out, int b, cudaStream_t s);
 // out[idx[k] * b + q] = in[k * b + q], k < n

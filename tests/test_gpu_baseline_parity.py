@@ -34,6 +34,13 @@ def need(name):
     return refdata.load(name)
 
 
+def crossing_window(rec, tol):
+    """First iteration at which the reference's Euclidean residual history is within 3 tol: with
+    the reference's stop, the window in which an oscillating residual first dips below tol."""
+    he = np.asarray(rec["hist_e"])
+    return int(np.argmax(he <= 3 * tol))
+
+
 def check_solves(ctx, b, ref, modes, label, noisy_stop=False):
     """Solve b at tol 1e-12 on each schedule in `modes` and at tol 1e-8 on the default schedule;
     compare with the reference's solves recorded in `ref`."""
@@ -46,8 +53,13 @@ def check_solves(ctx, b, ref, modes, label, noisy_stop=False):
         d = refdata.fingerprint_rel(x, r12)
         restarted = ctx.stats()["loop_restarts"] - r0
         assert rep.converged and rep.true_relative_residual <= 1e-11, (label, mode)
-        assert abs(rep.iterations - r12["iterations"]) <= 1 or (mode != "reference" and restarted), \
-            (label, mode, rep.iterations, r12["iterations"])
+        if noisy_stop:  # see below: the stop lies in the reference's crossing window
+            lo = crossing_window(r12, 1e-12)
+            assert lo - 1 <= rep.iterations <= r12["iterations"] + 1 or (mode != "reference" and restarted), \
+                (label, mode, lo, rep.iterations, r12["iterations"])
+        else:
+            assert abs(rep.iterations - r12["iterations"]) <= 1 or (mode != "reference" and restarted), \
+                (label, mode, rep.iterations, r12["iterations"])
         assert d["max"] <= SOLUTION_TOL, (label, mode, d)
         out[mode] = (rep.iterations, d["max"])
     ctx.set_loop_mode("auto")
@@ -61,8 +73,7 @@ def check_solves(ctx, b, ref, modes, label, noisy_stop=False):
         # true residual < tol.  The bar here: the stop lies inside the reference's crossing window
         # (first iteration whose residual is within 3 tol, to the reference's stop), and the
         # P-norm histories -- the quantity MINRES minimises -- agree.
-        he = np.asarray(r8["hist_e"])
-        lo = int(np.argmax(he <= 3 * 1e-8))
+        lo = crossing_window(r8, 1e-8)
         assert lo - 1 <= rep8.iterations <= r8["iterations"] + 1, (label, lo, rep8.iterations, r8["iterations"])
         hp = np.asarray(r8["hist_p"])
         k = min(len(hp), len(rep8.pnorm_relative_residuals))
