@@ -18,11 +18,13 @@
 #include <cmath>
 #include <cstdlib>
 #include <stdexcept>
+#include <cooperative_groups.h>
 #include <mutex>
 #include <set>
 #include <string>
 
 #include "kernels.cuh"
+#include "minres_scalars.cuh"
 
 namespace gnw {
 
@@ -989,6 +991,61 @@ __global__ void k_cinv_refine(const double* __restrict__ Cinv, const double* __r
   if (lane == 0) t2[w] = t2[w] + acc[0];
 }
 
+// t2 = C^-1 t (+ one refinement step) as ONE launch of a thread-block cluster: each CTA owns a
+// slice of the rows; the m-vectors live in shared memory and every CTA gathers the others'
+// slices through distributed shared memory between the phases.  The rows are summed exactly
+// as k_cinv_apply / k_cap_residual / k_cinv_refine sum them (warp per row, lane-strided, xor
+// tree), so the result is bit-identical to the three launches it replaces -- for small m
+// (C1 m = 32, C2 m = 256) those launches are pure latency on the MINRES critical path.
+__global__ void __launch_bounds__(1024) k_cap_solve_cluster(const double* __restrict__ Cinv, const double* __restrict__ C,
+                                                            const double* __restrict__ t, double* __restrict__ t2,
+                                                            int m, int refine) {
+  griddep_wait();
+  namespace cg = cooperative_groups;
+  cg::cluster_group cl = cg::this_cluster();
+  extern __shared__ double sm[];
+  double* ts = sm;           // t
+  double* xs = sm + m;       // t2
+  double* rs = sm + 2 * m;   // t - C t2
+  const int ncl = static_cast<int>(cl.num_blocks()), me = static_cast<int>(cl.block_rank());
+  const int per = (m + ncl - 1) / ncl, r0 = me * per, r1 = min(m, r0 + per);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int i = threadIdx.x; i < m; i += blockDim.x) ts[i] = t[i];
+  __syncthreads();
+  auto rowdot = [&](const double* __restrict__ A, const double* x, int w) {
+    double acc[1] = {0.0};
+    for (int j = lane; j < m; j += 32) acc[0] = acc[0] + __ldg(&A[static_cast<long long>(w) * m + j]) * x[j];
+    warp_reduce<1>(acc);
+    return acc[0];
+  };
+  auto gather = [&](double* v) {  // the other CTAs' slices of v into this CTA's copy
+    cl.sync();
+    for (int i = threadIdx.x; i < m; i += blockDim.x) {
+      const int owner = i / per;
+      if (owner != me) v[i] = cl.map_shared_rank(v, owner)[i];
+    }
+    cl.sync();
+  };
+  for (int w = r0 + warp; w < r1; w += nw) {
+    const double a = rowdot(Cinv, ts, w);
+    if (lane == 0) xs[w] = a;
+  }
+  if (refine) {
+    gather(xs);
+    for (int w = r0 + warp; w < r1; w += nw) {
+      const double a = rowdot(C, xs, w);
+      if (lane == 0) rs[w] = ts[w] - a;
+    }
+    gather(rs);
+    for (int w = r0 + warp; w < r1; w += nw) {
+      const double a = rowdot(Cinv, rs, w);
+      if (lane == 0) xs[w] = xs[w] + a;
+    }
+  }
+  __syncthreads();
+  for (int i = r0 + static_cast<int>(threadIdx.x); i < r1; i += blockDim.x) t2[i] = xs[i];
+}
+
 // t2 = L^-T L^-1 t in one CTA (x in shared memory, L read from L2): right-looking forward and
 // backward substitution, each step's updates spread over the threads.  The fallback for an
 // ill-conditioned capacitance matrix (PrecArgs::cap_tri); O(m) barriers, ~0.1 ms at m ~ 1000.
@@ -1024,6 +1081,27 @@ void capacitance_solve(const PrecArgs& pa, const double* t, double* t2, cudaStre
   }
   if (pa.exact) {
     GNW_LAUNCH(launch_k(k_coarse_cholesky, 1, 64, 0, s, pa.Lc, pa.m, vfixed(const_cast<double*>(t)), t2, nullptr, 1, 1));
+  } else if (pa.m <= kCapClusterMaxM) {  // one cluster launch instead of three (small m: latency)
+    const int refine = (pa.Cfull && pa.cres) ? 1 : 0;
+    const int ncl = std::min(8, std::max(1, (pa.m + 31) / 32));
+    const size_t smem = 3 * static_cast<size_t>(pa.m) * sizeof(double);
+    smem_optin(reinterpret_cast<const void*>(k_cap_solve_cluster), 3 * kCapClusterMaxM * 8);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(ncl);
+    cfg.blockDim = dim3(1024);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[2];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = ncl;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[1].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = g_pdl ? 2 : 1;
+    GNW_LAUNCH(cudaLaunchKernelEx(&cfg, k_cap_solve_cluster, pa.Cinv, static_cast<const double*>(pa.Cfull), t, t2,
+                                  pa.m, refine));
   } else {
     const unsigned g = grid_for(static_cast<long long>(pa.m) * 32);
     GNW_LAUNCH(launch_k(k_cinv_apply, g, kTpb, 0, s, pa.Cinv, t, t2, pa.m));
@@ -1055,9 +1133,6 @@ void mirror_lower(double* C, int n, cudaStream_t s) {
   check_launch("mirror_lower");
 }
 
-__device__ void finish_scalars(const double (&tot)[3], const double* __restrict__ dots_edge, int n_edge_blocks,
-                               int loop, MinresState* st, double* red);
-__device__ void givens_step(double gsq, double zz, double vv, MinresState* st);
 
 template <int B>
 __global__ void __launch_bounds__(kTpb, B >= 16 ? 5 : 8) k_finish_prec(PrecArgs pa, const double* __restrict__ svc,
@@ -1097,51 +1172,6 @@ __global__ void __launch_bounds__(kTpb, B >= 16 ? 5 : 8) k_finish_prec(PrecArgs 
   double tot[3];
   if (!grid_reduce_last<3>(d, part, counter, red, tot)) return;
   finish_scalars(tot, dots_edge, n_edge_blocks, loop, st, red);
-}
-
-// k_finish_prec's tail: add the combine kernel's partials (edge blocks: all three; cell
-// blocks: <v,v>) to the cell totals, then gamma_next and the Givens rotation.
-__device__ void finish_scalars(const double (&tot)[3], const double* __restrict__ dots_edge, int n_edge_blocks,
-                               int loop, MinresState* st, double* red) {
-  double e3[3] = {0.0, 0.0, 0.0};
-  for (int b = threadIdx.x; b < n_edge_blocks; b += blockDim.x)
-    for (int k = 0; k < 3; ++k) e3[k] += __ldcg(&dots_edge[b * 3 + k]);
-  block_reduce<3>(e3, red);
-  if (threadIdx.x != 0) return;
-  const double gsq = e3[0] + tot[0], zz = e3[1] + tot[1], vv = e3[2] + tot[2];
-  if (!loop) {
-    st->scratch[0] = gsq;
-    st->scratch[1] = zz;
-    st->scratch[2] = vv;
-    return;
-  }
-  givens_step(gsq, zz, vv, st);
-}
-
-// minres.cpp:79-101: gamma_next and the Givens rotation from <z,v>, <z,z>, <v,v>
-__device__ void givens_step(double gsq, double zz, double vv, MinresState* st) {
-  if (gsq < -1e-12 * (sqrt(zz) * sqrt(vv) + 1.0)) {
-    st->status = kErrNotPD;
-    return;
-  }
-  const double gamma_next = sqrt(fmax(gsq, 0.0));
-  const double delta = st->delta, gc = st->gamma_cur;
-  const double alpha0 = st->c_cur * delta - st->c_prev * st->s_cur * gc;
-  const double alpha1 = sqrt(alpha0 * alpha0 + gamma_next * gamma_next);
-  const double alpha2 = st->s_cur * delta + st->c_prev * st->c_cur * gc;
-  const double alpha3 = st->s_prev * gc;
-  if (alpha1 == 0.0) {
-    st->status = kErrStagnated;
-    return;
-  }
-  st->gamma_next = gamma_next;
-  st->c_next = alpha0 / alpha1;
-  st->s_next = gamma_next / alpha1;
-  st->alpha2 = alpha2;
-  st->alpha3 = alpha3;
-  st->inv_alpha1 = 1.0 / alpha1;
-  st->tau = st->c_next * st->eta;
-  st->eta = -st->s_next * st->eta;
 }
 
 __global__ void k_givens_from_scratch(MinresState* st) {
