@@ -3,6 +3,8 @@
 
 #include <algorithm>
 #include <cstdlib>
+#include <cstring>
+#include <unordered_map>
 
 namespace gnw {
 
@@ -32,32 +34,74 @@ DCsr upload_csr(DeviceMemory& mem, const host::Csr& A, cudaStream_t s) {
   return d;
 }
 
-DSell upload_sell(DeviceMemory& mem, const host::Csr& A, cudaStream_t s) {
+DSell upload_sell(DeviceMemory& mem, const host::Csr& A, cudaStream_t s, int encode) {
   DSell d;
   int64_t w = 0;
   for (int64_t r = 0; r < A.n_rows; ++r) w = std::max(w, A.rowptr[r + 1] - A.rowptr[r]);
   if (A.n_rows == 0 || w == 0 || w > kSellMaxWidth || A.n_rows > 0x7fffffffLL) return d;
+  // the value encoding (common.cuh DSell): signs in the columns, or one-byte codes
+  std::vector<double> table;
+  std::unordered_map<uint64_t, unsigned char> code_of;  // value bits -> code
+  auto bits = [](double v) {
+    uint64_t b;
+    std::memcpy(&b, &v, sizeof b);
+    return b;
+  };
+  if (encode == 1)
+    for (double v : A.vals)
+      if (v != 1.0 && v != -1.0) encode = 2;
+  if (encode == 2) {
+    for (double v : A.vals) {
+      if (code_of.count(bits(v))) continue;
+      if (table.size() == 256) {
+        encode = 0;
+        break;
+      }
+      code_of[bits(v)] = static_cast<unsigned char>(table.size());
+      table.push_back(v);
+    }
+  }
   const int64_t slices = (A.n_rows + 31) / 32;
   const size_t len = static_cast<size_t>(slices * 32 * w);
   std::vector<int> cols(len, -1);
-  std::vector<double> vals(len, 0.0);
+  std::vector<double> vals(encode == 0 ? len : 0, 0.0);
+  std::vector<unsigned char> codes(encode == 2 ? len : 0, 0);
   for (int64_t r = 0; r < A.n_rows; ++r) {
     const int64_t base = (r / 32) * 32 * w + (r % 32);
     for (int64_t k = A.rowptr[r]; k < A.rowptr[r + 1]; ++k) {
-      const int64_t j = k - A.rowptr[r];
-      cols[static_cast<size_t>(base + 32 * j)] = A.cols[static_cast<size_t>(k)];
-      vals[static_cast<size_t>(base + 32 * j)] = A.vals[static_cast<size_t>(k)];
+      const size_t at = static_cast<size_t>(base + 32 * (k - A.rowptr[r]));
+      const int c = A.cols[static_cast<size_t>(k)];
+      const double v = A.vals[static_cast<size_t>(k)];
+      if (encode == 1) {
+        cols[at] = v == 1.0 ? c : -c - 2;
+      } else if (encode == 2) {
+        cols[at] = c;
+        codes[at] = code_of.at(bits(v));
+      } else {
+        cols[at] = c;
+        vals[at] = v;
+      }
     }
   }
   int* dc = mem.alloc<int>(len);
-  double* dv = mem.alloc<double>(len);
   GNW_CUDA_CHECK(cudaMemcpyAsync(dc, cols.data(), len * sizeof(int), cudaMemcpyHostToDevice, s));
-  GNW_CUDA_CHECK(cudaMemcpyAsync(dv, vals.data(), len * sizeof(double), cudaMemcpyHostToDevice, s));
+  if (encode == 0) {
+    double* dv = mem.alloc<double>(len);
+    GNW_CUDA_CHECK(cudaMemcpyAsync(dv, vals.data(), len * sizeof(double), cudaMemcpyHostToDevice, s));
+    d.vals = dv;
+  } else if (encode == 2) {
+    unsigned char* dh = mem.alloc<unsigned char>(len);
+    double* dt = mem.alloc<double>(table.size());
+    GNW_CUDA_CHECK(cudaMemcpyAsync(dh, codes.data(), len, cudaMemcpyHostToDevice, s));
+    GNW_CUDA_CHECK(cudaMemcpyAsync(dt, table.data(), table.size() * sizeof(double), cudaMemcpyHostToDevice, s));
+    d.codes = dh;
+    d.table = dt;
+  }
+  d.signed_cols = encode == 1 ? 1 : 0;
   GNW_CUDA_CHECK(cudaStreamSynchronize(s));  // host vectors are temporaries
   d.n_rows = static_cast<int>(A.n_rows);
   d.width = static_cast<int>(w);
   d.cols = dc;
-  d.vals = dv;
   return d;
 }
 

@@ -41,8 +41,10 @@ struct DeviceMemory {
 };
 
 DCsr upload_csr(DeviceMemory& mem, const host::Csr& A, cudaStream_t s);
-// SELL-32 copy of A (common.cuh); width 0 (nothing allocated) if a row exceeds kSellMaxWidth
-DSell upload_sell(DeviceMemory& mem, const host::Csr& A, cudaStream_t s);
+// SELL-32 copy of A (common.cuh); width 0 (nothing allocated) if a row exceeds kSellMaxWidth.
+// encode: 0 values as doubles; 1 signs in the columns (all values +-1, else falls back to 2);
+// 2 one-byte value codes (at most 256 distinct values, else falls back to 0)
+DSell upload_sell(DeviceMemory& mem, const host::Csr& A, cudaStream_t s, int encode = 0);
 // sparse_matmul on the device, bit-identical to host::spgemm (spgemm.cu)
 host::Csr device_spgemm(const host::Csr& A, const host::Csr& B, cudaStream_t s);
 

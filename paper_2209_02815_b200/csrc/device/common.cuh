@@ -131,24 +131,32 @@ struct DCsr {
 // padding has col = -1 and is skipped, so a row sum adds exactly the CSR terms in the CSR
 // order (bit-identical to the CSR loop).  width = 0: not built (row longer than kSellMaxWidth).
 constexpr int kSellMaxWidth = 8;
+// Compact encodings of the VALUES (the saddle operator's Q, D, D^T; context.cu):
+//   signed_cols: every value is +1 or -1 (D, D^T: cell_edge_signs) -- no value array; entry
+//     (c, -1) is stored as column -c - 2 (padding keeps -1);
+//   codes: at most 256 distinct values (Q of a unit-square mesh has four: 2/3, 1/3, -1/6, 0) --
+//     one byte per entry indexing `table`.
+// The decoded value is the same double, so every product and sum is bit-identical; the saddle
+// kernel then streams 4-5 bytes per entry instead of 12.
 struct DSell {
   int n_rows = 0, width = 0;
   const int* cols = nullptr;
   const double* vals = nullptr;
+  const unsigned char* codes = nullptr;
+  const double* table = nullptr;
+  int signed_cols = 0;
 };
 
 // sum_k vals[k] * (x[off + cols[k]] * sc)  (sc applied only when scaled), in CSR order
 template <int W>
+__device__ __forceinline__ void sell_load(const DSell& A, long long row, int (&c)[W], double (&v)[W]);
+
+template <int W>
 __device__ __forceinline__ double sell_row_w(const DSell& A, long long row, const double* __restrict__ x,
                                              long long off, bool scaled, double sc) {
-  const long long base = (row >> 5) * 32LL * W + (row & 31);
   int c[W];
   double v[W];
-#pragma unroll
-  for (int k = 0; k < W; ++k) {
-    c[k] = __ldg(A.cols + base + 32 * k);
-    v[k] = __ldg(A.vals + base + 32 * k);
-  }
+  sell_load<W>(A, row, c, v);
 #pragma unroll
   for (int k = 0; k < W; ++k) {
     const double xv = c[k] >= 0 ? x[off + c[k]] : 0.0;
@@ -166,10 +174,28 @@ __device__ __forceinline__ double sell_row_w(const DSell& A, long long row, cons
 template <int W>
 __device__ __forceinline__ void sell_load(const DSell& A, long long row, int (&c)[W], double (&v)[W]) {
   const long long base = (row >> 5) * 32LL * W + (row & 31);
+  if (A.signed_cols) {
 #pragma unroll
-  for (int k = 0; k < W; ++k) {
-    c[k] = __ldg(A.cols + base + 32 * k);
-    v[k] = __ldg(A.vals + base + 32 * k);
+    for (int k = 0; k < W; ++k) {
+      const int q = __ldg(A.cols + base + 32 * k);
+      c[k] = q >= -1 ? q : -q - 2;
+      v[k] = q >= -1 ? 1.0 : -1.0;
+    }
+  } else if (A.codes) {
+    unsigned char h[W];
+#pragma unroll
+    for (int k = 0; k < W; ++k) {
+      c[k] = __ldg(A.cols + base + 32 * k);
+      h[k] = __ldg(A.codes + base + 32 * k);
+    }
+#pragma unroll
+    for (int k = 0; k < W; ++k) v[k] = __ldg(A.table + h[k]);
+  } else {
+#pragma unroll
+    for (int k = 0; k < W; ++k) {
+      c[k] = __ldg(A.cols + base + 32 * k);
+      v[k] = __ldg(A.vals + base + 32 * k);
+    }
   }
 }
 template <int W>

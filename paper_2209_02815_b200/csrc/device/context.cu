@@ -61,6 +61,7 @@ Context::Context(int device) : device_(device) {
   }
   for (auto& e : mev_) GNW_CUDA_CHECK(cudaEventCreate(&e));
   for (auto& e : rhs_ev_) GNW_CUDA_CHECK(cudaEventCreate(&e));
+  for (auto& e : tri_ev_) GNW_CUDA_CHECK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   // host->device staging of the next Jacobian (prefetch_jacobian) runs on its own stream
   GNW_CUDA_CHECK(cudaStreamCreateWithFlags(&copy_, cudaStreamNonBlocking));
   for (auto& e : stage_ev_) GNW_CUDA_CHECK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
@@ -84,6 +85,8 @@ Context::~Context() {
   for (auto& e : jev_)
     if (e) cudaEventDestroy(e);
   for (auto& e : rhs_ev_)
+    if (e) cudaEventDestroy(e);
+  for (auto& e : tri_ev_)
     if (e) cudaEventDestroy(e);
   for (auto& e : mev_)
     if (e) cudaEventDestroy(e);
@@ -332,9 +335,11 @@ void Context::upload_structure() {
     const host::Csr Dt = host::transpose(D_);
     op_.Dt = upload_csr(mem_, Dt, s);
     if (!std::getenv("GNW_SADDLE_CSR")) {  // experiment switch: the CSR loops of round 1
-      op_.Qs = upload_sell(mem_, Q_, s);
-      op_.Ds = upload_sell(mem_, D_, s);
-      op_.Dts = upload_sell(mem_, Dt, s);
+      const char* ee = std::getenv("GNW_SADDLE_ENCODE");  // 0: plain double values (A/B experiments)
+      const int enc = (ee && std::atoi(ee) == 0) ? 0 : 1;
+      op_.Qs = upload_sell(mem_, Q_, s, 2 * enc);
+      op_.Ds = upload_sell(mem_, D_, s, enc);
+      op_.Dts = upload_sell(mem_, Dt, s, enc);
     }
   }
   op_.K = K_;
@@ -382,6 +387,7 @@ void Context::alloc_vectors(long long n_alloc, long long K, long long N) {
   plan_ = plan_h_ = row_gemv_plan(N, 1);  // re-planned for the row count by set_jacobian
   n_comb_blocks_ = combine_blocks(K, N);
   cpart_ = mem_.alloc<double>(3 * (static_cast<size_t>(n_comb_blocks_) + 16));  // one triple per combine block
+  ctot_ = mem_.alloc<double>(4);  // their sum (k_sum_triples)
 }
 
 void Context::upload_hierarchy() {
@@ -765,9 +771,23 @@ void Context::precondition_into(VSel y, VSel yv2, VSel z, MinresState* st, int l
   auto reduce_t = [&]() {
     if (comm_) reduce_m(t_part_, t_, pa.m, stream_);
   };
+  // single GPU: the combine kernel's dot partials are pre-summed on a side branch beside the
+  // dense sweeps (k_sum_triples), so the finish kernel adds one triple
+  static const bool tri_branch = [] {  // env GNW_TRI_BRANCH=0: the finish kernel sums the partials
+    const char* e = std::getenv("GNW_TRI_BRANCH");
+    return !(e && std::atoi(e) == 0);
+  }();
+  const bool pre = tri_branch && fork_ && !comm_ && !(exp_skip_ & 4);
+  if (pre) {
+    GNW_CUDA_CHECK(cudaEventRecord(tri_ev_[0], stream_));
+    GNW_CUDA_CHECK(cudaStreamWaitEvent(side_, tri_ev_[0], 0));
+    sum_triples(cpart_, n_comb_blocks_, ctot_, side_);
+    GNW_CUDA_CHECK(cudaEventRecord(tri_ev_[1], side_));
+  }
   auto finish = [&](const PrecArgs& pf) {
-    finish_precondition(pf, svc_, t2_, y, z, comm_ ? 0 : loop, st, cpart_, n_comb_blocks_, fpart_, counters_ + 3,
-                        stream_);
+    if (pre) GNW_CUDA_CHECK(cudaStreamWaitEvent(stream_, tri_ev_[1], 0));
+    finish_precondition(pf, svc_, t2_, y, z, comm_ ? 0 : loop, st, pre ? ctot_ : cpart_, pre ? 1 : n_comb_blocks_,
+                        fpart_, counters_ + 3, stream_);
     if (comm_) {
       reduce_scratch(st, 0, 3);
       if (loop) givens_from_scratch(st, stream_);

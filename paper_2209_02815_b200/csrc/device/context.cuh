@@ -228,6 +228,8 @@ class Context {
   cudaEvent_t jev_[4] = {};    // set_jacobian phase timers
   cudaEvent_t mev_[2] = {};    // minres timers
   cudaEvent_t rhs_ev_[2] = {};  // assemble_rhs timers
+  cudaEvent_t tri_ev_[2] = {};  // fork / join of the dot-partials branch (k_sum_triples)
+  double* ctot_ = nullptr;      // the combine kernel's dots, pre-summed
   int64_t jm_m_ = -1;          // shape of the persistent Jacobian buffers
   bool jm_owned_ = false;
   double* jown_ = nullptr;     // owned copy of J (host-pointer mode)

@@ -76,9 +76,9 @@ void Context::setup_rowpart() {
   op_.Q = upload_csr(mem_, sp.Q, s);
   op_.D = upload_csr(mem_, sp.D, s);
   op_.Dt = upload_csr(mem_, sp.Dt, s);
-  op_.Qs = upload_sell(mem_, sp.Q, s);
-  op_.Ds = upload_sell(mem_, sp.D, s);
-  op_.Dts = upload_sell(mem_, sp.Dt, s);
+  op_.Qs = upload_sell(mem_, sp.Q, s, 2);
+  op_.Ds = upload_sell(mem_, sp.D, s, 1);
+  op_.Dts = upload_sell(mem_, sp.Dt, s, 1);
   op_.K = Kl_;
   op_.N = Nl_;
   // local -> global maps: the saddle layout (own + ghosts) and the cell vector of the rhs

@@ -732,7 +732,26 @@ static int g_rg_wide_m = [] {  // env GNW_RG_WIDE_M: m from which the 8-rows-per
   return e ? std::atoi(e) : 1024;
 }();
 static inline bool rg_wide(int m) { return m >= g_rg_wide_m; }
-#define K_ROW_GEMV_NARROW k_row_gemv<4, 4, 4>
+// narrow variant (m < 1024): env GNW_RG_VARIANT picks <R, U, min CTAs/SM> for experiments
+using RgKernel = void (*)(const double*, int, long long, long long, VSel, long long, int, const MinresState*, double*,
+                          unsigned*, double*, int);
+struct RgVariant {
+  RgKernel k;
+  int rows_per_warp;
+};
+static RgVariant rg_narrow() {
+  static const int v = [] {
+    const char* e = std::getenv("GNW_RG_VARIANT");
+    return e ? std::atoi(e) : 0;
+  }();
+  switch (v) {
+    case 1: return {k_row_gemv<4, 2, 6>, 4};
+    case 2: return {k_row_gemv<2, 4, 6>, 2};
+    case 3: return {k_row_gemv<4, 8, 3>, 4};
+    default: return {k_row_gemv<4, 4, 4>, 4};
+  }
+}
+#define K_ROW_GEMV_NARROW (rg_narrow().k)
 #define K_ROW_GEMV_WIDE k_row_gemv<8, 2, 3>
 
 RowGemv row_gemv_plan(long long N, int m, int reserve) {
@@ -746,7 +765,7 @@ RowGemv row_gemv_plan(long long N, int m, int reserve) {
     cudaGetLastError();
   }
   const bool wide = rg_wide(m);
-  const int rows_cta = (wide ? 8 : 4) * (kTpb / 32);
+  const int rows_cta = (wide ? 8 : rg_narrow().rows_per_warp) * (kTpb / 32);
   // reserve: CTA slots per SM left free for a concurrent graph branch (the V-cycle)
   const int slots = sms * std::max(1, (wide ? occw : occ) - reserve);
   RowGemv p;
@@ -763,7 +782,7 @@ void row_gemv(const double* A, int m, long long N, long long ld, VSel x, long lo
               const MinresState* st, double* partial, unsigned* counter, double* out, const RowGemv& plan,
               cudaStream_t s) {
   const bool wide = rg_wide(m);
-  const int rows_cta = (wide ? 8 : 4) * (kTpb / 32);
+  const int rows_cta = (wide ? 8 : rg_narrow().rows_per_warp) * (kTpb / 32);
   const dim3 grid(plan.nchunks, (m + rows_cta - 1) / rows_cta);
   GNW_LAUNCH(launch_k(wide ? K_ROW_GEMV_WIDE : K_ROW_GEMV_NARROW, grid, kTpb, 0, s, A, m, N, ld, x, x_off, scaled, st,
                       partial, counter, out, plan.chunk));
@@ -941,6 +960,27 @@ __global__ void __launch_bounds__(kTpb) k_combine_elem(PrecArgs pa, VSel azs, VS
 
 int combine_blocks(long long K, long long N) { return static_cast<int>(grid_for((K + N + 1) / 2)); }
 
+// the combine kernel's per-block dot partials (n triples) summed in a fixed order by one CTA:
+// run on a side graph branch beside the dense sweeps, so the finish kernel's last block adds
+// one triple instead of thousands (its serial L2 round trips were on the critical path)
+__global__ void __launch_bounds__(1024) k_sum_triples(const double* __restrict__ parts, int n, double* __restrict__ out) {
+  griddep_wait();
+  __shared__ double red[3 * 32];
+  double a[3] = {0.0, 0.0, 0.0};
+  for (int b = threadIdx.x; b < n; b += blockDim.x)
+#pragma unroll
+    for (int k = 0; k < 3; ++k) a[k] += __ldcg(&parts[b * 3 + k]);
+  block_reduce<3>(a, red);
+  if (threadIdx.x == 0)
+#pragma unroll
+    for (int k = 0; k < 3; ++k) out[k] = a[k];
+}
+
+void sum_triples(const double* parts, int n, double* out, cudaStream_t s) {
+  GNW_LAUNCH(launch_k(k_sum_triples, 1, 1024, 0, s, parts, n, out));
+  check_launch("sum_triples");
+}
+
 void combine_elem(const PrecArgs& pa, VSel az, VSel vcur, VSel vprev, VSel vnext, VSel znext, int loop,
                   MinresState* st, double* dots_part, cudaStream_t s) {
   GNW_LAUNCH(launch_k(k_combine_elem, combine_blocks(pa.K, pa.N), kTpb, 0, s, pa, az, vcur, vprev, vnext, znext, loop, st, dots_part));
@@ -1072,6 +1112,14 @@ __global__ void __launch_bounds__(1024) k_cap_tri_solve(const double* __restrict
   for (int i = threadIdx.x; i < m; i += blockDim.x) t2[i] = xs[i];
 }
 
+static bool cap_cluster_on() {  // env GNW_CAP_CLUSTER=0: the three launches (A/B experiments)
+  static const bool on = [] {
+    const char* e = std::getenv("GNW_CAP_CLUSTER");
+    return !(e && std::atoi(e) == 0);
+  }();
+  return on;
+}
+
 void capacitance_solve(const PrecArgs& pa, const double* t, double* t2, cudaStream_t s) {
   if (pa.m == 0) return;
   if (pa.cap_tri && !pa.exact) {
@@ -1081,7 +1129,7 @@ void capacitance_solve(const PrecArgs& pa, const double* t, double* t2, cudaStre
   }
   if (pa.exact) {
     GNW_LAUNCH(launch_k(k_coarse_cholesky, 1, 64, 0, s, pa.Lc, pa.m, vfixed(const_cast<double*>(t)), t2, nullptr, 1, 1));
-  } else if (pa.m <= kCapClusterMaxM) {  // one cluster launch instead of three (small m: latency)
+  } else if (pa.m <= kCapClusterMaxM && cap_cluster_on()) {  // one cluster launch instead of three (small m)
     const int refine = (pa.Cfull && pa.cres) ? 1 : 0;
     const int ncl = std::min(8, std::max(1, (pa.m + 31) / 32));
     const size_t smem = 3 * static_cast<size_t>(pa.m) * sizeof(double);

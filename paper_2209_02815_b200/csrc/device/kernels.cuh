@@ -109,6 +109,8 @@ struct RowGemv {
 RowGemv row_gemv_plan(long long N, int m, int reserve = 0);
 // number of blocks of the elementwise combine kernel (dots partials)
 int combine_blocks(long long K, long long N);
+// out[0..2] = the n triples of parts summed in a fixed order (one CTA)
+void sum_triples(const double* parts, int n, double* out, cudaStream_t s);
 void row_gemv(const double* A, int m, long long N, long long ld, VSel x, long long x_off, int scaled,
               const MinresState* st, double* partial, unsigned* counter, double* out,
               const RowGemv& plan, cudaStream_t s);
