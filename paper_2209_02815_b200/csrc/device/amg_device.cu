@@ -105,6 +105,14 @@ DSell upload_sell(DeviceMemory& mem, const host::Csr& A, cudaStream_t s, int enc
   return d;
 }
 
+int DeviceAmg::collapse_max() {
+  static const int v = [] {
+    const char* e = std::getenv("GNW_VC_COLLAPSE_MAX");
+    return e ? std::atoi(e) : 2048;
+  }();
+  return v;
+}
+
 void DeviceAmg::reset() {
   bmem_.reset();
   bmem_b_ = 0;
@@ -125,7 +133,7 @@ void DeviceAmg::upload(const host::AmgHierarchy& h, cudaStream_t s, int min_coll
   const bool fused_on = !(fe && std::atoi(fe) == 0);
   int stop = static_cast<int>(L) - 1;
   for (int l = min_collapse_; l + 1 < static_cast<int>(L); ++l)
-    if (h.levels[l].A.n_rows <= kCollapseMax) {
+    if (h.levels[l].A.n_rows <= collapse_max()) {
       stop = l;
       break;
     }
@@ -203,7 +211,7 @@ void DeviceAmg::build_collapse(cudaStream_t s) {
   const int L = static_cast<int>(lv_.size());
   int lc = -1;
   for (int l = min_collapse_; l < L - 1; ++l)
-    if (lv_[l].n <= kCollapseMax) {
+    if (lv_[l].n <= collapse_max()) {
       lc = l;
       break;
     }

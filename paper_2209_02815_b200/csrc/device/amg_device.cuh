@@ -72,7 +72,9 @@ class DeviceAmg {
 
   int collapse_level() const { return collapse_l_; }
   bool fused() const { return fused_; }
-  static constexpr int kCollapseMax = 2048;  // dense collapsed tail from the first level this small
+  // the dense collapsed tail starts at the first level with at most this many rows (env
+  // GNW_VC_COLLAPSE_MAX); the dense map is L2-resident up to ~3000 rows (72 MB)
+  static int collapse_max();
 
  private:
   DLevel level(int l, int exact) const;

@@ -18,8 +18,6 @@ namespace gnw {
 constexpr int kWarp = 32;
 // largest m whose m-vector is staged in shared memory by the dense sweeps (gnw_set_jacobian cap)
 constexpr int kMaxStageM = 8192;
-// m up to which C^-1 t runs as one thread-block-cluster launch (kernels.cu k_cap_solve_cluster)
-constexpr int kCapClusterMaxM = 512;
 
 // Programmatic dependent launch: every kernel starts with griddep_wait(), so a
 // launch may be issued (and its CTAs made resident) while its predecessor on the

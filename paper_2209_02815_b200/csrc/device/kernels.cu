@@ -18,7 +18,6 @@
 #include <cmath>
 #include <cstdlib>
 #include <stdexcept>
-#include <cooperative_groups.h>
 #include <mutex>
 #include <set>
 #include <string>
@@ -732,26 +731,7 @@ static int g_rg_wide_m = [] {  // env GNW_RG_WIDE_M: m from which the 8-rows-per
   return e ? std::atoi(e) : 1024;
 }();
 static inline bool rg_wide(int m) { return m >= g_rg_wide_m; }
-// narrow variant (m < 1024): env GNW_RG_VARIANT picks <R, U, min CTAs/SM> for experiments
-using RgKernel = void (*)(const double*, int, long long, long long, VSel, long long, int, const MinresState*, double*,
-                          unsigned*, double*, int);
-struct RgVariant {
-  RgKernel k;
-  int rows_per_warp;
-};
-static RgVariant rg_narrow() {
-  static const int v = [] {
-    const char* e = std::getenv("GNW_RG_VARIANT");
-    return e ? std::atoi(e) : 0;
-  }();
-  switch (v) {
-    case 1: return {k_row_gemv<4, 2, 6>, 4};
-    case 2: return {k_row_gemv<2, 4, 6>, 2};
-    case 3: return {k_row_gemv<4, 8, 3>, 4};
-    default: return {k_row_gemv<4, 4, 4>, 4};
-  }
-}
-#define K_ROW_GEMV_NARROW (rg_narrow().k)
+#define K_ROW_GEMV_NARROW k_row_gemv<4, 4, 4>
 #define K_ROW_GEMV_WIDE k_row_gemv<8, 2, 3>
 
 RowGemv row_gemv_plan(long long N, int m, int reserve) {
@@ -765,7 +745,7 @@ RowGemv row_gemv_plan(long long N, int m, int reserve) {
     cudaGetLastError();
   }
   const bool wide = rg_wide(m);
-  const int rows_cta = (wide ? 8 : rg_narrow().rows_per_warp) * (kTpb / 32);
+  const int rows_cta = (wide ? 8 : 4) * (kTpb / 32);
   // reserve: CTA slots per SM left free for a concurrent graph branch (the V-cycle)
   const int slots = sms * std::max(1, (wide ? occw : occ) - reserve);
   RowGemv p;
@@ -782,7 +762,7 @@ void row_gemv(const double* A, int m, long long N, long long ld, VSel x, long lo
               const MinresState* st, double* partial, unsigned* counter, double* out, const RowGemv& plan,
               cudaStream_t s) {
   const bool wide = rg_wide(m);
-  const int rows_cta = (wide ? 8 : rg_narrow().rows_per_warp) * (kTpb / 32);
+  const int rows_cta = (wide ? 8 : 4) * (kTpb / 32);
   const dim3 grid(plan.nchunks, (m + rows_cta - 1) / rows_cta);
   GNW_LAUNCH(launch_k(wide ? K_ROW_GEMV_WIDE : K_ROW_GEMV_NARROW, grid, kTpb, 0, s, A, m, N, ld, x, x_off, scaled, st,
                       partial, counter, out, plan.chunk));
@@ -1031,61 +1011,6 @@ __global__ void k_cinv_refine(const double* __restrict__ Cinv, const double* __r
   if (lane == 0) t2[w] = t2[w] + acc[0];
 }
 
-// t2 = C^-1 t (+ one refinement step) as ONE launch of a thread-block cluster: each CTA owns a
-// slice of the rows; the m-vectors live in shared memory and every CTA gathers the others'
-// slices through distributed shared memory between the phases.  The rows are summed exactly
-// as k_cinv_apply / k_cap_residual / k_cinv_refine sum them (warp per row, lane-strided, xor
-// tree), so the result is bit-identical to the three launches it replaces -- for small m
-// (C1 m = 32, C2 m = 256) those launches are pure latency on the MINRES critical path.
-__global__ void __launch_bounds__(1024) k_cap_solve_cluster(const double* __restrict__ Cinv, const double* __restrict__ C,
-                                                            const double* __restrict__ t, double* __restrict__ t2,
-                                                            int m, int refine) {
-  griddep_wait();
-  namespace cg = cooperative_groups;
-  cg::cluster_group cl = cg::this_cluster();
-  extern __shared__ double sm[];
-  double* ts = sm;           // t
-  double* xs = sm + m;       // t2
-  double* rs = sm + 2 * m;   // t - C t2
-  const int ncl = static_cast<int>(cl.num_blocks()), me = static_cast<int>(cl.block_rank());
-  const int per = (m + ncl - 1) / ncl, r0 = me * per, r1 = min(m, r0 + per);
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  for (int i = threadIdx.x; i < m; i += blockDim.x) ts[i] = t[i];
-  __syncthreads();
-  auto rowdot = [&](const double* __restrict__ A, const double* x, int w) {
-    double acc[1] = {0.0};
-    for (int j = lane; j < m; j += 32) acc[0] = acc[0] + __ldg(&A[static_cast<long long>(w) * m + j]) * x[j];
-    warp_reduce<1>(acc);
-    return acc[0];
-  };
-  auto gather = [&](double* v) {  // the other CTAs' slices of v into this CTA's copy
-    cl.sync();
-    for (int i = threadIdx.x; i < m; i += blockDim.x) {
-      const int owner = i / per;
-      if (owner != me) v[i] = cl.map_shared_rank(v, owner)[i];
-    }
-    cl.sync();
-  };
-  for (int w = r0 + warp; w < r1; w += nw) {
-    const double a = rowdot(Cinv, ts, w);
-    if (lane == 0) xs[w] = a;
-  }
-  if (refine) {
-    gather(xs);
-    for (int w = r0 + warp; w < r1; w += nw) {
-      const double a = rowdot(C, xs, w);
-      if (lane == 0) rs[w] = ts[w] - a;
-    }
-    gather(rs);
-    for (int w = r0 + warp; w < r1; w += nw) {
-      const double a = rowdot(Cinv, rs, w);
-      if (lane == 0) xs[w] = xs[w] + a;
-    }
-  }
-  __syncthreads();
-  for (int i = r0 + static_cast<int>(threadIdx.x); i < r1; i += blockDim.x) t2[i] = xs[i];
-}
-
 // t2 = L^-T L^-1 t in one CTA (x in shared memory, L read from L2): right-looking forward and
 // backward substitution, each step's updates spread over the threads.  The fallback for an
 // ill-conditioned capacitance matrix (PrecArgs::cap_tri); O(m) barriers, ~0.1 ms at m ~ 1000.
@@ -1112,14 +1037,6 @@ __global__ void __launch_bounds__(1024) k_cap_tri_solve(const double* __restrict
   for (int i = threadIdx.x; i < m; i += blockDim.x) t2[i] = xs[i];
 }
 
-static bool cap_cluster_on() {  // env GNW_CAP_CLUSTER=0: the three launches (A/B experiments)
-  static const bool on = [] {
-    const char* e = std::getenv("GNW_CAP_CLUSTER");
-    return !(e && std::atoi(e) == 0);
-  }();
-  return on;
-}
-
 void capacitance_solve(const PrecArgs& pa, const double* t, double* t2, cudaStream_t s) {
   if (pa.m == 0) return;
   if (pa.cap_tri && !pa.exact) {
@@ -1129,27 +1046,6 @@ void capacitance_solve(const PrecArgs& pa, const double* t, double* t2, cudaStre
   }
   if (pa.exact) {
     GNW_LAUNCH(launch_k(k_coarse_cholesky, 1, 64, 0, s, pa.Lc, pa.m, vfixed(const_cast<double*>(t)), t2, nullptr, 1, 1));
-  } else if (pa.m <= kCapClusterMaxM && cap_cluster_on()) {  // one cluster launch instead of three (small m)
-    const int refine = (pa.Cfull && pa.cres) ? 1 : 0;
-    const int ncl = std::min(8, std::max(1, (pa.m + 31) / 32));
-    const size_t smem = 3 * static_cast<size_t>(pa.m) * sizeof(double);
-    smem_optin(reinterpret_cast<const void*>(k_cap_solve_cluster), 3 * kCapClusterMaxM * 8);
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(ncl);
-    cfg.blockDim = dim3(1024);
-    cfg.dynamicSmemBytes = smem;
-    cfg.stream = s;
-    cudaLaunchAttribute attr[2];
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = ncl;
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = 1;
-    attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr[1].val.programmaticStreamSerializationAllowed = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = g_pdl ? 2 : 1;
-    GNW_LAUNCH(cudaLaunchKernelEx(&cfg, k_cap_solve_cluster, pa.Cinv, static_cast<const double*>(pa.Cfull), t, t2,
-                                  pa.m, refine));
   } else {
     const unsigned g = grid_for(static_cast<long long>(pa.m) * 32);
     GNW_LAUNCH(launch_k(k_cinv_apply, g, kTpb, 0, s, pa.Cinv, t, t2, pa.m));

@@ -161,7 +161,7 @@ void PartAmg::build(const host::AmgHierarchy& h, const std::vector<int32_t>& cel
   const char* ce = std::getenv("GNW_VC_COLLAPSE");
   if (!(ce && std::atoi(ce) == 0))
     for (int l = 1; l + 1 < L; ++l)
-      if (h.levels[l].A.n_rows <= DeviceAmg::kCollapseMax) {
+      if (h.levels[l].A.n_rows <= DeviceAmg::collapse_max()) {
         gc = l;
         break;
       }
