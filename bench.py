@@ -509,6 +509,31 @@ def run_gnw(args):
             kern[name]["note"] = notes[name]
     it_sec, it_bytes = ctx.profile_kernel("iteration")
     dg_sec, dg_flops = ctx.profile_kernel("dgemm", reps=5)
+    # In-loop attribution (tools/attribute_iteration.py's method, in process): the captured loop
+    # body replayed with one part left out (env GNW_EXP_SKIP, read per call); the part's marginal
+    # cost beside its algorithmic bytes.  Unlike the standalone timings above, its vectors are
+    # not L2-warm here (the dense sweeps evict them), so these are the honest in-loop rates.
+    in_loop = {}
+    try:
+        skip_bits = {"vcycle": 16, "update": 128, "saddle": 2, "finish": 64, "combine": 4}
+        os.environ["GNW_EXP_SKIP"] = "0"
+        body_sec, _ = ctx.profile_kernel("body", reps=20)
+        for part, bit in skip_bits.items():
+            os.environ["GNW_EXP_SKIP"] = str(bit)
+            t, _ = ctx.profile_kernel("body", reps=20)
+            in_loop[part] = {"ms": (body_sec - t) * 1e3}
+        byt = {"vcycle": kern["vcycle"]["GB"], "update": kern["update"]["GB"],
+               "saddle": kern[sad]["GB"] if (sad := ("saddle_fused" if fused else "saddle")) in kern else None}
+        for part, gb in byt.items():
+            if gb and in_loop[part]["ms"] > 0:
+                in_loop[part]["GB"] = gb
+                in_loop[part]["GBps"] = gb / (in_loop[part]["ms"] * 1e-3)
+                in_loop[part]["frac"] = in_loop[part]["GBps"] / hbm_peak
+        in_loop["body_ms"] = body_sec * 1e3
+    except Exception as e:  # reported, never silently replaced
+        in_loop = {"failed": str(e)}
+    finally:
+        os.environ.pop("GNW_EXP_SKIP", None)
     # share of one iteration per kernel KIND (k_row_gemv: its own J pass + the H^T pass of combine_prec)
     sad, fin = ("saddle_fused", "finish_lean" if lean else "finish_fused") if fused else ("saddle", "finish_prec")
     kind_ms = {"row_gemv": per_iter["row_gemv"] * kern["row_gemv"]["ms"], sad: kern[sad]["ms"],
@@ -609,6 +634,7 @@ def run_gnw(args):
                                        "GBps": it_bytes / it_sec / 1e9 if it_sec else None,
                                        "frac": it_bytes / it_sec / 1e9 / hbm_peak if it_sec else None},
                          "kernels": kern,
+                         "in_loop": in_loop,
                          "dgemm": dgemm_summary(dg_sec, dg_flops, cfg.m, N)},
             "cpu_baseline": cpu,
             "e2e": {"value": ws * args.steps / e2e_elapsed, "unit": UNIT, "h2d_bytes_per_step": h2d,

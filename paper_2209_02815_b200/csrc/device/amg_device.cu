@@ -108,7 +108,7 @@ DSell upload_sell(DeviceMemory& mem, const host::Csr& A, cudaStream_t s, int enc
 int DeviceAmg::collapse_max() {
   static const int v = [] {
     const char* e = std::getenv("GNW_VC_COLLAPSE_MAX");
-    return e ? std::atoi(e) : 2048;
+    return e ? std::atoi(e) : 3072;  // C1: level 1 (2058 rows, 34 MB) -> 0.051 -> 0.047 ms per iteration
   }();
   return v;
 }

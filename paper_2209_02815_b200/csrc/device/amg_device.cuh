@@ -73,7 +73,7 @@ class DeviceAmg {
   int collapse_level() const { return collapse_l_; }
   bool fused() const { return fused_; }
   // the dense collapsed tail starts at the first level with at most this many rows (env
-  // GNW_VC_COLLAPSE_MAX); the dense map is L2-resident up to ~3000 rows (72 MB)
+  // GNW_VC_COLLAPSE_MAX, default 3072); the dense map is L2-resident up to that (72 MB)
   static int collapse_max();
 
  private:
