@@ -777,7 +777,7 @@ void Context::precondition_into(VSel y, VSel yv2, VSel z, MinresState* st, int l
     const char* e = std::getenv("GNW_TRI_BRANCH");
     return !(e && std::atoi(e) == 0);
   }();
-  const bool pre = tri_branch && fork_ && !comm_ && !(exp_skip_ & 4);
+  const bool pre = tri_branch && fork_ && !comm_ && !(exp_skip_ & (4 | 64));  // the finish kernel joins the branch
   if (pre) {
     GNW_CUDA_CHECK(cudaEventRecord(tri_ev_[0], stream_));
     GNW_CUDA_CHECK(cudaStreamWaitEvent(side_, tri_ev_[0], 0));
@@ -1308,6 +1308,15 @@ void Context::profile_kernel(int kernel, int reps, double* seconds, double* algo
       GNW_CUDA_CHECK(cudaGraphInstantiate(&ge, g, 0));
     } catch (...) {
       exp_skip_ = 0;
+      // leave neither stream capturing and no sticky error behind for the next launch
+      cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+      if (cudaStreamIsCapturing(s, &cs) == cudaSuccess && cs != cudaStreamCaptureStatusNone) {
+        cudaGraph_t dead = nullptr;
+        cudaStreamEndCapture(s, &dead);
+        if (dead) cudaGraphDestroy(dead);
+      }
+      if (g) cudaGraphDestroy(g);
+      cudaGetLastError();
       throw;
     }
     exp_skip_ = 0;

@@ -91,7 +91,14 @@ def check_solves(ctx, b, ref, modes, label, noisy_stop=False):
     d8 = refdata.fingerprint_rel(x8, r8)    # against the reference's own tol-1e-8 solution
     d8c = refdata.fingerprint_rel(x8, r12)  # against the converged solution (the solve error)
     # same iteration count: the two tol-1e-8 iterates are the same Krylov iterate up to rounding
-    assert d8["max"] <= (SOLUTION_TOL if rep8.iterations == r8["iterations"] else LOOSE_TOL), (label, d8)
+    loose = LOOSE_TOL
+    if noisy_stop:
+        # inside the crossing window the iterates still move at the scale of the solve error itself:
+        # the reference's own tol-1e-8 iterate is e_ref from its converged solution (C3 mesh: 8e-6,
+        # window 201..235), so two stops in the window may differ by a few e_ref
+        e_ref = float(np.linalg.norm(np.asarray(r8["sub"]) - np.asarray(r12["sub"])) / np.linalg.norm(r12["sub"]))
+        loose = max(LOOSE_TOL, 4.0 * e_ref)
+    assert d8["max"] <= (SOLUTION_TOL if rep8.iterations == r8["iterations"] else loose), (label, d8, loose)
     assert d8c["max"] <= 1e-4, (label, d8c)  # a tol-1e-8 solve's own error (C2 alpha=1e-4: ~2e-6)
     out["auto@1e-8"] = (rep8.iterations, d8["max"], ctx.loop_schedule())
     print(label, out)
