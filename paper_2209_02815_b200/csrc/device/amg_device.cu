@@ -105,6 +105,56 @@ DSell upload_sell(DeviceMemory& mem, const host::Csr& A, cudaStream_t s, int enc
   return d;
 }
 
+DLell upload_lell(DeviceMemory& mem, const host::Csr& A, int G, cudaStream_t s) {
+  DLell d;
+  int64_t longest = 0;
+  for (int64_t r = 0; r < A.n_rows; ++r) longest = std::max(longest, A.rowptr[r + 1] - A.rowptr[r]);
+  if (A.n_rows == 0 || longest == 0 || G < 1 || G > 32) return d;
+  const int64_t W = (longest + G - 1) / G, rpw = 32 / G;
+  const int64_t slices = ((A.n_rows + rpw - 1) / rpw + 7) / 8 * 8;  // every warp of the grid's CTAs
+  const int64_t len = slices * W * 32;
+  // a level whose padding would more than triple the entries keeps its CSR kernels
+  if (len > 3 * A.nnz() + 8192 || len > 0x7fffffffLL) return d;
+  std::unordered_map<uint64_t, unsigned> code_of;  // value bits -> code
+  std::vector<double> table;
+  int col_bits = 1;
+  while ((int64_t{1} << col_bits) < A.n_cols) ++col_bits;
+  const size_t max_codes = col_bits >= 31 ? 0 : size_t{1} << (31 - col_bits);
+  for (double v : A.vals) {
+    uint64_t b;
+    std::memcpy(&b, &v, sizeof b);
+    if (code_of.count(b)) continue;
+    if (table.size() >= max_codes) return d;  // too many distinct values for a 32-bit entry
+    code_of[b] = static_cast<unsigned>(table.size());
+    table.push_back(v);
+  }
+  std::vector<unsigned> words(static_cast<size_t>(len), 0xffffffffu);
+  for (int64_t r = 0; r < A.n_rows; ++r) {
+    const int64_t base = (r / rpw) * W * 32 + (r % rpw) * G;
+    for (int64_t k = A.rowptr[r]; k < A.rowptr[r + 1]; ++k) {
+      const int64_t e = k - A.rowptr[r];
+      const double v = A.vals[static_cast<size_t>(k)];
+      uint64_t b;
+      std::memcpy(&b, &v, sizeof b);
+      words[static_cast<size_t>(base + (e / G) * 32 + e % G)] =
+          (code_of.at(b) << col_bits) | static_cast<unsigned>(A.cols[static_cast<size_t>(k)]);
+    }
+  }
+  unsigned* dw = mem.alloc<unsigned>(words.size());
+  double* dt = mem.alloc<double>(table.size());
+  GNW_CUDA_CHECK(cudaMemcpyAsync(dw, words.data(), words.size() * sizeof(unsigned), cudaMemcpyHostToDevice, s));
+  GNW_CUDA_CHECK(cudaMemcpyAsync(dt, table.data(), table.size() * sizeof(double), cudaMemcpyHostToDevice, s));
+  GNW_CUDA_CHECK(cudaStreamSynchronize(s));  // host vectors are temporaries
+  d.n_rows = static_cast<int>(A.n_rows);
+  d.width = static_cast<int>(W);
+  d.lanes = G;
+  d.shift = col_bits;
+  d.mask = (1u << col_bits) - 1u;
+  d.words = dw;
+  d.table = dt;
+  return d;
+}
+
 int DeviceAmg::collapse_max() {
   static const int v = [] {
     const char* e = std::getenv("GNW_VC_COLLAPSE_MAX");
@@ -175,6 +225,12 @@ void DeviceAmg::upload(const host::AmgHierarchy& h, cudaStream_t s, int min_coll
         d.gS = vc_group_lanes(f.S.nnz() + f.T.nnz(), f.S.n_rows);
         d.gTt = vc_group_lanes(f.Tt.nnz(), f.Tt.n_rows);
         d.fused = 1;
+        const char* le = std::getenv("GNW_VC_LELL");  // experiment switch: 0 keeps the CSR loops
+        if (!(le && std::atoi(le) == 0)) {
+          d.Sl = upload_lell(mem_, f.S, d.gS, s);
+          d.Tl = upload_lell(mem_, f.T, d.gS, s);
+          d.Ttl = upload_lell(mem_, f.Tt, d.gTt, s);
+        }
       }
       vres_[l] = mem_.alloc<double>(d.n);
       vx_[l] = mem_.alloc<double>(d.n);

@@ -45,6 +45,9 @@ DCsr upload_csr(DeviceMemory& mem, const host::Csr& A, cudaStream_t s);
 // encode: 0 values as doubles; 1 signs in the columns (all values +-1, else falls back to 2);
 // 2 one-byte value codes (at most 256 distinct values, else falls back to 0)
 DSell upload_sell(DeviceMemory& mem, const host::Csr& A, cudaStream_t s, int encode = 0);
+// lane-ELL copy for G lanes per row with coded values (common.cuh DLell); words == nullptr when
+// the padding would be excessive or an entry does not fit 32 bits
+DLell upload_lell(DeviceMemory& mem, const host::Csr& A, int G, cudaStream_t s);
 // sparse_matmul on the device, bit-identical to host::spgemm (spgemm.cu)
 host::Csr device_spgemm(const host::Csr& A, const host::Csr& B, cudaStream_t s);
 

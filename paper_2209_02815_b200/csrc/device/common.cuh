@@ -145,6 +145,25 @@ struct DSell {
   int signed_cols = 0;
 };
 
+// Lane-ELL copy of a CSR matrix for the G-lanes-per-row kernels of the loop's V-cycle
+// (vcycle_fused.cu).  A warp holds 32 / G rows; lane (row % (32 / G)) * G + j sums entries
+// j, j + G, ... of its row, exactly like the CSR kernels, so entry e of row r sits at
+//   ((r / (32 / G)) * width + e / G) * 32 + (r % (32 / G)) * G + e % G
+// with `width` entries per lane (the longest row, rounded up).  The k-th load of a warp is one
+// contiguous 128-byte segment and no rowptr is read first.  Padding (0xffffffff) comes last in
+// its lane, so every lane adds the CSR terms in the CSR order: bit-identical sums.
+// Each entry is ONE 32-bit word: the level operators of a structured mesh hold few distinct
+// doubles (C2: 11 in S_0, 79 in T_0, 4172 in T_3), so the value is a code into `table` (the
+// decoded double is the same bits) packed above the column: word = code << shift | col.
+// Built only when column bits + code bits <= 31; otherwise the level keeps its CSR kernels.
+// Slices are allocated for every warp of the launch grid (multiples of 8 warps).
+struct DLell {
+  int n_rows = 0, width = 0, lanes = 0, shift = 0;
+  unsigned mask = 0;
+  const unsigned* words = nullptr;
+  const double* table = nullptr;
+};
+
 // sum_k vals[k] * (x[off + cols[k]] * sc)  (sc applied only when scaled), in CSR order
 template <int W>
 __device__ __forceinline__ void sell_load(const DSell& A, long long row, int (&c)[W], double (&v)[W]);

@@ -260,48 +260,37 @@ __global__ void k_coarse_inverse(const double* __restrict__ Ainv, int n, VSel rs
 }
 
 // Single right-hand side (the MINRES V-cycle's coarse / collapsed-tail apply, C2: n = 1147):
-// one warp per row with four independent accumulators, so each lane keeps four loads of the
-// row in flight instead of one dependent add chain of n / 32 L2 round trips (14 us at C2 with
-// one warp per SM).  Deterministic; not the reference order (the reference solves with the
-// Cholesky factor, k_coarse_cholesky, in exact mode).
-__global__ void k_coarse_inverse1(const double* __restrict__ Ainv, int n, VSel rs, double* __restrict__ x,
-                                  const MinresState* st) {
+// one 128-thread CTA per row.  Thread t owns columns t, t + 128, ...; the first 16 of its
+// matrix entries (all of them for n <= 2048) are loaded BEFORE the grid-dependency wait -- the
+// matrix is fixed per hierarchy, so under programmatic dependent launch these loads overlap the
+// predecessor's drain -- and the products are added in column order, then lanes (xor tree),
+// then the four warps in order.  One warp per row walked 72 dependent loads per lane in
+// batches (14.1, later 10.3 us at C2 for a 10.5 MB L2-resident matrix).  Deterministic; not
+// the reference order (the reference solves with the Cholesky factor, k_coarse_cholesky, in
+// exact mode).
+constexpr int kCoarseTpb = 128;
+__global__ void __launch_bounds__(kCoarseTpb) k_coarse_inverse1(const double* __restrict__ Ainv, int n, VSel rs,
+                                                                double* __restrict__ x, const MinresState* st) {
+  const int i = blockIdx.x, t = threadIdx.x;
+  const double* __restrict__ row = Ainv + static_cast<long long>(i) * n;
+  double mm[16];
+#pragma unroll
+  for (int u = 0; u < 16; ++u) mm[u] = t + kCoarseTpb * u < n ? ldg(&row[t + kCoarseTpb * u]) : 0.0;
   griddep_wait();
   const double* __restrict__ r = vsel(rs, st);
-  const long long i = (static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31;
-  if (i >= n) return;
-  const double* __restrict__ row = Ainv + i * n;
-  double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
-  int j = lane;
-  // four 128-column blocks at a time: 16 loads per lane in flight, the adds in the same order
-  for (; j + 96 + 384 < n; j += 512) {
-    double mm[16], rr[16];
+  double rr[16];
 #pragma unroll
-    for (int u = 0; u < 16; ++u) {
-      mm[u] = ldg(&row[j + 32 * u]);
-      rr[u] = r[j + 32 * u];
-    }
+  for (int u = 0; u < 16; ++u) rr[u] = t + kCoarseTpb * u < n ? r[t + kCoarseTpb * u] : 0.0;
+  double a = 0.0;
 #pragma unroll
-    for (int b = 0; b < 4; ++b) {
-      a0 = a0 + mm[4 * b] * rr[4 * b];
-      a1 = a1 + mm[4 * b + 1] * rr[4 * b + 1];
-      a2 = a2 + mm[4 * b + 2] * rr[4 * b + 2];
-      a3 = a3 + mm[4 * b + 3] * rr[4 * b + 3];
-    }
-  }
-  for (; j + 96 < n; j += 128) {
-    const double m0 = ldg(&row[j]), m1 = ldg(&row[j + 32]), m2 = ldg(&row[j + 64]), m3 = ldg(&row[j + 96]);
-    const double r0 = r[j], r1 = r[j + 32], r2 = r[j + 64], r3 = r[j + 96];
-    a0 = a0 + m0 * r0;
-    a1 = a1 + m1 * r1;
-    a2 = a2 + m2 * r2;
-    a3 = a3 + m3 * r3;
-  }
-  for (; j < n; j += 32) a0 = a0 + ldg(&row[j]) * r[j];
-  double acc[1] = {(a0 + a1) + (a2 + a3)};
+  for (int u = 0; u < 16; ++u) a = a + mm[u] * rr[u];
+  for (int j = t + 16 * kCoarseTpb; j < n; j += kCoarseTpb) a = a + ldg(&row[j]) * r[j];
+  double acc[1] = {a};
   warp_reduce<1>(acc);
-  if (lane == 0) x[i] = acc[0];
+  __shared__ double part[kCoarseTpb / 32];
+  if ((t & 31) == 0) part[t >> 5] = acc[0];
+  __syncthreads();
+  if (t == 0) x[i] = ((part[0] + part[1]) + part[2]) + part[3];
 }
 
 // cholesky_solve (linalg.cpp:107-123) replayed exactly, one thread per rhs column
@@ -439,7 +428,7 @@ void coarse_inverse(const double* Ainv, int n, VSel r, double* x, const MinresSt
                     cudaStream_t s) {
   const long long threads = static_cast<long long>(n) * nrhs * 32;
   if (nrhs == 1) {
-    GNW_LAUNCH(launch_k(k_coarse_inverse1, grid_for(threads, 128), 128, 0, s, Ainv, n, r, x, st));
+    GNW_LAUNCH(launch_k(k_coarse_inverse1, n, kCoarseTpb, 0, s, Ainv, n, r, x, st));
     return check_launch("coarse_inverse1");
   }
   GNW_LAUNCH(launch_k(k_coarse_inverse, grid_for(threads), kTpb, 0, s, Ainv, n, r, x, st, nrhs));

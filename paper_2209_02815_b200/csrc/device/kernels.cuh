@@ -24,6 +24,8 @@ struct DLevel {
   // r_c = Tt r, e = S r + T e_c; fused = 0: not built for this level
   DCsr S, T, Tt;
   int gS = 1, gTt = 1, fused = 0;
+  // lane-ELL copies with coded values read by the single-RHS kernels (words == nullptr: CSR)
+  DLell Sl, Tl, Ttl;
 };
 
 // one pass per level each way (vcycle_fused.cu): rc = Tt r; out = S r + T ec

@@ -63,6 +63,79 @@ __global__ void __launch_bounds__(kTpbF) k_vcf_up(DCsr S, DCsr T, VSel rs, const
   if (ok && sub == 0) out[i] = sa + sb;
 }
 
+
+// ---------------------------------------------- lane-ELL levels with coded values (DLell)
+// One batch of four lane entries: the four words are loaded together, then the table look-ups
+// and gathers are issued together, then the products are added in entry order (padding, which
+// has the sign bit set, is skipped).
+struct LellBatch {
+  unsigned w[4];
+  __device__ __forceinline__ void load(const unsigned* __restrict__ p, int k, int width) {
+#pragma unroll
+    for (int u = 0; u < 4; ++u) w[u] = k + u < width ? __ldg(p + 32 * (k + u)) : 0xffffffffu;
+  }
+  template <class F>
+  __device__ __forceinline__ double add(const DLell& A, double acc, F f) const {
+    double v[4], x[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const bool ok = static_cast<int>(w[u]) >= 0;
+      v[u] = ok ? __ldg(A.table + (w[u] >> A.shift)) : 0.0;
+      x[u] = ok ? f(static_cast<int>(w[u] & A.mask)) : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      if (static_cast<int>(w[u]) >= 0) acc = acc + v[u] * x[u];
+    return acc;
+  }
+};
+
+template <int G>
+__global__ void __launch_bounds__(kTpbF) k_vcl_restrict(DLell Tt, VSel rs, const MinresState* st,
+                                                        double* __restrict__ rc) {
+  const unsigned warp = blockIdx.x * (kTpbF / 32) + threadIdx.x / 32;
+  const unsigned* __restrict__ p = Tt.words + warp * static_cast<unsigned>(Tt.width * 32) + (threadIdx.x & 31);
+  LellBatch b0;
+  b0.load(p, 0, Tt.width);  // the matrix does not depend on the predecessor kernel
+  griddep_wait();
+  const double* __restrict__ r = vsel(rs, st);
+  double acc = b0.add(Tt, 0.0, [&](int c) { return r[c]; });
+  for (int k = 4; k < Tt.width; k += 4) {
+    LellBatch b;
+    b.load(p, k, Tt.width);
+    acc = b.add(Tt, acc, [&](int c) { return r[c]; });
+  }
+  const double s = gsum<G>(acc);
+  const int i = blockIdx.x * (kTpbF / G) + threadIdx.x / G;
+  if (i < Tt.n_rows && threadIdx.x % G == 0) rc[i] = s;
+}
+
+template <int G>
+__global__ void __launch_bounds__(kTpbF) k_vcl_up(DLell S, DLell T, VSel rs, const double* __restrict__ ec,
+                                                  double* __restrict__ out, const MinresState* st) {
+  const unsigned warp = blockIdx.x * (kTpbF / 32) + threadIdx.x / 32;
+  const unsigned* __restrict__ ps = S.words + warp * static_cast<unsigned>(S.width * 32) + (threadIdx.x & 31);
+  const unsigned* __restrict__ pt = T.words + warp * static_cast<unsigned>(T.width * 32) + (threadIdx.x & 31);
+  LellBatch s0, t0;
+  s0.load(ps, 0, S.width);
+  t0.load(pt, 0, T.width);
+  griddep_wait();
+  const double* __restrict__ r = vsel(rs, st);
+  double a = s0.add(S, 0.0, [&](int c) { return r[c]; });
+  double b = t0.add(T, 0.0, [&](int c) { return ec[c]; });
+  const int W = S.width > T.width ? S.width : T.width;
+  for (int k = 4; k < W; k += 4) {
+    LellBatch sb, tb;
+    sb.load(ps, k, S.width);
+    tb.load(pt, k, T.width);
+    a = sb.add(S, a, [&](int c) { return r[c]; });
+    b = tb.add(T, b, [&](int c) { return ec[c]; });
+  }
+  const double sa = gsum<G>(a), sb2 = gsum<G>(b);
+  const int i = blockIdx.x * (kTpbF / G) + threadIdx.x / G;
+  if (i < S.n_rows && threadIdx.x % G == 0) out[i] = sa + sb2;
+}
+
 // ------------------------------------------------------------ multi-RHS (X[row * b + q])
 __device__ __forceinline__ double2 ld2(const double* p) { return *reinterpret_cast<const double2*>(p); }
 
@@ -155,11 +228,38 @@ __global__ void __launch_bounds__(256) k_mvcf_up_rows(DCsr S, DCsr T, const doub
     default: GNW_LAUNCH(launch_k(KERNEL<32>, (ROWS + kTpbF / 32 - 1) / (kTpbF / 32), kTpbF, 0, __VA_ARGS__)); break; \
   }
 
+
+template <int G>
+void launch_lrestrict(const DLevel& L, VSel r, double* rc, const MinresState* st, cudaStream_t s) {
+  GNW_LAUNCH(launch_k(k_vcl_restrict<G>, (L.Ttl.n_rows + kTpbF / G - 1) / (kTpbF / G), kTpbF, 0, s, L.Ttl, r, st, rc));
+}
+template <int G>
+void launch_lup(const DLevel& L, VSel r, const double* ec, double* out, const MinresState* st, cudaStream_t s) {
+  GNW_LAUNCH(launch_k(k_vcl_up<G>, (L.n + kTpbF / G - 1) / (kTpbF / G), kTpbF, 0, s, L.Sl, L.Tl, r, ec, out, st));
+}
+#define GNW_L_DISPATCH(G, FN, ...) \
+  switch (G) {                     \
+    case 1: FN<1>(__VA_ARGS__); break;   \
+    case 2: FN<2>(__VA_ARGS__); break;   \
+    case 4: FN<4>(__VA_ARGS__); break;   \
+    case 8: FN<8>(__VA_ARGS__); break;   \
+    case 16: FN<16>(__VA_ARGS__); break; \
+    default: FN<32>(__VA_ARGS__); break; \
+  }
+
 void vcf_restrict(const DLevel& L, VSel r, double* rc, const MinresState* st, cudaStream_t s) {
+  if (L.Ttl.words != nullptr) {
+    GNW_L_DISPATCH(L.gTt, launch_lrestrict, L, r, rc, st, s);
+    return note_launch("vcl_restrict");
+  }
   GNW_F_DISPATCH(L.gTt, k_vcf_restrict, L.Tt.n_rows, s, L.Tt, r, st, rc);
   note_launch("vcf_restrict");
 }
 void vcf_up(const DLevel& L, VSel r, const double* ec, double* out, const MinresState* st, cudaStream_t s) {
+  if (L.Sl.words != nullptr && L.Tl.words != nullptr) {
+    GNW_L_DISPATCH(L.gS, launch_lup, L, r, ec, out, st, s);
+    return note_launch("vcl_up");
+  }
   GNW_F_DISPATCH(L.gS, k_vcf_up, L.n, s, L.S, L.T, r, ec, out, st);
   note_launch("vcf_up");
 }
