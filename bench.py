@@ -653,10 +653,31 @@ def run_gnw(args):
     # driver's 1/2/4/8-GPU runs also trace the partitioned curve.
     part_cfg = os.environ.get("GNW_BENCH_PARTITIONED_CONFIG", "C3")
     if ws > 1 or os.environ.get("GNW_BENCH_PARTITIONED") == "1":
+        # watchdog: a rank that fails inside a collective leaves the others waiting; the replica
+        # line must still be printed, so on timeout rank 0 prints it (partitioned: failed) and
+        # every rank leaves without the NCCL teardown
+        limit = float(os.environ.get("GNW_BENCH_PARTITIONED_TIMEOUT", "600"))
+
+        def give_up():
+            if rank == 0:
+                line["partitioned"] = {"failed": f"timeout after {limit:.0f} s"}
+                print(json.dumps(line), flush=True)
+            os._exit(0)
+
+        dog = threading.Timer(limit, give_up)
+        dog.daemon = True
+        dog.start()
         try:
             part = partitioned_leg(part_cfg, steps=2, warmup=1)
         except Exception as e:  # reported, never silently replaced
             part = {"failed": f"{type(e).__name__}: {e}"}
+            if ws > 1:  # the other ranks may be inside a collective: no barrier, no teardown
+                dog.cancel()
+                if rank == 0:
+                    line["partitioned"] = part
+                    print(json.dumps(line), flush=True)
+                os._exit(0)
+        dog.cancel()
         if rank == 0:
             line["partitioned"] = part
     if rank == 0:
