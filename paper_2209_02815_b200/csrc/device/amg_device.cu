@@ -1,7 +1,10 @@
 // amg_device.cu -- device SA-AMG hierarchy and V-cycle orchestration (amg.cpp:90-111).
 #include "amg_device.cuh"
+#include "sparse_device.cuh"
 
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <unordered_map>
@@ -66,6 +69,7 @@ DSell upload_sell(DeviceMemory& mem, const host::Csr& A, cudaStream_t s, int enc
   std::vector<int> cols(len, -1);
   std::vector<double> vals(encode == 0 ? len : 0, 0.0);
   std::vector<unsigned char> codes(encode == 2 ? len : 0, 0);
+#pragma omp parallel for schedule(static)
   for (int64_t r = 0; r < A.n_rows; ++r) {
     const int64_t base = (r / 32) * 32 * w + (r % 32);
     for (int64_t k = A.rowptr[r]; k < A.rowptr[r + 1]; ++k) {
@@ -129,6 +133,7 @@ DLell upload_lell(DeviceMemory& mem, const host::Csr& A, int G, cudaStream_t s) 
     table.push_back(v);
   }
   std::vector<unsigned> words(static_cast<size_t>(len), 0xffffffffu);
+#pragma omp parallel for schedule(static)
   for (int64_t r = 0; r < A.n_rows; ++r) {
     const int64_t base = (r / rpw) * W * 32 + (r % rpw) * G;
     for (int64_t k = A.rowptr[r]; k < A.rowptr[r + 1]; ++k) {
@@ -172,7 +177,8 @@ void DeviceAmg::reset() {
   mem_.release_all();
 }
 
-void DeviceAmg::upload(const host::AmgHierarchy& h, cudaStream_t s, int min_collapse_level) {
+void DeviceAmg::upload(const host::AmgHierarchy& h, cudaStream_t s, int min_collapse_level,
+                       std::vector<DevFusedOps>* fused_dev) {
   reset();
   min_collapse_ = min_collapse_level;
   const double omega = h.options.jacobi_damping;
@@ -190,6 +196,15 @@ void DeviceAmg::upload(const host::AmgHierarchy& h, cudaStream_t s, int min_coll
   if (const char* e = std::getenv("GNW_VC_COLLAPSE"))
     if (std::atoi(e) == 0) stop = static_cast<int>(L) - 1;
   fused_ = false;
+  const bool timing = [] {
+    const char* e = std::getenv("GNW_SETUP_TIMING");
+    return e != nullptr && std::atoi(e) != 0;
+  }();
+  double t_csr = 0, t_sell = 0, t_fops = 0, t_fup = 0, t_lell = 0;
+  auto now = [] { return std::chrono::steady_clock::now(); };
+  auto ms = [](std::chrono::steady_clock::time_point a, std::chrono::steady_clock::time_point b) {
+    return std::chrono::duration<double, std::milli>(b - a).count();
+  };
   vr_.assign(L, nullptr);
   ve_.assign(L, nullptr);
   vres_.assign(L, nullptr);
@@ -199,15 +214,19 @@ void DeviceAmg::upload(const host::AmgHierarchy& h, cudaStream_t s, int min_coll
     DLevel d;
     d.n = static_cast<int>(H.A.n_rows);
     if (l + 1 < L) {
+      auto ta = now();
       d.A = upload_csr(mem_, H.A, s);
       d.P = upload_csr(mem_, H.P, s);
       const host::Csr Rt = host::transpose(H.P);
       d.R = upload_csr(mem_, Rt, s);
+      auto tb = now();
+      t_csr += ms(ta, tb);
       if (!std::getenv("GNW_VC_CSR")) {  // experiment switch: CSR thread-per-row kernels
         d.As = upload_sell(mem_, H.A, s);
         d.Ps = upload_sell(mem_, H.P, s);
         d.Rs = upload_sell(mem_, Rt, s);
       }
+      t_sell += ms(tb, now());
       d.gA = vc_group_lanes(H.A.nnz(), H.A.n_rows);
       d.gP = vc_group_lanes(H.P.nnz(), H.P.n_rows);
       d.gR = vc_group_lanes(H.P.nnz(), H.P.n_cols);
@@ -218,19 +237,46 @@ void DeviceAmg::upload(const host::AmgHierarchy& h, cudaStream_t s, int min_coll
       GNW_CUDA_CHECK(cudaStreamSynchronize(s));
       if (fused_on && static_cast<int>(l) < stop) {
         fused_ = true;  // levels above the dense tail (vcycle_fused.cu)
-        const host::FusedCycleOps f = host::fused_cycle_ops(H.A, H.P, wd);
-        d.S = upload_csr(mem_, f.S, s);
-        d.T = upload_csr(mem_, f.T, s);
-        d.Tt = upload_csr(mem_, f.Tt, s);
-        d.gS = vc_group_lanes(f.S.nnz() + f.T.nnz(), f.S.n_rows);
-        d.gTt = vc_group_lanes(f.Tt.nnz(), f.Tt.n_rows);
-        d.fused = 1;
+        auto tc = now();
         const char* le = std::getenv("GNW_VC_LELL");  // experiment switch: 0 keeps the CSR loops
-        if (!(le && std::atoi(le) == 0)) {
-          d.Sl = upload_lell(mem_, f.S, d.gS, s);
-          d.Tl = upload_lell(mem_, f.T, d.gS, s);
-          d.Ttl = upload_lell(mem_, f.Tt, d.gTt, s);
+        const bool lell_on = !(le && std::atoi(le) == 0);
+        if (fused_dev != nullptr && l < fused_dev->size()) {
+          // formed by the device setup (amg_setup_device.cu): adopted where they are, and their
+          // lane-ELL copies are built on the device
+          DevFusedOps& fd = (*fused_dev)[l];
+          const long long nnz_st = fd.S.nnz + fd.T.nnz, nnz_tt = fd.Tt.nnz, rows_tt = fd.Tt.n_rows;
+          d.S = adopt_csr(mem_, fd.S, s);
+          d.T = adopt_csr(mem_, fd.T, s);
+          d.Tt = adopt_csr(mem_, fd.Tt, s);
+          d.gS = vc_group_lanes(nnz_st, d.n);
+          d.gTt = vc_group_lanes(nnz_tt, rows_tt);
+          auto te = now();
+          t_fup += ms(tc, te);
+          if (lell_on) {
+            d.Sl = build_lell_device(mem_, d.S, d.gS, s);
+            d.Tl = build_lell_device(mem_, d.T, d.gS, s);
+            d.Ttl = build_lell_device(mem_, d.Tt, d.gTt, s);
+          }
+          t_lell += ms(te, now());
+        } else {
+          const host::FusedCycleOps f = host::fused_cycle_ops(H.A, H.P, wd);
+          auto td = now();
+          t_fops += ms(tc, td);
+          d.S = upload_csr(mem_, f.S, s);
+          d.T = upload_csr(mem_, f.T, s);
+          d.Tt = upload_csr(mem_, f.Tt, s);
+          d.gS = vc_group_lanes(f.S.nnz() + f.T.nnz(), f.S.n_rows);
+          d.gTt = vc_group_lanes(f.Tt.nnz(), f.Tt.n_rows);
+          auto te = now();
+          t_fup += ms(td, te);
+          if (lell_on) {
+            d.Sl = upload_lell(mem_, f.S, d.gS, s);
+            d.Tl = upload_lell(mem_, f.T, d.gS, s);
+            d.Ttl = upload_lell(mem_, f.Tt, d.gTt, s);
+          }
+          t_lell += ms(te, now());
         }
+        d.fused = 1;
       }
       vres_[l] = mem_.alloc<double>(d.n);
       vx_[l] = mem_.alloc<double>(d.n);
@@ -249,7 +295,13 @@ void DeviceAmg::upload(const host::AmgHierarchy& h, cudaStream_t s, int min_coll
   GNW_CUDA_CHECK(cudaMemcpyAsync(coarse_L_, h.coarse_chol.data(), h.coarse_chol.size() * sizeof(double),
                                  cudaMemcpyHostToDevice, s));
   GNW_CUDA_CHECK(cudaStreamSynchronize(s));
+  auto tf = now();
   build_collapse(s);
+  if (timing)
+    std::fprintf(stderr,
+                 "[gnw setup] device hierarchy: CSR uploads %.1f ms, SELL copies %.1f ms, fused ops (host) %.1f ms, "
+                 "fused uploads %.1f ms, lane-ELL %.1f ms, collapsed tail %.1f ms\n",
+                 t_csr, t_sell, t_fops, t_fup, t_lell, ms(tf, now()));
 }
 
 // Collapsed coarse tail.  Below some level the V-cycle is a small LINEAR map of that

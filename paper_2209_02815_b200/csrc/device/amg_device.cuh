@@ -51,11 +51,16 @@ DLell upload_lell(DeviceMemory& mem, const host::Csr& A, int G, cudaStream_t s);
 // sparse_matmul on the device, bit-identical to host::spgemm (spgemm.cu)
 host::Csr device_spgemm(const host::Csr& A, const host::Csr& B, cudaStream_t s);
 
+struct DevFusedOps;  // sparse_device.cuh
+
 class DeviceAmg {
  public:
   // min_collapse_level: the first level the dense collapsed tail may start at (1 for a whole
   // hierarchy; 0 for the replicated tail of a partitioned cycle that starts at the collapse level)
-  void upload(const host::AmgHierarchy& h, cudaStream_t s, int min_collapse_level = 1);
+  // fused_dev: the leading levels' one-pass operators where the device setup already formed
+  // them; they are adopted (the vector's matrices are left empty)
+  void upload(const host::AmgHierarchy& h, cudaStream_t s, int min_collapse_level = 1,
+              std::vector<DevFusedOps>* fused_dev = nullptr);
   void reset();
   bool empty() const { return lv_.empty(); }
   int n() const { return lv_.empty() ? 0 : lv_[0].n; }

@@ -7,6 +7,7 @@
 // recurred residual crosses tol (the reference's true-residual verification,
 // minres.cpp:108-120), on exhaustion, on maxit or on a numerical error.
 #include "context.cuh"
+#include "sparse_device.cuh"
 
 #include <algorithm>
 #include <chrono>
@@ -160,9 +161,16 @@ void Context::assemble(const double* vertices, int64_t nv, const int64_t* cells,
   const auto t1q = std::chrono::steady_clock::now();
   D_ = host::assemble_D(mesh_);                          // fem_mixed.cpp:70-82
   const auto t1d = std::chrono::steady_clock::now();
-  S_ = host::lumped_schur(Q_, D_);                       // fem_mixed.cpp:84-94
+  // Device contexts run the Schur complement's product and the whole level pipeline of
+  // amg_setup on the device (sparse_device.cuh, bit-identical; only the greedy aggregation
+  // stays on the host).  Env GNW_DEVICE_SETUP=0: the host code.
+  const bool dev_setup = device_setup_enabled();
+  fused_pre_.clear();
+  if (dev_setup) GNW_CUDA_CHECK(cudaSetDevice(device_));
+  S_ = dev_setup ? device_lumped_schur(Q_, D_, stream_) : host::lumped_schur(Q_, D_);  // fem_mixed.cpp:84-94
   const auto t2 = std::chrono::steady_clock::now();
-  amg_ = host::amg_setup(S_, o);                         // amg.cpp:115-187
+  amg_ = dev_setup ? device_amg_setup(S_, o, stream_, comm_ ? nullptr : &fused_pre_, DeviceAmg::collapse_max())
+                   : host::amg_setup(S_, o);             // amg.cpp:115-187
   if (const char* e = std::getenv("GNW_SETUP_TIMING"))
     if (std::atoi(e) != 0)
       std::fprintf(stderr, "[gnw setup] finalize_mesh %.1f ms, assemble Q %.1f ms, D %.1f ms, S_hat %.1f ms\n",
@@ -206,8 +214,19 @@ void Context::finish_assembly() {
     if (comm_) {  // row partition (context_rowpart.cu): local operators, halos, partitioned V-cycle
       setup_rowpart();
     } else {
+      const bool timing = [] {
+        const char* e = std::getenv("GNW_SETUP_TIMING");
+        return e != nullptr && std::atoi(e) != 0;
+      }();
+      const auto t0 = std::chrono::steady_clock::now();
       upload_structure();
+      sync();
+      const auto t1 = std::chrono::steady_clock::now();
       upload_hierarchy();
+      if (timing)
+        std::fprintf(stderr, "[gnw setup] upload saddle structure %.1f ms, hierarchy (device V-cycle operators) %.1f ms\n",
+                     std::chrono::duration<double, std::milli>(t1 - t0).count(),
+                     std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t1).count());
     }
     sync();
   }
@@ -241,7 +260,13 @@ void Context::assemble_saddle_csr(int64_t K, int64_t N, const int64_t* qrp, cons
   D_ = csr(N, K, drp, dci, dv);
   mesh_ = host::Mesh{};
   S_ = host::lumped_schur(Q_, D_);                        // fem_mixed.cpp:84-94
-  amg_ = o ? host::amg_setup(S_, *o) : host::AmgHierarchy{};  // amg.cpp:115-187
+  fused_pre_.clear();
+  if (o && device_setup_enabled()) {
+    GNW_CUDA_CHECK(cudaSetDevice(device_));
+    amg_ = device_amg_setup(S_, *o, stream_, &fused_pre_, DeviceAmg::collapse_max());
+  } else {
+    amg_ = o ? host::amg_setup(S_, *o) : host::AmgHierarchy{};  // amg.cpp:115-187
+  }
   K_ = K;
   N_ = N;
   mixed_ = true;
@@ -390,8 +415,18 @@ void Context::alloc_vectors(long long n_alloc, long long K, long long N) {
   ctot_ = mem_.alloc<double>(4);  // their sum (k_sum_triples)
 }
 
+bool Context::device_setup_enabled() const {
+  if (!has_device()) return false;
+  const char* e = std::getenv("GNW_DEVICE_SETUP");
+  return !(e && std::atoi(e) == 0);
+}
+
 void Context::upload_hierarchy() {
-  if (!amg_.levels.empty()) damg_.upload(amg_, stream_);
+  if (!amg_.levels.empty()) damg_.upload(amg_, stream_, 1, fused_pre_.empty() ? nullptr : &fused_pre_);  // adopts them
+  const bool had_dev = !fused_pre_.empty();
+  fused_pre_.clear();
+  fused_pre_.shrink_to_fit();
+  if (had_dev || device_setup_enabled()) device_setup_trim();  // the setup's pool blocks go back to the driver
   svc_ = mem_.alloc<double>(std::max<int64_t>(N_, 1));
   sync();
 }

@@ -11,6 +11,7 @@
 #include "../host/ert.hpp"
 #include "../host/setup.hpp"
 #include "amg_device.cuh"
+#include "sparse_device.cuh"
 #include "comm.cuh"
 #include "ert_gmg.cuh"
 #include "ert_kernels.cuh"
@@ -186,6 +187,8 @@ class Context {
   host::Mesh mesh_;
   host::Csr Q_, D_, S_;
   host::AmgHierarchy amg_;
+  std::vector<DevFusedOps> fused_pre_;  // one-pass level operators formed (and kept) on the device by the setup
+  bool device_setup_enabled() const;
   int64_t K_ = 0, N_ = 0;
 
   // device structure

@@ -434,8 +434,6 @@ Csr from_triplets(int64_t n_rows, int64_t n_cols, std::vector<int64_t> rows, std
   return A;
 }
 
-namespace {
-
 std::vector<double> inverse_diagonal(const Csr& A) {  // amg.cpp:81-88
   std::vector<double> d = diagonal(A);
   for (double& v : d) {
@@ -498,8 +496,6 @@ std::vector<int64_t> aggregate(const Csr& A, const AmgOptions& o, int64_t& n_agg
   return agg;
 }
 
-}  // namespace
-
 namespace {
 // env GNW_SETUP_TIMING=1: per-phase wall times of the host setup on stderr
 bool setup_timing() {
@@ -522,12 +518,14 @@ struct PhaseTimer {
 }  // namespace
 
 // amg_setup, amg.cpp:115-187
-AmgHierarchy amg_setup(const Csr& S, const AmgOptions& o) {
+AmgHierarchy amg_setup(const Csr& S, const AmgOptions& o, bool check_symmetry) {
   PhaseTimer pt;
   if (S.n_rows != S.n_cols) throw std::invalid_argument("amg_setup: matrix not square");
   double max_abs = 0.0;
   for (double v : S.vals) max_abs = std::max(max_abs, std::abs(v));
-  if (symmetry_error(S) > 1e-12 * std::max(max_abs, 1.0))
+  // check_symmetry = false: S is a coarse level of a hierarchy being continued (the device
+  // setup hands its small levels back), which amg.cpp:115-187 does not re-check
+  if (check_symmetry && symmetry_error(S) > 1e-12 * std::max(max_abs, 1.0))
     throw std::invalid_argument("amg_setup: matrix not symmetric");
   AmgHierarchy h;
   h.options = o;

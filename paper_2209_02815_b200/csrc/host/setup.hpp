@@ -77,7 +77,11 @@ Csr lumped_schur(const Csr& Q, const Csr& D);
 /// Sorted-triplet construction with duplicate summation (sparse.cpp:19-51).
 Csr from_triplets(int64_t n_rows, int64_t n_cols, std::vector<int64_t> rows,
                   std::vector<int64_t> cols, std::vector<double> vals);
-AmgHierarchy amg_setup(const Csr& S, const AmgOptions& opt);
+AmgHierarchy amg_setup(const Csr& S, const AmgOptions& opt, bool check_symmetry = true);
+/// The pieces of amg_setup the device-resident setup (device/sparse_device.cuh) shares:
+/// the sequential greedy aggregation (amg.cpp:13-68) and 1 / diag(A) (amg.cpp:81-88).
+std::vector<int64_t> aggregate(const Csr& A, const AmgOptions& o, int64_t& n_agg);
+std::vector<double> inverse_diagonal(const Csr& A);
 /// One level of the default-mode V-cycle (amg.cpp:90-111) as two sparse operators.  With
 /// Wd = omega diag(A)^-1 the level computes x1 = Wd r + P e_c, e = x1 + Wd (r - A x1) and passes
 /// r_c = P^T (r - A Wd r) down; for symmetric A that is

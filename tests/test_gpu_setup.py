@@ -40,3 +40,49 @@ def test_device_setup_products_bitwise(monkeypatch, oracle, n, thr):
             for w in (3, 4):
                 for x, y in zip(ref.csr(w, l), eg[(w, l)]):
                     assert np.array_equal(np.asarray(x), np.asarray(y)), (w, l)
+
+
+@pytest.mark.parametrize("n,thr,min_rows", [(32, 64, 0), (64, 64, 0), (256, 64, 0), (256, 64, None)])
+def test_device_amg_setup_bitwise(monkeypatch, n, thr, min_rows):
+    """The device-resident amg_setup (amg_setup_device.cu: filter, tentative prolongator, smoothing
+    product, P merge, transposes, Galerkin product; default on device contexts) against the host
+    setup: every level bit for bit, and the V-cycle built on the device-formed one-pass operators
+    (S, T, T^T) bitwise the one built on the host-formed ones."""
+    mesh = W.unit_square_mesh(n)
+    monkeypatch.setenv("GNW_DEVICE_SETUP", "1")
+    if min_rows is not None:  # every level on the device (by default levels <= 100000 rows finish on the host)
+        monkeypatch.setenv("GNW_DEVICE_SETUP_MIN_ROWS", str(min_rows))
+    gpu = Context(0)
+    gpu.assemble(mesh, AmgOptions(coarse_threshold=thr))
+    monkeypatch.setenv("GNW_DEVICE_SETUP", "0")
+    ref = Context(0)
+    ref.assemble(mesh, AmgOptions(coarse_threshold=thr))
+    host = Context(None)
+    host.assemble(mesh, AmgOptions(coarse_threshold=thr))
+    ig, ih = gpu.info(), host.info()
+    assert (ig["n_levels"], ig["coarse_n"]) == (ih["n_levels"], ih["coarse_n"])
+    eg, eh = exported(gpu, ig["n_levels"]), exported(host, ih["n_levels"])
+    for k in eh:
+        for x, y in zip(eg[k], eh[k]):
+            assert np.array_equal(np.asarray(x), np.asarray(y)), k
+    rng = np.random.default_rng(n)
+    r = rng.standard_normal(mesh.n_cells)
+    assert np.array_equal(gpu.amg_apply(r), ref.amg_apply(r))
+
+
+def test_device_amg_setup_baseline_mesh_hashes(monkeypatch):
+    """BASELINE C5 mesh (n = 1024, threshold 1024): the device setup's hierarchy against the
+    SHA-256 hashes of the unmodified reference's own amg_setup (tests/golden/ref_p1024.json)."""
+    import refdata
+
+    if not refdata.available("p1024"):
+        pytest.skip("fixture ref_p1024.json not generated")
+    ref = refdata.load("p1024")
+    monkeypatch.setenv("GNW_DEVICE_SETUP", "1")
+    monkeypatch.setenv("GNW_DEVICE_SETUP_MIN_ROWS", "0")
+    c = Context(0).assemble(W.unit_square_mesh(ref["n"]), AmgOptions(coarse_threshold=ref["coarse_threshold"]))
+    info = c.info()
+    assert info["n_levels"] == ref["n_levels"] and info["coarse_n"] == ref["coarse_n"]
+    got = refdata.level_hashes_of(c.export_csr, info["n_levels"])
+    for l, (g, r) in enumerate(zip(got, ref["levels"])):
+        assert g == r, f"level {l}"
