@@ -1623,10 +1623,13 @@ void capacitance_dgemm(const double* J, long long ldj, const double* Ht, long lo
       if (plan.full || j <= i) hp[np++] = make_int2(i, j);
   int2* dpairs = reinterpret_cast<int2*>(part + static_cast<long long>(plan.splits) * plan.npairs * dg::BM * dg::BN);
   cudaMemcpyAsync(dpairs, hp, np * sizeof(int2), cudaMemcpyHostToDevice, s);
-  smem_optin(reinterpret_cast<const void*>(k_dgemm_nt), dg::SMEM);
-  dim3 grid(plan.npairs, plan.splits);
-  GNW_LAUNCH(launch_k(k_dgemm_nt, grid, 256, dg::SMEM, s, J, ldj, Ht, ldh, m, N, plan.kchunk, dpairs, plan.npairs, part));
-  check_launch("dgemm_nt");
+  // TMA-staged, warp-specialised kernel (dgemm_tma.cu); the cp.async kernel is the fallback
+  if (!capacitance_dgemm_tma(J, ldj, Ht, ldh, m, N, plan, dpairs, part, s)) {
+    smem_optin(reinterpret_cast<const void*>(k_dgemm_nt), dg::SMEM);
+    dim3 grid(plan.npairs, plan.splits);
+    GNW_LAUNCH(launch_k(k_dgemm_nt, grid, 256, dg::SMEM, s, J, ldj, Ht, ldh, m, N, plan.kchunk, dpairs, plan.npairs, part));
+    check_launch("dgemm_nt");
+  }
   dim3 g2((dg::BM * dg::BN + 255) / 256, plan.npairs);
   GNW_LAUNCH(launch_k(k_dgemm_finalize, g2, 256, 0, s, part, dpairs, plan.npairs, plan.splits, m, beta, C));
   check_launch("dgemm_finalize");

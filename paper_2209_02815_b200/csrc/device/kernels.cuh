@@ -202,6 +202,9 @@ struct DgemmPlan {
 DgemmPlan dgemm_plan(int m, long long N, int full, int sm_count);
 void capacitance_dgemm(const double* J, long long ldj, const double* Ht, long long ldh, int m, long long N,
                        double beta, const DgemmPlan& plan, double* part, double* C, cudaStream_t s);
+// the split-K partial tiles by the TMA-staged kernel (dgemm_tma.cu); false when it cannot run
+bool capacitance_dgemm_tma(const double* J, long long ldj, const double* Ht, long long ldh, int m, long long N,
+                           const DgemmPlan& plan, const int2* dpairs, double* part, cudaStream_t s);
 // dense_cholesky (linalg.cpp:88-105), operation order preserved; *fail = 1 on a
 // non-positive pivot.
 void cholesky(const double* C, double* L, int n, int* fail, cudaStream_t s);
