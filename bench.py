@@ -14,7 +14,8 @@ per solve) are far larger than the 126 MB L2, so no L2 flush is needed between s
 * value  -- device-resident inputs (torch CUDA tensors, device-pointer mode), timed with CUDA
             events on the library's stream; whole-job throughput (N replicas, max over ranks).
 * e2e    -- the same solves through the C-ABI with HOST buffers (pinned): J, m, m_ref, g, g_obs
-            copied H2D every step inside the timed region; rhs and x copied back D2H.  Step k+1's
+            copied H2D every step inside the timed region, x copied back D2H (gnw_set_jacobian +
+            gnw_gn_step_solve: the reference's GN step, inversion.cpp:244-265).  Step k+1's
             J (1.07 GB) is staged with gnw_prefetch_jacobian during step k's MINRES (copy stream);
             step 0 copies its own J, so every step's input transfer is inside the timed region.
 * roofline -- the dominant per-iteration kernel measured in isolation with CUDA events
@@ -446,10 +447,9 @@ def run_gnw(args):
     zN = torch.from_numpy(inp.rhs_mref).cuda()
     zm = torch.from_numpy(inp.rhs_gobs).cuda()
 
-    def solve_dev(alpha):
+    def solve_dev(alpha):  # the reference's GN step: inversion.cpp:244-265
         tm = ctx.set_jacobian(J_d, alpha)
-        b = ctx.assemble_rhs(dm_d, zN, dg_d, zm)
-        x, rep = ctx.minres(b, tol=tol)
+        x, rep = ctx.gn_step_solve(dm_d, zN, dg_d, zm, tol=tol)
         st = ctx.stats()
         return tm, rep, st
 
@@ -568,16 +568,16 @@ def run_gnw(args):
     zN_h = torch.from_numpy(inp.rhs_mref).pin_memory().numpy()
     zm_h = torch.from_numpy(inp.rhs_gobs).pin_memory().numpy()
 
-    b_h = torch.empty(K + N, dtype=torch.float64, pin_memory=True).numpy()   # rhs (D2H, then H2D)
-    x0_h = torch.zeros(K + N, dtype=torch.float64, pin_memory=True).numpy()
     x_h = torch.empty(K + N, dtype=torch.float64, pin_memory=True).numpy()   # solution (D2H)
 
     def solve_host(alpha, prefetch_next):
+        # the reference's GN step (inversion.cpp:244-265): build_woodbury_preconditioner, then
+        # b = assemble_gn_rhs(...), x0 = 0, minres -- the last three as one C-ABI call
+        # (gnw_gn_step_solve): host m, m_ref, g, g_obs in, host x out
         ctx.set_jacobian(J_h, alpha)  # takes the staged copy when the previous step prefetched it
-        b = ctx.assemble_rhs(dm_h, zN_h, dg_h, zm_h, out=b_h)
         if prefetch_next:  # the next step's J crosses PCIe during this step's MINRES
             ctx.prefetch_jacobian(J_h)
-        x, rep = ctx.minres(b, x0=x0_h, tol=tol, out=x_h)
+        x, rep = ctx.gn_step_solve(dm_h, zN_h, dg_h, zm_h, tol=tol, out=x_h)
         return x, rep
 
     solve_host(alphas[0], False)  # nothing staged when the timed region opens: step 0 copies J itself
@@ -590,8 +590,8 @@ def run_gnw(args):
     ctx.event_record(3)
     e2e_elapsed = max_over_ranks(ctx.event_elapsed(2, 3))
     barrier()
-    h2d = 8 * (cfg.m * N + 3 * N + 2 * cfg.m) + 8 * 2 * (K + N)  # J, m, m_ref, g, g_obs, then b, x0
-    d2h = 8 * (K + N) * 2 + 8 * 2 * (rep_h.iterations + 1)        # rhs, x, residual histories
+    h2d = 8 * (cfg.m * N + 2 * N + 2 * cfg.m)               # J, m, m_ref, g, g_obs
+    d2h = 8 * (K + N) + 8 * 2 * (rep_h.iterations + 1)      # x, residual histories
 
     # ---------------------------------------------------------- CPU baseline
     cpu = None

@@ -198,6 +198,14 @@ gnw_status gnw_assemble_rhs(gnw_ctx* ctx, const double* m, const double* m_ref,
                             const double* g, const double* g_obs, double* rhs);
 gnw_status gnw_minres_solve(gnw_ctx* ctx, const double* b, const double* x0, double* x,
                             double tol, uint64_t maxit, gnw_report* report);
+/* The reference's GN-step solve in one call (gauss_newton, inversion.cpp:259-265):
+ *   b = assemble_gn_rhs(m, m_ref, g, g_obs, J, D, beta); x0 = 0; minres(op, pc, b, x0, tol, maxit).
+ * Same results as gnw_assemble_rhs + gnw_minres_solve with a zero x0, bit for bit; the
+ * right-hand side stays on the device and the zero start is not transferred.  x: K + N.
+ * gnw_minres_solve itself accepts x0 == NULL for the zero start.  Single-GPU contexts. */
+gnw_status gnw_gn_step_solve(gnw_ctx* ctx, const double* m, const double* m_ref, const double* g,
+                             const double* g_obs, double* x, double tol, uint64_t maxit,
+                             gnw_report* report);
 /* The full residual histories of the last gnw_minres_solve (MinresReport::relative_residuals
  * and ::pnorm_relative_residuals, minres.hpp:15-16), for callers whose report capacity was
  * smaller than n_hist: copies min(cap, n_hist) entries; *n_hist = the full length. */

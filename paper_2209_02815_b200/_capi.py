@@ -73,7 +73,7 @@ EXPORTED = [
     "gnw_set_coarse_mode", "gnw_set_preconditioner", "gnw_set_loop_mode", "gnw_assemble", "gnw_assemble_amg_csr",
     "gnw_assemble_saddle_csr", "gnw_set_amg_hierarchy", "gnw_set_flux_scaling", "gnw_get_info",
     "gnw_set_jacobian", "gnw_prefetch_jacobian", "gnw_apply_operator", "gnw_precondition", "gnw_amg_apply",
-    "gnw_get_woodbury", "gnw_assemble_rhs", "gnw_minres_solve", "gnw_minres_history", "gnw_export_csr",
+    "gnw_get_woodbury", "gnw_assemble_rhs", "gnw_minres_solve", "gnw_gn_step_solve", "gnw_minres_history", "gnw_export_csr",
     "gnw_export_mesh", "gnw_dense_cholesky", "gnw_get_stats", "gnw_event_record",
     "gnw_event_elapsed", "gnw_profile_kernel", "gnw_set_electrodes", "gnw_response_jacobian",
     "gnw_geometric_factor", "gnw_nccl_unique_id", "gnw_create_partitioned", "gnw_create_local_group",
@@ -145,6 +145,7 @@ def load() -> C.CDLL:
     L.gnw_get_woodbury.argtypes = [vp, vp, vp]
     L.gnw_assemble_rhs.argtypes = [vp, vp, vp, vp, vp, vp]
     L.gnw_minres_solve.argtypes = [vp, vp, vp, vp, dbl, u64, C.POINTER(Report)]
+    L.gnw_gn_step_solve.argtypes = [vp, vp, vp, vp, vp, vp, dbl, u64, C.POINTER(Report)]
     L.gnw_minres_history.argtypes = [vp, vp, vp, u64, C.POINTER(u64)]
     L.gnw_export_csr.argtypes = [vp, i32, u64, C.POINTER(u64), C.POINTER(u64), C.POINTER(u64), vp, vp, vp]
     L.gnw_export_mesh.argtypes = [vp, vp, vp, vp, vp, vp, vp]

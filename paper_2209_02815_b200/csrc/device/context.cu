@@ -942,6 +942,36 @@ void Context::assemble_rhs(const double* mdl, const double* mref, const double* 
   t_rhs = ms * 1e-3;
 }
 
+// The reference's GN-step solve (inversion.cpp:259-265): b = assemble_gn_rhs(...), x0 = 0,
+// minres(op, pc, b, x0, tol, maxit) as ONE call.  The right-hand side is assembled straight into
+// the solver's b on the device and never visits the host; the zero start needs no transfer.
+MinresResult Context::gn_step_solve(const double* mdl, const double* mref, const double* g, const double* gobs,
+                                    double* x, double tol, uint64_t maxit) {
+  if (!(tol > 0.0)) throw std::invalid_argument("minres: tol must be positive");
+  require_mixed();
+  require_device();
+  if (comm_) throw std::invalid_argument("gn_step_solve: single-GPU contexts (partitioned: assemble_rhs + minres_solve)");
+  if (m_ == 0) throw std::invalid_argument("assemble_gn_rhs: shape mismatch");
+  const double* dgv = g;
+  const double* dgo = gobs;
+  if (ptr_mode != 1) {
+    h2d(t_, g, m_, stream_);
+    h2d(t2_, gobs, m_, stream_);
+    dgv = t_;
+    dgo = t2_;
+  }
+  double* dm = stage_in(mdl, N_, io_a_);
+  double* dmr = stage_in(mref, N_, io_b_);
+  GNW_CUDA_CHECK(cudaEventRecord(rhs_ev_[0], stream_));
+  gnw::assemble_rhs(op_, beta_, dm, dmr, dgv, dgo, b_, stream_);
+  GNW_CUDA_CHECK(cudaEventRecord(rhs_ev_[1], stream_));
+  MinresResult r = minres(nullptr, nullptr, x, tol, maxit);
+  float ms = 0.f;
+  GNW_CUDA_CHECK(cudaEventElapsedTime(&ms, rhs_ev_[0], rhs_ev_[1]));
+  t_rhs = ms * 1e-3;
+  return r;
+}
+
 // ------------------------------------------------------------------ MINRES
 // One MINRES iteration (minres.cpp:70-148) as device work, ring slots chosen on the
 // device from st_->j.  Captured once into the conditional-WHILE graph body, or
@@ -1022,15 +1052,26 @@ MinresResult Context::minres(const double* b, const double* x0, double* x, doubl
   cudaEvent_t e0, e1;
   GNW_CUDA_CHECK(cudaEventCreate(&e0));
   GNW_CUDA_CHECK(cudaEventCreate(&e1));
+  // b == nullptr: b_ already holds the right-hand side (gn_step_solve assembled it there);
+  // x0 == nullptr: the zero start of the reference's GN step (inversion.cpp:261)
+  if (comm_ && (b == nullptr || x0 == nullptr))
+    throw std::invalid_argument("minres: partitioned solves take b and x0 explicitly");
   if (comm_) {
     global_to_local(global_in(b, K_ + N_, gio_a_), b_, false);
     global_to_local(global_in(x0, K_ + N_, gio_b_), x_, false);
-  } else if (ptr_mode == 1) {
-    GNW_CUDA_CHECK(cudaMemcpyAsync(b_, b, n * sizeof(double), cudaMemcpyDeviceToDevice, s));
-    GNW_CUDA_CHECK(cudaMemcpyAsync(x_, x0, n * sizeof(double), cudaMemcpyDeviceToDevice, s));
   } else {
-    h2d(b_, b, n, s);
-    h2d(x_, x0, n, s);
+    if (b != nullptr) {
+      if (ptr_mode == 1)
+        GNW_CUDA_CHECK(cudaMemcpyAsync(b_, b, n * sizeof(double), cudaMemcpyDeviceToDevice, s));
+      else
+        h2d(b_, b, n, s);
+    }
+    if (x0 == nullptr)
+      GNW_CUDA_CHECK(cudaMemsetAsync(x_, 0, n * sizeof(double), s));
+    else if (ptr_mode == 1)
+      GNW_CUDA_CHECK(cudaMemcpyAsync(x_, x0, n * sizeof(double), cudaMemcpyDeviceToDevice, s));
+    else
+      h2d(x_, x0, n, s);
   }
   GNW_CUDA_CHECK(cudaEventRecord(e0, s));
   auto read_plain = [&]() {
@@ -1038,8 +1079,12 @@ MinresResult Context::minres(const double* b, const double* x0, double* x, doubl
     sync();
     return h_st_[1];
   };
-  // r = b - A x  (and ||b||)
-  operator_into(vfixed(x_), 0, vfixed(az_), st_plain_, 0);
+  // r = b - A x  (and ||b||).  With the zero start A x0 is exactly zero (every product is a
+  // signed zero and every row sum +0.0, so b - A x0 = b bit for bit): no operator pass
+  if (x0 == nullptr)
+    GNW_CUDA_CHECK(cudaMemsetAsync(az_, 0, n * sizeof(double), s));
+  else
+    operator_into(vfixed(x_), 0, vfixed(az_), st_plain_, 0);
   residual(n, b_, az_, r_, st_plain_, 1, rpart_, counters_ + 5, s);
   if (comm_) reduce_scratch(st_plain_, 4, 2);
   MinresState ps = read_plain();

@@ -95,6 +95,9 @@ class Context {
   void amg_apply(const double* r, double* z);
   void assemble_rhs(const double* mdl, const double* mref, const double* g, const double* gobs, double* rhs);
   MinresResult minres(const double* b, const double* x0, double* x, double tol, uint64_t maxit);
+  // assemble_gn_rhs + minres from the zero start in one call (inversion.cpp:259-265)
+  MinresResult gn_step_solve(const double* mdl, const double* mref, const double* g, const double* gobs, double* x,
+                             double tol, uint64_t maxit);
   void get_woodbury(double* H, double* L);
   void dense_cholesky(int64_t n, const double* C, double* L);
   void event_record(int slot);

@@ -263,6 +263,26 @@ gnw_status gnw_minres_solve(gnw_ctx* ctx, const double* b, const double* x0, dou
   }, ctx);
 }
 
+gnw_status gnw_gn_step_solve(gnw_ctx* ctx, const double* m, const double* m_ref, const double* g, const double* g_obs,
+                             double* x, double tol, uint64_t maxit, gnw_report* report) {
+  return guard([&] {
+    gnw::MinresResult r = ctx_of(ctx).gn_step_solve(m, m_ref, g, g_obs, x, tol, maxit);
+    ctx->hist_e = r.hist_e;
+    ctx->hist_p = r.hist_p;
+    if (report) {
+      report->iterations = r.iterations;
+      report->converged = r.converged ? 1 : 0;
+      report->true_relative_residual = r.true_rel;
+      report->n_hist = r.hist_e.size();
+      const uint64_t h = std::min<uint64_t>(report->hist_cap, r.hist_e.size());
+      for (uint64_t k = 0; k < h; ++k) {
+        if (report->relative_residuals) report->relative_residuals[k] = r.hist_e[k];
+        if (report->pnorm_relative_residuals) report->pnorm_relative_residuals[k] = r.hist_p[k];
+      }
+    }
+  }, ctx);
+}
+
 gnw_status gnw_minres_history(const gnw_ctx* ctx, double* relative_residuals, double* pnorm_relative_residuals,
                               uint64_t cap, uint64_t* n_hist) {
   return guard([&] {

@@ -53,6 +53,7 @@ class Context:
         self.h = h
         self.device = device
         self.device_pointers = False
+        self._partitioned = False
         self.K = self.N = self.m = 0
 
     # ------------------------------------------------ partitioned (multi-GPU)
@@ -63,6 +64,7 @@ class Context:
         self.h = handle
         self.device = device
         self.device_pointers = False
+        self._partitioned = True  # _adopt wraps the handles of partitioned / local-group contexts
         self.K = self.N = self.m = 0
         return self
 
@@ -239,18 +241,39 @@ class Context:
         host array (e.g. pinned) that receives x."""
         n = self.K + self.N
         b = self._in(b)
-        if x0 is None:
+        if x0 is None and not self._partitioned:
+            x0p = None  # NULL: the zero start, nothing transferred (gnw.h)
+        elif x0 is None:
             x0 = self._out(n, b)
             if self.device_pointers:
                 x0.zero_()
+            x0p = _dptr(x0)
         else:
             x0 = self._in(x0)
+            x0p = _dptr(x0)
         maxit = 2 * n if maxit is None else int(maxit)
         x = self._out(n, b) if out is None else self._check_out(out, n)
         he = np.zeros(hist_cap)
         hp = np.zeros(hist_cap)
         rep = A.Report(0, 0, 0.0, 0, he.ctypes.data, hp.ctypes.data, hist_cap)
-        A.check(self.L.gnw_minres_solve(self.h, _dptr(b), _dptr(x0), _dptr(x), tol, maxit, C.byref(rep)))
+        A.check(self.L.gnw_minres_solve(self.h, _dptr(b), x0p, _dptr(x), tol, maxit, C.byref(rep)))
+        nh = min(int(rep.n_hist), hist_cap)
+        return x, MinresReport(int(rep.iterations), he[:nh].copy(), hp[:nh].copy(), bool(rep.converged),
+                               float(rep.true_relative_residual))
+
+    def gn_step_solve(self, m, m_ref, g, g_obs, tol: float = 1e-8, maxit: int | None = None,
+                      hist_cap: int = 1 << 16, out=None):
+        """The reference's GN-step solve in one call (inversion.cpp:259-265): b = assemble_gn_rhs(...),
+        x0 = 0, minres(op, pc, b, x0, tol, maxit).  The right-hand side never leaves the device."""
+        n = self.K + self.N
+        m, m_ref, g, g_obs = (self._in(v) for v in (m, m_ref, g, g_obs))
+        maxit = 2 * n if maxit is None else int(maxit)
+        x = self._out(n, m) if out is None else self._check_out(out, n)
+        he = np.zeros(hist_cap)
+        hp = np.zeros(hist_cap)
+        rep = A.Report(0, 0, 0.0, 0, he.ctypes.data, hp.ctypes.data, hist_cap)
+        A.check(self.L.gnw_gn_step_solve(self.h, _dptr(m), _dptr(m_ref), _dptr(g), _dptr(g_obs), _dptr(x), tol, maxit,
+                                         C.byref(rep)))
         nh = min(int(rep.n_hist), hist_cap)
         return x, MinresReport(int(rep.iterations), he[:nh].copy(), hp[:nh].copy(), bool(rep.converged),
                                float(rep.true_relative_residual))

@@ -388,3 +388,20 @@ def test_prefetch_jacobian_partial_stage_same_bits(c1, monkeypatch):
     assert np.array_equal(H0, H1) and np.array_equal(L0, L1)
     assert r0.iterations == r1.iterations and np.array_equal(x0, x1) and np.array_equal(x0, x0b)
     ctx.close()
+
+
+def test_gn_step_solve_is_rhs_plus_minres(gpu_ctx_factory):
+    """gnw_gn_step_solve (inversion.cpp:259-265 in one call: rhs on the device, zero start not
+    transferred) against gnw_assemble_rhs + gnw_minres_solve with an explicit zero x0: bitwise."""
+    inp = W.gnstep_inputs(32, 8, 0)
+    ctx = gpu_ctx_factory(inp.mesh)
+    ctx.set_jacobian(inp.J, 1e-2)
+    zN, zm = np.zeros(inp.mesh.n_cells), np.zeros(8)
+    b = ctx.assemble_rhs(inp.dm, zN, inp.dg, zm)
+    x_ref, rep_ref = ctx.minres(b, x0=np.zeros_like(b), tol=1e-10)
+    x_null, rep_null = ctx.minres(b, tol=1e-10)  # x0 = NULL: the zero start without the operator pass
+    x_one, rep_one = ctx.gn_step_solve(inp.dm, zN, inp.dg, zm, tol=1e-10)
+    assert rep_ref.converged and rep_one.converged and rep_null.converged
+    assert rep_one.iterations == rep_ref.iterations == rep_null.iterations
+    assert np.array_equal(x_one, x_ref) and np.array_equal(x_null, x_ref)
+    assert np.array_equal(rep_one.relative_residuals, rep_ref.relative_residuals)
