@@ -117,24 +117,41 @@ class GnStepSolver {
     r.pnorm_relative_residuals = hp.data();
     r.hist_cap = he.size();
     throw_on(gnw_minres_solve(ctx_, b.data(), x0.data(), x.data(), tol, maxit, &r));
-    if (report) {
-      report->iterations = r.iterations;
-      report->converged = r.converged != 0;
-      report->true_relative_residual = r.true_relative_residual;
-      if (r.n_hist > he.size()) {
-        he.resize(r.n_hist);
-        hp.resize(r.n_hist);
-        throw_on(gnw_minres_history(ctx_, he.data(), hp.data(), he.size(), nullptr));
-      }
-      const std::size_t nh = std::min<std::size_t>(r.n_hist, he.size());
-      report->relative_residuals.assign(he.begin(), he.begin() + static_cast<std::ptrdiff_t>(nh));
-      report->pnorm_relative_residuals.assign(hp.begin(), hp.begin() + static_cast<std::ptrdiff_t>(nh));
-    }
+    if (report) fill_report(r, he, hp, report);
+    return x;
+  }
+  // The reference's GN-step solve as it appears in gauss_newton (inversion.cpp:259-265):
+  // b = assemble_gn_rhs(...), x0 = 0, minres(op, pc, b, x0, tol, maxit) -- one call, b stays
+  // on the device
+  std::vector<double> solve_gn_step(const std::vector<double>& m, const std::vector<double>& m_ref,
+                                    const std::vector<double>& g, const std::vector<double>& g_obs, double tol,
+                                    std::size_t maxit, MinresReport* report = nullptr) {
+    std::vector<double> x(K_ + N_);
+    std::vector<double> he(std::min<std::size_t>(maxit, 4095) + 1), hp(he.size());
+    gnw_report r{};
+    r.relative_residuals = he.data();
+    r.pnorm_relative_residuals = hp.data();
+    r.hist_cap = he.size();
+    throw_on(gnw_gn_step_solve(ctx_, m.data(), m_ref.data(), g.data(), g_obs.data(), x.data(), tol, maxit, &r));
+    if (report) fill_report(r, he, hp, report);
     return x;
   }
   gnw_ctx* handle() { return ctx_; }
 
  private:
+  void fill_report(const gnw_report& r, std::vector<double>& he, std::vector<double>& hp, MinresReport* report) {
+    report->iterations = r.iterations;
+    report->converged = r.converged != 0;
+    report->true_relative_residual = r.true_relative_residual;
+    if (r.n_hist > he.size()) {
+      he.resize(r.n_hist);
+      hp.resize(r.n_hist);
+      throw_on(gnw_minres_history(ctx_, he.data(), hp.data(), he.size(), nullptr));
+    }
+    const std::size_t nh = std::min<std::size_t>(r.n_hist, he.size());
+    report->relative_residuals.assign(he.begin(), he.begin() + static_cast<std::ptrdiff_t>(nh));
+    report->pnorm_relative_residuals.assign(hp.begin(), hp.begin() + static_cast<std::ptrdiff_t>(nh));
+  }
   void set_jacobian(const double* J, std::size_t m, double beta, WoodburyBuildTimings* timings) {
     gnw_timings t{};
     throw_on(gnw_set_jacobian(ctx_, J, m, N_, beta, &t));

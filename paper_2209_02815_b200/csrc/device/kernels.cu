@@ -767,7 +767,8 @@ template <int B>
 __global__ void __launch_bounds__(kTpb, B >= 16 ? 5 : 8) k_saddle(OperatorArgs op, VSel xs, int scaled, const double* __restrict__ u,
                                                  VSel ys, MinresState* st, int loop, int nb_edge,
                                                  double* part, unsigned* counter) {
-  griddep_wait();
+  // the operator's entries are fixed per assembly: their loads are issued BEFORE the
+  // grid-dependency wait, so they overlap the predecessor's drain (its last-block reduction)
   extern __shared__ double usm[];
   __shared__ double red[kTpb / 32];
   double dotv[1] = {0.0};
@@ -782,6 +783,7 @@ __global__ void __launch_bounds__(kTpb, B >= 16 ? 5 : 8) k_saddle(OperatorArgs o
       sell_load<5>(op.Qs, e, cq, vq);
       sell_load<2>(op.Dts, e, ct, vt);
     }
+    griddep_wait();
     const double* __restrict__ z = vsel(xs, st);
     double* __restrict__ y = vsel(ys, st);
     const double sc = scaled ? st->inv_gamma : 1.0;
@@ -815,6 +817,7 @@ __global__ void __launch_bounds__(kTpb, B >= 16 ? 5 : 8) k_saddle(OperatorArgs o
     int cd[3];
     double vd[3];
     if (fast) sell_load<3>(op.Ds, c, cd, vd);
+    griddep_wait();
     const double* __restrict__ z = vsel(xs, st);
     double* __restrict__ y = vsel(ys, st);
     const double sc = scaled ? st->inv_gamma : 1.0;
@@ -879,18 +882,26 @@ void saddle_operator(const OperatorArgs& op, VSel x, int scaled, const double* u
 __global__ void __launch_bounds__(kTpb) k_combine_elem(PrecArgs pa, VSel azs, VSel vcs, VSel vps, VSel vns,
                                                        VSel zns, int loop, const MinresState* st,
                                                        double* dots_part) {
-  griddep_wait();
   __shared__ double red[3 * (kTpb / 32)];
+  const long long n = pa.K + pa.N;
+  // two consecutive elements per thread, 16-byte loads (all vectors are separate allocations)
+  const long long i0 = 2 * (static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x);
+  // v_cur and v_prev (and the iteration index that selects their ring slots) were written before
+  // the predecessor (the operator) started: loaded BEFORE the grid-dependency wait, under the
+  // operator's last-block reduction
+  const double* __restrict__ vc = loop ? vsel(vcs, st) : nullptr;
+  const double* __restrict__ vp = loop ? vsel(vps, st) : nullptr;
+  double2 pb = make_double2(0.0, 0.0), pc = make_double2(0.0, 0.0);
+  if (loop && i0 + 1 < n) {
+    pb = *reinterpret_cast<const double2*>(vc + i0);
+    pc = *reinterpret_cast<const double2*>(vp + i0);
+  }
+  griddep_wait();
   const double* __restrict__ az = vsel(azs, st);
   double* __restrict__ vn = vsel(vns, st);
   double* __restrict__ zn = vsel(zns, st);
   const double c1 = loop ? st->coef_v1 : 0.0, c2 = loop ? st->coef_v2 : 0.0;
-  const double* __restrict__ vc = loop ? vsel(vcs, st) : nullptr;
-  const double* __restrict__ vp = loop ? vsel(vps, st) : nullptr;
   double d[3] = {0.0, 0.0, 0.0};  // <z, v>, <z, z>, <v, v>
-  const long long n = pa.K + pa.N;
-  // two consecutive elements per thread, 16-byte loads (all vectors are separate allocations)
-  const long long i0 = 2 * (static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x);
   auto one = [&](long long i, double a, double b, double c) {
     double v;
     if (loop) {
@@ -910,11 +921,7 @@ __global__ void __launch_bounds__(kTpb) k_combine_elem(PrecArgs pa, VSel azs, VS
   };
   if (i0 + 1 < n) {
     const double2 a = *reinterpret_cast<const double2*>(az + i0);
-    double2 b = make_double2(0.0, 0.0), c = make_double2(0.0, 0.0);
-    if (loop) {
-      b = *reinterpret_cast<const double2*>(vc + i0);
-      c = *reinterpret_cast<const double2*>(vp + i0);
-    }
+    const double2 b = pb, c = pc;
     const double v0 = one(i0, a.x, b.x, c.x);
     const double v1 = one(i0 + 1, a.y, b.y, c.y);
     if (loop) *reinterpret_cast<double2*>(vn + i0) = make_double2(v0, v1);
@@ -1231,18 +1238,18 @@ void capacitance_reduce(const double* parts, int P, int m, double beta, double* 
 // ======================================================================
 __device__ void update_tail(double rr, MinresState* st, double* hist_e, double* hist_p, long long hist_cap);
 
-__global__ void __launch_bounds__(kTpb) k_minres_update(long long n, VSel zs, VSel azs, VSel wps, VSel wcs, VSel wns,
-                                                        VSel ups, VSel ucs, VSel uns, double* __restrict__ x,
-                                                        double* __restrict__ r, MinresState* st,
-                                                        double* hist_e, double* hist_p, long long hist_cap,
-                                                        double* part, unsigned* counter,
-                                                        cudaGraphConditionalHandle handle, int use_cond) {
-  griddep_wait();
+__global__ void __launch_bounds__(kTpb, 4) k_minres_update(long long n, VSel zs, VSel azs, VSel wps, VSel wcs, VSel wns,
+                                                           VSel ups, VSel ucs, VSel uns, double* __restrict__ x,
+                                                           double* __restrict__ r, MinresState* st,
+                                                           double* hist_e, double* hist_p, long long hist_cap,
+                                                           double* part, unsigned* counter,
+                                                           cudaGraphConditionalHandle handle, int use_cond) {
   __shared__ double red[kTpb / 32];
-  if (use_cond != 2 && st->status != kRunning) {  // use_cond == 2: isolated timing, no loop control
-    if (use_cond == 1 && blockIdx.x == 0 && threadIdx.x == 0) cudaGraphSetConditional(handle, 0);
-    return;
-  }
+  // One pair of elements per thread (16-byte loads/stores).  Every vector this kernel reads
+  // (z_cur, A z, w, u, x, r) and the iteration index were written before the predecessor (the
+  // preconditioner's finish kernel) started; only the Givens scalars come from it.  All eight
+  // loads are therefore issued BEFORE the grid-dependency wait, under the finish kernel's
+  // last-block reduction.
   const double* __restrict__ z = vsel(zs, st);
   const double* __restrict__ az = vsel(azs, st);
   const double* __restrict__ wp = vsel(wps, st);
@@ -1251,31 +1258,40 @@ __global__ void __launch_bounds__(kTpb) k_minres_update(long long n, VSel zs, VS
   const double* __restrict__ up = vsel(ups, st);
   const double* __restrict__ uc = vsel(ucs, st);
   double* __restrict__ un = vsel(uns, st);
+  const long long np = n / 2;
+  auto ld2 = [](const double* p, long long k) { return *reinterpret_cast<const double2*>(p + 2 * k); };
+  const long long k = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  double2 zv, wpv, wcv, azv, upv, ucv, xv, rv;
+  zv = wpv = wcv = azv = upv = ucv = xv = rv = make_double2(0.0, 0.0);
+  if (k < np) {
+    zv = ld2(z, k), wpv = ld2(wp, k), wcv = ld2(wc, k), azv = ld2(az, k);
+    upv = ld2(up, k), ucv = ld2(uc, k), xv = ld2(x, k), rv = ld2(r, k);
+  }
+  griddep_wait();
+  if (use_cond != 2 && st->status != kRunning) {  // use_cond == 2: isolated timing, no loop control
+    if (use_cond == 1 && blockIdx.x == 0 && threadIdx.x == 0) cudaGraphSetConditional(handle, 0);
+    return;
+  }
   const double ig = st->inv_gamma, na3 = -st->alpha3, na2 = -st->alpha2, ia = st->inv_alpha1;
   const double tau = st->tau, ntau = -tau;
   double rr[1] = {0.0};
-  // minres.cpp:93-106 per element; pairs of elements with 16-byte loads/stores
-  auto elem = [&](double zv, double wpv, double wcv, double azv, double upv, double ucv, double xv, double rv,
+  // minres.cpp:93-106 per element
+  auto elem = [&](double zv_, double wpv_, double wcv_, double azv_, double upv_, double ucv_, double xv_, double rv_,
                   double& wo, double& uo, double& xo, double& ro) {
-    const double zh = zv * ig;
-    double w = zh + na3 * wpv;
-    w = w + na2 * wcv;
+    const double zh = zv_ * ig;
+    double w = zh + na3 * wpv_;
+    w = w + na2 * wcv_;
     w = w * ia;
-    double uu = azv + na3 * upv;
-    uu = uu + na2 * ucv;
+    double uu = azv_ + na3 * upv_;
+    uu = uu + na2 * ucv_;
     uu = uu * ia;
     wo = w;
     uo = uu;
-    xo = xv + tau * w;
-    ro = rv + ntau * uu;
+    xo = xv_ + tau * w;
+    ro = rv_ + ntau * uu;
     rr[0] = rr[0] + ro * ro;
   };
-  const long long np = n / 2;
-  auto ld2 = [](const double* p, long long k) { return *reinterpret_cast<const double2*>(p + 2 * k); };
-  for (long long k = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; k < np;
-       k += static_cast<long long>(gridDim.x) * blockDim.x) {
-    const double2 zv = ld2(z, k), wpv = ld2(wp, k), wcv = ld2(wc, k), azv = ld2(az, k), upv = ld2(up, k),
-                  ucv = ld2(uc, k), xv = ld2(x, k), rv = ld2(r, k);
+  if (k < np) {
     double2 wo, uo, xo, ro;
     elem(zv.x, wpv.x, wcv.x, azv.x, upv.x, ucv.x, xv.x, rv.x, wo.x, uo.x, xo.x, ro.x);
     elem(zv.y, wpv.y, wcv.y, azv.y, upv.y, ucv.y, xv.y, rv.y, wo.y, uo.y, xo.y, ro.y);
@@ -1338,7 +1354,7 @@ void update_tail_from_scratch(MinresState* st, double* hist_e, double* hist_p, l
 void minres_update(long long n, VSel z, VSel az, VSel wprev, VSel wcur, VSel wnext, VSel uprev, VSel ucur, VSel unext,
                    double* x, double* r, MinresState* st, double* hist_e, double* hist_p, long long hist_cap,
                    double* part, unsigned* counter, unsigned long long cond_handle, int use_cond, cudaStream_t s) {
-  const unsigned grid = std::min<unsigned>(grid_for((n + 1) / 2), 148u * 8u);
+  const unsigned grid = grid_for((n + 1) / 2);  // one pair per thread
   GNW_LAUNCH(launch_k(k_minres_update, grid, kTpb, 0, s, n, z, az, wprev, wcur, wnext, uprev, ucur, unext, x, r, st, hist_e, hist_p,
                                         hist_cap, part, counter,
                                         static_cast<cudaGraphConditionalHandle>(cond_handle), use_cond));
