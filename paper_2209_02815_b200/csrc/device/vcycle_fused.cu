@@ -218,60 +218,6 @@ __global__ void __launch_bounds__(256) k_mvcf_up_rows(DCsr S, DCsr T, const doub
     dst[0] = tile[2 * h][cq];
 }
 
-// the same with 4 columns per thread (two 16-byte gathers per entry behind one index / value
-// load): short rows (level 0: 4 + 5 entries) leave each thread few loads in flight, and the
-// entry loads are amortised over twice the data.  CTA = 8 rows x 128 columns.
-__global__ void __launch_bounds__(256) k_mvcf_up_rows4(DCsr S, DCsr T, const double* __restrict__ r,
-                                                       const double* __restrict__ ec, double* __restrict__ ht,
-                                                       long long ldh, int b) {
-  griddep_wait();
-  __shared__ double tile[8][129];
-  const int ty = threadIdx.y, lane = threadIdx.x;
-  const int i0 = blockIdx.x * 8, i = i0 + ty;
-  const int qb = blockIdx.y * 128, q = qb + 4 * lane;
-  if (i < S.n_rows && q < b) {
-    double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0, t0 = 0.0, t1 = 0.0, t2 = 0.0, t3 = 0.0;
-    const int a0 = S.rowptr[i], a1 = S.rowptr[i + 1];
-#pragma unroll 4
-    for (int k = a0; k < a1; ++k) {
-      const double* p = r + static_cast<long long>(__ldg(&S.cols[k])) * b + q;
-      const double2 x = ld2(p), y = ld2(p + 2);
-      const double v = __ldg(&S.vals[k]);
-      s0 = s0 + v * x.x;
-      s1 = s1 + v * x.y;
-      s2 = s2 + v * y.x;
-      s3 = s3 + v * y.y;
-    }
-    const int b0 = T.rowptr[i], b1 = T.rowptr[i + 1];
-#pragma unroll 4
-    for (int k = b0; k < b1; ++k) {
-      const double* p = ec + static_cast<long long>(__ldg(&T.cols[k])) * b + q;
-      const double2 x = ld2(p), y = ld2(p + 2);
-      const double v = __ldg(&T.vals[k]);
-      t0 = t0 + v * x.x;
-      t1 = t1 + v * x.y;
-      t2 = t2 + v * y.x;
-      t3 = t3 + v * y.y;
-    }
-    tile[ty][4 * lane] = s0 + t0;
-    tile[ty][4 * lane + 1] = s1 + t1;
-    tile[ty][4 * lane + 2] = s2 + t2;
-    tile[ty][4 * lane + 3] = s3 + t3;
-  }
-  __syncthreads();
-  // 128 columns x 2 half-rows: thread t writes rows 4h .. 4h + 3 of column t / 2 (a 32-byte run)
-  const int t = ty * 32 + lane, cq = t >> 1, h = t & 1;
-  const int qq = qb + cq, rr = i0 + 4 * h;
-  if (qq >= b || rr >= S.n_rows) return;
-  double* dst = ht + static_cast<long long>(qq) * ldh + rr;
-  if (rr + 3 < S.n_rows) {
-    *reinterpret_cast<double2*>(dst) = make_double2(tile[4 * h][cq], tile[4 * h + 1][cq]);
-    *reinterpret_cast<double2*>(dst + 2) = make_double2(tile[4 * h + 2][cq], tile[4 * h + 3][cq]);
-  } else {
-    for (int u = 0; u < 4 && rr + u < S.n_rows; ++u) dst[u] = tile[4 * h + u][cq];
-  }
-}
-
 }  // namespace
 
 #define GNW_F_DISPATCH(G, KERNEL, ROWS, ...)                                                                        \
@@ -328,17 +274,6 @@ void mvcf_restrict(const DLevel& L, const double* r, double* rc, int b, cudaStre
 }
 bool mvcf_up(const DLevel& L, const double* r, const double* ec, double* out, int b, double* ht, long long ldh,
              cudaStream_t s) {
-  static const int wide = [] {  // env GNW_MVCF_V=1: 2 columns per thread everywhere
-    const char* e = std::getenv("GNW_MVCF_V");
-    return e ? std::atoi(e) : 2;
-  }();
-  if (ht != nullptr && wide >= 2 && b % 128 == 0 && ldh % 2 == 0 && L.n >= 65536 &&
-      static_cast<long long>(L.S.nnz) + L.T.nnz <= 12LL * L.n) {
-    const dim3 grid((L.n + 7) / 8, b / 128);
-    GNW_LAUNCH(launch_k(k_mvcf_up_rows4, grid, dim3(32, 8), 0, s, L.S, L.T, r, ec, ht, ldh, b));
-    note_launch("mvcf_up_rows4");
-    return true;
-  }
   if (ht != nullptr && b % 2 == 0 && ldh % 2 == 0) {
     const dim3 grid((L.n + 7) / 8, (b + 63) / 64);
     GNW_LAUNCH(launch_k(k_mvcf_up_rows, grid, dim3(32, 8), 0, s, L.S, L.T, r, ec, ht, ldh, b));
