@@ -155,7 +155,12 @@ gnw_status gnw_set_preconditioner(gnw_ctx* ctx, int kind);
  * Both keep C t' = t backward stable with one refinement step on the explicit C^-1.
  * GNW_LOOP_AUTO (default): for solves with tol >= 1e-8, lean when a sweep over J moves more
  * bytes than two V-cycles (else fused); the reference schedule below 1e-8. */
-enum { GNW_LOOP_REFERENCE = 0, GNW_LOOP_FUSED = 1, GNW_LOOP_AUTO = 2, GNW_LOOP_LEAN = 3 };
+enum { GNW_LOOP_REFERENCE = 0, GNW_LOOP_FUSED = 1, GNW_LOOP_AUTO = 2, GNW_LOOP_LEAN = 3, GNW_LOOP_PERSISTENT = 4 };
+/* GNW_LOOP_PERSISTENT: the lean schedule's arithmetic with the whole loop in ONE persistent
+ * cooperative kernel (grid barriers instead of kernel boundaries), for problems whose working
+ * set is L2-resident (BASELINE C1).  Falls back to GNW_LOOP_LEAN when the problem is not
+ * eligible (m > 64, working set above ~96 MB, exact coarse mode, partitioned).  GNW_LOOP_AUTO
+ * picks it by itself for eligible problems at tol >= 1e-8 (env GNW_PERSISTENT=0: never). */
 gnw_status gnw_set_loop_mode(gnw_ctx* ctx, int mode);
 
 gnw_status gnw_assemble(gnw_ctx* ctx, const gnw_mesh* mesh, const gnw_amg_options* opts);
@@ -292,6 +297,7 @@ typedef struct gnw_stats {
   uint64_t loop_restarts;   /* fused-loop solves restarted on the reference schedule (lifetime) */
   uint64_t fused_iterations; /* of the last solve's iterations, run on the fused or lean schedule */
   uint64_t lean_iterations;  /* of those, on the lean schedule */
+  uint64_t persistent_iterations; /* of those, inside the persistent kernel (GNW_LOOP_PERSISTENT) */
   uint64_t comm_calls;       /* partitioned: exchanges this rank issued in the last solve */
   double comm_bytes;         /* partitioned: bytes this rank sent in them */
 } gnw_stats;

@@ -17,7 +17,7 @@ LIB_PATH = os.path.join(HERE, "libgnw.so")
 GNW_OK, GNW_INVALID_ARGUMENT, GNW_NUMERICAL, GNW_DEVICE = 0, 1, 2, 3
 GNW_HOST_POINTERS, GNW_DEVICE_POINTERS = 0, 1
 GNW_COARSE_INVERSE, GNW_COARSE_CHOLESKY = 0, 1
-GNW_LOOP_REFERENCE, GNW_LOOP_FUSED, GNW_LOOP_AUTO, GNW_LOOP_LEAN = 0, 1, 2, 3
+GNW_LOOP_REFERENCE, GNW_LOOP_FUSED, GNW_LOOP_AUTO, GNW_LOOP_LEAN, GNW_LOOP_PERSISTENT = 0, 1, 2, 3, 4
 
 
 class GnwDeviceError(RuntimeError):
@@ -64,7 +64,8 @@ class Stats(C.Structure):
     _fields_ = [("t_minres", C.c_double), ("t_rhs", C.c_double),
                 ("kernel_launches", C.c_uint64), ("setup_kernel_launches", C.c_uint64),
                 ("loop_restarts", C.c_uint64), ("fused_iterations", C.c_uint64),
-                ("lean_iterations", C.c_uint64), ("comm_calls", C.c_uint64), ("comm_bytes", C.c_double)]
+                ("lean_iterations", C.c_uint64), ("persistent_iterations", C.c_uint64), ("comm_calls", C.c_uint64),
+                ("comm_bytes", C.c_double)]
 
 
 # every symbol include/gnw.h declares (checked by tests/test_capi_symbols.py)

@@ -1,5 +1,6 @@
 // amg_device.cu -- device SA-AMG hierarchy and V-cycle orchestration (amg.cpp:90-111).
 #include "amg_device.cuh"
+#include "minres_persistent.cuh"
 #include "sparse_device.cuh"
 
 #include <algorithm>
@@ -195,6 +196,19 @@ void DeviceAmg::upload(const host::AmgHierarchy& h, cudaStream_t s, int min_coll
     }
   if (const char* e = std::getenv("GNW_VC_COLLAPSE"))
     if (std::atoi(e) == 0) stop = static_cast<int>(L) - 1;
+  // Small hierarchies (candidates for the persistent MINRES kernel, minres_persistent.cu) also
+  // get a SECOND, deeper dense tail: every pass of that kernel streams the tail's matrix from L2
+  // (34 MB at C1's level 1), while a level of grid barriers costs ~4 us -- so its tail starts at
+  // the first level with <= 640 rows (C1: level 2, 2 MB), and the levels in between get their
+  // one-pass operators too.
+  pstop_ = -1;
+  if (fused_on && stop < static_cast<int>(L) - 1 && h.levels[0].A.n_rows <= 65536 && h.levels[stop].A.n_rows > 640)
+    for (int l = stop + 1; l + 1 < static_cast<int>(L); ++l)
+      if (h.levels[l].A.n_rows <= 640) {
+        pstop_ = l;
+        break;
+      }
+  const int fused_stop = pstop_ > stop ? pstop_ : stop;
   fused_ = false;
   const bool timing = [] {
     const char* e = std::getenv("GNW_SETUP_TIMING");
@@ -235,7 +249,7 @@ void DeviceAmg::upload(const host::AmgHierarchy& h, cudaStream_t s, int min_coll
       d.wd = mem_.alloc<double>(wd.size());
       GNW_CUDA_CHECK(cudaMemcpyAsync(d.wd, wd.data(), wd.size() * sizeof(double), cudaMemcpyHostToDevice, s));
       GNW_CUDA_CHECK(cudaStreamSynchronize(s));
-      if (fused_on && static_cast<int>(l) < stop) {
+      if (fused_on && static_cast<int>(l) < fused_stop) {
         fused_ = true;  // levels above the dense tail (vcycle_fused.cu)
         auto tc = now();
         const char* le = std::getenv("GNW_VC_LELL");  // experiment switch: 0 keeps the CSR loops
@@ -311,19 +325,7 @@ void DeviceAmg::upload(const host::AmgHierarchy& h, cudaStream_t s, int min_coll
 // (10.5 MB, L2-resident) applied by one warp-per-row launch.  M is formed once per
 // hierarchy by running the sub-cycle on the unit vectors.  Default mode only: the exact
 // mode keeps the reference's level-by-level order.  Env GNW_VC_COLLAPSE=0 disables it.
-void DeviceAmg::build_collapse(cudaStream_t s) {
-  collapse_l_ = -1;
-  collapse_M_ = nullptr;
-  if (const char* e = std::getenv("GNW_VC_COLLAPSE"))
-    if (std::atoi(e) == 0) return;
-  const int L = static_cast<int>(lv_.size());
-  int lc = -1;
-  for (int l = min_collapse_; l < L - 1; ++l)
-    if (lv_[l].n <= collapse_max()) {
-      lc = l;
-      break;
-    }
-  if (lc < 0) return;
+double* DeviceAmg::collapse_matrix(int lc, cudaStream_t s) {
   const int n = lv_[lc].n;
   DeviceMemory tmp;
   double* I = tmp.alloc<double>(static_cast<size_t>(n) * n);
@@ -331,9 +333,35 @@ void DeviceAmg::build_collapse(cudaStream_t s) {
   identity_rows(I, n, s);
   for (int j = 0; j < n; ++j)  // row j of MT = sub-cycle(e_j) = column j of M
     cycle_levels(lc, vfixed(I + static_cast<size_t>(j) * n), MT + static_cast<size_t>(j) * n, nullptr, 0, false, s);
-  collapse_M_ = mem_.alloc<double>(static_cast<size_t>(n) * n);
-  transpose_square(MT, collapse_M_, n, s);
+  double* M = mem_.alloc<double>(static_cast<size_t>(n) * n);
+  transpose_square(MT, M, n, s);
   GNW_CUDA_CHECK(cudaStreamSynchronize(s));
+  return M;
+}
+
+void DeviceAmg::build_collapse(cudaStream_t s) {
+  collapse_l_ = -1;
+  collapse_M_ = nullptr;
+  pcollapse_M_ = nullptr;
+  if (const char* e = std::getenv("GNW_VC_COLLAPSE"))
+    if (std::atoi(e) == 0) {
+      pstop_ = -1;
+      return;
+    }
+  const int L = static_cast<int>(lv_.size());
+  int lc = -1;
+  for (int l = min_collapse_; l < L - 1; ++l)
+    if (lv_[l].n <= collapse_max()) {
+      lc = l;
+      break;
+    }
+  if (lc < 0) {
+    pstop_ = -1;
+    return;
+  }
+  // collapse_l_ stays -1 while the matrices are formed: cycle_levels then runs every level
+  if (pstop_ > lc) pcollapse_M_ = collapse_matrix(pstop_, s);
+  collapse_M_ = collapse_matrix(lc, s);
   collapse_l_ = lc;
 }
 
@@ -361,6 +389,31 @@ void DeviceAmg::cycle_levels(int l0, VSel r, double* out, const MinresState* st,
     vc_up1(lev, at(l), ve_[l + 1], vx_[l], st, s);
     vc_up2(lev, at(l), vx_[l], l == l0 ? out : ve_[l], st, s);
   }
+}
+
+bool DeviceAmg::fill_persist(PersistArgs& a) const {
+  if (lv_.empty() || (!fused_ && lv_.size() > 1)) return false;
+  const int L = static_cast<int>(lv_.size());
+  const bool deep = pstop_ > 0 && pcollapse_M_ != nullptr;  // the persistent kernel's own, deeper tail
+  const int stop = deep ? pstop_ : (collapse_l_ >= 0 ? collapse_l_ : L - 1);
+  if (stop > kPersistMaxLevels) return false;
+  for (int l = 0; l < stop; ++l) {
+    const DLevel& d = lv_[l];
+    if (!d.fused || !d.Sl.words || !d.Tl.words || !d.Ttl.words) return false;
+    a.S[l] = d.Sl;
+    a.T[l] = d.Tl;
+    a.Tt[l] = d.Ttl;
+    a.gS[l] = d.gS;
+    a.gTt[l] = d.gTt;
+  }
+  for (int l = 1; l <= stop; ++l) {
+    a.vr[l] = vr_[l];
+    a.ve[l] = ve_[l];
+  }
+  a.nlev = stop;
+  a.M = deep ? pcollapse_M_ : (collapse_l_ >= 0 ? collapse_M_ : coarse_inv_);
+  a.nM = lv_[stop].n;
+  return a.M != nullptr;
 }
 
 // Level l as launched: the reference-order (thread-per-row) kernels everywhere in

@@ -79,6 +79,9 @@ class DeviceAmg {
   double* batch_out() const { return bX0_; }
 
   int collapse_level() const { return collapse_l_; }
+  // the V-cycle part of the persistent MINRES kernel's arguments (one-pass lane-ELL levels above
+  // the dense tail); false when a level has no lane-ELL copy or there are too many levels
+  bool fill_persist(struct PersistArgs& a) const;
   bool fused() const { return fused_; }
   // the dense collapsed tail starts at the first level with at most this many rows (env
   // GNW_VC_COLLAPSE_MAX, default 3072); the dense map is L2-resident up to that (72 MB)
@@ -90,11 +93,14 @@ class DeviceAmg {
   // collapse_l_ down are replaced by the dense operator collapse_M_ (default mode only).
   void cycle_levels(int l0, VSel r, double* out, const MinresState* st, int exact, bool collapse, cudaStream_t s);
   void build_collapse(cudaStream_t s);
+  double* collapse_matrix(int lc, cudaStream_t s);  // the sub-cycle from level lc as one dense matrix
 
   bool fused_ = false;             // fused per-level operators built (vcycle_fused.cu)
   int min_collapse_ = 1;
   int collapse_l_ = -1;           // first level with n <= kCollapseMax above the coarsest, or -1
   double* collapse_M_ = nullptr;  // n x n row-major: column j = the sub-cycle applied to e_j
+  int pstop_ = -1;                // the persistent kernel's deeper tail level (small hierarchies), or -1
+  double* pcollapse_M_ = nullptr;
   DeviceMemory mem_;
   std::vector<DLevel> lv_;
   double* coarse_inv_ = nullptr;

@@ -205,6 +205,9 @@ void Context::finish_assembly() {
     dq_ = nullptr;
     pa_.m = 0;
     mem_.release_all();
+    ppart_ = ptpart_ = nullptr;
+    pbar_ = nullptr;
+    ppart_m_ = 0;
     st_ = mem_.alloc<MinresState>(1);
     st_plain_ = mem_.alloc<MinresState>(1);
     counters_ = mem_.alloc<unsigned>(16);
@@ -338,6 +341,9 @@ void Context::assemble_amg_csr(int64_t n, const int64_t* rowptr, const int64_t* 
     dq_ = nullptr;
     pa_.m = 0;
     mem_.release_all();
+    ppart_ = ptpart_ = nullptr;
+    pbar_ = nullptr;
+    ppart_m_ = 0;
     st_ = mem_.alloc<MinresState>(1);
     st_plain_ = mem_.alloc<MinresState>(1);
     counters_ = mem_.alloc<unsigned>(16);
@@ -769,6 +775,27 @@ int Context::loop_sched() const {
   return 8.0 * static_cast<double>(m_) * static_cast<double>(N_) > 2.0 * vcycle_bytes() ? 2 : 1;
 }
 
+// The persistent cooperative kernel (minres_persistent.cu) runs the lean schedule's arithmetic
+// for problems whose working set stays in L2: requested (GNW_LOOP_PERSISTENT) or picked by
+// GNW_LOOP_AUTO (env GNW_PERSISTENT=0: never).
+bool Context::persistent_eligible() const {
+  static const bool env_on = [] {
+    const char* e = std::getenv("GNW_PERSISTENT");
+    return !(e && std::atoi(e) == 0);
+  }();
+  if (persist_mode_ == 0 || (persist_mode_ == 1 && !env_on)) return false;
+  if (comm_ || no_graph_ || coarse_mode != 0 || pc_laplace || loop_sched() == 0) return false;
+  if (m_ < 1 || m_ > persistent_max_m() || pa_.cap_tri || !cinv_refine_ || dC_ == nullptr || dq_ == nullptr || bq_ == nullptr)
+    return false;
+  if (op_.Qs.width <= 0 || op_.Dts.width <= 0 || op_.Ds.width <= 0) return false;
+  PersistArgs probe;
+  if (!damg_.fill_persist(probe)) return false;
+  // the vectors, J, H and the dense tail together must stay L2-resident (B200: 126 MB)
+  const double bytes = 16.0 * static_cast<double>(m_) * static_cast<double>(N_) + 8.0 * 20.0 * static_cast<double>(K_ + N_) +
+                       8.0 * static_cast<double>(probe.nM) * probe.nM;
+  return bytes <= 96e6;
+}
+
 void Context::apply_operator(const double* x, double* y) {
   require_mixed();
   require_device();
@@ -1171,7 +1198,70 @@ MinresResult Context::minres(const double* b, const double* x0, double* x, doubl
     }
     return graph_exec_[slot];
   };
-  if (!host_loop) ensure_graph();
+  // the persistent kernel replaces the graph loop while the fast schedules are active
+  uint64_t persist_iters = 0;
+  auto run_persistent = [&]() -> bool {
+    if (!persistent_eligible()) return false;
+    PersistArgs a;
+    if (!damg_.fill_persist(a)) return false;
+    const int nb = sm_count_;
+    if (ppart_ == nullptr || ppart_m_ < static_cast<int>(m_)) {
+      ppart_ = mem_.alloc<double>(static_cast<size_t>(nb) * 8);
+      ptpart_ = mem_.alloc<double>(static_cast<size_t>(nb) * static_cast<size_t>(persistent_max_m()));
+      pbar_ = mem_.alloc<unsigned>(4);
+      ppart_m_ = persistent_max_m();
+    }
+    a.op = op_;
+    a.K = K_;
+    a.N = N_;
+    a.m = static_cast<int>(m_);
+    a.qinv = pa_.qinv;
+    a.Ht = pa_.Ht;
+    a.ldh = pa_.ldh;
+    a.J = dJ_;
+    a.ldj = ldj_;
+    a.Cinv = pa_.Cinv;
+    a.Cfull = dC_;
+    a.neg_inv_beta = pa_.neg_inv_beta;
+    for (int k = 0; k < 3; ++k) {
+      a.V[k] = V_[k];
+      a.W[k] = W_[k];
+      a.U[k] = U_[k];
+    }
+    a.Z[0] = Z_[0];
+    a.Z[1] = Z_[1];
+    a.az = az_;
+    a.x = x_;
+    a.r = r_;
+    a.bq = bq_;
+    a.dq = dq_;
+    a.st = st_;
+    a.hist_e = hist_e_;
+    a.hist_p = hist_p_;
+    a.hist_cap = hist_cap_;
+    a.part = ppart_;
+    a.tpart = ptpart_;
+    a.bar = pbar_;
+    a.max_iters = 1 << 20;
+    static const bool prof = [] {  // env GNW_PERSIST_PROFILE=1: phase times of CTA 0 on stderr
+      const char* e = std::getenv("GNW_PERSIST_PROFILE");
+      return e && std::atoi(e) != 0;
+    }();
+    if (!prof) return launch_minres_persistent(a, sm_count_, s);
+    unsigned long long* dprof = nullptr;
+    GNW_CUDA_CHECK(cudaMalloc(&dprof, 8 * sizeof(unsigned long long)));
+    GNW_CUDA_CHECK(cudaMemsetAsync(dprof, 0, 8 * sizeof(unsigned long long), s));
+    a.prof = dprof;
+    const bool ok = launch_minres_persistent(a, sm_count_, s);
+    unsigned long long hp[8];
+    GNW_CUDA_CHECK(cudaMemcpyAsync(hp, dprof, sizeof hp, cudaMemcpyDeviceToHost, s));
+    sync();
+    cudaFree(dprof);
+    std::fprintf(stderr, "[gnw persistent] ns per phase (whole launch): B %llu, C %llu, restrict %llu, dense %llu, up+dots %llu, "
+                         "F+A %llu, tail %llu\n", hp[0], hp[1], hp[2], hp[3], hp[4], hp[5], hp[6]);
+    return ok;
+  };
+  if (!host_loop && !persistent_eligible()) ensure_graph();
   std::vector<std::pair<uint64_t, double>> overrides;  // verified residuals replace recurred ones
   auto true_residual_rel = [&](double* rout) {
     operator_into(vfixed(x_), 0, vfixed(tmp2_), st_plain_, 0);
@@ -1190,6 +1280,13 @@ MinresResult Context::minres(const double* b, const double* x0, double* x, doubl
       GNW_CUDA_CHECK(cudaMemcpyAsync(h_st_, st_, sizeof(MinresState), cudaMemcpyDeviceToHost, s));
       sync();
       if (h_st_->status == kRunning) continue;
+    } else if (h_st_->status == kRunning && run_persistent()) {
+      const long long it0 = h_st_->iterations;
+      GNW_CUDA_CHECK(cudaMemcpyAsync(h_st_, st_, sizeof(MinresState), cudaMemcpyDeviceToHost, s));
+      sync();
+      const uint64_t done_now = static_cast<uint64_t>(h_st_->iterations - it0);
+      persist_iters += done_now;
+      sched_iters[2] += done_now;  // the lean schedule's arithmetic
     } else if (h_st_->status == kRunning) {
       const long long it0 = h_st_->iterations;
       const cudaGraphExec_t ge = ensure_graph();
@@ -1268,6 +1365,7 @@ MinresResult Context::minres(const double* b, const double* x0, double* x, doubl
   last_iterations = res.iterations;
   for (int k = 0; k < 3; ++k) last_sched_iters_[k] = std::min<uint64_t>(sched_iters[k], res.iterations);
   last_fused_iters_ = last_sched_iters_[1] + last_sched_iters_[2];
+  last_persist_iters_ = std::min<uint64_t>(persist_iters, res.iterations);
   const uint64_t nh = std::min<uint64_t>(res.iterations + 1, static_cast<uint64_t>(hist_cap_));
   std::vector<double> he(nh), hp(nh);
   GNW_CUDA_CHECK(cudaMemcpyAsync(he.data(), hist_e_, nh * sizeof(double), cudaMemcpyDeviceToHost, s));

@@ -12,6 +12,7 @@
 #include "../host/setup.hpp"
 #include "amg_device.cuh"
 #include "sparse_device.cuh"
+#include "minres_persistent.cuh"
 #include "comm.cuh"
 #include "ert_gmg.cuh"
 #include "ert_kernels.cuh"
@@ -72,7 +73,14 @@ class Context {
   static constexpr double kAutoFusedTol = 1e-8;
   int auto_sched_ = 0;  // schedule auto picks: 0 by sweep vs V-cycle bytes, 1 fused, 2 lean (env GNW_AUTO_SCHED)
   double vcycle_bytes() const;
-  void set_fused(int mode) { fused_ = mode; }
+  // mode 4 (GNW_LOOP_PERSISTENT): lean arithmetic inside the persistent kernel when eligible
+  void set_fused(int mode) {
+    persist_mode_ = mode == 4 ? 2 : (mode == 2 ? 1 : 0);
+    fused_ = mode == 4 ? 3 : mode;
+  }
+  int persist_mode_ = 1;  // 0 never, 1 auto (with GNW_LOOP_AUTO), 2 requested
+  bool persistent_eligible() const;
+  uint64_t last_persist_iters_ = 0;
   int fused() const { return fused_; }
   uint64_t loop_restarts = 0;  // fused-loop solves restarted on the reference schedule
   void set_coarse(int mode) {
@@ -104,6 +112,9 @@ class Context {
   double event_elapsed(int a, int b);
   void profile_kernel(int kernel, int reps, double* seconds, double* algorithmic);
   uint64_t last_iterations = 0;
+  double *ppart_ = nullptr, *ptpart_ = nullptr;  // persistent kernel: partial sums
+  unsigned* pbar_ = nullptr;                     // and its grid-barrier counter
+  int ppart_m_ = 0;
   uint64_t last_fused_iters_ = 0;  // of last_iterations, run on the fused or lean schedule
   uint64_t last_sched_iters_[3] = {0, 0, 0};  // of last_iterations, per schedule (reference, fused, lean)
 

@@ -123,7 +123,8 @@ gnw_status gnw_set_preconditioner(gnw_ctx* ctx, int kind) {
 gnw_status gnw_set_loop_mode(gnw_ctx* ctx, int mode) {
   return guard([&] {
     if (mode != GNW_LOOP_REFERENCE && mode != GNW_LOOP_FUSED && mode != GNW_LOOP_AUTO &&
-        mode != GNW_LOOP_LEAN) throw std::invalid_argument("gnw_set_loop_mode: bad mode");
+        mode != GNW_LOOP_LEAN && mode != GNW_LOOP_PERSISTENT)
+      throw std::invalid_argument("gnw_set_loop_mode: bad mode");
     ctx_of(ctx).set_fused(mode);
   });
 }
@@ -530,6 +531,7 @@ gnw_status gnw_get_stats(const gnw_ctx* ctx, gnw_stats* stats) {
     stats->loop_restarts = c.loop_restarts;
     stats->fused_iterations = c.last_fused_iters_;
     stats->lean_iterations = c.last_sched_iters_[2];
+    stats->persistent_iterations = c.last_persist_iters_;
     stats->comm_calls = c.comm_calls();
     stats->comm_bytes = c.comm_bytes();
   });

@@ -1236,7 +1236,6 @@ void capacitance_reduce(const double* parts, int P, int m, double beta, double* 
 // ======================================================================
 // MINRES vector recurrences (minres.cpp:93-106) and loop control
 // ======================================================================
-__device__ void update_tail(double rr, MinresState* st, double* hist_e, double* hist_p, long long hist_cap);
 
 __global__ void __launch_bounds__(kTpb, 4) k_minres_update(long long n, VSel zs, VSel azs, VSel wps, VSel wcs, VSel wns,
                                                            VSel ups, VSel ucs, VSel uns, double* __restrict__ x,
@@ -1312,33 +1311,6 @@ __global__ void __launch_bounds__(kTpb, 4) k_minres_update(long long n, VSel zs,
   }
   update_tail(tot[0], st, hist_e, hist_p, hist_cap);
   if (use_cond == 1) cudaGraphSetConditional(handle, st->status == kRunning ? 1u : 0u);
-}
-
-// minres.cpp:93-148 after the vector updates: history, convergence / exhaustion, rotation, j++
-__device__ void update_tail(double rr, MinresState* st, double* hist_e, double* hist_p, long long hist_cap) {
-  const long long j = st->j;
-  const double rel = sqrt(rr) / st->bnorm;
-  st->iterations = j;
-  st->rel = rel;
-  if (j < hist_cap) {
-    hist_e[j] = rel;
-    hist_p[j] = fabs(st->eta) / st->gamma1;
-  }
-  if (rel <= st->tol) {
-    st->status = kVerify;
-  } else if (st->gamma_next <= st->exhausted_tol) {
-    st->status = kExhausted;
-  } else {
-    st->gamma_prev = st->gamma_cur;
-    st->gamma_cur = st->gamma_next;
-    st->c_prev = st->c_cur;
-    st->c_cur = st->c_next;
-    st->s_prev = st->s_cur;
-    st->s_cur = st->s_next;
-    st->inv_gamma = 1.0 / st->gamma_cur;
-    st->j = j + 1;
-    if (j + 1 > st->maxit) st->status = kMaxit;
-  }
 }
 
 __global__ void k_update_tail_from_scratch(MinresState* st, double* hist_e, double* hist_p, long long hist_cap) {

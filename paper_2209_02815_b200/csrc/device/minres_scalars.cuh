@@ -53,4 +53,31 @@ __device__ __forceinline__ void finish_scalars(const double (&tot)[3], const dou
   givens_step(gsq, zz, vv, st);
 }
 
+// minres.cpp:93-148 after the vector updates: history, convergence / exhaustion, rotation, j++
+__device__ __forceinline__ void update_tail(double rr, MinresState* st, double* hist_e, double* hist_p, long long hist_cap) {
+  const long long j = st->j;
+  const double rel = sqrt(rr) / st->bnorm;
+  st->iterations = j;
+  st->rel = rel;
+  if (j < hist_cap) {
+    hist_e[j] = rel;
+    hist_p[j] = fabs(st->eta) / st->gamma1;
+  }
+  if (rel <= st->tol) {
+    st->status = kVerify;
+  } else if (st->gamma_next <= st->exhausted_tol) {
+    st->status = kExhausted;
+  } else {
+    st->gamma_prev = st->gamma_cur;
+    st->gamma_cur = st->gamma_next;
+    st->c_prev = st->c_cur;
+    st->c_cur = st->c_next;
+    st->s_prev = st->s_cur;
+    st->s_cur = st->s_next;
+    st->inv_gamma = 1.0 / st->gamma_cur;
+    st->j = j + 1;
+    if (j + 1 > st->maxit) st->status = kMaxit;
+  }
+}
+
 }  // namespace gnw

@@ -13,6 +13,7 @@
 #include <cstdlib>
 
 #include "kernels.cuh"
+#include "lell.cuh"
 
 namespace gnw {
 
@@ -33,13 +34,6 @@ __device__ __forceinline__ double grow(const DCsr& A, int i, int sub, bool valid
   }
   return acc;
 }
-template <int G>
-__device__ __forceinline__ double gsum(double acc) {
-#pragma unroll
-  for (int o = G / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-  return acc;
-}
-
 template <int G>
 __global__ void __launch_bounds__(kTpbF) k_vcf_restrict(DCsr Tt, VSel rs, const MinresState* st,
                                                         double* __restrict__ rc) {
@@ -66,32 +60,7 @@ __global__ void __launch_bounds__(kTpbF) k_vcf_up(DCsr S, DCsr T, VSel rs, const
 }
 
 
-// ---------------------------------------------- lane-ELL levels with coded values (DLell)
-// One batch of four lane entries: the four words are loaded together, then the table look-ups
-// and gathers are issued together, then the products are added in entry order (padding, which
-// has the sign bit set, is skipped).
-struct LellBatch {
-  unsigned w[4];
-  __device__ __forceinline__ void load(const unsigned* __restrict__ p, int k, int width) {
-#pragma unroll
-    for (int u = 0; u < 4; ++u) w[u] = k + u < width ? __ldg(p + 32 * (k + u)) : 0xffffffffu;
-  }
-  template <class F>
-  __device__ __forceinline__ double add(const DLell& A, double acc, F f) const {
-    double v[4], x[4];
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const bool ok = static_cast<int>(w[u]) >= 0;
-      v[u] = ok ? __ldg(A.table + (w[u] >> A.shift)) : 0.0;
-      x[u] = ok ? f(static_cast<int>(w[u] & A.mask)) : 0.0;
-    }
-#pragma unroll
-    for (int u = 0; u < 4; ++u)
-      if (static_cast<int>(w[u]) >= 0) acc = acc + v[u] * x[u];
-    return acc;
-  }
-};
-
+// ---------------------------------------------- lane-ELL levels with coded values (DLell, lell.cuh)
 template <int G>
 __global__ void __launch_bounds__(kTpbF) k_vcl_restrict(DLell Tt, VSel rs, const MinresState* st,
                                                         double* __restrict__ rc) {

@@ -113,12 +113,15 @@ class Context:
         over J; True / "fused" = one sweep (Woodbury identity); "auto" (the default) = fused
         for tol >= 1e-8, reference below."""
         modes = {False: A.GNW_LOOP_REFERENCE, True: A.GNW_LOOP_FUSED, "reference": A.GNW_LOOP_REFERENCE,
-                 "fused": A.GNW_LOOP_FUSED, "auto": A.GNW_LOOP_AUTO, "lean": A.GNW_LOOP_LEAN}
+                 "fused": A.GNW_LOOP_FUSED, "auto": A.GNW_LOOP_AUTO, "lean": A.GNW_LOOP_LEAN,
+                 "persistent": A.GNW_LOOP_PERSISTENT}
         A.check(self.L.gnw_set_loop_mode(self.h, modes[mode]))
 
     def loop_schedule(self) -> str:
-        """The schedule most of the last solve's iterations ran: "reference", "fused" or "lean"."""
+        """The schedule the last solve's iterations ran: "reference", "fused", "lean" or "persistent"."""
         st = self.stats()
+        if st["persistent_iterations"] > 0:
+            return "persistent"
         if st["lean_iterations"] > 0:
             return "lean"
         return "fused" if st["fused_iterations"] > 0 else "reference"

@@ -205,7 +205,7 @@ def test_operator_without_J_bitwise(c1, gpu_ctx_factory):
     assert np.array_equal(ctx.apply_operator(x), prob.apply_operator(x))
 
 
-@pytest.mark.parametrize("mode", ["reference", "fused", "lean"])
+@pytest.mark.parametrize("mode", ["reference", "fused", "lean", "persistent"])
 @pytest.mark.parametrize("alpha", [1e-4, 1e-2, 1.0])
 def test_minres_c1_parity(c1, gpu_ctx_factory, alpha, mode):
     mesh, inp, prob = c1[64]
@@ -236,7 +236,7 @@ def test_minres_c1_parity(c1, gpu_ctx_factory, alpha, mode):
     assert rel(x, xr12) <= 1e-5 and rel(xr, xr12) <= 1e-5
 
 
-@pytest.mark.parametrize("mode", ["fused", "lean"])
+@pytest.mark.parametrize("mode", ["fused", "lean", "persistent"])
 def test_fused_schedule_restarts_on_identity_drift(c1, gpu_ctx_factory, mode):
     """GNW_LOOP_FUSED and GNW_LOOP_LEAN take J zhat2 from the Woodbury identity C^-1 H^T v2; its rounding
     grows like 1/beta.  A tolerance below that drift fails the true-residual check
@@ -405,3 +405,36 @@ def test_gn_step_solve_is_rhs_plus_minres(gpu_ctx_factory):
     assert rep_one.iterations == rep_ref.iterations == rep_null.iterations
     assert np.array_equal(x_one, x_ref) and np.array_equal(x_null, x_ref)
     assert np.array_equal(rep_one.relative_residuals, rep_ref.relative_residuals)
+
+
+def test_persistent_kernel_small_and_maxit(c1, gpu_ctx_factory):
+    """The persistent cooperative kernel (GNW_LOOP_PERSISTENT) on the small instance (fewer CTAs than
+    SMs, the dense tail right below level 0 or level 1), its maxit behaviour, and the automatic
+    choice: GNW_LOOP_AUTO runs eligible (L2-resident) problems in it."""
+    mesh, inp, prob = c1[16]
+    ctx = gpu_ctx_factory(mesh)
+    ctx.set_jacobian(inp.J, 1e-2)
+    prob.set_jacobian(inp.J, 1e-2)
+    b = prob.assemble_rhs(inp.dm, np.zeros(prob.N), inp.dg, np.zeros(inp.J.shape[0]))
+    xr, rr = prob.minres(b, tol=1e-10)
+    x_auto, rep_auto = ctx.minres(b, tol=1e-8)  # AUTO
+    assert ctx.loop_schedule() == "persistent" and rep_auto.converged
+    ctx.set_loop_mode("persistent")
+    x, rep = ctx.minres(b, tol=1e-10)
+    assert ctx.loop_schedule() == "persistent"
+    assert rep.converged and abs(rep.iterations - rr["iterations"]) <= 1
+    assert rel(x, xr) <= 1e-8
+    assert len(rep.relative_residuals) == rep.iterations + 1
+    ctx.set_loop_mode("lean")
+    x_lean, rep_lean = ctx.minres(b, tol=1e-10)
+    assert ctx.loop_schedule() == "lean" and abs(rep_lean.iterations - rep.iterations) <= 1
+    assert rel(x, x_lean) <= 1e-9
+    # the residual histories of the two loops agree while rounding has not grown (first half; the
+    # recurred Euclidean residual oscillates near the tolerance, where rounding decides its phase)
+    k = min(len(rep.relative_residuals), len(rep_lean.relative_residuals)) - 1
+    assert np.allclose(rep.relative_residuals[:k // 2], rep_lean.relative_residuals[:k // 2], rtol=1e-5, atol=0)
+    ctx.set_loop_mode("persistent")
+    x5, rep5 = ctx.minres(b, tol=1e-10, maxit=5)
+    xr5, rr5 = prob.minres(b, tol=1e-10, maxit=5)
+    assert not rep5.converged and rep5.iterations == 5 == rr5["iterations"]
+    assert rel(x5, xr5) <= 1e-9
