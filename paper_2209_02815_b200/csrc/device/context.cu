@@ -1208,7 +1208,7 @@ MinresResult Context::minres(const double* b, const double* x0, double* x, doubl
     if (ppart_ == nullptr || ppart_m_ < static_cast<int>(m_)) {
       ppart_ = mem_.alloc<double>(static_cast<size_t>(nb) * 8);
       ptpart_ = mem_.alloc<double>(static_cast<size_t>(nb) * static_cast<size_t>(persistent_max_m()));
-      pbar_ = mem_.alloc<unsigned>(4);
+      pbar_ = mem_.alloc<unsigned>(64);  // arrival counter and released epoch
       ppart_m_ = persistent_max_m();
     }
     a.op = op_;

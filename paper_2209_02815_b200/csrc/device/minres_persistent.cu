@@ -50,16 +50,15 @@ __device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
   asm volatile("ld.acquire.gpu.global.u32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
-__device__ __forceinline__ void red_release(unsigned* p) {
-  asm volatile("red.release.gpu.global.add.u32 [%0], 1;\n" ::"l"(p) : "memory");
-}
 
-// grid barrier: a monotone arrival counter (zeroed by the host before the launch)
+// grid barrier: a monotone arrival counter (zeroed by the host before the launch), polled by
+// one thread per CTA.  (Measured against a last-arriver-publishes-a-flag variant: the flag adds
+// a third L2 round trip per barrier, C1 iteration 0.034 -> 0.038 ms.)
 __device__ __forceinline__ void grid_sync(unsigned* bar, unsigned& epoch) {
   __syncthreads();
   ++epoch;
   if (threadIdx.x == 0) {
-    red_release(bar);
+    asm volatile("red.release.gpu.global.add.u32 [%0], 1;\n" ::"l"(bar) : "memory");
     const unsigned target = epoch * gridDim.x;
     while (ld_acquire(bar) < target) {
     }
@@ -75,6 +74,20 @@ __device__ __forceinline__ double total_of(const double* part, int k) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
   return a;
+}
+
+// the same for NS consecutive slots k0 .. k0 + NS - 1 in one pass (one L2 round trip)
+template <int NS>
+__device__ __forceinline__ void totals_of(const double* part, int k0, double (&out)[NS]) {
+#pragma unroll
+  for (int k = 0; k < NS; ++k) out[k] = 0.0;
+  for (int c = threadIdx.x & 31; c < static_cast<int>(gridDim.x); c += 32)
+#pragma unroll
+    for (int k = 0; k < NS; ++k) out[k] += __ldcg(&part[c * kSlots + k0 + k]);
+#pragma unroll
+  for (int k = 0; k < NS; ++k)
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) out[k] += __shfl_xor_sync(0xffffffffu, out[k], o);
 }
 
 // block sum of NV values; result in every thread (red: NV * kPW doubles)
@@ -284,7 +297,7 @@ __global__ void __launch_bounds__(kPT, 1) k_minres_persistent(PersistArgs a) {
       d[0] = d[0] + o * (z_c * ig);
     }
     block_sum<1>(d, red);
-    if (tid == 0) part[cta * kSlots + 0] = d[0];
+    if (tid == 0) part[cta * kSlots + 5] = d[0];  // delta partial
   };
 
   int iters = 0;
@@ -294,6 +307,8 @@ __global__ void __launch_bounds__(kPT, 1) k_minres_persistent(PersistArgs a) {
     grid_sync(a.bar, epoch);
   }
   if (prof) tprev = gtime();
+  bool first_pass = true;
+  double delta_next = 0.0;
   while (ls.status == kRunning && iters < a.max_iters) {
     const long long j = ls.j;
     const double* __restrict__ vp = ring_slot(a.V, 3, j, 0);
@@ -306,7 +321,8 @@ __global__ void __launch_bounds__(kPT, 1) k_minres_persistent(PersistArgs a) {
     const double az_e = has_e ? a.az[e0] : 0.0, vc_e = has_e ? vc[e0] : 0.0, vp_e = has_e ? vp[e0] : 0.0;
     const double az_c = has_c ? a.az[K + c0] : 0.0, vc_c = has_c ? vc[K + c0] : 0.0, vp_c = has_c ? vp[K + c0] : 0.0;
     {
-      const double delta = total_of(part, 0);
+      const double delta = first_pass ? total_of(part, 5) : delta_next;
+      first_pass = false;
       if (tid == 0) {
         ls.delta = delta;
         ls.coef_v1 = -delta / ls.gamma_cur;
@@ -485,8 +501,9 @@ __global__ void __launch_bounds__(kPT, 1) k_minres_persistent(PersistArgs a) {
       in_c[0] = zc[i], in_c[1] = wp[i], in_c[2] = wc[i], in_c[3] = up[i], in_c[4] = uc[i], in_c[5] = a.x[i], in_c[6] = a.r[i];
     }
     {
-      const double gsq = total_of(part, 1), zz = total_of(part, 2), vv = total_of(part, 3);
-      if (tid == 0) givens_step(gsq, zz, vv, &ls);
+      double t3[3];
+      totals_of<3>(part, 1, t3);  // <z, v>, <z, z>, <v, v>
+      if (tid == 0) givens_step(t3[0], t3[1], t3[2], &ls);
       __syncthreads();
     }
     if (ls.status != kRunning) break;  // kErrNotPD / kErrStagnated, the same on every CTA
@@ -519,8 +536,10 @@ __global__ void __launch_bounds__(kPT, 1) k_minres_persistent(PersistArgs a) {
     grid_sync(a.bar, epoch);
     lap(5);
     {
-      const double rr = total_of(part, 4);
-      if (tid == 0) update_tail(rr, &ls, a.hist_e, a.hist_p, cta == 0 ? a.hist_cap : 0);
+      double t2[2];
+      totals_of<2>(part, 4, t2);  // ||r||^2 and the next iteration's delta, one pass
+      delta_next = t2[1];
+      if (tid == 0) update_tail(t2[0], &ls, a.hist_e, a.hist_p, cta == 0 ? a.hist_cap : 0);
       __syncthreads();
     }
     lap(6);
@@ -544,9 +563,16 @@ bool launch_minres_persistent(PersistArgs a, int sm_count, cudaStream_t s) {
   if (a.op.Qs.width < 1 || a.op.Qs.width > 5 || a.op.Dts.width < 1 || a.op.Dts.width > 2 || a.op.Ds.width < 1 ||
       a.op.Ds.width > 3)
     return false;  // the register row caches hold triangle-mesh rows (5 + 2 and 3 entries)
-  // one CTA per SM, but no more CTAs than there are 64-cell groups (tiny problems); every thread
-  // owns at most one edge and one cell
-  const int grid = static_cast<int>(std::max<long long>(1, std::min<long long>(sm_count, (a.N + 63) / 64)));
+  // As few CTAs as the one-row-per-thread ownership allows (~192 of the 256 threads own an edge):
+  // a grid barrier costs less with fewer arrivals (C1: 128 CTAs 0.034 ms per iteration, 64 CTAs
+  // 0.032), and the level phases still have a warp per row slice.
+  static const int env_ctas = [] {  // env GNW_PERSIST_CTAS: the CTA count (experiments)
+    const char* e = std::getenv("GNW_PERSIST_CTAS");
+    return e ? std::atoi(e) : 0;
+  }();
+  long long want = std::max<long long>((a.K + 191) / 192, (a.N + 191) / 192);
+  if (env_ctas > 0) want = env_ctas;
+  const int grid = static_cast<int>(std::max<long long>(1, std::min<long long>(sm_count, want)));
   const long long e_max = (a.K + grid - 1) / grid + 1, c_max = (a.N + grid - 1) / grid + 1;
   if (e_max > kPT || c_max > kPT) return false;
   const size_t smem = (static_cast<size_t>(2) * a.m * (a.m + 1) + static_cast<size_t>(2) * a.m * c_max) * sizeof(double);
@@ -555,7 +581,7 @@ bool launch_minres_persistent(PersistArgs a, int sm_count, cudaStream_t s) {
   int per_sm = 0;
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_minres_persistent, kPT, smem) != cudaSuccess || per_sm < 1)
     return false;
-  if (cudaMemsetAsync(a.bar, 0, sizeof(unsigned), s) != cudaSuccess) return false;
+  if (cudaMemsetAsync(a.bar, 0, 64 * sizeof(unsigned), s) != cudaSuccess) return false;
   void* args[] = {&a};
   GNW_LAUNCH(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(k_minres_persistent), dim3(grid), dim3(kPT), args,
                                          smem, s));
