@@ -576,8 +576,10 @@ bool launch_minres_persistent(PersistArgs a, int sm_count, cudaStream_t s) {
   const long long e_max = (a.K + grid - 1) / grid + 1, c_max = (a.N + grid - 1) / grid + 1;
   if (e_max > kPT || c_max > kPT) return false;
   const size_t smem = (static_cast<size_t>(2) * a.m * (a.m + 1) + static_cast<size_t>(2) * a.m * c_max) * sizeof(double);
-  if (smem > 200 * 1024) return false;
-  smem_optin(reinterpret_cast<const void*>(k_minres_persistent), static_cast<int>(smem));
+  constexpr int kSmemCap = 200 * 1024;
+  if (smem > kSmemCap) return false;
+  // the opt-in is recorded once per (kernel, device): always ask for the cap, not this launch's size
+  smem_optin(reinterpret_cast<const void*>(k_minres_persistent), kSmemCap);
   int per_sm = 0;
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_minres_persistent, kPT, smem) != cudaSuccess || per_sm < 1)
     return false;
