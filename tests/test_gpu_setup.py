@@ -86,3 +86,18 @@ def test_device_amg_setup_baseline_mesh_hashes(monkeypatch):
     got = refdata.level_hashes_of(c.export_csr, info["n_levels"])
     for l, (g, r) in enumerate(zip(got, ref["levels"])):
         assert g == r, f"level {l}"
+
+
+def test_setup_error_parity_nonpositive_filtered_diagonal(oracle):
+    """The reference's amg_setup throws std::invalid_argument("amg_setup: non-positive diagonal
+    entry") on the 48 x 48 unit square with default options (lumping the weak couplings empties a
+    filtered diagonal, amg.cpp:141-166 + 81-88).  The host setup and the device setup raise the
+    same error, with the reference's text."""
+    mesh = W.unit_square_mesh(48)
+    with pytest.raises(Exception) as ref_err:
+        orc.Problem.mixed(oracle, mesh)
+    assert "non-positive diagonal entry" in str(ref_err.value)
+    for dev in (None, 0):
+        with pytest.raises(ValueError) as err:
+            Context(dev).assemble(mesh)
+        assert str(err.value) == "amg_setup: non-positive diagonal entry"

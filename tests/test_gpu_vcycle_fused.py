@@ -51,3 +51,52 @@ def test_fused_batched_setup_matches_four_pass(monkeypatch, oracle):
     xa, ra = a.minres(ba, tol=1e-10)
     xb, rb = b.minres(ba, tol=1e-10)
     assert abs(ra.iterations - rb.iterations) <= 1 and rel(xa, xb) <= 1e-8
+
+
+def jittered_mesh(n, seed, amp=0.25):
+    """unit_square_mesh(n) with its interior vertices moved by up to amp / n: no two level-operator
+    entries share a value, so the coded lane-ELL tables are as large as the matrices."""
+    mesh = W.unit_square_mesh(n)
+    v = mesh.vertices.copy()
+    rng = np.random.default_rng(seed)
+    interior = (v[:, 0] > 0) & (v[:, 0] < 1) & (v[:, 1] > 0) & (v[:, 1] < 1)
+    v[interior] += rng.uniform(-amp / n, amp / n, size=(int(interior.sum()), 2))
+    return W.Mesh(np.ascontiguousarray(v), mesh.cells)
+
+
+@pytest.mark.parametrize("make", ["unit", "jittered"])
+def test_lane_ell_levels_bitwise_csr(monkeypatch, oracle, make):
+    """The lane-ELL level kernels with coded 32-bit entries (k_vcl_*) against the CSR kernels they
+    replace (GNW_VC_LELL=0, still the fallback for operators whose entries do not fit): the same
+    sums in the same order, bit for bit -- on the structured mesh (a few distinct values per
+    operator) and on a jittered one (every entry its own table slot), where the whole GN-step
+    solve is also checked against the oracle."""
+    n, m = 40, 12
+    mesh = W.unit_square_mesh(n) if make == "unit" else jittered_mesh(n, 3)
+    monkeypatch.setenv("GNW_VC_LELL", "1")
+    a = Context(0)
+    a.assemble(mesh)
+    monkeypatch.setenv("GNW_VC_LELL", "0")
+    b = Context(0)
+    b.assemble(mesh)
+    p = orc.Problem.mixed(oracle, mesh)
+    for seed in range(3):
+        r = W.gaussian(700 + seed, a.N)
+        za, zb = a.amg_apply(r), b.amg_apply(r)
+        assert np.array_equal(za, zb)
+        assert rel(za, p.amg_apply(r)) <= 1e-12
+    J = W.synthetic_jacobian(m, mesh.n_cells, 5)
+    a.set_jacobian(J, 1e-2)
+    p.set_jacobian(J, 1e-2)
+    bvec = p.assemble_rhs(W.gaussian(1, a.N), np.zeros(a.N), W.gaussian(2, m), np.zeros(m))
+    xr6, rr6 = p.minres(bvec, tol=1e-6)
+    xr, rr = p.minres(bvec, tol=1e-10)
+    for mode in ("lean", "persistent"):
+        a.set_loop_mode(mode)
+        x6, rep6 = a.minres(bvec, tol=1e-6)
+        assert rep6.converged and abs(rep6.iterations - rr6["iterations"]) <= 1
+        # near 1e-10 the recurred residual of the jittered problem plateaus (5.97e-11, 5.95e-11,
+        # 3.6e-11 ...) and rounding decides where it crosses: the solutions are the bar there
+        x, rep = a.minres(bvec, tol=1e-10)
+        assert rep.converged and abs(rep.iterations - rr["iterations"]) <= 3
+        assert rel(x, xr) <= 1e-8
