@@ -438,3 +438,22 @@ def test_persistent_kernel_small_and_maxit(c1, gpu_ctx_factory):
     xr5, rr5 = prob.minres(b, tol=1e-10, maxit=5)
     assert not rep5.converged and rep5.iterations == 5 == rr5["iterations"]
     assert rel(x5, xr5) <= 1e-9
+
+
+def test_persistent_kernel_is_deterministic(c1, gpu_ctx_factory):
+    """compute-sanitizer's racecheck is closed on this pool, so the persistent kernel's cross-CTA
+    hand-offs (partials read after a grid barrier, ring slots, the shared-memory slices) are
+    checked by repetition: ten solves on C1 give the same bits, histories included; a missed
+    barrier would show as run-to-run variation."""
+    mesh, inp, prob = c1[64]
+    ctx = gpu_ctx_factory(mesh)
+    ctx.set_loop_mode("persistent")
+    ctx.set_jacobian(inp.J, 1e-3)
+    b = ctx.assemble_rhs(inp.dm, np.zeros(prob.N), inp.dg, np.zeros(inp.J.shape[0]))
+    x0, rep0 = ctx.minres(b, tol=1e-9)
+    assert ctx.loop_schedule() == "persistent" and rep0.converged
+    for _ in range(9):
+        x, rep = ctx.minres(b, tol=1e-9)
+        assert rep.iterations == rep0.iterations
+        assert np.array_equal(x, x0)
+        assert np.array_equal(rep.relative_residuals, rep0.relative_residuals)
