@@ -139,11 +139,21 @@ void PartAmg::build(const host::AmgHierarchy& h, const std::vector<int32_t>& cel
     const host::Halo& H = halos[l][me];
     v.halo = upload_halo(mem_, H, s);
     v.d.n = static_cast<int>(H.n_own);
-    v.d.S = upload_csr(mem_, host::localize(ops[l].S, mine, H), s);
-    v.d.T = upload_csr(mem_, host::localize(ops[l].T, mine, halos[l + 1][me]), s);
-    v.d.Tt = upload_csr(mem_, host::localize(ops[l].Tt, mine1, H), s);
+    const host::Csr lS = host::localize(ops[l].S, mine, H), lT = host::localize(ops[l].T, mine, halos[l + 1][me]),
+                    lTt = host::localize(ops[l].Tt, mine1, H);
+    v.d.S = upload_csr(mem_, lS, s);
+    v.d.T = upload_csr(mem_, lT, s);
+    v.d.Tt = upload_csr(mem_, lTt, s);
     v.d.gS = vc_group_lanes(v.d.S.nnz + v.d.T.nnz, std::max(v.d.n, 1));
     v.d.gTt = vc_group_lanes(v.d.Tt.nnz, std::max(v.d.Tt.n_rows, 1));
+    // lane-ELL copies with coded entries for the single-RHS level kernels, like the single-GPU
+    // hierarchy (same sums in the same order: the partitioned cycle stays bitwise the single-GPU one)
+    const char* le = std::getenv("GNW_VC_LELL");
+    if (!(le && std::atoi(le) == 0) && lS.n_rows > 0 && lTt.n_rows > 0) {
+      v.d.Sl = upload_lell(mem_, lS, v.d.gS, s);
+      v.d.Tl = upload_lell(mem_, lT, v.d.gS, s);
+      v.d.Ttl = upload_lell(mem_, lTt, v.d.gTt, s);
+    }
     v.d.fused = 1;
     v.d.R = v.d.Tt;  // the batched restriction reads R (mvcf_restrict)
     v.r = mem_.alloc<double>(H.n_local());
