@@ -1237,18 +1237,18 @@ void capacitance_reduce(const double* parts, int P, int m, double beta, double* 
 // MINRES vector recurrences (minres.cpp:93-106) and loop control
 // ======================================================================
 
-__global__ void __launch_bounds__(kTpb, 4) k_minres_update(long long n, VSel zs, VSel azs, VSel wps, VSel wcs, VSel wns,
-                                                           VSel ups, VSel ucs, VSel uns, double* __restrict__ x,
-                                                           double* __restrict__ r, MinresState* st,
-                                                           double* hist_e, double* hist_p, long long hist_cap,
-                                                           double* part, unsigned* counter,
-                                                           cudaGraphConditionalHandle handle, int use_cond) {
+__global__ void __launch_bounds__(kTpb) k_minres_update(long long n, VSel zs, VSel azs, VSel wps, VSel wcs, VSel wns,
+                                                        VSel ups, VSel ucs, VSel uns, double* __restrict__ x,
+                                                        double* __restrict__ r, MinresState* st,
+                                                        double* hist_e, double* hist_p, long long hist_cap,
+                                                        double* part, unsigned* counter,
+                                                        cudaGraphConditionalHandle handle, int use_cond) {
+  griddep_wait();
   __shared__ double red[kTpb / 32];
-  // One pair of elements per thread (16-byte loads/stores).  Every vector this kernel reads
-  // (z_cur, A z, w, u, x, r) and the iteration index were written before the predecessor (the
-  // preconditioner's finish kernel) started; only the Givens scalars come from it.  All eight
-  // loads are therefore issued BEFORE the grid-dependency wait, under the finish kernel's
-  // last-block reduction.
+  if (use_cond != 2 && st->status != kRunning) {  // use_cond == 2: isolated timing, no loop control
+    if (use_cond == 1 && blockIdx.x == 0 && threadIdx.x == 0) cudaGraphSetConditional(handle, 0);
+    return;
+  }
   const double* __restrict__ z = vsel(zs, st);
   const double* __restrict__ az = vsel(azs, st);
   const double* __restrict__ wp = vsel(wps, st);
@@ -1257,40 +1257,31 @@ __global__ void __launch_bounds__(kTpb, 4) k_minres_update(long long n, VSel zs,
   const double* __restrict__ up = vsel(ups, st);
   const double* __restrict__ uc = vsel(ucs, st);
   double* __restrict__ un = vsel(uns, st);
-  const long long np = n / 2;
-  auto ld2 = [](const double* p, long long k) { return *reinterpret_cast<const double2*>(p + 2 * k); };
-  const long long k = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
-  double2 zv, wpv, wcv, azv, upv, ucv, xv, rv;
-  zv = wpv = wcv = azv = upv = ucv = xv = rv = make_double2(0.0, 0.0);
-  if (k < np) {
-    zv = ld2(z, k), wpv = ld2(wp, k), wcv = ld2(wc, k), azv = ld2(az, k);
-    upv = ld2(up, k), ucv = ld2(uc, k), xv = ld2(x, k), rv = ld2(r, k);
-  }
-  griddep_wait();
-  if (use_cond != 2 && st->status != kRunning) {  // use_cond == 2: isolated timing, no loop control
-    if (use_cond == 1 && blockIdx.x == 0 && threadIdx.x == 0) cudaGraphSetConditional(handle, 0);
-    return;
-  }
   const double ig = st->inv_gamma, na3 = -st->alpha3, na2 = -st->alpha2, ia = st->inv_alpha1;
   const double tau = st->tau, ntau = -tau;
   double rr[1] = {0.0};
-  // minres.cpp:93-106 per element
-  auto elem = [&](double zv_, double wpv_, double wcv_, double azv_, double upv_, double ucv_, double xv_, double rv_,
+  // minres.cpp:93-106 per element; pairs of elements with 16-byte loads/stores
+  auto elem = [&](double zv, double wpv, double wcv, double azv, double upv, double ucv, double xv, double rv,
                   double& wo, double& uo, double& xo, double& ro) {
-    const double zh = zv_ * ig;
-    double w = zh + na3 * wpv_;
-    w = w + na2 * wcv_;
+    const double zh = zv * ig;
+    double w = zh + na3 * wpv;
+    w = w + na2 * wcv;
     w = w * ia;
-    double uu = azv_ + na3 * upv_;
-    uu = uu + na2 * ucv_;
+    double uu = azv + na3 * upv;
+    uu = uu + na2 * ucv;
     uu = uu * ia;
     wo = w;
     uo = uu;
-    xo = xv_ + tau * w;
-    ro = rv_ + ntau * uu;
+    xo = xv + tau * w;
+    ro = rv + ntau * uu;
     rr[0] = rr[0] + ro * ro;
   };
-  if (k < np) {
+  const long long np = n / 2;
+  auto ld2 = [](const double* p, long long k) { return *reinterpret_cast<const double2*>(p + 2 * k); };
+  for (long long k = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; k < np;
+       k += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const double2 zv = ld2(z, k), wpv = ld2(wp, k), wcv = ld2(wc, k), azv = ld2(az, k), upv = ld2(up, k),
+                  ucv = ld2(uc, k), xv = ld2(x, k), rv = ld2(r, k);
     double2 wo, uo, xo, ro;
     elem(zv.x, wpv.x, wcv.x, azv.x, upv.x, ucv.x, xv.x, rv.x, wo.x, uo.x, xo.x, ro.x);
     elem(zv.y, wpv.y, wcv.y, azv.y, upv.y, ucv.y, xv.y, rv.y, wo.y, uo.y, xo.y, ro.y);
@@ -1326,7 +1317,7 @@ void update_tail_from_scratch(MinresState* st, double* hist_e, double* hist_p, l
 void minres_update(long long n, VSel z, VSel az, VSel wprev, VSel wcur, VSel wnext, VSel uprev, VSel ucur, VSel unext,
                    double* x, double* r, MinresState* st, double* hist_e, double* hist_p, long long hist_cap,
                    double* part, unsigned* counter, unsigned long long cond_handle, int use_cond, cudaStream_t s) {
-  const unsigned grid = grid_for((n + 1) / 2);  // one pair per thread
+  const unsigned grid = std::min<unsigned>(grid_for((n + 1) / 2), 148u * 8u);
   GNW_LAUNCH(launch_k(k_minres_update, grid, kTpb, 0, s, n, z, az, wprev, wcur, wnext, uprev, ucur, unext, x, r, st, hist_e, hist_p,
                                         hist_cap, part, counter,
                                         static_cast<cudaGraphConditionalHandle>(cond_handle), use_cond));
