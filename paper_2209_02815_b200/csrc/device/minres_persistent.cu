@@ -2,9 +2,10 @@
 // kernel, for problems whose whole working set is L2-resident (BASELINE C1: 64^2 mesh, m = 32).
 //
 // At that size every kernel of the graph loop is latency-bound: an iteration is ~20 dependent
-// launches of ~2 us each (C1: 0.046 ms for 14.5 MB).  Here one CTA per SM stays resident for the
-// whole solve and the phases of an iteration are separated by grid barriers (one global atomic
-// counter, release/acquire) instead of kernel boundaries: six barriers per iteration at C1.
+// launches of ~2 us each (C1: 0.044 ms for 14.5 MB).  Here a few dozen CTAs (one per ~192 edge
+// rows; C1: 65) stay resident for the whole solve and the phases of an iteration are separated
+// by grid barriers (one global arrival counter, release/acquire) instead of kernel boundaries:
+// eight barriers per iteration at C1 (two one-pass levels above a 519-row dense tail).
 // The arithmetic is the lean schedule's (q = J^T t' feeds the next operator,
 // z2 = B (v2 - q / beta), one refinement step on t' = C^-1 t):
 //
