@@ -586,8 +586,13 @@ bool launch_minres_persistent(PersistArgs a, int sm_count, cudaStream_t s) {
     return false;
   if (cudaMemsetAsync(a.bar, 0, 64 * sizeof(unsigned), s) != cudaSuccess) return false;
   void* args[] = {&a};
-  GNW_LAUNCH(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(k_minres_persistent), dim3(grid), dim3(kPT), args,
-                                         smem, s));
+  // a cooperative launch fails (rather than deadlocks) when the grid cannot be co-resident, e.g.
+  // with another process on the GPU: the caller then runs the graph loop
+  if (cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(k_minres_persistent), dim3(grid), dim3(kPT), args, smem,
+                                  s) != cudaSuccess) {
+    cudaGetLastError();  // clear the launch error
+    return false;
+  }
   note_launch("minres_persistent");
   return true;
 }
