@@ -70,16 +70,20 @@ def test_device_amg_setup_bitwise(monkeypatch, n, thr, min_rows):
     assert np.array_equal(gpu.amg_apply(r), ref.amg_apply(r))
 
 
-def test_device_amg_setup_baseline_mesh_hashes(monkeypatch):
-    """BASELINE C5 mesh (n = 1024, threshold 1024): the device setup's hierarchy against the
-    SHA-256 hashes of the unmodified reference's own amg_setup (tests/golden/ref_p1024.json)."""
+@pytest.mark.parametrize("name,min_rows", [("p1024", "0"), ("p2048", None)])
+def test_device_amg_setup_baseline_mesh_hashes(monkeypatch, name, min_rows):
+    """BASELINE C5 mesh (n = 1024, threshold 1024; every level forced onto the device) and C3 mesh
+    (n = 2048, threshold 4096; the default split: levels above 100 000 rows on the device, the
+    rest on the host): the device setup's hierarchy against the SHA-256 hashes of the unmodified
+    reference's own amg_setup (tests/golden/ref_p1024.json, ref_p2048.json)."""
     import refdata
 
-    if not refdata.available("p1024"):
-        pytest.skip("fixture ref_p1024.json not generated")
-    ref = refdata.load("p1024")
+    if not refdata.available(name):
+        pytest.skip(f"fixture ref_{name}.json not generated")
+    ref = refdata.load(name)
     monkeypatch.setenv("GNW_DEVICE_SETUP", "1")
-    monkeypatch.setenv("GNW_DEVICE_SETUP_MIN_ROWS", "0")
+    if min_rows is not None:
+        monkeypatch.setenv("GNW_DEVICE_SETUP_MIN_ROWS", min_rows)
     c = Context(0).assemble(W.unit_square_mesh(ref["n"]), AmgOptions(coarse_threshold=ref["coarse_threshold"]))
     info = c.info()
     assert info["n_levels"] == ref["n_levels"] and info["coarse_n"] == ref["coarse_n"]
