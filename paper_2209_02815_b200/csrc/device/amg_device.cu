@@ -3,12 +3,15 @@
 #include "minres_persistent.cuh"
 #include "sparse_device.cuh"
 
+#include <omp.h>
+
 #include <algorithm>
 #include <chrono>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <unordered_map>
+#include <unordered_set>
 
 namespace gnw {
 
@@ -38,6 +41,46 @@ DCsr upload_csr(DeviceMemory& mem, const host::Csr& A, cudaStream_t s) {
   return d;
 }
 
+namespace {
+// The distinct values of v (as bit patterns, ascending) if there are at most `cap` of them;
+// empty + false otherwise.  Chunks are scanned in parallel, each bailing out early.
+bool distinct_values(const std::vector<double>& v, size_t cap, std::vector<uint64_t>& out) {
+  out.clear();
+  const int nt = std::max(1, omp_get_max_threads());
+  std::vector<std::unordered_set<uint64_t>> local(nt);
+  std::vector<char> over(nt, 0);
+#pragma omp parallel num_threads(nt)
+  {
+    const int t = omp_get_thread_num();
+    const size_t a = v.size() * t / nt, b = v.size() * (t + 1) / nt;
+    std::unordered_set<uint64_t>& mine = local[t];
+    uint64_t last = 0;
+    bool have_last = false;
+    for (size_t k = a; k < b; ++k) {
+      uint64_t bits;
+      std::memcpy(&bits, &v[k], sizeof bits);
+      if (have_last && bits == last) continue;
+      last = bits;
+      have_last = true;
+      if (mine.insert(bits).second && mine.size() > cap) {
+        over[t] = 1;
+        break;
+      }
+    }
+  }
+  for (int t = 0; t < nt; ++t)
+    if (over[t]) return false;
+  for (int t = 0; t < nt; ++t) out.insert(out.end(), local[t].begin(), local[t].end());
+  std::sort(out.begin(), out.end());
+  out.erase(std::unique(out.begin(), out.end()), out.end());
+  if (out.size() > cap) {
+    out.clear();
+    return false;
+  }
+  return true;
+}
+}  // namespace
+
 DSell upload_sell(DeviceMemory& mem, const host::Csr& A, cudaStream_t s, int encode) {
   DSell d;
   int64_t w = 0;
@@ -55,14 +98,16 @@ DSell upload_sell(DeviceMemory& mem, const host::Csr& A, cudaStream_t s, int enc
     for (double v : A.vals)
       if (v != 1.0 && v != -1.0) encode = 2;
   if (encode == 2) {
-    for (double v : A.vals) {
-      if (code_of.count(bits(v))) continue;
-      if (table.size() == 256) {
-        encode = 0;
-        break;
+    std::vector<uint64_t> dv;
+    if (distinct_values(A.vals, 256, dv)) {
+      for (uint64_t b : dv) {
+        double v;
+        std::memcpy(&v, &b, sizeof v);
+        code_of[b] = static_cast<unsigned char>(table.size());
+        table.push_back(v);
       }
-      code_of[bits(v)] = static_cast<unsigned char>(table.size());
-      table.push_back(v);
+    } else {
+      encode = 0;
     }
   }
   const int64_t slices = (A.n_rows + 31) / 32;
@@ -125,13 +170,15 @@ DLell upload_lell(DeviceMemory& mem, const host::Csr& A, int G, cudaStream_t s) 
   int col_bits = 1;
   while ((int64_t{1} << col_bits) < A.n_cols) ++col_bits;
   const size_t max_codes = col_bits >= 31 ? 0 : size_t{1} << (31 - col_bits);
-  for (double v : A.vals) {
-    uint64_t b;
-    std::memcpy(&b, &v, sizeof b);
-    if (code_of.count(b)) continue;
-    if (table.size() >= max_codes) return d;  // too many distinct values for a 32-bit entry
-    code_of[b] = static_cast<unsigned>(table.size());
-    table.push_back(v);
+  {
+    std::vector<uint64_t> dv;
+    if (max_codes == 0 || !distinct_values(A.vals, max_codes, dv)) return d;  // too many distinct values for a 32-bit entry
+    for (uint64_t b : dv) {
+      double v;
+      std::memcpy(&v, &b, sizeof v);
+      code_of[b] = static_cast<unsigned>(table.size());
+      table.push_back(v);
+    }
   }
   std::vector<unsigned> words(static_cast<size_t>(len), 0xffffffffu);
 #pragma omp parallel for schedule(static)
