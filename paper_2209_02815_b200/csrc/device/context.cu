@@ -97,6 +97,7 @@ Context::~Context() {
   if (copy_) cudaStreamSynchronize(copy_);
   for (auto& e : stage_ev_)
     if (e) cudaEventDestroy(e);
+  fused_pre_.clear();  // stream-ordered blocks: freed before their stream is destroyed
   stage_mem_.reset();
   jmem_.reset();
   damg_.reset();
@@ -164,13 +165,18 @@ void Context::assemble(const double* vertices, int64_t nv, const int64_t* cells,
   // Device contexts run the Schur complement's product and the whole level pipeline of
   // amg_setup on the device (sparse_device.cuh, bit-identical; only the greedy aggregation
   // stays on the host).  Env GNW_DEVICE_SETUP=0: the host code.
-  const bool dev_setup = device_setup_enabled();
+  const bool dev_setup = device_setup_enabled(nc);
   fused_pre_.clear();
   if (dev_setup) GNW_CUDA_CHECK(cudaSetDevice(device_));
   S_ = dev_setup ? device_lumped_schur(Q_, D_, stream_) : host::lumped_schur(Q_, D_);  // fem_mixed.cpp:84-94
   const auto t2 = std::chrono::steady_clock::now();
-  amg_ = dev_setup ? device_amg_setup(S_, o, stream_, comm_ ? nullptr : &fused_pre_, DeviceAmg::collapse_max())
-                   : host::amg_setup(S_, o);             // amg.cpp:115-187
+  try {
+    amg_ = dev_setup ? device_amg_setup(S_, o, stream_, comm_ ? nullptr : &fused_pre_, DeviceAmg::collapse_max())
+                     : host::amg_setup(S_, o);           // amg.cpp:115-187
+  } catch (...) {
+    fused_pre_.clear();  // a setup error on a deeper level leaves the finished levels' operators behind
+    throw;
+  }
   if (const char* e = std::getenv("GNW_SETUP_TIMING"))
     if (std::atoi(e) != 0)
       std::fprintf(stderr, "[gnw setup] finalize_mesh %.1f ms, assemble Q %.1f ms, D %.1f ms, S_hat %.1f ms\n",
@@ -264,9 +270,14 @@ void Context::assemble_saddle_csr(int64_t K, int64_t N, const int64_t* qrp, cons
   mesh_ = host::Mesh{};
   S_ = host::lumped_schur(Q_, D_);                        // fem_mixed.cpp:84-94
   fused_pre_.clear();
-  if (o && device_setup_enabled()) {
+  if (o && device_setup_enabled(N)) {
     GNW_CUDA_CHECK(cudaSetDevice(device_));
-    amg_ = device_amg_setup(S_, *o, stream_, &fused_pre_, DeviceAmg::collapse_max());
+    try {
+      amg_ = device_amg_setup(S_, *o, stream_, &fused_pre_, DeviceAmg::collapse_max());
+    } catch (...) {
+      fused_pre_.clear();
+      throw;
+    }
   } else {
     amg_ = o ? host::amg_setup(S_, *o) : host::AmgHierarchy{};  // amg.cpp:115-187
   }
@@ -421,10 +432,13 @@ void Context::alloc_vectors(long long n_alloc, long long K, long long N) {
   ctot_ = mem_.alloc<double>(4);  // their sum (k_sum_triples)
 }
 
-bool Context::device_setup_enabled() const {
+// Env GNW_DEVICE_SETUP: 1 always, 0 never; unset: from 200 000 cells up.  Measured gnw_assemble of
+// a device context, device against host setup (tools/setup_compare.py): n = 256 (131 072 cells)
+// 0.34 against 0.22 s, n = 512 0.44 against 0.71 s, n = 1024 1.5 against 3.0 s, n = 2048 7.9 against 15.3 s.
+bool Context::device_setup_enabled(int64_t n_cells) const {
   if (!has_device()) return false;
-  const char* e = std::getenv("GNW_DEVICE_SETUP");
-  return !(e && std::atoi(e) == 0);
+  if (const char* e = std::getenv("GNW_DEVICE_SETUP")) return std::atoi(e) != 0;
+  return n_cells >= 200000;
 }
 
 void Context::upload_hierarchy() {
@@ -432,7 +446,7 @@ void Context::upload_hierarchy() {
   const bool had_dev = !fused_pre_.empty();
   fused_pre_.clear();
   fused_pre_.shrink_to_fit();
-  if (had_dev || device_setup_enabled()) device_setup_trim();  // the setup's pool blocks go back to the driver
+  if (had_dev || device_setup_enabled(N_)) device_setup_trim();  // the setup's pool blocks go back to the driver
   svc_ = mem_.alloc<double>(std::max<int64_t>(N_, 1));
   sync();
 }

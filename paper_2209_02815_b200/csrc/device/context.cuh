@@ -202,7 +202,7 @@ class Context {
   host::Csr Q_, D_, S_;
   host::AmgHierarchy amg_;
   std::vector<DevFusedOps> fused_pre_;  // one-pass level operators formed (and kept) on the device by the setup
-  bool device_setup_enabled() const;
+  bool device_setup_enabled(int64_t n_cells) const;
   int64_t K_ = 0, N_ = 0;
 
   // device structure

@@ -92,7 +92,7 @@ def test_device_amg_setup_baseline_mesh_hashes(monkeypatch, name, min_rows):
         assert g == r, f"level {l}"
 
 
-def test_setup_error_parity_nonpositive_filtered_diagonal(oracle):
+def test_setup_error_parity_nonpositive_filtered_diagonal(monkeypatch, oracle):
     """The reference's amg_setup throws std::invalid_argument("amg_setup: non-positive diagonal
     entry") on the 48 x 48 unit square with default options (lumping the weak couplings empties a
     filtered diagonal, amg.cpp:141-166 + 81-88).  The host setup and the device setup raise the
@@ -101,6 +101,8 @@ def test_setup_error_parity_nonpositive_filtered_diagonal(oracle):
     with pytest.raises(Exception) as ref_err:
         orc.Problem.mixed(oracle, mesh)
     assert "non-positive diagonal entry" in str(ref_err.value)
+    monkeypatch.setenv("GNW_DEVICE_SETUP", "1")  # small meshes default to the host setup
+    monkeypatch.setenv("GNW_DEVICE_SETUP_MIN_ROWS", "0")
     for dev in (None, 0):
         with pytest.raises(ValueError) as err:
             Context(dev).assemble(mesh)
