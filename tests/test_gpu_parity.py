@@ -457,3 +457,20 @@ def test_persistent_kernel_is_deterministic(c1, gpu_ctx_factory):
         assert rep.iterations == rep0.iterations
         assert np.array_equal(x, x0)
         assert np.array_equal(rep.relative_residuals, rep0.relative_residuals)
+
+
+def test_gn_step_solve_error_behaviour(gpu_ctx_factory):
+    """gnw_gn_step_solve keeps the reference's error behaviour: no Jacobian -> assemble_gn_rhs's
+    shape error; tol <= 0 -> minres's argument error; the context stays usable afterwards."""
+    inp = W.gnstep_inputs(16, 8, 0)
+    ctx = gpu_ctx_factory(inp.mesh)
+    zN, zm = np.zeros(inp.mesh.n_cells), np.zeros(8)
+    with pytest.raises(ValueError, match="shape mismatch"):
+        ctx.gn_step_solve(inp.dm, zN, inp.dg, zm)
+    ctx.set_jacobian(inp.J, 1e-2)
+    with pytest.raises(ValueError, match="tol must be positive"):
+        ctx.gn_step_solve(inp.dm, zN, inp.dg, zm, tol=0.0)
+    x, rep = ctx.gn_step_solve(inp.dm, zN, inp.dg, zm, tol=1e-9)
+    assert rep.converged
+    x5, rep5 = ctx.gn_step_solve(inp.dm, zN, inp.dg, zm, tol=1e-9, maxit=5)
+    assert not rep5.converged and rep5.iterations == 5
