@@ -107,3 +107,29 @@ def test_setup_error_parity_nonpositive_filtered_diagonal(monkeypatch, oracle):
         with pytest.raises(ValueError) as err:
             Context(dev).assemble(mesh)
         assert str(err.value) == "amg_setup: non-positive diagonal entry"
+
+
+@pytest.mark.parametrize("n", [2, 3, 5, 8, 12, 24, 40])
+@pytest.mark.parametrize("thr", [4, 64])
+def test_device_amg_setup_small_meshes(monkeypatch, n, thr):
+    """Edge sizes through the forced device setup (a single level, tiny coarse levels, odd sizes):
+    the hierarchy bit for bit the host's, and the V-cycles built on them equal bit for bit."""
+    mesh = W.unit_square_mesh(n)
+    opts = AmgOptions(coarse_threshold=thr)
+    host = Context(None)
+    host.assemble(mesh, opts)
+    monkeypatch.setenv("GNW_DEVICE_SETUP", "1")
+    monkeypatch.setenv("GNW_DEVICE_SETUP_MIN_ROWS", "0")
+    dev = Context(0)
+    dev.assemble(mesh, opts)
+    monkeypatch.setenv("GNW_DEVICE_SETUP", "0")
+    ref = Context(0)
+    ref.assemble(mesh, opts)
+    ih, ig = host.info(), dev.info()
+    assert (ih["n_levels"], ih["coarse_n"]) == (ig["n_levels"], ig["coarse_n"])
+    eg, eh = exported(dev, ig["n_levels"]), exported(host, ih["n_levels"])
+    for k in eh:
+        for x, y in zip(eg[k], eh[k]):
+            assert np.array_equal(np.asarray(x), np.asarray(y)), k
+    r = np.random.default_rng(n).standard_normal(mesh.n_cells)
+    assert np.array_equal(dev.amg_apply(r), ref.amg_apply(r))
