@@ -474,3 +474,22 @@ def test_gn_step_solve_error_behaviour(gpu_ctx_factory):
     assert rep.converged
     x5, rep5 = ctx.gn_step_solve(inp.dm, zN, inp.dg, zm, tol=1e-9, maxit=5)
     assert not rep5.converged and rep5.iterations == 5
+
+
+@pytest.mark.parametrize("n,m", [(3, 1), (5, 7), (12, 33), (20, 64), (33, 5), (128, 64)])
+def test_persistent_kernel_shapes(gpu_ctx_factory, n, m):
+    """Odd shapes through the persistent kernel: a single-level hierarchy (the dense tail at level
+    0), m = 1 and m = 64, CTAs with ragged ownership -- against the reference schedule of the same
+    context; n = 128 is not eligible (more rows per CTA than threads) and falls back to lean."""
+    mesh = W.unit_square_mesh(n)
+    ctx = gpu_ctx_factory(mesh)
+    J = W.synthetic_jacobian(m, mesh.n_cells, 3)
+    ctx.set_jacobian(J, 1e-2)
+    b = ctx.assemble_rhs(W.gaussian(1, ctx.N), np.zeros(ctx.N), W.gaussian(2, m), np.zeros(m))
+    ctx.set_loop_mode("reference")
+    xr, rr = ctx.minres(b, tol=1e-10)
+    ctx.set_loop_mode("persistent")
+    x, rep = ctx.minres(b, tol=1e-10)
+    assert ctx.loop_schedule() == ("lean" if n == 128 else "persistent")
+    assert rep.converged and abs(rep.iterations - rr.iterations) <= 2
+    assert rel(x, xr) <= 1e-8
