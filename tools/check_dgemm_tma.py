@@ -2,7 +2,7 @@
 (GNW_DGEMM_TMA=0): Cholesky factors bit for bit, and t_C of both.  Run each mode in its own
 process (the switch is read once).
 
-    python tools/check_dgemm_tma.py [C2|C4|C1|m868]
+    python tools/check_dgemm_tma.py [C2|C4|C1|m868|n7m5 ...]
 """
 import os
 import subprocess
@@ -16,7 +16,13 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 def child(cfgname, out):
     import torch
     from paper_2209_02815_b200 import AmgOptions, Context, workload as W
-    if cfgname.startswith("m"):
+    if cfgname.startswith("n"):  # nXXmYY: mesh n = XX (N = 2 XX^2 cells), m = YY rows
+        n, m = (int(v) for v in cfgname[1:].split("m"))
+        mesh = W.unit_square_mesh(n)
+        ctx = Context(0)
+        ctx.assemble(mesh, AmgOptions(coarse_threshold=64))
+        J = W.synthetic_jacobian_device(m, mesh.n_cells, 9, "cuda")
+    elif cfgname.startswith("m"):
         n, m = 128, int(cfgname[1:])
         mesh = W.unit_square_mesh(n)
         ctx = Context(0)
